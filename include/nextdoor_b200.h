@@ -1,0 +1,205 @@
+/*
+ * nextdoor_b200.h — C-ABI of the B200 transit-parallel sampling engine.
+ *
+ * The drop-in boundary for the reference `trawl` sampling path
+ * (/root/reference/pkg/src/trawl).  Two nested levels, as in the reference:
+ *
+ *  Level 1 — the kernel-backend ABI that `trawl.kernels` exposes
+ *  (kernels/__init__.py:29-44) and that _kernel_pairs / _kernel_exec / _batch
+ *  call (transit_parallel.py:111-120, sample_parallel.py:43-53, chain.py:43-61):
+ *      nd_individual_batch      <- individual_batch   (_ckernels.pyx:136-271)
+ *      nd_segmented_prefix_sum  <- segmented_prefix_sum (_ckernels.pyx:103-116)
+ *      nd_segment_max           <- segment_max        (_ckernels.pyx:119-133)
+ *      nd_keyed_u64             <- keyed_u64          (_pykernels.py:61-68)
+ *
+ *  Level 2 — the engine entry `tp_run/sp_run(app, graph, samples, config)`
+ *  (transit_parallel.py:249-257, sample_parallel.py:102-110), split into
+ *      nd_graph_*               <- Graph / from_edges (graph.py:36-129)
+ *      nd_run_walk              <- run_chain          (chain.py:64-164)
+ *      nd_run_individual        <- run_loop + tp_step (driver.py:203-235,
+ *                                  transit_parallel.py:185-230)
+ *      nd_run_collective        <- tp_step collective branch +
+ *                                  build_combined/collective_select
+ *                                  (transit_parallel.py:187-198, collective.py:39-141)
+ *      nd_transit_schedule      <- build_transit_map + partition_work_classes
+ *                                  (transit_parallel.py:71-101)
+ *      nd_result_*              <- SampleSetOutput fields (output.py:43-69)
+ *
+ * Conventions: plain pointers and sizes only.  Pointers are DEVICE pointers
+ * unless a name says `host_`.  `stream` is a cudaStream_t passed as void*
+ * (NULL = legacy default stream).  Every entry returns an int status; the
+ * Python shim maps them onto the reference's exceptions:
+ *      ND_ERR_STALL -> SamplerStallError (_ckernels.pyx:263-269)
+ *      ND_ERR_APP   -> ValueError("unknown app code") (_ckernels.pyx:270-271)
+ *      ND_ERR_ARG   -> ValueError, ND_ERR_CUDA -> DeviceError
+ * Calls are re-entrant; a graph handle is read-only after creation and may
+ * be shared by concurrent runs on different streams.
+ */
+#ifndef NEXTDOOR_B200_H
+#define NEXTDOOR_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ND_OK 0
+#define ND_ERR_STALL 1
+#define ND_ERR_APP 2
+#define ND_ERR_ARG 3
+#define ND_ERR_CUDA 4
+#define ND_ERR_NOMEM 5
+
+/* individual app codes (kernels/_pykernels.py:32-36) */
+#define ND_DEEPWALK 0
+#define ND_PPR 1
+#define ND_NODE2VEC 2
+#define ND_KHOP 3
+#define ND_MULTIRW 4
+
+/* collective app kinds (apps.py:247-386) */
+#define ND_LAYER 0
+#define ND_IMPORTANCE 1 /* fastgcn / ladies */
+#define ND_MVS 2
+#define ND_CLUSTERGCN 3
+
+/* paradigms (bench.py:91-96 --paradigm) */
+#define ND_SP 0
+#define ND_TP 1
+
+typedef struct nd_graph nd_graph;
+typedef struct nd_result nd_result;
+
+/* last error text of this thread (for the Python shim) */
+const char *nd_last_error(void);
+int nd_version(void);
+/* cudaMemcpyDefault copy helper for bindings without a CUDA runtime of their
+ * own (synchronous when stream is NULL) */
+int nd_copy(void *dst, const void *src, int64_t bytes, void *stream);
+
+/* ---- level 1: kernel backend (_ckernels.pyx:103-271) --------------------- */
+/* Sequential per-segment inclusive f64 prefix (bit-identical to the Cython
+ * loop; one thread owns a segment). */
+int nd_segmented_prefix_sum(const double *values, const int64_t *offsets,
+                            int64_t n_segments, double *out, void *stream);
+/* Per-segment max, 0.0 for empty segments. */
+int nd_segment_max(const double *values, const int64_t *offsets,
+                   int64_t n_segments, double *out, void *stream);
+/* individual_batch over the reference's own array layout (int64 CSR, f64
+ * weights/prefix/max, int64 item arrays).  seed is the reference's
+ * `seed & (2^64-1)`.  Writes out[i] or -1.  Returns ND_ERR_APP for an unknown
+ * code (before any work), ND_ERR_STALL on a node2vec cap hit. */
+int nd_individual_batch(int app_code, const double *host_params, int64_t n_params,
+                        const int64_t *row_offsets, const int64_t *col_indices,
+                        const double *weights, const double *weight_prefix,
+                        const double *max_weight, const int64_t *transits,
+                        const int64_t *t_prev, const int64_t *sample_ids,
+                        const int64_t *transit_idxs, const int64_t *slots, int64_t n,
+                        uint64_t seed, int64_t step, int64_t *out, void *stream);
+/* out[i] = u[i] % d[i] with the engine's exact fp64-assisted modulo (fuzz hook) */
+int nd_mod_u64(const uint64_t *u, const uint64_t *d, int64_t n, uint64_t *out, void *stream);
+/* keyed_u64 over id arrays (transit_idxs/slots may be NULL = zeros). */
+int nd_keyed_u64(uint64_t seed, const int64_t *sample_ids, int64_t step,
+                 const int64_t *transit_idxs, const int64_t *slots, int64_t domain,
+                 int64_t draw, int64_t n, uint64_t *out, void *stream);
+
+/* ---- level 2: graph residency (graph.py:36-129) ------------------------------ */
+/* Device CSR from reference-layout arrays (host or device pointers, flag
+ * `arrays_on_host`).  weights may be NULL (unit).  prefix/max are computed on
+ * device when NULL.  Columns are stored int32 (requires V < 2^31). */
+int nd_graph_create(const int64_t *row_offsets, const int64_t *col_indices,
+                    const double *weights, const double *weight_prefix,
+                    const double *max_weight, int64_t n_vertices, int64_t n_edges,
+                    int arrays_on_host, void *stream, nd_graph **out);
+/* Build on device from an edge list (from_edges semantics: stable lexsort
+ * by (src, dst); parallel edges stay in input order). */
+int nd_graph_from_edges(const int64_t *src, const int64_t *dst, const double *weights,
+                        int64_t n_edges, int64_t n_vertices, void *stream,
+                        nd_graph **out);
+/* Keyed RMAT graph generated and built on device. */
+int nd_graph_rmat(int scale, int64_t n_edges, uint32_t ta, uint32_t tab, uint32_t tabc,
+                  uint64_t seed, int undirected, int weighted, void *stream,
+                  nd_graph **out);
+int nd_graph_destroy(nd_graph *g);
+/* sizes and device pointers (read-only views) */
+int nd_graph_info(const nd_graph *g, int64_t *n_vertices, int64_t *n_edges, int *unit_weights,
+                  int64_t *bytes);
+int nd_graph_arrays(const nd_graph *g, const int64_t **row_offsets, const int32_t **col,
+                    const double **weights, const double **prefix, const double **max_w);
+
+/* ---- level 2: engine runs ------------------------------------------------------ */
+/* Keyed roots (apps.py:83-103): count per sample, distinct when V >= count. */
+int nd_uniform_roots(const nd_graph *g, int64_t count, uint64_t seed, int64_t sample_lo,
+                     int64_t n_samples, int64_t *roots, void *stream);
+
+/* Chain walks: DeepWalk / PPR / node2vec / MultiRW (chain.py:64-179).
+ * roots: device int64 [n_samples * roots_per_sample] or NULL for the keyed
+ * default roots.  steps < 0 means INF (capped at step_cap). */
+int nd_run_walk(const nd_graph *g, int app_code, const double *host_params, int64_t n_params,
+                int64_t sample_lo, int64_t n_samples, const int64_t *roots,
+                int64_t roots_per_sample, uint64_t seed, int64_t steps, int64_t step_cap,
+                int paradigm, void *stream, nd_result **out);
+
+/* Multi-slot individual apps (k-hop) through the run loop: fanouts[n_steps]
+ * (host array).  roots: device int64 [n_samples * roots_per_sample] or NULL. */
+int nd_run_individual(const nd_graph *g, int app_code, const double *host_params,
+                      int64_t n_params, const int64_t *host_fanouts, int64_t n_fanouts,
+                      int64_t sample_lo, int64_t n_samples, const int64_t *roots,
+                      int64_t roots_per_sample, uint64_t seed, int64_t step_cap,
+                      int paradigm, void *stream, nd_result **out);
+
+/* Collective apps (layer / fastgcn / ladies / mvs / clustergcn).
+ * roots_off[n+1] / roots (device, ragged) or NULL for the app's keyed default
+ * roots (batch_size roots, or ClusterGCN clusters). */
+int nd_run_collective(const nd_graph *g, int kind, int64_t step_size, int64_t max_size,
+                      int distribution, int64_t steps, int64_t batch_size,
+                      int64_t clusters_per_sample, int64_t num_clusters,
+                      int64_t sample_lo, int64_t n_samples, const int64_t *roots_off,
+                      const int64_t *roots, uint64_t seed, int64_t step_cap,
+                      void *stream, nd_result **out);
+
+/* build_transit_map + partition_work_classes for one step's pairs (device
+ * int64 pair_transit[n], sample-major).  Outputs (device, caller-allocated,
+ * size n / n+1): order (member pair ids, group-major), group_start[G+1],
+ * group_transit[G], group_class[G] (0 small,1 medium,2 large),
+ * sched_index[G] (rank within class, transit-ascending); *n_groups = G. */
+int nd_transit_schedule(const int64_t *pair_transit, int64_t n_pairs, int64_t m,
+                        int64_t *order, int64_t *group_start, int64_t *group_transit,
+                        int32_t *group_class, int64_t *sched_index, int64_t *n_groups,
+                        void *stream);
+
+/* ---- results (output.py:43-69) ----------------------------------------------------
+ * A result owns device buffers.  Field ids for nd_result_field: */
+#define ND_F_FINAL_OFF 0   /* int64 [n+1] final-layout row offsets          */
+#define ND_F_FINAL_IDS 1   /* int64 [total] roots + non-NULL sampled ids    */
+#define ND_F_ROOTS 2       /* int64 [n*R] (walks) / ragged (others) roots  */
+#define ND_F_ROOTS_OFF 3   /* int64 [n+1]                                  */
+#define ND_F_CHAIN_LEN 4   /* int64 [n] walk chain lengths (NULL included) */
+#define ND_F_STEP_COUNTS 5 /* int64 [S*n] slots per sample per step        */
+#define ND_F_STEP_VALS 6   /* int64 step-major slot values (NULLs kept)    */
+#define ND_F_REC_COUNTS 7  /* int64 [S*n] recorded edges per sample/step   */
+#define ND_F_REC_T 8       /* int64 recorded edge sources (step-major)     */
+#define ND_F_REC_V 9       /* int64 recorded edge targets                  */
+#define ND_F_STATS 10      /* int64 [S*4] {small, medium, large, fetches}  */
+#define ND_F_CHAIN_VALS 11 /* int64 walk chains incl. NULL (multirw)       */
+int nd_result_info(const nd_result *r, int64_t *n_samples, int64_t *n_steps,
+                   int64_t *total_sampled, int64_t *total_recorded);
+/* device pointer + element count of one field (ptr NULL if absent) */
+int nd_result_field(const nd_result *r, int field, const void **ptr, int64_t *count);
+/* counters for the roofline byte model: {items, pairs, n2v_tries,
+ * n2v_probe_sectors, search_sectors} */
+int nd_result_counters(const nd_result *r, int64_t *host_counters, int64_t n);
+/* copy a field into caller memory (host or device; cudaMemcpyDefault) on
+ * `stream`; synchronous when stream is NULL */
+int nd_result_copy(const nd_result *r, int field, void *dst, void *stream);
+/* event-timed phases when nd_set_profiling(1): {schedule_ms, sample_ms,
+ * compaction_ms, 0} */
+int nd_result_profile(const nd_result *r, double *ms, int64_t n);
+int nd_set_profiling(int on);
+int nd_result_destroy(nd_result *r);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

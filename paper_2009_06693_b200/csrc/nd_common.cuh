@@ -1,0 +1,162 @@
+// nd_common.cuh — shared device primitives for the NextDoor B200 engine.
+//
+// Keyed counter RNG (bit-identical to trawl/rng.py:43-77 and
+// _ckernels.pyx:38-62), exact weighted pick / membership searches
+// (_ckernels.pyx:65-100), the device CSR layout, status codes and the
+// stream-ordered allocator helpers used by every translation unit.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/nextdoor_b200.h"
+
+namespace nd {
+
+// ---- RNG constants (rng.py:22-30) -----------------------------------------
+constexpr uint64_t C_SAMPLE = 0x9E3779B97F4A7C15ull;
+constexpr uint64_t C_STEP = 0xC2B2AE3D27D4EB4Full;
+constexpr uint64_t C_TRANSIT = 0x165667B19E3779F9ull;
+constexpr uint64_t C_SLOT = 0x27D4EB2F165667C5ull;
+constexpr uint64_t C_DOMAIN = 0x85EBCA77C2B2AE63ull;
+constexpr uint64_t C_DRAW = 0xD6E8FEB86659FD93ull;
+constexpr uint64_t MIX_A = 0xBF58476D1CE4E5B9ull;
+constexpr uint64_t MIX_B = 0x94D049BB133111EBull;
+
+constexpr int32_t NULLV = -1;
+constexpr int64_t N2V_MAX_TRIES = 1000000;   // apps.py:35
+constexpr int64_t SMALL_MAX_WORK = 32;       // transit_parallel.py:37
+constexpr int64_t LARGE_MIN_WORK = 1024;     // transit_parallel.py:38
+
+__host__ __device__ __forceinline__ uint64_t fin64(uint64_t z) {
+  z = (z ^ (z >> 30)) * MIX_A;
+  z = (z ^ (z >> 27)) * MIX_B;
+  return z ^ (z >> 31);
+}
+
+// Step/domain/draw part of the Weyl key (seed + C_STEP(step+1) +
+// C_DOMAIN(dom+1) + C_DRAW(draw+1)); _ckernels.pyx:56-58.
+__host__ __device__ __forceinline__ uint64_t key_base(uint64_t seed, uint64_t step,
+                                                      uint64_t domain, uint64_t draw) {
+  return seed + C_STEP * (step + 1) + C_DOMAIN * (domain + 1) + C_DRAW * (draw + 1);
+}
+
+// Per-item part (sample, transit index, slot); _ckernels.pyx:47-53.
+__host__ __device__ __forceinline__ uint64_t key_item(uint64_t sid, uint64_t tix, uint64_t slot) {
+  return C_SAMPLE * (sid + 1) + C_TRANSIT * (tix + 1) + C_SLOT * (slot + 1);
+}
+
+__host__ __device__ __forceinline__ uint64_t draw_u64(uint64_t base, uint64_t item) {
+  return fin64(fin64(base + item));
+}
+
+// (u >> 11) * 2^-53, exact (rng.py:74-77)
+__device__ __forceinline__ double to_unit(uint64_t u) {
+  return __ull2double_rn(u >> 11) * (1.0 / 9007199254740992.0);
+}
+
+// Exact u % d (the reference's uint64 modulo, _ckernels.pyx:222) without the
+// ~70-instruction 64-bit division routine: for d < 2^32 two fp64 quotient
+// estimates (hi word, then the 64-bit remainder-extended low word), each off by
+// at most one and corrected exactly.  Fuzzed against `%` in tests/test_gpu_kernels.py.
+__device__ __forceinline__ uint64_t mod_u64(uint64_t u, uint64_t d) {
+  if (d > 0xFFFFFFFFull) return u % d;
+  const double inv = __drcp_rn((double)d);
+  const int64_t sd = (int64_t)d;
+  uint64_t hi = u >> 32;
+  uint64_t q1 = (uint64_t)__dmul_rz(__ull2double_rn(hi), inv);
+  int64_t r1 = (int64_t)(hi - q1 * d);
+  if (r1 < 0) r1 += sd; else if (r1 >= sd) r1 -= sd;
+  uint64_t x = ((uint64_t)r1 << 32) | (u & 0xFFFFFFFFull);
+  uint64_t q2 = (uint64_t)__dmul_rz(__ull2double_rn(x), inv);
+  int64_t r2 = (int64_t)(x - q2 * d);
+  if (r2 < 0) r2 += sd; else if (r2 >= sd) r2 -= sd;
+  return (uint64_t)r2;
+}
+
+// ---- device CSR -------------------------------------------------------------
+// Layout in HBM: int64 row offsets, int32 column ids (V <
+// 2^31), f64 weights / inclusive per-row prefix / per-row max.  Unit-weight
+// graphs keep neither weights nor prefix: the upper-bound search over the
+// integer prefix 1..deg reduces exactly to floor(r*deg).
+struct DevGraph {
+  int64_t V = 0, E = 0;
+  const int64_t* row = nullptr;
+  const int32_t* col = nullptr;
+  const double* w = nullptr;     // null when unit
+  const double* pre = nullptr;   // null when unit
+  const double* mx = nullptr;
+  int unit = 0;
+};
+
+// first index in [lo, hi) with a[i] > x (upper bound; _ckernels.pyx:65-74)
+__device__ __forceinline__ int64_t upper_bound_f64(const double* __restrict__ a, int64_t lo,
+                                                   int64_t hi, double x) {
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (__ldg(a + mid) <= x) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// lower-bound membership over a sorted int32 row (_ckernels.pyx:77-87)
+__device__ __forceinline__ bool row_contains(const int32_t* __restrict__ a, int64_t lo, int64_t hi,
+                                             int32_t t) {
+  int64_t end = hi;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (__ldg(a + mid) < t) lo = mid + 1; else hi = mid;
+  }
+  return lo < end && __ldg(a + lo) == t;
+}
+
+// Weighted pick (_ckernels.pyx:90-100): idx = upper_bound(prefix, r*total),
+// clamped to the last entry.  Unit weights: prefix[lo+k] = k+1 exactly, so the
+// first entry > r*deg is floor(r*deg).
+__device__ __forceinline__ int64_t weighted_index(const DevGraph& g, int64_t lo, int64_t deg,
+                                                  double r) {
+  if (g.unit) {
+    double x = __dmul_rn(r, (double)deg);
+    int64_t k = (int64_t)x;  // x >= 0, floor
+    return lo + (k < deg - 1 ? k : deg - 1);
+  }
+  double total = __ldg(g.pre + lo + deg - 1);
+  int64_t idx = upper_bound_f64(g.pre, lo, lo + deg, __dmul_rn(r, total));
+  return idx < lo + deg - 1 ? idx : lo + deg - 1;
+}
+
+}  // namespace nd
+
+// ---- error plumbing -----------------------------------------------------------
+#define ND_CUDA_TRY(expr)                                   \
+  do {                                                      \
+    cudaError_t _e = (expr);                                \
+    if (_e != cudaSuccess) {                                \
+      nd_set_last_error(cudaGetErrorString(_e), __FILE__, __LINE__); \
+      return ND_ERR_CUDA;                                   \
+    }                                                       \
+  } while (0)
+
+#define ND_TRY(expr)                  \
+  do {                                \
+    int _rc = (expr);                 \
+    if (_rc != ND_OK) return _rc;     \
+  } while (0)
+
+void nd_set_last_error(const char* msg, const char* file, int line);
+
+// stream-ordered scratch allocation (cudaMallocAsync from the device pool)
+template <typename T>
+inline cudaError_t nd_alloc(T** p, size_t n, cudaStream_t s) {
+  return cudaMallocAsync((void**)p, (n ? n : 1) * sizeof(T), s);
+}
+inline void nd_free(void* p, cudaStream_t s) {
+  if (p) cudaFreeAsync(p, s);
+}
+
+inline int nd_grid(int64_t n, int block, int cap = 148 * 32) {
+  int64_t g = (n + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (int)g;
+}

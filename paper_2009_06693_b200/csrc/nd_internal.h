@@ -1,0 +1,57 @@
+// nd_internal.h — host-side structs shared by the translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <vector>
+
+#include "nd_common.cuh"
+
+struct nd_graph {
+  nd::DevGraph g;       // device views
+  int64_t* row = nullptr;
+  int32_t* col = nullptr;
+  double* w = nullptr;
+  double* pre = nullptr;
+  double* mx = nullptr;
+  int64_t bytes = 0;
+  int device = 0;
+};
+
+constexpr int ND_N_FIELDS = 12;
+constexpr int ND_N_COUNTERS = 8;
+
+struct nd_result {
+  int64_t n = 0;
+  int64_t n_steps = 0;
+  int64_t total_sampled = 0;
+  int64_t total_recorded = 0;
+  void* ptr[ND_N_FIELDS] = {};
+  int64_t cnt[ND_N_FIELDS] = {};
+  int64_t counters[ND_N_COUNTERS] = {};
+  double prof_ms[4] = {};  // schedule, sample, compaction (nd_set_profiling)
+  cudaStream_t stream = nullptr;
+
+  void set(int f, void* p, int64_t c) {
+    ptr[f] = p;
+    cnt[f] = c;
+  }
+};
+
+// counters slots (nd_result_counters)
+enum { NDC_ITEMS = 0, NDC_PAIRS = 1, NDC_N2V_TRIES = 2, NDC_N2V_PROBES = 3, NDC_SEARCH = 4,
+       NDC_PAIR_BYTES = 5, NDC_SLOT_BYTES = 6, NDC_STEPS = 7 };
+
+// app parameters as the kernels see them (_ckernels.pyx:157-181)
+struct NdApp {
+  int code = 0;
+  double term = 0.0;
+  double f_ret = 0.0, f_adj = 0.0, f_far = 0.0, f_max = 0.0;
+};
+
+int nd_make_app(int code, const double* params, int64_t n_params, NdApp* a);
+
+// device counters block reset/read helpers
+int nd_uniform_roots_i32(const nd::DevGraph& g, int64_t count, uint64_t seed, int64_t sample_lo,
+                         int64_t n, int32_t* roots, cudaStream_t s);

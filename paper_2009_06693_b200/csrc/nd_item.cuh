@@ -1,0 +1,157 @@
+// nd_item.cuh — the per-slot `next` of every individual app, on device.
+//
+// One work item = (transit v, previous vertex t, sample id, transit index,
+// slot) exactly as in individual_batch (_ckernels.pyx:184-265, draw protocol
+// _pykernels.py:161-167):
+//   deepwalk  draw 0 -> weighted pick
+//   ppr       draw 0 < term -> NULL, else draw 1 -> weighted pick
+//   khop/mrw  draw 0 -> col[lo + u % deg]
+//   node2vec  t < 0: draw 0 weighted pick; else tries j: draw 2j pick,
+//             draw 2j+1 accept test r*env < w*factor (no FMA: products only)
+// v's row is read through a row source: global memory (GRow) or a copy
+// staged in shared memory by the transit-parallel class kernels (SRow).
+// t's row (node2vec membership) is always read from the global CSR.
+#pragma once
+
+#include "nd_common.cuh"
+#include "nd_internal.h"
+
+namespace nd {
+
+template <typename ColT>
+struct GView {
+  const int64_t* row;
+  const ColT* col;
+  const double* w;    // may be null when unit
+  const double* pre;  // may be null when unit
+  const double* mx;
+  int unit;
+};
+
+__host__ __device__ inline GView<int32_t> view(const DevGraph& g) {
+  return GView<int32_t>{g.row, g.col, g.w, g.pre, g.mx, g.unit};
+}
+
+// v's row in global memory, indexed relative to its start
+template <typename ColT>
+struct GRow {
+  const ColT* col;
+  const double* pre;
+  const double* w;
+  __device__ __forceinline__ int64_t c(int64_t k) const { return (int64_t)__ldg(col + k); }
+  __device__ __forceinline__ double p(int64_t k) const { return __ldg(pre + k); }
+  __device__ __forceinline__ double wt(int64_t k) const { return __ldg(w + k); }
+};
+
+template <typename ColT>
+__device__ __forceinline__ GRow<ColT> grow(const GView<ColT>& g, int64_t lo) {
+  return GRow<ColT>{g.col + lo, g.unit ? nullptr : g.pre + lo, g.unit ? nullptr : g.w + lo};
+}
+
+// v's row staged in shared memory
+struct SRow {
+  const int32_t* col;
+  const double* pre;
+  const double* w;
+  __device__ __forceinline__ int64_t c(int64_t k) const { return (int64_t)col[k]; }
+  __device__ __forceinline__ double p(int64_t k) const { return pre[k]; }
+  __device__ __forceinline__ double wt(int64_t k) const { return w[k]; }
+};
+
+// upper-bound inverse-CDF pick (_ckernels.pyx:65-74, 90-100); returns k in [0, deg)
+template <typename RowT>
+__device__ __forceinline__ int64_t pick_rel(const RowT& r, int unit, int64_t deg, double u01) {
+  if (unit) {
+    double x = __dmul_rn(u01, (double)deg);
+    int64_t k = (int64_t)x;
+    return k < deg - 1 ? k : deg - 1;
+  }
+  const double x = __dmul_rn(u01, r.p(deg - 1));
+  int64_t lo = 0, hi = deg;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (r.p(mid) <= x) lo = mid + 1; else hi = mid;
+  }
+  return lo < deg - 1 ? lo : deg - 1;
+}
+
+template <typename ColT>
+__device__ __forceinline__ bool has_edge(const ColT* __restrict__ a, int64_t lo, int64_t hi,
+                                         int64_t t) {
+  int64_t end = hi;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if ((int64_t)__ldg(a + mid) < t) lo = mid + 1; else hi = mid;
+  }
+  return lo < end && (int64_t)__ldg(a + lo) == t;
+}
+
+// ceil(log2(ceil(deg/4))): binary-search sectors over 8-byte entries (SURVEY §8 d)
+__device__ __forceinline__ int search_sectors(int64_t deg) {
+  int64_t s = (deg + 3) >> 2;
+  if (s <= 1) return 0;
+  return 64 - __clzll(s - 1);
+}
+
+// Algorithmic-byte model of SURVEY §8(d) (S = 32-byte sector): accumulated by
+// the kernels so the roofline numerator is counted, not estimated.
+struct ItemStats {
+  int64_t bytes = 0;
+  int64_t tries = 0;
+};
+constexpr int64_t SECTOR = 32;
+
+// Evaluate one item.  `base0` = key_base(seed, step, 0, 0); `ik` =
+// key_item(sid, tix, slot).  `deg` is v's degree.  Returns the vertex or -1.
+template <typename ColT, typename RowT>
+__device__ __forceinline__ int64_t run_item(const GView<ColT>& g, const RowT& r, const NdApp& a,
+                                            int64_t v, int64_t deg, int64_t t, uint64_t base0,
+                                            uint64_t ik, ItemStats& st, int* stall) {
+  if (deg <= 0) return -1;
+  const int64_t wsec = g.unit ? 0 : SECTOR * search_sectors(deg);
+  switch (a.code) {
+    case ND_DEEPWALK: {
+      st.bytes += SECTOR + wsec + SECTOR + 8;
+      return r.c(pick_rel(r, g.unit, deg, to_unit(draw_u64(base0, ik))));
+    }
+    case ND_PPR: {
+      if (to_unit(draw_u64(base0, ik)) < a.term) return -1;
+      st.bytes += SECTOR + wsec + SECTOR + 8;
+      return r.c(pick_rel(r, g.unit, deg, to_unit(draw_u64(base0 + C_DRAW, ik))));
+    }
+    case ND_KHOP:
+    case ND_MULTIRW: {
+      st.bytes += SECTOR + 8;
+      return r.c((int64_t)mod_u64(draw_u64(base0, ik), (uint64_t)deg));
+    }
+    case ND_NODE2VEC: {
+      if (t < 0) {
+        st.bytes += SECTOR + wsec + SECTOR + 8;
+        return r.c(pick_rel(r, g.unit, deg, to_unit(draw_u64(base0, ik))));
+      }
+      const int64_t t_lo = __ldg(g.row + t), t_hi = __ldg(g.row + t + 1);
+      const double env = __dmul_rn(__ldg(g.mx + v), a.f_max);
+      const int64_t probe = SECTOR * search_sectors(t_hi - t_lo);
+      st.bytes += 2 * SECTOR + 8;
+      uint64_t b = base0;
+      for (int64_t j = 0; j < N2V_MAX_TRIES; j++) {
+        const int64_t k = (int64_t)mod_u64(draw_u64(b, ik), (uint64_t)deg);
+        const int64_t nb = r.c(k);
+        const double w = g.unit ? 1.0 : r.wt(k);
+        double f;
+        st.tries++;
+        st.bytes += 2 * SECTOR + probe;
+        if (nb == t) f = a.f_ret;
+        else f = has_edge(g.col, t_lo, t_hi, nb) ? a.f_adj : a.f_far;
+        const double u01 = to_unit(draw_u64(b + C_DRAW, ik));
+        if (env <= 0.0 || __dmul_rn(u01, env) < __dmul_rn(w, f)) return nb;
+        b += 2 * C_DRAW;
+      }
+      *stall = 1;
+      return -1;
+    }
+  }
+  return -1;
+}
+
+}  // namespace nd

@@ -1,0 +1,557 @@
+// nd_walk.cu — whole-run chain walks on device (engine/chain.py:64-179).
+//
+// DeepWalk / PPR / node2vec: walker state (current transit, packed
+// (walker id, previous transit)) lives in HBM; each step either runs the flat
+// sample-parallel kernel (SP) or the transit-parallel step of nd_tp.cuh (TP).
+// Every item appends a step record (walker, vertex) and, if alive, its next
+// state (warp-aggregated compaction); a NULL result records the walker's
+// death step (chain.py:152-155: walks die after a NULL pick).  After the loop
+// the records are scattered into the compacted final layout
+// (roots, then non-NULL vertices in step order; core.py:116-123).
+//
+// MultiRW (root pick, chain.py:102-108,144-151): every walker is alive every
+// step; the transit is roots[key(domain 1) % R]; the sampled vertex replaces
+// the first root equal to the transit.  Values go to a dense [steps, N] slab.
+#include <cub/cub.cuh>
+
+#include <vector>
+
+#include "nd_tp.cuh"
+
+using namespace nd;
+
+namespace {
+
+struct ChainAct {
+  GView<int32_t> gv;
+  NdApp a;
+  uint64_t base0;
+  int64_t sample_lo;
+  int step;
+  int32_t* rec_w;
+  int32_t* rec_v;
+  uint32_t* ncur;
+  uint64_t* nwp;
+  int* ncount;
+  int32_t* dstep;
+  int* stall;
+
+  template <class RowT>
+  __device__ __forceinline__ void operator()(int64_t i, int64_t v, uint64_t val, const RowT& row,
+                                             int64_t deg, ItemStats& st) const {
+    const int32_t w = (int32_t)(val >> 32);
+    const int64_t t = (int64_t)(int32_t)(uint32_t)(val & 0xFFFFFFFFull);
+    int stl = 0;
+    const int64_t out = run_item(gv, row, a, v, deg, t, base0,
+                                 key_item((uint64_t)(sample_lo + w), 0, 0), st, &stl);
+    if (stl) atomicExch(stall, 1);
+    rec_w[i] = w;
+    rec_v[i] = (int32_t)out;
+    const int64_t slot = warp_append(out >= 0, ncount);
+    if (slot >= 0) {
+      ncur[slot] = (uint32_t)out;
+      nwp[slot] = ((uint64_t)(uint32_t)w << 32) | (uint32_t)v;
+    } else {
+      dstep[w] = step;
+    }
+  }
+};
+
+struct RootPickAct {
+  GView<int32_t> gv;
+  NdApp a;
+  uint64_t base0;
+  int64_t sample_lo;
+  int32_t* roots;  // [N, R] mutated
+  int64_t R;
+  int32_t* slab;   // this step's [N] values
+  int* stall;
+
+  template <class RowT>
+  __device__ __forceinline__ void operator()(int64_t i, int64_t v, uint64_t val, const RowT& row,
+                                             int64_t deg, ItemStats& st) const {
+    const int64_t w = (int64_t)(val >> 32);
+    int stl = 0;
+    const int64_t out = run_item(gv, row, a, v, deg, -1, base0,
+                                 key_item((uint64_t)(sample_lo + w), 0, 0), st, &stl);
+    slab[w] = (int32_t)out;
+    if (out >= 0) {
+      int32_t* rr = roots + w * R;
+      for (int64_t c = 0; c < R; c++)
+        if (rr[c] == (int32_t)v) { rr[c] = (int32_t)out; break; }
+    }
+  }
+};
+
+__global__ void k_init_chain(const int64_t* __restrict__ roots64, const int32_t* __restrict__ roots32,
+                             int64_t n, int64_t R, uint32_t* __restrict__ cur,
+                             uint64_t* __restrict__ wp, int32_t* __restrict__ dstep) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    cur[i] = roots64 ? (uint32_t)roots64[i * R] : (uint32_t)roots32[i * R];
+    wp[i] = ((uint64_t)(uint32_t)i << 32) | 0xFFFFFFFFull;  // prev = NULL
+    dstep[i] = -1;
+  }
+}
+
+// root pick (domain 1): key = roots[w, key_u64(seed, sid, step, 0, 0, 1) % R]
+__global__ void k_rootpick_keys(const int32_t* __restrict__ roots, int64_t n, int64_t R,
+                                uint64_t base1, int64_t sample_lo, uint32_t* __restrict__ keys,
+                                uint64_t* __restrict__ vals) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t u = draw_u64(base1, key_item((uint64_t)(sample_lo + i), 0, 0));
+    const int64_t pick = (int64_t)mod_u64(u, (uint64_t)R);
+    keys[i] = (uint32_t)roots[i * R + pick];
+    vals[i] = (uint64_t)i << 32;
+  }
+}
+
+__global__ void k_chain_lengths(const int32_t* __restrict__ dstep, int64_t n, int64_t R,
+                                int64_t n_steps, int64_t* __restrict__ flen,
+                                int64_t* __restrict__ clen) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (i == n) { flen[n] = 0; continue; }
+    const int32_t d = dstep[i];
+    const int64_t nnz = d >= 0 ? d : n_steps;
+    flen[i] = R + nnz;
+    clen[i] = d >= 0 ? d + 1 : n_steps;
+  }
+}
+
+template <typename RootT>
+__global__ void k_write_roots(const RootT* __restrict__ roots, int64_t n, int64_t R,
+                              const int64_t* __restrict__ off, int64_t* __restrict__ ids,
+                              int64_t* __restrict__ roots_out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * R;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t w = i / R, k = i - w * R;
+    const int64_t r = (int64_t)roots[i];
+    ids[off[w] + k] = r;
+    if (roots_out) roots_out[i] = r;
+  }
+}
+
+__global__ void k_scatter_records(const int32_t* __restrict__ rec_w, const int32_t* __restrict__ rec_v,
+                                  int64_t total, const int64_t* __restrict__ step_base,
+                                  int64_t n_steps, const int64_t* __restrict__ off, int64_t R,
+                                  int64_t* __restrict__ ids) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < total;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = rec_v[r];
+    if (v < 0) continue;
+    int64_t lo = 0, hi = n_steps;  // last step s with step_base[s] <= r
+    while (hi - lo > 1) {
+      int64_t mid = (lo + hi) >> 1;
+      if (step_base[mid] <= r) lo = mid; else hi = mid;
+    }
+    ids[off[rec_w[r]] + R + lo] = v;
+  }
+}
+
+// multirw: per-walker non-NULL counts over the slab, then the final rows
+__global__ void k_slab_counts(const int32_t* __restrict__ slab, int64_t n, int64_t S, int64_t R,
+                              int64_t* __restrict__ flen) {
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w <= n;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    if (w == n) { flen[n] = 0; continue; }
+    int64_t c = 0;
+    for (int64_t s = 0; s < S; s++) c += slab[s * n + w] >= 0;
+    flen[w] = R + c;
+  }
+}
+
+__global__ void k_slab_write(const int32_t* __restrict__ slab, int64_t n, int64_t S, int64_t R,
+                             const int64_t* __restrict__ off, int64_t* __restrict__ ids,
+                             int64_t* __restrict__ chain) {
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < n;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    int64_t p = off[w] + R;
+    for (int64_t s = 0; s < S; s++) {
+      const int32_t v = slab[s * n + w];
+      if (chain) chain[w * S + s] = v;
+      if (v >= 0) ids[p++] = v;
+    }
+  }
+}
+
+__global__ void k_stats_fetch(unsigned long long* stats, unsigned long long n) { stats[3] += n; }
+
+struct Profiler {
+  bool on = false;
+  cudaStream_t s;
+  std::vector<cudaEvent_t> ev;
+  double sched_ms = 0, sample_ms = 0, final_ms = 0;
+  void mark() {
+    if (!on) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, s);
+    ev.push_back(e);
+  }
+  float between(size_t a, size_t b) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, ev[a], ev[b]);
+    return ms;
+  }
+  void destroy() {
+    for (auto e : ev) cudaEventDestroy(e);
+  }
+};
+
+}  // namespace
+
+static int g_profile = 0;
+extern "C" int nd_set_profiling(int on) {
+  g_profile = on;
+  return ND_OK;
+}
+
+// byte-model counters (see nd_item.cuh): ctr[0]=bytes, ctr[1]=tries
+static int run_chain_walk(const nd_graph* G, const NdApp& a, int64_t sample_lo, int64_t n,
+                          const int64_t* roots, int64_t R, uint64_t seed, int64_t steps,
+                          int64_t step_cap, int paradigm, cudaStream_t s, nd_result* res) {
+  const DevGraph& g = G->g;
+  const int key_bits = key_bits_for(g.V);
+  uint32_t *cur0 = nullptr, *cur1 = nullptr;
+  uint64_t *wp0 = nullptr, *wp1 = nullptr;
+  int32_t *dstep = nullptr, *rec_w = nullptr, *rec_v = nullptr, *roots32 = nullptr;
+  int* ncount = nullptr;
+  int* stall = nullptr;
+  unsigned long long* ctr = nullptr;
+  unsigned long long* stats = nullptr;
+  const int64_t max_steps = steps >= 0 ? (steps < step_cap ? steps : step_cap) : step_cap;
+  int64_t rec_cap = 0;
+  TPScratch S;
+  ND_CUDA_TRY(nd_alloc(&cur0, n, s));
+  ND_CUDA_TRY(nd_alloc(&cur1, n, s));
+  ND_CUDA_TRY(nd_alloc(&wp0, n, s));
+  ND_CUDA_TRY(nd_alloc(&wp1, n, s));
+  ND_CUDA_TRY(nd_alloc(&dstep, n, s));
+  ND_CUDA_TRY(nd_alloc(&ncount, 1, s));
+  ND_CUDA_TRY(nd_alloc(&stall, 1, s));
+  ND_CUDA_TRY(nd_alloc(&ctr, 4, s));
+  ND_CUDA_TRY(nd_alloc(&stats, 4 * (max_steps + 1), s));
+  ND_CUDA_TRY(cudaMemsetAsync(ctr, 0, 4 * sizeof(unsigned long long), s));
+  ND_CUDA_TRY(cudaMemsetAsync(stats, 0, 4 * (max_steps + 1) * sizeof(unsigned long long), s));
+  ND_CUDA_TRY(cudaMemsetAsync(stall, 0, sizeof(int), s));
+  if (paradigm == ND_TP) ND_TRY(S.alloc(n, key_bits, s));
+  if (!roots) {
+    ND_CUDA_TRY(nd_alloc(&roots32, n * R, s));
+    ND_TRY(nd_uniform_roots_i32(g, R, seed, sample_lo, n, roots32, s));
+  }
+  if (n) k_init_chain<<<nd_grid(n, 256), 256, 0, s>>>(roots, roots32, n, R, cur0, wp0, dstep);
+  rec_cap = steps >= 0 ? n * max_steps : n * 128;
+  ND_CUDA_TRY(nd_alloc(&rec_w, rec_cap, s));
+  ND_CUDA_TRY(nd_alloc(&rec_v, rec_cap, s));
+
+  Profiler prof;
+  prof.on = g_profile;
+  prof.s = s;
+  std::vector<int64_t> step_base;
+  int64_t A = n, rec_base = 0, step = 0;
+  uint32_t* cur_in = cur0;
+  uint64_t* wp_in = wp0;
+  uint32_t* cur_alt = cur1;
+  uint64_t* wp_alt = wp1;
+  int* h_count = nullptr;
+  ND_CUDA_TRY(cudaMallocHost(&h_count, sizeof(int)));
+  double sched_ms = 0, sample_ms = 0;
+  while (A > 0) {
+    if (steps >= 0 && step >= steps) break;
+    if (step >= step_cap) break;
+    if (rec_base + A > rec_cap) {
+      int64_t nc = rec_cap * 2 > rec_base + A ? rec_cap * 2 : rec_base + A;
+      int32_t *nw = nullptr, *nv = nullptr;
+      ND_CUDA_TRY(nd_alloc(&nw, nc, s));
+      ND_CUDA_TRY(nd_alloc(&nv, nc, s));
+      ND_CUDA_TRY(cudaMemcpyAsync(nw, rec_w, rec_base * 4, cudaMemcpyDeviceToDevice, s));
+      ND_CUDA_TRY(cudaMemcpyAsync(nv, rec_v, rec_base * 4, cudaMemcpyDeviceToDevice, s));
+      nd_free(rec_w, s);
+      nd_free(rec_v, s);
+      rec_w = nw;
+      rec_v = nv;
+      rec_cap = nc;
+    }
+    ND_CUDA_TRY(cudaMemsetAsync(ncount, 0, sizeof(int), s));
+    size_t e0 = prof.ev.size();
+    prof.mark();
+    const int need_pre = !g.unit && (a.code == ND_DEEPWALK || a.code == ND_PPR ||
+                                     (a.code == ND_NODE2VEC && step == 0));
+    const int need_w = !g.unit && a.code == ND_NODE2VEC && step > 0;
+    unsigned long long* st_step = stats + 4 * step;
+    if (paradigm == ND_TP) {
+      cub::DoubleBuffer<uint32_t> dk(cur_in, cur_alt);
+      cub::DoubleBuffer<uint64_t> dv(wp_in, wp_alt);
+      ND_TRY(tp_sort(dk, dv, A, key_bits, S, s));
+      prof.mark();
+      // the sorted state is Current(); the next state is written to Alternate()
+      ChainAct act{view(g), a, key_base(seed, (uint64_t)step, 0, 0), sample_lo, (int)step,
+                   rec_w + rec_base, rec_v + rec_base, dk.Alternate(), dv.Alternate(), ncount,
+                   dstep, stall};
+      ND_TRY(tp_run_sorted(dk.Current(), dv.Current(), A, 1, g, stage_spec(need_pre, need_w), act,
+                           S, ctr, st_step, s));
+      cur_in = dk.Alternate();
+      wp_in = dv.Alternate();
+      cur_alt = dk.Current();
+      wp_alt = dv.Current();
+    } else {
+      prof.mark();
+      ChainAct act{view(g), a, key_base(seed, (uint64_t)step, 0, 0), sample_lo, (int)step,
+                   rec_w + rec_base, rec_v + rec_base, cur_alt, wp_alt, ncount, dstep, stall};
+      ND_TRY(sp_step(cur_in, wp_in, A, g, act, ctr, st_step, s));
+      k_stats_fetch<<<1, 1, 0, s>>>(st_step, (unsigned long long)A);
+      std::swap(cur_in, cur_alt);
+      std::swap(wp_in, wp_alt);
+    }
+    prof.mark();
+    ND_CUDA_TRY(cudaMemcpyAsync(h_count, ncount, sizeof(int), cudaMemcpyDeviceToHost, s));
+    ND_CUDA_TRY(cudaStreamSynchronize(s));
+    if (prof.on) {
+      sched_ms += prof.between(e0, e0 + 1);
+      sample_ms += prof.between(e0 + 1, e0 + 2);
+    }
+    step_base.push_back(rec_base);
+    rec_base += A;
+    A = *h_count;
+    step++;
+  }
+  cudaFreeHost(h_count);
+  const int64_t n_steps = step;
+  step_base.push_back(rec_base);
+  // ---- output compaction -----------------------------------------------------------
+  prof.mark();
+  const size_t ef = prof.ev.size() - 1;
+  int64_t *flen = nullptr, *final_off = nullptr, *clen = nullptr, *final_ids = nullptr,
+          *roots_out = nullptr, *d_step_base = nullptr;
+  ND_CUDA_TRY(nd_alloc(&flen, n + 1, s));
+  ND_CUDA_TRY(nd_alloc(&final_off, n + 1, s));
+  ND_CUDA_TRY(nd_alloc(&clen, n, s));
+  ND_CUDA_TRY(nd_alloc(&roots_out, n * R, s));
+  ND_CUDA_TRY(nd_alloc(&d_step_base, n_steps + 1, s));
+  ND_CUDA_TRY(cudaMemcpyAsync(d_step_base, step_base.data(), (n_steps + 1) * sizeof(int64_t),
+                              cudaMemcpyHostToDevice, s));
+  k_chain_lengths<<<nd_grid(n + 1, 256), 256, 0, s>>>(dstep, n, R, n_steps, flen, clen);
+  {
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, flen, final_off, n + 1, s);
+    void* tmp = nullptr;
+    ND_CUDA_TRY(nd_alloc((char**)&tmp, tb, s));
+    ND_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tb, flen, final_off, n + 1, s));
+    nd_free(tmp, s);
+  }
+  int64_t total = 0;
+  ND_CUDA_TRY(cudaMemcpyAsync(&total, final_off + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  ND_CUDA_TRY(cudaStreamSynchronize(s));
+  ND_CUDA_TRY(nd_alloc(&final_ids, total, s));
+  if (n) {
+    if (roots)
+      k_write_roots<int64_t><<<nd_grid(n * R, 256), 256, 0, s>>>(roots, n, R, final_off, final_ids,
+                                                                roots_out);
+    else
+      k_write_roots<int32_t><<<nd_grid(n * R, 256), 256, 0, s>>>(roots32, n, R, final_off,
+                                                                final_ids, roots_out);
+  }
+  if (rec_base)
+    k_scatter_records<<<nd_grid(rec_base, 256, 148 * 64), 256, 0, s>>>(
+        rec_w, rec_v, rec_base, d_step_base, n_steps, final_off, R, final_ids);
+  prof.mark();
+  ND_CUDA_TRY(cudaGetLastError());
+  int h_stall = 0;
+  unsigned long long h_ctr[4];
+  ND_CUDA_TRY(cudaMemcpyAsync(&h_stall, stall, sizeof(int), cudaMemcpyDeviceToHost, s));
+  ND_CUDA_TRY(cudaMemcpyAsync(h_ctr, ctr, sizeof(h_ctr), cudaMemcpyDeviceToHost, s));
+  ND_CUDA_TRY(cudaStreamSynchronize(s));
+  if (prof.on) res->counters[NDC_STEPS] = 0;
+  double final_ms = prof.on ? prof.between(ef, ef + 1) : 0.0;
+  prof.destroy();
+
+  // stats as int64 (unsigned long long has the same layout)
+  res->n = n;
+  res->n_steps = n_steps;
+  res->total_sampled = total - n * R;
+  res->set(ND_F_FINAL_OFF, final_off, n + 1);
+  res->set(ND_F_FINAL_IDS, final_ids, total);
+  res->set(ND_F_ROOTS, roots_out, n * R);
+  res->set(ND_F_CHAIN_LEN, clen, n);
+  res->set(ND_F_STATS, stats, 4 * n_steps);
+  res->counters[NDC_ITEMS] = rec_base;
+  res->counters[NDC_PAIRS] = rec_base;
+  res->counters[NDC_N2V_TRIES] = (int64_t)h_ctr[1];
+  res->counters[NDC_SLOT_BYTES] = (int64_t)h_ctr[0];
+  res->counters[NDC_STEPS] = n_steps;
+  res->prof_ms[0] = sched_ms;
+  res->prof_ms[1] = sample_ms;
+  res->prof_ms[2] = final_ms;
+
+  nd_free(cur0, s); nd_free(cur1, s); nd_free(wp0, s); nd_free(wp1, s);
+  nd_free(dstep, s); nd_free(ncount, s); nd_free(stall, s); nd_free(ctr, s);
+  nd_free(rec_w, s); nd_free(rec_v, s); nd_free(roots32, s); nd_free(flen, s);
+  nd_free(d_step_base, s);
+  if (paradigm == ND_TP) S.release(s);
+  return h_stall ? ND_ERR_STALL : ND_OK;
+}
+
+__global__ void k_narrow(const int64_t* __restrict__ in, int64_t n, int32_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (int32_t)in[i];
+}
+
+static int run_rootpick_walk(const nd_graph* G, const NdApp& a, int64_t sample_lo, int64_t n,
+                             const int64_t* roots, int64_t R, uint64_t seed, int64_t steps,
+                             int64_t step_cap, int paradigm, cudaStream_t s, nd_result* res) {
+  const DevGraph& g = G->g;
+  const int key_bits = key_bits_for(g.V);
+  const int64_t S_ = steps >= 0 ? (steps < step_cap ? steps : step_cap) : step_cap;
+  const int64_t n_steps = (n > 0 && R > 0) ? S_ : 0;
+  int32_t *roots32 = nullptr, *slab = nullptr;
+  uint32_t *k0 = nullptr, *k1 = nullptr;
+  uint64_t *v0 = nullptr, *v1 = nullptr;
+  int* stall = nullptr;
+  unsigned long long *ctr = nullptr, *stats = nullptr;
+  TPScratch S;
+  ND_CUDA_TRY(nd_alloc(&roots32, n * R, s));
+  ND_CUDA_TRY(nd_alloc(&slab, n * (n_steps ? n_steps : 1), s));
+  ND_CUDA_TRY(nd_alloc(&k0, n, s));
+  ND_CUDA_TRY(nd_alloc(&k1, n, s));
+  ND_CUDA_TRY(nd_alloc(&v0, n, s));
+  ND_CUDA_TRY(nd_alloc(&v1, n, s));
+  ND_CUDA_TRY(nd_alloc(&stall, 1, s));
+  ND_CUDA_TRY(nd_alloc(&ctr, 4, s));
+  ND_CUDA_TRY(nd_alloc(&stats, 4 * (n_steps + 1), s));
+  ND_CUDA_TRY(cudaMemsetAsync(ctr, 0, 4 * sizeof(unsigned long long), s));
+  ND_CUDA_TRY(cudaMemsetAsync(stats, 0, 4 * (n_steps + 1) * sizeof(unsigned long long), s));
+  ND_CUDA_TRY(cudaMemsetAsync(stall, 0, sizeof(int), s));
+  if (roots) {
+    if (n * R) k_narrow<<<nd_grid(n * R, 256), 256, 0, s>>>(roots, n * R, roots32);
+  } else {
+    ND_TRY(nd_uniform_roots_i32(g, R, seed, sample_lo, n, roots32, s));
+  }
+  if (paradigm == ND_TP) ND_TRY(S.alloc(n, key_bits, s));
+  Profiler prof;
+  prof.on = g_profile;
+  prof.s = s;
+  double sched_ms = 0, sample_ms = 0;
+  for (int64_t step = 0; step < n_steps; step++) {
+    size_t e0 = prof.ev.size();
+    prof.mark();
+    k_rootpick_keys<<<nd_grid(n, 256), 256, 0, s>>>(roots32, n, R, key_base(seed, step, 1, 0),
+                                                     sample_lo, k0, v0);
+    RootPickAct act{view(g), a, key_base(seed, (uint64_t)step, 0, 0), sample_lo, roots32, R,
+                    slab + step * n, stall};
+    unsigned long long* st_step = stats + 4 * step;
+    if (paradigm == ND_TP) {
+      cub::DoubleBuffer<uint32_t> dk(k0, k1);
+      cub::DoubleBuffer<uint64_t> dv(v0, v1);
+      ND_TRY(tp_sort(dk, dv, n, key_bits, S, s));
+      prof.mark();
+      ND_TRY(tp_run_sorted(dk.Current(), dv.Current(), n, 1, g, stage_spec(0, 0), act, S, ctr,
+                           st_step, s));
+    } else {
+      prof.mark();
+      ND_TRY(sp_step(k0, v0, n, g, act, ctr, st_step, s));
+      k_stats_fetch<<<1, 1, 0, s>>>(st_step, (unsigned long long)n);
+    }
+    prof.mark();
+    if (prof.on) {
+      ND_CUDA_TRY(cudaStreamSynchronize(s));
+      sched_ms += prof.between(e0, e0 + 1);
+      sample_ms += prof.between(e0 + 1, e0 + 2);
+    }
+  }
+  prof.mark();
+  const size_t ef = prof.ev.size() - 1;
+  int64_t *flen = nullptr, *final_off = nullptr, *final_ids = nullptr, *roots_out = nullptr,
+          *chain = nullptr, *clen = nullptr;
+  ND_CUDA_TRY(nd_alloc(&flen, n + 1, s));
+  ND_CUDA_TRY(nd_alloc(&final_off, n + 1, s));
+  ND_CUDA_TRY(nd_alloc(&roots_out, n * R, s));
+  ND_CUDA_TRY(nd_alloc(&chain, n * n_steps, s));
+  ND_CUDA_TRY(nd_alloc(&clen, n, s));
+  k_slab_counts<<<nd_grid(n + 1, 256), 256, 0, s>>>(slab, n, n_steps, R, flen);
+  {
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, flen, final_off, n + 1, s);
+    void* tmp = nullptr;
+    ND_CUDA_TRY(nd_alloc((char**)&tmp, tb, s));
+    ND_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tb, flen, final_off, n + 1, s));
+    nd_free(tmp, s);
+  }
+  int64_t total = 0;
+  ND_CUDA_TRY(cudaMemcpyAsync(&total, final_off + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  ND_CUDA_TRY(cudaStreamSynchronize(s));
+  ND_CUDA_TRY(nd_alloc(&final_ids, total, s));
+  if (n * R)
+    k_write_roots<int32_t><<<nd_grid(n * R, 256), 256, 0, s>>>(roots32, n, R, final_off, final_ids,
+                                                              roots_out);
+  if (n) k_slab_write<<<nd_grid(n, 128), 128, 0, s>>>(slab, n, n_steps, R, final_off, final_ids, chain);
+  {
+    std::vector<int64_t> h(n, n_steps);
+    if (n) ND_CUDA_TRY(cudaMemcpyAsync(clen, h.data(), n * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    prof.mark();
+    unsigned long long h_ctr[4];
+    ND_CUDA_TRY(cudaMemcpyAsync(h_ctr, ctr, sizeof(h_ctr), cudaMemcpyDeviceToHost, s));
+    ND_CUDA_TRY(cudaStreamSynchronize(s));
+    res->counters[NDC_N2V_TRIES] = (int64_t)h_ctr[1];
+    res->counters[NDC_SLOT_BYTES] = (int64_t)h_ctr[0];
+  }
+  ND_CUDA_TRY(cudaGetLastError());
+  res->prof_ms[0] = sched_ms;
+  res->prof_ms[1] = sample_ms;
+  res->prof_ms[2] = prof.on ? prof.between(ef, ef + 1) : 0.0;
+  prof.destroy();
+  res->n = n;
+  res->n_steps = n_steps;
+  res->total_sampled = total - n * R;
+  res->set(ND_F_FINAL_OFF, final_off, n + 1);
+  res->set(ND_F_FINAL_IDS, final_ids, total);
+  res->set(ND_F_ROOTS, roots_out, n * R);
+  res->set(ND_F_CHAIN_LEN, clen, n);
+  res->set(ND_F_CHAIN_VALS, chain, n * n_steps);
+  res->set(ND_F_STATS, stats, 4 * n_steps);
+  res->counters[NDC_ITEMS] = n * n_steps;
+  res->counters[NDC_PAIRS] = n * n_steps;
+  res->counters[NDC_STEPS] = n_steps;
+  nd_free(roots32, s); nd_free(slab, s); nd_free(k0, s); nd_free(k1, s); nd_free(v0, s);
+  nd_free(v1, s); nd_free(stall, s); nd_free(ctr, s); nd_free(flen, s);
+  if (paradigm == ND_TP) S.release(s);
+  return ND_OK;
+}
+
+extern "C" int nd_run_walk(const nd_graph* g, int app_code, const double* host_params,
+                           int64_t n_params, int64_t sample_lo, int64_t n_samples,
+                           const int64_t* roots, int64_t roots_per_sample, uint64_t seed,
+                           int64_t steps, int64_t step_cap, int paradigm, void* stream,
+                           nd_result** out) {
+  NdApp a;
+  ND_TRY(nd_make_app(app_code, host_params, n_params, &a));
+  if (!g || n_samples < 0 || roots_per_sample < 1 || step_cap < 0 || sample_lo < 0)
+    return ND_ERR_ARG;
+  if (n_samples >= (1ll << 31)) return ND_ERR_ARG;
+  if (app_code == ND_KHOP) return ND_ERR_ARG;  // multi-slot: nd_run_individual
+  cudaStream_t s = (cudaStream_t)stream;
+  nd_result* res = new nd_result();
+  res->stream = s;
+  int rc;
+  if (app_code == ND_MULTIRW)
+    rc = run_rootpick_walk(g, a, sample_lo, n_samples, roots, roots_per_sample, seed, steps,
+                           step_cap, paradigm, s, res);
+  else
+    rc = run_chain_walk(g, a, sample_lo, n_samples, roots, roots_per_sample, seed, steps,
+                        step_cap, paradigm, s, res);
+  if (rc != ND_OK) {
+    cudaStreamSynchronize(s);
+    nd_result_destroy(res);
+    return rc;
+  }
+  *out = res;
+  return ND_OK;
+}
+
+extern "C" int nd_result_profile(const nd_result* r, double* ms, int64_t n) {
+  if (!r) return ND_ERR_ARG;
+  for (int64_t i = 0; i < n && i < 4; i++) ms[i] = r->prof_ms[i];
+  return ND_OK;
+}

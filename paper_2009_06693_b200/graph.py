@@ -1,0 +1,325 @@
+"""CSR graphs: the host mirror of trawl.graph.Graph and the HBM-resident
+device graph the engine samples from.
+
+``Graph`` keeps the reference's field names (graph.py:36-55) so reference
+``Graph`` objects and ours are interchangeable inputs.  ``DeviceGraph`` is the
+handle of a CSR resident in HBM (int64 row offsets, int32 columns, f64
+weights / inclusive per-row prefix / per-row max; unit-weight graphs store
+neither weights nor prefix).  It is built from host arrays, from an edge list
+on device (stable (src, dst) radix sort = from_edges' lexsort), or by the
+keyed RMAT generator directly on device.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import struct
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .errors import EmptyGraphError, GraphParseError, NoNeighborsError
+from .rng import DOMAIN_EDGE_WEIGHT, key_uniform
+
+CACHE_MAGIC = b"NDGR"
+CACHE_VERSION = 1
+
+
+@dataclass
+class Graph:
+    """Host CSR with the reference field names.  ``per_vertex_*`` are computed
+    on the GPU (nd_segmented_prefix_sum / nd_segment_max) on first use."""
+
+    n_vertices: int
+    row_offsets: np.ndarray
+    col_indices: np.ndarray
+    weights: np.ndarray
+    remap: np.ndarray
+    _prefix: np.ndarray | None = field(default=None, repr=False)
+    _max: np.ndarray | None = field(default=None, repr=False)
+    _device: "DeviceGraph | None" = field(default=None, repr=False)
+
+    @property
+    def n_edges(self) -> int:
+        return len(self.col_indices)
+
+    @property
+    def per_vertex_weight_prefix(self) -> np.ndarray:
+        if self._prefix is None:
+            from .kernels import segmented_prefix_sum
+            self._prefix = segmented_prefix_sum(self.weights, self.row_offsets)
+        return self._prefix
+
+    @property
+    def per_vertex_max_weight(self) -> np.ndarray:
+        if self._max is None:
+            from .kernels import segment_max
+            self._max = segment_max(self.weights, self.row_offsets)
+        return self._max
+
+    def degree(self, v: int) -> int:
+        return int(self.row_offsets[v + 1] - self.row_offsets[v])
+
+    def degrees(self) -> np.ndarray:
+        return self.row_offsets[1:] - self.row_offsets[:-1]
+
+    def neighbors(self, v: int):
+        lo, hi = self.row_offsets[v], self.row_offsets[v + 1]
+        return self.col_indices[lo:hi], self.weights[lo:hi]
+
+    def has_edge(self, v: int, u: int) -> bool:
+        lo, hi = self.row_offsets[v], self.row_offsets[v + 1]
+        i = lo + np.searchsorted(self.col_indices[lo:hi], u, side="left")
+        return bool(i < hi and self.col_indices[i] == u)
+
+    def weighted_pick(self, v: int, r: float) -> int:
+        lo, hi = int(self.row_offsets[v]), int(self.row_offsets[v + 1])
+        if hi <= lo:
+            raise NoNeighborsError(f"vertex {v} has no outgoing edges")
+        pre = self.per_vertex_weight_prefix
+        idx = lo + int(np.searchsorted(pre[lo:hi], r * pre[hi - 1], side="right"))
+        return int(self.col_indices[min(idx, hi - 1)])
+
+    def to_device(self) -> "DeviceGraph":
+        if self._device is None:
+            self._device = DeviceGraph.from_arrays(self.row_offsets, self.col_indices, self.weights,
+                                                   remap=self.remap)
+        return self._device
+
+
+def from_edges(src, dst, weights=None, n_vertices=None, remap=None) -> Graph:
+    """Host CSR build with from_edges semantics (graph.py:107-129): rows
+    dst-sorted, parallel edges stable in input order."""
+    src = np.asarray(src, dtype=np.int64)
+    dst = np.asarray(dst, dtype=np.int64)
+    if n_vertices is None:
+        n_vertices = int(max(src.max(initial=-1), dst.max(initial=-1)) + 1)
+    w = np.ones(len(src)) if weights is None else np.asarray(weights, dtype=np.float64)
+    if (w < 0).any():
+        raise ValueError("edge weights must be non-negative")
+    order = np.lexsort((dst, src))
+    row = np.zeros(n_vertices + 1, dtype=np.int64)
+    np.add.at(row, src + 1, 1)
+    np.cumsum(row, out=row)
+    rm = np.arange(n_vertices, dtype=np.int64) if remap is None else np.asarray(remap, np.int64)
+    return Graph(n_vertices, row, np.ascontiguousarray(dst[order]),
+                 np.ascontiguousarray(w[order]), rm)
+
+
+def load_edge_list(path, weighted=False, default_weight_range=(1.0, 5.0), undirected=False,
+                   seed=0) -> Graph:
+    """Edge-list parser with the reference's rules (graph.py:132-188):
+    '#' comments, 2 or 3 fields, ids compacted onto [0, n) with the original
+    ids in ``remap``, missing weights keyed on (seed, line number)."""
+    srcs, dsts, wts = [], [], []
+    lo_w, hi_w = float(default_weight_range[0]), float(default_weight_range[1])
+    with open(path, "r", encoding="utf-8") as fh:
+        for line_no, raw in enumerate(fh, start=1):
+            line = raw.strip()
+            if not line or line.startswith("#"):
+                continue
+            parts = line.split()
+            if len(parts) not in (2, 3):
+                raise GraphParseError(line_no, f"expected 2 or 3 fields, got {len(parts)}")
+            try:
+                s, d = int(parts[0]), int(parts[1])
+            except ValueError as exc:
+                raise GraphParseError(line_no, f"bad vertex id: {exc}") from None
+            if s < 0 or d < 0:
+                raise GraphParseError(line_no, "vertex ids must be non-negative")
+            if weighted:
+                if len(parts) == 3:
+                    try:
+                        w = float(parts[2])
+                    except ValueError as exc:
+                        raise GraphParseError(line_no, f"bad weight: {exc}") from None
+                    if w < 0:
+                        raise GraphParseError(line_no, "weight must be non-negative")
+                else:
+                    w = lo_w + (hi_w - lo_w) * key_uniform(seed, sample_id=line_no,
+                                                           domain=DOMAIN_EDGE_WEIGHT)
+            else:
+                w = 1.0
+            srcs.append(s); dsts.append(d); wts.append(w)
+            if undirected:
+                srcs.append(d); dsts.append(s); wts.append(w)
+    if not srcs:
+        raise EmptyGraphError(f"{path}: no edges found")
+    src = np.asarray(srcs, dtype=np.int64)
+    dst = np.asarray(dsts, dtype=np.int64)
+    original = np.unique(np.concatenate([src, dst]))
+    return from_edges(np.searchsorted(original, src), np.searchsorted(original, dst),
+                      np.asarray(wts), n_vertices=len(original), remap=original)
+
+
+def save_cache(graph, path) -> None:
+    """NDGR binary cache (graph.py:191-201)."""
+    with open(path, "wb") as fh:
+        fh.write(CACHE_MAGIC)
+        fh.write(struct.pack("<I", CACHE_VERSION))
+        fh.write(struct.pack("<QQ", graph.n_vertices, len(graph.col_indices)))
+        for a, dt in ((graph.row_offsets, "<i8"), (graph.col_indices, "<i8"),
+                      (graph.weights, "<f8"), (graph.remap, "<i8")):
+            fh.write(np.asarray(a).astype(dt).tobytes())
+
+
+def load_cache(path) -> Graph:
+    with open(path, "rb") as fh:
+        magic = fh.read(4)
+        if magic != CACHE_MAGIC:
+            raise GraphParseError(1, f"bad magic {magic!r}, expected {CACHE_MAGIC!r}")
+        (version,) = struct.unpack("<I", fh.read(4))
+        if version != CACHE_VERSION:
+            raise GraphParseError(1, f"unsupported cache version {version}")
+        n, m = struct.unpack("<QQ", fh.read(16))
+        row = np.frombuffer(fh.read(8 * (n + 1)), dtype="<i8").astype(np.int64)
+        col = np.frombuffer(fh.read(8 * m), dtype="<i8").astype(np.int64)
+        w = np.frombuffer(fh.read(8 * m), dtype="<f8").astype(np.float64)
+        rm = np.frombuffer(fh.read(8 * n), dtype="<i8").astype(np.int64)
+    return Graph(int(n), row, col, w, rm)
+
+
+class _CudaArray:
+    """__cuda_array_interface__ shim: zero-copy torch views of ABI buffers."""
+
+    def __init__(self, ptr: int, n: int, typestr: str, owner):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr,
+                                         "data": (ptr, False), "version": 3}
+        self._owner = owner
+
+
+def device_view(ptr, n, dtype, owner):
+    import torch
+    typestr = {"int64": "<i8", "int32": "<i4", "float64": "<f8", "uint64": "<u8"}[dtype]
+    if n == 0 or not ptr:
+        return torch.empty(0, dtype=getattr(torch, dtype), device="cuda")
+    return torch.as_tensor(_CudaArray(int(ptr), int(n), typestr, owner), device="cuda")
+
+
+class DeviceGraph:
+    """Handle of a CSR resident in HBM (nd_graph_*)."""
+
+    def __init__(self, handle, remap=None):
+        self._h = handle
+        L = _lib.load()
+        V, E, B = C.c_int64(), C.c_int64(), C.c_int64()
+        unit = C.c_int()
+        _lib.check(L.nd_graph_info(handle, C.byref(V), C.byref(E), C.byref(unit), C.byref(B)))
+        self.n_vertices = V.value
+        self.n_edges = E.value
+        self.unit_weights = bool(unit.value)
+        self.bytes = B.value
+        self._remap = remap
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def remap(self):
+        return self._remap
+
+    @classmethod
+    def from_arrays(cls, row_offsets, col_indices, weights=None, prefix=None, max_w=None,
+                    remap=None, stream=None) -> "DeviceGraph":
+        torch = _lib.require_cuda()
+        L = _lib.load()
+        on_host = not (hasattr(row_offsets, "is_cuda") and row_offsets.is_cuda)
+        conv = (lambda a, dt: None if a is None else np.ascontiguousarray(a, dtype=dt)) if on_host \
+            else (lambda a, dt: None if a is None else a.contiguous())
+        row = conv(row_offsets, np.int64)
+        col = conv(col_indices, np.int64)
+        w = conv(weights, np.float64)
+        pre = conv(prefix, np.float64)
+        mx = conv(max_w, np.float64)
+        h = C.c_void_p()
+        _lib.check(L.nd_graph_create(_lib.ptr(row), _lib.ptr(col), _lib.ptr(w), _lib.ptr(pre),
+                                     _lib.ptr(mx), len(row) - 1, len(col), int(on_host),
+                                     _lib.stream_ptr(stream), C.byref(h)), "nd_graph_create")
+        return cls(h, remap)
+
+    @classmethod
+    def from_graph(cls, g) -> "DeviceGraph":
+        """Upload a reference-shaped Graph (ours or trawl's)."""
+        if isinstance(g, DeviceGraph):
+            return g
+        if isinstance(g, Graph):
+            return g.to_device()
+        pre = getattr(g, "per_vertex_weight_prefix", None)
+        mx = getattr(g, "per_vertex_max_weight", None)
+        return cls.from_arrays(g.row_offsets, g.col_indices, g.weights, pre, mx,
+                               remap=getattr(g, "remap", None))
+
+    @classmethod
+    def from_edges(cls, src, dst, weights, n_vertices, stream=None) -> "DeviceGraph":
+        """Device CSR build (stable radix sort of (src, dst))."""
+        torch = _lib.require_cuda()
+        L = _lib.load()
+        t = lambda a, dt: None if a is None else torch.as_tensor(a, dtype=dt, device="cuda").contiguous()
+        s, d = t(src, torch.int64), t(dst, torch.int64)
+        w = t(weights, torch.float64)
+        h = C.c_void_p()
+        _lib.check(L.nd_graph_from_edges(_lib.ptr(s), _lib.ptr(d), _lib.ptr(w), len(s),
+                                         int(n_vertices), _lib.stream_ptr(stream), C.byref(h)),
+                   "nd_graph_from_edges")
+        return cls(h)
+
+    @classmethod
+    def rmat(cls, scale, edge_factor=16, seed=0, undirected=False, weighted=True,
+             abc=(0.57, 0.19, 0.19), n_edges=None, stream=None) -> "DeviceGraph":
+        """Keyed RMAT generated and built on device."""
+        _lib.require_cuda()
+        L = _lib.load()
+        a, b, c = abc
+        ta, tab, tabc = int(a * 65536), int((a + b) * 65536), int((a + b + c) * 65536)
+        m = n_edges if n_edges is not None else (1 << scale) * edge_factor
+        h = C.c_void_p()
+        _lib.check(L.nd_graph_rmat(int(scale), int(m), ta, tab, tabc, C.c_uint64(seed),
+                                   int(undirected), int(weighted), _lib.stream_ptr(stream),
+                                   C.byref(h)), "nd_graph_rmat")
+        return cls(h)
+
+    def arrays(self):
+        """Zero-copy torch views: row_offsets (i64), col (i32), weights, prefix,
+        max_w (f64; weights/prefix None for unit graphs)."""
+        L = _lib.load()
+        ps = [C.c_void_p() for _ in range(5)]
+        _lib.check(L.nd_graph_arrays(self._h, *[C.byref(p) for p in ps]))
+        V, E = self.n_vertices, self.n_edges
+        out = {"row_offsets": device_view(ps[0].value, V + 1, "int64", self),
+               "col": device_view(ps[1].value, E, "int32", self),
+               "weights": None if self.unit_weights else device_view(ps[2].value, E, "float64", self),
+               "prefix": None if self.unit_weights else device_view(ps[3].value, E, "float64", self),
+               "max_w": device_view(ps[4].value, V, "float64", self)}
+        return out
+
+    def to_host(self):
+        """Download into a host Graph-shaped record (for the oracle)."""
+        a = self.arrays()
+        g = Graph(self.n_vertices, a["row_offsets"].cpu().numpy(),
+                  a["col"].cpu().numpy().astype(np.int64),
+                  (np.ones(self.n_edges) if self.unit_weights else a["weights"].cpu().numpy()),
+                  np.arange(self.n_vertices, dtype=np.int64) if self._remap is None else self._remap)
+        g._prefix = (np.concatenate([np.arange(1, d + 1, dtype=np.float64)
+                                     for d in np.diff(g.row_offsets)]) if self.unit_weights and self.n_edges
+                     else (a["prefix"].cpu().numpy() if not self.unit_weights else np.empty(0)))
+        g._max = a["max_w"].cpu().numpy()
+        return g
+
+    def close(self):
+        if self._h is not None and _lib._lib is not None:
+            _lib._lib.nd_graph_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def as_device_graph(graph) -> DeviceGraph:
+    if isinstance(graph, DeviceGraph):
+        return graph
+    return DeviceGraph.from_graph(graph)

@@ -1,0 +1,99 @@
+"""Device kernel backend with the ``trawl.kernels`` surface
+(kernels/__init__.py:29-44): ``individual_batch``, ``segmented_prefix_sum``,
+``segment_max``, ``keyed_u64`` and the app codes.
+
+Arguments may be numpy arrays (copied to the GPU and back, same call shape
+as the reference backend) or CUDA torch tensors (zero-copy, results written
+in place).  Every call goes through the C-ABI into sm_100a kernels; there is
+no CPU path.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+
+K_DEEPWALK, K_PPR, K_NODE2VEC, K_KHOP, K_MULTIRW = 0, 1, 2, 3, 4
+NODE2VEC_MAX_TRIES = 1_000_000
+BACKEND_NAME = "cuda-sm100a"
+HAVE_COMPILED = True
+
+
+def _is_cuda(a):
+    return hasattr(a, "is_cuda") and a.is_cuda
+
+
+def _dev(a, dtype):
+    """(device tensor, needs_copy_back) for numpy or torch input."""
+    torch = _lib.require_cuda()
+    tdt = {np.int64: torch.int64, np.float64: torch.float64, np.uint64: torch.uint64}[dtype]
+    if a is None:
+        return None
+    if _is_cuda(a):
+        if a.dtype != tdt:
+            raise ValueError(f"expected {tdt}, got {a.dtype}")
+        return a.contiguous()
+    arr = np.ascontiguousarray(a, dtype=dtype)
+    return torch.from_numpy(arr.view(np.int64) if dtype == np.uint64 else arr).cuda()
+
+
+def individual_batch(app_code, params, row_offsets, col_indices, weights, weight_prefix,
+                     max_weight, transits, t_prev, sample_ids, transit_idxs, slots, seed, step,
+                     out):
+    """One app's next over a flat batch of items (_ckernels.pyx:136-271).
+    out[i] receives the sampled vertex or -1.  Raises SamplerStallError /
+    ValueError like the reference."""
+    torch = _lib.require_cuda()
+    L = _lib.load()
+    prm = np.ascontiguousarray(params if params is not None else [], dtype=np.float64)
+    args = [_dev(row_offsets, np.int64), _dev(col_indices, np.int64), _dev(weights, np.float64),
+            _dev(weight_prefix, np.float64), _dev(max_weight, np.float64)]
+    items = [_dev(x, np.int64) for x in (transits, t_prev, sample_ids, transit_idxs, slots)]
+    n = len(items[0])
+    dout = out if _is_cuda(out) else torch.empty(n, dtype=torch.int64, device="cuda")
+    rc = L.nd_individual_batch(int(app_code), _lib.ptr(prm), len(prm), *[_lib.ptr(a) for a in args],
+                               *[_lib.ptr(a) for a in items], n, C.c_uint64(int(seed) & (2**64 - 1)),
+                               int(step), _lib.ptr(dout), _lib.stream_ptr())
+    _lib.check(rc, "nd_individual_batch")
+    if not _is_cuda(out):
+        out[:] = dout.cpu().numpy()
+
+
+def segmented_prefix_sum(values, offsets):
+    """Inclusive per-segment prefix, sequential accumulation (_ckernels.pyx:103-116)."""
+    torch = _lib.require_cuda()
+    v = _dev(values, np.float64)
+    o = _dev(offsets, np.int64)
+    out = torch.empty_like(v)
+    _lib.check(_lib.load().nd_segmented_prefix_sum(_lib.ptr(v), _lib.ptr(o), len(o) - 1,
+                                                   _lib.ptr(out), _lib.stream_ptr()))
+    return out if _is_cuda(values) else out.cpu().numpy()
+
+
+def segment_max(values, offsets):
+    """Per-segment maximum, 0.0 for empty segments (_ckernels.pyx:119-133)."""
+    torch = _lib.require_cuda()
+    v = _dev(values, np.float64)
+    o = _dev(offsets, np.int64)
+    out = torch.empty(len(o) - 1, dtype=torch.float64, device="cuda")
+    _lib.check(_lib.load().nd_segment_max(_lib.ptr(v), _lib.ptr(o), len(o) - 1, _lib.ptr(out),
+                                          _lib.stream_ptr()))
+    return out if _is_cuda(values) else out.cpu().numpy()
+
+
+def keyed_u64(seed, sample_ids, step, transit_idxs=None, slots=None, domain=0, draw=0):
+    """Vectorised keyed draw (_pykernels.py:61-68); uint64 result."""
+    torch = _lib.require_cuda()
+    s = _dev(sample_ids, np.int64)
+    t = _dev(transit_idxs, np.int64)
+    sl = _dev(slots, np.int64)
+    out = torch.empty(len(s), dtype=torch.int64, device="cuda")
+    _lib.check(_lib.load().nd_keyed_u64(C.c_uint64(int(seed) & (2**64 - 1)), _lib.ptr(s), int(step),
+                                        _lib.ptr(t), _lib.ptr(sl), int(domain), int(draw), len(s),
+                                        _lib.ptr(out), _lib.stream_ptr()))
+    if _is_cuda(sample_ids):
+        return out
+    return out.cpu().numpy().view(np.uint64)
