@@ -14,6 +14,9 @@ from .errors import (ContractViolationError, DeviceError, SamplerStallError,
                      TrawlError, UnsupportedAppError)
 from .output import (LAYOUT_FINAL, LAYOUT_PER_STEP, SampleSetOutput, emit,
                      render_text)
+from .engine import (DeviceRun, EngineConfig, RunStats, StepTiming, make_samples,
+                     run_device, sp_run, tp_run)
+from .graph import DeviceGraph, Graph, from_edges, load_cache, load_edge_list, save_cache
 from .rng import RngStream, key_u64, key_uniform
 from .sharding import worker_ranges
 

@@ -23,6 +23,23 @@ void nd_set_last_error(const char* msg, const char* file, int line) {
 extern "C" const char* nd_last_error(void) { return g_last_error.c_str(); }
 extern "C" int nd_version(void) { return 1; }
 
+// Keep stream-ordered allocations cached in the device pool between runs
+// (the default release threshold of 0 returns memory to the OS at every
+// synchronisation, which costs milliseconds per multi-GB run).
+int nd_pool_init() {
+  static thread_local int done_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (done_dev == dev) return ND_OK;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done_dev = dev;
+  return ND_OK;
+}
+
 extern "C" int nd_copy(void* dst, const void* src, int64_t bytes, void* stream) {
   if (bytes < 0) return ND_ERR_ARG;
   if (!bytes) return ND_OK;
@@ -33,6 +50,7 @@ extern "C" int nd_copy(void* dst, const void* src, int64_t bytes, void* stream) 
 }
 
 int nd_make_app(int code, const double* params, int64_t n_params, NdApp* a) {
+  nd_pool_init();
   *a = NdApp{};
   a->code = code;
   if (code == ND_PPR) {
@@ -276,11 +294,13 @@ extern "C" int nd_graph_destroy(nd_graph* G) {
   return ND_OK;
 }
 
+int nd_pool_init();
 extern "C" int nd_graph_create(const int64_t* row_offsets, const int64_t* col_indices,
                                const double* weights, const double* weight_prefix,
                                const double* max_weight, int64_t n_vertices, int64_t n_edges,
                                int arrays_on_host, void* stream, nd_graph** out) {
   if (n_vertices < 0 || n_edges < 0 || n_vertices >= (1ll << 31)) return ND_ERR_ARG;
+  nd_pool_init();
   cudaStream_t s = (cudaStream_t)stream;
   nd_graph* G = new nd_graph();
   cudaGetDevice(&G->device);
@@ -382,6 +402,7 @@ static int ceil_log2(int64_t x) {
 static int build_from_edges_dev(const int64_t* src, const int64_t* dst, const double* w,
                                 int64_t E, int64_t V, cudaStream_t s, nd_graph** out) {
   if (V <= 0 || V >= (1ll << 31) || E < 0) return ND_ERR_ARG;
+  nd_pool_init();
   const int bits = ceil_log2(V);
   if (2 * bits > 64) return ND_ERR_ARG;
   nd_graph* G = new nd_graph();

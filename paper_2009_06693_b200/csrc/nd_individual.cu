@@ -1,10 +1,527 @@
-// nd_individual.cu — multi-slot individual apps (k-hop) — placeholder until
-// the engine lands.
-#include "nd_internal.h"
+// nd_individual.cu — multi-slot individual apps (GraphSAGE k-hop) on device.
+//
+// The reference's generic run loop (driver.py:203-235) with StepPlan
+// semantics (driver.py:80-144): at step s every alive sample contributes one
+// pair per transit (sample-major; transit_idx = rank among the previous
+// step's non-NULL slots, core.py:84-97,168-184) and each pair expands into
+// m = fanout[s] slots at out[pair*m + slot].  A sample stays alive while it
+// has transits (core.py:195-203).
+//
+// Transit-parallel step (transit_parallel.py:185-230): the pairs are radix
+// sorted by transit, grouped, classed by work = members*m and run by
+//   small  — one warp per group, lanes = the group's (member, slot) items
+//            (the paper's sub-warp kernel: one row header, m lanes per sample);
+//   medium — one CTA per group, adjacency staged in shared memory (cp.async);
+//   large  — groups split into chunks of ~1024 items, one CTA per chunk.
+// The next step's pairs come from a stable compaction of the non-NULL slots
+// (exclusive scan), which also yields transit_idx and per-sample counts.
+#include <cub/cub.cuh>
 
-extern "C" int nd_run_individual(const nd_graph*, int, const double*, int64_t, const int64_t*,
-                                 int64_t, int64_t, int64_t, const int64_t*, int64_t, uint64_t,
-                                 int64_t, int, void*, nd_result**) {
-  nd_set_last_error("nd_run_individual: not built yet", __FILE__, __LINE__);
-  return ND_ERR_ARG;
+#include <vector>
+
+#include "nd_tp.cuh"
+
+using namespace nd;
+
+namespace {
+
+constexpr int IND_BLOCK = 256;
+
+struct IndCtx {
+  GView<int32_t> gv;
+  NdApp a;
+  uint64_t base0;
+  int64_t sample_lo;
+  int64_t m;
+  const uint32_t* pt;    // pair transit
+  const int32_t* psid;   // pair sample (local)
+  const int32_t* ptix;   // pair transit index
+  int32_t* out;          // [P*m]
+  int* stall;
+};
+
+template <class RowT>
+__device__ __forceinline__ void ind_item(const IndCtx& c, int64_t p, int64_t slot, int64_t v,
+                                         const RowT& row, int64_t deg, ItemStats& st) {
+  int stl = 0;
+  const uint64_t ik = key_item((uint64_t)(c.sample_lo + c.psid[p]), (uint64_t)c.ptix[p],
+                               (uint64_t)slot);
+  const int64_t o = run_item(c.gv, row, c.a, v, deg, -1, c.base0, ik, st, &stl);
+  if (stl) atomicExch(c.stall, 1);
+  c.out[p * c.m + slot] = (int32_t)o;
+}
+
+// sample-parallel: one thread per (pair, slot) item in plan order
+__global__ void __launch_bounds__(IND_BLOCK) k_ind_flat(IndCtx c, int64_t P,
+                                                        unsigned long long* ctr) {
+  ItemStats st;
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j < P * c.m) {
+    const int64_t p = j / c.m, slot = j - p * c.m;
+    const int64_t v = c.pt[p];
+    const int64_t lo = __ldg(c.gv.row + v), deg = __ldg(c.gv.row + v + 1) - lo;
+    if (slot == 0) st.bytes += SECTOR + 8;
+    ind_item(c, p, slot, v, grow(c.gv, lo), deg, st);
+  }
+  flush_stats(st, ctr);
+}
+
+// classes for the multi-slot engine: every class gets a work list
+__global__ void k_ind_classify(const int* __restrict__ gstart, const int* __restrict__ n_groups,
+                               int64_t m, int* __restrict__ small_list, int* __restrict__ n_small,
+                               int2* __restrict__ units, int* __restrict__ n_units,
+                               unsigned long long* __restrict__ stats) {
+  const int G = *n_groups;
+  int cnt[3] = {0, 0, 0};
+  const int per_chunk = (int)(LARGE_CHUNK / m > 0 ? LARGE_CHUNK / m : 1);
+  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < G; g += gridDim.x * blockDim.x) {
+    const int size = gstart[g + 1] - gstart[g];
+    const int64_t work = (int64_t)size * m;
+    const int c = work < SMALL_MAX_WORK ? 0 : (work <= LARGE_MIN_WORK ? 1 : 2);
+    cnt[c]++;
+    if (c == 0) {
+      small_list[atomicAdd(n_small, 1)] = g;
+    } else if (c == 1) {
+      units[atomicAdd(n_units, 1)] = make_int2(g, -1);
+    } else {
+      const int chunks = (size + per_chunk - 1) / per_chunk;
+      const int b = atomicAdd(n_units, chunks);
+      for (int k = 0; k < chunks; k++) units[b + k] = make_int2(g, k);
+    }
+  }
+  for (int c = 0; c < 3; c++) {
+    int v = cnt[c];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(stats + c, (unsigned long long)v);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(stats + 3, (unsigned long long)G);
+}
+
+// small class: one warp per group; lanes walk the group's (member, slot) items
+__global__ void __launch_bounds__(IND_BLOCK) k_ind_small(IndCtx c, const uint32_t* __restrict__ keys,
+                                                         const uint64_t* __restrict__ vals,
+                                                         const int* __restrict__ gstart,
+                                                         const int* __restrict__ list,
+                                                         const int* __restrict__ n_list,
+                                                         unsigned long long* ctr) {
+  ItemStats st;
+  const int lane = threadIdx.x & 31;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int U = *n_list;
+  for (int u = warp; u < U; u += nwarps) {
+    const int g = list[u];
+    const int gs = gstart[g], size = gstart[g + 1] - gs;
+    const int64_t v = keys[gs];
+    int64_t lo = 0, hi = 0;
+    if (lane == 0) {
+      lo = __ldg(c.gv.row + v);
+      hi = __ldg(c.gv.row + v + 1);
+    }
+    lo = __shfl_sync(0xffffffffu, lo, 0);
+    hi = __shfl_sync(0xffffffffu, hi, 0);
+    const auto row = grow(c.gv, lo);
+    const int64_t items = (int64_t)size * c.m;
+    for (int64_t j = lane; j < items; j += 32) {
+      const int64_t q = gs + j / c.m, slot = j - (j / c.m) * c.m;
+      if (slot == 0) st.bytes += SECTOR + 8;
+      ind_item(c, (int64_t)vals[q], slot, v, row, hi - lo, st);
+    }
+  }
+  flush_stats(st, ctr);
+}
+
+// medium groups (chunk -1) and large-group chunks: one CTA each, row staged
+__global__ void __launch_bounds__(IND_BLOCK) k_ind_group(IndCtx c, const uint32_t* __restrict__ keys,
+                                                         const uint64_t* __restrict__ vals,
+                                                         const int* __restrict__ gstart,
+                                                         const int2* __restrict__ units,
+                                                         const int* __restrict__ n_units,
+                                                         DevGraph g, StageSpec sp,
+                                                         unsigned long long* ctr) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  ItemStats st;
+  const int U = *n_units;
+  const int per_chunk = (int)(LARGE_CHUNK / c.m > 0 ? LARGE_CHUNK / c.m : 1);
+  for (int u = blockIdx.x; u < U; u += gridDim.x) {
+    const int2 un = units[u];
+    const int gs = gstart[un.x], ge = gstart[un.x + 1];
+    const int ms = un.y < 0 ? gs : gs + un.y * per_chunk;
+    const int me = un.y < 0 ? ge : min(ge, ms + per_chunk);
+    const int64_t v = keys[gs];
+    const int64_t lo = __ldg(g.row + v), deg = __ldg(g.row + v + 1) - lo;
+    const int64_t items = (int64_t)(me - ms) * c.m;
+    if (deg > 0 && deg <= sp.cap) {
+      const SRow r = stage_row(g, lo, deg, sp, smem);
+      for (int64_t j = threadIdx.x; j < items; j += blockDim.x) {
+        const int64_t q = ms + j / c.m, slot = j - (j / c.m) * c.m;
+        if (slot == 0) st.bytes += SECTOR + 8;
+        ind_item(c, (int64_t)vals[q], slot, v, r, deg, st);
+      }
+    } else {
+      const auto r = grow(c.gv, lo);
+      for (int64_t j = threadIdx.x; j < items; j += blockDim.x) {
+        const int64_t q = ms + j / c.m, slot = j - (j / c.m) * c.m;
+        if (slot == 0) st.bytes += SECTOR + 8;
+        ind_item(c, (int64_t)vals[q], slot, v, r, deg, st);
+      }
+    }
+    __syncthreads();
+  }
+  flush_stats(st, ctr);
+}
+
+__global__ void k_ind_init(const int64_t* __restrict__ roots64, const int32_t* __restrict__ roots32,
+                           int64_t n, int64_t R, uint32_t* __restrict__ pt, int32_t* __restrict__ psid,
+                           int32_t* __restrict__ ptix, int64_t* __restrict__ spo) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * R;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = i / R;
+    pt[i] = roots64 ? (uint32_t)roots64[i] : (uint32_t)roots32[i];
+    psid[i] = (int32_t)s;
+    ptix[i] = (int32_t)(i - s * R);
+    if (i - s * R == 0) spo[s] = s * R;
+    if (i == n * R - 1) spo[n] = n * R;
+  }
+}
+
+__global__ void k_iota_pairs(const uint32_t* __restrict__ pt, int64_t P, uint32_t* __restrict__ keys,
+                             uint64_t* __restrict__ vals) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    keys[p] = pt[p];
+    vals[p] = (uint64_t)p;
+  }
+}
+
+__global__ void k_flags_nonnull(const int32_t* __restrict__ out, int64_t n, int32_t* __restrict__ f) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x)
+    f[j] = out[j] >= 0;
+}
+
+// per-sample slot counts and non-NULL counts of this step
+__global__ void k_ind_counts(const int64_t* __restrict__ spo, int64_t n, int64_t m,
+                             const int64_t* __restrict__ sc, int64_t* __restrict__ cnt_row,
+                             int64_t* __restrict__ nnz, int64_t* __restrict__ tot) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (i == n) { nnz[n] = 0; continue; }
+    const int64_t a = spo[i] * m, b = spo[i + 1] * m;
+    cnt_row[i] = b - a;
+    const int64_t k = sc[b] - sc[a];
+    nnz[i] = k;
+    tot[i] += k;
+  }
+}
+
+// next pairs from the non-NULL slots (stable), with transit_idx = rank in sample
+__global__ void k_ind_compact(const int32_t* __restrict__ out, int64_t items, int64_t m,
+                              const int64_t* __restrict__ sc, const int32_t* __restrict__ psid,
+                              const int64_t* __restrict__ spo_next, uint32_t* __restrict__ npt,
+                              int32_t* __restrict__ npsid, int32_t* __restrict__ nptix) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < items;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = out[j];
+    if (v < 0) continue;
+    const int64_t pos = sc[j];
+    const int32_t s = psid[j / m];
+    npt[pos] = (uint32_t)v;
+    npsid[pos] = s;
+    nptix[pos] = (int32_t)(pos - spo_next[s]);
+  }
+}
+
+__global__ void k_widen(const int32_t* __restrict__ in, int64_t n, int64_t* __restrict__ out) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x)
+    out[j] = in[j];
+}
+
+// final rows: roots, then each step's compacted values at R + cum + tix
+template <typename RootT>
+__global__ void k_ind_roots(const RootT* __restrict__ roots, int64_t n, int64_t R,
+                            const int64_t* __restrict__ off, int64_t* __restrict__ ids,
+                            int64_t* __restrict__ roots_out, int64_t* __restrict__ roots_off) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * R;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = i / R;
+    ids[off[s] + (i - s * R)] = (int64_t)roots[i];
+    roots_out[i] = (int64_t)roots[i];
+    if (i - s * R == 0) roots_off[s] = s * R;
+    if (i == n * R - 1) roots_off[n] = n * R;
+  }
+}
+
+__global__ void k_ind_final(const uint32_t* __restrict__ npt, const int32_t* __restrict__ npsid,
+                            const int32_t* __restrict__ nptix, int64_t cnt,
+                            const int64_t* __restrict__ off, const int64_t* __restrict__ cum,
+                            int64_t R, int64_t* __restrict__ ids) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < cnt;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t s = npsid[j];
+    ids[off[s] + R + cum[s] + nptix[j]] = (int64_t)npt[j];
+  }
+}
+
+
+__global__ void k_plus_r(int64_t* __restrict__ a, int64_t n, int64_t R) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    a[i] += R;
+}
+
+
+struct StepData {
+  int32_t* out = nullptr;   // [P*m]
+  int64_t items = 0;
+  uint32_t* npt = nullptr;  // compacted next pairs
+  int32_t* npsid = nullptr;
+  int32_t* nptix = nullptr;
+  int64_t nnext = 0;
+  int64_t* cum = nullptr;   // per-sample nnz before this step (for the final rows)
+};
+
+}  // namespace
+
+extern "C" int nd_run_individual(const nd_graph* G, int app_code, const double* host_params,
+                                 int64_t n_params, const int64_t* host_fanouts, int64_t n_fanouts,
+                                 int64_t sample_lo, int64_t n, const int64_t* roots, int64_t R,
+                                 uint64_t seed, int64_t step_cap, int paradigm, void* stream,
+                                 nd_result** out_res) {
+  NdApp a;
+  ND_TRY(nd_make_app(app_code, host_params, n_params, &a));
+  if (!G || n < 0 || R < 1 || n_fanouts < 0 || sample_lo < 0 || n >= (1ll << 31)) return ND_ERR_ARG;
+  if (app_code == ND_NODE2VEC || app_code == ND_MULTIRW) return ND_ERR_ARG;  // walk engine
+  for (int64_t k = 0; k < n_fanouts; k++)
+    if (host_fanouts[k] < 1) return ND_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  const DevGraph& g = G->g;
+  const int key_bits = key_bits_for(g.V);
+  const int64_t S_max = n_fanouts < step_cap ? n_fanouts : step_cap;
+
+  int32_t* roots32 = nullptr;
+  if (!roots) {
+    ND_CUDA_TRY(nd_alloc(&roots32, n * R, s));
+    ND_TRY(nd_uniform_roots_i32(g, R, seed, sample_lo, n, roots32, s));
+  }
+  int64_t P = n * R;
+  uint32_t* pt = nullptr;
+  int32_t *psid = nullptr, *ptix = nullptr;
+  int64_t *spo = nullptr, *tot = nullptr, *nnz = nullptr, *stats = nullptr;
+  unsigned long long* ctr = nullptr;
+  int* stall = nullptr;
+  ND_CUDA_TRY(nd_alloc(&pt, P, s));
+  ND_CUDA_TRY(nd_alloc(&psid, P, s));
+  ND_CUDA_TRY(nd_alloc(&ptix, P, s));
+  ND_CUDA_TRY(nd_alloc(&spo, n + 1, s));
+  ND_CUDA_TRY(nd_alloc(&tot, n + 1, s));
+  ND_CUDA_TRY(nd_alloc(&nnz, n + 1, s));
+  ND_CUDA_TRY(nd_alloc(&ctr, 4, s));
+  ND_CUDA_TRY(nd_alloc(&stall, 1, s));
+  ND_CUDA_TRY(nd_alloc(&stats, 4 * (S_max + 1), s));
+  ND_CUDA_TRY(cudaMemsetAsync(ctr, 0, 4 * sizeof(unsigned long long), s));
+  ND_CUDA_TRY(cudaMemsetAsync(stall, 0, sizeof(int), s));
+  ND_CUDA_TRY(cudaMemsetAsync(tot, 0, (n + 1) * sizeof(int64_t), s));
+  ND_CUDA_TRY(cudaMemsetAsync(stats, 0, 4 * (S_max + 1) * sizeof(int64_t), s));
+  ND_CUDA_TRY(cudaMemsetAsync(spo, 0, (n + 1) * sizeof(int64_t), s));
+  if (P) k_ind_init<<<nd_grid(P, 256), 256, 0, s>>>(roots, roots32, n, R, pt, psid, ptix, spo);
+
+  // step-count matrix [S_max, n] and scratch
+  int64_t* step_counts = nullptr;
+  ND_CUDA_TRY(nd_alloc(&step_counts, S_max * n, s));
+  std::vector<StepData> steps;
+  TPScratch TS;
+  int64_t tp_cap = 0;
+  int64_t* h_tmp = nullptr;
+  ND_CUDA_TRY(cudaMallocHost(&h_tmp, 2 * sizeof(int64_t)));
+  int64_t step = 0;
+  while (step < S_max && P > 0) {
+    const int64_t m = host_fanouts[step];
+    const int64_t items = P * m;
+    StepData sd;
+    sd.items = items;
+    ND_CUDA_TRY(nd_alloc(&sd.out, items, s));
+    ND_CUDA_TRY(nd_alloc(&sd.cum, n, s));
+    ND_CUDA_TRY(cudaMemcpyAsync(sd.cum, tot, n * sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+    IndCtx c{view(g), a, key_base(seed, (uint64_t)step, 0, 0), sample_lo, m, pt, psid, ptix,
+             sd.out, stall};
+    unsigned long long* st_step = reinterpret_cast<unsigned long long*>(stats + 4 * step);
+    if (paradigm == ND_TP) {
+      if (P > tp_cap) {
+        if (tp_cap) TS.release(s);
+        ND_TRY(TS.alloc(P, key_bits, s));
+        tp_cap = P;
+      }
+      uint32_t *k0, *k1;
+      uint64_t *v0, *v1;
+      ND_CUDA_TRY(nd_alloc(&k0, P, s));
+      ND_CUDA_TRY(nd_alloc(&k1, P, s));
+      ND_CUDA_TRY(nd_alloc(&v0, P, s));
+      ND_CUDA_TRY(nd_alloc(&v1, P, s));
+      k_iota_pairs<<<nd_grid(P, 256), 256, 0, s>>>(pt, P, k0, v0);
+      cub::DoubleBuffer<uint32_t> dk(k0, k1);
+      cub::DoubleBuffer<uint64_t> dv(v0, v1);
+      ND_TRY(tp_sort(dk, dv, P, key_bits, TS, s));
+      const uint32_t* keys = dk.Current();
+      const uint64_t* vals = dv.Current();
+      k_mark<<<nd_grid(P, 256), 256, 0, s>>>(keys, P, TS.flags);
+      size_t tb = TS.cub_bytes;
+      ND_CUDA_TRY(cub::DeviceScan::InclusiveSum(TS.cub_tmp, tb, TS.flags, TS.gid, (int)P, s));
+      ND_CUDA_TRY(cudaMemsetAsync(TS.counters, 0, 4 * sizeof(int), s));
+      k_gstart<<<nd_grid(P, 256), 256, 0, s>>>(TS.flags, TS.gid, P, TS.gstart, TS.counters);
+      // lists: small groups -> med_list, medium/large units -> large_units
+      k_ind_classify<<<nd_grid(P, 256), 256, 0, s>>>(TS.gstart, TS.counters, m, TS.med_list,
+                                                      TS.counters + 1, TS.large_units,
+                                                      TS.counters + 2, st_step);
+      const StageSpec sp = stage_spec(!g.unit && (app_code == ND_DEEPWALK || app_code == ND_PPR), 0);
+      k_ind_small<<<148 * 8, IND_BLOCK, 0, s>>>(c, keys, vals, TS.gstart, TS.med_list,
+                                                TS.counters + 1, ctr);
+      k_ind_group<<<148 * 4, IND_BLOCK, STAGE_BYTES, s>>>(c, keys, vals, TS.gstart,
+                                                          TS.large_units, TS.counters + 2, g, sp,
+                                                          ctr);
+      ND_CUDA_TRY(cudaGetLastError());
+      nd_free(k0, s); nd_free(k1, s); nd_free(v0, s); nd_free(v1, s);
+    } else {
+      k_ind_flat<<<(unsigned)((items + IND_BLOCK - 1) / IND_BLOCK), IND_BLOCK, 0, s>>>(c, P, ctr);
+      int64_t hP = P;
+      ND_CUDA_TRY(cudaMemcpyAsync(h_tmp, &hP, sizeof(int64_t), cudaMemcpyHostToDevice, s));
+      ND_CUDA_TRY(cudaStreamSynchronize(s));
+      unsigned long long add = (unsigned long long)P;
+      // fetches for SP = pairs (one adjacency read per (sample, transit))
+      ND_CUDA_TRY(cudaMemcpyAsync(stats + 4 * step + 3, &add, sizeof(add), cudaMemcpyHostToDevice, s));
+      ND_CUDA_TRY(cudaStreamSynchronize(s));
+    }
+    // stable compaction of the non-NULL slots -> next pairs
+    int32_t* flags = nullptr;
+    int64_t *sc = nullptr, *spo_next = nullptr;
+    ND_CUDA_TRY(nd_alloc(&flags, items + 1, s));
+    ND_CUDA_TRY(nd_alloc(&sc, items + 1, s));
+    ND_CUDA_TRY(nd_alloc(&spo_next, n + 1, s));
+    ND_CUDA_TRY(cudaMemsetAsync(flags + items, 0, sizeof(int32_t), s));
+    k_flags_nonnull<<<nd_grid(items, 256), 256, 0, s>>>(sd.out, items, flags);
+    {
+      size_t tb = 0;
+      cub::DeviceScan::ExclusiveSum(nullptr, tb, flags, sc, items + 1, s);
+      void* tmp;
+      ND_CUDA_TRY(nd_alloc((char**)&tmp, tb, s));
+      ND_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tb, flags, sc, items + 1, s));
+      k_ind_counts<<<nd_grid(n + 1, 256), 256, 0, s>>>(spo, n, m, sc, step_counts + step * n, nnz,
+                                                       tot);
+      size_t tb2 = 0;
+      cub::DeviceScan::ExclusiveSum(nullptr, tb2, nnz, spo_next, n + 1, s);
+      void* tmp2;
+      ND_CUDA_TRY(nd_alloc((char**)&tmp2, tb2, s));
+      ND_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp2, tb2, nnz, spo_next, n + 1, s));
+      nd_free(tmp, s);
+      nd_free(tmp2, s);
+    }
+    ND_CUDA_TRY(cudaMemcpyAsync(h_tmp, sc + items, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    ND_CUDA_TRY(cudaStreamSynchronize(s));
+    const int64_t Pn = h_tmp[0];
+    sd.nnext = Pn;
+    ND_CUDA_TRY(nd_alloc(&sd.npt, Pn, s));
+    ND_CUDA_TRY(nd_alloc(&sd.npsid, Pn, s));
+    ND_CUDA_TRY(nd_alloc(&sd.nptix, Pn, s));
+    if (items)
+      k_ind_compact<<<nd_grid(items, 256), 256, 0, s>>>(sd.out, items, m, sc, psid, spo_next,
+                                                         sd.npt, sd.npsid, sd.nptix);
+    ND_CUDA_TRY(cudaGetLastError());
+    nd_free(flags, s);
+    nd_free(sc, s);
+    nd_free(spo, s);
+    spo = spo_next;
+    if (step > 0) { nd_free(pt, s); nd_free(psid, s); nd_free(ptix, s); }
+    else { nd_free(pt, s); nd_free(psid, s); nd_free(ptix, s); }
+    pt = nullptr; psid = nullptr; ptix = nullptr;
+    // the next step's pairs are this step's compacted list (kept for the final rows)
+    pt = sd.npt;
+    psid = sd.npsid;
+    ptix = sd.nptix;
+    P = Pn;
+    steps.push_back(sd);
+    step++;
+  }
+  const int64_t n_steps = step;
+  // ---- outputs ------------------------------------------------------------------
+  int64_t *flen = nullptr, *final_off = nullptr, *final_ids = nullptr, *roots_out = nullptr,
+          *roots_off = nullptr, *step_vals = nullptr;
+  ND_CUDA_TRY(nd_alloc(&flen, n + 1, s));
+  ND_CUDA_TRY(nd_alloc(&final_off, n + 1, s));
+  ND_CUDA_TRY(nd_alloc(&roots_out, n * R, s));
+  ND_CUDA_TRY(nd_alloc(&roots_off, n + 1, s));
+  ND_CUDA_TRY(cudaMemcpyAsync(flen, tot, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+  ND_CUDA_TRY(cudaMemsetAsync(flen + n, 0, sizeof(int64_t), s));
+  if (n) k_plus_r<<<nd_grid(n, 256), 256, 0, s>>>(flen, n, R);
+  {
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, flen, final_off, n + 1, s);
+    void* tmp;
+    ND_CUDA_TRY(nd_alloc((char**)&tmp, tb, s));
+    ND_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tb, flen, final_off, n + 1, s));
+    nd_free(tmp, s);
+  }
+  ND_CUDA_TRY(cudaMemcpyAsync(h_tmp, final_off + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  ND_CUDA_TRY(cudaStreamSynchronize(s));
+  const int64_t total = h_tmp[0];
+  ND_CUDA_TRY(nd_alloc(&final_ids, total, s));
+  if (n * R) {
+    if (roots)
+      k_ind_roots<int64_t><<<nd_grid(n * R, 256), 256, 0, s>>>(roots, n, R, final_off, final_ids,
+                                                              roots_out, roots_off);
+    else
+      k_ind_roots<int32_t><<<nd_grid(n * R, 256), 256, 0, s>>>(roots32, n, R, final_off,
+                                                              final_ids, roots_out, roots_off);
+  } else {
+    ND_CUDA_TRY(cudaMemsetAsync(roots_off, 0, (n + 1) * sizeof(int64_t), s));
+  }
+  int64_t total_items = 0;
+  for (auto& sd : steps) total_items += sd.items;
+  ND_CUDA_TRY(nd_alloc(&step_vals, total_items, s));
+  int64_t pos = 0;
+  for (auto& sd : steps) {
+    if (sd.nnext)
+      k_ind_final<<<nd_grid(sd.nnext, 256), 256, 0, s>>>(sd.npt, sd.npsid, sd.nptix, sd.nnext,
+                                                          final_off, sd.cum, R, final_ids);
+    if (sd.items) k_widen<<<nd_grid(sd.items, 256), 256, 0, s>>>(sd.out, sd.items, step_vals + pos);
+    pos += sd.items;
+  }
+  ND_CUDA_TRY(cudaGetLastError());
+  int h_stall = 0;
+  unsigned long long h_ctr[4];
+  ND_CUDA_TRY(cudaMemcpyAsync(&h_stall, stall, sizeof(int), cudaMemcpyDeviceToHost, s));
+  ND_CUDA_TRY(cudaMemcpyAsync(h_ctr, ctr, sizeof(h_ctr), cudaMemcpyDeviceToHost, s));
+  ND_CUDA_TRY(cudaStreamSynchronize(s));
+  cudaFreeHost(h_tmp);
+  for (auto& sd : steps) {
+    nd_free(sd.out, s);
+    nd_free(sd.cum, s);
+    if (sd.npt != pt) { nd_free(sd.npt, s); nd_free(sd.npsid, s); nd_free(sd.nptix, s); }
+  }
+  nd_free(pt, s); nd_free(psid, s); nd_free(ptix, s);
+  nd_free(spo, s); nd_free(tot, s); nd_free(nnz, s); nd_free(ctr, s); nd_free(stall, s);
+  nd_free(flen, s); nd_free(roots32, s);
+  if (tp_cap) TS.release(s);
+  if (h_stall) {
+    nd_free(final_off, s); nd_free(final_ids, s); nd_free(roots_out, s); nd_free(roots_off, s);
+    nd_free(step_vals, s); nd_free(step_counts, s); nd_free(stats, s);
+    return ND_ERR_STALL;
+  }
+  nd_result* res = new nd_result();
+  res->stream = s;
+  res->n = n;
+  res->n_steps = n_steps;
+  res->total_sampled = total - n * R;
+  res->set(ND_F_FINAL_OFF, final_off, n + 1);
+  res->set(ND_F_FINAL_IDS, final_ids, total);
+  res->set(ND_F_ROOTS, roots_out, n * R);
+  res->set(ND_F_ROOTS_OFF, roots_off, n + 1);
+  res->set(ND_F_STEP_COUNTS, step_counts, n_steps * n);
+  res->set(ND_F_STEP_VALS, step_vals, total_items);
+  res->set(ND_F_STATS, stats, 4 * n_steps);
+  res->counters[NDC_ITEMS] = total_items;
+  res->counters[NDC_SLOT_BYTES] = (int64_t)h_ctr[0];
+  res->counters[NDC_STEPS] = n_steps;
+  *out_res = res;
+  return ND_OK;
 }

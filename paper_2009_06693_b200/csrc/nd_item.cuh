@@ -106,7 +106,8 @@ constexpr int64_t SECTOR = 32;
 template <typename ColT, typename RowT>
 __device__ __forceinline__ int64_t run_item(const GView<ColT>& g, const RowT& r, const NdApp& a,
                                             int64_t v, int64_t deg, int64_t t, uint64_t base0,
-                                            uint64_t ik, ItemStats& st, int* stall) {
+                                            uint64_t ik, ItemStats& st, int* stall,
+                                            int64_t t_lo_known = -1, int64_t t_hi_known = -1) {
   if (deg <= 0) return -1;
   const int64_t wsec = g.unit ? 0 : SECTOR * search_sectors(deg);
   switch (a.code) {
@@ -129,7 +130,8 @@ __device__ __forceinline__ int64_t run_item(const GView<ColT>& g, const RowT& r,
         st.bytes += SECTOR + wsec + SECTOR + 8;
         return r.c(pick_rel(r, g.unit, deg, to_unit(draw_u64(base0, ik))));
       }
-      const int64_t t_lo = __ldg(g.row + t), t_hi = __ldg(g.row + t + 1);
+      const int64_t t_lo = t_lo_known >= 0 ? t_lo_known : __ldg(g.row + t);
+      const int64_t t_hi = t_lo_known >= 0 ? t_hi_known : __ldg(g.row + t + 1);
       const double env = __dmul_rn(__ldg(g.mx + v), a.f_max);
       const int64_t probe = SECTOR * search_sectors(t_hi - t_lo);
       st.bytes += 2 * SECTOR + 8;

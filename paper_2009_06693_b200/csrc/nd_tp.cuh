@@ -103,13 +103,13 @@ __device__ __forceinline__ void flush_stats(const ItemStats& st, unsigned long l
 
 // ---- grouping kernels ------------------------------------------------------------
 
-__global__ void k_mark(const uint32_t* __restrict__ keys, int64_t n, int* __restrict__ flags) {
+static __global__ void k_mark(const uint32_t* __restrict__ keys, int64_t n, int* __restrict__ flags) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     flags[i] = (i == 0 || keys[i] != keys[i - 1]) ? 1 : 0;
 }
 
-__global__ void k_gstart(const int* __restrict__ flags, const int* __restrict__ gid, int64_t n,
+static __global__ void k_gstart(const int* __restrict__ flags, const int* __restrict__ gid, int64_t n,
                          int* __restrict__ gstart, int* __restrict__ n_groups) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -123,7 +123,7 @@ __global__ void k_gstart(const int* __restrict__ flags, const int* __restrict__ 
 
 // classes by work = members*m; per-step class counts into stats[0..3];
 // medium groups and large-group chunks appended to work lists
-__global__ void k_classify(const int* __restrict__ gstart, const int* __restrict__ n_groups,
+static __global__ void k_classify(const int* __restrict__ gstart, const int* __restrict__ n_groups,
                            int64_t m, signed char* __restrict__ gclass, int* __restrict__ med_list,
                            int* __restrict__ n_med, int2* __restrict__ large_units,
                            int* __restrict__ n_large, unsigned long long* __restrict__ stats) {

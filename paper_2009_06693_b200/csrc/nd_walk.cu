@@ -200,6 +200,154 @@ struct Profiler {
   }
 };
 
+
+// ---- walker-major persistent kernel (SP) ------------------------------------------
+// Each lane owns one walker at a time and advances it step after step with the
+// walker state in registers (no per-step state traffic, no global sync); when
+// its walker dies or leaves the step window it takes the next walker from a
+// warp-aggregated work queue, so divergent walk lengths (PPR) keep every lane
+// busy.  Values go to a row-major window [rows, Lw] (one row per walker).
+struct PWArgs {
+  GView<int32_t> gv;
+  NdApp a;
+  uint64_t seed;
+  int64_t sample_lo;
+  int64_t n;                 // rows this window
+  const int32_t* wid;        // row -> walker (nullptr: identity)
+  const int32_t* v0;         // row start transit (nullptr: roots)
+  const int32_t* t0;         // row previous vertex
+  const int64_t* roots64;
+  const int32_t* roots32;
+  int64_t R;
+  int64_t step0, step_end;
+  int64_t Lw;
+  int32_t* out;              // [n, Lw]
+  int32_t* nnz;              // per row: non-NULL values written
+  int32_t* died;             // per walker: 1 when its walk ended with NULL
+  int32_t* cont_wid;         // continuation (alive at step_end)
+  int32_t* cont_v;
+  int32_t* cont_t;
+  int* cont_n;
+  int* queue;
+  int* max_len;
+  int* stall;
+  unsigned long long* ctr;
+};
+
+__global__ void __launch_bounds__(256) k_walk_persistent(PWArgs A) {
+  ItemStats st;
+  const int lane = threadIdx.x & 31;
+  int64_t row = -1, w = 0, v = 0, t = -1, s = 0, lo = 0, deg = 0, tlo = -1, thi = -1;
+  uint64_t ik = 0;
+  int32_t* orow = nullptr;
+  while (true) {
+    const bool need = row < 0;
+    const unsigned m = __ballot_sync(0xffffffffu, need);
+    if (m) {
+      int base = 0;
+      const int leader = __ffs(m) - 1;
+      if (lane == leader) base = atomicAdd(A.queue, __popc(m));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      if (need) {
+        row = base + __popc(m & ((1u << lane) - 1));
+        if (row < A.n) {
+          w = A.wid ? A.wid[row] : row;
+          if (A.v0) {
+            v = A.v0[row];
+            t = A.t0[row];
+          } else {
+            v = A.roots64 ? A.roots64[w * A.R] : A.roots32[w * A.R];
+            t = -1;
+          }
+          tlo = thi = -1;
+          s = A.step0;
+          ik = key_item((uint64_t)(A.sample_lo + w), 0, 0);
+          orow = A.out + row * A.Lw;
+          lo = __ldg(A.gv.row + v);
+          deg = __ldg(A.gv.row + v + 1) - lo;
+        }
+      }
+    }
+    if (__all_sync(0xffffffffu, row >= A.n)) break;
+    if (row >= A.n) continue;
+    // one step of this lane's walker
+    st.bytes += SECTOR + 8;
+    int stl = 0;
+    const int64_t o = run_item(A.gv, grow(A.gv, lo), A.a, v, deg, t,
+                               key_base(A.seed, (uint64_t)s, 0, 0), ik, st, &stl, tlo, thi);
+    if (stl) atomicExch(A.stall, 1);
+    orow[s - A.step0] = (int32_t)o;
+    s++;
+    if (o < 0) {
+      A.nnz[row] = (int32_t)(s - 1 - A.step0);
+      A.died[w] = 1;
+      atomicMax(A.max_len, (int)s);
+      row = -1;
+    } else if (s == A.step_end) {
+      A.nnz[row] = (int32_t)(s - A.step0);
+      atomicMax(A.max_len, (int)s);
+      const int slot = atomicAdd(A.cont_n, 1);
+      A.cont_wid[slot] = (int32_t)w;
+      A.cont_v[slot] = (int32_t)o;
+      A.cont_t[slot] = (int32_t)v;
+      row = -1;
+    } else {
+      tlo = lo;
+      thi = lo + deg;
+      t = v;
+      v = o;
+      lo = __ldg(A.gv.row + v);
+      deg = __ldg(A.gv.row + v + 1) - lo;
+    }
+  }
+  flush_stats(st, A.ctr);
+}
+
+// per-walker totals across windows
+__global__ void k_pw_accum(const int32_t* __restrict__ wid, const int32_t* __restrict__ nnz,
+                           int64_t n, int64_t* __restrict__ tot) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x)
+    tot[wid ? wid[r] : r] += nnz[r];
+}
+
+__global__ void k_pw_lengths(const int64_t* __restrict__ tot, const int32_t* __restrict__ died,
+                             int64_t n, int64_t R, int64_t* __restrict__ flen,
+                             int64_t* __restrict__ clen, unsigned long long* __restrict__ hist) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (i == n) { flen[n] = 0; continue; }
+    flen[i] = R + tot[i];
+    const int64_t c = tot[i] + died[i];
+    clen[i] = c;
+    atomicAdd(hist + c, 1ull);
+  }
+}
+
+// copy one window's rows into the final layout: thread per (row, k)
+__global__ void k_pw_emit(const int32_t* __restrict__ wid, const int32_t* __restrict__ out,
+                          const int32_t* __restrict__ nnz, int64_t n, int64_t Lw, int64_t step0,
+                          const int64_t* __restrict__ off, int64_t R, int64_t* __restrict__ ids) {
+  const int64_t total = n * Lw;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < total;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = j / Lw, k = j - r * Lw;
+    if (k >= nnz[r]) continue;
+    const int64_t w = wid ? wid[r] : r;
+    ids[off[w] + R + step0 + k] = (int64_t)out[j];
+  }
+}
+
+// per-step fetch stats (SP): alive at step s = #{walkers: chain length > s}
+__global__ void k_pw_stats(const unsigned long long* __restrict__ hist, int64_t n_steps,
+                           int64_t n, unsigned long long* __restrict__ stats) {
+  if (blockIdx.x || threadIdx.x) return;
+  unsigned long long alive = (unsigned long long)n;
+  for (int64_t s = 0; s < n_steps; s++) {
+    alive -= hist[s];  // walkers with chain length == s stop before step s
+    stats[4 * s + 3] = alive;
+  }
+}
 }  // namespace
 
 static int g_profile = 0;
@@ -399,6 +547,144 @@ __global__ void k_narrow(const int64_t* __restrict__ in, int64_t n, int32_t* __r
     out[i] = (int32_t)in[i];
 }
 
+
+// SP chain walk: walker-major persistent kernel over step windows of Lw.
+static int run_chain_walk_sp(const nd_graph* G, const NdApp& a, int64_t sample_lo, int64_t n,
+                             const int64_t* roots, int64_t R, uint64_t seed, int64_t steps,
+                             int64_t step_cap, cudaStream_t s, nd_result* res) {
+  const DevGraph& g = G->g;
+  const int64_t limit = steps >= 0 ? (steps < step_cap ? steps : step_cap) : step_cap;
+  const int64_t Lw_base = steps >= 0 ? (limit > 0 ? limit : 1) : 128;
+  int32_t *roots32 = nullptr, *died = nullptr;
+  int64_t* tot = nullptr;
+  int* ctl = nullptr;  // [0]=queue [1]=cont_n [2]=max_len [3]=stall
+  unsigned long long* ctr = nullptr;
+  ND_CUDA_TRY(nd_alloc(&died, n, s));
+  ND_CUDA_TRY(nd_alloc(&tot, n, s));
+  ND_CUDA_TRY(nd_alloc(&ctl, 4, s));
+  ND_CUDA_TRY(nd_alloc(&ctr, 4, s));
+  ND_CUDA_TRY(cudaMemsetAsync(died, 0, n * sizeof(int32_t), s));
+  ND_CUDA_TRY(cudaMemsetAsync(tot, 0, n * sizeof(int64_t), s));
+  ND_CUDA_TRY(cudaMemsetAsync(ctl, 0, 4 * sizeof(int), s));
+  ND_CUDA_TRY(cudaMemsetAsync(ctr, 0, 4 * sizeof(unsigned long long), s));
+  if (!roots) {
+    ND_CUDA_TRY(nd_alloc(&roots32, n * R, s));
+    ND_TRY(nd_uniform_roots_i32(g, R, seed, sample_lo, n, roots32, s));
+  }
+  struct Window {
+    int32_t *wid, *out, *nnz;
+    int64_t n, step0, Lw;
+  };
+  std::vector<Window> wins;
+  int32_t *cwid = nullptr, *cv = nullptr, *ct = nullptr;  // current window inputs
+  int64_t rows = limit > 0 ? n : 0, step0 = 0;
+  int* h = nullptr;
+  ND_CUDA_TRY(cudaMallocHost(&h, 4 * sizeof(int)));
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  int occ = 4;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_walk_persistent, 256, 0);
+  if (occ < 1) occ = 1;
+  while (rows > 0 && step0 < limit) {
+    const int64_t Lw = (limit - step0) < Lw_base ? (limit - step0) : Lw_base;
+    Window W{nullptr, nullptr, nullptr, rows, step0, Lw};
+    ND_CUDA_TRY(nd_alloc(&W.out, rows * Lw, s));
+    ND_CUDA_TRY(nd_alloc(&W.nnz, rows, s));
+    int32_t *nw = nullptr, *nv = nullptr, *nt = nullptr;
+    ND_CUDA_TRY(nd_alloc(&nw, rows, s));
+    ND_CUDA_TRY(nd_alloc(&nv, rows, s));
+    ND_CUDA_TRY(nd_alloc(&nt, rows, s));
+    ND_CUDA_TRY(cudaMemsetAsync(ctl, 0, 2 * sizeof(int), s));
+    PWArgs A{view(g), a, seed, sample_lo, rows, cwid, cv, ct, roots, roots32, R, step0,
+             step0 + Lw, Lw, W.out, W.nnz, died, nw, nv, nt, ctl + 1, ctl, ctl + 2, ctl + 3, ctr};
+    int64_t grid = (int64_t)nsm * occ;
+    const int64_t need = (rows + 255) / 256;
+    if (grid > need) grid = need;
+    k_walk_persistent<<<(unsigned)grid, 256, 0, s>>>(A);
+    ND_CUDA_TRY(cudaGetLastError());
+    W.wid = cwid;
+    ND_CUDA_TRY(cudaMemcpyAsync(h, ctl, 4 * sizeof(int), cudaMemcpyDeviceToHost, s));
+    ND_CUDA_TRY(cudaStreamSynchronize(s));
+    k_pw_accum<<<nd_grid(rows, 256), 256, 0, s>>>(cwid, W.nnz, rows, tot);
+    wins.push_back(W);
+    if (cv) { nd_free(cv, s); nd_free(ct, s); }
+    cwid = nw;
+    cv = nv;
+    ct = nt;
+    rows = h[1];
+    step0 += Lw;
+  }
+  const int h_stall = h[3];
+  const int64_t n_steps = h[2];
+  nd_free(cwid, s); nd_free(cv, s); nd_free(ct, s);
+  // ---- compaction into the final layout -------------------------------------------
+  int64_t *flen = nullptr, *final_off = nullptr, *clen = nullptr, *final_ids = nullptr,
+          *roots_out = nullptr;
+  unsigned long long *hist = nullptr, *stats = nullptr;
+  ND_CUDA_TRY(nd_alloc(&flen, n + 1, s));
+  ND_CUDA_TRY(nd_alloc(&final_off, n + 1, s));
+  ND_CUDA_TRY(nd_alloc(&clen, n, s));
+  ND_CUDA_TRY(nd_alloc(&roots_out, n * R, s));
+  ND_CUDA_TRY(nd_alloc(&hist, limit + 2, s));
+  ND_CUDA_TRY(nd_alloc(&stats, 4 * (n_steps + 1), s));
+  ND_CUDA_TRY(cudaMemsetAsync(hist, 0, (limit + 2) * sizeof(unsigned long long), s));
+  ND_CUDA_TRY(cudaMemsetAsync(stats, 0, 4 * (n_steps + 1) * sizeof(unsigned long long), s));
+  k_pw_lengths<<<nd_grid(n + 1, 256), 256, 0, s>>>(tot, died, n, R, flen, clen, hist);
+  k_pw_stats<<<1, 1, 0, s>>>(hist, n_steps, n, stats);
+  {
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, flen, final_off, n + 1, s);
+    void* tmp = nullptr;
+    ND_CUDA_TRY(nd_alloc((char**)&tmp, tb, s));
+    ND_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tb, flen, final_off, n + 1, s));
+    nd_free(tmp, s);
+  }
+  int64_t total = 0;
+  ND_CUDA_TRY(cudaMemcpyAsync(&total, final_off + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  ND_CUDA_TRY(cudaStreamSynchronize(s));
+  ND_CUDA_TRY(nd_alloc(&final_ids, total, s));
+  if (n * R) {
+    if (roots)
+      k_write_roots<int64_t><<<nd_grid(n * R, 256), 256, 0, s>>>(roots, n, R, final_off, final_ids,
+                                                                roots_out);
+    else
+      k_write_roots<int32_t><<<nd_grid(n * R, 256), 256, 0, s>>>(roots32, n, R, final_off,
+                                                                final_ids, roots_out);
+  }
+  int64_t items = 0;
+  for (auto& W : wins) {
+    if (W.n * W.Lw)
+      k_pw_emit<<<nd_grid(W.n * W.Lw, 256, 148 * 64), 256, 0, s>>>(W.wid, W.out, W.nnz, W.n, W.Lw,
+                                                                  W.step0, final_off, R, final_ids);
+    items += W.n;  // rows touched (upper bound of pairs)
+  }
+  unsigned long long h_ctr[4];
+  ND_CUDA_TRY(cudaMemcpyAsync(h_ctr, ctr, sizeof(h_ctr), cudaMemcpyDeviceToHost, s));
+  ND_CUDA_TRY(cudaGetLastError());
+  ND_CUDA_TRY(cudaStreamSynchronize(s));
+  for (auto& W : wins) {
+    nd_free(W.out, s);
+    nd_free(W.nnz, s);
+    if (W.wid) nd_free(W.wid, s);
+  }
+  cudaFreeHost(h);
+  nd_free(died, s); nd_free(tot, s); nd_free(ctl, s); nd_free(ctr, s); nd_free(roots32, s);
+  nd_free(flen, s); nd_free(hist, s);
+  res->n = n;
+  res->n_steps = n_steps;
+  res->total_sampled = total - n * R;
+  res->set(ND_F_FINAL_OFF, final_off, n + 1);
+  res->set(ND_F_FINAL_IDS, final_ids, total);
+  res->set(ND_F_ROOTS, roots_out, n * R);
+  res->set(ND_F_CHAIN_LEN, clen, n);
+  res->set(ND_F_STATS, stats, 4 * n_steps);
+  res->counters[NDC_N2V_TRIES] = (int64_t)h_ctr[1];
+  res->counters[NDC_SLOT_BYTES] = (int64_t)h_ctr[0];
+  res->counters[NDC_STEPS] = n_steps;
+  return h_stall ? ND_ERR_STALL : ND_OK;
+}
+
 static int run_rootpick_walk(const nd_graph* G, const NdApp& a, int64_t sample_lo, int64_t n,
                              const int64_t* roots, int64_t R, uint64_t seed, int64_t steps,
                              int64_t step_cap, int paradigm, cudaStream_t s, nd_result* res) {
@@ -538,6 +824,9 @@ extern "C" int nd_run_walk(const nd_graph* g, int app_code, const double* host_p
   if (app_code == ND_MULTIRW)
     rc = run_rootpick_walk(g, a, sample_lo, n_samples, roots, roots_per_sample, seed, steps,
                            step_cap, paradigm, s, res);
+  else if (paradigm == ND_SP)
+    rc = run_chain_walk_sp(g, a, sample_lo, n_samples, roots, roots_per_sample, seed, steps,
+                           step_cap, s, res);
   else
     rc = run_chain_walk(g, a, sample_lo, n_samples, roots, roots_per_sample, seed, steps,
                         step_cap, paradigm, s, res);

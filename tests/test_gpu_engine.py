@@ -114,3 +114,80 @@ def test_walks_on_rmat_vs_oracle(app, params, weighted):
             assert np.array_equal(got.reshape(-1, 3), ref.stats[:, :3])
             assert st.adjacency_fetches == int(ref.stats[:, 3].sum())
         dr.close()
+
+
+@pytest.mark.parametrize("paradigm", ["tp", "sp"])
+@pytest.mark.parametrize("meta", _cases(("khop",)), ids=lambda m: f"{m['idx']}-{m['app']}-{m['graph']}")
+def test_khop_runs_match_reference(meta, paradigm):
+    out = _device_run(meta, paradigm)
+    tf, ts = texts(out)
+    assert out.n_steps == meta["n_steps"]
+    assert sha16(tf) == meta["hash_final"]
+    assert sha16(ts) == meta["hash_per_step"]
+    if paradigm == "tp":
+        rs = golden("runs.npz")
+        groups = np.array([[t.groups_small, t.groups_medium, t.groups_large] for t in out.stats.timings])
+        assert np.array_equal(groups.reshape(-1, 3), rs[f"r{meta['idx']}/groups"])
+        assert out.stats.adjacency_fetches == meta["adjacency_fetches"]
+
+
+def test_khop_on_rmat_vs_oracle():
+    """Reddit-shaped (symmetric RMAT, unit weights) 2-hop 25/10 on 3000 roots:
+    device == oracle for every step slot, final rows and TP class counts."""
+    from paper_2009_06693_b200 import make_app
+    from paper_2009_06693_b200.engine import run_device
+    from paper_2009_06693_b200.graph import DeviceGraph
+    dg = DeviceGraph.rmat(13, 16, seed=3, undirected=True, weighted=False)
+    hg = dg.to_host()
+    og = O.OGraph(hg.n_vertices, hg.row_offsets, hg.col_indices, hg.weights,
+                  hg.per_vertex_weight_prefix, hg.per_vertex_max_weight, np.arange(hg.n_vertices))
+    meta = {"app": "khop", "params": {}, "n_samples": 3000, "seed": 4}
+    ref = oracle_run(meta, og, paradigm="tp")
+    for par in ("tp", "sp"):
+        dr = run_device(make_app("khop"), dg, n_samples=3000, seed=4, paradigm=par)
+        out = dr.to_output()
+        assert np.array_equal(out.step_counts, ref.step_counts)
+        assert np.array_equal(out.step_vals, ref.step_vals)
+        off, ids = out.final_csr()
+        roff, rids = ref.final_csr()
+        assert np.array_equal(off, roff) and np.array_equal(ids, rids)
+        if par == "tp":
+            st = dr.stats()
+            got = np.array([[t.groups_small, t.groups_medium, t.groups_large] for t in st.timings])
+            assert np.array_equal(got.reshape(-1, 3), ref.stats[:, :3])
+        dr.close()
+
+
+@pytest.mark.parametrize("ci", range(5))
+def test_schedule_export_matches_reference(ci):
+    from paper_2009_06693_b200.schedule import transit_schedule
+    d = golden("schedule.npz")
+    r = transit_schedule(d[f"s{ci}/pair_transit"], int(d[f"s{ci}/m"][0]))
+    assert np.array_equal(r["order"], d[f"s{ci}/order"])
+    assert np.array_equal(np.diff(r["group_start"]), d[f"s{ci}/group_size"])
+    assert np.array_equal(r["group_transit"], d[f"s{ci}/group_transit"])
+    assert np.array_equal(r["group_class"], d[f"s{ci}/group_class"])
+    assert np.array_equal(r["sched_index"], d[f"s{ci}/sched_index"])
+
+
+def test_reference_app_objects_accepted():
+    """A reference-shaped app (duck-typed SamplingApp with kernel_code and
+    params, closure-based init_roots) runs unchanged."""
+    from paper_2009_06693_b200 import EngineConfig, tp_run
+    from paper_2009_06693_b200.core import INDIVIDUAL, SamplingApp
+    from paper_2009_06693_b200.engine import make_samples
+    from paper_2009_06693_b200.graph import DeviceGraph
+    meta = [m for m in golden("runs.json") if m["app"] == "deepwalk" and m["graph"].startswith("powerlaw:2000")][0]
+    g = golden_graph(meta["graph"])
+
+    def init(graph, sid, seed):  # the reference's closure shape (apps.py:83-103)
+        from paper_2009_06693_b200.apps import UniformRoots
+        return UniformRoots(1)(graph, sid, seed)
+
+    app = SamplingApp(name="deepwalk", sampling_type=INDIVIDUAL, steps=100,
+                      sample_size=lambda s: 1, next_fn=lambda *a: -1, init_roots=init,
+                      chain_walk=True, kernel_code=0, params={"walk_length": 100})
+    samples = [make_samples(app, g, meta["n_samples"], meta["seed"])[i] for i in range(meta["n_samples"])]
+    out = tp_run(app, DeviceGraph.from_arrays(g.row_offsets, g.col_indices, g.weights), samples,
+                 EngineConfig(seed=meta["seed"]))
+    assert sha16(texts(out)[0]) == meta["hash_final"]
