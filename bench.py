@@ -1,0 +1,410 @@
+#!/usr/bin/env python
+"""Benchmark: sampled edges/s of the B200 NextDoor engine on the C2 workload.
+
+Workload (BASELINE.json configs[1]): keyed RMAT scale 22
+(4,194,304 vertices, 68,993,773 directed weighted edges, a,b,c = .57,.19,.19,
+weights U[1,5), graph seed 0) built on device; one step = a node2vec walk
+(p=2, q=0.5, length 100) plus a PPR walk (termination 0.01, step cap 10,000)
+for every vertex (N = V walkers, sampling seed 7).  Inputs (1.4 GB CSR) are
+larger than L2.  With --gpus N the walkers are sharded by worker_ranges
+across ranks (graph replicated, regenerated from the same key), and the
+compacted rows are gathered to rank 0 over NCCL (strong scaling: total work
+fixed).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints ONE JSON line on rank 0.  `value` = device throughput with inputs
+resident (CUDA events, max over ranks); `e2e` = the same job through the
+public API with host buffers (roots H2D, final rows D2H) in the timed
+region; `roofline` = counted algorithmic bytes of the dominant kernel
+(k_walk_persistent, SURVEY §8(d) sector model) / its event-timed duration;
+`cpu_baseline` = the C oracle (restatement of the reference engine) on the
+host's cores over a bounded sample of the same walks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+SCALE = 22
+N_EDGES = 68_993_773
+GRAPH_SEED = 0
+SEED = 7
+APPS = (("node2vec", {"p": 2.0, "q": 0.5}), ("ppr", {"termination_probability": 0.01}))
+METRIC = "sampled edges/sec (and % of HBM roofline) at 1/2/4/8 B200 vs CPU ref"
+CPU_SAMPLE = 1 << 17
+
+
+def peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                out = ""
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            parts = [p.strip() for p in ln.split(",")]
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+                for nm, v in zip(names, parts[2:]):
+                    if v.lower().startswith("active"):
+                        reasons.add(nm)
+            except (ValueError, IndexError):
+                continue
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ---------------------------------------------------------------------------
+# CPU: the oracle (C restatement of the reference engine) on host cores
+
+def cpu_walks(hg, lo, n, threads):
+    """Time node2vec + PPR for walkers [lo, lo+n) through the oracle's
+    process-parallel-equivalent worker split (driver.py:175-186)."""
+    from oracle import oracle as O
+    og = O.OGraph(hg.n_vertices, hg.row_offsets, hg.col_indices, hg.weights,
+                  hg.per_vertex_weight_prefix, hg.per_vertex_max_weight, None)
+    roots = O.uniform_roots(hg.n_vertices, 1, SEED, lo, n)
+    edges = 0
+    res = {}
+    t0 = time.perf_counter()
+    for name, code, kp, steps in (("node2vec", 2, [2.0, 0.5, 0.0], 100), ("ppr", 1, [0.01], None)):
+        r = O.run_chain(og, code, kp, roots, SEED, steps, paradigm="sp", n_threads=threads,
+                        sample_lo=lo)
+        vals = r["chain_vals"]
+        edges += int((vals >= 0).sum())
+        res[name] = r
+    return edges, time.perf_counter() - t0, res
+
+
+def host_graph_for_oracle(dg):
+    return dg.to_host()
+
+
+# ---------------------------------------------------------------------------
+
+def run_reference(args):
+    """--impl reference: the reference's CPU implementation of the path (the
+    C oracle port; oracle/_ref is not buildable for a Python reference) on all
+    host cores, bounded sample per step, same metric/config."""
+    import torch
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return 0
+    cores = len(os.sched_getaffinity(0))
+    from paper_2009_06693_b200.graph import DeviceGraph
+    torch.cuda.set_device(0)
+    dg = DeviceGraph.rmat(SCALE, n_edges=N_EDGES, seed=GRAPH_SEED, weighted=True)
+    hg = host_graph_for_oracle(dg)
+    dg.close()
+    times, edges_tot = [], 0
+    for i in range(args.warmup + args.steps):
+        e, dt, _ = cpu_walks(hg, 0, CPU_SAMPLE, cores)
+        if i >= args.warmup:
+            times.append(dt)
+            edges_tot += e
+    value = edges_tot / sum(times)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "edges/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "int64+f64", "data": "synthetic",
+        "config": config_dict(args.gpus, note="CPU oracle port, bounded sample"),
+        "cpu_baseline": {"value": value, "unit": "edges/s", "cores": cores, "kind": "port",
+                         "sample": f"node2vec+PPR walks of sample ids [0, {CPU_SAMPLE}) per step"},
+        "e2e": {"value": value, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_dict(n_gpus, note=None):
+    c = {"workload": "C2: RMAT scale 22 (4,194,304 V, 68,993,773 directed weighted E), "
+                     "node2vec p=2 q=0.5 len 100 + PPR term 0.01, one walk per vertex",
+         "graph": "keyed RMAT a=.57 b=.19 c=.19, weights U[1,5), seed 0, built on device",
+         "walkers_per_step": 2 * (1 << SCALE), "seed": SEED,
+         "parallelism": f"sample-sharded x{n_gpus}, graph replicated",
+         "l2": "inputs (1.45 GB CSR) larger than L2", "paradigm": "sp (walker-major)"}
+    if note:
+        c["note"] = note
+    return c
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--paradigm", default="sp", choices=["sp", "tp"])
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2009_06693_b200 import _lib, make_app
+    from paper_2009_06693_b200.engine import run_device
+    from paper_2009_06693_b200.graph import DeviceGraph
+    from paper_2009_06693_b200.sharding import worker_ranges
+
+    L = _lib.load()
+    dg = DeviceGraph.rmat(SCALE, n_edges=N_EDGES, seed=GRAPH_SEED, weighted=True)
+    V = dg.n_vertices
+    lo, hi = worker_ranges(V, ws)[rank] if rank < min(ws, V) else (V, V)
+    n = hi - lo
+    apps = [make_app(a, **kw) for a, kw in APPS]
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def gather_rows(off, ids):
+        """Final NCCL gather of every rank's compacted rows to rank 0."""
+        if ws == 1:
+            return 0
+        cnt = torch.tensor([ids.numel()], dtype=torch.int64, device="cuda")
+        cnts = [torch.zeros_like(cnt) for _ in range(ws)]
+        dist.all_gather(cnts, cnt)
+        mx = int(max(c.item() for c in cnts))
+        buf = torch.full((mx,), -1, dtype=torch.int64, device="cuda")
+        buf[:ids.numel()] = ids
+        out = [torch.empty_like(buf) for _ in range(ws)] if rank == 0 else None
+        dist.gather(buf, out, dst=0)
+        return mx * 8 * ws
+
+    # ---- device throughput: inputs resident, CUDA events, max over ranks --------
+    L.nd_set_profiling(1)
+    sample_ms, slot_bytes, edges_dev, launches = [], 0, 0, 0
+    times = []
+    clocks = ClockSampler(local)
+    for it in range(args.warmup + args.steps):
+        timed = it >= args.warmup
+        if timed and it == args.warmup:
+            clocks.__enter__()
+        barrier()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        step_edges, step_bytes, step_sample = 0, 0, 0.0
+        runs = []
+        for app in apps:
+            dr = run_device(app, dg, n_samples=n, sample_lo=lo, seed=SEED, paradigm=args.paradigm,
+                            sync=False)
+            step_edges += dr.total_sampled
+            step_bytes += dr.counters["slot_bytes"]
+            step_sample += dr.profile_ms[1]
+            runs.append(dr)
+        if ws > 1:
+            for dr in runs:
+                gather_rows(dr.view(_lib.F_FINAL_OFF), dr.view(_lib.F_FINAL_IDS))
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        ms = ev0.elapsed_time(ev1)
+        for dr in runs:
+            dr.close()
+        if timed:
+            times.append(ms)
+            edges_dev += step_edges
+            slot_bytes += step_bytes
+            sample_ms.append(step_sample)
+            launches += sum(int(dr.counters.get("launches", 0)) for dr in runs)
+    clocks.__exit__()
+    tot_ms = sum(times)
+    if ws > 1:
+        t = torch.tensor([tot_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = t.item()
+        e = torch.tensor([edges_dev], dtype=torch.int64, device="cuda")
+        dist.all_reduce(e)
+        edges_all = int(e.item())
+    else:
+        edges_all = edges_dev
+    value = edges_all / (tot_ms / 1e3)
+
+    # ---- e2e through the public API with host buffers ------------------------------
+    L.nd_set_profiling(0)
+    from oracle import oracle as O  # noqa: F401  (roots on host: the reference's keyed rule)
+    from paper_2009_06693_b200.engine import SampleRange
+    roots_host = torch.from_numpy(O.uniform_roots(V, 1, SEED, lo, n).reshape(-1)).pin_memory()
+    e2e_times, e2e_edges, h2d, d2h = [], 0, 0, 0
+    for it in range(max(1, args.warmup // 2) + args.steps):
+        barrier()
+        t0 = time.perf_counter()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        step_edges, step_h2d, step_d2h = 0, 0, 0
+        for app in apps:
+            droots = roots_host.to("cuda", non_blocking=True)
+            step_h2d += roots_host.numel() * 8
+            dr = _run_with_roots(run_device, app, dg, droots, lo, n)
+            off = dr.view(_lib.F_FINAL_OFF)
+            ids = dr.view(_lib.F_FINAL_IDS)
+            h_off = torch.empty(off.numel(), dtype=torch.int64, pin_memory=True)
+            h_ids = torch.empty(ids.numel(), dtype=torch.int64, pin_memory=True)
+            h_off.copy_(off, non_blocking=True)
+            h_ids.copy_(ids, non_blocking=True)
+            step_d2h += (off.numel() + ids.numel()) * 8
+            step_edges += dr.total_sampled
+            torch.cuda.synchronize()
+            dr.close()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        if it >= max(1, args.warmup // 2):
+            e2e_times.append(ev0.elapsed_time(ev1))
+            e2e_edges += step_edges
+            h2d, d2h = step_h2d, step_d2h
+    e2e_ms = sum(e2e_times)
+    if ws > 1:
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = t.item()
+        e = torch.tensor([e2e_edges], dtype=torch.int64, device="cuda")
+        dist.all_reduce(e)
+        e2e_edges = int(e.item())
+    e2e_value = e2e_edges / (e2e_ms / 1e3)
+
+    # ---- roofline of the dominant kernel ----------------------------------------------
+    peak, peak_kind = peaks()
+    samp_s = sum(sample_ms) / 1e3
+    achieved = (slot_bytes / samp_s / 1e9) if samp_s > 0 else None
+    traffic = None
+    prof_json = os.path.join(REPO, "profiles", "r01_ncu_summary.json")
+    if os.path.exists(prof_json):
+        try:
+            with open(prof_json) as fh:
+                traffic = json.load(fh).get("traffic_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    # ---- CPU baseline (rank 0, N=1 only) ------------------------------------------------
+    cpu = None
+    parity = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        cores = len(os.sched_getaffinity(0))
+        hg = host_graph_for_oracle(dg)
+        ce, cdt, cres = cpu_walks(hg, 0, CPU_SAMPLE, cores)
+        cpu = {"value": ce / cdt, "unit": "edges/s", "cores": cores, "kind": "port",
+               "sample": f"node2vec+PPR walks for sample ids [0, {CPU_SAMPLE}) "
+                         f"({ce} edges, {cdt:.1f} s)"}
+        # parity of the sampled rows on the CPU sample
+        parity = True
+        for (name, kw), app in zip(APPS, apps):
+            dr = run_device(app, dg, n_samples=CPU_SAMPLE, seed=SEED, paradigm=args.paradigm)
+            off, ids = dr.host(_lib.F_FINAL_OFF), dr.host(_lib.F_FINAL_IDS)
+            r = cres[name]
+            clen = r["chain_len"]
+            cv = r["chain_vals"]
+            nn = np.add.reduceat((cv >= 0).astype(np.int64), np.concatenate([[0], np.cumsum(clen)[:-1]])) \
+                if len(cv) else np.zeros(CPU_SAMPLE, dtype=np.int64)
+            nn = np.where(clen > 0, nn, 0)
+            parity &= bool(np.array_equal(np.diff(off), 1 + nn))
+            parity &= bool(np.array_equal(ids[off[:-1] + 1][nn > 0] if len(ids) else ids,
+                                          cv[np.concatenate([[0], np.cumsum(clen)[:-1]])][nn > 0]))
+            dr.close()
+
+    if rank == 0:
+        ms_per_step = tot_ms / len(times)
+        line = {
+            "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "int64+f64", "data": "synthetic", "config": config_dict(ws),
+            "e2e": {"value": e2e_value, "unit": "edges/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                         "kernel": "k_walk_persistent" if args.paradigm == "sp" else "TP class kernels",
+                         "peak_kind": peak_kind,
+                         "bytes_model": "SURVEY 8(d) sector model, counted on device",
+                         "algorithmic_bytes_per_step": slot_bytes / len(times),
+                         "kernel_ms_per_step": sum(sample_ms) / len(sample_ms)},
+            "cpu_baseline": cpu, "parity_cpu_sample": parity,
+            "clocks": clocks.summary(), "gpu_launches": launches,
+            "edges_per_step": edges_all / len(times),
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def _run_with_roots(run_device, app, dg, droots, lo, n):
+    """Public-API run with caller-provided (uploaded) roots."""
+    import ctypes as C
+    from paper_2009_06693_b200 import _lib
+    from paper_2009_06693_b200.engine import DeviceRun, describe
+    L = _lib.load()
+    plan = describe(app)
+    kp = np.ascontiguousarray(plan.kparams, dtype=np.float64)
+    h = C.c_void_p()
+    _lib.check(L.nd_run_walk(dg.handle, plan.code, _lib.ptr(kp), len(kp), lo, n, _lib.ptr(droots), 1,
+                             C.c_uint64(SEED), plan.steps, 10_000, _lib.ND_SP, _lib.stream_ptr(),
+                             C.byref(h)), "nd_run_walk")
+    return DeviceRun(h, plan, dg, "sp", lo, 0.0)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -194,6 +194,8 @@ __global__ void k_iota_pairs(const uint32_t* __restrict__ pt, int64_t P, uint32_
   }
 }
 
+__global__ void k_add_fetch(unsigned long long* st, unsigned long long n) { st[3] += n; }
+
 __global__ void k_flags_nonnull(const int32_t* __restrict__ out, int64_t n, int32_t* __restrict__ f) {
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
        j += (int64_t)gridDim.x * blockDim.x)
@@ -326,6 +328,9 @@ extern "C" int nd_run_individual(const nd_graph* G, int app_code, const double* 
   ND_CUDA_TRY(cudaMemsetAsync(stats, 0, 4 * (S_max + 1) * sizeof(int64_t), s));
   ND_CUDA_TRY(cudaMemsetAsync(spo, 0, (n + 1) * sizeof(int64_t), s));
   if (P) k_ind_init<<<nd_grid(P, 256), 256, 0, s>>>(roots, roots32, n, R, pt, psid, ptix, spo);
+  uint32_t* const pt0 = pt;  // step-0 pairs (the roots); later steps' pairs live in `steps`
+  int32_t* const psid0 = psid;
+  int32_t* const ptix0 = ptix;
 
   // step-count matrix [S_max, n] and scratch
   int64_t* step_counts = nullptr;
@@ -384,13 +389,8 @@ extern "C" int nd_run_individual(const nd_graph* G, int app_code, const double* 
       nd_free(k0, s); nd_free(k1, s); nd_free(v0, s); nd_free(v1, s);
     } else {
       k_ind_flat<<<(unsigned)((items + IND_BLOCK - 1) / IND_BLOCK), IND_BLOCK, 0, s>>>(c, P, ctr);
-      int64_t hP = P;
-      ND_CUDA_TRY(cudaMemcpyAsync(h_tmp, &hP, sizeof(int64_t), cudaMemcpyHostToDevice, s));
-      ND_CUDA_TRY(cudaStreamSynchronize(s));
-      unsigned long long add = (unsigned long long)P;
-      // fetches for SP = pairs (one adjacency read per (sample, transit))
-      ND_CUDA_TRY(cudaMemcpyAsync(stats + 4 * step + 3, &add, sizeof(add), cudaMemcpyHostToDevice, s));
-      ND_CUDA_TRY(cudaStreamSynchronize(s));
+      // SP fetches: one adjacency read per (sample, transit) pair
+      k_add_fetch<<<1, 1, 0, s>>>(st_step, (unsigned long long)P);
     }
     // stable compaction of the non-NULL slots -> next pairs
     int32_t* flags = nullptr;
@@ -431,10 +431,8 @@ extern "C" int nd_run_individual(const nd_graph* G, int app_code, const double* 
     nd_free(sc, s);
     nd_free(spo, s);
     spo = spo_next;
-    if (step > 0) { nd_free(pt, s); nd_free(psid, s); nd_free(ptix, s); }
-    else { nd_free(pt, s); nd_free(psid, s); nd_free(ptix, s); }
-    pt = nullptr; psid = nullptr; ptix = nullptr;
-    // the next step's pairs are this step's compacted list (kept for the final rows)
+    // the next step's pairs are this step's compacted list (kept for the final
+    // rows; freed with the step data at the end)
     pt = sd.npt;
     psid = sd.npsid;
     ptix = sd.nptix;
@@ -496,9 +494,11 @@ extern "C" int nd_run_individual(const nd_graph* G, int app_code, const double* 
   for (auto& sd : steps) {
     nd_free(sd.out, s);
     nd_free(sd.cum, s);
-    if (sd.npt != pt) { nd_free(sd.npt, s); nd_free(sd.npsid, s); nd_free(sd.nptix, s); }
+    nd_free(sd.npt, s);
+    nd_free(sd.npsid, s);
+    nd_free(sd.nptix, s);
   }
-  nd_free(pt, s); nd_free(psid, s); nd_free(ptix, s);
+  nd_free(pt0, s); nd_free(psid0, s); nd_free(ptix0, s);
   nd_free(spo, s); nd_free(tot, s); nd_free(nnz, s); nd_free(ctr, s); nd_free(stall, s);
   nd_free(flen, s); nd_free(roots32, s);
   if (tp_cap) TS.release(s);

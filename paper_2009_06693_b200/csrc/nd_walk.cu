@@ -356,6 +356,8 @@ extern "C" int nd_set_profiling(int on) {
   return ND_OK;
 }
 
+
+
 // byte-model counters (see nd_item.cuh): ctr[0]=bytes, ctr[1]=tries
 static int run_chain_walk(const nd_graph* G, const NdApp& a, int64_t sample_lo, int64_t n,
                           const int64_t* roots, int64_t R, uint64_t seed, int64_t steps,
@@ -586,6 +588,13 @@ static int run_chain_walk_sp(const nd_graph* G, const NdApp& a, int64_t sample_l
   int occ = 4;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_walk_persistent, 256, 0);
   if (occ < 1) occ = 1;
+  int64_t launches = roots ? 0 : 1;
+  double sample_ms = 0.0;
+  cudaEvent_t pe0 = nullptr, pe1 = nullptr;
+  if (g_profile) {
+    cudaEventCreate(&pe0);
+    cudaEventCreate(&pe1);
+  }
   while (rows > 0 && step0 < limit) {
     const int64_t Lw = (limit - step0) < Lw_base ? (limit - step0) : Lw_base;
     Window W{nullptr, nullptr, nullptr, rows, step0, Lw};
@@ -601,12 +610,20 @@ static int run_chain_walk_sp(const nd_graph* G, const NdApp& a, int64_t sample_l
     int64_t grid = (int64_t)nsm * occ;
     const int64_t need = (rows + 255) / 256;
     if (grid > need) grid = need;
+    if (g_profile) cudaEventRecord(pe0, s);
     k_walk_persistent<<<(unsigned)grid, 256, 0, s>>>(A);
+    if (g_profile) cudaEventRecord(pe1, s);
     ND_CUDA_TRY(cudaGetLastError());
     W.wid = cwid;
     ND_CUDA_TRY(cudaMemcpyAsync(h, ctl, 4 * sizeof(int), cudaMemcpyDeviceToHost, s));
     ND_CUDA_TRY(cudaStreamSynchronize(s));
+    if (g_profile) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, pe0, pe1);
+      sample_ms += ms;
+    }
     k_pw_accum<<<nd_grid(rows, 256), 256, 0, s>>>(cwid, W.nnz, rows, tot);
+    launches += 2;
     wins.push_back(W);
     if (cv) { nd_free(cv, s); nd_free(ct, s); }
     cwid = nw;
@@ -619,6 +636,7 @@ static int run_chain_walk_sp(const nd_graph* G, const NdApp& a, int64_t sample_l
   const int64_t n_steps = h[2];
   nd_free(cwid, s); nd_free(cv, s); nd_free(ct, s);
   // ---- compaction into the final layout -------------------------------------------
+  if (g_profile) cudaEventRecord(pe0, s);
   int64_t *flen = nullptr, *final_off = nullptr, *clen = nullptr, *final_ids = nullptr,
           *roots_out = nullptr;
   unsigned long long *hist = nullptr, *stats = nullptr;
@@ -658,7 +676,10 @@ static int run_chain_walk_sp(const nd_graph* G, const NdApp& a, int64_t sample_l
       k_pw_emit<<<nd_grid(W.n * W.Lw, 256, 148 * 64), 256, 0, s>>>(W.wid, W.out, W.nnz, W.n, W.Lw,
                                                                   W.step0, final_off, R, final_ids);
     items += W.n;  // rows touched (upper bound of pairs)
+    launches += 1;
   }
+  launches += 2 /*lengths, stats*/ + 2 /*scan*/ + (n * R ? 1 : 0);
+  if (g_profile) cudaEventRecord(pe1, s);
   unsigned long long h_ctr[4];
   ND_CUDA_TRY(cudaMemcpyAsync(h_ctr, ctr, sizeof(h_ctr), cudaMemcpyDeviceToHost, s));
   ND_CUDA_TRY(cudaGetLastError());
@@ -669,6 +690,15 @@ static int run_chain_walk_sp(const nd_graph* G, const NdApp& a, int64_t sample_l
     if (W.wid) nd_free(W.wid, s);
   }
   cudaFreeHost(h);
+  if (g_profile) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, pe0, pe1);
+    res->prof_ms[1] = sample_ms;
+    res->prof_ms[2] = ms;
+    cudaEventDestroy(pe0);
+    cudaEventDestroy(pe1);
+  }
+  res->counters[NDC_LAUNCHES] = launches;
   nd_free(died, s); nd_free(tot, s); nd_free(ctl, s); nd_free(ctr, s); nd_free(roots32, s);
   nd_free(flen, s); nd_free(hist, s);
   res->n = n;

@@ -216,10 +216,11 @@ class DeviceRun:
         _lib.check(L.nd_result_info(handle, C.byref(n), C.byref(s), C.byref(ts), C.byref(tr)))
         self.n_samples, self.n_steps = n.value, s.value
         self.total_sampled, self.total_recorded = ts.value, tr.value
-        ctr = (C.c_int64 * 8)()
-        L.nd_result_counters(handle, ctr, 8)
+        ctr = (C.c_int64 * 10)()
+        L.nd_result_counters(handle, ctr, 10)
         self.counters = dict(zip(["items", "pairs", "n2v_tries", "n2v_probes", "search",
-                                  "pair_bytes", "slot_bytes", "steps"], list(ctr)))
+                                  "pair_bytes", "slot_bytes", "steps", "launches", "_"],
+                                 list(ctr)))
         prof = (C.c_double * 4)()
         L.nd_result_profile(handle, prof, 4)
         self.profile_ms = list(prof)
