@@ -1,9 +1,811 @@
-// nd_collective.cu — collective apps — placeholder until the engine lands.
-#include "nd_internal.h"
+// nd_collective.cu — collective apps on device (layer, FastGCN/LADIES, MVS,
+// ClusterGCN).
+//
+// Reference path: tp_step's collective branch (transit_parallel.py:187-198)
+// -> build_combined (collective.py:39-120) -> collective_select
+// (collective.py:123-141) -> the apps' next functions (apps.py:247-386).
+// Per step every alive sample's transits are its previous step's non-NULL
+// vertices (roots at step 0, duplicates kept, core.py:168-184); the combined
+// neighbourhood is the concatenation of the transits' adjacency lists in
+// transit order.  The device never materialises it: a combined entry e of
+// sample i is located by a binary search over the per-sample exclusive scan
+// of transit degrees (entry e -> transit k, offset e - cdeg[k]).
+//   layer       take = min(m, max(0, cap - size)); slot < take -> combined[u % n]
+//   importance  v = u % V (or the deg^2 inverse CDF); record (t, v) for every
+//               transit t with an edge t->v (slot-major, transit order)
+//   mvs         i = u % n; record (src_transit[i], nbr[i])
+//   clustergcn  record every combined entry whose neighbour is a root
+//               (per-sample root bitmap; one warp per (sample, transit) pair
+//               walks the adjacency twice: count, then ordered write)
+// The transit-parallel build statistics (groups of equal transits classed
+// by members * degree, collective.py:107-114) are computed on device from a
+// radix sort of the step's transit occurrences.
+#include <cub/cub.cuh>
 
-extern "C" int nd_run_collective(const nd_graph*, int, int64_t, int64_t, int, int64_t, int64_t,
-                                 int64_t, int64_t, int64_t, int64_t, const int64_t*,
-                                 const int64_t*, uint64_t, int64_t, void*, nd_result**) {
-  nd_set_last_error("nd_run_collective: not built yet", __FILE__, __LINE__);
-  return ND_ERR_ARG;
+#include <algorithm>
+#include <vector>
+
+#include "nd_tp.cuh"
+
+using namespace nd;
+
+namespace {
+
+template <typename T>
+int scan_excl(const T* in, T* out, int64_t n, cudaStream_t s) {
+  size_t tb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, n, s);
+  void* tmp = nullptr;
+  ND_CUDA_TRY(nd_alloc((char**)&tmp, tb, s));
+  ND_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tb, in, out, n, s));
+  nd_free(tmp, s);
+  return ND_OK;
+}
+
+template <typename T>
+int dcopy_to_host(T* h, const T* d, int64_t n, cudaStream_t s) {
+  ND_CUDA_TRY(cudaMemcpyAsync(h, d, n * sizeof(T), cudaMemcpyDeviceToHost, s));
+  ND_CUDA_TRY(cudaStreamSynchronize(s));
+  return ND_OK;
+}
+
+// degrees of the flattened transits (+1 trailing 0 for the exclusive scan)
+__global__ void k_tdeg(const int32_t* __restrict__ tv, int64_t T, const int64_t* __restrict__ row,
+                       int64_t* __restrict__ d) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j <= T;
+       j += (int64_t)gridDim.x * blockDim.x)
+    d[j] = j < T ? row[tv[j] + 1] - row[tv[j]] : 0;
+}
+
+// locate combined entry e of sample i: transit index k in [a, b) with
+// cdeg[k] - cdeg[a] <= e < cdeg[k+1] - cdeg[a]
+__device__ __forceinline__ int64_t locate(const int64_t* __restrict__ cdeg, int64_t a, int64_t b,
+                                          int64_t e) {
+  const int64_t base = cdeg[a];
+  int64_t lo = a, hi = b;  // last k with cdeg[k] - base <= e
+  while (hi - lo > 1) {
+    int64_t mid = (lo + hi) >> 1;
+    if (cdeg[mid] - base <= e) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+struct SelCtx {
+  DevGraph g;
+  int kind;
+  int64_t m, max_size, V;
+  uint64_t base0;
+  int64_t sample_lo;
+  const int64_t* toff;     // [n+1] transit offsets per sample (this step)
+  const int32_t* tv;       // transits
+  const int64_t* cdeg;     // [T+1] exclusive scan of transit degrees
+  const int64_t* size;     // per sample size before this step
+  const uint8_t* alive;
+  const double* cum;       // deg^2 CDF (importance, degree_sq)
+  int distribution;
+  int32_t* out;            // [n*m]
+  int32_t* rec_t1;         // mvs: one record per slot ([n*m], -1 = none)
+};
+
+// layer / importance / mvs slot selection: one thread per (sample, slot)
+__global__ void k_select(SelCtx c, int64_t n) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n * c.m;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = j / c.m, slot = j - i * c.m;
+    int32_t o = -1, rt = -1;
+    if (c.alive[i]) {
+      const int64_t a = c.toff[i], b = c.toff[i + 1];
+      const int64_t total = c.cdeg[b] - c.cdeg[a];
+      const uint64_t u = draw_u64(c.base0, key_item((uint64_t)(c.sample_lo + i), 0, (uint64_t)slot));
+      if (c.kind == ND_LAYER) {
+        int64_t take = c.max_size - c.size[i];
+        if (take < 0) take = 0;
+        if (take > c.m) take = c.m;
+        if (total > 0 && slot < take) {
+          const int64_t e = (int64_t)mod_u64(u, (uint64_t)total);
+          const int64_t k = locate(c.cdeg, a, b, e);
+          const int64_t t = c.tv[k];
+          o = __ldg(c.g.col + __ldg(c.g.row + t) + (e - (c.cdeg[k] - c.cdeg[a])));
+        }
+      } else if (c.kind == ND_MVS) {
+        if (total > 0) {
+          const int64_t e = (int64_t)mod_u64(u, (uint64_t)total);
+          const int64_t k = locate(c.cdeg, a, b, e);
+          const int64_t t = c.tv[k];
+          o = __ldg(c.g.col + __ldg(c.g.row + t) + (e - (c.cdeg[k] - c.cdeg[a])));
+          rt = (int32_t)t;
+        }
+      } else {  // importance
+        if (c.distribution == 0) {
+          o = (int32_t)mod_u64(u, (uint64_t)c.V);
+        } else {
+          const double x = __dmul_rn(to_unit(u), c.cum[c.V - 1]);
+          int64_t lo = 0, hi = c.V;
+          while (lo < hi) {
+            int64_t mid = (lo + hi) >> 1;
+            if (c.cum[mid] <= x) lo = mid + 1; else hi = mid;
+          }
+          o = (int32_t)(lo < c.V - 1 ? lo : c.V - 1);
+        }
+      }
+    }
+    c.out[j] = o;
+    if (c.rec_t1) c.rec_t1[j] = rt;
+  }
+}
+
+// importance hits: one thread per (sample, slot, transit) triple
+__global__ void k_imp_hits(const DevGraph g, const int64_t* __restrict__ toff,
+                           const int32_t* __restrict__ tv, const int32_t* __restrict__ out,
+                           const uint8_t* __restrict__ alive, const int64_t* __restrict__ tri_off,
+                           int64_t n, int64_t m, int64_t total_tri, uint8_t* __restrict__ flag) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < total_tri;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = 0, hi = n;  // sample: last i with tri_off[i] <= j
+    while (hi - lo > 1) {
+      int64_t mid = (lo + hi) >> 1;
+      if (tri_off[mid] <= j) lo = mid; else hi = mid;
+    }
+    const int64_t i = lo;
+    const int64_t T = toff[i + 1] - toff[i];
+    const int64_t r = j - tri_off[i];
+    const int64_t slot = r / T, k = r - slot * T;
+    const int64_t t = tv[toff[i] + k];
+    const int64_t v = out[i * m + slot];
+    flag[j] = has_edge(g.col, __ldg(g.row + t), __ldg(g.row + t + 1), v) ? 1 : 0;
+  }
+}
+
+__global__ void k_imp_write(const int64_t* __restrict__ toff, const int32_t* __restrict__ tv,
+                            const int32_t* __restrict__ out, const int64_t* __restrict__ tri_off,
+                            int64_t n, int64_t m, int64_t total_tri, const uint8_t* __restrict__ flag,
+                            const int64_t* __restrict__ pos, int64_t* __restrict__ rt,
+                            int64_t* __restrict__ rv) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < total_tri;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    if (!flag[j]) continue;
+    int64_t lo = 0, hi = n;
+    while (hi - lo > 1) {
+      int64_t mid = (lo + hi) >> 1;
+      if (tri_off[mid] <= j) lo = mid; else hi = mid;
+    }
+    const int64_t i = lo;
+    const int64_t T = toff[i + 1] - toff[i];
+    const int64_t r = j - tri_off[i];
+    const int64_t slot = r / T, k = r - slot * T;
+    rt[pos[j]] = tv[toff[i] + k];
+    rv[pos[j]] = out[i * m + slot];
+  }
+}
+
+// per-sample triple offsets (importance): m * transits, 0 when dead
+__global__ void k_tri_len(const int64_t* __restrict__ toff, const uint8_t* __restrict__ alive,
+                          int64_t n, int64_t m, int64_t* __restrict__ len) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    len[i] = (i < n && alive[i]) ? m * (toff[i + 1] - toff[i]) : 0;
+}
+
+// per-sample counts between offsets of a scanned flag array
+__global__ void k_seg_counts(const int64_t* __restrict__ seg, const int64_t* __restrict__ pos,
+                             int64_t n, int64_t* __restrict__ cnt) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    cnt[i] = pos[seg[i + 1]] - pos[seg[i]];
+}
+
+// ---- clustergcn -------------------------------------------------------------------
+__global__ void k_bitmap_set(const int64_t* __restrict__ roff, const int32_t* __restrict__ roots,
+                             int64_t n, int64_t words, uint32_t* __restrict__ bm) {
+  for (int64_t i = blockIdx.y; i < n; i += gridDim.y)
+    for (int64_t k = roff[i] + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < roff[i + 1];
+         k += (int64_t)gridDim.x * blockDim.x) {
+      const uint32_t v = (uint32_t)roots[k];
+      atomicOr(bm + i * words + (v >> 5), 1u << (v & 31));
+    }
+}
+
+// one warp per (sample, transit) pair; pass 0 counts hits, pass 1 writes them
+// in adjacency order at the pair's scanned offset
+template <int PASS>
+__global__ void k_cgcn(const DevGraph g, const int64_t* __restrict__ toff, const int32_t* __restrict__ tv,
+                       int64_t n, int64_t T, const uint32_t* __restrict__ bm, int64_t words,
+                       int64_t* __restrict__ cnt, const int64_t* __restrict__ off,
+                       int64_t* __restrict__ rt, int64_t* __restrict__ rv) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t p = warp; p < T; p += nw) {
+    int64_t lo = 0, hi = n;  // owner sample of pair p
+    while (hi - lo > 1) {
+      int64_t mid = (lo + hi) >> 1;
+      if (toff[mid] <= p) lo = mid; else hi = mid;
+    }
+    const uint32_t* b = bm + lo * words;
+    const int64_t t = tv[p];
+    const int64_t r0 = __ldg(g.row + t), r1 = __ldg(g.row + t + 1);
+    int64_t acc = PASS == 1 ? off[p] : 0;
+    for (int64_t e = r0; e < r1; e += 32) {
+      const int64_t ee = e + lane;
+      bool hit = false;
+      uint32_t v = 0;
+      if (ee < r1) {
+        v = (uint32_t)__ldg(g.col + ee);
+        hit = (__ldg(b + (v >> 5)) >> (v & 31)) & 1u;
+      }
+      const unsigned mk = __ballot_sync(0xffffffffu, hit);
+      if (PASS == 1 && hit) {
+        const int64_t q = acc + __popc(mk & ((1u << lane) - 1));
+        rt[q] = t;
+        rv[q] = v;
+      }
+      acc += __popc(mk);
+    }
+    if (PASS == 0 && lane == 0) cnt[p] = acc;
+  }
+}
+
+// ---- step plumbing ----------------------------------------------------------------------
+__global__ void k_alive_from_toff(const int64_t* __restrict__ toff, int64_t n,
+                                  uint8_t* __restrict__ alive) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    alive[i] = toff[i + 1] > toff[i];
+}
+
+__global__ void k_step_counts(const uint8_t* __restrict__ alive, int64_t n, int64_t m,
+                              int64_t* __restrict__ cnt, int64_t* __restrict__ nn_flags_len) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    cnt[i] = alive[i] ? m : 0;
+}
+
+// non-NULL slots of alive samples -> next transits; per-sample next counts
+__global__ void k_nonnull(const int32_t* __restrict__ out, const uint8_t* __restrict__ alive,
+                          int64_t n, int64_t m, int64_t* __restrict__ flag) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j <= n * m;
+       j += (int64_t)gridDim.x * blockDim.x)
+    flag[j] = (j < n * m && alive[j / m] && out[j] >= 0) ? 1 : 0;
+}
+
+__global__ void k_next_transits(const int32_t* __restrict__ out, const int64_t* __restrict__ flag,
+                                const int64_t* __restrict__ pos, int64_t nm, int32_t* __restrict__ ntv) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nm;
+       j += (int64_t)gridDim.x * blockDim.x)
+    if (flag[j]) ntv[pos[j]] = out[j];
+}
+
+__global__ void k_next_toff(const int64_t* __restrict__ pos, int64_t n, int64_t m,
+                            int64_t* __restrict__ ntoff, int64_t* __restrict__ size) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    ntoff[i] = pos[i * m];
+    if (i < n) size[i] += pos[(i + 1) * m] - pos[i * m];
+  }
+}
+
+// out slots of alive samples, compacted in step-major sample order
+__global__ void k_emit_slots(const int32_t* __restrict__ out, const uint8_t* __restrict__ alive,
+                             const int64_t* __restrict__ base, int64_t n, int64_t m,
+                             int64_t* __restrict__ vals) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n * m;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = j / m;
+    if (alive[i]) vals[base[i] * m + (j - i * m)] = out[j];
+  }
+}
+
+__global__ void k_alive_idx(const uint8_t* __restrict__ alive, int64_t n, int64_t* __restrict__ a) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    a[i] = i < n ? alive[i] : 0;
+}
+
+// mvs: records from one-per-slot (t, v) where v non-NULL
+__global__ void k_mvs_flags(const int32_t* __restrict__ rec_t1, int64_t nm, int64_t* __restrict__ f) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j <= nm;
+       j += (int64_t)gridDim.x * blockDim.x)
+    f[j] = (j < nm && rec_t1[j] >= 0) ? 1 : 0;
+}
+
+__global__ void k_mvs_write(const int32_t* __restrict__ rec_t1, const int32_t* __restrict__ out,
+                            const int64_t* __restrict__ f, const int64_t* __restrict__ pos, int64_t nm,
+                            int64_t* __restrict__ rt, int64_t* __restrict__ rv) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nm;
+       j += (int64_t)gridDim.x * blockDim.x)
+    if (f[j]) {
+      rt[pos[j]] = rec_t1[j];
+      rv[pos[j]] = out[j];
+    }
+}
+
+__global__ void k_mvs_counts(const int64_t* __restrict__ pos, int64_t n, int64_t m,
+                             int64_t* __restrict__ cnt) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    cnt[i] = pos[(i + 1) * m] - pos[i * m];
+}
+
+// TP build stats: group classes with work = members * degree(transit)
+__global__ void k_classify_deg(const uint32_t* __restrict__ keys, const int* __restrict__ gstart,
+                               const int* __restrict__ n_groups, const int64_t* __restrict__ row,
+                               unsigned long long* __restrict__ stats) {
+  const int G = *n_groups;
+  int cnt[3] = {0, 0, 0};
+  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < G; g += gridDim.x * blockDim.x) {
+    const uint32_t t = keys[gstart[g]];
+    const int64_t work = (int64_t)(gstart[g + 1] - gstart[g]) * (row[t + 1] - row[t]);
+    cnt[work < SMALL_MAX_WORK ? 0 : (work <= LARGE_MIN_WORK ? 1 : 2)]++;
+  }
+  for (int c = 0; c < 3; c++) {
+    int v = cnt[c];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(stats + c, (unsigned long long)v);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(stats + 3, (unsigned long long)G);
+}
+
+__global__ void k_u32(const int32_t* __restrict__ a, int64_t n, uint32_t* __restrict__ k,
+                      uint64_t* __restrict__ v) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    k[j] = (uint32_t)a[j];
+    v[j] = (uint64_t)j;
+  }
+}
+
+__global__ void k_deg2(const int64_t* __restrict__ row, int64_t V, int64_t* __restrict__ d2) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t d = row[v + 1] - row[v];
+    d2[v] = d * d;
+  }
+}
+
+__global__ void k_i64_to_f64(const int64_t* __restrict__ a, int64_t n, double* __restrict__ b) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x)
+    b[v] = (double)a[v];
+}
+
+// clustergcn roots: cluster of each vertex keyed on (seed, vertex) domain 4
+__global__ void k_cluster_flags(int64_t V, uint64_t base4, int64_t nc, const uint8_t* __restrict__ chosen,
+                                int64_t* __restrict__ flag) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v <= V;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    if (v == V) { flag[V] = 0; continue; }
+    const uint64_t u = draw_u64(base4, key_item((uint64_t)v, 0, 0));
+    flag[v] = chosen[mod_u64(u, (uint64_t)nc)] ? 1 : 0;
+  }
+}
+
+__global__ void k_cluster_write(const int64_t* __restrict__ flag, const int64_t* __restrict__ pos,
+                                int64_t V, int32_t* __restrict__ out) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V;
+       v += (int64_t)gridDim.x * blockDim.x)
+    if (flag[v]) out[pos[v]] = (int32_t)v;
+}
+
+__global__ void k_widen32(const int32_t* __restrict__ a, int64_t n, int64_t* __restrict__ b) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x)
+    b[j] = a[j];
+}
+
+__global__ void k_narrow64(const int64_t* __restrict__ a, int64_t n, int32_t* __restrict__ b) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x)
+    b[j] = (int32_t)a[j];
+}
+
+// final rows: roots then every step's non-NULL slots
+__global__ void k_coll_final(const int64_t* __restrict__ roff, const int32_t* __restrict__ roots,
+                             int64_t n, const int64_t* __restrict__ off, int64_t* __restrict__ ids) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    for (int64_t k = roff[i]; k < roff[i + 1]; k++) ids[off[i] + (k - roff[i])] = roots[k];
+}
+
+__global__ void k_coll_final_step(const int32_t* __restrict__ ntv, const int64_t* __restrict__ ntoff,
+                                  int64_t n, const int64_t* __restrict__ off,
+                                  const int64_t* __restrict__ fill, int64_t* __restrict__ ids) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    for (int64_t k = ntoff[i]; k < ntoff[i + 1]; k++)
+      ids[off[i] + fill[i] + (k - ntoff[i])] = ntv[k];
+}
+
+__global__ void k_fill_add(int64_t* __restrict__ fill, const int64_t* __restrict__ ntoff, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    fill[i] += ntoff[i + 1] - ntoff[i];
+}
+
+struct CStep {
+  int64_t* counts = nullptr;     // [n]
+  int64_t* vals = nullptr;       // alive*m
+  int64_t nvals = 0;
+  int64_t* rec_cnt = nullptr;    // [n]
+  int64_t* rec_t = nullptr;
+  int64_t* rec_v = nullptr;
+  int64_t nrec = 0;
+  int32_t* ntv = nullptr;        // next transits (non-NULL of this step)
+  int64_t* ntoff = nullptr;      // [n+1]
+};
+
+}  // namespace
+
+extern "C" int nd_run_collective(const nd_graph* G, int kind, int64_t step_size, int64_t max_size,
+                                 int distribution, int64_t steps, int64_t batch_size,
+                                 int64_t clusters_per_sample, int64_t num_clusters,
+                                 int64_t sample_lo, int64_t n, const int64_t* roots_off_in,
+                                 const int64_t* roots_in, uint64_t seed, int64_t step_cap,
+                                 void* stream, nd_result** out_res) {
+  nd_pool_init();
+  if (!G || n < 0 || sample_lo < 0 || step_size < 1 || kind < 0 || kind > 3) return kind < 0 || kind > 3 ? ND_ERR_APP : ND_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  const DevGraph& g = G->g;
+  const int64_t V = g.V;
+  const int64_t m = step_size;
+  const int64_t S_max = steps >= 0 ? std::min(steps, step_cap) : step_cap;
+  std::vector<int64_t> h_roff(n + 1, 0);
+
+  // ---- roots (CSR, int32) ---------------------------------------------------------
+  int64_t* roff = nullptr;
+  int32_t* roots = nullptr;
+  ND_CUDA_TRY(nd_alloc(&roff, n + 1, s));
+  if (roots_in) {
+    ND_CUDA_TRY(cudaMemcpyAsync(roff, roots_off_in, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+    ND_TRY(dcopy_to_host(h_roff.data(), roff, n + 1, s));
+    ND_CUDA_TRY(nd_alloc(&roots, h_roff[n], s));
+    if (h_roff[n]) k_narrow64<<<nd_grid(h_roff[n], 256), 256, 0, s>>>(roots_in, h_roff[n], roots);
+  } else if (kind == ND_CLUSTERGCN) {
+    if (num_clusters < 1 || clusters_per_sample < 0) return ND_ERR_ARG;
+    // chosen clusters per sample (apps.py:357-366): keyed draws until distinct
+    const int64_t want = std::min(clusters_per_sample, num_clusters);
+    std::vector<std::vector<int32_t>> parts(n);
+    int64_t* flag = nullptr;
+    int64_t* pos = nullptr;
+    uint8_t* chosen = nullptr;
+    ND_CUDA_TRY(nd_alloc(&flag, V + 1, s));
+    ND_CUDA_TRY(nd_alloc(&pos, V + 1, s));
+    ND_CUDA_TRY(nd_alloc(&chosen, num_clusters, s));
+    std::vector<int32_t*> rparts(n, nullptr);
+    for (int64_t i = 0; i < n; i++) {
+      std::vector<uint8_t> ch(num_clusters, 0);
+      int64_t have = 0;
+      uint64_t b = key_base(seed, 0, 5, 0);
+      const uint64_t ik = key_item((uint64_t)(sample_lo + i), 0, 0);
+      while (have < want) {
+        const uint64_t c = fin64(fin64(b + ik)) % (uint64_t)num_clusters;
+        b += C_DRAW;
+        if (!ch[c]) { ch[c] = 1; have++; }
+      }
+      ND_CUDA_TRY(cudaMemcpyAsync(chosen, ch.data(), num_clusters, cudaMemcpyHostToDevice, s));
+      k_cluster_flags<<<nd_grid(V + 1, 256), 256, 0, s>>>(V, key_base(seed, 0, 4, 0), num_clusters,
+                                                           chosen, flag);
+      ND_TRY(scan_excl(flag, pos, V + 1, s));
+      int64_t cnt = 0;
+      ND_TRY(dcopy_to_host(&cnt, pos + V, 1, s));
+      ND_CUDA_TRY(nd_alloc(&rparts[i], cnt, s));
+      if (V) k_cluster_write<<<nd_grid(V, 256), 256, 0, s>>>(flag, pos, V, rparts[i]);
+      h_roff[i + 1] = h_roff[i] + cnt;
+    }
+    ND_CUDA_TRY(nd_alloc(&roots, h_roff[n], s));
+    for (int64_t i = 0; i < n; i++) {
+      const int64_t c = h_roff[i + 1] - h_roff[i];
+      if (c) ND_CUDA_TRY(cudaMemcpyAsync(roots + h_roff[i], rparts[i], c * 4, cudaMemcpyDeviceToDevice, s));
+      nd_free(rparts[i], s);
+    }
+    ND_CUDA_TRY(cudaMemcpyAsync(roff, h_roff.data(), (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    nd_free(flag, s); nd_free(pos, s); nd_free(chosen, s);
+  } else {
+    const int64_t R = kind == ND_LAYER ? 1 : batch_size;
+    if (R < 1) return ND_ERR_ARG;
+    for (int64_t i = 0; i <= n; i++) h_roff[i] = i * R;
+    ND_CUDA_TRY(cudaMemcpyAsync(roff, h_roff.data(), (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    ND_CUDA_TRY(nd_alloc(&roots, n * R, s));
+    ND_TRY(nd_uniform_roots_i32(g, R, seed, sample_lo, n, roots, s));
+  }
+  const int64_t n_roots = h_roff[n];
+
+  // deg^2 CDF (apps.py:291-296): exact integer prefix converted to f64
+  double* cum = nullptr;
+  if (kind == ND_IMPORTANCE && distribution == 1 && V > 0) {
+    int64_t *d2 = nullptr, *c2 = nullptr;
+    ND_CUDA_TRY(nd_alloc(&d2, V, s));
+    ND_CUDA_TRY(nd_alloc(&c2, V, s));
+    ND_CUDA_TRY(nd_alloc(&cum, V, s));
+    k_deg2<<<nd_grid(V, 256), 256, 0, s>>>(g.row, V, d2);
+    size_t tb = 0;
+    cub::DeviceScan::InclusiveSum(nullptr, tb, d2, c2, V, s);
+    void* tmp;
+    ND_CUDA_TRY(nd_alloc((char**)&tmp, tb, s));
+    ND_CUDA_TRY(cub::DeviceScan::InclusiveSum(tmp, tb, d2, c2, V, s));
+    k_i64_to_f64<<<nd_grid(V, 256), 256, 0, s>>>(c2, V, cum);
+    nd_free(tmp, s); nd_free(d2, s); nd_free(c2, s);
+  }
+
+  // ---- step loop -----------------------------------------------------------------------
+  int64_t *size = nullptr, *toff = nullptr;
+  uint8_t* alive = nullptr;
+  int32_t* tv = roots;
+  unsigned long long* stats = nullptr;
+  ND_CUDA_TRY(nd_alloc(&size, n, s));
+  ND_CUDA_TRY(nd_alloc(&alive, n, s));
+  ND_CUDA_TRY(nd_alloc(&toff, n + 1, s));
+  ND_CUDA_TRY(nd_alloc(&stats, 4 * (S_max + 1), s));
+  ND_CUDA_TRY(cudaMemsetAsync(stats, 0, 4 * (S_max + 1) * sizeof(unsigned long long), s));
+  ND_CUDA_TRY(cudaMemcpyAsync(toff, roff, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+  {
+    std::vector<int64_t> hs(n);
+    for (int64_t i = 0; i < n; i++) hs[i] = h_roff[i + 1] - h_roff[i];
+    if (n) ND_CUDA_TRY(cudaMemcpyAsync(size, hs.data(), n * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    ND_CUDA_TRY(cudaStreamSynchronize(s));
+  }
+  int64_t T = n_roots;
+  std::vector<CStep> steps_v;
+  const int key_bits = key_bits_for(V);
+  int64_t step = 0;
+  int64_t total_rec = 0;
+  while (step < S_max) {
+    if (n) k_alive_from_toff<<<nd_grid(n, 256), 256, 0, s>>>(toff, n, alive);
+    if (T == 0) break;  // no sample has transits (is_alive, core.py:195-203)
+    CStep cs;
+    // TP build statistics over the step's transit occurrences
+    {
+      TPScratch S;
+      ND_TRY(S.alloc(T, key_bits, s));
+      uint32_t *k0, *k1;
+      uint64_t *v0, *v1;
+      ND_CUDA_TRY(nd_alloc(&k0, T, s)); ND_CUDA_TRY(nd_alloc(&k1, T, s));
+      ND_CUDA_TRY(nd_alloc(&v0, T, s)); ND_CUDA_TRY(nd_alloc(&v1, T, s));
+      k_u32<<<nd_grid(T, 256), 256, 0, s>>>(tv, T, k0, v0);
+      cub::DoubleBuffer<uint32_t> dk(k0, k1);
+      cub::DoubleBuffer<uint64_t> dv(v0, v1);
+      ND_TRY(tp_sort(dk, dv, T, key_bits, S, s));
+      k_mark<<<nd_grid(T, 256), 256, 0, s>>>(dk.Current(), T, S.flags);
+      size_t tb = S.cub_bytes;
+      ND_CUDA_TRY(cub::DeviceScan::InclusiveSum(S.cub_tmp, tb, S.flags, S.gid, (int)T, s));
+      ND_CUDA_TRY(cudaMemsetAsync(S.counters, 0, 4 * sizeof(int), s));
+      k_gstart<<<nd_grid(T, 256), 256, 0, s>>>(S.flags, S.gid, T, S.gstart, S.counters);
+      k_classify_deg<<<nd_grid(T, 256), 256, 0, s>>>(dk.Current(), S.gstart, S.counters, g.row,
+                                                      stats + 4 * step);
+      nd_free(k0, s); nd_free(k1, s); nd_free(v0, s); nd_free(v1, s);
+      S.release(s);
+    }
+    // combined-neighbourhood index: exclusive scan of transit degrees
+    int64_t *dg = nullptr, *cdeg = nullptr;
+    ND_CUDA_TRY(nd_alloc(&dg, T + 1, s));
+    ND_CUDA_TRY(nd_alloc(&cdeg, T + 1, s));
+    k_tdeg<<<nd_grid(T + 1, 256), 256, 0, s>>>(tv, T, g.row, dg);
+    ND_TRY(scan_excl(dg, cdeg, T + 1, s));
+    int32_t* out = nullptr;
+    int32_t* rec1 = nullptr;
+    ND_CUDA_TRY(nd_alloc(&out, n * m, s));
+    ND_CUDA_TRY(nd_alloc(&cs.counts, n, s));
+    ND_CUDA_TRY(nd_alloc(&cs.rec_cnt, n, s));
+    ND_CUDA_TRY(cudaMemsetAsync(cs.rec_cnt, 0, n * sizeof(int64_t), s));
+    if (kind == ND_MVS) ND_CUDA_TRY(nd_alloc(&rec1, n * m, s));
+    if (kind != ND_CLUSTERGCN) {
+      SelCtx c{g, kind, m, max_size, V, key_base(seed, (uint64_t)step, 0, 0), sample_lo, toff, tv,
+               cdeg, size, alive, cum, distribution, out, rec1};
+      if (n * m) k_select<<<nd_grid(n * m, 256, 148 * 64), 256, 0, s>>>(c, n);
+    } else {
+      ND_CUDA_TRY(cudaMemsetAsync(out, 0xFF, n * m * sizeof(int32_t), s));  // all NULL
+    }
+    // recorded edges
+    if (kind == ND_IMPORTANCE) {
+      int64_t *tl = nullptr, *tri_off = nullptr;
+      ND_CUDA_TRY(nd_alloc(&tl, n + 1, s));
+      ND_CUDA_TRY(nd_alloc(&tri_off, n + 1, s));
+      k_tri_len<<<nd_grid(n + 1, 256), 256, 0, s>>>(toff, alive, n, m, tl);
+      ND_TRY(scan_excl(tl, tri_off, n + 1, s));
+      int64_t tot_tri = 0;
+      ND_TRY(dcopy_to_host(&tot_tri, tri_off + n, 1, s));
+      uint8_t* fl = nullptr;
+      int64_t* pos = nullptr;
+      ND_CUDA_TRY(nd_alloc(&fl, tot_tri + 1, s));
+      ND_CUDA_TRY(nd_alloc(&pos, tot_tri + 1, s));
+      ND_CUDA_TRY(cudaMemsetAsync(fl, 0, tot_tri + 1, s));
+      if (tot_tri)
+        k_imp_hits<<<nd_grid(tot_tri, 256, 148 * 64), 256, 0, s>>>(g, toff, tv, out, alive, tri_off,
+                                                                   n, m, tot_tri, fl);
+      // widen flags for the scan
+      {
+        auto widen = [] __device__(uint8_t x) { return (int64_t)x; };
+        cub::TransformInputIterator<int64_t, decltype(widen), const uint8_t*> it(fl, widen);
+        size_t tb = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, tb, it, pos, tot_tri + 1, s);
+        void* tmp;
+        ND_CUDA_TRY(nd_alloc((char**)&tmp, tb, s));
+        ND_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tb, it, pos, tot_tri + 1, s));
+        nd_free(tmp, s);
+      }
+      ND_TRY(dcopy_to_host(&cs.nrec, pos + tot_tri, 1, s));
+      ND_CUDA_TRY(nd_alloc(&cs.rec_t, cs.nrec, s));
+      ND_CUDA_TRY(nd_alloc(&cs.rec_v, cs.nrec, s));
+      if (tot_tri)
+        k_imp_write<<<nd_grid(tot_tri, 256, 148 * 64), 256, 0, s>>>(toff, tv, out, tri_off, n, m,
+                                                                    tot_tri, fl, pos, cs.rec_t,
+                                                                    cs.rec_v);
+      if (n) k_seg_counts<<<nd_grid(n, 256), 256, 0, s>>>(tri_off, pos, n, cs.rec_cnt);
+      nd_free(tl, s); nd_free(tri_off, s); nd_free(fl, s); nd_free(pos, s);
+    } else if (kind == ND_MVS) {
+      int64_t *f = nullptr, *pos = nullptr;
+      ND_CUDA_TRY(nd_alloc(&f, n * m + 1, s));
+      ND_CUDA_TRY(nd_alloc(&pos, n * m + 1, s));
+      k_mvs_flags<<<nd_grid(n * m + 1, 256), 256, 0, s>>>(rec1, n * m, f);
+      ND_TRY(scan_excl(f, pos, n * m + 1, s));
+      ND_TRY(dcopy_to_host(&cs.nrec, pos + n * m, 1, s));
+      ND_CUDA_TRY(nd_alloc(&cs.rec_t, cs.nrec, s));
+      ND_CUDA_TRY(nd_alloc(&cs.rec_v, cs.nrec, s));
+      if (n * m) k_mvs_write<<<nd_grid(n * m, 256), 256, 0, s>>>(rec1, out, f, pos, n * m, cs.rec_t, cs.rec_v);
+      if (n) k_mvs_counts<<<nd_grid(n, 256), 256, 0, s>>>(pos, n, m, cs.rec_cnt);
+      nd_free(f, s); nd_free(pos, s);
+    } else if (kind == ND_CLUSTERGCN) {
+      // the sample's own roots as a bitmap (np.isin against sample.roots)
+      const int64_t words = (V + 31) / 32;
+      uint32_t* bm = nullptr;
+      int64_t *cnt = nullptr, *off = nullptr;
+      ND_CUDA_TRY(nd_alloc(&bm, n * words, s));
+      ND_CUDA_TRY(cudaMemsetAsync(bm, 0, n * words * sizeof(uint32_t), s));
+      ND_CUDA_TRY(nd_alloc(&cnt, T + 1, s));
+      ND_CUDA_TRY(nd_alloc(&off, T + 1, s));
+      ND_CUDA_TRY(cudaMemsetAsync(cnt, 0, (T + 1) * sizeof(int64_t), s));
+      if (n_roots) {
+        dim3 gr((unsigned)std::min<int64_t>(1024, (n_roots / std::max<int64_t>(n, 1) + 255) / 256 + 1),
+                (unsigned)std::min<int64_t>(n, 65535));
+        k_bitmap_set<<<gr, 256, 0, s>>>(roff, roots, n, words, bm);
+      }
+      // m slots each record the same set (apps.py:372-379 runs per slot)
+      for (int64_t sl = 0; sl < m; sl++) {
+        k_cgcn<0><<<148 * 16, 256, 0, s>>>(g, toff, tv, n, T, bm, words, cnt, nullptr, nullptr, nullptr);
+        ND_TRY(scan_excl(cnt, off, T + 1, s));
+        int64_t nr = 0;
+        ND_TRY(dcopy_to_host(&nr, off + T, 1, s));
+        int64_t *rt = nullptr, *rv = nullptr;
+        ND_CUDA_TRY(nd_alloc(&rt, cs.nrec + nr, s));
+        ND_CUDA_TRY(nd_alloc(&rv, cs.nrec + nr, s));
+        if (cs.nrec) {
+          ND_CUDA_TRY(cudaMemcpyAsync(rt, cs.rec_t, cs.nrec * 8, cudaMemcpyDeviceToDevice, s));
+          ND_CUDA_TRY(cudaMemcpyAsync(rv, cs.rec_v, cs.nrec * 8, cudaMemcpyDeviceToDevice, s));
+        }
+        k_cgcn<1><<<148 * 16, 256, 0, s>>>(g, toff, tv, n, T, bm, words, nullptr, off, rt + cs.nrec,
+                                           rv + cs.nrec);
+        nd_free(cs.rec_t, s);
+        nd_free(cs.rec_v, s);
+        cs.rec_t = rt;
+        cs.rec_v = rv;
+        cs.nrec += nr;
+      }
+      // per-sample record counts: records of sample i are pairs [toff[i], toff[i+1])
+      if (n) k_seg_counts<<<nd_grid(n, 256), 256, 0, s>>>(toff, off, n, cs.rec_cnt);
+      nd_free(bm, s); nd_free(cnt, s); nd_free(off, s);
+    }
+    total_rec += cs.nrec;
+    // per-step slots of alive samples
+    if (n) k_step_counts<<<nd_grid(n, 256), 256, 0, s>>>(alive, n, m, cs.counts, nullptr);
+    {
+      int64_t *ai = nullptr, *abase = nullptr;
+      ND_CUDA_TRY(nd_alloc(&ai, n + 1, s));
+      ND_CUDA_TRY(nd_alloc(&abase, n + 1, s));
+      k_alive_idx<<<nd_grid(n + 1, 256), 256, 0, s>>>(alive, n, ai);
+      ND_TRY(scan_excl(ai, abase, n + 1, s));
+      int64_t na = 0;
+      ND_TRY(dcopy_to_host(&na, abase + n, 1, s));
+      cs.nvals = na * m;
+      ND_CUDA_TRY(nd_alloc(&cs.vals, cs.nvals, s));
+      if (n * m) k_emit_slots<<<nd_grid(n * m, 256), 256, 0, s>>>(out, alive, abase, n, m, cs.vals);
+      nd_free(ai, s);
+      nd_free(abase, s);
+    }
+    // next transits = non-NULL slots (stable); sizes grow by the same count
+    {
+      int64_t *f = nullptr, *pos = nullptr;
+      ND_CUDA_TRY(nd_alloc(&f, n * m + 1, s));
+      ND_CUDA_TRY(nd_alloc(&pos, n * m + 1, s));
+      k_nonnull<<<nd_grid(n * m + 1, 256), 256, 0, s>>>(out, alive, n, m, f);
+      ND_TRY(scan_excl(f, pos, n * m + 1, s));
+      int64_t nt = 0;
+      ND_TRY(dcopy_to_host(&nt, pos + n * m, 1, s));
+      ND_CUDA_TRY(nd_alloc(&cs.ntv, nt, s));
+      ND_CUDA_TRY(nd_alloc(&cs.ntoff, n + 1, s));
+      if (n * m) k_next_transits<<<nd_grid(n * m, 256), 256, 0, s>>>(out, f, pos, n * m, cs.ntv);
+      k_next_toff<<<nd_grid(n + 1, 256), 256, 0, s>>>(pos, n, m, cs.ntoff, size);
+      ND_CUDA_TRY(cudaMemcpyAsync(toff, cs.ntoff, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+      T = nt;
+      tv = cs.ntv;
+      nd_free(f, s);
+      nd_free(pos, s);
+    }
+    nd_free(out, s); nd_free(rec1, s); nd_free(dg, s); nd_free(cdeg, s);
+    ND_CUDA_TRY(cudaGetLastError());
+    steps_v.push_back(cs);
+    step++;
+  }
+  const int64_t n_steps = step;
+  ND_CUDA_TRY(cudaStreamSynchronize(s));
+
+  // ---- outputs ------------------------------------------------------------------------
+  int64_t *final_off = nullptr, *final_ids = nullptr, *flen = nullptr, *fill = nullptr,
+          *roots_out = nullptr, *roots_off = nullptr, *step_counts = nullptr, *step_vals = nullptr,
+          *rec_counts = nullptr, *rec_t = nullptr, *rec_v = nullptr;
+  ND_CUDA_TRY(nd_alloc(&flen, n + 1, s));
+  ND_CUDA_TRY(nd_alloc(&final_off, n + 1, s));
+  ND_CUDA_TRY(nd_alloc(&fill, n, s));
+  // size[] = roots + all non-NULL slots = final row lengths
+  ND_CUDA_TRY(cudaMemsetAsync(flen + n, 0, sizeof(int64_t), s));
+  if (n) ND_CUDA_TRY(cudaMemcpyAsync(flen, size, n * sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+  ND_TRY(scan_excl(flen, final_off, n + 1, s));
+  int64_t total = 0;
+  ND_TRY(dcopy_to_host(&total, final_off + n, 1, s));
+  ND_CUDA_TRY(nd_alloc(&final_ids, total, s));
+  if (n) k_coll_final<<<nd_grid(n, 128), 128, 0, s>>>(roff, roots, n, final_off, final_ids);
+  {
+    // fill = root counts
+    std::vector<int64_t> hr(n);
+    for (int64_t i = 0; i < n; i++) hr[i] = h_roff[i + 1] - h_roff[i];
+    if (n) ND_CUDA_TRY(cudaMemcpyAsync(fill, hr.data(), n * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    ND_CUDA_TRY(cudaStreamSynchronize(s));
+  }
+  for (auto& cs : steps_v) {
+    if (n) {
+      k_coll_final_step<<<nd_grid(n, 128), 128, 0, s>>>(cs.ntv, cs.ntoff, n, final_off, fill, final_ids);
+      k_fill_add<<<nd_grid(n, 256), 256, 0, s>>>(fill, cs.ntoff, n);
+    }
+  }
+  ND_CUDA_TRY(nd_alloc(&roots_out, n_roots, s));
+  ND_CUDA_TRY(nd_alloc(&roots_off, n + 1, s));
+  if (n_roots) k_widen32<<<nd_grid(n_roots, 256), 256, 0, s>>>(roots, n_roots, roots_out);
+  ND_CUDA_TRY(cudaMemcpyAsync(roots_off, roff, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+  int64_t tot_vals = 0;
+  for (auto& cs : steps_v) tot_vals += cs.nvals;
+  ND_CUDA_TRY(nd_alloc(&step_counts, n_steps * n, s));
+  ND_CUDA_TRY(nd_alloc(&step_vals, tot_vals, s));
+  ND_CUDA_TRY(nd_alloc(&rec_counts, n_steps * n, s));
+  ND_CUDA_TRY(nd_alloc(&rec_t, total_rec, s));
+  ND_CUDA_TRY(nd_alloc(&rec_v, total_rec, s));
+  int64_t pv = 0, pr = 0;
+  for (int64_t st = 0; st < n_steps; st++) {
+    CStep& cs = steps_v[st];
+    if (n) {
+      ND_CUDA_TRY(cudaMemcpyAsync(step_counts + st * n, cs.counts, n * 8, cudaMemcpyDeviceToDevice, s));
+      ND_CUDA_TRY(cudaMemcpyAsync(rec_counts + st * n, cs.rec_cnt, n * 8, cudaMemcpyDeviceToDevice, s));
+    }
+    if (cs.nvals) ND_CUDA_TRY(cudaMemcpyAsync(step_vals + pv, cs.vals, cs.nvals * 8, cudaMemcpyDeviceToDevice, s));
+    if (cs.nrec) {
+      ND_CUDA_TRY(cudaMemcpyAsync(rec_t + pr, cs.rec_t, cs.nrec * 8, cudaMemcpyDeviceToDevice, s));
+      ND_CUDA_TRY(cudaMemcpyAsync(rec_v + pr, cs.rec_v, cs.nrec * 8, cudaMemcpyDeviceToDevice, s));
+    }
+    pv += cs.nvals;
+    pr += cs.nrec;
+  }
+  ND_CUDA_TRY(cudaGetLastError());
+  ND_CUDA_TRY(cudaStreamSynchronize(s));
+  for (auto& cs : steps_v) {
+    nd_free(cs.counts, s); nd_free(cs.vals, s); nd_free(cs.rec_cnt, s); nd_free(cs.rec_t, s);
+    nd_free(cs.rec_v, s); nd_free(cs.ntv, s); nd_free(cs.ntoff, s);
+  }
+  nd_free(size, s); nd_free(alive, s); nd_free(toff, s); nd_free(cum, s); nd_free(flen, s);
+  nd_free(fill, s); nd_free(roff, s); nd_free(roots, s);
+  nd_result* res = new nd_result();
+  res->stream = s;
+  res->n = n;
+  res->n_steps = n_steps;
+  res->total_sampled = total - n_roots;
+  res->total_recorded = total_rec;
+  res->set(ND_F_FINAL_OFF, final_off, n + 1);
+  res->set(ND_F_FINAL_IDS, final_ids, total);
+  res->set(ND_F_ROOTS, roots_out, n_roots);
+  res->set(ND_F_ROOTS_OFF, roots_off, n + 1);
+  res->set(ND_F_STEP_COUNTS, step_counts, n_steps * n);
+  res->set(ND_F_STEP_VALS, step_vals, tot_vals);
+  res->set(ND_F_REC_COUNTS, rec_counts, n_steps * n);
+  res->set(ND_F_REC_T, rec_t, total_rec);
+  res->set(ND_F_REC_V, rec_v, total_rec);
+  res->set(ND_F_STATS, stats, 4 * n_steps);
+  res->counters[NDC_STEPS] = n_steps;
+  *out_res = res;
+  return ND_OK;
 }

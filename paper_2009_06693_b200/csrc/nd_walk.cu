@@ -320,7 +320,10 @@ __global__ void k_pw_lengths(const int64_t* __restrict__ tot, const int32_t* __r
     flen[i] = R + tot[i];
     const int64_t c = tot[i] + died[i];
     clen[i] = c;
-    atomicAdd(hist + c, 1ull);
+    // warp-aggregated histogram: most walkers share a length
+    const unsigned act = __activemask();
+    const unsigned peers = __match_any_sync(act, (unsigned long long)c);
+    if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(hist + c, (unsigned long long)__popc(peers));
   }
 }
 

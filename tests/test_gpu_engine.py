@@ -191,3 +191,50 @@ def test_reference_app_objects_accepted():
     out = tp_run(app, DeviceGraph.from_arrays(g.row_offsets, g.col_indices, g.weights), samples,
                  EngineConfig(seed=meta["seed"]))
     assert sha16(texts(out)[0]) == meta["hash_final"]
+
+
+COLLECTIVE = ("layer", "fastgcn", "ladies", "mvs", "clustergcn")
+
+
+@pytest.mark.parametrize("meta", _cases(COLLECTIVE), ids=lambda m: f"{m['idx']}-{m['app']}-{m['graph']}")
+def test_collective_runs_match_reference(meta):
+    out = _device_run(meta, "tp")
+    tf, ts = texts(out)
+    assert out.n_steps == meta["n_steps"]
+    assert sha16(tf) == meta["hash_final"]
+    assert sha16(ts) == meta["hash_per_step"]
+    rs = golden("runs.npz")
+    assert recorded_equal(out, rs, f"r{meta['idx']}")
+    assert out.total_recorded() == meta["recorded"]
+    groups = np.array([[t.groups_small, t.groups_medium, t.groups_large] for t in out.stats.timings])
+    assert np.array_equal(groups.reshape(-1, 3), rs[f"r{meta['idx']}/groups"])
+    assert out.stats.adjacency_fetches == meta["adjacency_fetches"]
+
+
+@pytest.mark.parametrize("app,params", [("fastgcn", {}), ("ladies", {"distribution": "degree_sq"}),
+                                        ("mvs", {}), ("layer", {"max_size": 500, "step_size": 100}),
+                                        ("clustergcn", {"clusters_per_sample": 3, "num_clusters": 10})])
+def test_collective_on_rmat_vs_oracle(app, params):
+    """Orkut-shaped (symmetric RMAT, unit weights) collective sampling at scale 12
+    vs the oracle: slots, recorded edges, final rows."""
+    from paper_2009_06693_b200 import make_app
+    from paper_2009_06693_b200.engine import run_device
+    from paper_2009_06693_b200.graph import DeviceGraph
+    dg = DeviceGraph.rmat(12, 16, seed=8, undirected=True, weighted=False)
+    hg = dg.to_host()
+    og = O.OGraph(hg.n_vertices, hg.row_offsets, hg.col_indices, hg.weights,
+                  hg.per_vertex_weight_prefix, hg.per_vertex_max_weight, np.arange(hg.n_vertices))
+    n = 6 if app == "clustergcn" else 96
+    meta = {"app": app, "params": params, "n_samples": n, "seed": 12}
+    ref = oracle_run(meta, og)
+    dr = run_device(make_app(app, **params), dg, n_samples=n, seed=12)
+    out = dr.to_output()
+    assert out.n_steps == ref.n_steps
+    assert np.array_equal(out.step_counts, ref.step_counts)
+    assert np.array_equal(out.step_vals, ref.step_vals)
+    assert np.array_equal(np.asarray(out.rec_counts), np.asarray(ref.rec_counts))
+    assert np.array_equal(out.rec_t, ref.rec_t) and np.array_equal(out.rec_v, ref.rec_v)
+    off, ids = out.final_csr()
+    roff, rids = ref.final_csr()
+    assert np.array_equal(off, roff) and np.array_equal(ids, rids)
+    dr.close()
