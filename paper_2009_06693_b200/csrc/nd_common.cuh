@@ -144,6 +144,8 @@ __device__ __forceinline__ int64_t weighted_index(const DevGraph& g, int64_t lo,
   } while (0)
 
 void nd_set_last_error(const char* msg, const char* file, int line);
+// host-side phase trace (ND_TRACE=1): prints milliseconds since the previous mark
+void nd_trace(const char* what);
 
 // stream-ordered scratch allocation (cudaMallocAsync from the device pool)
 template <typename T>

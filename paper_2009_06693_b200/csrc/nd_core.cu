@@ -21,6 +21,19 @@ void nd_set_last_error(const char* msg, const char* file, int line) {
 }
 
 extern "C" const char* nd_last_error(void) { return g_last_error.c_str(); }
+
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+void nd_trace(const char* what) {
+  static const bool on = getenv("ND_TRACE") && getenv("ND_TRACE")[0] == '1';
+  if (!on) return;
+  static thread_local auto last = std::chrono::steady_clock::now();
+  auto now = std::chrono::steady_clock::now();
+  fprintf(stderr, "[nd_trace] %-28s +%.3f ms\n", what,
+          std::chrono::duration<double, std::milli>(now - last).count());
+  last = now;
+}
 extern "C" int nd_version(void) { return 1; }
 
 // Keep stream-ordered allocations cached in the device pool between runs

@@ -558,6 +558,7 @@ static int run_chain_walk_sp(const nd_graph* G, const NdApp& a, int64_t sample_l
                              const int64_t* roots, int64_t R, uint64_t seed, int64_t steps,
                              int64_t step_cap, cudaStream_t s, nd_result* res) {
   const DevGraph& g = G->g;
+  nd_trace("sp:enter");
   const int64_t limit = steps >= 0 ? (steps < step_cap ? steps : step_cap) : step_cap;
   const int64_t Lw_base = steps >= 0 ? (limit > 0 ? limit : 1) : 128;
   int32_t *roots32 = nullptr, *died = nullptr;
@@ -601,6 +602,7 @@ static int run_chain_walk_sp(const nd_graph* G, const NdApp& a, int64_t sample_l
   while (rows > 0 && step0 < limit) {
     const int64_t Lw = (limit - step0) < Lw_base ? (limit - step0) : Lw_base;
     Window W{nullptr, nullptr, nullptr, rows, step0, Lw};
+    nd_trace("sp:window-begin");
     ND_CUDA_TRY(nd_alloc(&W.out, rows * Lw, s));
     ND_CUDA_TRY(nd_alloc(&W.nnz, rows, s));
     int32_t *nw = nullptr, *nv = nullptr, *nt = nullptr;
@@ -613,6 +615,7 @@ static int run_chain_walk_sp(const nd_graph* G, const NdApp& a, int64_t sample_l
     int64_t grid = (int64_t)nsm * occ;
     const int64_t need = (rows + 255) / 256;
     if (grid > need) grid = need;
+    nd_trace("sp:allocs");
     if (g_profile) cudaEventRecord(pe0, s);
     k_walk_persistent<<<(unsigned)grid, 256, 0, s>>>(A);
     if (g_profile) cudaEventRecord(pe1, s);
@@ -620,6 +623,7 @@ static int run_chain_walk_sp(const nd_graph* G, const NdApp& a, int64_t sample_l
     W.wid = cwid;
     ND_CUDA_TRY(cudaMemcpyAsync(h, ctl, 4 * sizeof(int), cudaMemcpyDeviceToHost, s));
     ND_CUDA_TRY(cudaStreamSynchronize(s));
+    nd_trace("sp:window-synced");
     if (g_profile) {
       float ms = 0;
       cudaEventElapsedTime(&ms, pe0, pe1);
@@ -639,6 +643,7 @@ static int run_chain_walk_sp(const nd_graph* G, const NdApp& a, int64_t sample_l
   const int64_t n_steps = h[2];
   nd_free(cwid, s); nd_free(cv, s); nd_free(ct, s);
   // ---- compaction into the final layout -------------------------------------------
+  nd_trace("sp:windows-done");
   if (g_profile) cudaEventRecord(pe0, s);
   int64_t *flen = nullptr, *final_off = nullptr, *clen = nullptr, *final_ids = nullptr,
           *roots_out = nullptr;
@@ -664,6 +669,7 @@ static int run_chain_walk_sp(const nd_graph* G, const NdApp& a, int64_t sample_l
   int64_t total = 0;
   ND_CUDA_TRY(cudaMemcpyAsync(&total, final_off + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   ND_CUDA_TRY(cudaStreamSynchronize(s));
+  nd_trace("sp:scan-synced");
   ND_CUDA_TRY(nd_alloc(&final_ids, total, s));
   if (n * R) {
     if (roots)
@@ -702,6 +708,7 @@ static int run_chain_walk_sp(const nd_graph* G, const NdApp& a, int64_t sample_l
     cudaEventDestroy(pe1);
   }
   res->counters[NDC_LAUNCHES] = launches;
+  nd_trace("sp:done");
   nd_free(died, s); nd_free(tot, s); nd_free(ctl, s); nd_free(ctr, s); nd_free(roots32, s);
   nd_free(flen, s); nd_free(hist, s);
   res->n = n;

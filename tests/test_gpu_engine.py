@@ -232,8 +232,11 @@ def test_collective_on_rmat_vs_oracle(app, params):
     assert out.n_steps == ref.n_steps
     assert np.array_equal(out.step_counts, ref.step_counts)
     assert np.array_equal(out.step_vals, ref.step_vals)
-    assert np.array_equal(np.asarray(out.rec_counts), np.asarray(ref.rec_counts))
-    assert np.array_equal(out.rec_t, ref.rec_t) and np.array_equal(out.rec_v, ref.rec_v)
+    if app != "layer":  # layer records no edges (apps.py:247-283)
+        assert np.array_equal(np.asarray(out.rec_counts), np.asarray(ref.rec_counts))
+        assert np.array_equal(out.rec_t, ref.rec_t) and np.array_equal(out.rec_v, ref.rec_v)
+    else:
+        assert out.rec_t is None and len(ref.rec_t) == 0
     off, ids = out.final_csr()
     roff, rids = ref.final_csr()
     assert np.array_equal(off, roff) and np.array_equal(ids, rids)
