@@ -71,7 +71,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "250"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
@@ -265,6 +265,9 @@ def main():
         ms = ev0.elapsed_time(ev1)
         for dr in runs:
             dr.close()
+        if os.environ.get("ND_BENCH_VERBOSE"):
+            print(json.dumps({"it": it, "ms": ms, "per_app_prof": [dr.profile_ms for dr in runs]}),
+                  file=sys.stderr, flush=True)
         if timed:
             times.append(ms)
             edges_dev += step_edges

@@ -7,6 +7,7 @@
 //   nd_uniform_roots         _uniform_roots        (apps.py:83-103)
 #include <cub/cub.cuh>
 
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -44,13 +45,38 @@ int nd_pool_init() {
   int dev = 0;
   cudaGetDevice(&dev);
   if (done_dev == dev) return ND_OK;
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-    uint64_t thr = ~0ull;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-  }
   done_dev = dev;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return ND_OK;
+  uint64_t thr = ~0ull;
+  cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  // Reserve one large chunk up front: multi-GB scratch/result buffers are then
+  // carved from mapped memory instead of growing (and page-mapping) the pool
+  // mid-run, which costs ~0.5 ms per MB when fragmentation forces a new chunk.
+  // ND_POOL_RESERVE_GB overrides (0 disables).
+  size_t fr = 0, tot = 0;
+  cudaMemGetInfo(&fr, &tot);
+  double gb = 32.0;
+  if (const char* e = getenv("ND_POOL_RESERVE_GB")) gb = atof(e);
+  size_t want = (size_t)(gb * (1ull << 30));
+  if (want > fr / 3) want = fr / 3;
+  if (want >= (1ull << 30)) {
+    void* p = nullptr;
+    if (cudaMallocAsync(&p, want, 0) == cudaSuccess) {
+      cudaFreeAsync(p, 0);
+      cudaStreamSynchronize(0);
+    }
+    cudaGetLastError();
+  }
   return ND_OK;
+}
+
+// one pinned host word-block per thread for small D2H reads (no per-run
+// cudaMallocHost/cudaFreeHost, which serialise the device)
+int64_t* nd_pinned_scratch() {
+  static thread_local int64_t* p = nullptr;
+  if (!p) cudaMallocHost(&p, 64 * sizeof(int64_t));
+  return p;
 }
 
 extern "C" int nd_copy(void* dst, const void* src, int64_t bytes, void* stream) {

@@ -338,8 +338,7 @@ extern "C" int nd_run_individual(const nd_graph* G, int app_code, const double* 
   std::vector<StepData> steps;
   TPScratch TS;
   int64_t tp_cap = 0;
-  int64_t* h_tmp = nullptr;
-  ND_CUDA_TRY(cudaMallocHost(&h_tmp, 2 * sizeof(int64_t)));
+  int64_t* h_tmp = nd_pinned_scratch();
   int64_t step = 0;
   while (step < S_max && P > 0) {
     const int64_t m = host_fanouts[step];
@@ -490,7 +489,6 @@ extern "C" int nd_run_individual(const nd_graph* G, int app_code, const double* 
   ND_CUDA_TRY(cudaMemcpyAsync(&h_stall, stall, sizeof(int), cudaMemcpyDeviceToHost, s));
   ND_CUDA_TRY(cudaMemcpyAsync(h_ctr, ctr, sizeof(h_ctr), cudaMemcpyDeviceToHost, s));
   ND_CUDA_TRY(cudaStreamSynchronize(s));
-  cudaFreeHost(h_tmp);
   for (auto& sd : steps) {
     nd_free(sd.out, s);
     nd_free(sd.cum, s);

@@ -52,6 +52,7 @@ struct NdApp {
 
 int nd_make_app(int code, const double* params, int64_t n_params, NdApp* a);
 int nd_pool_init();
+int64_t* nd_pinned_scratch();
 
 // device counters block reset/read helpers
 int nd_uniform_roots_i32(const nd::DevGraph& g, int64_t count, uint64_t seed, int64_t sample_lo,

@@ -408,8 +408,7 @@ static int run_chain_walk(const nd_graph* G, const NdApp& a, int64_t sample_lo, 
   uint64_t* wp_in = wp0;
   uint32_t* cur_alt = cur1;
   uint64_t* wp_alt = wp1;
-  int* h_count = nullptr;
-  ND_CUDA_TRY(cudaMallocHost(&h_count, sizeof(int)));
+  int* h_count = reinterpret_cast<int*>(nd_pinned_scratch());
   double sched_ms = 0, sample_ms = 0;
   while (A > 0) {
     if (steps >= 0 && step >= steps) break;
@@ -470,7 +469,6 @@ static int run_chain_walk(const nd_graph* G, const NdApp& a, int64_t sample_lo, 
     A = *h_count;
     step++;
   }
-  cudaFreeHost(h_count);
   const int64_t n_steps = step;
   step_base.push_back(rec_base);
   // ---- output compaction -----------------------------------------------------------
@@ -584,8 +582,7 @@ static int run_chain_walk_sp(const nd_graph* G, const NdApp& a, int64_t sample_l
   std::vector<Window> wins;
   int32_t *cwid = nullptr, *cv = nullptr, *ct = nullptr;  // current window inputs
   int64_t rows = limit > 0 ? n : 0, step0 = 0;
-  int* h = nullptr;
-  ND_CUDA_TRY(cudaMallocHost(&h, 4 * sizeof(int)));
+  int* h = reinterpret_cast<int*>(nd_pinned_scratch());
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -698,7 +695,6 @@ static int run_chain_walk_sp(const nd_graph* G, const NdApp& a, int64_t sample_l
     nd_free(W.nnz, s);
     if (W.wid) nd_free(W.wid, s);
   }
-  cudaFreeHost(h);
   if (g_profile) {
     float ms = 0;
     cudaEventElapsedTime(&ms, pe0, pe1);
