@@ -194,6 +194,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--paradigm", default="sp", choices=["sp", "tp"])
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-tp", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -226,15 +227,9 @@ def main():
         """Final NCCL gather of every rank's compacted rows to rank 0."""
         if ws == 1:
             return 0
-        cnt = torch.tensor([ids.numel()], dtype=torch.int64, device="cuda")
-        cnts = [torch.zeros_like(cnt) for _ in range(ws)]
-        dist.all_gather(cnts, cnt)
-        mx = int(max(c.item() for c in cnts))
-        buf = torch.full((mx,), -1, dtype=torch.int64, device="cuda")
-        buf[:ids.numel()] = ids
-        out = [torch.empty_like(buf) for _ in range(ws)] if rank == 0 else None
-        dist.gather(buf, out, dst=0)
-        return mx * 8 * ws
+        from paper_2009_06693_b200.multigpu import gather_rows as g
+        g(off, ids)
+        return 0
 
     # ---- device throughput: inputs resident, CUDA events, max over ranks --------
     L.nd_set_profiling(1)
@@ -286,6 +281,24 @@ def main():
     else:
         edges_all = edges_dev
     value = edges_all / (tot_ms / 1e3)
+
+    # ---- the transit-parallel paradigm on the same job (reported alongside) ----------
+    tp_info = None
+    if args.paradigm == "sp" and not args.no_tp:
+        tp_ms = []
+        for it in range(3):
+            barrier()
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ev0.record(stream)
+            for app in apps:
+                run_device(app, dg, n_samples=n, sample_lo=lo, seed=SEED, paradigm="tp").close()
+            ev1.record(stream)
+            torch.cuda.synchronize()
+            if it:
+                tp_ms.append(ev0.elapsed_time(ev1))
+        tp_info = {"ms_per_step": sum(tp_ms) / len(tp_ms),
+                   "value": (edges_all / len(times)) / (sum(tp_ms) / len(tp_ms) / 1e3),
+                   "note": "TP = per-step radix sort + work classes + sub-warp/CTA/grid kernels"}
 
     # ---- e2e through the public API with host buffers ------------------------------
     L.nd_set_profiling(0)
@@ -384,7 +397,7 @@ def main():
                          "bytes_model": "SURVEY 8(d) sector model, counted on device",
                          "algorithmic_bytes_per_step": slot_bytes / len(times),
                          "kernel_ms_per_step": sum(sample_ms) / len(sample_ms)},
-            "cpu_baseline": cpu, "parity_cpu_sample": parity,
+            "cpu_baseline": cpu, "parity_cpu_sample": parity, "paradigm_tp": tp_info,
             "clocks": clocks.summary(), "gpu_launches": launches,
             "edges_per_step": edges_all / len(times),
         }
