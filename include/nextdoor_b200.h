@@ -122,6 +122,10 @@ int nd_graph_rmat(int scale, int64_t n_edges, uint32_t ta, uint32_t tab, uint32_
                   uint64_t seed, int undirected, int weighted, void *stream,
                   nd_graph **out);
 int nd_graph_destroy(nd_graph *g);
+/* Build the exact search indexes (flags: 1 = node2vec membership hash sets,
+ * 2 = weighted-pick guide tables).  nd_run_walk builds what it needs on first
+ * use; answers are identical to the reference's binary searches. */
+int nd_graph_build_index(nd_graph *g, int flags, void *stream);
 /* sizes and device pointers (read-only views) */
 int nd_graph_info(const nd_graph *g, int64_t *n_vertices, int64_t *n_edges, int *unit_weights,
                   int64_t *bytes);

@@ -39,6 +39,7 @@ SIGNATURES = {
     "nd_graph_from_edges": [vp, vp, vp, i64, i64, vp, pp],
     "nd_graph_rmat": [i32, i64, u32, u32, u32, u64, i32, i32, vp, pp],
     "nd_graph_destroy": [vp],
+    "nd_graph_build_index": [vp, i32, vp],
     "nd_graph_info": [vp, pi64, pi64, C.POINTER(C.c_int), pi64],
     "nd_graph_arrays": [vp, pp, pp, pp, pp, pp],
     "nd_uniform_roots": [vp, i64, u64, i64, i64, vp, vp],

@@ -79,6 +79,17 @@ __device__ __forceinline__ uint64_t mod_u64(uint64_t u, uint64_t d) {
 // 2^31), f64 weights / inclusive per-row prefix / per-row max.  Unit-weight
 // graphs keep neither weights nor prefix: the upper-bound search over the
 // integer prefix 1..deg reduces exactly to floor(r*deg).
+// Optional exact indexes (built on first use, see nd_index.cu):
+//   hset  — per-row open-addressing hash set of the row's neighbours, table of
+//           next_pow2(2*deg) int32 slots at offset 4*row[v] (rows with
+//           deg > HASH_MIN_DEG); answers has_edge (node2vec) in ~1 probe.
+//   guide — per-row guide table of deg int32 entries at offset row[v]:
+//           guide[j] = upper_bound(prefix row, j*(total/deg)) (rows with
+//           deg > GUIDE_MIN_DEG); narrows the inverse-CDF search to ~3 entries.
+// Both return exactly what the reference's binary searches return.
+constexpr int64_t HASH_MIN_DEG = 32;
+constexpr int64_t GUIDE_MIN_DEG = 16;
+
 struct DevGraph {
   int64_t V = 0, E = 0;
   const int64_t* row = nullptr;
@@ -86,8 +97,19 @@ struct DevGraph {
   const double* w = nullptr;     // null when unit
   const double* pre = nullptr;   // null when unit
   const double* mx = nullptr;
+  const int32_t* hset = nullptr;  // optional, 4E slots
+  const int32_t* guide = nullptr; // optional, E entries
   int unit = 0;
 };
+
+__host__ __device__ __forceinline__ int64_t hset_size(int64_t deg) {
+  // next_pow2(2*deg) <= 4*deg
+  int64_t t = 1;
+  while (t < 2 * deg) t <<= 1;
+  return t;
+}
+
+__device__ __forceinline__ uint32_t hset_hash(uint32_t u) { return u * 0x9E3779B1u; }
 
 // first index in [lo, hi) with a[i] > x (upper bound; _ckernels.pyx:65-74)
 __device__ __forceinline__ int64_t upper_bound_f64(const double* __restrict__ a, int64_t lo,

@@ -197,7 +197,7 @@ extern "C" int nd_individual_batch(int app_code, const double* host_params, int6
   int* stall = nullptr;
   ND_CUDA_TRY(nd_alloc(&stall, 1, s));
   ND_CUDA_TRY(cudaMemsetAsync(stall, 0, sizeof(int), s));
-  GView<int64_t> g{row_offsets, col_indices, weights, weight_prefix, max_weight, 0};
+  GView<int64_t> g{row_offsets, col_indices, weights, weight_prefix, max_weight, 0, nullptr, nullptr};
   k_individual_batch_ref<<<nd_grid(n, 256), 256, 0, s>>>(g, a, transits, t_prev, sample_ids,
                                                           transit_idxs, slots, n,
                                                           key_base(seed, (uint64_t)step, 0, 0),
@@ -329,6 +329,8 @@ extern "C" int nd_graph_destroy(nd_graph* G) {
   cudaFree(G->w);
   cudaFree(G->pre);
   cudaFree(G->mx);
+  cudaFree(G->hset);
+  cudaFree(G->guide);
   delete G;
   return ND_OK;
 }

@@ -1,0 +1,92 @@
+// nd_index.cu — exact per-row indexes that shorten the sampler's dependent
+// search chains (DESIGN.md §3/§8):
+//   * guide tables for the inverse-CDF weighted pick (DeepWalk, PPR, node2vec
+//     step 0): guide[lo+j] = upper_bound(prefix[lo:hi], j*(total/deg));
+//   * hash sets for node2vec's has_edge(t, u) (graph.py:78-81,
+//     _ckernels.pyx:77-87): open addressing, linear probing, load <= 1/2.
+// Built once per graph on first use; answers are identical to the binary
+// searches they replace (tests/test_gpu_kernels.py::test_index_equivalence).
+#include <cstdlib>
+
+#include "nd_internal.h"
+
+using namespace nd;
+
+namespace {
+
+__global__ void k_build_guide(const int64_t* __restrict__ row, const double* __restrict__ pre,
+                              int64_t V, int32_t* __restrict__ guide) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t v = warp; v < V; v += nw) {
+    const int64_t lo = row[v], deg = row[v + 1] - lo;
+    if (deg <= GUIDE_MIN_DEG) continue;
+    const double total = pre[lo + deg - 1];
+    const double width = __ddiv_rn(total, (double)deg);
+    for (int64_t j = lane; j < deg; j += 32) {
+      const double y = __dmul_rn(width, (double)j);
+      int64_t a = 0, b = deg;
+      while (a < b) {
+        const int64_t mid = (a + b) >> 1;
+        if (pre[lo + mid] <= y) a = mid + 1; else b = mid;
+      }
+      guide[lo + j] = (int32_t)a;
+    }
+  }
+}
+
+__global__ void k_build_hset(const int64_t* __restrict__ row, const int32_t* __restrict__ col,
+                             int64_t V, int32_t* __restrict__ hset) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t v = warp; v < V; v += nw) {
+    const int64_t lo = row[v], deg = row[v + 1] - lo;
+    if (deg <= HASH_MIN_DEG) continue;
+    int32_t* tab = hset + 4 * lo;
+    const int64_t size = hset_size(deg);
+    const uint32_t mask = (uint32_t)size - 1;
+    const int sh = 32 - (63 - __clzll(size));
+    for (int64_t e = lane; e < deg; e += 32) {
+      const int32_t u = col[lo + e];
+      uint32_t p = hset_hash((uint32_t)u) >> sh;
+      while (true) {
+        const int32_t old = atomicCAS(tab + p, -1, u);
+        if (old == -1 || old == u) break;
+        p = (p + 1) & mask;
+      }
+    }
+  }
+}
+
+}  // namespace
+
+int nd_graph_ensure_index(nd_graph* G, int want_hset, int want_guide, cudaStream_t s) {
+  static const bool disabled = getenv("ND_NO_INDEX") && getenv("ND_NO_INDEX")[0] == '1';
+  if (disabled) return ND_OK;
+  const int64_t V = G->g.V, E = G->g.E;
+  if (want_guide && !G->guide && !G->g.unit && E > 0) {
+    ND_CUDA_TRY(cudaMalloc(&G->guide, E * sizeof(int32_t)));
+    G->bytes += E * 4;
+    k_build_guide<<<148 * 16, 256, 0, s>>>(G->row, G->pre, V, G->guide);
+    ND_CUDA_TRY(cudaGetLastError());
+    ND_CUDA_TRY(cudaStreamSynchronize(s));
+    G->g.guide = G->guide;
+  }
+  if (want_hset && !G->hset && E > 0) {
+    ND_CUDA_TRY(cudaMalloc(&G->hset, 4 * E * sizeof(int32_t)));
+    G->bytes += 16 * E;
+    ND_CUDA_TRY(cudaMemsetAsync(G->hset, 0xFF, 4 * E * sizeof(int32_t), s));
+    k_build_hset<<<148 * 16, 256, 0, s>>>(G->row, G->col, V, G->hset);
+    ND_CUDA_TRY(cudaGetLastError());
+    ND_CUDA_TRY(cudaStreamSynchronize(s));
+    G->g.hset = G->hset;
+  }
+  return ND_OK;
+}
+
+extern "C" int nd_graph_build_index(nd_graph* g, int flags, void* stream) {
+  if (!g) return ND_ERR_ARG;
+  return nd_graph_ensure_index(g, flags & 1, flags & 2, (cudaStream_t)stream);
+}

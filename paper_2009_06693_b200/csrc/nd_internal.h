@@ -15,6 +15,8 @@ struct nd_graph {
   double* w = nullptr;
   double* pre = nullptr;
   double* mx = nullptr;
+  int32_t* hset = nullptr;   // optional exact indexes (nd_index.cu)
+  int32_t* guide = nullptr;
   int64_t bytes = 0;
   int device = 0;
 };
@@ -53,6 +55,7 @@ struct NdApp {
 int nd_make_app(int code, const double* params, int64_t n_params, NdApp* a);
 int nd_pool_init();
 int64_t* nd_pinned_scratch();
+int nd_graph_ensure_index(nd_graph* G, int want_hset, int want_guide, cudaStream_t s);
 
 // device counters block reset/read helpers
 int nd_uniform_roots_i32(const nd::DevGraph& g, int64_t count, uint64_t seed, int64_t sample_lo,

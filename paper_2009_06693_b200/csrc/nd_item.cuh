@@ -26,10 +26,12 @@ struct GView {
   const double* pre;  // may be null when unit
   const double* mx;
   int unit;
+  const int32_t* hset;   // optional exact membership index (int32 CSR only)
+  const int32_t* guide;  // optional guide table
 };
 
 __host__ __device__ inline GView<int32_t> view(const DevGraph& g) {
-  return GView<int32_t>{g.row, g.col, g.w, g.pre, g.mx, g.unit};
+  return GView<int32_t>{g.row, g.col, g.w, g.pre, g.mx, g.unit, g.hset, g.guide};
 }
 
 // v's row in global memory, indexed relative to its start
@@ -38,6 +40,7 @@ struct GRow {
   const ColT* col;
   const double* pre;
   const double* w;
+  const int32_t* gd;  // guide table of this row (or null)
   __device__ __forceinline__ int64_t c(int64_t k) const { return (int64_t)__ldg(col + k); }
   __device__ __forceinline__ double p(int64_t k) const { return __ldg(pre + k); }
   __device__ __forceinline__ double wt(int64_t k) const { return __ldg(w + k); }
@@ -45,7 +48,8 @@ struct GRow {
 
 template <typename ColT>
 __device__ __forceinline__ GRow<ColT> grow(const GView<ColT>& g, int64_t lo) {
-  return GRow<ColT>{g.col + lo, g.unit ? nullptr : g.pre + lo, g.unit ? nullptr : g.w + lo};
+  return GRow<ColT>{g.col + lo, g.unit ? nullptr : g.pre + lo, g.unit ? nullptr : g.w + lo,
+                    g.guide ? g.guide + lo : nullptr};
 }
 
 // v's row staged in shared memory
@@ -53,12 +57,17 @@ struct SRow {
   const int32_t* col;
   const double* pre;
   const double* w;
+  const int32_t* gd = nullptr;
   __device__ __forceinline__ int64_t c(int64_t k) const { return (int64_t)col[k]; }
   __device__ __forceinline__ double p(int64_t k) const { return pre[k]; }
   __device__ __forceinline__ double wt(int64_t k) const { return w[k]; }
 };
 
-// upper-bound inverse-CDF pick (_ckernels.pyx:65-74, 90-100); returns k in [0, deg)
+// upper-bound inverse-CDF pick (_ckernels.pyx:65-74, 90-100); returns k in [0, deg).
+// With a guide table the search starts at guide[j-1] and ends at guide[j+2]
+// (j = floor(u*deg)): every entry before guide[j-1] is <= j-1 buckets' worth
+// <= x and prefix[guide[j+2]] > x, so the first entry > x is the same one
+// the full-row upper bound finds.
 template <typename RowT>
 __device__ __forceinline__ int64_t pick_rel(const RowT& r, int unit, int64_t deg, double u01) {
   if (unit) {
@@ -68,11 +77,31 @@ __device__ __forceinline__ int64_t pick_rel(const RowT& r, int unit, int64_t deg
   }
   const double x = __dmul_rn(u01, r.p(deg - 1));
   int64_t lo = 0, hi = deg;
+  if (r.gd != nullptr && deg > GUIDE_MIN_DEG) {
+    int64_t j = (int64_t)__dmul_rn(u01, (double)deg);
+    if (j > deg - 1) j = deg - 1;
+    if (j >= 1) lo = __ldg(r.gd + j - 1);
+    if (j + 2 < deg) hi = (int64_t)__ldg(r.gd + j + 2) + 1;
+  }
   while (lo < hi) {
     int64_t mid = (lo + hi) >> 1;
     if (r.p(mid) <= x) lo = mid + 1; else hi = mid;
   }
   return lo < deg - 1 ? lo : deg - 1;
+}
+
+// exact membership through the per-row hash set (open addressing, linear probe)
+__device__ __forceinline__ bool hset_contains(const int32_t* __restrict__ tab, int64_t size,
+                                              int32_t u) {
+  const uint32_t mask = (uint32_t)size - 1;
+  const int sh = 32 - (63 - __clzll(size));  // log2(size) top bits
+  uint32_t p = size > 1 ? (hset_hash((uint32_t)u) >> sh) : 0;
+  while (true) {
+    const int32_t x = __ldg(tab + p);
+    if (x == u) return true;
+    if (x < 0) return false;
+    p = (p + 1) & mask;
+  }
 }
 
 template <typename ColT>
@@ -144,6 +173,8 @@ __device__ __forceinline__ int64_t run_item(const GView<ColT>& g, const RowT& r,
         st.tries++;
         st.bytes += 2 * SECTOR + probe;
         if (nb == t) f = a.f_ret;
+        else if (g.hset != nullptr && t_hi - t_lo > HASH_MIN_DEG)
+          f = hset_contains(g.hset + 4 * t_lo, hset_size(t_hi - t_lo), (int32_t)nb) ? a.f_adj : a.f_far;
         else f = has_edge(g.col, t_lo, t_hi, nb) ? a.f_adj : a.f_far;
         const double u01 = to_unit(draw_u64(b + C_DRAW, ik));
         if (env <= 0.0 || __dmul_rn(u01, env) < __dmul_rn(w, f)) return nb;

@@ -854,6 +854,10 @@ extern "C" int nd_run_walk(const nd_graph* g, int app_code, const double* host_p
   if (n_samples >= (1ll << 31)) return ND_ERR_ARG;
   if (app_code == ND_KHOP) return ND_ERR_ARG;  // multi-slot: nd_run_individual
   cudaStream_t s = (cudaStream_t)stream;
+  // exact search indexes (built once per graph): guide tables for weighted
+  // picks, hash sets for node2vec membership
+  ND_TRY(nd_graph_ensure_index(const_cast<nd_graph*>(g), app_code == ND_NODE2VEC,
+                               app_code != ND_MULTIRW, s));
   nd_result* res = new nd_result();
   res->stream = s;
   int rc;

@@ -241,3 +241,38 @@ def test_collective_on_rmat_vs_oracle(app, params):
     roff, rids = ref.final_csr()
     assert np.array_equal(off, roff) and np.array_equal(ids, rids)
     dr.close()
+
+
+@pytest.mark.parametrize("app", ["deepwalk", "ppr", "node2vec"])
+def test_index_paths_on_adversarial_hub_graph(app):
+    """Guide-table picks and hash-set membership on rows far above the index
+    thresholds, with zero weights (flat prefix runs), weights spanning six
+    decades, parallel edges and a dense hub neighbourhood: device == oracle."""
+    from paper_2009_06693_b200 import make_app
+    from paper_2009_06693_b200.engine import run_device
+    from paper_2009_06693_b200.graph import DeviceGraph
+    rng = np.random.default_rng(21)
+    V, hub_deg = 3000, 5000
+    src = [np.zeros(hub_deg, dtype=np.int64)]
+    dst = [rng.integers(1, V, hub_deg)]
+    # every other vertex: a few edges back to the hub and to random vertices
+    for v in range(1, V):
+        k = int(rng.integers(1, 60))
+        src.append(np.full(k, v))
+        d = rng.integers(0, V, k)
+        d[0] = 0
+        dst.append(d)
+    src, dst = np.concatenate(src), np.concatenate(dst)
+    w = 10.0 ** rng.uniform(-3, 3, len(src))
+    w[rng.random(len(src)) < 0.1] = 0.0
+    og = O.from_edges(src, dst, w, V)
+    dg = DeviceGraph.from_arrays(og.row_offsets, og.col_indices, og.weights)
+    n = 4000
+    meta = {"app": app, "params": {}, "n_samples": n, "seed": 33}
+    ref = oracle_run(meta, og)
+    for par in ("sp", "tp"):
+        dr = run_device(make_app(app), dg, n_samples=n, seed=33, paradigm=par)
+        off, ids = dr.host(0), dr.host(1)
+        roff, rids = ref.final_csr()
+        assert np.array_equal(off, roff) and np.array_equal(ids, rids), par
+        dr.close()
