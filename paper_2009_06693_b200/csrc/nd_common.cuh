@@ -90,6 +90,25 @@ __device__ __forceinline__ uint64_t mod_u64(uint64_t u, uint64_t d) {
 constexpr int64_t HASH_MIN_DEG = 32;
 constexpr int64_t GUIDE_MIN_DEG = 16;
 
+// Packed records for the walker-major kernels: the fields one step reads
+// together share one 32-byte sector.
+struct __align__(32) VRec {   // per vertex
+  int64_t lo;                 // row start
+  int64_t deg;
+  double mx;                  // per-row max weight (node2vec envelope)
+  double total;               // prefix[hi-1] (weighted pick); deg for unit rows
+};
+struct __align__(16) EdgeCW {  // node2vec try: neighbour + its weight
+  int32_t col;
+  int32_t pad;
+  double w;
+};
+struct __align__(16) EdgePC {  // weighted pick: prefix + the neighbour it selects
+  double pre;
+  int32_t col;
+  int32_t pad;
+};
+
 struct DevGraph {
   int64_t V = 0, E = 0;
   const int64_t* row = nullptr;
@@ -99,6 +118,9 @@ struct DevGraph {
   const double* mx = nullptr;
   const int32_t* hset = nullptr;  // optional, 4E slots
   const int32_t* guide = nullptr; // optional, E entries
+  const VRec* vrec = nullptr;     // optional packed vertex records
+  const EdgeCW* ecw = nullptr;    // optional packed (col, w) records
+  const EdgePC* epc = nullptr;    // optional packed (prefix, col) records
   int unit = 0;
 };
 

@@ -331,6 +331,9 @@ extern "C" int nd_graph_destroy(nd_graph* G) {
   cudaFree(G->mx);
   cudaFree(G->hset);
   cudaFree(G->guide);
+  cudaFree(G->vrec);
+  cudaFree(G->ecw);
+  cudaFree(G->epc);
   delete G;
   return ND_OK;
 }

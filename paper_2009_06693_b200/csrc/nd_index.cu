@@ -60,7 +60,63 @@ __global__ void k_build_hset(const int64_t* __restrict__ row, const int32_t* __r
   }
 }
 
+__global__ void k_build_vrec(const int64_t* __restrict__ row, const double* __restrict__ mx,
+                             const double* __restrict__ pre, int64_t V, VRec* __restrict__ out) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    VRec r;
+    r.lo = row[v];
+    r.deg = row[v + 1] - r.lo;
+    r.mx = mx[v];
+    r.total = pre ? (r.deg > 0 ? pre[r.lo + r.deg - 1] : 0.0) : (double)r.deg;
+    out[v] = r;
+  }
+}
+
+__global__ void k_build_edges(const int32_t* __restrict__ col, const double* __restrict__ w,
+                              const double* __restrict__ pre, int64_t E, EdgeCW* __restrict__ cw,
+                              EdgePC* __restrict__ pc) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    EdgeCW a;
+    a.col = col[e];
+    a.pad = 0;
+    a.w = w[e];
+    cw[e] = a;
+    EdgePC b;
+    b.pre = pre[e];
+    b.col = col[e];
+    b.pad = 0;
+    pc[e] = b;
+  }
+}
+
 }  // namespace
+
+int nd_graph_ensure_records(nd_graph* G, cudaStream_t s) {
+  static const bool disabled = getenv("ND_NO_PACK") && getenv("ND_NO_PACK")[0] == '1';
+  if (disabled) return ND_OK;
+  const int64_t V = G->g.V, E = G->g.E;
+  if (!G->vrec && V > 0) {
+    ND_CUDA_TRY(cudaMalloc(&G->vrec, V * sizeof(VRec)));
+    G->bytes += V * sizeof(VRec);
+    k_build_vrec<<<nd_grid(V, 256), 256, 0, s>>>(G->row, G->mx, G->g.unit ? nullptr : G->pre, V,
+                                                  G->vrec);
+    ND_CUDA_TRY(cudaGetLastError());
+    G->g.vrec = G->vrec;
+  }
+  if (!G->ecw && !G->g.unit && E > 0) {
+    ND_CUDA_TRY(cudaMalloc(&G->ecw, E * sizeof(EdgeCW)));
+    ND_CUDA_TRY(cudaMalloc(&G->epc, E * sizeof(EdgePC)));
+    G->bytes += E * (sizeof(EdgeCW) + sizeof(EdgePC));
+    k_build_edges<<<nd_grid(E, 256), 256, 0, s>>>(G->col, G->w, G->pre, E, G->ecw, G->epc);
+    ND_CUDA_TRY(cudaGetLastError());
+    G->g.ecw = G->ecw;
+    G->g.epc = G->epc;
+  }
+  ND_CUDA_TRY(cudaStreamSynchronize(s));
+  return ND_OK;
+}
 
 int nd_graph_ensure_index(nd_graph* G, int want_hset, int want_guide, cudaStream_t s) {
   static const bool disabled = getenv("ND_NO_INDEX") && getenv("ND_NO_INDEX")[0] == '1';
@@ -88,5 +144,7 @@ int nd_graph_ensure_index(nd_graph* G, int want_hset, int want_guide, cudaStream
 
 extern "C" int nd_graph_build_index(nd_graph* g, int flags, void* stream) {
   if (!g) return ND_ERR_ARG;
-  return nd_graph_ensure_index(g, flags & 1, flags & 2, (cudaStream_t)stream);
+  ND_TRY(nd_graph_ensure_index(g, flags & 1, flags & 2, (cudaStream_t)stream));
+  if (flags & 4) ND_TRY(nd_graph_ensure_records(g, (cudaStream_t)stream));
+  return ND_OK;
 }

@@ -17,6 +17,9 @@ struct nd_graph {
   double* mx = nullptr;
   int32_t* hset = nullptr;   // optional exact indexes (nd_index.cu)
   int32_t* guide = nullptr;
+  nd::VRec* vrec = nullptr;  // packed records (nd_index.cu)
+  nd::EdgeCW* ecw = nullptr;
+  nd::EdgePC* epc = nullptr;
   int64_t bytes = 0;
   int device = 0;
 };
@@ -56,6 +59,7 @@ int nd_make_app(int code, const double* params, int64_t n_params, NdApp* a);
 int nd_pool_init();
 int64_t* nd_pinned_scratch();
 int nd_graph_ensure_index(nd_graph* G, int want_hset, int want_guide, cudaStream_t s);
+int nd_graph_ensure_records(nd_graph* G, cudaStream_t s);
 
 // device counters block reset/read helpers
 int nd_uniform_roots_i32(const nd::DevGraph& g, int64_t count, uint64_t seed, int64_t sample_lo,

@@ -44,6 +44,33 @@ struct GRow {
   __device__ __forceinline__ int64_t c(int64_t k) const { return (int64_t)__ldg(col + k); }
   __device__ __forceinline__ double p(int64_t k) const { return __ldg(pre + k); }
   __device__ __forceinline__ double wt(int64_t k) const { return __ldg(w + k); }
+  __device__ __forceinline__ void cw(int64_t k, int64_t& c_, double& w_, int unit) const {
+    c_ = (int64_t)__ldg(col + k);
+    w_ = unit ? 1.0 : __ldg(w + k);
+  }
+};
+
+// v's row through the packed edge records (one 16-byte load per try / probe)
+struct PRow {
+  const EdgeCW* ecw;
+  const EdgePC* epc;
+  const int32_t* col;  // plain column ids (unit graphs)
+  const int32_t* gd;
+  __device__ __forceinline__ int64_t c(int64_t k) const {
+    return epc ? (int64_t)__ldg(&epc[k].col) : (int64_t)__ldg(col + k);
+  }
+  __device__ __forceinline__ double p(int64_t k) const { return __ldg(&epc[k].pre); }
+  __device__ __forceinline__ double wt(int64_t k) const { return __ldg(&ecw[k].w); }
+  __device__ __forceinline__ void cw(int64_t k, int64_t& c_, double& w_, int unit) const {
+    if (unit || !ecw) {
+      c_ = (int64_t)__ldg(col + k);
+      w_ = 1.0;
+      return;
+    }
+    const double2 r = __ldg(reinterpret_cast<const double2*>(ecw + k));
+    c_ = (int64_t)(int32_t)(uint32_t)(__double_as_longlong(r.x) & 0xFFFFFFFFull);
+    w_ = r.y;
+  }
 };
 
 template <typename ColT>
@@ -61,6 +88,10 @@ struct SRow {
   __device__ __forceinline__ int64_t c(int64_t k) const { return (int64_t)col[k]; }
   __device__ __forceinline__ double p(int64_t k) const { return pre[k]; }
   __device__ __forceinline__ double wt(int64_t k) const { return w[k]; }
+  __device__ __forceinline__ void cw(int64_t k, int64_t& c_, double& w_, int unit) const {
+    c_ = (int64_t)col[k];
+    w_ = unit ? 1.0 : w[k];
+  }
 };
 
 // upper-bound inverse-CDF pick (_ckernels.pyx:65-74, 90-100); returns k in [0, deg).
@@ -69,13 +100,14 @@ struct SRow {
 // <= x and prefix[guide[j+2]] > x, so the first entry > x is the same one
 // the full-row upper bound finds.
 template <typename RowT>
-__device__ __forceinline__ int64_t pick_rel(const RowT& r, int unit, int64_t deg, double u01) {
+__device__ __forceinline__ int64_t pick_rel(const RowT& r, int unit, int64_t deg, double u01,
+                                            double total_known = -1.0) {
   if (unit) {
     double x = __dmul_rn(u01, (double)deg);
     int64_t k = (int64_t)x;
     return k < deg - 1 ? k : deg - 1;
   }
-  const double x = __dmul_rn(u01, r.p(deg - 1));
+  const double x = __dmul_rn(u01, total_known >= 0.0 ? total_known : r.p(deg - 1));
   int64_t lo = 0, hi = deg;
   if (r.gd != nullptr && deg > GUIDE_MIN_DEG) {
     int64_t j = (int64_t)__dmul_rn(u01, (double)deg);
@@ -136,18 +168,19 @@ template <typename ColT, typename RowT>
 __device__ __forceinline__ int64_t run_item(const GView<ColT>& g, const RowT& r, const NdApp& a,
                                             int64_t v, int64_t deg, int64_t t, uint64_t base0,
                                             uint64_t ik, ItemStats& st, int* stall,
-                                            int64_t t_lo_known = -1, int64_t t_hi_known = -1) {
+                                            int64_t t_lo_known = -1, int64_t t_hi_known = -1,
+                                            double mx_known = -1.0, double tot_known = -1.0) {
   if (deg <= 0) return -1;
   const int64_t wsec = g.unit ? 0 : SECTOR * search_sectors(deg);
   switch (a.code) {
     case ND_DEEPWALK: {
       st.bytes += SECTOR + wsec + SECTOR + 8;
-      return r.c(pick_rel(r, g.unit, deg, to_unit(draw_u64(base0, ik))));
+      return r.c(pick_rel(r, g.unit, deg, to_unit(draw_u64(base0, ik)), tot_known));
     }
     case ND_PPR: {
       if (to_unit(draw_u64(base0, ik)) < a.term) return -1;
       st.bytes += SECTOR + wsec + SECTOR + 8;
-      return r.c(pick_rel(r, g.unit, deg, to_unit(draw_u64(base0 + C_DRAW, ik))));
+      return r.c(pick_rel(r, g.unit, deg, to_unit(draw_u64(base0 + C_DRAW, ik)), tot_known));
     }
     case ND_KHOP:
     case ND_MULTIRW: {
@@ -157,18 +190,19 @@ __device__ __forceinline__ int64_t run_item(const GView<ColT>& g, const RowT& r,
     case ND_NODE2VEC: {
       if (t < 0) {
         st.bytes += SECTOR + wsec + SECTOR + 8;
-        return r.c(pick_rel(r, g.unit, deg, to_unit(draw_u64(base0, ik))));
+        return r.c(pick_rel(r, g.unit, deg, to_unit(draw_u64(base0, ik)), tot_known));
       }
       const int64_t t_lo = t_lo_known >= 0 ? t_lo_known : __ldg(g.row + t);
       const int64_t t_hi = t_lo_known >= 0 ? t_hi_known : __ldg(g.row + t + 1);
-      const double env = __dmul_rn(__ldg(g.mx + v), a.f_max);
+      const double env = __dmul_rn(mx_known >= 0.0 ? mx_known : __ldg(g.mx + v), a.f_max);
       const int64_t probe = SECTOR * search_sectors(t_hi - t_lo);
       st.bytes += 2 * SECTOR + 8;
       uint64_t b = base0;
       for (int64_t j = 0; j < N2V_MAX_TRIES; j++) {
         const int64_t k = (int64_t)mod_u64(draw_u64(b, ik), (uint64_t)deg);
-        const int64_t nb = r.c(k);
-        const double w = g.unit ? 1.0 : r.wt(k);
+        int64_t nb;
+        double w;
+        r.cw(k, nb, w, g.unit);
         double f;
         st.tries++;
         st.bytes += 2 * SECTOR + probe;

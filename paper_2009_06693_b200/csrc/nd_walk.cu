@@ -14,6 +14,7 @@
 // the first root equal to the transit.  Values go to a dense [steps, N] slab.
 #include <cub/cub.cuh>
 
+#include <cstdlib>
 #include <vector>
 
 #include "nd_tp.cuh"
@@ -232,12 +233,35 @@ struct PWArgs {
   int* max_len;
   int* stall;
   unsigned long long* ctr;
+  const VRec* vrec;   // packed vertex records (or null)
+  const EdgeCW* ecw;
+  const EdgePC* epc;
 };
 
-__global__ void __launch_bounds__(256) k_walk_persistent(PWArgs A) {
+// one 32-byte sector: row bounds, max weight and prefix total of v
+__device__ __forceinline__ void load_vertex(const PWArgs& A, int64_t v, int64_t& lo, int64_t& deg,
+                                            double& mx, double& tot) {
+  if (A.vrec != nullptr) {
+    const longlong2 a = __ldg(reinterpret_cast<const longlong2*>(A.vrec + v));
+    const double2 b = __ldg(reinterpret_cast<const double2*>(A.vrec + v) + 1);
+    lo = a.x;
+    deg = a.y;
+    mx = b.x;
+    tot = b.y;
+  } else {
+    lo = __ldg(A.gv.row + v);
+    deg = __ldg(A.gv.row + v + 1) - lo;
+    mx = -1.0;
+    tot = -1.0;
+  }
+}
+
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB) k_walk_persistent(PWArgs A) {
   ItemStats st;
   const int lane = threadIdx.x & 31;
   int64_t row = -1, w = 0, v = 0, t = -1, s = 0, lo = 0, deg = 0, tlo = -1, thi = -1;
+  double mx = -1.0, tot = -1.0;
   uint64_t ik = 0;
   int32_t* orow = nullptr;
   while (true) {
@@ -263,8 +287,7 @@ __global__ void __launch_bounds__(256) k_walk_persistent(PWArgs A) {
           s = A.step0;
           ik = key_item((uint64_t)(A.sample_lo + w), 0, 0);
           orow = A.out + row * A.Lw;
-          lo = __ldg(A.gv.row + v);
-          deg = __ldg(A.gv.row + v + 1) - lo;
+          load_vertex(A, v, lo, deg, mx, tot);
         }
       }
     }
@@ -273,8 +296,16 @@ __global__ void __launch_bounds__(256) k_walk_persistent(PWArgs A) {
     // one step of this lane's walker
     st.bytes += SECTOR + 8;
     int stl = 0;
-    const int64_t o = run_item(A.gv, grow(A.gv, lo), A.a, v, deg, t,
-                               key_base(A.seed, (uint64_t)s, 0, 0), ik, st, &stl, tlo, thi);
+    int64_t o;
+    if (A.vrec != nullptr) {
+      const PRow pr{A.ecw ? A.ecw + lo : nullptr, A.epc ? A.epc + lo : nullptr, A.gv.col + lo,
+                    A.gv.guide ? A.gv.guide + lo : nullptr};
+      o = run_item(A.gv, pr, A.a, v, deg, t, key_base(A.seed, (uint64_t)s, 0, 0), ik, st, &stl,
+                   tlo, thi, mx, tot);
+    } else {
+      o = run_item(A.gv, grow(A.gv, lo), A.a, v, deg, t, key_base(A.seed, (uint64_t)s, 0, 0), ik,
+                   st, &stl, tlo, thi);
+    }
     if (stl) atomicExch(A.stall, 1);
     orow[s - A.step0] = (int32_t)o;
     s++;
@@ -296,8 +327,7 @@ __global__ void __launch_bounds__(256) k_walk_persistent(PWArgs A) {
       thi = lo + deg;
       t = v;
       v = o;
-      lo = __ldg(A.gv.row + v);
-      deg = __ldg(A.gv.row + v + 1) - lo;
+      load_vertex(A, v, lo, deg, mx, tot);
     }
   }
   flush_stats(st, A.ctr);
@@ -586,8 +616,14 @@ static int run_chain_walk_sp(const nd_graph* G, const NdApp& a, int64_t sample_l
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  // register/occupancy variant of the persistent kernel (ND_WALK_MINB = 4|5|6|8
+  // resident CTAs per SM requested from ptxas; default measured best)
+  static const int minb = getenv("ND_WALK_MINB") ? atoi(getenv("ND_WALK_MINB")) : 4;
+  auto kern = minb >= 8 ? k_walk_persistent<8>
+              : minb == 6 ? k_walk_persistent<6>
+              : minb == 5 ? k_walk_persistent<5> : k_walk_persistent<4>;
   int occ = 4;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_walk_persistent, 256, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, 0);
   if (occ < 1) occ = 1;
   int64_t launches = roots ? 0 : 1;
   double sample_ms = 0.0;
@@ -596,8 +632,13 @@ static int run_chain_walk_sp(const nd_graph* G, const NdApp& a, int64_t sample_l
     cudaEventCreate(&pe0);
     cudaEventCreate(&pe1);
   }
+  // window budget: later windows (few long PPR walks) get proportionally
+  // more steps so the geometric tail runs in one or two launches
+  const int64_t budget = (rows * Lw_base > (1ll << 24)) ? rows * Lw_base : (1ll << 24);
   while (rows > 0 && step0 < limit) {
-    const int64_t Lw = (limit - step0) < Lw_base ? (limit - step0) : Lw_base;
+    int64_t Lw = step0 == 0 ? Lw_base : budget / rows;
+    if (Lw < Lw_base) Lw = Lw_base;
+    if (Lw > limit - step0) Lw = limit - step0;
     Window W{nullptr, nullptr, nullptr, rows, step0, Lw};
     nd_trace("sp:window-begin");
     ND_CUDA_TRY(nd_alloc(&W.out, rows * Lw, s));
@@ -608,13 +649,14 @@ static int run_chain_walk_sp(const nd_graph* G, const NdApp& a, int64_t sample_l
     ND_CUDA_TRY(nd_alloc(&nt, rows, s));
     ND_CUDA_TRY(cudaMemsetAsync(ctl, 0, 2 * sizeof(int), s));
     PWArgs A{view(g), a, seed, sample_lo, rows, cwid, cv, ct, roots, roots32, R, step0,
-             step0 + Lw, Lw, W.out, W.nnz, died, nw, nv, nt, ctl + 1, ctl, ctl + 2, ctl + 3, ctr};
+             step0 + Lw, Lw, W.out, W.nnz, died, nw, nv, nt, ctl + 1, ctl, ctl + 2, ctl + 3, ctr,
+             g.vrec, g.ecw, g.epc};
     int64_t grid = (int64_t)nsm * occ;
     const int64_t need = (rows + 255) / 256;
     if (grid > need) grid = need;
     nd_trace("sp:allocs");
     if (g_profile) cudaEventRecord(pe0, s);
-    k_walk_persistent<<<(unsigned)grid, 256, 0, s>>>(A);
+    kern<<<(unsigned)grid, 256, 0, s>>>(A);
     if (g_profile) cudaEventRecord(pe1, s);
     ND_CUDA_TRY(cudaGetLastError());
     W.wid = cwid;
@@ -858,6 +900,8 @@ extern "C" int nd_run_walk(const nd_graph* g, int app_code, const double* host_p
   // picks, hash sets for node2vec membership
   ND_TRY(nd_graph_ensure_index(const_cast<nd_graph*>(g), app_code == ND_NODE2VEC,
                                app_code != ND_MULTIRW, s));
+  if (app_code != ND_MULTIRW && paradigm == ND_SP)
+    ND_TRY(nd_graph_ensure_records(const_cast<nd_graph*>(g), s));
   nd_result* res = new nd_result();
   res->stream = s;
   int rc;
