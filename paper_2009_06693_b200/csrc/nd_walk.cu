@@ -256,24 +256,56 @@ __device__ __forceinline__ void load_vertex(const PWArgs& A, int64_t v, int64_t&
   }
 }
 
+// node2vec rejection try j for a walker at v with previous vertex t
+// (_ckernels.pyx:243-262); returns the neighbour on acceptance, -2 on reject.
+template <class RowT>
+__device__ __forceinline__ int64_t n2v_try(const PWArgs& A, const RowT& r, int64_t deg, int64_t t,
+                                           int64_t tlo, int64_t thi, double env, uint64_t b,
+                                           uint64_t ik, ItemStats& st) {
+  const int64_t k = (int64_t)mod_u64(draw_u64(b, ik), (uint64_t)deg);
+  int64_t nb;
+  double w;
+  r.cw(k, nb, w, A.gv.unit);
+  double f;
+  st.tries++;
+  st.bytes += 2 * SECTOR + SECTOR * search_sectors(thi - tlo);
+  if (nb == t) f = A.a.f_ret;
+  else if (A.gv.hset != nullptr && thi - tlo > HASH_MIN_DEG)
+    f = hset_contains(A.gv.hset + 4 * tlo, hset_size(thi - tlo), (int32_t)nb) ? A.a.f_adj : A.a.f_far;
+  else f = has_edge(A.gv.col, tlo, thi, nb) ? A.a.f_adj : A.a.f_far;
+  const double u01 = to_unit(draw_u64(b + C_DRAW, ik));
+  return (env <= 0.0 || __dmul_rn(u01, env) < __dmul_rn(w, f)) ? nb : -2;
+}
+
+constexpr int PW_CHUNK = 64;  // walkers a warp claims per queue atomic
+
 template <int MINB>
 __global__ void __launch_bounds__(256, MINB) k_walk_persistent(PWArgs A) {
   ItemStats st;
   const int lane = threadIdx.x & 31;
+  const unsigned lt_mask = (1u << lane) - 1;
   int64_t row = -1, w = 0, v = 0, t = -1, s = 0, lo = 0, deg = 0, tlo = -1, thi = -1;
   double mx = -1.0, tot = -1.0;
+  int64_t j = 0;          // node2vec try index of the current step
   uint64_t ik = 0;
   int32_t* orow = nullptr;
+  int64_t wbeg = 0, wend = 0;  // this warp's claimed walker range (warp-uniform)
+  const bool n2v = A.a.code == ND_NODE2VEC;
   while (true) {
+    // ---- hand out walkers from the warp's chunk (one atomic per PW_CHUNK)
     const bool need = row < 0;
     const unsigned m = __ballot_sync(0xffffffffu, need);
     if (m) {
-      int base = 0;
-      const int leader = __ffs(m) - 1;
-      if (lane == leader) base = atomicAdd(A.queue, __popc(m));
-      base = __shfl_sync(0xffffffffu, base, leader);
+      const int c = __popc(m);
+      const int rank = __popc(m & lt_mask);
+      int64_t rem = wend - wbeg, nbeg = 0;
+      if (rem < c) {
+        int base = 0;
+        if (lane == 0) base = atomicAdd(A.queue, PW_CHUNK);
+        nbeg = __shfl_sync(0xffffffffu, base, 0);
+      }
       if (need) {
-        row = base + __popc(m & ((1u << lane) - 1));
+        row = rank < rem ? wbeg + rank : nbeg + (rank - rem);
         if (row < A.n) {
           w = A.wid ? A.wid[row] : row;
           if (A.v0) {
@@ -285,30 +317,56 @@ __global__ void __launch_bounds__(256, MINB) k_walk_persistent(PWArgs A) {
           }
           tlo = thi = -1;
           s = A.step0;
+          j = 0;
           ik = key_item((uint64_t)(A.sample_lo + w), 0, 0);
           orow = A.out + row * A.Lw;
           load_vertex(A, v, lo, deg, mx, tot);
+          st.bytes += SECTOR + 8;
         }
+      }
+      if (rem < c) {
+        wbeg = nbeg + (c - rem);
+        wend = nbeg + PW_CHUNK;
+      } else {
+        wbeg += c;
       }
     }
     if (__all_sync(0xffffffffu, row >= A.n)) break;
     if (row >= A.n) continue;
-    // one step of this lane's walker
-    st.bytes += SECTOR + 8;
+    // ---- one unit of work: a node2vec try (step >= 1) or a whole step
     int stl = 0;
     int64_t o;
-    if (A.vrec != nullptr) {
+    const uint64_t base0 = key_base(A.seed, (uint64_t)s, 0, 0);
+    if (n2v && t >= 0 && deg > 0) {
+      if (j == 0) st.bytes += 2 * SECTOR;  // t offsets + max_w (§8 d pair term)
+      const double env = __dmul_rn(mx >= 0.0 ? mx : __ldg(A.gv.mx + v), A.a.f_max);
+      if (A.vrec != nullptr) {
+        const PRow pr{A.ecw ? A.ecw + lo : nullptr, A.epc ? A.epc + lo : nullptr, A.gv.col + lo,
+                      A.gv.guide ? A.gv.guide + lo : nullptr};
+        o = n2v_try(A, pr, deg, t, tlo, thi, env, base0 + 2 * C_DRAW * (uint64_t)j, ik, st);
+      } else {
+        o = n2v_try(A, grow(A.gv, lo), deg, t, tlo, thi, env, base0 + 2 * C_DRAW * (uint64_t)j, ik,
+                    st);
+      }
+      if (o == -2) {
+        if (++j >= N2V_MAX_TRIES) {
+          atomicExch(A.stall, 1);
+          o = -1;
+        } else {
+          continue;  // rejected: the lane tries again next iteration
+        }
+      }
+    } else if (A.vrec != nullptr) {
       const PRow pr{A.ecw ? A.ecw + lo : nullptr, A.epc ? A.epc + lo : nullptr, A.gv.col + lo,
                     A.gv.guide ? A.gv.guide + lo : nullptr};
-      o = run_item(A.gv, pr, A.a, v, deg, t, key_base(A.seed, (uint64_t)s, 0, 0), ik, st, &stl,
-                   tlo, thi, mx, tot);
+      o = run_item(A.gv, pr, A.a, v, deg, t, base0, ik, st, &stl, tlo, thi, mx, tot);
     } else {
-      o = run_item(A.gv, grow(A.gv, lo), A.a, v, deg, t, key_base(A.seed, (uint64_t)s, 0, 0), ik,
-                   st, &stl, tlo, thi);
+      o = run_item(A.gv, grow(A.gv, lo), A.a, v, deg, t, base0, ik, st, &stl, tlo, thi);
     }
     if (stl) atomicExch(A.stall, 1);
     orow[s - A.step0] = (int32_t)o;
     s++;
+    j = 0;
     if (o < 0) {
       A.nnz[row] = (int32_t)(s - 1 - A.step0);
       A.died[w] = 1;
@@ -328,6 +386,7 @@ __global__ void __launch_bounds__(256, MINB) k_walk_persistent(PWArgs A) {
       t = v;
       v = o;
       load_vertex(A, v, lo, deg, mx, tot);
+      st.bytes += SECTOR + 8;
     }
   }
   flush_stats(st, A.ctr);
