@@ -402,31 +402,42 @@ __global__ void k_pw_accum(const int32_t* __restrict__ wid, const int32_t* __res
 
 __global__ void k_pw_lengths(const int64_t* __restrict__ tot, const int32_t* __restrict__ died,
                              int64_t n, int64_t R, int64_t* __restrict__ flen,
-                             int64_t* __restrict__ clen, unsigned long long* __restrict__ hist) {
+                             int64_t* __restrict__ clen, unsigned long long* __restrict__ hist,
+                             int64_t hist_len) {
+  // chain-length histogram (per-step alive counts for RunStats): shared-memory
+  // bins for short lengths, global atomics beyond
+  constexpr int SH = 4096;
+  __shared__ unsigned int sh[SH];
+  for (int k = threadIdx.x; k < SH; k += blockDim.x) sh[k] = 0;
+  __syncthreads();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n;
        i += (int64_t)gridDim.x * blockDim.x) {
     if (i == n) { flen[n] = 0; continue; }
     flen[i] = R + tot[i];
     const int64_t c = tot[i] + died[i];
     clen[i] = c;
-    // warp-aggregated histogram: most walkers share a length
-    const unsigned act = __activemask();
-    const unsigned peers = __match_any_sync(act, (unsigned long long)c);
-    if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(hist + c, (unsigned long long)__popc(peers));
+    if (c < SH) atomicAdd(sh + c, 1u);
+    else if (c < hist_len) atomicAdd(hist + c, 1ull);
   }
+  __syncthreads();
+  for (int k = threadIdx.x; k < SH && k < hist_len; k += blockDim.x)
+    if (sh[k]) atomicAdd(hist + k, (unsigned long long)sh[k]);
 }
 
-// copy one window's rows into the final layout: thread per (row, k)
+// copy one window's rows into the final layout: one warp per row, lanes
+// stream the row's non-NULL prefix (int32 reads, int64 writes, both coalesced)
 __global__ void k_pw_emit(const int32_t* __restrict__ wid, const int32_t* __restrict__ out,
                           const int32_t* __restrict__ nnz, int64_t n, int64_t Lw, int64_t step0,
                           const int64_t* __restrict__ off, int64_t R, int64_t* __restrict__ ids) {
-  const int64_t total = n * Lw;
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < total;
-       j += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = j / Lw, k = j - r * Lw;
-    if (k >= nnz[r]) continue;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = warp; r < n; r += nw) {
+    const int64_t k_end = nnz[r];
     const int64_t w = wid ? wid[r] : r;
-    ids[off[w] + R + step0 + k] = (int64_t)out[j];
+    int64_t* dst = ids + off[w] + R + step0;
+    const int32_t* src = out + r * Lw;
+    for (int64_t k = lane; k < k_end; k += 32) dst[k] = (int64_t)src[k];
   }
 }
 
@@ -754,7 +765,7 @@ static int run_chain_walk_sp(const nd_graph* G, const NdApp& a, int64_t sample_l
   ND_CUDA_TRY(nd_alloc(&stats, 4 * (n_steps + 1), s));
   ND_CUDA_TRY(cudaMemsetAsync(hist, 0, (limit + 2) * sizeof(unsigned long long), s));
   ND_CUDA_TRY(cudaMemsetAsync(stats, 0, 4 * (n_steps + 1) * sizeof(unsigned long long), s));
-  k_pw_lengths<<<nd_grid(n + 1, 256), 256, 0, s>>>(tot, died, n, R, flen, clen, hist);
+  k_pw_lengths<<<nd_grid(n + 1, 256, 148 * 4), 256, 0, s>>>(tot, died, n, R, flen, clen, hist, limit + 2);
   k_pw_stats<<<1, 1, 0, s>>>(hist, n_steps, n, stats);
   {
     size_t tb = 0;
@@ -780,8 +791,8 @@ static int run_chain_walk_sp(const nd_graph* G, const NdApp& a, int64_t sample_l
   int64_t items = 0;
   for (auto& W : wins) {
     if (W.n * W.Lw)
-      k_pw_emit<<<nd_grid(W.n * W.Lw, 256, 148 * 64), 256, 0, s>>>(W.wid, W.out, W.nnz, W.n, W.Lw,
-                                                                  W.step0, final_off, R, final_ids);
+      k_pw_emit<<<nd_grid(W.n * 32, 256, 148 * 32), 256, 0, s>>>(W.wid, W.out, W.nnz, W.n, W.Lw,
+                                                                W.step0, final_off, R, final_ids);
     items += W.n;  // rows touched (upper bound of pairs)
     launches += 1;
   }
