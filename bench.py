@@ -202,9 +202,14 @@ def main():
     import torch
     import torch.distributed as dist
     ws, rank, local = dist_env()
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
+    backend = os.environ.get("ND_DIST_BACKEND", "nccl")  # gloo: multi-rank check on one GPU
     if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     from paper_2009_06693_b200 import _lib, make_app
     from paper_2009_06693_b200.engine import run_device
     from paper_2009_06693_b200.graph import DeviceGraph
@@ -219,9 +224,9 @@ def main():
     stream = torch.cuda.current_stream()
 
     def barrier():
+        torch.cuda.synchronize()
         if ws > 1:
             dist.barrier()
-        torch.cuda.synchronize()
 
     def gather_rows(off, ids):
         """Final NCCL gather of every rank's compacted rows to rank 0."""
@@ -271,11 +276,12 @@ def main():
             launches += sum(int(dr.counters.get("launches", 0)) for dr in runs)
     clocks.__exit__()
     tot_ms = sum(times)
+    rdev = "cuda" if backend == "nccl" else "cpu"
     if ws > 1:
-        t = torch.tensor([tot_ms], dtype=torch.float64, device="cuda")
+        t = torch.tensor([tot_ms], dtype=torch.float64, device=rdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tot_ms = t.item()
-        e = torch.tensor([edges_dev], dtype=torch.int64, device="cuda")
+        e = torch.tensor([edges_dev], dtype=torch.int64, device=rdev)
         dist.all_reduce(e)
         edges_all = int(e.item())
     else:
@@ -306,38 +312,46 @@ def main():
     from paper_2009_06693_b200.engine import SampleRange
     roots_host = torch.from_numpy(O.uniform_roots(V, 1, SEED, lo, n).reshape(-1)).pin_memory()
     e2e_times, e2e_edges, h2d, d2h = [], 0, 0, 0
+    copy_stream = torch.cuda.Stream()
     for it in range(max(1, args.warmup // 2) + args.steps):
         barrier()
-        t0 = time.perf_counter()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record(stream)
         step_edges, step_h2d, step_d2h = 0, 0, 0
+        held = []
         for app in apps:
             droots = roots_host.to("cuda", non_blocking=True)
             step_h2d += roots_host.numel() * 8
             dr = _run_with_roots(run_device, app, dg, droots, lo, n)
             off = dr.view(_lib.F_FINAL_OFF)
             ids = dr.view(_lib.F_FINAL_IDS)
-            h_off = torch.empty(off.numel(), dtype=torch.int64, pin_memory=True)
-            h_ids = torch.empty(ids.numel(), dtype=torch.int64, pin_memory=True)
-            h_off.copy_(off, non_blocking=True)
-            h_ids.copy_(ids, non_blocking=True)
+            # D2H of this app's rows on a copy stream, overlapping the next app
+            done = torch.cuda.Event()
+            done.record(stream)
+            copy_stream.wait_event(done)
+            with torch.cuda.stream(copy_stream):
+                h_off = torch.empty(off.numel(), dtype=torch.int64, pin_memory=True)
+                h_ids = torch.empty(ids.numel(), dtype=torch.int64, pin_memory=True)
+                h_off.copy_(off, non_blocking=True)
+                h_ids.copy_(ids, non_blocking=True)
             step_d2h += (off.numel() + ids.numel()) * 8
             step_edges += dr.total_sampled
-            torch.cuda.synchronize()
-            dr.close()
+            held.append((dr, h_off, h_ids))
+        stream.wait_stream(copy_stream)
         ev1.record(stream)
         torch.cuda.synchronize()
+        for dr, _, _ in held:
+            dr.close()
         if it >= max(1, args.warmup // 2):
             e2e_times.append(ev0.elapsed_time(ev1))
             e2e_edges += step_edges
             h2d, d2h = step_h2d, step_d2h
     e2e_ms = sum(e2e_times)
     if ws > 1:
-        t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device=rdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = t.item()
-        e = torch.tensor([e2e_edges], dtype=torch.int64, device="cuda")
+        e = torch.tensor([e2e_edges], dtype=torch.int64, device=rdev)
         dist.all_reduce(e)
         e2e_edges = int(e.item())
     e2e_value = e2e_edges / (e2e_ms / 1e3)

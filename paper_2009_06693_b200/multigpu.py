@@ -27,6 +27,8 @@ def gather_rows(off, ids, group=None, dst: int = 0):
     import torch.distributed as dist
     ws = dist.get_world_size(group)
     rank = dist.get_rank(group)
+    if dist.get_backend(group) == "gloo" and ids.is_cuda:
+        off, ids = off.cpu(), ids.cpu()  # gloo gathers host tensors
     dev = ids.device
     sizes = torch.tensor([off.numel() - 1, ids.numel()], dtype=torch.int64, device=dev)
     all_sizes = [torch.zeros_like(sizes) for _ in range(ws)]
