@@ -499,6 +499,14 @@ static int build_from_edges_dev(const int64_t* src, const int64_t* dst, const do
   nd_free(k0, s); nd_free(k1, s); nd_free(i0, s); nd_free(i1, s);
   nd_free(bad, s); nd_free(wtmp, s); nd_free(tmp, s);
   cudaStreamSynchronize(s);
+  // the build's sort buffers (~32 B/edge) go back to the OS: the resident graph
+  // and the sampler's own working set are what the pool should keep
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+  }
   if (rc != ND_OK) {
     nd_graph_destroy(G);
     return rc;
