@@ -340,7 +340,9 @@ extern "C" int nd_run_individual(const nd_graph* G, int app_code, const double* 
   int64_t tp_cap = 0;
   int64_t* h_tmp = nd_pinned_scratch();
   int64_t step = 0;
+  nd_trace("ind:start");
   while (step < S_max && P > 0) {
+    nd_trace("ind:step-begin");
     const int64_t m = host_fanouts[step];
     const int64_t items = P * m;
     StepData sd;
@@ -391,6 +393,7 @@ extern "C" int nd_run_individual(const nd_graph* G, int app_code, const double* 
       // SP fetches: one adjacency read per (sample, transit) pair
       k_add_fetch<<<1, 1, 0, s>>>(st_step, (unsigned long long)P);
     }
+    nd_trace("ind:sampled(issued)");
     // stable compaction of the non-NULL slots -> next pairs
     int32_t* flags = nullptr;
     int64_t *sc = nullptr, *spo_next = nullptr;
@@ -418,6 +421,7 @@ extern "C" int nd_run_individual(const nd_graph* G, int app_code, const double* 
     ND_CUDA_TRY(cudaMemcpyAsync(h_tmp, sc + items, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     ND_CUDA_TRY(cudaStreamSynchronize(s));
     const int64_t Pn = h_tmp[0];
+    nd_trace("ind:compacted(synced)");
     sd.nnext = Pn;
     ND_CUDA_TRY(nd_alloc(&sd.npt, Pn, s));
     ND_CUDA_TRY(nd_alloc(&sd.npsid, Pn, s));
@@ -461,6 +465,7 @@ extern "C" int nd_run_individual(const nd_graph* G, int app_code, const double* 
   ND_CUDA_TRY(cudaMemcpyAsync(h_tmp, final_off + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   ND_CUDA_TRY(cudaStreamSynchronize(s));
   const int64_t total = h_tmp[0];
+  nd_trace("ind:final-scan(synced)");
   ND_CUDA_TRY(nd_alloc(&final_ids, total, s));
   if (n * R) {
     if (roots)
@@ -489,6 +494,7 @@ extern "C" int nd_run_individual(const nd_graph* G, int app_code, const double* 
   ND_CUDA_TRY(cudaMemcpyAsync(&h_stall, stall, sizeof(int), cudaMemcpyDeviceToHost, s));
   ND_CUDA_TRY(cudaMemcpyAsync(h_ctr, ctr, sizeof(h_ctr), cudaMemcpyDeviceToHost, s));
   ND_CUDA_TRY(cudaStreamSynchronize(s));
+  nd_trace("ind:done(synced)");
   for (auto& sd : steps) {
     nd_free(sd.out, s);
     nd_free(sd.cum, s);
