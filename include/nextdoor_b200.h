@@ -146,12 +146,15 @@ int nd_run_walk(const nd_graph *g, int app_code, const double *host_params, int6
                 int paradigm, void *stream, nd_result **out);
 
 /* Multi-slot individual apps (k-hop) through the run loop: fanouts[n_steps]
- * (host array).  roots: device int64 [n_samples * roots_per_sample] or NULL. */
+ * (host array).  roots: device int64 [n_samples * roots_per_sample] or NULL.
+ * host_unique[s] != 0 marks unique() steps (finish_step dedup, driver.py:
+ * 165-172; steps >= n_unique repeat the last flag; NULL = none). */
 int nd_run_individual(const nd_graph *g, int app_code, const double *host_params,
                       int64_t n_params, const int64_t *host_fanouts, int64_t n_fanouts,
                       int64_t sample_lo, int64_t n_samples, const int64_t *roots,
                       int64_t roots_per_sample, uint64_t seed, int64_t step_cap,
-                      int paradigm, void *stream, nd_result **out);
+                      int paradigm, const uint8_t *host_unique, int64_t n_unique,
+                      void *stream, nd_result **out);
 
 /* Collective apps (layer / fastgcn / ladies / mvs / clustergcn).
  * roots_off[n+1] / roots (device, ragged) or NULL for the app's keyed default
@@ -161,7 +164,8 @@ int nd_run_collective(const nd_graph *g, int kind, int64_t step_size, int64_t ma
                       int64_t clusters_per_sample, int64_t num_clusters,
                       int64_t sample_lo, int64_t n_samples, const int64_t *roots_off,
                       const int64_t *roots, uint64_t seed, int64_t step_cap,
-                      void *stream, nd_result **out);
+                      const uint8_t *host_unique, int64_t n_unique, void *stream,
+                      nd_result **out);
 
 /* build_transit_map + partition_work_classes for one step's pairs (device
  * int64 pair_transit[n], sample-major).  Outputs (device, caller-allocated,

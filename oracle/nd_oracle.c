@@ -498,6 +498,27 @@ int ndo_run_chain(const int64_t *row_offsets, const int64_t *col_indices,
  * core.py:168-203 (transits / liveness), transit_parallel.py:185-230.
  * Per step output: step_counts[s*n + i] slots for sample i (pairs*m, 0 when
  * not alive), vals step-major (sample-major inside a step, NULLs kept). */
+static int cmp_i64(const void *a, const void *b) {
+  int64_t x = *(const int64_t *)a, y = *(const int64_t *)b;
+  return x < y ? -1 : (x > y);
+}
+
+/* output.py:27-31 dedup_step: sorted distinct non-NULL values, in place;
+ * returns the new length */
+static int64_t dedup_inplace(int64_t *a, int64_t len) {
+  int64_t w = 0;
+  for (int64_t k = 0; k < len; k++) if (a[k] != NULLV) a[w++] = a[k];
+  qsort(a, (size_t)w, sizeof(int64_t), cmp_i64);
+  int64_t u = 0;
+  for (int64_t k = 0; k < w; k++) if (u == 0 || a[k] != a[u - 1]) a[u++] = a[k];
+  return u;
+}
+
+static int is_unique_step(const uint8_t *mask, int64_t n_mask, int64_t step) {
+  if (!mask || n_mask <= 0) return 0;
+  return mask[step < n_mask ? step : n_mask - 1] != 0;
+}
+
 int ndo_run_individual(const int64_t *row_offsets, const int64_t *col_indices,
                        const double *weights, const double *weight_prefix,
                        const double *max_weight, int64_t n_vertices, int app_code,
@@ -506,7 +527,8 @@ int ndo_run_individual(const int64_t *row_offsets, const int64_t *col_indices,
                        int root_pick, int needs_prev2, int64_t sample_lo,
                        int64_t n, const int64_t *roots_off, int64_t *roots,
                        uint64_t seed, int64_t steps, int64_t step_cap,
-                       int paradigm, int64_t *n_steps_out,
+                       int paradigm, const uint8_t *unique_mask, int64_t n_mask,
+                       int64_t *n_steps_out,
                        int64_t **step_counts, int64_t **vals, int64_t *n_vals,
                        int64_t **stats_out) {
   app_t a;
@@ -519,6 +541,7 @@ int ndo_run_individual(const int64_t *row_offsets, const int64_t *col_indices,
   int64_t *slice_off = malloc((size_t)(cap_steps * n + 1) * sizeof(int64_t));
   int64_t *slice_len = malloc((size_t)(cap_steps * n + 1) * sizeof(int64_t));
   char *alive = malloc((size_t)(n ? n : 1));
+  char *fallback = calloc((size_t)(n ? n : 1), 1);  /* driver.py:171 _sp_fallback */
   for (int64_t i = 0; i < n; i++) alive[i] = 1;
   vec_t pt = {0}, pp = {0}, pti = {0}, pprev = {0};
   int64_t step = 0;
@@ -571,15 +594,25 @@ int ndo_run_individual(const int64_t *row_offsets, const int64_t *col_indices,
     int64_t np_ = pt.len;
     int64_t st4[4] = {0, 0, 0, 0};
     if (paradigm == 1) {
-      int64_t *order = malloc((size_t)np_ * sizeof(int64_t)), *tmp = malloc((size_t)np_ * sizeof(int64_t));
-      int64_t *sk = malloc((size_t)np_ * sizeof(int64_t));
-      stable_argsort(pt.vals, np_, order, tmp);
-      for (int64_t k = 0; k < np_; k++) sk[k] = pt.vals[order[k]];
-      class_counts(sk, np_, m, st4);
-      free(order); free(tmp); free(sk);
+      /* transit_parallel.py:200-231: samples flagged by the previous unique
+       * step run sample-parallel (one fetch per pair, outside the groups) */
+      int64_t *keep = malloc((size_t)(np_ ? np_ : 1) * sizeof(int64_t));
+      int64_t nk = 0, nflag = 0;
+      for (int64_t k = 0; k < np_; k++) {
+        if (fallback[pp.vals[k]]) nflag++;
+        else keep[nk++] = pt.vals[k];
+      }
+      int64_t *order = malloc((size_t)(nk ? nk : 1) * sizeof(int64_t)), *tmp = malloc((size_t)(nk ? nk : 1) * sizeof(int64_t));
+      int64_t *sk = malloc((size_t)(nk ? nk : 1) * sizeof(int64_t));
+      stable_argsort(keep, nk, order, tmp);
+      for (int64_t k = 0; k < nk; k++) sk[k] = keep[order[k]];
+      class_counts(sk, nk, m, st4);
+      st4[3] += nflag;
+      free(order); free(tmp); free(sk); free(keep);
     } else {
       st4[3] = np_;
     }
+    for (int64_t i = 0; i < n; i++) fallback[i] = 0;
     for (int c = 0; c < 4; c++) vec_push(&S, st4[c]);
     /* outputs are order independent (keyed RNG): compute sample-major */
     int64_t base = V.len;
@@ -596,6 +629,23 @@ int ndo_run_individual(const int64_t *row_offsets, const int64_t *col_indices,
       int64_t i = pp.vals[p];
       if (slice_len[step * n + i] == 0) slice_off[step * n + i] = base + p * m;
       slice_len[step * n + i] += m;
+    }
+    if (is_unique_step(unique_mask, n_mask, step)) {
+      /* driver.py:165-172 finish_step: dedup every alive sample's step, then
+       * compact V (samples' slices are contiguous and sample-ordered) */
+      int64_t wpos = base;
+      for (int64_t i = 0; i < n; i++) {
+        int64_t sl = slice_len[step * n + i];
+        if (sl == 0) continue;
+        int64_t so = slice_off[step * n + i];
+        int64_t u = dedup_inplace(V.vals + so, sl);
+        memmove(V.vals + wpos, V.vals + so, (size_t)u * sizeof(int64_t));
+        slice_off[step * n + i] = wpos;
+        slice_len[step * n + i] = u;
+        fallback[i] = (0 < u && u < m);
+        wpos += u;
+      }
+      V.len = wpos;
     }
     if (root_pick) {
       /* apps.py:228-235 multirw_post_step */
@@ -617,7 +667,7 @@ out:
   *vals = V.vals ? V.vals : malloc(8);
   *n_vals = V.len;
   *stats_out = S.vals ? S.vals : malloc(8);
-  free(slice_off); free(slice_len); free(alive);
+  free(slice_off); free(slice_len); free(alive); free(fallback);
   free(pt.vals); free(pp.vals); free(pti.vals); free(pprev.vals);
   return rc;
 }
@@ -630,6 +680,7 @@ int ndo_run_collective(const int64_t *row_offsets, const int64_t *col_indices,
                        int64_t max_size, int distribution, int64_t sample_lo,
                        int64_t n, const int64_t *roots_off, const int64_t *roots,
                        uint64_t seed, int64_t steps, int64_t step_cap,
+                       const uint8_t *unique_mask, int64_t n_mask,
                        int64_t *n_steps_out, int64_t **step_counts,
                        int64_t **vals, int64_t *n_vals, int64_t **rec_counts,
                        int64_t **rec_t, int64_t **rec_v, int64_t *n_rec,
@@ -766,7 +817,15 @@ int ndo_run_collective(const int64_t *row_offsets, const int64_t *col_indices,
         rc = NDO_ERR_APP;
         goto out;
       }
-      for (int64_t sl = 0; sl < m; sl++) if (V.vals[new_off[i] + sl] != NULLV) size_[i]++;
+      if (is_unique_step(unique_mask, n_mask, step)) {
+        /* finish_step dedup (driver.py:165-172) of this sample's slots */
+        int64_t u = dedup_inplace(V.vals + new_off[i], m);
+        V.len = new_off[i] + u;
+        new_len[i] = u;
+        size_[i] += u;
+      } else {
+        for (int64_t sl = 0; sl < m; sl++) if (V.vals[new_off[i] + sl] != NULLV) size_[i]++;
+      }
       step_rec[i] = RT.len - rec_before;
     }
     if (!any) { free(allt.vals); free(new_off); free(new_len); free(step_rec); break; }

@@ -88,7 +88,8 @@ int ndo_run_individual(const int64_t *row_offsets, const int64_t *col_indices,
                        int root_pick, int needs_prev2, int64_t sample_lo,
                        int64_t n, const int64_t *roots_off, int64_t *roots,
                        uint64_t seed, int64_t steps, int64_t step_cap,
-                       int paradigm, int64_t *n_steps_out,
+                       int paradigm, const uint8_t *unique_mask, int64_t n_mask,
+                       int64_t *n_steps_out,
                        int64_t **step_counts, int64_t **vals, int64_t *n_vals,
                        int64_t **stats_out);
 
@@ -98,6 +99,7 @@ int ndo_run_collective(const int64_t *row_offsets, const int64_t *col_indices,
                        int64_t max_size, int distribution, int64_t sample_lo,
                        int64_t n, const int64_t *roots_off, const int64_t *roots,
                        uint64_t seed, int64_t steps, int64_t step_cap,
+                       const uint8_t *unique_mask, int64_t n_mask,
                        int64_t *n_steps_out, int64_t **step_counts,
                        int64_t **vals, int64_t *n_vals, int64_t **rec_counts,
                        int64_t **rec_t, int64_t **rec_v, int64_t *n_rec,

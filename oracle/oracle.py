@@ -199,9 +199,16 @@ def run_chain(g: OGraph, app_code, params, roots, seed, steps, step_cap=10_000,
                 n_steps=n_steps.value, stats=stats)
 
 
+def _mask(unique):
+    if unique is None:
+        return None, 0
+    m = np.ascontiguousarray(np.asarray(unique, dtype=np.uint8))
+    return m, len(m)
+
+
 def run_individual(g: OGraph, app_code, params, fanouts, roots_list, seed, steps,
                    step_cap=10_000, root_pick=False, needs_prev2=False,
-                   paradigm="tp", sample_lo=0):
+                   paradigm="tp", sample_lo=0, unique=None):
     """driver.py:203-235 run loop with StepPlan semantics (generic path)."""
     n = len(roots_list)
     roots_off = np.zeros(n + 1, dtype=np.int64)
@@ -212,13 +219,15 @@ def run_individual(g: OGraph, app_code, params, fanouts, roots_list, seed, steps
     n_steps = C.c_int64()
     cnt_p, vals_p, stats_p = C.c_void_p(), C.c_void_p(), C.c_void_p()
     n_vals = C.c_int64()
+    um, nm = _mask(unique)
     rc = lib().ndo_run_individual(
         _p(g.row_offsets), _p(g.col_indices), _p(g.weights), _p(g.per_vertex_weight_prefix),
         _p(g.per_vertex_max_weight), C.c_int64(g.n_vertices), C.c_int(app_code), _p(prm),
         C.c_int64(len(prm)), _p(fan), C.c_int64(len(fan)), C.c_int(int(root_pick)),
         C.c_int(int(needs_prev2)), C.c_int64(sample_lo), C.c_int64(n), _p(roots_off),
         _p(roots), C.c_uint64(seed & (2**64 - 1)), C.c_int64(-1 if steps is None else steps),
-        C.c_int64(step_cap), C.c_int(1 if paradigm == "tp" else 0), C.byref(n_steps),
+        C.c_int64(step_cap), C.c_int(1 if paradigm == "tp" else 0),
+        _p(um) if um is not None else None, C.c_int64(nm), C.byref(n_steps),
         C.byref(cnt_p), C.byref(vals_p), C.byref(n_vals), C.byref(stats_p))
     S = n_steps.value
     counts = _take(cnt_p, S * n).reshape(S, n)
@@ -230,7 +239,7 @@ def run_individual(g: OGraph, app_code, params, fanouts, roots_list, seed, steps
 
 
 def run_collective(g: OGraph, kind, step_size, roots_list, seed, steps, max_size=0,
-                   distribution=0, step_cap=10_000, sample_lo=0):
+                   distribution=0, step_cap=10_000, sample_lo=0, unique=None):
     n = len(roots_list)
     roots_off = np.zeros(n + 1, dtype=np.int64)
     roots_off[1:] = np.cumsum([len(r) for r in roots_list])
@@ -238,12 +247,14 @@ def run_collective(g: OGraph, kind, step_size, roots_list, seed, steps, max_size
     n_steps = C.c_int64()
     ptrs = [C.c_void_p() for _ in range(6)]
     n_vals, n_rec = C.c_int64(), C.c_int64()
+    um, nm = _mask(unique)
     rc = lib().ndo_run_collective(
         _p(g.row_offsets), _p(g.col_indices), C.c_int64(g.n_vertices), C.c_int(kind),
         C.c_int64(step_size), C.c_int64(max_size), C.c_int(distribution),
         C.c_int64(sample_lo), C.c_int64(n), _p(roots_off), _p(roots),
         C.c_uint64(seed & (2**64 - 1)), C.c_int64(-1 if steps is None else steps),
-        C.c_int64(step_cap), C.byref(n_steps), C.byref(ptrs[0]), C.byref(ptrs[1]),
+        C.c_int64(step_cap), _p(um) if um is not None else None, C.c_int64(nm),
+        C.byref(n_steps), C.byref(ptrs[0]), C.byref(ptrs[1]),
         C.byref(n_vals), C.byref(ptrs[2]), C.byref(ptrs[3]), C.byref(ptrs[4]),
         C.byref(n_rec), C.byref(ptrs[5]))
     S = n_steps.value

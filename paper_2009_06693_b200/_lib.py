@@ -44,9 +44,10 @@ SIGNATURES = {
     "nd_graph_arrays": [vp, pp, pp, pp, pp, pp],
     "nd_uniform_roots": [vp, i64, u64, i64, i64, vp, vp],
     "nd_run_walk": [vp, i32, vp, i64, i64, i64, vp, i64, u64, i64, i64, i32, vp, pp],
-    "nd_run_individual": [vp, i32, vp, i64, vp, i64, i64, i64, vp, i64, u64, i64, i32, vp, pp],
+    "nd_run_individual": [vp, i32, vp, i64, vp, i64, i64, i64, vp, i64, u64, i64, i32, vp, i64, vp,
+                          pp],
     "nd_run_collective": [vp, i32, i64, i64, i32, i64, i64, i64, i64, i64, i64, vp, vp, u64, i64,
-                          vp, pp],
+                          vp, i64, vp, pp],
     "nd_transit_schedule": [vp, i64, i64, vp, vp, vp, vp, vp, pi64, vp],
     "nd_result_info": [vp, pi64, pi64, pi64, pi64],
     "nd_result_field": [vp, i32, pp, pi64],

@@ -275,6 +275,23 @@ __global__ void k_next_transits(const int32_t* __restrict__ out, const int64_t* 
     if (flag[j]) ntv[pos[j]] = out[j];
 }
 
+__global__ void k_next_transits_sid(const int32_t* __restrict__ out, const int64_t* __restrict__ flag,
+                                    const int64_t* __restrict__ pos, int64_t nm, int64_t m,
+                                    int32_t* __restrict__ ntv, int32_t* __restrict__ nsid) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nm;
+       j += (int64_t)gridDim.x * blockDim.x)
+    if (flag[j]) {
+      ntv[pos[j]] = out[j];
+      nsid[pos[j]] = (int32_t)(j / m);
+    }
+}
+
+__global__ void k_size_add(int64_t* __restrict__ size, const int64_t* __restrict__ c, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    size[i] += c[i];
+}
+
 __global__ void k_next_toff(const int64_t* __restrict__ pos, int64_t n, int64_t m,
                             int64_t* __restrict__ ntoff, int64_t* __restrict__ size) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n;
@@ -440,7 +457,8 @@ extern "C" int nd_run_collective(const nd_graph* G, int kind, int64_t step_size,
                                  int64_t clusters_per_sample, int64_t num_clusters,
                                  int64_t sample_lo, int64_t n, const int64_t* roots_off_in,
                                  const int64_t* roots_in, uint64_t seed, int64_t step_cap,
-                                 void* stream, nd_result** out_res) {
+                                 const uint8_t* host_unique, int64_t n_unique, void* stream,
+                                 nd_result** out_res) {
   nd_pool_init();
   if (!G || n < 0 || sample_lo < 0 || step_size < 1 || kind < 0 || kind > 3) return kind < 0 || kind > 3 ? ND_ERR_APP : ND_ERR_ARG;
   cudaStream_t s = (cudaStream_t)stream;
@@ -684,23 +702,10 @@ extern "C" int nd_run_collective(const nd_graph* G, int kind, int64_t step_size,
       nd_free(bm, s); nd_free(cnt, s); nd_free(off, s);
     }
     total_rec += cs.nrec;
-    // per-step slots of alive samples
-    if (n) k_step_counts<<<nd_grid(n, 256), 256, 0, s>>>(alive, n, m, cs.counts, nullptr);
-    {
-      int64_t *ai = nullptr, *abase = nullptr;
-      ND_CUDA_TRY(nd_alloc(&ai, n + 1, s));
-      ND_CUDA_TRY(nd_alloc(&abase, n + 1, s));
-      k_alive_idx<<<nd_grid(n + 1, 256), 256, 0, s>>>(alive, n, ai);
-      ND_TRY(scan_excl(ai, abase, n + 1, s));
-      int64_t na = 0;
-      ND_TRY(dcopy_to_host(&na, abase + n, 1, s));
-      cs.nvals = na * m;
-      ND_CUDA_TRY(nd_alloc(&cs.vals, cs.nvals, s));
-      if (n * m) k_emit_slots<<<nd_grid(n * m, 256), 256, 0, s>>>(out, alive, abase, n, m, cs.vals);
-      nd_free(ai, s);
-      nd_free(abase, s);
-    }
-    // next transits = non-NULL slots (stable); sizes grow by the same count
+    const bool uniq = nd_unique_at(host_unique, n_unique, step);
+    // next transits = non-NULL slots (stable); with unique() the sorted distinct
+    // values per sample (finish_step, driver.py:165-172)
+    int32_t* nsid = nullptr;
     {
       int64_t *f = nullptr, *pos = nullptr;
       ND_CUDA_TRY(nd_alloc(&f, n * m + 1, s));
@@ -711,8 +716,45 @@ extern "C" int nd_run_collective(const nd_graph* G, int kind, int64_t step_size,
       ND_TRY(dcopy_to_host(&nt, pos + n * m, 1, s));
       ND_CUDA_TRY(nd_alloc(&cs.ntv, nt, s));
       ND_CUDA_TRY(nd_alloc(&cs.ntoff, n + 1, s));
-      if (n * m) k_next_transits<<<nd_grid(n * m, 256), 256, 0, s>>>(out, f, pos, n * m, cs.ntv);
-      k_next_toff<<<nd_grid(n + 1, 256), 256, 0, s>>>(pos, n, m, cs.ntoff, size);
+      if (uniq) {
+        ND_CUDA_TRY(nd_alloc(&nsid, nt, s));
+        if (n * m) k_next_transits_sid<<<nd_grid(n * m, 256), 256, 0, s>>>(out, f, pos, n * m, m, cs.ntv, nsid);
+        int32_t *usid = nullptr, *uval = nullptr;
+        int64_t um = 0;
+        int64_t* cnt_u = nullptr;
+        ND_CUDA_TRY(nd_alloc(&cnt_u, n + 1, s));
+        ND_TRY(nd_dedup_segments(nsid, cs.ntv, nt, n, V, &usid, &uval, &um, cnt_u, s));
+        ND_CUDA_TRY(cudaMemsetAsync(cnt_u + n, 0, sizeof(int64_t), s));
+        ND_TRY(scan_excl(cnt_u, cs.ntoff, n + 1, s));
+        if (n) k_size_add<<<nd_grid(n, 256), 256, 0, s>>>(size, cnt_u, n);
+        if (n) ND_CUDA_TRY(cudaMemcpyAsync(cs.counts, cnt_u, n * sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+        nd_free(cs.ntv, s);
+        nd_free(nsid, s);
+        nd_free(usid, s);
+        nd_free(cnt_u, s);
+        cs.ntv = uval;
+        nt = um;
+        cs.nvals = um;
+        ND_CUDA_TRY(nd_alloc(&cs.vals, um, s));
+        if (um) k_widen32<<<nd_grid(um, 256), 256, 0, s>>>(uval, um, cs.vals);
+      } else {
+        if (n * m) k_next_transits<<<nd_grid(n * m, 256), 256, 0, s>>>(out, f, pos, n * m, cs.ntv);
+        k_next_toff<<<nd_grid(n + 1, 256), 256, 0, s>>>(pos, n, m, cs.ntoff, size);
+        // per-step slots of alive samples (NULLs kept)
+        if (n) k_step_counts<<<nd_grid(n, 256), 256, 0, s>>>(alive, n, m, cs.counts, nullptr);
+        int64_t *ai = nullptr, *abase = nullptr;
+        ND_CUDA_TRY(nd_alloc(&ai, n + 1, s));
+        ND_CUDA_TRY(nd_alloc(&abase, n + 1, s));
+        k_alive_idx<<<nd_grid(n + 1, 256), 256, 0, s>>>(alive, n, ai);
+        ND_TRY(scan_excl(ai, abase, n + 1, s));
+        int64_t na = 0;
+        ND_TRY(dcopy_to_host(&na, abase + n, 1, s));
+        cs.nvals = na * m;
+        ND_CUDA_TRY(nd_alloc(&cs.vals, cs.nvals, s));
+        if (n * m) k_emit_slots<<<nd_grid(n * m, 256), 256, 0, s>>>(out, alive, abase, n, m, cs.vals);
+        nd_free(ai, s);
+        nd_free(abase, s);
+      }
       ND_CUDA_TRY(cudaMemcpyAsync(toff, cs.ntoff, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
       T = nt;
       tv = cs.ntv;

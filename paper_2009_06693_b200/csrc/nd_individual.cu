@@ -213,7 +213,6 @@ __global__ void k_ind_counts(const int64_t* __restrict__ spo, int64_t n, int64_t
     cnt_row[i] = b - a;
     const int64_t k = sc[b] - sc[a];
     nnz[i] = k;
-    tot[i] += k;
   }
 }
 
@@ -232,6 +231,52 @@ __global__ void k_ind_compact(const int32_t* __restrict__ out, int64_t items, in
     npsid[pos] = s;
     nptix[pos] = (int32_t)(pos - spo_next[s]);
   }
+}
+
+__global__ void k_tot_add(int64_t* __restrict__ tot, const int64_t* __restrict__ c, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    tot[i] += c[i];
+}
+
+// transit_idx of a deduped list = rank within its sample; fallback flags
+// (output.py:34-40: 0 < distinct < m)
+__global__ void k_dedup_tix(const int32_t* __restrict__ sid, int64_t cnt,
+                            const int64_t* __restrict__ spo_next, int32_t* __restrict__ tix) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < cnt;
+       j += (int64_t)gridDim.x * blockDim.x)
+    tix[j] = (int32_t)(j - spo_next[sid[j]]);
+}
+
+__global__ void k_fallback(const int64_t* __restrict__ cnt, int64_t n, int64_t m,
+                           uint8_t* __restrict__ fb, int* __restrict__ nfb) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const bool f = cnt[i] > 0 && cnt[i] < m;
+    fb[i] = f;
+    if (f) atomicAdd(nfb, 1);
+  }
+}
+
+// pairs of samples not flagged for the SP fallback (their transits form the
+// TP groups, transit_parallel.py:200-209); flagged pairs count as fetches
+__global__ void k_keep_unflagged(const uint32_t* __restrict__ pt, const int32_t* __restrict__ psid,
+                                 const uint8_t* __restrict__ fb, int64_t P,
+                                 int64_t* __restrict__ flag) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p <= P;
+       p += (int64_t)gridDim.x * blockDim.x)
+    flag[p] = (p < P && !fb[psid[p]]) ? 1 : 0;
+}
+
+__global__ void k_keep_write(const uint32_t* __restrict__ pt, const int64_t* __restrict__ flag,
+                             const int64_t* __restrict__ pos, int64_t P, uint32_t* __restrict__ keys,
+                             uint64_t* __restrict__ vals) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P;
+       p += (int64_t)gridDim.x * blockDim.x)
+    if (flag[p]) {
+      keys[pos[p]] = pt[p];
+      vals[pos[p]] = (uint64_t)p;
+    }
 }
 
 __global__ void k_widen(const int32_t* __restrict__ in, int64_t n, int64_t* __restrict__ out) {
@@ -277,6 +322,7 @@ __global__ void k_plus_r(int64_t* __restrict__ a, int64_t n, int64_t R) {
 struct StepData {
   int32_t* out = nullptr;   // [P*m]
   int64_t items = 0;
+  bool dedup = false;       // unique() step: the step's slots are npt (distinct, sorted)
   uint32_t* npt = nullptr;  // compacted next pairs
   int32_t* npsid = nullptr;
   int32_t* nptix = nullptr;
@@ -289,7 +335,8 @@ struct StepData {
 extern "C" int nd_run_individual(const nd_graph* G, int app_code, const double* host_params,
                                  int64_t n_params, const int64_t* host_fanouts, int64_t n_fanouts,
                                  int64_t sample_lo, int64_t n, const int64_t* roots, int64_t R,
-                                 uint64_t seed, int64_t step_cap, int paradigm, void* stream,
+                                 uint64_t seed, int64_t step_cap, int paradigm,
+                                 const uint8_t* host_unique, int64_t n_unique, void* stream,
                                  nd_result** out_res) {
   NdApp a;
   ND_TRY(nd_make_app(app_code, host_params, n_params, &a));
@@ -339,6 +386,13 @@ extern "C" int nd_run_individual(const nd_graph* G, int app_code, const double* 
   TPScratch TS;
   int64_t tp_cap = 0;
   int64_t* h_tmp = nd_pinned_scratch();
+  uint8_t* fb = nullptr;      // per-sample SP-fallback flags after a unique step
+  int* nfb = nullptr;
+  unsigned long long* scratch_stats = nullptr;
+  ND_CUDA_TRY(nd_alloc(&fb, n, s));
+  ND_CUDA_TRY(nd_alloc(&nfb, 1, s));
+  ND_CUDA_TRY(nd_alloc(&scratch_stats, 4, s));
+  int64_t n_flagged = 0;      // host copy for the current step
   int64_t step = 0;
   nd_trace("ind:start");
   while (step < S_max && P > 0) {
@@ -353,6 +407,49 @@ extern "C" int nd_run_individual(const nd_graph* G, int app_code, const double* 
     IndCtx c{view(g), a, key_base(seed, (uint64_t)step, 0, 0), sample_lo, m, pt, psid, ptix,
              sd.out, stall};
     unsigned long long* st_step = reinterpret_cast<unsigned long long*>(stats + 4 * step);
+    if (paradigm == ND_TP && n_flagged > 0) {
+      // statistics over the unflagged pairs only; flagged pairs are single fetches
+      int64_t *kf = nullptr, *kp = nullptr;
+      ND_CUDA_TRY(nd_alloc(&kf, P + 1, s));
+      ND_CUDA_TRY(nd_alloc(&kp, P + 1, s));
+      k_keep_unflagged<<<nd_grid(P + 1, 256), 256, 0, s>>>(pt, psid, fb, P, kf);
+      size_t tb = 0;
+      cub::DeviceScan::ExclusiveSum(nullptr, tb, kf, kp, P + 1, s);
+      void* tmp;
+      ND_CUDA_TRY(nd_alloc((char**)&tmp, tb, s));
+      ND_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tb, kf, kp, P + 1, s));
+      ND_CUDA_TRY(cudaMemcpyAsync(h_tmp, kp + P, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+      ND_CUDA_TRY(cudaStreamSynchronize(s));
+      const int64_t K = h_tmp[0];
+      if (K > tp_cap) {
+        if (tp_cap) TS.release(s);
+        ND_TRY(TS.alloc(K, key_bits, s));
+        tp_cap = K;
+      }
+      if (K) {
+        uint32_t *k0, *k1;
+        uint64_t *v0, *v1;
+        ND_CUDA_TRY(nd_alloc(&k0, K, s)); ND_CUDA_TRY(nd_alloc(&k1, K, s));
+        ND_CUDA_TRY(nd_alloc(&v0, K, s)); ND_CUDA_TRY(nd_alloc(&v1, K, s));
+        k_keep_write<<<nd_grid(P, 256), 256, 0, s>>>(pt, kf, kp, P, k0, v0);
+        cub::DoubleBuffer<uint32_t> dk(k0, k1);
+        cub::DoubleBuffer<uint64_t> dv(v0, v1);
+        ND_TRY(tp_sort(dk, dv, K, key_bits, TS, s));
+        k_mark<<<nd_grid(K, 256), 256, 0, s>>>(dk.Current(), K, TS.flags);
+        size_t t2 = TS.cub_bytes;
+        ND_CUDA_TRY(cub::DeviceScan::InclusiveSum(TS.cub_tmp, t2, TS.flags, TS.gid, (int)K, s));
+        ND_CUDA_TRY(cudaMemsetAsync(TS.counters, 0, 4 * sizeof(int), s));
+        k_gstart<<<nd_grid(K, 256), 256, 0, s>>>(TS.flags, TS.gid, K, TS.gstart, TS.counters);
+        k_ind_classify<<<nd_grid(K, 256), 256, 0, s>>>(TS.gstart, TS.counters, m, TS.med_list,
+                                                        TS.counters + 1, TS.large_units,
+                                                        TS.counters + 2, st_step);
+        nd_free(k0, s); nd_free(k1, s); nd_free(v0, s); nd_free(v1, s);
+      }
+      k_add_fetch<<<1, 1, 0, s>>>(st_step, (unsigned long long)(P - K));
+      nd_free(kf, s); nd_free(kp, s); nd_free(tmp, s);
+      st_step = scratch_stats;  // the execution below still runs TP; its stats are discarded
+      ND_CUDA_TRY(cudaMemsetAsync(scratch_stats, 0, 4 * sizeof(unsigned long long), s));
+    }
     if (paradigm == ND_TP) {
       if (P > tp_cap) {
         if (tp_cap) TS.release(s);
@@ -430,6 +527,44 @@ extern "C" int nd_run_individual(const nd_graph* G, int app_code, const double* 
       k_ind_compact<<<nd_grid(items, 256), 256, 0, s>>>(sd.out, items, m, sc, psid, spo_next,
                                                          sd.npt, sd.npsid, sd.nptix);
     ND_CUDA_TRY(cudaGetLastError());
+    n_flagged = 0;
+    if (nd_unique_at(host_unique, n_unique, step)) {
+      // finish_step (driver.py:165-172): each sample's step becomes its sorted
+      // distinct non-NULL vertices; the next transits are that list
+      int32_t *usid = nullptr, *uval = nullptr;
+      int64_t um = 0;
+      ND_TRY(nd_dedup_segments(sd.npsid, reinterpret_cast<const int32_t*>(sd.npt), Pn, n, g.V,
+                               &usid, &uval, &um, nnz, s));
+      ND_CUDA_TRY(cudaMemsetAsync(nnz + n, 0, sizeof(int64_t), s));
+      {
+        size_t tb = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, tb, nnz, spo_next, n + 1, s);
+        void* tmp;
+        ND_CUDA_TRY(nd_alloc((char**)&tmp, tb, s));
+        ND_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tb, nnz, spo_next, n + 1, s));
+        nd_free(tmp, s);
+      }
+      int32_t* utix = nullptr;
+      ND_CUDA_TRY(nd_alloc(&utix, um, s));
+      if (um) k_dedup_tix<<<nd_grid(um, 256), 256, 0, s>>>(usid, um, spo_next, utix);
+      if (n) ND_CUDA_TRY(cudaMemcpyAsync(step_counts + step * n, nnz, n * sizeof(int64_t),
+                                         cudaMemcpyDeviceToDevice, s));
+      ND_CUDA_TRY(cudaMemsetAsync(nfb, 0, sizeof(int), s));
+      if (n) k_fallback<<<nd_grid(n, 256), 256, 0, s>>>(nnz, n, m, fb, nfb);
+      int hn = 0;
+      ND_CUDA_TRY(cudaMemcpyAsync(&hn, nfb, sizeof(int), cudaMemcpyDeviceToHost, s));
+      ND_CUDA_TRY(cudaStreamSynchronize(s));
+      n_flagged = hn;
+      nd_free(sd.npt, s);
+      nd_free(sd.npsid, s);
+      nd_free(sd.nptix, s);
+      sd.npt = reinterpret_cast<uint32_t*>(uval);
+      sd.npsid = usid;
+      sd.nptix = utix;
+      sd.nnext = um;
+      sd.dedup = true;
+    }
+    if (n) k_tot_add<<<nd_grid(n, 256), 256, 0, s>>>(tot, nnz, n);
     nd_free(flags, s);
     nd_free(sc, s);
     nd_free(spo, s);
@@ -439,7 +574,7 @@ extern "C" int nd_run_individual(const nd_graph* G, int app_code, const double* 
     pt = sd.npt;
     psid = sd.npsid;
     ptix = sd.nptix;
-    P = Pn;
+    P = sd.nnext;
     steps.push_back(sd);
     step++;
   }
@@ -478,15 +613,22 @@ extern "C" int nd_run_individual(const nd_graph* G, int app_code, const double* 
     ND_CUDA_TRY(cudaMemsetAsync(roots_off, 0, (n + 1) * sizeof(int64_t), s));
   }
   int64_t total_items = 0;
-  for (auto& sd : steps) total_items += sd.items;
+  for (auto& sd : steps) total_items += sd.dedup ? sd.nnext : sd.items;
   ND_CUDA_TRY(nd_alloc(&step_vals, total_items, s));
   int64_t pos = 0;
   for (auto& sd : steps) {
     if (sd.nnext)
       k_ind_final<<<nd_grid(sd.nnext, 256), 256, 0, s>>>(sd.npt, sd.npsid, sd.nptix, sd.nnext,
                                                           final_off, sd.cum, R, final_ids);
-    if (sd.items) k_widen<<<nd_grid(sd.items, 256), 256, 0, s>>>(sd.out, sd.items, step_vals + pos);
-    pos += sd.items;
+    if (sd.dedup) {
+      if (sd.nnext)
+        k_widen<<<nd_grid(sd.nnext, 256), 256, 0, s>>>(reinterpret_cast<const int32_t*>(sd.npt),
+                                                       sd.nnext, step_vals + pos);
+      pos += sd.nnext;
+    } else {
+      if (sd.items) k_widen<<<nd_grid(sd.items, 256), 256, 0, s>>>(sd.out, sd.items, step_vals + pos);
+      pos += sd.items;
+    }
   }
   ND_CUDA_TRY(cudaGetLastError());
   int h_stall = 0;
@@ -504,6 +646,7 @@ extern "C" int nd_run_individual(const nd_graph* G, int app_code, const double* 
   }
   nd_free(pt0, s); nd_free(psid0, s); nd_free(ptix0, s);
   nd_free(spo, s); nd_free(tot, s); nd_free(nnz, s); nd_free(ctr, s); nd_free(stall, s);
+  nd_free(fb, s); nd_free(nfb, s); nd_free(scratch_stats, s);
   nd_free(flen, s); nd_free(roots32, s);
   if (tp_cap) TS.release(s);
   if (h_stall) {

@@ -60,6 +60,13 @@ int nd_pool_init();
 int64_t* nd_pinned_scratch();
 int nd_graph_ensure_index(nd_graph* G, int want_hset, int want_guide, cudaStream_t s);
 int nd_graph_ensure_records(nd_graph* G, cudaStream_t s);
+int nd_dedup_segments(const int32_t* sid, const int32_t* val, int64_t m, int64_t n_samples,
+                      int64_t n_vertices, int32_t** out_sid, int32_t** out_val, int64_t* out_m,
+                      int64_t* counts, cudaStream_t s);
+inline bool nd_unique_at(const uint8_t* mask, int64_t n, int64_t step) {
+  if (!mask || n <= 0) return false;
+  return mask[step < n ? step : n - 1] != 0;
+}
 
 // device counters block reset/read helpers
 int nd_uniform_roots_i32(const nd::DevGraph& g, int64_t count, uint64_t seed, int64_t sample_lo,

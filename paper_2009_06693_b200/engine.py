@@ -102,6 +102,8 @@ class DevicePlan:
     distribution: int = 0
     cps: int = 0
     nc: int = 0
+    unique: Optional[np.ndarray] = None   # uint8 per step (run loop apps only)
+    roots_kind: str = "keyed"             # "keyed" | "host" (custom init_roots)
 
 
 def describe(app) -> DevicePlan:
@@ -111,23 +113,29 @@ def describe(app) -> DevicePlan:
     p = dict(getattr(app, "params", {}) or {})
     steps = -1 if app.steps == INF_STEPS or (isinstance(app.steps, float) and math.isinf(app.steps)) \
         else int(app.steps)
-    n_check = 64 if steps < 0 else min(steps, 64)
-    if any(app.unique(s) for s in range(n_check)):
-        raise UnsupportedAppError(f"{name}: unique() steps are not supported by the device engine yet")
+    n_check = 4096 if steps < 0 else max(steps, 1)
+    um = np.asarray([1 if app.unique(s) else 0 for s in range(n_check)], dtype=np.uint8)
+    umask = um if um.any() else None
     if getattr(app, "step_transits_fn", None) is not None:
         raise UnsupportedAppError(f"{name}: custom step_transits_fn needs a Python callback")
     code = getattr(app, "kernel_code", None)
+    if code is None and name in _BUNDLED_CODES:
+        code = _BUNDLED_CODES[name]  # object-mode bundled app: same draws as its kernel
     kp = np.asarray(getattr(app, "kernel_params", np.zeros(0)), dtype=np.float64)
     init = getattr(app, "init_roots", None)
     R = int(getattr(init, "count", 0) or 0)
+    if len(kp) == 0 and code in (1, 2):
+        kp = _default_kparams(name, p)
     if code in (0, 1, 2, 4) and getattr(app, "chain_walk", False):
+        # chain walks ignore unique() like the reference's run_chain (chain.py:31-40)
         if code == 4:
             R = R or int(p.get("roots_per_sample", 100))
-        return DevicePlan("walk", name, code=code, kparams=kp, steps=steps, R=R or 1)
+        return DevicePlan("walk", name, code=code, kparams=kp, steps=steps, R=R or 1,
+                          roots_kind=_roots_kind(app))
     if code == 3:
         fan = [int(f) for f in p.get("fanouts", [app.sample_size(s) for s in range(max(steps, 0))])]
         return DevicePlan("individual", name, code=code, kparams=kp, steps=len(fan), R=R or 1,
-                          fanouts=fan)
+                          fanouts=fan, unique=umask, roots_kind=_roots_kind(app))
     if code in (0, 1, 2, 4):
         # kernel app without chain_walk: generic run loop, one slot per step
         m = [int(app.sample_size(s)) for s in range(max(steps, 1))] if steps >= 0 else [1]
@@ -136,7 +144,8 @@ def describe(app) -> DevicePlan:
         return DevicePlan("walk", name, code=code, kparams=kp, steps=steps, R=R or 1)
     if name in COLLECTIVE_KINDS:
         ck = COLLECTIVE_KINDS[name]
-        plan = DevicePlan("collective", name, ckind=ck, steps=steps)
+        plan = DevicePlan("collective", name, ckind=ck, steps=steps, unique=umask,
+                          roots_kind=_roots_kind(app))
         if ck == 0:
             plan.step_size = int(p.get("step_size", app.sample_size(0)))
             plan.max_size = int(p.get("max_size", 2000))
@@ -153,6 +162,34 @@ def describe(app) -> DevicePlan:
     raise UnsupportedAppError(
         f"app {name!r} has no device implementation (custom Python next_fn); the B200 "
         "engine runs the bundled apps' kernels only and has no CPU fallback")
+
+
+_BUNDLED_CODES = {"deepwalk": 0, "ppr": 1, "node2vec": 2, "khop": 3, "multirw": 4}
+
+
+def _default_kparams(name, p):
+    if name == "ppr":
+        return np.asarray([p.get("termination_probability", 0.01)], dtype=np.float64)
+    if name == "node2vec":
+        conv = p.get("factor_convention", "reciprocal")
+        return np.asarray([p.get("p", 2.0), p.get("q", 0.5), 0.0 if conv == "reciprocal" else 1.0])
+    return np.zeros(0)
+
+
+def _roots_kind(app) -> str:
+    """'keyed' when init_roots is one of the bundled keyed initialisers (ours or
+    the reference's closures, apps.py:83-103, 340-370): the device draws the
+    same roots itself.  Anything else is evaluated on the host and uploaded."""
+    init = getattr(app, "init_roots", None)
+    if init is None:
+        return "keyed"
+    from .apps import ClusterRoots, UniformRoots
+    if isinstance(init, (UniformRoots, ClusterRoots)):
+        return "keyed"
+    qn = getattr(init, "__qualname__", "")
+    if qn in ("_uniform_roots.<locals>.init", "make_clustergcn.<locals>.init"):
+        return "keyed"
+    return "host"
 
 
 class SampleRange(Sequence):
@@ -184,7 +221,7 @@ def make_samples(app, graph, n_samples: int, seed: int, lo: int = 0) -> SampleRa
 def _sample_spec(samples, plan, seed):
     """(sample_lo, n, roots) for the ABI; roots None = keyed on device."""
     if isinstance(samples, SampleRange):
-        if samples.seed == seed:
+        if samples.seed == seed and plan.roots_kind == "keyed":
             return samples.lo, samples.n, None, None
         samples = [samples[i] for i in range(samples.n)]
     samples = list(samples)
@@ -357,19 +394,23 @@ def run_device(app, graph, samples=None, *, seed: int = 0, paradigm: str = "tp",
             droots = torch.from_numpy(roots).cuda()
         kp = np.ascontiguousarray(plan.kparams, dtype=np.float64)
         fan = np.ascontiguousarray(plan.fanouts, dtype=np.int64)
+        um = None if plan.unique is None else np.ascontiguousarray(plan.unique)
         rc = L.nd_run_individual(dg.handle, plan.code, _lib.ptr(kp), len(kp), _lib.ptr(fan),
                                  len(fan), lo, n, _lib.ptr(droots), R,
-                                 C.c_uint64(seed & (2**64 - 1)), step_cap, par, sp, C.byref(h))
+                                 C.c_uint64(seed & (2**64 - 1)), step_cap, par, _lib.ptr(um),
+                                 0 if um is None else len(um), sp, C.byref(h))
         _lib.check(rc, "nd_run_individual")
     else:
         droff = dro = None
         if roots is not None:
             droff = torch.from_numpy(roots_off).cuda()
             dro = torch.from_numpy(roots).cuda()
+        um = None if plan.unique is None else np.ascontiguousarray(plan.unique)
         rc = L.nd_run_collective(dg.handle, plan.ckind, plan.step_size, plan.max_size,
                                  plan.distribution, plan.steps, plan.R, plan.cps, plan.nc, lo, n,
                                  _lib.ptr(droff), _lib.ptr(dro), C.c_uint64(seed & (2**64 - 1)),
-                                 step_cap, sp, C.byref(h))
+                                 step_cap, _lib.ptr(um), 0 if um is None else len(um), sp,
+                                 C.byref(h))
         _lib.check(rc, "nd_run_collective")
     if sync:
         torch.cuda.synchronize()

@@ -190,15 +190,37 @@ def main():
         ("mvs", "powerlaw:1000", False, 8, 4, {"batch_size": 16, "step_size": 10}),
         ("clustergcn", "powerlaw:1000", False, 3, 4, {"clusters_per_sample": 5, "num_clusters": 20}),
     ]
+    # unique()/dedup + SP-fallback routing (driver.py:165-172,
+    # transit_parallel.py:200-231; tests/test_engines.py:194-215 pattern)
+    cases += [
+        ("khop", "cycle:200", True, 10, 14, {"fanouts": [12, 4], "unique": [0]}),
+        ("khop", "powerlaw:1000", False, 30, 6, {"fanouts": [10, 5], "unique": "all"}),
+        ("khop", "powerlaw:1000", False, 30, 6, {"fanouts": [25, 10], "unique": [1]}),
+        ("khop", "star:300", True, 12, 2, {"fanouts": [40, 3], "unique": [0]}),
+        ("layer", "powerlaw:1000", False, 6, 4, {"max_size": 300, "step_size": 50, "unique": "all"}),
+        ("fastgcn", "powerlaw:1000", False, 6, 4, {"unique": [0, 2]}),
+        ("mvs", "powerlaw:1000", False, 8, 4, {"batch_size": 16, "step_size": 40, "unique": "all"}),
+    ]
+
+    def apply_unique(app, kw):
+        u = kw.get("unique")
+        if u == "all":
+            app.unique = lambda step: True
+        elif u is not None:
+            us = set(u)
+            app.unique = lambda step, us=us: step in us
+        return app
+
     for idx, (app_name, spec, weighted, ns, seed, kw) in enumerate(cases):
         gkey, g = G(spec, weighted, seed)
-        app = make_app(app_name, **kw)
+        mk = {k: v for k, v in kw.items() if k != "unique"}
+        app = apply_unique(make_app(app_name, **mk), kw)
         samples = make_samples(app, g, ns, seed)
         out = tp_run(app, g, samples, EngineConfig(seed=seed))
         text_final = render_text(out, LAYOUT_FINAL)
         text_step = render_text(out, LAYOUT_PER_STEP)
         # SP must agree byte for byte (reference invariant)
-        app2 = make_app(app_name, **kw)
+        app2 = apply_unique(make_app(app_name, **mk), kw)
         out_sp = sp_run(app2, g, make_samples(app2, g, ns, seed), EngineConfig(seed=seed))
         assert render_text(out_sp, LAYOUT_FINAL) == text_final
         rows = out.final_rows()

@@ -42,9 +42,19 @@ APP_CODES = {"deepwalk": 0, "ppr": 1, "node2vec": 2, "khop": 3, "multirw": 4}
 COLLECTIVE_KINDS = {"layer": 0, "fastgcn": 1, "ladies": 1, "mvs": 2, "clustergcn": 3}
 
 
+def unique_mask(params, n=64):
+    """The golden cases' unique() spec: "all" or a list of unique steps."""
+    u = params.get("unique")
+    if u is None:
+        return None
+    if u == "all":
+        return [1] * n
+    return [1 if s in u else 0 for s in range(n)]
+
+
 def app_spec(app, params):
     """Reference defaults (apps.py:37-80) merged with the overrides."""
-    p = dict(params)
+    p = {k: v for k, v in params.items() if k != "unique"}
     if app == "deepwalk":
         return dict(code=0, kparams=[], steps=p.get("walk_length", 100), R=1)
     if app == "ppr":
@@ -79,16 +89,19 @@ def oracle_run(meta, g: O.OGraph, paradigm="tp", n_threads=1):
         roots = [O.cluster_roots(g.n_vertices, sp["cps"], sp["nc"], seed, i) for i in range(n)]
     else:
         roots = list(O.uniform_roots(g.n_vertices, sp["R"], seed, 0, n))
+    um = unique_mask(meta["params"])
     if "kind" in sp:
         r = O.run_collective(g, sp["kind"], sp["m"], roots, seed, sp["steps"],
-                             max_size=sp.get("max_size", 0), distribution=sp.get("distribution", 0))
+                             max_size=sp.get("max_size", 0), distribution=sp.get("distribution", 0),
+                             unique=um)
         roff = np.concatenate([[0], np.cumsum([len(x) for x in roots])])
         out = SampleSetOutput(ids, roff, np.concatenate(roots), r["n_steps"], stats=r["stats"],
                               step_counts=r["step_counts"], step_vals=r["vals"],
                               rec_counts=r["rec_counts"], rec_t=r["rec_t"], rec_v=r["rec_v"])
         return out
     if app == "khop":
-        r = O.run_individual(g, 3, [], sp["fanouts"], roots, seed, sp["steps"], paradigm=paradigm)
+        r = O.run_individual(g, 3, [], sp["fanouts"], roots, seed, sp["steps"], paradigm=paradigm,
+                             unique=um)
         roff = np.concatenate([[0], np.cumsum([len(x) for x in r["roots"]])])
         return SampleSetOutput(ids, roff, np.concatenate(r["roots"]), r["n_steps"], stats=r["stats"],
                                step_counts=r["step_counts"], step_vals=r["vals"])
@@ -110,3 +123,17 @@ def recorded_equal(out, rstore, pre):
     return (np.array_equal(np.asarray(out.rec_counts), rstore[f"{pre}/rec_cnt"])
             and np.array_equal(out.rec_t, rstore[f"{pre}/rec_t"])
             and np.array_equal(out.rec_v, rstore[f"{pre}/rec_v"]))
+
+
+def build_app(meta):
+    """make_app with the golden case's overrides, incl. the unique() spec."""
+    from paper_2009_06693_b200 import make_app
+    kw = {k: v for k, v in meta["params"].items() if k != "unique"}
+    app = make_app(meta["app"], **kw)
+    u = meta["params"].get("unique")
+    if u == "all":
+        app.unique = lambda step: True
+    elif u is not None:
+        us = set(u)
+        app.unique = lambda step, us=us: step in us
+    return app

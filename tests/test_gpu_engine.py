@@ -5,7 +5,7 @@ import numpy as np
 import pytest
 
 from oracle import oracle as O
-from tests.helpers import golden, golden_graph, oracle_run, recorded_equal, sha16, texts
+from tests.helpers import build_app, golden, golden_graph, oracle_run, recorded_equal, sha16, texts
 
 pytestmark = pytest.mark.gpu
 
@@ -21,7 +21,7 @@ def _device_run(meta, paradigm):
     from paper_2009_06693_b200.graph import DeviceGraph
     g = golden_graph(meta["graph"])
     dg = DeviceGraph.from_arrays(g.row_offsets, g.col_indices, g.weights)
-    app = make_app(meta["app"], **meta["params"])
+    app = build_app(meta)
     samples = make_samples(app, g, meta["n_samples"], meta["seed"])
     run = tp_run if paradigm == "tp" else sp_run
     return run(app, dg, samples, EngineConfig(seed=meta["seed"]))
@@ -276,3 +276,47 @@ def test_index_paths_on_adversarial_hub_graph(app):
         roff, rids = ref.final_csr()
         assert np.array_equal(off, roff) and np.array_equal(ids, rids), par
         dr.close()
+
+
+def test_unique_fallback_routing_object_mode():
+    """tests/test_engines.py:194-215 of the reference: an object-mode k-hop
+    (kernel_code None) with a unique first step on a degree-1 cycle: every
+    sample dedups to one vertex, is flagged for the SP fallback, and TP/SP
+    outputs agree."""
+    from paper_2009_06693_b200 import EngineConfig, make_app, make_samples, sp_run, tp_run
+    from paper_2009_06693_b200.synth import cycle_graph
+    g = cycle_graph(40, weighted=True, seed=2)
+
+    def build():
+        app = make_app("khop", fanouts=[12, 4])
+        app.unique = lambda step: step == 0
+        app.kernel_code = None
+        return app
+
+    texts_ = {}
+    for run, label in [(sp_run, "sp"), (tp_run, "tp")]:
+        app = build()
+        out = run(app, g, make_samples(app, g, 10, seed=14), EngineConfig(seed=14))
+        assert all(len(s.vertices_at(0)) == 1 for s in out.samples)
+        assert all(len(s.vertices_at(1)) == 4 for s in out.samples)
+        texts_[label] = texts(out)[0]
+        if label == "tp":
+            # all 10 samples flagged: step 1 runs sample-parallel, no TP groups
+            t1 = out.stats.timings[1]
+            assert (t1.groups_small, t1.groups_medium, t1.groups_large) == (0, 0, 0)
+    assert texts_["sp"] == texts_["tp"]
+
+
+def test_custom_init_roots_star_single_giant_group():
+    """tests/test_engines.py:218-228: custom init_roots (every sample rooted
+    at the hub) -> one TP group at step 0, classed medium (work 60)."""
+    from paper_2009_06693_b200 import EngineConfig, make_app, make_samples, tp_run
+    from paper_2009_06693_b200.synth import star_graph
+    g = star_graph(200)
+    app = make_app("khop", fanouts=[2, 2])
+    app.init_roots = lambda graph, sid, seed: np.asarray([0], dtype=np.int64)
+    out = tp_run(app, g, make_samples(app, g, 30, seed=1), EngineConfig(seed=1))
+    t0 = out.stats.timings[0]
+    assert (t0.groups_small + t0.groups_medium + t0.groups_large) == 1
+    assert t0.groups_medium == 1
+    assert all(r[0] == 0 for r in out.final_rows())
