@@ -320,3 +320,19 @@ def test_custom_init_roots_star_single_giant_group():
     assert (t0.groups_small + t0.groups_medium + t0.groups_large) == 1
     assert t0.groups_medium == 1
     assert all(r[0] == 0 for r in out.final_rows())
+
+
+@pytest.mark.parametrize("case", golden("cli.json"), ids=lambda c: "-".join(c["args"][1:2] + c["args"][3:4]))
+def test_cli_output_matches_reference_cli(case, tmp_path):
+    """The device CLI writes the reference CLI's bytes (output text, .remap
+    sidecar) and the same deterministic report keys (cli.py:88-137)."""
+    import hashlib
+    from paper_2009_06693_b200.cli import main
+    o, r = tmp_path / "out.txt", tmp_path / "rep.txt"
+    assert main([*case["args"], "--output", str(o), "--report", str(r)]) == 0
+    sha = lambda p: hashlib.sha256(open(p, "rb").read()).hexdigest()[:16]
+    assert sha(o) == case["output"]
+    assert sha(str(o) + ".remap") == case["remap"]
+    rep = dict(line.split("=", 1) for line in open(r).read().splitlines())
+    for k, v in case["report"].items():
+        assert rep[k] == v, k

@@ -84,7 +84,8 @@ def c1():
     dt = time.perf_counter() - t0
     edges = int((ref["chain_vals"] >= 0).sum())
     res["cpu"] = {"s": dt, "edges_per_s": edges / dt, "cores": CORES, "kind": "port", "sample": "full job"}
-    _, _, off, ids = dev_rows(app, dg, N, seed, "sp")
+    r = dev_rows(app, dg, N, seed, "sp")
+    off, ids = r[2], r[3]
     cl = ref["chain_len"]
     st = np.concatenate([[0], np.cumsum(cl)])
     exp = np.concatenate([np.concatenate([roots[i], ref["chain_vals"][st[i]:st[i + 1]][ref["chain_vals"][st[i]:st[i + 1]] >= 0]]) for i in range(N)])
