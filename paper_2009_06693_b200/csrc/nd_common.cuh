@@ -109,6 +109,30 @@ struct __align__(16) EdgePC {  // weighted pick: prefix + the neighbour it selec
   int32_t pad;
 };
 
+// Neighbour records for the walker-major kernel: each edge record also
+// carries its destination's row header, so the record that selects the next
+// vertex delivers that vertex's header in the same sector (no separate
+// vertex-record load per step).
+struct __align__(32) NbrW {   // node2vec try: neighbour, its weight, its header
+  int32_t col;
+  int32_t deg;
+  int64_t lo;
+  double w;
+  double mx;
+};
+struct __align__(32) NbrP {   // weighted pick: prefix, neighbour, its header
+  double pre;
+  int32_t col;
+  int32_t deg;
+  int64_t lo;
+  double total;
+};
+struct __align__(16) NbrU {   // unit-weight graphs: neighbour + its header
+  int32_t col;
+  int32_t deg;
+  int64_t lo;
+};
+
 struct DevGraph {
   int64_t V = 0, E = 0;
   const int64_t* row = nullptr;
@@ -121,6 +145,9 @@ struct DevGraph {
   const VRec* vrec = nullptr;     // optional packed vertex records
   const EdgeCW* ecw = nullptr;    // optional packed (col, w) records
   const EdgePC* epc = nullptr;    // optional packed (prefix, col) records
+  const NbrW* nbw = nullptr;      // optional neighbour records (node2vec tries)
+  const NbrP* nbp = nullptr;      // optional neighbour records (weighted picks)
+  const NbrU* nbu = nullptr;      // optional neighbour records (unit graphs)
   int unit = 0;
 };
 

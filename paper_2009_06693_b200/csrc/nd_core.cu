@@ -334,6 +334,9 @@ extern "C" int nd_graph_destroy(nd_graph* G) {
   cudaFree(G->vrec);
   cudaFree(G->ecw);
   cudaFree(G->epc);
+  cudaFree(G->nbw);
+  cudaFree(G->nbp);
+  cudaFree(G->nbu);
   delete G;
   return ND_OK;
 }

@@ -73,27 +73,46 @@ __global__ void k_build_vrec(const int64_t* __restrict__ row, const double* __re
   }
 }
 
-__global__ void k_build_edges(const int32_t* __restrict__ col, const double* __restrict__ w,
-                              const double* __restrict__ pre, int64_t E, EdgeCW* __restrict__ cw,
-                              EdgePC* __restrict__ pc) {
+__global__ void k_build_nbr(const int64_t* __restrict__ row, const int32_t* __restrict__ col,
+                            const double* __restrict__ w, const double* __restrict__ pre,
+                            const double* __restrict__ mx, int64_t E, NbrW* __restrict__ nw,
+                            NbrP* __restrict__ np_, NbrU* __restrict__ nu) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E;
        e += (int64_t)gridDim.x * blockDim.x) {
-    EdgeCW a;
-    a.col = col[e];
-    a.pad = 0;
-    a.w = w[e];
-    cw[e] = a;
-    EdgePC b;
-    b.pre = pre[e];
-    b.col = col[e];
-    b.pad = 0;
-    pc[e] = b;
+    const int32_t u = col[e];
+    const int64_t lo = row[u], deg = row[u + 1] - lo;
+    if (nu) {
+      NbrU r;
+      r.col = u;
+      r.deg = (int32_t)deg;
+      r.lo = lo;
+      nu[e] = r;
+      continue;
+    }
+    if (nw) {
+      NbrW r;
+      r.col = u;
+      r.deg = (int32_t)deg;
+      r.lo = lo;
+      r.w = w[e];
+      r.mx = mx[u];
+      nw[e] = r;
+    }
+    if (np_) {
+      NbrP r;
+      r.pre = pre[e];
+      r.col = u;
+      r.deg = (int32_t)deg;
+      r.lo = lo;
+      r.total = deg > 0 ? pre[lo + deg - 1] : 0.0;
+      np_[e] = r;
+    }
   }
 }
 
 }  // namespace
 
-int nd_graph_ensure_records(nd_graph* G, cudaStream_t s) {
+int nd_graph_ensure_records(nd_graph* G, int want_tries, cudaStream_t s) {
   static const bool disabled = getenv("ND_NO_PACK") && getenv("ND_NO_PACK")[0] == '1';
   if (disabled) return ND_OK;
   const int64_t V = G->g.V, E = G->g.E;
@@ -105,14 +124,24 @@ int nd_graph_ensure_records(nd_graph* G, cudaStream_t s) {
     ND_CUDA_TRY(cudaGetLastError());
     G->g.vrec = G->vrec;
   }
-  if (!G->ecw && !G->g.unit && E > 0) {
-    ND_CUDA_TRY(cudaMalloc(&G->ecw, E * sizeof(EdgeCW)));
-    ND_CUDA_TRY(cudaMalloc(&G->epc, E * sizeof(EdgePC)));
-    G->bytes += E * (sizeof(EdgeCW) + sizeof(EdgePC));
-    k_build_edges<<<nd_grid(E, 256), 256, 0, s>>>(G->col, G->w, G->pre, E, G->ecw, G->epc);
-    ND_CUDA_TRY(cudaGetLastError());
-    G->g.ecw = G->ecw;
-    G->g.epc = G->epc;
+  if (E > 0) {
+    NbrW* nw = nullptr;
+    NbrP* np_ = nullptr;
+    NbrU* nu = nullptr;
+    if (G->g.unit) {
+      if (!G->nbu) ND_CUDA_TRY(cudaMalloc(&nu, E * sizeof(NbrU)));
+    } else {
+      if (!G->nbp) ND_CUDA_TRY(cudaMalloc(&np_, E * sizeof(NbrP)));
+      if (want_tries && !G->nbw) ND_CUDA_TRY(cudaMalloc(&nw, E * sizeof(NbrW)));
+    }
+    if (nw || np_ || nu) {
+      k_build_nbr<<<nd_grid(E, 256, 148 * 64), 256, 0, s>>>(G->row, G->col, G->w, G->pre, G->mx,
+                                                             E, nw, np_, nu);
+      ND_CUDA_TRY(cudaGetLastError());
+      if (nw) { G->nbw = nw; G->g.nbw = nw; G->bytes += E * sizeof(NbrW); }
+      if (np_) { G->nbp = np_; G->g.nbp = np_; G->bytes += E * sizeof(NbrP); }
+      if (nu) { G->nbu = nu; G->g.nbu = nu; G->bytes += E * sizeof(NbrU); }
+    }
   }
   ND_CUDA_TRY(cudaStreamSynchronize(s));
   return ND_OK;
@@ -145,6 +174,6 @@ int nd_graph_ensure_index(nd_graph* G, int want_hset, int want_guide, cudaStream
 extern "C" int nd_graph_build_index(nd_graph* g, int flags, void* stream) {
   if (!g) return ND_ERR_ARG;
   ND_TRY(nd_graph_ensure_index(g, flags & 1, flags & 2, (cudaStream_t)stream));
-  if (flags & 4) ND_TRY(nd_graph_ensure_records(g, (cudaStream_t)stream));
+  if (flags & 4) ND_TRY(nd_graph_ensure_records(g, flags & 1, (cudaStream_t)stream));
   return ND_OK;
 }

@@ -236,6 +236,9 @@ struct PWArgs {
   const VRec* vrec;   // packed vertex records (or null)
   const EdgeCW* ecw;
   const EdgePC* epc;
+  const NbrW* nbw;    // neighbour records (or null)
+  const NbrP* nbp;
+  const NbrU* nbu;
 };
 
 // one 32-byte sector: row bounds, max weight and prefix total of v
@@ -266,6 +269,89 @@ __device__ __forceinline__ int64_t n2v_try(const PWArgs& A, const RowT& r, int64
   int64_t nb;
   double w;
   r.cw(k, nb, w, A.gv.unit);
+  double f;
+  st.tries++;
+  st.bytes += 2 * SECTOR + SECTOR * search_sectors(thi - tlo);
+  if (nb == t) f = A.a.f_ret;
+  else if (A.gv.hset != nullptr && thi - tlo > HASH_MIN_DEG)
+    f = hset_contains(A.gv.hset + 4 * tlo, hset_size(thi - tlo), (int32_t)nb) ? A.a.f_adj : A.a.f_far;
+  else f = has_edge(A.gv.col, tlo, thi, nb) ? A.a.f_adj : A.a.f_far;
+  const double u01 = to_unit(draw_u64(b + C_DRAW, ik));
+  return (env <= 0.0 || __dmul_rn(u01, env) < __dmul_rn(w, f)) ? nb : -2;
+}
+
+
+// ---- neighbour-record step: the record that selects the next
+// vertex carries its header (row start, degree, max weight / prefix total).
+struct NextHdr {
+  int64_t lo = -1;
+  int64_t deg = 0;
+  double mx = -1.0;
+  double tot = -1.0;
+};
+
+__device__ __forceinline__ int64_t rec_pick(const PWArgs& A, int64_t lo, int64_t deg, double tot,
+                                            double u01, NextHdr& nh, ItemStats& st) {
+  if (A.nbu != nullptr) {  // unit weights: floor identity
+    int64_t k = (int64_t)__dmul_rn(u01, (double)deg);
+    if (k > deg - 1) k = deg - 1;
+    const int4 r = __ldg(reinterpret_cast<const int4*>(A.nbu + lo + k));
+    nh.deg = r.y;
+    nh.lo = (int64_t)(((uint64_t)(uint32_t)r.w << 32) | (uint32_t)r.z);
+    nh.mx = nh.deg > 0 ? 1.0 : 0.0;
+    nh.tot = (double)nh.deg;
+    st.bytes += SECTOR + 8;
+    return r.x;
+  }
+  const NbrP* rp = A.nbp + lo;
+  const double x = __dmul_rn(u01, tot);
+  int64_t a = 0, b = deg;
+  if (A.gv.guide != nullptr && deg > GUIDE_MIN_DEG) {
+    int64_t j = (int64_t)__dmul_rn(u01, (double)deg);
+    if (j > deg - 1) j = deg - 1;
+    const int32_t* gd = A.gv.guide + lo;
+    if (j >= 1) a = __ldg(gd + j - 1);
+    if (j + 2 < deg) b = (int64_t)__ldg(gd + j + 2) + 1;
+  }
+  while (a < b) {
+    const int64_t mid = (a + b) >> 1;
+    if (__ldg(&rp[mid].pre) <= x) a = mid + 1; else b = mid;
+  }
+  const int64_t k = a < deg - 1 ? a : deg - 1;
+  const int4 r0 = __ldg(reinterpret_cast<const int4*>(rp + k));
+  const double2 r1 = __ldg(reinterpret_cast<const double2*>(rp + k) + 1);
+  nh.deg = r0.w;
+  nh.lo = __double_as_longlong(r1.x);
+  nh.tot = r1.y;
+  nh.mx = -1.0;
+  st.bytes += SECTOR + SECTOR * search_sectors(deg) + SECTOR + 8;
+  return r0.z;
+}
+
+// one node2vec rejection try over the neighbour records; -2 = rejected
+__device__ __forceinline__ int64_t rec_try(const PWArgs& A, int64_t lo, int64_t deg, int64_t t,
+                                           int64_t tlo, int64_t thi, double env, uint64_t b,
+                                           uint64_t ik, NextHdr& nh, ItemStats& st) {
+  const int64_t k = (int64_t)mod_u64(draw_u64(b, ik), (uint64_t)deg);
+  int64_t nb;
+  double w;
+  if (A.nbu != nullptr) {
+    const int4 r = __ldg(reinterpret_cast<const int4*>(A.nbu + lo + k));
+    nb = r.x;
+    w = 1.0;
+    nh.deg = r.y;
+    nh.lo = (int64_t)(((uint64_t)(uint32_t)r.w << 32) | (uint32_t)r.z);
+    nh.mx = nh.deg > 0 ? 1.0 : 0.0;
+  } else {
+    const int4 r0 = __ldg(reinterpret_cast<const int4*>(A.nbw + lo + k));
+    const double2 r1 = __ldg(reinterpret_cast<const double2*>(A.nbw + lo + k) + 1);
+    nb = r0.x;
+    nh.deg = r0.y;
+    nh.lo = (int64_t)(((uint64_t)(uint32_t)r0.w << 32) | (uint32_t)r0.z);
+    w = r1.x;
+    nh.mx = r1.y;
+  }
+  nh.tot = -1.0;
   double f;
   st.tries++;
   st.bytes += 2 * SECTOR + SECTOR * search_sectors(thi - tlo);
@@ -336,8 +422,31 @@ __global__ void __launch_bounds__(256, MINB) k_walk_persistent(PWArgs A) {
     // ---- one unit of work: a node2vec try (step >= 1) or a whole step
     int stl = 0;
     int64_t o;
+    NextHdr nh;
     const uint64_t base0 = key_base(A.seed, (uint64_t)s, 0, 0);
-    if (n2v && t >= 0 && deg > 0) {
+    const bool recs = (A.nbp != nullptr || A.nbu != nullptr) && (!n2v || A.nbw || A.nbu);
+    if (recs) {
+      if (deg <= 0) {
+        o = -1;
+      } else if (n2v && t >= 0) {
+        if (j == 0) st.bytes += 2 * SECTOR;  // t offsets + max_w (§8 d pair term)
+        const double env = __dmul_rn(mx, A.a.f_max);
+        o = rec_try(A, lo, deg, t, tlo, thi, env, base0 + 2 * C_DRAW * (uint64_t)j, ik, nh, st);
+        if (o == -2) {
+          if (++j >= N2V_MAX_TRIES) {
+            atomicExch(A.stall, 1);
+            o = -1;
+          } else {
+            continue;  // rejected: the lane tries again next iteration
+          }
+        }
+      } else if (A.a.code == ND_PPR) {
+        if (to_unit(draw_u64(base0, ik)) < A.a.term) o = -1;
+        else o = rec_pick(A, lo, deg, tot, to_unit(draw_u64(base0 + C_DRAW, ik)), nh, st);
+      } else {  // DeepWalk, node2vec step 0: draw 0 weighted pick
+        o = rec_pick(A, lo, deg, tot, to_unit(draw_u64(base0, ik)), nh, st);
+      }
+    } else if (n2v && t >= 0 && deg > 0) {
       if (j == 0) st.bytes += 2 * SECTOR;  // t offsets + max_w (§8 d pair term)
       const double env = __dmul_rn(mx >= 0.0 ? mx : __ldg(A.gv.mx + v), A.a.f_max);
       if (A.vrec != nullptr) {
@@ -385,7 +494,15 @@ __global__ void __launch_bounds__(256, MINB) k_walk_persistent(PWArgs A) {
       thi = lo + deg;
       t = v;
       v = o;
-      load_vertex(A, v, lo, deg, mx, tot);
+      if (nh.lo >= 0) {  // header delivered by the selecting record
+        lo = nh.lo;
+        deg = nh.deg;
+        mx = nh.mx;
+        tot = nh.tot;
+        if (n2v && mx < 0.0) mx = __ldg(A.gv.mx + v);  // after node2vec's step-0 pick
+      } else {
+        load_vertex(A, v, lo, deg, mx, tot);
+      }
       st.bytes += SECTOR + 8;
     }
   }
@@ -720,7 +837,7 @@ static int run_chain_walk_sp(const nd_graph* G, const NdApp& a, int64_t sample_l
     ND_CUDA_TRY(cudaMemsetAsync(ctl, 0, 2 * sizeof(int), s));
     PWArgs A{view(g), a, seed, sample_lo, rows, cwid, cv, ct, roots, roots32, R, step0,
              step0 + Lw, Lw, W.out, W.nnz, died, nw, nv, nt, ctl + 1, ctl, ctl + 2, ctl + 3, ctr,
-             g.vrec, g.ecw, g.epc};
+             g.vrec, g.ecw, g.epc, g.nbw, g.nbp, g.nbu};
     int64_t grid = (int64_t)nsm * occ;
     const int64_t need = (rows + 255) / 256;
     if (grid > need) grid = need;
@@ -971,7 +1088,7 @@ extern "C" int nd_run_walk(const nd_graph* g, int app_code, const double* host_p
   ND_TRY(nd_graph_ensure_index(const_cast<nd_graph*>(g), app_code == ND_NODE2VEC,
                                app_code != ND_MULTIRW, s));
   if (app_code != ND_MULTIRW && paradigm == ND_SP)
-    ND_TRY(nd_graph_ensure_records(const_cast<nd_graph*>(g), s));
+    ND_TRY(nd_graph_ensure_records(const_cast<nd_graph*>(g), app_code == ND_NODE2VEC, s));
   nd_result* res = new nd_result();
   res->stream = s;
   int rc;
