@@ -40,6 +40,18 @@ extern "C" int nd_version(void) { return 1; }
 // Keep stream-ordered allocations cached in the device pool between runs
 // (the default release threshold of 0 returns memory to the OS at every
 // synchronisation, which costs milliseconds per multi-GB run).
+// bytes the sampler keeps mapped in the stream-ordered pool
+size_t nd_pool_reserve_bytes(size_t free_bytes) {
+  static size_t cached = 0;
+  if (cached) return cached;
+  double gb = 32.0;
+  if (const char* e = getenv("ND_POOL_RESERVE_GB")) gb = atof(e);
+  size_t want = (size_t)(gb * (1ull << 30));
+  if (free_bytes && want > free_bytes / 3) want = free_bytes / 3;
+  cached = want;
+  return want;
+}
+
 int nd_pool_init() {
   static thread_local int done_dev = -1;
   int dev = 0;
@@ -56,10 +68,7 @@ int nd_pool_init() {
   // ND_POOL_RESERVE_GB overrides (0 disables).
   size_t fr = 0, tot = 0;
   cudaMemGetInfo(&fr, &tot);
-  double gb = 32.0;
-  if (const char* e = getenv("ND_POOL_RESERVE_GB")) gb = atof(e);
-  size_t want = (size_t)(gb * (1ull << 30));
-  if (want > fr / 3) want = fr / 3;
+  size_t want = nd_pool_reserve_bytes(fr);
   if (want >= (1ull << 30)) {
     void* p = nullptr;
     if (cudaMallocAsync(&p, want, 0) == cudaSuccess) {
@@ -502,13 +511,14 @@ static int build_from_edges_dev(const int64_t* src, const int64_t* dst, const do
   nd_free(k0, s); nd_free(k1, s); nd_free(i0, s); nd_free(i1, s);
   nd_free(bad, s); nd_free(wtmp, s); nd_free(tmp, s);
   cudaStreamSynchronize(s);
-  // the build's sort buffers (~32 B/edge) go back to the OS: the resident graph
-  // and the sampler's own working set are what the pool should keep
+  // the build's sort buffers (~32 B/edge) go back to the OS down to the
+  // sampler's reserve, which stays mapped for the runs that follow
   {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess)
+      cudaMemPoolTrimTo(pool, nd_pool_reserve_bytes(0));
   }
   if (rc != ND_OK) {
     nd_graph_destroy(G);
