@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(IND_BLOCK) k_ind_group(IndCtx c, const uint32_
     const int64_t v = keys[gs];
     const int64_t lo = __ldg(g.row + v), deg = __ldg(g.row + v + 1) - lo;
     const int64_t items = (int64_t)(me - ms) * c.m;
-    if (deg > 0 && deg <= sp.cap) {
+    if (deg > 0 && deg <= sp.cap && 4 * items >= deg) {
       const SRow r = stage_row(g, lo, deg, sp, smem);
       for (int64_t j = threadIdx.x; j < items; j += blockDim.x) {
         const int64_t q = ms + j / c.m, slot = j - (j / c.m) * c.m;

@@ -218,7 +218,9 @@ __global__ void __launch_bounds__(TP_BLOCK) k_medium(const uint32_t* __restrict_
     const int start = gstart[gi], size = gstart[gi + 1] - start;
     const int64_t v = keys[start];
     const int64_t lo = __ldg(g.row + v), deg = __ldg(g.row + v + 1) - lo;
-    if (deg <= sp.cap && deg > 0) {
+    // stage only when the members re-read a fair share of the row (each
+    // member touches ~1-2 entries); otherwise the copy costs more than it saves
+    if (deg <= sp.cap && deg > 0 && 4 * (int64_t)size >= deg) {
       SRow r = stage_row(g, lo, deg, sp, smem);
       for (int k = threadIdx.x; k < size; k += blockDim.x) {
         st.bytes += SECTOR + 8;
@@ -254,7 +256,7 @@ __global__ void __launch_bounds__(TP_BLOCK) k_large(const uint32_t* __restrict__
     const int end = min(ge, start + LARGE_CHUNK);
     const int64_t v = keys[gs];
     const int64_t lo = __ldg(g.row + v), deg = __ldg(g.row + v + 1) - lo;
-    if (deg <= sp.cap && deg > 0) {
+    if (deg <= sp.cap && deg > 0 && 4 * (int64_t)(end - start) >= deg) {
       SRow r = stage_row(g, lo, deg, sp, smem);
       for (int k = start + threadIdx.x; k < end; k += blockDim.x) {
         st.bytes += SECTOR + 8;
