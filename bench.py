@@ -28,7 +28,6 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -57,51 +56,87 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """SM clocks and clock-event (throttle) reasons sampled through NVML every
+    ~5 ms from a background thread while the timed region runs (the timed
+    region is ~0.1-0.2 s, shorter than nvidia-smi's start-up, so the CLI's
+    `-lms` loop would see none of it).  The GPU is matched by UUID."""
 
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+               ("hw_power_brake", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
 
-    def __init__(self, index=0):
+    def __init__(self, index=0, period_s=0.005):
         self.index = index
-        self.proc = None
+        self.period = period_s
+        self.samples = []
+        self.max_mhz = None
+        self.error = None
+        self._stop = threading.Event()
+        self._thr = None
+        self._nv = None
+        self._h = None
+        try:
+            import pynvml as nv
+            import torch
+            nv.nvmlInit()
+            self._nv = nv
+            h = None
+            try:
+                uuid = str(torch.cuda.get_device_properties(index).uuid)
+                for i in range(nv.nvmlDeviceGetCount()):
+                    hh = nv.nvmlDeviceGetHandleByIndex(i)
+                    u = nv.nvmlDeviceGetUUID(hh)
+                    u = u.decode() if isinstance(u, bytes) else u
+                    if u.replace("GPU-", "") == uuid.replace("GPU-", ""):
+                        h = hh
+                        break
+            except Exception:
+                h = None
+            self._h = h if h is not None else nv.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(self._h, nv.NVML_CLOCK_SM))
+        except Exception as e:  # no NVML: the line says so
+            self.error = f"nvml unavailable: {e}"
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                mhz = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                self.samples.append((float(mhz), int(rs)))
+            except Exception as e:
+                self.error = str(e)
+                return
+            time.sleep(self.period)
 
     def __enter__(self):
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "250"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-        except Exception:
-            self.proc = None
+        if self._h is not None:
+            self._stop.clear()
+            self._thr = threading.Thread(target=self._run, daemon=True)
+            self._thr.start()
         return self
 
     def __exit__(self, *a):
-        self.lines = []
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                out, _ = self.proc.communicate(timeout=5)
-            except Exception:
-                out = ""
-            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+        if self._thr is not None:
+            self._stop.set()
+            self._thr.join(timeout=2)
+            self._thr = None
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in getattr(self, "lines", []):
-            parts = [p.strip() for p in ln.split(",")]
-            try:
-                sm.append(float(parts[0]))
-                mx = float(parts[1])
-                for nm, v in zip(names, parts[2:]):
-                    if v.lower().startswith("active"):
-                        reasons.add(nm)
-            except (ValueError, IndexError):
-                continue
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        reasons = set()
+        if self._nv is not None:
+            for name, attr in self.REASONS:
+                bit = getattr(self._nv, attr, 0)
+                if any(r & bit for _, r in self.samples):
+                    reasons.add(name)
+        sm = [m for m, _ in self.samples]
+        out = {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.max_mhz,
+               "reasons": sorted(reasons), "samples": len(sm), "source": "nvml"}
+        if self.error:
+            out["error"] = self.error
+        return out
 
 
 def dist_env():
@@ -174,13 +209,14 @@ def run_reference(args):
     return 0
 
 
-def config_dict(n_gpus, note=None):
+def config_dict(n_gpus, note=None, concurrent=True):
     c = {"workload": "C2: RMAT scale 22 (4,194,304 V, 68,993,773 directed weighted E), "
                      "node2vec p=2 q=0.5 len 100 + PPR term 0.01, one walk per vertex",
          "graph": "keyed RMAT a=.57 b=.19 c=.19, weights U[1,5), seed 0, built on device",
          "walkers_per_step": 2 * (1 << SCALE), "seed": SEED,
          "parallelism": f"sample-sharded x{n_gpus}, graph replicated",
-         "l2": "inputs (1.45 GB CSR) larger than L2", "paradigm": "sp (walker-major)"}
+         "l2": "inputs (1.45 GB CSR) larger than L2", "paradigm": "sp (walker-major)",
+         "apps": "node2vec and PPR concurrently on two streams" if concurrent else "node2vec then PPR"}
     if note:
         c["note"] = note
     return c
@@ -195,6 +231,10 @@ def main():
     ap.add_argument("--paradigm", default="sp", choices=["sp", "tp"])
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-tp", action="store_true")
+    ap.add_argument("--serial-apps", action="store_true",
+                    help="run node2vec then PPR instead of concurrently on two streams")
+    ap.add_argument("--e2e-chunks", type=int, default=2,
+                    help="sample-id chunks of the host pipeline (D2H of chunk c overlaps chunk c+1)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -211,7 +251,7 @@ def main():
         else:
             dist.init_process_group(backend)
     from paper_2009_06693_b200 import _lib, make_app
-    from paper_2009_06693_b200.engine import run_device
+    from paper_2009_06693_b200.engine import run_device, run_device_concurrent
     from paper_2009_06693_b200.graph import DeviceGraph
     from paper_2009_06693_b200.sharding import worker_ranges
 
@@ -249,14 +289,16 @@ def main():
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record(stream)
         step_edges, step_bytes, step_sample = 0, 0, 0.0
-        runs = []
-        for app in apps:
-            dr = run_device(app, dg, n_samples=n, sample_lo=lo, seed=SEED, paradigm=args.paradigm,
-                            sync=False)
+        if args.serial_apps:
+            runs = [run_device(app, dg, n_samples=n, sample_lo=lo, seed=SEED, paradigm=args.paradigm,
+                               sync=False) for app in apps]
+        else:  # node2vec and PPR concurrently (PPR's long-walk tail overlaps node2vec)
+            runs = run_device_concurrent([dict(app=app, n_samples=n, sample_lo=lo, seed=SEED)
+                                          for app in apps], dg, paradigm=args.paradigm)
+        for dr in runs:
             step_edges += dr.total_sampled
             step_bytes += dr.counters["slot_bytes"]
             step_sample += dr.profile_ms[1]
-            runs.append(dr)
         if ws > 1:
             for dr in runs:
                 gather_rows(dr.view(_lib.F_FINAL_OFF), dr.view(_lib.F_FINAL_IDS))
@@ -307,50 +349,35 @@ def main():
                    "note": "TP = per-step radix sort + work classes + sub-warp/CTA/grid kernels"}
 
     # ---- e2e through the public API with host buffers ------------------------------
+    # HostPipeline (paper_2009_06693_b200/streaming.py): roots uploaded from
+    # pinned host memory per chunk, final rows (int64 offsets + int32 ids)
+    # copied back into pinned host buffers while the next chunk samples.
     L.nd_set_profiling(0)
     from oracle import oracle as O  # noqa: F401  (roots on host: the reference's keyed rule)
-    from paper_2009_06693_b200.engine import SampleRange
+    from paper_2009_06693_b200.streaming import HostPipeline
     roots_host = torch.from_numpy(O.uniform_roots(V, 1, SEED, lo, n).reshape(-1)).pin_memory()
     e2e_times, e2e_edges, h2d, d2h = [], 0, 0, 0
-    copy_stream = torch.cuda.Stream()
-    pinned = {}  # caller-owned pinned result buffers, sized on the first (warm-up) step
-
-    def host_buf(key, numel):
-        b = pinned.get(key)
-        if b is None or b.numel() < numel:
-            b = torch.empty(numel, dtype=torch.int64, pin_memory=True)
-            pinned[key] = b
-        return b[:numel]
-
+    e2e_ok = True
+    pipe = HostPipeline(chunks=args.e2e_chunks)
+    jobs = [(app, n, SEED, lo, roots_host) for app in apps]
     for it in range(max(1, args.warmup // 2) + args.steps):
         barrier()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record(stream)
-        step_edges, step_h2d, step_d2h = 0, 0, 0
-        held = []
-        for app in apps:
-            droots = roots_host.to("cuda", non_blocking=True)
-            step_h2d += roots_host.numel() * 8
-            dr = _run_with_roots(run_device, app, dg, droots, lo, n)
-            off = dr.view(_lib.F_FINAL_OFF)
-            ids = dr.view(_lib.F_FINAL_IDS)
-            # D2H of this app's rows on a copy stream, overlapping the next app
-            done = torch.cuda.Event()
-            done.record(stream)
-            copy_stream.wait_event(done)
-            h_off = host_buf((app.name, "off"), off.numel())
-            h_ids = host_buf((app.name, "ids"), ids.numel())
-            with torch.cuda.stream(copy_stream):
-                h_off.copy_(off, non_blocking=True)
-                h_ids.copy_(ids, non_blocking=True)
-            step_d2h += (off.numel() + ids.numel()) * 8
-            step_edges += dr.total_sampled
-            held.append((dr, h_off, h_ids))
-        stream.wait_stream(copy_stream)
+        res = pipe.run_jobs(dg, jobs)
         ev1.record(stream)
         torch.cuda.synchronize()
-        for dr, _, _ in held:
-            dr.close()
+        step_edges = sum(c.total_sampled for chunks in res for c in chunks)
+        step_h2d = roots_host.numel() * roots_host.element_size() * len(apps)
+        step_d2h = sum(c.offsets.numel() * c.offsets.element_size() + c.ids.numel() * c.ids.element_size()
+                       for chunks in res for c in chunks)
+        if it == 0:  # host rows == device rows of a plain run (checksums, outside the timed steps)
+            for app, chunks in zip(apps, res):
+                dr = run_device(app, dg, n_samples=n, sample_lo=lo, seed=SEED, paradigm=args.paradigm)
+                ref_ids = dr.view(_lib.F_FINAL_IDS)
+                e2e_ok &= bool(sum(int(c.ids.sum()) for c in chunks) == int(ref_ids.sum().item()))
+                e2e_ok &= bool(sum(c.ids.numel() for c in chunks) == ref_ids.numel())
+                dr.close()
         if it >= max(1, args.warmup // 2):
             e2e_times.append(ev0.elapsed_time(ev1))
             e2e_edges += step_edges
@@ -410,9 +437,12 @@ def main():
             "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "int64+f64", "data": "synthetic", "config": config_dict(ws),
+            "dtype": "int64+f64", "data": "synthetic",
+            "config": config_dict(ws, concurrent=not args.serial_apps),
             "e2e": {"value": e2e_value, "unit": "edges/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h},
+                    "d2h_bytes_per_step": d2h, "host_rows_match_device": e2e_ok,
+                    "result": "final rows: int64 offsets + int32 vertex ids, pinned host",
+                    "chunks": args.e2e_chunks},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                          "kernel": "k_walk_persistent" if args.paradigm == "sp" else "TP class kernels",
@@ -428,21 +458,6 @@ def main():
     if ws > 1:
         dist.destroy_process_group()
     return 0
-
-
-def _run_with_roots(run_device, app, dg, droots, lo, n):
-    """Public-API run with caller-provided (uploaded) roots."""
-    import ctypes as C
-    from paper_2009_06693_b200 import _lib
-    from paper_2009_06693_b200.engine import DeviceRun, describe
-    L = _lib.load()
-    plan = describe(app)
-    kp = np.ascontiguousarray(plan.kparams, dtype=np.float64)
-    h = C.c_void_p()
-    _lib.check(L.nd_run_walk(dg.handle, plan.code, _lib.ptr(kp), len(kp), lo, n, _lib.ptr(droots), 1,
-                             C.c_uint64(SEED), plan.steps, 10_000, _lib.ND_SP, _lib.stream_ptr(),
-                             C.byref(h)), "nd_run_walk")
-    return DeviceRun(h, plan, dg, "sp", lo, 0.0)
 
 
 if __name__ == "__main__":

@@ -191,6 +191,7 @@ int nd_transit_schedule(const int64_t *pair_transit, int64_t n_pairs, int64_t m,
 #define ND_F_REC_V 9       /* int64 recorded edge targets                  */
 #define ND_F_STATS 10      /* int64 [S*4] {small, medium, large, fetches}  */
 #define ND_F_CHAIN_VALS 11 /* int64 walk chains incl. NULL (multirw)       */
+#define ND_F_FINAL_IDS32 12 /* int32 [total] FINAL_IDS narrowed (nd_result_narrow_ids) */
 int nd_result_info(const nd_result *r, int64_t *n_samples, int64_t *n_steps,
                    int64_t *total_sampled, int64_t *total_recorded);
 /* device pointer + element count of one field (ptr NULL if absent) */
@@ -198,6 +199,10 @@ int nd_result_field(const nd_result *r, int field, const void **ptr, int64_t *co
 /* counters for the roofline byte model: {items, pairs, n2v_tries,
  * n2v_probe_sectors, search_sectors} */
 int nd_result_counters(const nd_result *r, int64_t *host_counters, int64_t n);
+/* Fill ND_F_FINAL_IDS32: the final ids as int32 (vertex ids < 2^31, the
+ * device CSR's column width), halving the device->host bytes of a result
+ * read.  Idempotent; enqueued on `stream`. */
+int nd_result_narrow_ids(nd_result *r, void *stream);
 /* copy a field into caller memory (host or device; cudaMemcpyDefault) on
  * `stream`; synchronous when stream is NULL */
 int nd_result_copy(const nd_result *r, int field, void *dst, void *stream);

@@ -87,8 +87,8 @@ __device__ __forceinline__ uint64_t mod_u64(uint64_t u, uint64_t d) {
 //           guide[j] = upper_bound(prefix row, j*(total/deg)) (rows with
 //           deg > GUIDE_MIN_DEG); narrows the inverse-CDF search to ~3 entries.
 // Both return exactly what the reference's binary searches return.
-constexpr int64_t HASH_MIN_DEG = 32;
-constexpr int64_t GUIDE_MIN_DEG = 16;
+constexpr int64_t HASH_MIN_DEG = 0;  // every non-empty row (the table space is allocated anyway)
+constexpr int64_t GUIDE_MIN_DEG = 4;
 
 // Packed records for the walker-major kernels: the fields one step reads
 // together share one 32-byte sector.

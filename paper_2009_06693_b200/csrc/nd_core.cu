@@ -9,6 +9,7 @@
 
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 
 #include "nd_item.cuh"
@@ -53,11 +54,14 @@ size_t nd_pool_reserve_bytes(size_t free_bytes) {
 }
 
 int nd_pool_init() {
-  static thread_local int done_dev = -1;
+  // once per device per process (concurrent runs come from several host threads)
+  static std::mutex mu;
+  static bool done[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
-  if (done_dev == dev) return ND_OK;
-  done_dev = dev;
+  std::lock_guard<std::mutex> lock(mu);
+  if (dev < 0 || dev >= 64 || done[dev]) return ND_OK;
+  done[dev] = true;
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return ND_OK;
   uint64_t thr = ~0ull;
@@ -700,8 +704,33 @@ extern "C" int nd_result_copy(const nd_result* r, int field, void* dst, void* st
   if (!r || field < 0 || field >= ND_N_FIELDS) return ND_ERR_ARG;
   if (!r->ptr[field] || !r->cnt[field]) return ND_OK;
   cudaStream_t s = (cudaStream_t)stream;
-  ND_CUDA_TRY(cudaMemcpyAsync(dst, r->ptr[field], r->cnt[field] * sizeof(int64_t), cudaMemcpyDefault, s));
+  ND_CUDA_TRY(cudaMemcpyAsync(dst, r->ptr[field], r->cnt[field] * r->esz[field], cudaMemcpyDefault, s));
   if (!stream) ND_CUDA_TRY(cudaStreamSynchronize(s));
+  return ND_OK;
+}
+
+// int64 -> int32 ids: 16-byte loads, 8-byte stores, grid-stride over pairs
+__global__ void k_narrow_ids(const int64_t* __restrict__ in, int64_t n, int32_t* __restrict__ out) {
+  const int64_t half = n >> 1;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < half; i += stride) {
+    const longlong2 x = __ldcs(reinterpret_cast<const longlong2*>(in) + i);
+    __stcs(reinterpret_cast<int2*>(out) + i, make_int2((int32_t)x.x, (int32_t)x.y));
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) out[n - 1] = (int32_t)in[n - 1];
+}
+
+extern "C" int nd_result_narrow_ids(nd_result* r, void* stream) {
+  if (!r) return ND_ERR_ARG;
+  if (r->ptr[ND_F_FINAL_IDS32] || !r->ptr[ND_F_FINAL_IDS]) return ND_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t n = r->cnt[ND_F_FINAL_IDS];
+  int32_t* out = nullptr;
+  ND_CUDA_TRY(nd_alloc(&out, n > 0 ? n : 1, s));
+  if (n) k_narrow_ids<<<nd_grid((n + 1) / 2, 256, 148 * 16), 256, 0, s>>>(
+      static_cast<const int64_t*>(r->ptr[ND_F_FINAL_IDS]), n, out);
+  ND_CUDA_TRY(cudaGetLastError());
+  r->set(ND_F_FINAL_IDS32, out, n);
   return ND_OK;
 }
 

@@ -7,6 +7,7 @@
 // Built once per graph on first use; answers are identical to the binary
 // searches they replace (tests/test_gpu_kernels.py::test_index_equivalence).
 #include <cstdlib>
+#include <mutex>
 
 #include "nd_internal.h"
 
@@ -112,9 +113,13 @@ __global__ void k_build_nbr(const int64_t* __restrict__ row, const int32_t* __re
 
 }  // namespace
 
+// lazy index builds may be requested by concurrent runs on one graph
+static std::mutex g_index_mu;
+
 int nd_graph_ensure_records(nd_graph* G, int want_tries, cudaStream_t s) {
   static const bool disabled = getenv("ND_NO_PACK") && getenv("ND_NO_PACK")[0] == '1';
   if (disabled) return ND_OK;
+  std::lock_guard<std::mutex> lock(g_index_mu);
   const int64_t V = G->g.V, E = G->g.E;
   if (!G->vrec && V > 0) {
     ND_CUDA_TRY(cudaMalloc(&G->vrec, V * sizeof(VRec)));
@@ -150,9 +155,11 @@ int nd_graph_ensure_records(nd_graph* G, int want_tries, cudaStream_t s) {
 int nd_graph_ensure_index(nd_graph* G, int want_hset, int want_guide, cudaStream_t s) {
   static const bool disabled = getenv("ND_NO_INDEX") && getenv("ND_NO_INDEX")[0] == '1';
   if (disabled) return ND_OK;
+  std::lock_guard<std::mutex> lock(g_index_mu);
   const int64_t V = G->g.V, E = G->g.E;
   if (want_guide && !G->guide && !G->g.unit && E > 0) {
-    ND_CUDA_TRY(cudaMalloc(&G->guide, E * sizeof(int32_t)));
+    // +8 entries: the walker kernels read guide entries as aligned 32-byte chunks
+    ND_CUDA_TRY(cudaMalloc(&G->guide, (E + 8) * sizeof(int32_t)));
     G->bytes += E * 4;
     k_build_guide<<<148 * 16, 256, 0, s>>>(G->row, G->pre, V, G->guide);
     ND_CUDA_TRY(cudaGetLastError());
@@ -160,9 +167,10 @@ int nd_graph_ensure_index(nd_graph* G, int want_hset, int want_guide, cudaStream
     G->g.guide = G->guide;
   }
   if (want_hset && !G->hset && E > 0) {
-    ND_CUDA_TRY(cudaMalloc(&G->hset, 4 * E * sizeof(int32_t)));
+    // +8 slots: the walker kernels read the tables as aligned 32-byte chunks
+    ND_CUDA_TRY(cudaMalloc(&G->hset, (4 * E + 8) * sizeof(int32_t)));
     G->bytes += 16 * E;
-    ND_CUDA_TRY(cudaMemsetAsync(G->hset, 0xFF, 4 * E * sizeof(int32_t), s));
+    ND_CUDA_TRY(cudaMemsetAsync(G->hset, 0xFF, (4 * E + 8) * sizeof(int32_t), s));
     k_build_hset<<<148 * 16, 256, 0, s>>>(G->row, G->col, V, G->hset);
     ND_CUDA_TRY(cudaGetLastError());
     ND_CUDA_TRY(cudaStreamSynchronize(s));

@@ -147,6 +147,27 @@ __device__ __forceinline__ bool has_edge(const ColT* __restrict__ a, int64_t lo,
   return lo < end && (int64_t)__ldg(a + lo) == t;
 }
 
+// node2vec acceptance of one try (_ckernels.pyx:249-261):
+//   factor = f_ret if nbr == t, f_adj if nbr in adj(t), else f_far;
+//   accept iff env <= 0 or r*env < w*factor   (two rounded products, no FMA)
+// For nbr != t the membership test only matters when r*env falls between
+// w*f_adj and w*f_far: rounding is monotone, so r*env below both products
+// accepts and r*env at or above both rejects whatever has_edge(t, nbr) says.
+// `member()` (the probe into t's row) runs only in the band; `probed` reports
+// it for the byte model.
+template <class Member>
+__device__ __forceinline__ bool n2v_accept(const NdApp& a, int64_t nb, int64_t t, double w,
+                                           double u01, double env, Member member, bool& probed) {
+  if (env <= 0.0) return true;
+  const double lhs = __dmul_rn(u01, env);
+  if (nb == t) return lhs < __dmul_rn(w, a.f_ret);
+  const double pa = __dmul_rn(w, a.f_adj), pf = __dmul_rn(w, a.f_far);
+  if (lhs < pa && lhs < pf) return true;
+  if (!(lhs < pa) && !(lhs < pf)) return false;
+  probed = true;
+  return lhs < (member() ? pa : pf);
+}
+
 // ceil(log2(ceil(deg/4))): binary-search sectors over 8-byte entries (SURVEY §8 d)
 __device__ __forceinline__ int search_sectors(int64_t deg) {
   int64_t s = (deg + 3) >> 2;
@@ -203,15 +224,17 @@ __device__ __forceinline__ int64_t run_item(const GView<ColT>& g, const RowT& r,
         int64_t nb;
         double w;
         r.cw(k, nb, w, g.unit);
-        double f;
         st.tries++;
-        st.bytes += 2 * SECTOR + probe;
-        if (nb == t) f = a.f_ret;
-        else if (g.hset != nullptr && t_hi - t_lo > HASH_MIN_DEG)
-          f = hset_contains(g.hset + 4 * t_lo, hset_size(t_hi - t_lo), (int32_t)nb) ? a.f_adj : a.f_far;
-        else f = has_edge(g.col, t_lo, t_hi, nb) ? a.f_adj : a.f_far;
+        st.bytes += 2 * SECTOR;
         const double u01 = to_unit(draw_u64(b + C_DRAW, ik));
-        if (env <= 0.0 || __dmul_rn(u01, env) < __dmul_rn(w, f)) return nb;
+        bool probed = false;
+        const bool acc = n2v_accept(a, nb, t, w, u01, env, [&] {
+          if (g.hset != nullptr && t_hi - t_lo > HASH_MIN_DEG)
+            return hset_contains(g.hset + 4 * t_lo, hset_size(t_hi - t_lo), (int32_t)nb);
+          return has_edge(g.col, t_lo, t_hi, nb);
+        }, probed);
+        if (probed) st.bytes += probe;
+        if (acc) return nb;
         b += 2 * C_DRAW;
       }
       *stall = 1;

@@ -267,15 +267,21 @@ class DeviceRun:
         _lib.check(_lib.load().nd_result_field(self._h, f, C.byref(p), C.byref(c)))
         return p.value, c.value
 
+    def narrow_ids(self, stream=None):
+        """Produce F_FINAL_IDS32 (int32 final ids) on device; returns its view."""
+        _lib.check(_lib.load().nd_result_narrow_ids(
+            self._h, _lib.stream_ptr() if stream is None else stream), "nd_result_narrow_ids")
+        return self.view(_lib.F_FINAL_IDS32)
+
     def view(self, f):
         p, c = self.field_count(f)
-        return None if not p else device_view(p, c, "int64", self)
+        return None if not p else device_view(p, c, _lib.FIELD_DTYPE.get(f, "int64"), self)
 
     def host(self, f):
         p, c = self.field_count(f)
         if not p:
             return None
-        out = np.empty(c, dtype=np.int64)
+        out = np.empty(c, dtype=np.dtype(_lib.FIELD_DTYPE.get(f, "int64")))
         _lib.check(_lib.load().nd_result_copy(self._h, f, _lib.ptr(out), None))
         return out
 
@@ -415,6 +421,58 @@ def run_device(app, graph, samples=None, *, seed: int = 0, paradigm: str = "tp",
     if sync:
         torch.cuda.synchronize()
     return DeviceRun(h, plan, dg, paradigm, lo, time.perf_counter() - t0)
+
+
+_JOB_STREAMS = []
+_JOB_POOL = None
+
+
+def job_streams(k: int):
+    """k cached side streams (one per concurrent job)."""
+    import torch
+    while len(_JOB_STREAMS) < k:
+        _JOB_STREAMS.append(torch.cuda.Stream())
+    return _JOB_STREAMS[:k]
+
+
+def _job_pool(k: int):
+    """Persistent host threads for concurrent jobs (one per job)."""
+    import concurrent.futures as cf
+    global _JOB_POOL
+    if _JOB_POOL is None or _JOB_POOL._max_workers < k:
+        _JOB_POOL = cf.ThreadPoolExecutor(max(4, k), thread_name_prefix="nd-job")
+    return _JOB_POOL
+
+
+def run_device_concurrent(jobs, graph, *, paradigm: str = "sp",
+                          step_cap: int = DEFAULT_STEP_CAP) -> list:
+    """Several whole sampling jobs at once, each on its own stream and host
+    thread (the C-ABI call releases the GIL): a job = dict(app=..., n_samples=...,
+    sample_lo=0, seed=0).  A job whose tail leaves the GPU idle (a few long
+    PPR walks) overlaps the others' bulk.  Outputs are exactly those of
+    separate run_device calls.  The caller's current stream is ordered after
+    every job; returns the DeviceRuns in job order."""
+    import torch
+    _lib.require_cuda()
+    dg = as_device_graph(graph)
+    cur = torch.cuda.current_stream()
+    dev = torch.cuda.current_device()
+    streams = job_streams(len(jobs))
+    for st in streams:
+        st.wait_stream(cur)
+
+    def one(job, st):
+        torch.cuda.set_device(dev)
+        with torch.cuda.stream(st):
+            return run_device(job["app"], dg, n_samples=job["n_samples"],
+                              sample_lo=job.get("sample_lo", 0), seed=job.get("seed", 0),
+                              paradigm=paradigm, step_cap=step_cap, stream=st, sync=False)
+
+    runs = [f.result() for f in [_job_pool(len(jobs)).submit(one, j, st)
+                                  for j, st in zip(jobs, streams)]]
+    for st in streams:
+        cur.wait_stream(st)
+    return runs
 
 
 def _run(app, graph, samples, config, paradigm) -> SampleSetOutput:

@@ -1,0 +1,149 @@
+"""Host-streaming runs: sample rows delivered to pinned host memory while the
+device samples the next chunk.
+
+The reference hands a finished ``SampleSetOutput`` back to the caller
+(``tp_run``/``sp_run``, transit_parallel.py:249-257; the CLI then renders it,
+cli.py:95-137).  On B200 the device samples several times faster than PCIe
+can carry the rows back, so a run to host memory is split into contiguous
+sample-id chunks (the keyed RNG makes any split produce identical rows,
+driver.py:175-186): while chunk c+1 runs on the compute stream, chunk c's
+final rows (int64 offsets + int32 vertex ids) are copied device->host on a
+copy stream into caller-owned pinned buffers.  Only the last chunk's copy is
+exposed.
+
+    pipe = HostPipeline(chunks=4)
+    out = pipe.run(app, device_graph, n_samples=N, seed=7)   # list[HostChunk]
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .engine import DeviceRun, describe, run_device
+from .graph import as_device_graph
+from .sharding import worker_ranges
+
+
+@dataclass
+class HostChunk:
+    """Final rows of samples [sample_lo, sample_lo + n) in pinned host memory."""
+    sample_lo: int
+    n: int
+    offsets: "object"        # torch int64 [n+1], chunk-local row offsets
+    ids: "object"            # torch int32 [offsets[n]]: roots, then sampled vertices
+    total_sampled: int
+
+    def rows(self):
+        off = self.offsets.numpy()
+        ids = self.ids.numpy()
+        return [ids[off[i]:off[i + 1]] for i in range(self.n)]
+
+
+class HostPipeline:
+    """Chunked device run with overlapped device->host row copies.  Pinned
+    buffers are owned by the pipeline and reused across runs (sized on first
+    use), so steady-state runs allocate no host memory."""
+
+    def __init__(self, chunks: int = 4, paradigm: str = "sp", step_cap: int = 10_000):
+        self.chunks = max(1, int(chunks))
+        self.paradigm = paradigm
+        self.step_cap = step_cap
+        self._pinned = {}
+        self._copy_streams = []
+
+    def _buf(self, key, like):
+        import torch
+        b = self._pinned.get(key)
+        if b is None or b.numel() < like.numel() or b.dtype != like.dtype:
+            b = torch.empty(max(like.numel(), 1), dtype=like.dtype, pin_memory=True)
+            self._pinned[key] = b
+        return b[:like.numel()]
+
+    def run(self, app, graph, n_samples: int, seed: int = 0, sample_lo: int = 0,
+            roots_host=None) -> list:
+        """Run `app` for samples [sample_lo, sample_lo + n_samples).  `roots_host`
+        (optional pinned int64 [n_samples * R]) replaces the keyed default roots;
+        each chunk's slice is uploaded before the chunk runs.  Returns one
+        HostChunk per chunk, valid until the next run of this pipeline."""
+        return self.run_jobs(graph, [(app, n_samples, seed, sample_lo, roots_host)])[0]
+
+    def run_jobs(self, graph, jobs) -> list:
+        """Several apps at once through one pipeline: job = (app, n_samples,
+        seed, sample_lo, roots_host).  Each job runs on its own compute stream
+        and host thread (engine.run_device_concurrent's scheme) with its own
+        copy stream, so one job's copies and tail overlap the others' bulk;
+        one synchronisation at the end.  Returns one HostChunk list per job."""
+        import torch
+        from .engine import _job_pool, job_streams
+        dg = as_device_graph(graph)
+        k = len(jobs)
+        while len(self._copy_streams) < k:
+            self._copy_streams.append(torch.cuda.Stream())
+        cur = torch.cuda.current_stream()
+        dev = torch.cuda.current_device()
+        streams = job_streams(k)
+        for st in streams:
+            st.wait_stream(cur)
+
+        def one(ji, job, st, cs):
+            app, n_samples, seed, sample_lo, roots_host = job
+            torch.cuda.set_device(dev)
+            plan = describe(app)
+            parts = [(lo, hi) for lo, hi in worker_ranges(n_samples, self.chunks) if hi > lo]
+            out, held = [], []
+            with torch.cuda.stream(st):
+                for ci, (lo, hi) in enumerate(parts):
+                    n = hi - lo
+                    if roots_host is not None:
+                        R = len(roots_host) // max(n_samples, 1)
+                        droots = roots_host[lo * R:hi * R].to("cuda", non_blocking=True)
+                        held.append(droots)
+                        dr = _run_walk_with_roots(plan, dg, droots, R, sample_lo + lo, n, seed,
+                                                  self.paradigm, self.step_cap)
+                    else:
+                        dr = run_device(app, dg, n_samples=n, sample_lo=sample_lo + lo, seed=seed,
+                                        paradigm=self.paradigm, step_cap=self.step_cap, stream=st,
+                                        sync=False)
+                    off = dr.view(_lib.F_FINAL_OFF)
+                    ids = dr.narrow_ids(stream=_lib.stream_ptr(st))
+                    ready = torch.cuda.Event()
+                    ready.record(st)
+                    cs.wait_event(ready)
+                    h_off = self._buf((ji, ci, "off"), off)
+                    h_ids = self._buf((ji, ci, "ids"), ids)
+                    with torch.cuda.stream(cs):
+                        h_off.copy_(off, non_blocking=True)
+                        h_ids.copy_(ids, non_blocking=True)
+                    held.append(dr)
+                    out.append(HostChunk(sample_lo + lo, n, h_off, h_ids, dr.total_sampled))
+            return out, held
+
+        futs = [_job_pool(k).submit(one, ji, job, st, cs)
+                for ji, (job, st, cs) in enumerate(zip(jobs, streams, self._copy_streams))]
+        done = [f.result() for f in futs]
+        for cs in self._copy_streams[:k]:
+            cur.wait_stream(cs)
+        cur.synchronize()
+        for _, held in done:
+            for h in held:
+                if isinstance(h, DeviceRun):
+                    h.close()
+        return [out for out, _ in done]
+
+
+def _run_walk_with_roots(plan, dg, droots, R, lo, n, seed, paradigm, step_cap) -> DeviceRun:
+    """nd_run_walk with caller-uploaded roots (device int64 [n * R])."""
+    import ctypes as C
+    if plan.kind != "walk":
+        raise ValueError("explicit roots are supported for walk apps in the host pipeline")
+    L = _lib.load()
+    kp = np.ascontiguousarray(plan.kparams, dtype=np.float64)
+    h = C.c_void_p()
+    par = _lib.ND_TP if paradigm == "tp" else _lib.ND_SP
+    _lib.check(L.nd_run_walk(dg.handle, plan.code, _lib.ptr(kp), len(kp), lo, n, _lib.ptr(droots), R,
+                             C.c_uint64(seed & (2**64 - 1)), plan.steps, step_cap, par,
+                             _lib.stream_ptr(), C.byref(h)), "nd_run_walk")
+    return DeviceRun(h, plan, dg, paradigm, lo, 0.0)

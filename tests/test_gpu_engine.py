@@ -85,7 +85,12 @@ def test_device_rmat_matches_reference_from_edges(key):
 
 @pytest.mark.parametrize("app,params,weighted", [
     ("deepwalk", {}, True), ("deepwalk", {}, False), ("ppr", {}, True),
-    ("node2vec", {}, True), ("node2vec", {}, False), ("multirw", {"roots_per_sample": 8}, False)])
+    ("node2vec", {}, True), ("node2vec", {}, False), ("multirw", {"roots_per_sample": 8}, False),
+    # factor orders that move the membership band (n2v_accept): f_adj > f_far,
+    # the direct convention, and p = q = 1 (empty band: never probed)
+    ("node2vec", {"p": 0.5, "q": 2.0, "walk_length": 40}, True),
+    ("node2vec", {"p": 2.0, "q": 0.5, "factor_convention": "direct", "walk_length": 40}, True),
+    ("node2vec", {"p": 1.0, "q": 1.0, "walk_length": 40}, True)])
 def test_walks_on_rmat_vs_oracle(app, params, weighted):
     """Scale-14 RMAT (skewed degrees, zero-degree vertices, hubs that land in
     the medium/large TP classes): device == multi-threaded oracle, bit for bit,
@@ -336,3 +341,55 @@ def test_cli_output_matches_reference_cli(case, tmp_path):
     rep = dict(line.split("=", 1) for line in open(r).read().splitlines())
     for k, v in case["report"].items():
         assert rep[k] == v, k
+
+
+def test_narrowed_ids_match_int64_rows():
+    """nd_result_narrow_ids: the int32 final ids (the e2e D2H payload) equal the
+    int64 final ids element for element, and host copies of both agree."""
+    import torch
+    from paper_2009_06693_b200 import _lib, make_app
+    from paper_2009_06693_b200.engine import run_device
+    from paper_2009_06693_b200.graph import DeviceGraph
+    dg = DeviceGraph.rmat(12, 16, seed=3, weighted=True)
+    for app in ("node2vec", "ppr", "khop"):
+        dr = run_device(make_app(app), dg, n_samples=3001, seed=4, paradigm="sp")
+        v32 = dr.narrow_ids()
+        assert v32.dtype == torch.int32
+        assert dr.narrow_ids().data_ptr() == v32.data_ptr()  # idempotent
+        ids64 = dr.host(_lib.F_FINAL_IDS)
+        ids32 = dr.host(_lib.F_FINAL_IDS32)
+        assert ids32.dtype == np.int32 and np.array_equal(ids32.astype(np.int64), ids64)
+        assert torch.equal(v32.to(torch.int64), dr.view(_lib.F_FINAL_IDS))
+        dr.close()
+
+
+def test_concurrent_jobs_and_host_pipeline_match_plain_runs():
+    """run_device_concurrent (one stream + host thread per job) and the chunked
+    HostPipeline return exactly the rows of plain sequential runs."""
+    import torch
+    from paper_2009_06693_b200 import _lib, make_app
+    from paper_2009_06693_b200.engine import run_device, run_device_concurrent
+    from paper_2009_06693_b200.graph import DeviceGraph
+    from paper_2009_06693_b200.streaming import HostPipeline
+    dg = DeviceGraph.rmat(13, 16, seed=11, weighted=True)
+    apps = [make_app("node2vec"), make_app("ppr"), make_app("deepwalk")]
+    n, seed = 5000, 3
+    ref = []
+    for a in apps:
+        dr = run_device(a, dg, n_samples=n, sample_lo=17, seed=seed, paradigm="sp")
+        ref.append((dr.host(_lib.F_FINAL_OFF), dr.host(_lib.F_FINAL_IDS)))
+        dr.close()
+    runs = run_device_concurrent([dict(app=a, n_samples=n, sample_lo=17, seed=seed) for a in apps], dg)
+    torch.cuda.synchronize()
+    for dr, (off, ids) in zip(runs, ref):
+        assert np.array_equal(dr.host(_lib.F_FINAL_OFF), off)
+        assert np.array_equal(dr.host(_lib.F_FINAL_IDS), ids)
+        dr.close()
+    for chunks in (1, 3):
+        pipe = HostPipeline(chunks=chunks)
+        res = pipe.run_jobs(dg, [(a, n, seed, 17, None) for a in apps])
+        for parts, (off, ids) in zip(res, ref):
+            got_ids = np.concatenate([c.ids.numpy().astype(np.int64) for c in parts])
+            got_len = np.concatenate([np.diff(c.offsets.numpy()) for c in parts])
+            assert np.array_equal(got_ids, ids) and np.array_equal(got_len, np.diff(off))
+            assert sum(c.n for c in parts) == n and parts[0].sample_lo == 17
