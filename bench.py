@@ -233,8 +233,9 @@ def main():
     ap.add_argument("--no-tp", action="store_true")
     ap.add_argument("--serial-apps", action="store_true",
                     help="run node2vec then PPR instead of concurrently on two streams")
-    ap.add_argument("--e2e-chunks", type=int, default=2,
-                    help="sample-id chunks of the host pipeline (D2H of chunk c overlaps chunk c+1)")
+    ap.add_argument("--e2e-chunks", type=int, default=4,
+                    help="node2vec sample-id chunks of the host pipeline (D2H of chunk c overlaps chunk c+1)")
+    ap.add_argument("--e2e-ppr-chunks", type=int, default=1)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -278,7 +279,7 @@ def main():
 
     # ---- device throughput: inputs resident, CUDA events, max over ranks --------
     L.nd_set_profiling(1)
-    sample_ms, slot_bytes, edges_dev, launches = [], 0, 0, 0
+    sample_ms, slot_bytes, edges_dev, launches, rand_sect = [], 0, 0, 0, 0
     times = []
     clocks = ClockSampler(local)
     for it in range(args.warmup + args.steps):
@@ -288,7 +289,7 @@ def main():
         barrier()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record(stream)
-        step_edges, step_bytes, step_sample = 0, 0, 0.0
+        step_edges, step_bytes, step_sample, step_sect = 0, 0, 0.0, 0
         if args.serial_apps:
             runs = [run_device(app, dg, n_samples=n, sample_lo=lo, seed=SEED, paradigm=args.paradigm,
                                sync=False) for app in apps]
@@ -298,6 +299,7 @@ def main():
         for dr in runs:
             step_edges += dr.total_sampled
             step_bytes += dr.counters["slot_bytes"]
+            step_sect += dr.counters.get("rand_sectors", 0)
             step_sample += dr.profile_ms[1]
         if ws > 1:
             for dr in runs:
@@ -314,6 +316,7 @@ def main():
             times.append(ms)
             edges_dev += step_edges
             slot_bytes += step_bytes
+            rand_sect += step_sect
             sample_ms.append(step_sample)
             launches += sum(int(dr.counters.get("launches", 0)) for dr in runs)
     clocks.__exit__()
@@ -359,7 +362,10 @@ def main():
     e2e_times, e2e_edges, h2d, d2h = [], 0, 0, 0
     e2e_ok = True
     pipe = HostPipeline(chunks=args.e2e_chunks)
-    jobs = [(app, n, SEED, lo, roots_host) for app in apps]
+    # fixed-length node2vec splits into chunks freely; PPR stays whole (every
+    # chunk would repeat its long-walk tail) and overlaps node2vec instead
+    chunk_of = {"node2vec": args.e2e_chunks, "ppr": args.e2e_ppr_chunks}
+    jobs = [(app, n, SEED, lo, roots_host, chunk_of.get(app.name, args.e2e_chunks)) for app in apps]
     for it in range(max(1, args.warmup // 2) + args.steps):
         barrier()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -401,9 +407,23 @@ def main():
     if os.path.exists(prof_json):
         try:
             with open(prof_json) as fh:
-                traffic = json.load(fh).get("traffic_bytes_per_launch")
+                traffic = json.load(fh).get("traffic_bytes_per_step")
         except Exception:
             traffic = None
+    # the random-gather ceiling of this GPU (nd_gather_ceiling: dependent random
+    # 32-byte sector reads over a buffer the size of the graph's records), the
+    # roofline a gather-bound walk actually faces beside the copy peak
+    import ctypes as C
+    ceil = C.c_double(0.0)
+    ceil_bytes = int(min(dg.resident_bytes(), 8 << 30))
+    gather = None
+    if L.nd_gather_ceiling(ceil_bytes, 4, 64, C.byref(ceil), _lib.stream_ptr()) == 0 and samp_s > 0:
+        rate = rand_sect / samp_s
+        gather = {"sectors_per_s": rate, "ceiling_sectors_per_s": ceil.value,
+                  "frac": rate / ceil.value if ceil.value else None,
+                  "ceiling_how": f"dependent random 32 B reads, 1 chain/thread, 4x256 threads/SM, "
+                                 f"{ceil_bytes / 2**30:.1f} GiB buffer (nd_gather_ceiling)",
+                  "sectors": "random 32 B sector reads counted on device by the walk kernels"}
 
     # ---- CPU baseline (rank 0, N=1 only) ------------------------------------------------
     cpu = None
@@ -442,14 +462,15 @@ def main():
             "e2e": {"value": e2e_value, "unit": "edges/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "host_rows_match_device": e2e_ok,
                     "result": "final rows: int64 offsets + int32 vertex ids, pinned host",
-                    "chunks": args.e2e_chunks},
+                    "chunks": {"node2vec": args.e2e_chunks, "ppr": args.e2e_ppr_chunks}},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                          "kernel": "k_walk_persistent" if args.paradigm == "sp" else "TP class kernels",
                          "peak_kind": peak_kind,
                          "bytes_model": "SURVEY 8(d) sector model, counted on device",
                          "algorithmic_bytes_per_step": slot_bytes / len(times),
-                         "kernel_ms_per_step": sum(sample_ms) / len(sample_ms)},
+                         "kernel_ms_per_step": sum(sample_ms) / len(sample_ms),
+                         "gather": gather},
             "cpu_baseline": cpu, "parity_cpu_sample": parity, "paradigm_tp": tp_info,
             "clocks": clocks.summary(), "gpu_launches": launches,
             "edges_per_step": edges_all / len(times),

@@ -196,8 +196,9 @@ int nd_result_info(const nd_result *r, int64_t *n_samples, int64_t *n_steps,
                    int64_t *total_sampled, int64_t *total_recorded);
 /* device pointer + element count of one field (ptr NULL if absent) */
 int nd_result_field(const nd_result *r, int field, const void **ptr, int64_t *count);
-/* counters for the roofline byte model: {items, pairs, n2v_tries,
- * n2v_probe_sectors, search_sectors} */
+/* counters: {items, pairs, n2v_tries, n2v_probes, search, pair_bytes,
+ * slot_bytes (SURVEY 8(d) model bytes), steps, launches, rand_sectors (random
+ * 32-byte sector reads the walk kernels issued)} */
 int nd_result_counters(const nd_result *r, int64_t *host_counters, int64_t n);
 /* Fill ND_F_FINAL_IDS32: the final ids as int32 (vertex ids < 2^31, the
  * device CSR's column width), halving the device->host bytes of a result
@@ -210,6 +211,12 @@ int nd_result_copy(const nd_result *r, int field, void *dst, void *stream);
  * compaction_ms, 0} */
 int nd_result_profile(const nd_result *r, double *ms, int64_t n);
 int nd_set_profiling(int on);
+/* Measured ceiling of dependent random 32-byte sector reads (sectors/s): one
+ * pointer-chasing chain per thread, ctas_per_sm x 256 threads per SM, over a
+ * `bytes` buffer (rounded down to a power of two).  The roofline a
+ * gather-bound walk kernel actually faces (nd_probe.cu). */
+int nd_gather_ceiling(int64_t bytes, int ctas_per_sm, int iters, double *sectors_per_s,
+                      void *stream);
 int nd_result_destroy(nd_result *r);
 
 #ifdef __cplusplus

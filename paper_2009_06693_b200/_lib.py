@@ -57,6 +57,7 @@ SIGNATURES = {
     "nd_result_narrow_ids": [vp, vp],
     "nd_result_profile": [vp, C.POINTER(C.c_double), i64],
     "nd_set_profiling": [i32],
+    "nd_gather_ceiling": [i64, i32, i32, C.POINTER(C.c_double), vp],
     "nd_result_destroy": [vp],
 }
 _RESTYPE = {"nd_last_error": C.c_char_p}

@@ -124,11 +124,12 @@ __device__ __forceinline__ int64_t pick_rel(const RowT& r, int unit, int64_t deg
 
 // exact membership through the per-row hash set (open addressing, linear probe)
 __device__ __forceinline__ bool hset_contains(const int32_t* __restrict__ tab, int64_t size,
-                                              int32_t u) {
+                                              int32_t u, int64_t* loads = nullptr) {
   const uint32_t mask = (uint32_t)size - 1;
   const int sh = 32 - (63 - __clzll(size));  // log2(size) top bits
   uint32_t p = size > 1 ? (hset_hash((uint32_t)u) >> sh) : 0;
   while (true) {
+    if (loads) ++*loads;
     const int32_t x = __ldg(tab + p);
     if (x == u) return true;
     if (x < 0) return false;
@@ -180,6 +181,7 @@ __device__ __forceinline__ int search_sectors(int64_t deg) {
 struct ItemStats {
   int64_t bytes = 0;
   int64_t tries = 0;
+  int64_t sect = 0;  // random 32-byte sector reads issued (gather-ceiling comparison)
 };
 constexpr int64_t SECTOR = 32;
 

@@ -90,14 +90,17 @@ __device__ __forceinline__ int64_t warp_append(bool alive, int* counter) {
 
 // per-block reduction of the byte/try counters into global counters
 __device__ __forceinline__ void flush_stats(const ItemStats& st, unsigned long long* ctr) {
-  unsigned long long b = (unsigned long long)st.bytes, t = (unsigned long long)st.tries;
+  unsigned long long b = (unsigned long long)st.bytes, t = (unsigned long long)st.tries,
+                     q = (unsigned long long)st.sect;
   for (int o = 16; o > 0; o >>= 1) {
     b += __shfl_down_sync(0xffffffffu, b, o);
     t += __shfl_down_sync(0xffffffffu, t, o);
+    q += __shfl_down_sync(0xffffffffu, q, o);
   }
   if ((threadIdx.x & 31) == 0) {
     if (b) atomicAdd(ctr + 0, b);
     if (t) atomicAdd(ctr + 1, t);
+    if (q) atomicAdd(ctr + 2, q);
   }
 }
 

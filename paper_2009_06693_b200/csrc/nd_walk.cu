@@ -271,7 +271,8 @@ __device__ __forceinline__ int64_t n2v_decide(const PWArgs& A, int64_t nb, doubl
   bool probed = false;
   const bool acc = n2v_accept(A.a, nb, t, w, u01, env, [&] {
     if (A.gv.hset != nullptr && thi - tlo > HASH_MIN_DEG)
-      return hset_contains(A.gv.hset + 4 * tlo, hset_size(thi - tlo), (int32_t)nb);
+      return hset_contains(A.gv.hset + 4 * tlo, hset_size(thi - tlo), (int32_t)nb, &st.sect);
+    st.sect += 1 + search_sectors(thi - tlo);
     return has_edge(A.gv.col, tlo, thi, nb);
   }, probed);
   if (probed) st.bytes += SECTOR * search_sectors(thi - tlo);
@@ -312,6 +313,7 @@ __device__ __forceinline__ int64_t rec_pick(const PWArgs& A, int64_t lo, int64_t
     nh.mx = nh.deg > 0 ? 1.0 : 0.0;
     nh.tot = (double)nh.deg;
     st.bytes += SECTOR + 8;
+    st.sect += 1;
     return r.x;
   }
   const NbrP* rp = A.nbp + lo;
@@ -323,12 +325,19 @@ __device__ __forceinline__ int64_t rec_pick(const PWArgs& A, int64_t lo, int64_t
     const int32_t* gd = A.gv.guide + lo;
     if (j >= 1) a = __ldg(gd + j - 1);
     if (j + 2 < deg) b = (int64_t)__ldg(gd + j + 2) + 1;
+    const uintptr_t ga = reinterpret_cast<uintptr_t>(gd + (j >= 1 ? j - 1 : 0)) >> 5;
+    const uintptr_t gb = reinterpret_cast<uintptr_t>(gd + (j + 2 < deg ? j + 2 : 0)) >> 5;
+    st.sect += (j >= 1) + (j + 2 < deg) - ((j >= 1) && (j + 2 < deg) && ga == gb);
   }
+  int64_t last = -1;
   while (a < b) {
     const int64_t mid = (a + b) >> 1;
+    st.sect += 1;
+    last = mid;
     if (__ldg(&rp[mid].pre) <= x) a = mid + 1; else b = mid;
   }
   const int64_t k = a < deg - 1 ? a : deg - 1;
+  if (k != last) st.sect += 1;  // the selected record (else already in L1)
   const int4 r0 = __ldg(reinterpret_cast<const int4*>(rp + k));
   const double2 r1 = __ldg(reinterpret_cast<const double2*>(rp + k) + 1);
   nh.deg = r0.w;
@@ -346,6 +355,7 @@ __device__ __forceinline__ int64_t rec_try(const PWArgs& A, int64_t lo, int64_t 
   const int64_t k = (int64_t)mod_u64(draw_u64(b, ik), (uint64_t)deg);
   int64_t nb;
   double w;
+  st.sect += 1;
   if (A.nbu != nullptr) {
     const int4 r = __ldg(reinterpret_cast<const int4*>(A.nbu + lo + k));
     nb = r.x;
@@ -411,6 +421,7 @@ __global__ void __launch_bounds__(256, MINB) k_walk_persistent(PWArgs A) {
           orow = A.out + row * A.Lw;
           load_vertex(A, v, lo, deg, mx, tot);
           st.bytes += SECTOR + 8;
+          st.sect += 1;
         }
       }
       if (rem < c) {
@@ -502,9 +513,10 @@ __global__ void __launch_bounds__(256, MINB) k_walk_persistent(PWArgs A) {
         deg = nh.deg;
         mx = nh.mx;
         tot = nh.tot;
-        if (n2v && mx < 0.0) mx = __ldg(A.gv.mx + v);  // after node2vec's step-0 pick
+        if (n2v && mx < 0.0) { mx = __ldg(A.gv.mx + v); st.sect += 1; }  // after node2vec's step-0 pick
       } else {
         load_vertex(A, v, lo, deg, mx, tot);
+        st.sect += 1;
       }
       st.bytes += SECTOR + 8;
     }
@@ -659,8 +671,10 @@ __global__ void __launch_bounds__(256, MINB) k_walk_sm(PWArgs A) {
             const longlong2 q = __ldg(reinterpret_cast<const longlong2*>(A.vrec + L.t));
             L.tlo = q.x;
             L.tdeg = (int32_t)q.y;
+            st.sect += 1;
           }
           st.bytes += SECTOR + 8;
+          st.sect += 1;
           sm_begin<APP, UNIT>(A, L);
         }
       }
@@ -717,8 +731,9 @@ __global__ void __launch_bounds__(256, MINB) k_walk_sm(PWArgs A) {
     if (p0 != nullptr) {
       if (wide) ld32B(p0, r0, r1);
       else r0 = __ldg(reinterpret_cast<const int4*>(p0));
+      st.sect += 1;
     }
-    if (p1 != nullptr) ld32B(p1, r2, r3);
+    if (p1 != nullptr) { ld32B(p1, r2, r3); st.sect += 1; }
 
     // ---- 2. consume it (ALU only) ---------------------------------------------------
     int32_t o = -2;  // -2: the step continues next iteration
@@ -857,8 +872,10 @@ __global__ void __launch_bounds__(256, MINB) k_walk_sm(PWArgs A) {
     // ---- 3. the step is decided: byte model, output, next step -------------------------
     if (L.phase == PH_SEARCH || L.phase == PH_FINAL || L.phase == PH_GUIDE) {
       st.bytes += UNIT ? SECTOR + 8 : SECTOR + SECTOR * search_sectors(L.deg) + SECTOR + 8;
-      if (APP == ND_NODE2VEC && o >= 0)  // the next step tests against v's max weight
+      if (APP == ND_NODE2VEC && o >= 0) {  // the next step tests against v's max weight
         nhv = UNIT ? (nlo_deg > 0 ? 1.0 : 0.0) : __ldg(A.gv.mx + o);
+        st.sect += UNIT ? 0 : 1;
+      }
     }
     {
       const int32_t idx = L.s - step0;
@@ -1376,6 +1393,7 @@ static int run_chain_walk_sp(const nd_graph* G, const NdApp& a, int64_t sample_l
   res->set(ND_F_STATS, stats, 4 * n_steps);
   res->counters[NDC_N2V_TRIES] = (int64_t)h_ctr[1];
   res->counters[NDC_SLOT_BYTES] = (int64_t)h_ctr[0];
+  res->counters[NDC_RAND_SECTORS] = (int64_t)h_ctr[2];
   res->counters[NDC_STEPS] = n_steps;
   return h_stall ? ND_ERR_STALL : ND_OK;
 }

@@ -256,7 +256,7 @@ class DeviceRun:
         ctr = (C.c_int64 * 10)()
         L.nd_result_counters(handle, ctr, 10)
         self.counters = dict(zip(["items", "pairs", "n2v_tries", "n2v_probes", "search",
-                                  "pair_bytes", "slot_bytes", "steps", "launches", "_"],
+                                  "pair_bytes", "slot_bytes", "steps", "launches", "rand_sectors"],
                                  list(ctr)))
         prof = (C.c_double * 4)()
         L.nd_result_profile(handle, prof, 4)

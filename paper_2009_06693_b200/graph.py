@@ -216,6 +216,14 @@ class DeviceGraph:
     def handle(self):
         return self._h
 
+    def resident_bytes(self) -> int:
+        """HBM held by the graph now, including lazily built indexes/records."""
+        V, E, B = C.c_int64(), C.c_int64(), C.c_int64()
+        unit = C.c_int()
+        _lib.check(_lib.load().nd_graph_info(self._h, C.byref(V), C.byref(E), C.byref(unit),
+                                             C.byref(B)))
+        return B.value
+
     @property
     def remap(self):
         return self._remap

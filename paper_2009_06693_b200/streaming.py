@@ -72,7 +72,7 @@ class HostPipeline:
 
     def run_jobs(self, graph, jobs) -> list:
         """Several apps at once through one pipeline: job = (app, n_samples,
-        seed, sample_lo, roots_host).  Each job runs on its own compute stream
+        seed, sample_lo, roots_host[, chunks]).  Each job runs on its own compute stream
         and host thread (engine.run_device_concurrent's scheme) with its own
         copy stream, so one job's copies and tail overlap the others' bulk;
         one synchronisation at the end.  Returns one HostChunk list per job."""
@@ -89,10 +89,11 @@ class HostPipeline:
             st.wait_stream(cur)
 
         def one(ji, job, st, cs):
-            app, n_samples, seed, sample_lo, roots_host = job
+            app, n_samples, seed, sample_lo, roots_host = job[:5]
+            chunks = job[5] if len(job) > 5 and job[5] else self.chunks
             torch.cuda.set_device(dev)
             plan = describe(app)
-            parts = [(lo, hi) for lo, hi in worker_ranges(n_samples, self.chunks) if hi > lo]
+            parts = [(lo, hi) for lo, hi in worker_ranges(n_samples, chunks) if hi > lo]
             out, held = [], []
             with torch.cuda.stream(st):
                 for ci, (lo, hi) in enumerate(parts):

@@ -19,7 +19,7 @@ N = dg.n_vertices
 L = _lib.load()
 L.nd_set_profiling(1)
 tag = {k: v for k, v in os.environ.items() if k.startswith("ND_")}
-for name in sys.argv[1:] or ["node2vec", "ppr"]:
+for name in sys.argv[1:] or ["node2vec", "ppr", "deepwalk"]:
     a = make_app(name)
     ms, kms = [], []
     for it in range(6):
@@ -35,5 +35,6 @@ for name in sys.argv[1:] or ["node2vec", "ppr"]:
         dr.close()
     print(json.dumps({"env": tag, "app": name, "ms": statistics.median(ms), "kernel_ms": statistics.median(kms),
                       "edges": edges, "Gedges_s": edges / statistics.median(ms) / 1e6,
-                      "model_GBs": c["slot_bytes"] / statistics.median(kms) / 1e6, "tries": c["n2v_tries"]}),
+                      "model_GBs": c["slot_bytes"] / statistics.median(kms) / 1e6, "tries": c["n2v_tries"],
+                      "rand_sectors": c["rand_sectors"], "Gsect_s": c["rand_sectors"] / statistics.median(kms) / 1e6}),
           flush=True)
