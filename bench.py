@@ -235,7 +235,7 @@ def main():
                     help="run node2vec then PPR instead of concurrently on two streams")
     ap.add_argument("--e2e-chunks", type=int, default=4,
                     help="node2vec sample-id chunks of the host pipeline (D2H of chunk c overlaps chunk c+1)")
-    ap.add_argument("--e2e-ppr-chunks", type=int, default=1)
+    ap.add_argument("--e2e-ppr-chunks", type=int, default=2)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -252,7 +252,7 @@ def main():
         else:
             dist.init_process_group(backend)
     from paper_2009_06693_b200 import _lib, make_app
-    from paper_2009_06693_b200.engine import run_device, run_device_concurrent
+    from paper_2009_06693_b200.engine import job_streams, run_device, submit_device_concurrent
     from paper_2009_06693_b200.graph import DeviceGraph
     from paper_2009_06693_b200.sharding import worker_ranges
 
@@ -290,20 +290,26 @@ def main():
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record(stream)
         step_edges, step_bytes, step_sample, step_sect = 0, 0, 0.0, 0
+        runs = []
         if args.serial_apps:
-            runs = [run_device(app, dg, n_samples=n, sample_lo=lo, seed=SEED, paradigm=args.paradigm,
-                               sync=False) for app in apps]
+            for app in apps:
+                runs.append(run_device(app, dg, n_samples=n, sample_lo=lo, seed=SEED,
+                                       paradigm=args.paradigm, sync=False))
+                if ws > 1:
+                    gather_rows(runs[-1].view(_lib.F_FINAL_OFF), runs[-1].narrow_ids())
         else:  # node2vec and PPR concurrently (PPR's long-walk tail overlaps node2vec)
-            runs = run_device_concurrent([dict(app=app, n_samples=n, sample_lo=lo, seed=SEED)
-                                          for app in apps], dg, paradigm=args.paradigm)
+            futs = submit_device_concurrent([dict(app=app, n_samples=n, sample_lo=lo, seed=SEED)
+                                             for app in apps], dg, paradigm=args.paradigm)
+            for fut, st in zip(futs, job_streams(len(apps))):
+                runs.append(fut.result())
+                stream.wait_stream(st)
+                if ws > 1:  # this app's rows go to rank 0 while the other app still samples
+                    gather_rows(runs[-1].view(_lib.F_FINAL_OFF), runs[-1].narrow_ids())
         for dr in runs:
             step_edges += dr.total_sampled
             step_bytes += dr.counters["slot_bytes"]
             step_sect += dr.counters.get("rand_sectors", 0)
             step_sample += dr.profile_ms[1]
-        if ws > 1:
-            for dr in runs:
-                gather_rows(dr.view(_lib.F_FINAL_OFF), dr.view(_lib.F_FINAL_IDS))
         ev1.record(stream)
         torch.cuda.synchronize()
         ms = ev0.elapsed_time(ev1)

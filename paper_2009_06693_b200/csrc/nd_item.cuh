@@ -94,11 +94,26 @@ struct SRow {
   }
 };
 
+// Exact guide bucket of a pick target x (guide tables: nd_index.cu).  The
+// build stores guide[j] = upper_bound(prefix row, y_j) with
+// y_j = rn(rn(total/deg) * j).  For the bucket j with y_j <= x < y_{j+1},
+// found here by exact comparisons against those same rounded products, every
+// entry before guide[j] is <= y_j <= x and prefix[guide[j+1]] > y_{j+1} > x:
+// the upper bound of x lies in [guide[j], guide[j+1]] (for j = deg-1 in
+// [guide[deg-1], deg]), the same entry the full-row search finds.  Returns -1
+// when the bucket width is not positive (search the whole row).
+__device__ __forceinline__ int64_t guide_bucket(double x, double total, int64_t deg) {
+  const double width = __ddiv_rn(total, (double)deg);
+  if (!(width > 0.0) || !(x >= 0.0)) return -1;
+  const double q = __ddiv_rn(x, width);
+  int64_t j = q < (double)(deg - 1) ? (int64_t)q : deg - 1;
+  while (j > 0 && __dmul_rn(width, (double)j) > x) j--;
+  while (j + 1 < deg && __dmul_rn(width, (double)(j + 1)) <= x) j++;
+  return j;
+}
+
 // upper-bound inverse-CDF pick (_ckernels.pyx:65-74, 90-100); returns k in [0, deg).
-// With a guide table the search starts at guide[j-1] and ends at guide[j+2]
-// (j = floor(u*deg)): every entry before guide[j-1] is <= j-1 buckets' worth
-// <= x and prefix[guide[j+2]] > x, so the first entry > x is the same one
-// the full-row upper bound finds.
+// With a guide table the search runs over the exact bucket's bracket.
 template <typename RowT>
 __device__ __forceinline__ int64_t pick_rel(const RowT& r, int unit, int64_t deg, double u01,
                                             double total_known = -1.0) {
@@ -107,13 +122,15 @@ __device__ __forceinline__ int64_t pick_rel(const RowT& r, int unit, int64_t deg
     int64_t k = (int64_t)x;
     return k < deg - 1 ? k : deg - 1;
   }
-  const double x = __dmul_rn(u01, total_known >= 0.0 ? total_known : r.p(deg - 1));
+  const double total = total_known >= 0.0 ? total_known : r.p(deg - 1);
+  const double x = __dmul_rn(u01, total);
   int64_t lo = 0, hi = deg;
   if (r.gd != nullptr && deg > GUIDE_MIN_DEG) {
-    int64_t j = (int64_t)__dmul_rn(u01, (double)deg);
-    if (j > deg - 1) j = deg - 1;
-    if (j >= 1) lo = __ldg(r.gd + j - 1);
-    if (j + 2 < deg) hi = (int64_t)__ldg(r.gd + j + 2) + 1;
+    const int64_t j = guide_bucket(x, total, deg);
+    if (j >= 0) {
+      lo = __ldg(r.gd + j);
+      hi = j + 1 < deg ? (int64_t)__ldg(r.gd + j + 1) : deg;
+    }
   }
   while (lo < hi) {
     int64_t mid = (lo + hi) >> 1;

@@ -14,6 +14,7 @@
 // the first root equal to the transit.  Values go to a dense [steps, N] slab.
 #include <cub/cub.cuh>
 
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -320,32 +321,45 @@ __device__ __forceinline__ int64_t rec_pick(const PWArgs& A, int64_t lo, int64_t
   const double x = __dmul_rn(u01, tot);
   int64_t a = 0, b = deg;
   if (A.gv.guide != nullptr && deg > GUIDE_MIN_DEG) {
-    int64_t j = (int64_t)__dmul_rn(u01, (double)deg);
-    if (j > deg - 1) j = deg - 1;
-    const int32_t* gd = A.gv.guide + lo;
-    if (j >= 1) a = __ldg(gd + j - 1);
-    if (j + 2 < deg) b = (int64_t)__ldg(gd + j + 2) + 1;
-    const uintptr_t ga = reinterpret_cast<uintptr_t>(gd + (j >= 1 ? j - 1 : 0)) >> 5;
-    const uintptr_t gb = reinterpret_cast<uintptr_t>(gd + (j + 2 < deg ? j + 2 : 0)) >> 5;
-    st.sect += (j >= 1) + (j + 2 < deg) - ((j >= 1) && (j + 2 < deg) && ga == gb);
+    const int64_t j = guide_bucket(x, tot, deg);
+    if (j >= 0) {  // guide[j], guide[j+1]: adjacent, one sector unless they straddle
+      const int32_t* gd = A.gv.guide + lo + j;
+      a = __ldg(gd);
+      b = j + 1 < deg ? (int64_t)__ldg(gd + 1) : deg;
+      st.sect += 1 + (j + 1 < deg && (reinterpret_cast<uintptr_t>(gd) >> 5) !=
+                                         (reinterpret_cast<uintptr_t>(gd + 1) >> 5));
+    }
   }
-  int64_t last = -1;
+  // upper bound over [a, b) with whole-record (32-byte) probes: the probe
+  // that proves the answer is usually the selected record itself
+  int64_t have = -1;
+  int4 h0 = make_int4(0, 0, 0, 0), h1 = h0;
   while (a < b) {
     const int64_t mid = (a + b) >> 1;
+    int4 q0, q1;
+    ld32B(rp + mid, q0, q1);
     st.sect += 1;
-    last = mid;
-    if (__ldg(&rp[mid].pre) <= x) a = mid + 1; else b = mid;
+    const double pre = __longlong_as_double(((long long)(uint32_t)q0.y << 32) | (uint32_t)q0.x);
+    if (pre <= x) {
+      a = mid + 1;
+    } else {
+      b = mid;
+      have = mid;
+      h0 = q0;
+      h1 = q1;
+    }
   }
   const int64_t k = a < deg - 1 ? a : deg - 1;
-  if (k != last) st.sect += 1;  // the selected record (else already in L1)
-  const int4 r0 = __ldg(reinterpret_cast<const int4*>(rp + k));
-  const double2 r1 = __ldg(reinterpret_cast<const double2*>(rp + k) + 1);
-  nh.deg = r0.w;
-  nh.lo = __double_as_longlong(r1.x);
-  nh.tot = r1.y;
+  if (k != have) {
+    ld32B(rp + k, h0, h1);
+    st.sect += 1;
+  }
+  nh.deg = h0.w;
+  nh.lo = ((int64_t)(uint32_t)h1.y << 32) | (uint32_t)h1.x;
+  nh.tot = __longlong_as_double(((long long)(uint32_t)h1.w << 32) | (uint32_t)h1.z);
   nh.mx = -1.0;
   st.bytes += SECTOR + SECTOR * search_sectors(deg) + SECTOR + 8;
-  return r0.z;
+  return h0.z;
 }
 
 // one node2vec rejection try over the neighbour records; -2 = rejected
@@ -554,29 +568,6 @@ __device__ __forceinline__ int n2v_class(const NdApp& a, int32_t nb, int32_t t, 
 // divergent dependent loads of its lanes one branch after another.
 enum : int { PH_REC = 0, PH_PROBE = 1, PH_GUIDE = 2, PH_SEARCH = 3, PH_FINAL = 4, PH_NULL = 5 };
 
-// one 32-byte load (LDG.E.256): a whole record / hash-set chunk per request
-__device__ __forceinline__ void ld32B(const void* p, int4& lo, int4& hi) {
-  unsigned long long a, b, c, d;
-  asm volatile("ld.global.nc.v4.u64 {%0,%1,%2,%3}, [%4];" : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(p));
-  lo = make_int4((int)(uint32_t)a, (int)(uint32_t)(a >> 32), (int)(uint32_t)b, (int)(uint32_t)(b >> 32));
-  hi = make_int4((int)(uint32_t)c, (int)(uint32_t)(c >> 32), (int)(uint32_t)d, (int)(uint32_t)(d >> 32));
-}
-
-__device__ __forceinline__ void st32B(void* p, int32_t a0, int32_t a1, int32_t a2, int32_t a3,
-                                      int32_t a4, int32_t a5, int32_t a6, int32_t a7) {
-  auto pk = [](int32_t lo, int32_t hi) {
-    return (unsigned long long)(uint32_t)lo | ((unsigned long long)(uint32_t)hi << 32);
-  };
-  asm volatile("st.global.v4.u64 [%0], {%1,%2,%3,%4};" ::"l"(p), "l"(pk(a0, a1)), "l"(pk(a2, a3)),
-               "l"(pk(a4, a5)), "l"(pk(a6, a7))
-               : "memory");
-}
-
-__device__ __forceinline__ int32_t pick8(const int4& a, const int4& b, int q) {
-  return q < 4 ? (q == 0 ? a.x : q == 1 ? a.y : q == 2 ? a.z : a.w)
-               : (q == 4 ? b.x : q == 5 ? b.y : q == 6 ? b.z : b.w);
-}
-
 __device__ __forceinline__ int32_t pick4(const int4& r, int q) {  // r[q], no local memory
   return q == 0 ? r.x : q == 1 ? r.y : q == 2 ? r.z : r.w;
 }
@@ -605,17 +596,17 @@ __device__ __forceinline__ void sm_begin(const PWArgs& A, SMLane& L) {
   if (APP == ND_NODE2VEC && L.t >= 0) { L.phase = PH_REC; L.j = 0; return; }
   if (APP == ND_PPR && to_unit(draw_u64(base0, L.ik)) < A.a.term) { L.phase = PH_NULL; return; }
   const double u = to_unit(draw_u64(APP == ND_PPR ? base0 + C_DRAW : base0, L.ik));
-  int32_t jg = (int32_t)__dmul_rn(u, (double)L.deg);
-  if (jg > L.deg - 1) jg = L.deg - 1;
   if (UNIT) {  // floor identity: the record itself
-    L.sa = jg;
+    int32_t k = (int32_t)__dmul_rn(u, (double)L.deg);
+    L.sa = k < L.deg - 1 ? k : L.deg - 1;
     L.phase = PH_FINAL;
     return;
   }
   L.x = __dmul_rn(u, L.hv);
   L.have_c = false;
-  if (A.gv.guide != nullptr && L.deg > GUIDE_MIN_DEG) {
-    L.sa = jg;  // GUIDE reads guide[jg-1], guide[jg+2]
+  const int64_t jg = (A.gv.guide != nullptr && L.deg > GUIDE_MIN_DEG) ? guide_bucket(L.x, L.hv, L.deg) : -1;
+  if (jg >= 0) {
+    L.sa = (int32_t)jg;  // GUIDE reads guide[jg], guide[jg+1] (exact bucket bracket)
     L.phase = PH_GUIDE;
   } else {
     L.sa = 0;
@@ -708,8 +699,8 @@ __global__ void __launch_bounds__(256, MINB) k_walk_sm(PWArgs A) {
         break;
       case PH_GUIDE: {
         const int32_t* gd = A.gv.guide + L.lo;
-        const int32_t ja = L.sa >= 1 ? L.sa - 1 : 0;
-        const int32_t jb = L.sa + 2 < L.deg ? L.sa + 2 : L.deg - 1;
+        const int32_t ja = L.sa;
+        const int32_t jb = L.sa + 1 < L.deg ? L.sa + 1 : L.sa;
         const uintptr_t qa = reinterpret_cast<uintptr_t>(gd + ja), qb = reinterpret_cast<uintptr_t>(gd + jb);
         p0 = reinterpret_cast<const void*>(qa & ~(uintptr_t)31);
         if ((qb & ~(uintptr_t)31) != (qa & ~(uintptr_t)31)) p1 = reinterpret_cast<const void*>(qb & ~(uintptr_t)31);
@@ -817,8 +808,8 @@ __global__ void __launch_bounds__(256, MINB) k_walk_sm(PWArgs A) {
       }
       case PH_GUIDE: {
         const int32_t jg = L.sa;
-        L.sa = jg >= 1 ? pick8(r0, r1, ia) : 0;
-        L.sb = jg + 2 < L.deg ? (ib < 8 ? pick8(r0, r1, ib) : pick8(r2, r3, ib - 8)) + 1 : L.deg;
+        L.sa = pick8(r0, r1, ia);
+        L.sb = jg + 1 < L.deg ? (ib < 8 ? pick8(r0, r1, ib) : pick8(r2, r3, ib - 8)) : L.deg;
         L.phase = PH_SEARCH;
         if (L.sa >= L.sb) {  // empty bracket (defensive): the clamped upper bound
           L.sa = L.sa < L.deg - 1 ? L.sa : L.deg - 1;
@@ -1297,6 +1288,9 @@ static int run_chain_walk_sp(const nd_graph* G, const NdApp& a, int64_t sample_l
     ND_CUDA_TRY(cudaMemcpyAsync(h, ctl, 4 * sizeof(int), cudaMemcpyDeviceToHost, s));
     ND_CUDA_TRY(cudaStreamSynchronize(s));
     nd_trace("sp:window-synced");
+    if (getenv("ND_TRACE") && getenv("ND_TRACE")[0] == '1')
+      fprintf(stderr, "[nd_trace]   window step0=%lld Lw=%lld rows=%lld -> continuing %d\n",
+              (long long)step0, (long long)Lw, (long long)rows, h[1]);
     if (g_profile) {
       float ms = 0;
       cudaEventElapsedTime(&ms, pe0, pe1);

@@ -444,14 +444,14 @@ def _job_pool(k: int):
     return _JOB_POOL
 
 
-def run_device_concurrent(jobs, graph, *, paradigm: str = "sp",
-                          step_cap: int = DEFAULT_STEP_CAP) -> list:
-    """Several whole sampling jobs at once, each on its own stream and host
-    thread (the C-ABI call releases the GIL): a job = dict(app=..., n_samples=...,
-    sample_lo=0, seed=0).  A job whose tail leaves the GPU idle (a few long
-    PPR walks) overlaps the others' bulk.  Outputs are exactly those of
-    separate run_device calls.  The caller's current stream is ordered after
-    every job; returns the DeviceRuns in job order."""
+def submit_device_concurrent(jobs, graph, *, paradigm: str = "sp",
+                             step_cap: int = DEFAULT_STEP_CAP) -> list:
+    """Start several whole sampling jobs at once, each on its own stream and
+    host thread (the C-ABI call releases the GIL); a job = dict(app=...,
+    n_samples=..., sample_lo=0, seed=0).  Returns one future per job whose
+    result is a finished DeviceRun (its outputs complete in HBM); a job whose
+    tail leaves the GPU idle (a few long PPR walks) overlaps the others' bulk.
+    Outputs are exactly those of separate run_device calls."""
     import torch
     _lib.require_cuda()
     dg = as_device_graph(graph)
@@ -468,9 +468,18 @@ def run_device_concurrent(jobs, graph, *, paradigm: str = "sp",
                               sample_lo=job.get("sample_lo", 0), seed=job.get("seed", 0),
                               paradigm=paradigm, step_cap=step_cap, stream=st, sync=False)
 
-    runs = [f.result() for f in [_job_pool(len(jobs)).submit(one, j, st)
-                                  for j, st in zip(jobs, streams)]]
-    for st in streams:
+    return [_job_pool(len(jobs)).submit(one, j, st) for j, st in zip(jobs, streams)]
+
+
+def run_device_concurrent(jobs, graph, *, paradigm: str = "sp",
+                          step_cap: int = DEFAULT_STEP_CAP) -> list:
+    """submit_device_concurrent, waited: the caller's current stream is
+    ordered after every job; returns the DeviceRuns in job order."""
+    import torch
+    futs = submit_device_concurrent(jobs, graph, paradigm=paradigm, step_cap=step_cap)
+    runs = [f.result() for f in futs]
+    cur = torch.cuda.current_stream()
+    for st in job_streams(len(jobs)):
         cur.wait_stream(st)
     return runs
 

@@ -21,7 +21,8 @@ def gather_rows(off, ids, group=None, dst: int = 0):
     """Gather per-rank final-layout CSR pieces (off[n_r+1], ids) to `dst`.
 
     Works for any torch.distributed backend; tensors live on the backend's
-    device (CUDA for NCCL, CPU for gloo).  Returns (off, ids) concatenated in
+    device (CUDA for NCCL, CPU for gloo).  `ids` may be int64 (F_FINAL_IDS) or
+    int32 (F_FINAL_IDS32, half the NVLink bytes).  Returns (off, ids) concatenated in
     rank order on `dst` (None elsewhere)."""
     import torch
     import torch.distributed as dist
@@ -37,7 +38,7 @@ def gather_rows(off, ids, group=None, dst: int = 0):
     e_max = int(max(s[1].item() for s in all_sizes))
     pad_off = torch.zeros(n_max + 1, dtype=torch.int64, device=dev)
     pad_off[:off.numel()] = off
-    pad_ids = torch.full((max(e_max, 1),), -1, dtype=torch.int64, device=dev)
+    pad_ids = torch.full((max(e_max, 1),), -1, dtype=ids.dtype, device=dev)
     pad_ids[:ids.numel()] = ids
     offs = [torch.empty_like(pad_off) for _ in range(ws)] if rank == dst else None
     idss = [torch.empty_like(pad_ids) for _ in range(ws)] if rank == dst else None
@@ -56,7 +57,7 @@ def gather_rows(off, ids, group=None, dst: int = 0):
 
 def run_sharded(app, graph, n_samples: int, seed: int, paradigm: str = "sp", group=None):
     """This rank's share of an N-sample job on its GPU, gathered to rank 0.
-    Returns (final_off, final_ids) on rank 0, (None, None) elsewhere."""
+    Returns (final_off, final_ids int32) on rank 0, (None, None) elsewhere."""
     import torch.distributed as dist
     from . import _lib
     from .engine import run_device
@@ -64,7 +65,7 @@ def run_sharded(app, graph, n_samples: int, seed: int, paradigm: str = "sp", gro
     rank = dist.get_rank(group)
     lo, hi = shard_for_rank(n_samples, ws, rank)
     dr = run_device(app, graph, n_samples=hi - lo, sample_lo=lo, seed=seed, paradigm=paradigm)
-    off, ids = gather_rows(dr.view(_lib.F_FINAL_OFF), dr.view(_lib.F_FINAL_IDS), group)
+    off, ids = gather_rows(dr.view(_lib.F_FINAL_OFF), dr.narrow_ids(), group)
     if off is not None:
         off, ids = off.clone(), ids.clone()
     dr.close()

@@ -19,7 +19,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, ws, port, app, n, seed, q):
+def _worker(rank, ws, port, app, n, seed, q, id_dtype="int64"):
     import torch
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -43,22 +43,26 @@ def _worker(rank, ws, port, app, n, seed, q):
     rows = [np.concatenate([roots[i], vals[starts[i]:starts[i + 1]][vals[starts[i]:starts[i + 1]] >= 0]])
             for i in range(hi - lo)]
     off = torch.tensor(np.concatenate([[0], np.cumsum([len(x) for x in rows])]), dtype=torch.int64)
-    ids = torch.tensor(np.concatenate(rows) if rows else np.empty(0), dtype=torch.int64)
+    ids = torch.tensor(np.concatenate(rows) if rows else np.empty(0), dtype=getattr(torch, id_dtype))
     goff, gids = gather_rows(off, ids)
+    assert rank != 0 or gids.dtype == getattr(torch, id_dtype)
     if rank == 0:
         q.put((goff.numpy(), gids.numpy()))
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("app", ["deepwalk", "ppr", "node2vec"])
+@pytest.mark.parametrize("app,id_dtype", [("deepwalk", "int64"), ("ppr", "int64"),
+                                          ("node2vec", "int64"), ("node2vec", "int32")])
 @pytest.mark.parametrize("ws", [2, 3])
-def test_sharded_gather_equals_single_run(app, ws):
+def test_sharded_gather_equals_single_run(app, id_dtype, ws):
+    """int32 ids: the F_FINAL_IDS32 payload bench.py gathers over NCCL."""
     from tests.helpers import golden_graph, oracle_run
     n, seed = 101, 5
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, ws, port, app, n, seed, q)) for r in range(ws)]
+    procs = [ctx.Process(target=_worker, args=(r, ws, port, app, n, seed, q, id_dtype))
+             for r in range(ws)]
     for p in procs:
         p.start()
     goff, gids = q.get(timeout=120)
@@ -68,7 +72,7 @@ def test_sharded_gather_equals_single_run(app, ws):
     ref = oracle_run({"app": app, "params": {}, "n_samples": n, "seed": seed},
                      golden_graph("powerlaw:2000|1|7"))
     roff, rids = ref.final_csr()
-    assert np.array_equal(goff, roff) and np.array_equal(gids, rids)
+    assert np.array_equal(goff, roff) and np.array_equal(gids.astype(np.int64), rids)
 
 
 def test_worker_ranges_cover_exactly():
