@@ -152,7 +152,13 @@ __global__ void k_imp_hits(const DevGraph g, const int64_t* __restrict__ toff,
     const int64_t slot = r / T, k = r - slot * T;
     const int64_t t = tv[toff[i] + k];
     const int64_t v = out[i * m + slot];
-    flag[j] = has_edge(g.col, __ldg(g.row + t), __ldg(g.row + t + 1), v) ? 1 : 0;
+    const int64_t rlo = __ldg(g.row + t), rhi = __ldg(g.row + t + 1);
+    // has_edge(t, v) (graph.py:78-81): the exact hash set when built, else the
+    // sorted-row binary search; same answer
+    const bool hit = (g.hset != nullptr && rhi - rlo > HASH_MIN_DEG)
+                         ? (v >= 0 && hset_contains(g.hset + 4 * rlo, hset_size(rhi - rlo), (int32_t)v))
+                         : has_edge(g.col, rlo, rhi, v);
+    flag[j] = hit ? 1 : 0;
   }
 }
 
@@ -478,6 +484,9 @@ extern "C" int nd_run_collective(const nd_graph* G, int kind, int64_t step_size,
   nd_pool_init();
   if (!G || n < 0 || sample_lo < 0 || step_size < 1 || kind < 0 || kind > 3) return kind < 0 || kind > 3 ? ND_ERR_APP : ND_ERR_ARG;
   cudaStream_t s = (cudaStream_t)stream;
+  // FastGCN/LADIES test has_edge(t, v) for every (draw, transit) pair: build
+  // the exact per-row hash sets once per graph (nd_index.cu)
+  if (kind == ND_IMPORTANCE) ND_TRY(nd_graph_ensure_index(const_cast<nd_graph*>(G), 1, 0, s));
   const DevGraph& g = G->g;
   const int64_t V = g.V;
   const int64_t m = step_size;
