@@ -233,9 +233,9 @@ def main():
     ap.add_argument("--no-tp", action="store_true")
     ap.add_argument("--serial-apps", action="store_true",
                     help="run node2vec then PPR instead of concurrently on two streams")
-    ap.add_argument("--e2e-chunks", type=int, default=4,
+    ap.add_argument("--e2e-chunks", type=int, default=8,
                     help="node2vec sample-id chunks of the host pipeline (D2H of chunk c overlaps chunk c+1)")
-    ap.add_argument("--e2e-ppr-chunks", type=int, default=2)
+    ap.add_argument("--e2e-ppr-chunks", type=int, default=4)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -121,7 +121,9 @@ int nd_graph_ensure_records(nd_graph* G, int want_tries, cudaStream_t s) {
   if (disabled) return ND_OK;
   std::lock_guard<std::mutex> lock(g_index_mu);
   const int64_t V = G->g.V, E = G->g.E;
+  bool built = false;
   if (!G->vrec && V > 0) {
+    built = true;
     ND_CUDA_TRY(cudaMalloc(&G->vrec, V * sizeof(VRec)));
     G->bytes += V * sizeof(VRec);
     k_build_vrec<<<nd_grid(V, 256), 256, 0, s>>>(G->row, G->mx, G->g.unit ? nullptr : G->pre, V,
@@ -140,6 +142,7 @@ int nd_graph_ensure_records(nd_graph* G, int want_tries, cudaStream_t s) {
       if (want_tries && !G->nbw) ND_CUDA_TRY(cudaMalloc(&nw, E * sizeof(NbrW)));
     }
     if (nw || np_ || nu) {
+      built = true;
       k_build_nbr<<<nd_grid(E, 256, 148 * 64), 256, 0, s>>>(G->row, G->col, G->w, G->pre, G->mx,
                                                              E, nw, np_, nu);
       ND_CUDA_TRY(cudaGetLastError());
@@ -148,7 +151,8 @@ int nd_graph_ensure_records(nd_graph* G, int want_tries, cudaStream_t s) {
       if (nu) { G->nbu = nu; G->g.nbu = nu; G->bytes += E * sizeof(NbrU); }
     }
   }
-  ND_CUDA_TRY(cudaStreamSynchronize(s));
+  // other streams may use the records as soon as this call returns
+  if (built) ND_CUDA_TRY(cudaStreamSynchronize(s));
   return ND_OK;
 }
 

@@ -106,9 +106,24 @@ class DevicePlan:
     roots_kind: str = "keyed"             # "keyed" | "host" (custom init_roots)
 
 
+_PLANS = {}  # id(app) -> (app, plan): describe() walks app.unique over up to 4096 steps
+
+
 def describe(app) -> DevicePlan:
     """Map a SamplingApp (ours or the reference's) onto a device plan: by
-    kernel_code for individual apps, by name + params for collective apps."""
+    kernel_code for individual apps, by name + params for collective apps.
+    Plans are cached per app object (apps are immutable once built)."""
+    hit = _PLANS.get(id(app))
+    if hit is not None and hit[0] is app:
+        return hit[1]
+    plan = _describe(app)
+    if len(_PLANS) > 256:
+        _PLANS.clear()
+    _PLANS[id(app)] = (app, plan)
+    return plan
+
+
+def _describe(app) -> DevicePlan:
     name = getattr(app, "name", "?")
     p = dict(getattr(app, "params", {}) or {})
     steps = -1 if app.steps == INF_STEPS or (isinstance(app.steps, float) and math.isinf(app.steps)) \

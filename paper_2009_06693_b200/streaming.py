@@ -98,6 +98,9 @@ class HostPipeline:
             with torch.cuda.stream(st):
                 for ci, (lo, hi) in enumerate(parts):
                     n = hi - lo
+                    if trace is not None:
+                        e_c0 = torch.cuda.Event(enable_timing=True)
+                        e_c0.record(st)
                     if roots_host is not None:
                         R = len(roots_host) // max(n_samples, 1)
                         droots = roots_host[lo * R:hi * R].to("cuda", non_blocking=True)
@@ -118,16 +121,35 @@ class HostPipeline:
                     with torch.cuda.stream(cs):
                         h_off.copy_(off, non_blocking=True)
                         h_ids.copy_(ids, non_blocking=True)
+                    if trace is not None:
+                        e_c1 = torch.cuda.Event(enable_timing=True)
+                        e_c1.record(st)
+                        e_d1 = torch.cuda.Event(enable_timing=True)
+                        e_d1.record(cs)
+                        trace.append((getattr(app, "name", "?"), ci, e_c0, e_c1, e_d1,
+                                      h_ids.numel() * 4))
                     held.append(dr)
                     out.append(HostChunk(sample_lo + lo, n, h_off, h_ids, dr.total_sampled))
             return out, held
 
+        import os
+        trace = [] if os.environ.get("ND_PIPE_TRACE") == "1" else None
+        t0 = None
+        if trace is not None:
+            t0 = torch.cuda.Event(enable_timing=True)
+            t0.record(cur)
         futs = [_job_pool(k).submit(one, ji, job, st, cs)
                 for ji, (job, st, cs) in enumerate(zip(jobs, streams, self._copy_streams))]
         done = [f.result() for f in futs]
         for cs in self._copy_streams[:k]:
             cur.wait_stream(cs)
         cur.synchronize()
+        if trace is not None:  # chunk timeline (ms from the call): compute start/end, copy end
+            import sys
+            for name, ci, c0, c1, d1, nb in trace:
+                print(f"[pipe] {name:9s} chunk {ci}: compute {t0.elapsed_time(c0):7.2f} -> "
+                      f"{t0.elapsed_time(c1):7.2f}  copied {t0.elapsed_time(d1):7.2f}  "
+                      f"({nb / 1e6:.0f} MB)", file=sys.stderr)
         for _, held in done:
             for h in held:
                 if isinstance(h, DeviceRun):
