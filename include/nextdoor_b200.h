@@ -50,6 +50,7 @@ extern "C" {
 #define ND_ERR_ARG 3
 #define ND_ERR_CUDA 4
 #define ND_ERR_NOMEM 5
+#define ND_ERR_EMPTY 6 /* no edges (EmptyGraphError, graph.py:178-179) */
 
 /* individual app codes (kernels/_pykernels.py:32-36) */
 #define ND_DEEPWALK 0
@@ -117,6 +118,30 @@ int nd_graph_create(const int64_t *row_offsets, const int64_t *col_indices,
 int nd_graph_from_edges(const int64_t *src, const int64_t *dst, const double *weights,
                         int64_t n_edges, int64_t n_vertices, void *stream,
                         nd_graph **out);
+/* Edge-list ingestion on device (load_edge_list, graph.py:132-188), in three
+ * calls.  nd_text_parse uploads the file's bytes and parses every line on
+ * device (universal newlines, '#' comments, 2 or 3 whitespace-separated
+ * fields, int/float with Python's grammar, keyed default weights).
+ * host_info[4] = {n_lines, first malformed line (1-based, 0 = none), its error
+ * code (1 fields, 2 id, 3 negative id, 4 weight, 5 negative weight), number
+ * of lines left to the host}.  Lines left to the host (non-ASCII bytes, or
+ * numbers the device cannot convert bit-exactly) are listed by
+ * nd_text_host_lines (0-based line indexes, ascending; byte bounds via
+ * nd_text_line_bounds); the caller parses them with the reference rules and
+ * passes the results to nd_text_finish (kind 0 skip / 1 edge), which builds
+ * the device CSR with ids compacted onto [0, n) (nd_text_remap: the original
+ * ids).  ND_ERR_EMPTY when no line holds an edge. */
+typedef struct nd_text nd_text;
+int nd_text_parse(const char *host_text, int64_t n_bytes, int weighted, double lo_w, double hi_w,
+                  uint64_t seed, void *stream, nd_text **out, int64_t *host_info);
+int nd_text_host_lines(const nd_text *t, int64_t *host_lines);
+int nd_text_line_bounds(const nd_text *t, int64_t line_index, int64_t *host_lo_hi);
+int nd_text_finish(nd_text *t, const int64_t *host_line, const int64_t *host_src,
+                   const int64_t *host_dst, const double *host_w, const uint8_t *host_kind,
+                   int64_t n_patch, int undirected, void *stream, nd_graph **out,
+                   int64_t *n_vertices);
+int nd_text_remap(const nd_text *t, int64_t *host_remap);
+int nd_text_destroy(nd_text *t);
 /* Keyed RMAT graph generated and built on device. */
 int nd_graph_rmat(int scale, int64_t n_edges, uint32_t ta, uint32_t tab, uint32_t tabc,
                   uint64_t seed, int undirected, int weighted, void *stream,

@@ -10,12 +10,12 @@ from __future__ import annotations
 import ctypes as C
 import os
 
-from .errors import DeviceError, SamplerStallError
+from .errors import DeviceError, EmptyGraphError, SamplerStallError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libnextdoor_b200.so")
 
-ND_OK, ND_ERR_STALL, ND_ERR_APP, ND_ERR_ARG, ND_ERR_CUDA, ND_ERR_NOMEM = range(6)
+ND_OK, ND_ERR_STALL, ND_ERR_APP, ND_ERR_ARG, ND_ERR_CUDA, ND_ERR_NOMEM, ND_ERR_EMPTY = range(7)
 ND_SP, ND_TP = 0, 1
 (F_FINAL_OFF, F_FINAL_IDS, F_ROOTS, F_ROOTS_OFF, F_CHAIN_LEN, F_STEP_COUNTS, F_STEP_VALS,
  F_REC_COUNTS, F_REC_T, F_REC_V, F_STATS, F_CHAIN_VALS, F_FINAL_IDS32) = range(13)
@@ -39,6 +39,12 @@ SIGNATURES = {
     "nd_graph_create": [vp, vp, vp, vp, vp, i64, i64, i32, vp, pp],
     "nd_graph_from_edges": [vp, vp, vp, i64, i64, vp, pp],
     "nd_graph_rmat": [i32, i64, u32, u32, u32, u64, i32, i32, vp, pp],
+    "nd_text_parse": [C.c_char_p, i64, i32, dbl, dbl, u64, vp, pp, pi64],
+    "nd_text_host_lines": [vp, vp],
+    "nd_text_line_bounds": [vp, i64, pi64],
+    "nd_text_finish": [vp, vp, vp, vp, vp, vp, i64, i32, vp, pp, pi64],
+    "nd_text_remap": [vp, vp],
+    "nd_text_destroy": [vp],
     "nd_graph_destroy": [vp],
     "nd_graph_build_index": [vp, i32, vp],
     "nd_graph_info": [vp, pi64, pi64, C.POINTER(C.c_int), pi64],
@@ -98,6 +104,8 @@ def check(rc: int, what: str = "") -> None:
         raise ValueError(f"invalid argument ({msg})")
     if rc == ND_ERR_NOMEM:
         raise MemoryError(f"device allocation failed ({msg})")
+    if rc == ND_ERR_EMPTY:
+        raise EmptyGraphError(what or "no edges found")
     raise DeviceError(f"CUDA error ({msg})")
 
 

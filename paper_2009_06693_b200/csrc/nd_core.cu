@@ -532,6 +532,11 @@ static int build_from_edges_dev(const int64_t* src, const int64_t* dst, const do
   return ND_OK;
 }
 
+int nd_build_from_edges_dev(const int64_t* src, const int64_t* dst, const double* w, int64_t E,
+                            int64_t V, cudaStream_t s, nd_graph** out) {
+  return build_from_edges_dev(src, dst, w, E, V, s, out);
+}
+
 extern "C" int nd_graph_from_edges(const int64_t* src, const int64_t* dst, const double* weights,
                                    int64_t n_edges, int64_t n_vertices, void* stream,
                                    nd_graph** out) {

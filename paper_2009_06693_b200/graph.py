@@ -107,40 +107,54 @@ def from_edges(src, dst, weights=None, n_vertices=None, remap=None) -> Graph:
                  np.ascontiguousarray(w[order]), rm)
 
 
+def parse_edge_line(raw: str, line_no: int, weighted: bool, lo_w: float, hi_w: float,
+                    seed: int):
+    """One edge-list line under the reference's rules (graph.py:150-182):
+    None for blank/comment lines, else (src, dst, weight); raises
+    GraphParseError with the reference's messages.  Shared by the host parser
+    and by the device ingestion for the lines it leaves to the host."""
+    line = raw.strip()
+    if not line or line.startswith("#"):
+        return None
+    parts = line.split()
+    if len(parts) not in (2, 3):
+        raise GraphParseError(line_no, f"expected 2 or 3 fields, got {len(parts)}")
+    try:
+        s, d = int(parts[0]), int(parts[1])
+    except ValueError as exc:
+        raise GraphParseError(line_no, f"bad vertex id: {exc}") from None
+    if s < 0 or d < 0:
+        raise GraphParseError(line_no, "vertex ids must be non-negative")
+    if weighted:
+        if len(parts) == 3:
+            try:
+                w = float(parts[2])
+            except ValueError as exc:
+                raise GraphParseError(line_no, f"bad weight: {exc}") from None
+            if w < 0:
+                raise GraphParseError(line_no, "weight must be non-negative")
+        else:
+            w = lo_w + (hi_w - lo_w) * key_uniform(seed, sample_id=line_no,
+                                                   domain=DOMAIN_EDGE_WEIGHT)
+    else:
+        w = 1.0
+    return s, d, w
+
+
 def load_edge_list(path, weighted=False, default_weight_range=(1.0, 5.0), undirected=False,
                    seed=0) -> Graph:
-    """Edge-list parser with the reference's rules (graph.py:132-188):
+    """Host edge-list parser with the reference's rules (graph.py:132-188):
     '#' comments, 2 or 3 fields, ids compacted onto [0, n) with the original
-    ids in ``remap``, missing weights keyed on (seed, line number)."""
+    ids in ``remap``, missing weights keyed on (seed, line number).  The B200
+    path is ``DeviceGraph.from_edge_list`` (parse and CSR build on device)."""
     srcs, dsts, wts = [], [], []
     lo_w, hi_w = float(default_weight_range[0]), float(default_weight_range[1])
     with open(path, "r", encoding="utf-8") as fh:
         for line_no, raw in enumerate(fh, start=1):
-            line = raw.strip()
-            if not line or line.startswith("#"):
+            e = parse_edge_line(raw, line_no, weighted, lo_w, hi_w, seed)
+            if e is None:
                 continue
-            parts = line.split()
-            if len(parts) not in (2, 3):
-                raise GraphParseError(line_no, f"expected 2 or 3 fields, got {len(parts)}")
-            try:
-                s, d = int(parts[0]), int(parts[1])
-            except ValueError as exc:
-                raise GraphParseError(line_no, f"bad vertex id: {exc}") from None
-            if s < 0 or d < 0:
-                raise GraphParseError(line_no, "vertex ids must be non-negative")
-            if weighted:
-                if len(parts) == 3:
-                    try:
-                        w = float(parts[2])
-                    except ValueError as exc:
-                        raise GraphParseError(line_no, f"bad weight: {exc}") from None
-                    if w < 0:
-                        raise GraphParseError(line_no, "weight must be non-negative")
-                else:
-                    w = lo_w + (hi_w - lo_w) * key_uniform(seed, sample_id=line_no,
-                                                           domain=DOMAIN_EDGE_WEIGHT)
-            else:
-                w = 1.0
+            s, d, w = e
             srcs.append(s); dsts.append(d); wts.append(w)
             if undirected:
                 srcs.append(d); dsts.append(s); wts.append(w)
@@ -272,6 +286,73 @@ class DeviceGraph:
                                          int(n_vertices), _lib.stream_ptr(stream), C.byref(h)),
                    "nd_graph_from_edges")
         return cls(h)
+
+    @classmethod
+    def from_edge_list(cls, path, weighted=False, default_weight_range=(1.0, 5.0),
+                       undirected=False, seed=0, stream=None) -> "DeviceGraph":
+        """load_edge_list (graph.py:132-188) on device: the file's bytes are
+        parsed in HBM (nd_text_parse), the few lines the device leaves to the
+        host (non-ASCII, inexact numbers) go through ``parse_edge_line``, and
+        the CSR is built on device with the original ids as ``remap``.  Same
+        graph, same errors (GraphParseError line and message, EmptyGraphError)
+        as the reference's parser."""
+        _lib.require_cuda()
+        L = _lib.load()
+        with open(path, "rb") as fh:
+            data = fh.read()
+        if data and (np.frombuffer(data, dtype=np.uint8) >= 0x80).any():
+            data.decode("utf-8")  # the reference reads in text mode: invalid UTF-8 raises
+        lo_w, hi_w = float(default_weight_range[0]), float(default_weight_range[1])
+        info = (C.c_int64 * 4)()
+        t = C.c_void_p()
+        sp = _lib.stream_ptr(stream)
+        _lib.check(L.nd_text_parse(data, len(data), int(bool(weighted)), lo_w, hi_w,
+                                   C.c_uint64(seed & (2**64 - 1)), sp, C.byref(t), info),
+                   "nd_text_parse")
+        try:
+            n_lines, first_err, _code, n_host = (int(x) for x in info)
+            host_lines = np.empty(n_host, dtype=np.int64)
+            if n_host:
+                _lib.check(L.nd_text_host_lines(t, _lib.ptr(host_lines)), "nd_text_host_lines")
+
+            def line_text(k):
+                b = (C.c_int64 * 2)()
+                _lib.check(L.nd_text_line_bounds(t, int(k), b), "nd_text_line_bounds")
+                return data[b[0]:b[1]].decode("utf-8")
+
+            pl, ps, pd, pw, pk = [], [], [], [], []
+            for k in host_lines:  # ascending: the first error in line order wins
+                if first_err and k + 1 > first_err:
+                    break
+                e = parse_edge_line(line_text(k), int(k) + 1, weighted, lo_w, hi_w, seed)
+                pl.append(int(k))
+                if e is None:
+                    ps.append(0); pd.append(0); pw.append(1.0); pk.append(0)
+                else:
+                    ps.append(e[0]); pd.append(e[1]); pw.append(e[2]); pk.append(1)
+            if first_err:  # the device flagged it; the reference's message comes from re-parsing
+                parse_edge_line(line_text(first_err - 1), first_err, weighted, lo_w, hi_w, seed)
+                raise GraphParseError(first_err, "malformed line")  # not reached
+            arrs = [np.asarray(pl, np.int64), np.asarray(ps, np.int64), np.asarray(pd, np.int64),
+                    np.asarray(pw, np.float64), np.asarray(pk, np.uint8)]
+            h = C.c_void_p()
+            nv = C.c_int64()
+            rc = L.nd_text_finish(t, *[_lib.ptr(a) for a in arrs], len(pl), int(bool(undirected)),
+                                  sp, C.byref(h), C.byref(nv))
+            if rc == _lib.ND_ERR_EMPTY:
+                raise EmptyGraphError(f"{path}: no edges found")
+            _lib.check(rc, "nd_text_finish")
+            remap = np.empty(nv.value, dtype=np.int64)
+            _lib.check(L.nd_text_remap(t, _lib.ptr(remap)), "nd_text_remap")
+        finally:
+            L.nd_text_destroy(t)
+        return cls(h, remap=remap)
+
+    @classmethod
+    def from_cache(cls, path) -> "DeviceGraph":
+        """NDGR binary cache (graph.py:191-217) straight to HBM."""
+        g = load_cache(path)
+        return cls.from_arrays(g.row_offsets, g.col_indices, g.weights, remap=g.remap)
 
     @classmethod
     def rmat(cls, scale, edge_factor=16, seed=0, undirected=False, weighted=True,
