@@ -134,6 +134,10 @@ int nd_graph_from_edges(const int64_t *src, const int64_t *dst, const double *we
 typedef struct nd_text nd_text;
 int nd_text_parse(const char *host_text, int64_t n_bytes, int weighted, double lo_w, double hi_w,
                   uint64_t seed, void *stream, nd_text **out, int64_t *host_info);
+/* the same over bytes already in device memory (caller-owned, read-only) */
+int nd_text_parse_device(const char *dev_text, int64_t n_bytes, int weighted, double lo_w,
+                         double hi_w, uint64_t seed, void *stream, nd_text **out,
+                         int64_t *host_info);
 int nd_text_host_lines(const nd_text *t, int64_t *host_lines);
 int nd_text_line_bounds(const nd_text *t, int64_t line_index, int64_t *host_lo_hi);
 int nd_text_finish(nd_text *t, const int64_t *host_line, const int64_t *host_src,

@@ -40,6 +40,7 @@ SIGNATURES = {
     "nd_graph_from_edges": [vp, vp, vp, i64, i64, vp, pp],
     "nd_graph_rmat": [i32, i64, u32, u32, u32, u64, i32, i32, vp, pp],
     "nd_text_parse": [C.c_char_p, i64, i32, dbl, dbl, u64, vp, pp, pi64],
+    "nd_text_parse_device": [vp, i64, i32, dbl, dbl, u64, vp, pp, pi64],
     "nd_text_host_lines": [vp, vp],
     "nd_text_line_bounds": [vp, i64, pi64],
     "nd_text_finish": [vp, vp, vp, vp, vp, vp, i64, i32, vp, pp, pi64],

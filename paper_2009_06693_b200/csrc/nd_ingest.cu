@@ -357,10 +357,11 @@ int scan_op(const uint8_t* in, int64_t n, int64_t* out, cudaStream_t s) {
 
 extern "C" int nd_text_destroy(nd_text* T);
 
-extern "C" int nd_text_parse(const char* host_text, int64_t n_bytes, int weighted, double lo_w,
-                             double hi_w, uint64_t seed, void* stream, nd_text** out,
-                             int64_t* host_info) {
-  if (!out || !host_info || n_bytes < 0 || (n_bytes > 0 && !host_text)) return ND_ERR_ARG;
+static int text_parse(const char* host_text, const char* dev_text, int64_t n_bytes, int weighted,
+                      double lo_w, double hi_w, uint64_t seed, void* stream, nd_text** out,
+                      int64_t* host_info) {
+  if (!out || !host_info || n_bytes < 0 || (n_bytes > 0 && !host_text && !dev_text))
+    return ND_ERR_ARG;
   nd_pool_init();
   cudaStream_t s = (cudaStream_t)stream;
   nd_text* T = new nd_text();
@@ -377,14 +378,15 @@ extern "C" int nd_text_parse(const char* host_text, int64_t n_bytes, int weighte
     nd_text_destroy(T);
     return rc;
   };
-  if (nd_alloc(&text, n_bytes + 1, s) || nd_alloc(&flags, n_bytes + 1, s) ||
+  if ((!dev_text && nd_alloc(&text, n_bytes + 1, s)) || nd_alloc(&flags, n_bytes + 1, s) ||
       nd_alloc(&n_ends_d, 1, s) || nd_alloc(&ctl, 2, s))
     return fail(ND_ERR_NOMEM);
-  if (n_bytes) cudaMemcpyAsync(text, host_text, n_bytes, cudaMemcpyHostToDevice, s);
+  if (n_bytes && !dev_text) cudaMemcpyAsync(text, host_text, n_bytes, cudaMemcpyHostToDevice, s);
+  const uint8_t* tx = dev_text ? reinterpret_cast<const uint8_t*>(dev_text) : text;
   int64_t n_ends = 0, last_end = -1;
   if (n_bytes) {
     // count the terminators, then list their positions (no n_bytes-sized index array)
-    k_line_ends<<<nd_grid(n_bytes, 256, 148 * 32), 256, 0, s>>>(text, n_bytes, flags);
+    k_line_ends<<<nd_grid(n_bytes, 256, 148 * 32), 256, 0, s>>>(tx, n_bytes, flags);
     cub::TransformInputIterator<int64_t, U8ToI64, const uint8_t*> fl(flags, U8ToI64());
     size_t tb = 0;
     cub::DeviceReduce::Sum(nullptr, tb, fl, n_ends_d, n_bytes, s);
@@ -417,10 +419,10 @@ extern "C" int nd_text_parse(const char* host_text, int64_t n_bytes, int weighte
   const unsigned long long init[2] = {~0ull, 0ull};
   cudaMemcpyAsync(ctl, init, sizeof(init), cudaMemcpyHostToDevice, s);
   if (n_lines) {
-    k_line_bounds<<<nd_grid(n_lines, 256), 256, 0, s>>>(text, ends, n_ends, n_bytes, n_lines,
+    k_line_bounds<<<nd_grid(n_lines, 256), 256, 0, s>>>(tx, ends, n_ends, n_bytes, n_lines,
                                                         T->start, T->end);
     k_parse_lines<<<nd_grid(n_lines, 128, 148 * 64), 128, 0, s>>>(
-        text, n_lines, T->start, T->end, weighted, lo_w, hi_w - lo_w,
+        tx, n_lines, T->start, T->end, weighted, lo_w, hi_w - lo_w,
         key_base(seed, 0, 3, 0), T->kind, T->code, T->src, T->dst, T->w, ctl, ctl + 1);
   }
   unsigned long long hc[2];
@@ -441,6 +443,18 @@ extern "C" int nd_text_parse(const char* host_text, int64_t n_bytes, int weighte
   host_info[3] = h[1];  // lines for the host (non-ASCII / inexact numbers)
   *out = T;
   return ND_OK;
+}
+
+extern "C" int nd_text_parse(const char* host_text, int64_t n_bytes, int weighted, double lo_w,
+                             double hi_w, uint64_t seed, void* stream, nd_text** out,
+                             int64_t* host_info) {
+  return text_parse(host_text, nullptr, n_bytes, weighted, lo_w, hi_w, seed, stream, out, host_info);
+}
+
+extern "C" int nd_text_parse_device(const char* dev_text, int64_t n_bytes, int weighted,
+                                    double lo_w, double hi_w, uint64_t seed, void* stream,
+                                    nd_text** out, int64_t* host_info) {
+  return text_parse(nullptr, dev_text, n_bytes, weighted, lo_w, hi_w, seed, stream, out, host_info);
 }
 
 extern "C" int nd_text_host_lines(const nd_text* T, int64_t* host_lines) {

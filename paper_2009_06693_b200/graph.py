@@ -296,19 +296,21 @@ class DeviceGraph:
         the CSR is built on device with the original ids as ``remap``.  Same
         graph, same errors (GraphParseError line and message, EmptyGraphError)
         as the reference's parser."""
-        _lib.require_cuda()
+        torch = _lib.require_cuda()
         L = _lib.load()
-        with open(path, "rb") as fh:
-            data = fh.read()
-        if data and (np.frombuffer(data, dtype=np.uint8) >= 0x80).any():
-            data.decode("utf-8")  # the reference reads in text mode: invalid UTF-8 raises
+        # the file streams into HBM through pinned staging buffers (parallel
+        # reads, async copies); non-ASCII lines are decoded on the host below,
+        # so invalid UTF-8 raises UnicodeDecodeError as the reference's
+        # text-mode read does
+        text = _upload_file(path, torch)
         lo_w, hi_w = float(default_weight_range[0]), float(default_weight_range[1])
         info = (C.c_int64 * 4)()
         t = C.c_void_p()
         sp = _lib.stream_ptr(stream)
-        _lib.check(L.nd_text_parse(data, len(data), int(bool(weighted)), lo_w, hi_w,
-                                   C.c_uint64(seed & (2**64 - 1)), sp, C.byref(t), info),
-                   "nd_text_parse")
+        _lib.check(L.nd_text_parse_device(C.c_void_p(text.data_ptr()), text.numel(),
+                                          int(bool(weighted)), lo_w, hi_w,
+                                          C.c_uint64(seed & (2**64 - 1)), sp, C.byref(t), info),
+                   "nd_text_parse_device")
         try:
             n_lines, first_err, _code, n_host = (int(x) for x in info)
             host_lines = np.empty(n_host, dtype=np.int64)
@@ -318,7 +320,7 @@ class DeviceGraph:
             def line_text(k):
                 b = (C.c_int64 * 2)()
                 _lib.check(L.nd_text_line_bounds(t, int(k), b), "nd_text_line_bounds")
-                return data[b[0]:b[1]].decode("utf-8")
+                return text[b[0]:b[1]].cpu().numpy().tobytes().decode("utf-8")
 
             pl, ps, pd, pw, pk = [], [], [], [], []
             for k in host_lines:  # ascending: the first error in line order wins
@@ -406,6 +408,57 @@ class DeviceGraph:
             self.close()
         except Exception:
             pass
+
+
+_STAGE = []  # pinned staging buffers of _upload_file (allocated once per process)
+_STAGE_BYTES, _STAGE_N = 32 << 20, 8
+
+
+def _upload_file(path, torch):
+    """File bytes -> a device uint8 tensor: _STAGE_N readers fill pinned 32 MB
+    buffers with os.preadv (the GIL is released) while earlier chunks copy
+    host->device asynchronously on the current stream."""
+    import concurrent.futures as cf
+    import os
+    size = os.path.getsize(path)
+    dev = torch.empty(max(size, 1), dtype=torch.uint8, device="cuda")[:size]
+    if size == 0:
+        return dev
+    while len(_STAGE) < _STAGE_N:
+        _STAGE.append(torch.empty(_STAGE_BYTES, dtype=torch.uint8).pin_memory())
+    chunks = [(off, min(_STAGE_BYTES, size - off)) for off in range(0, size, _STAGE_BYTES)]
+    events = [None] * _STAGE_N
+    fd = os.open(path, os.O_RDONLY)
+    try:
+        def read(i):
+            off, n = chunks[i]
+            mv = memoryview(_STAGE[i % _STAGE_N].numpy())[:n]
+            got = 0
+            while got < n:
+                r = os.preadv(fd, [mv[got:]], off + got)
+                if r <= 0:
+                    raise OSError(f"{path}: short read")
+                got += r
+            return i
+
+        with cf.ThreadPoolExecutor(_STAGE_N) as ex:
+            pending, nxt = {}, 0
+            for i in range(len(chunks)):
+                while nxt < len(chunks) and nxt < i + _STAGE_N:
+                    b = nxt % _STAGE_N
+                    if events[b] is not None:
+                        events[b].synchronize()  # its previous chunk has left the buffer
+                    pending[nxt] = ex.submit(read, nxt)
+                    nxt += 1
+                pending.pop(i).result()
+                off, n = chunks[i]
+                dev[off:off + n].copy_(_STAGE[i % _STAGE_N][:n], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record()
+                events[i % _STAGE_N] = ev
+    finally:
+        os.close(fd)
+    return dev
 
 
 def as_device_graph(graph) -> DeviceGraph:
