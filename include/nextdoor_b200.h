@@ -209,7 +209,8 @@ int nd_transit_schedule(const int64_t *pair_transit, int64_t n_pairs, int64_t m,
 /* ---- results (output.py:43-69) ----------------------------------------------------
  * A result owns device buffers.  Field ids for nd_result_field: */
 #define ND_F_FINAL_OFF 0   /* int64 [n+1] final-layout row offsets          */
-#define ND_F_FINAL_IDS 1   /* int64 [total] roots + non-NULL sampled ids    */
+#define ND_F_FINAL_IDS 1   /* int64 [total] roots + non-NULL sampled ids
+                           (derived from ND_F_FINAL_IDS32 on first request) */
 #define ND_F_ROOTS 2       /* int64 [n*R] (walks) / ragged (others) roots  */
 #define ND_F_ROOTS_OFF 3   /* int64 [n+1]                                  */
 #define ND_F_CHAIN_LEN 4   /* int64 [n] walk chain lengths (NULL included) */
@@ -220,7 +221,9 @@ int nd_transit_schedule(const int64_t *pair_transit, int64_t n_pairs, int64_t m,
 #define ND_F_REC_V 9       /* int64 recorded edge targets                  */
 #define ND_F_STATS 10      /* int64 [S*4] {small, medium, large, fetches}  */
 #define ND_F_CHAIN_VALS 11 /* int64 walk chains incl. NULL (multirw)       */
-#define ND_F_FINAL_IDS32 12 /* int32 [total] FINAL_IDS narrowed (nd_result_narrow_ids) */
+#define ND_F_FINAL_IDS32 12 /* int32 [total] the final ids as every run writes them */
+#define ND_F_STEP_VALS32 13 /* int32 step-major slot values (k-hop runs write these;
+                               ND_F_STEP_VALS is derived from them on request) */
 int nd_result_info(const nd_result *r, int64_t *n_samples, int64_t *n_steps,
                    int64_t *total_sampled, int64_t *total_recorded);
 /* device pointer + element count of one field (ptr NULL if absent) */
@@ -229,9 +232,9 @@ int nd_result_field(const nd_result *r, int field, const void **ptr, int64_t *co
  * slot_bytes (SURVEY 8(d) model bytes), steps, launches, rand_sectors (random
  * 32-byte sector reads the walk kernels issued)} */
 int nd_result_counters(const nd_result *r, int64_t *host_counters, int64_t n);
-/* Fill ND_F_FINAL_IDS32: the final ids as int32 (vertex ids < 2^31, the
- * device CSR's column width), halving the device->host bytes of a result
- * read.  Idempotent; enqueued on `stream`. */
+/* Ensure ND_F_FINAL_IDS32 (int32 final ids; vertex ids < 2^31, the device
+ * CSR's column width).  Every run now writes it directly, so this is a no-op
+ * kept for callers of the round-1 ABI. */
 int nd_result_narrow_ids(nd_result *r, void *stream);
 /* copy a field into caller memory (host or device; cudaMemcpyDefault) on
  * `stream`; synchronous when stream is NULL */

@@ -18,8 +18,8 @@ LIB_PATH = os.path.join(HERE, "libnextdoor_b200.so")
 ND_OK, ND_ERR_STALL, ND_ERR_APP, ND_ERR_ARG, ND_ERR_CUDA, ND_ERR_NOMEM, ND_ERR_EMPTY = range(7)
 ND_SP, ND_TP = 0, 1
 (F_FINAL_OFF, F_FINAL_IDS, F_ROOTS, F_ROOTS_OFF, F_CHAIN_LEN, F_STEP_COUNTS, F_STEP_VALS,
- F_REC_COUNTS, F_REC_T, F_REC_V, F_STATS, F_CHAIN_VALS, F_FINAL_IDS32) = range(13)
-FIELD_DTYPE = {F_FINAL_IDS32: "int32"}  # every other result field is int64
+ F_REC_COUNTS, F_REC_T, F_REC_V, F_STATS, F_CHAIN_VALS, F_FINAL_IDS32, F_STEP_VALS32) = range(14)
+FIELD_DTYPE = {F_FINAL_IDS32: "int32", F_STEP_VALS32: "int32"}  # every other field is int64
 
 vp, i64, u64, i32, u32, dbl = C.c_void_p, C.c_int64, C.c_uint64, C.c_int, C.c_uint32, C.c_double
 pp = C.POINTER(C.c_void_p)

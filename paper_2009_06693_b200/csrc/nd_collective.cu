@@ -425,7 +425,7 @@ __global__ void k_narrow64(const int64_t* __restrict__ a, int64_t n, int32_t* __
 // samples (blockIdx.y) and threads over a sample's entries, so one huge
 // sample (ClusterGCN: ~20% of V roots) is copied by many blocks, coalesced.
 __global__ void k_coll_final(const int64_t* __restrict__ roff, const int32_t* __restrict__ roots,
-                             int64_t n, const int64_t* __restrict__ off, int64_t* __restrict__ ids) {
+                             int64_t n, const int64_t* __restrict__ off, int32_t* __restrict__ ids) {
   for (int64_t i = blockIdx.y; i < n; i += gridDim.y) {
     const int64_t a = roff[i], len = roff[i + 1] - a, o = off[i];
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < len;
@@ -436,7 +436,7 @@ __global__ void k_coll_final(const int64_t* __restrict__ roff, const int32_t* __
 
 __global__ void k_coll_final_step(const int32_t* __restrict__ ntv, const int64_t* __restrict__ ntoff,
                                   int64_t n, const int64_t* __restrict__ off,
-                                  const int64_t* __restrict__ fill, int64_t* __restrict__ ids) {
+                                  const int64_t* __restrict__ fill, int32_t* __restrict__ ids) {
   for (int64_t i = blockIdx.y; i < n; i += gridDim.y) {
     const int64_t a = ntoff[i], len = ntoff[i + 1] - a, o = off[i] + fill[i];
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < len;
@@ -795,7 +795,8 @@ extern "C" int nd_run_collective(const nd_graph* G, int kind, int64_t step_size,
   ND_CUDA_TRY(cudaStreamSynchronize(s));
 
   // ---- outputs ------------------------------------------------------------------------
-  int64_t *final_off = nullptr, *final_ids = nullptr, *flen = nullptr, *fill = nullptr,
+  int32_t* final_ids = nullptr;  // int32 vertex ids (F_FINAL_IDS32; int64 derived on request)
+  int64_t *final_off = nullptr, *flen = nullptr, *fill = nullptr,
           *roots_out = nullptr, *roots_off = nullptr, *step_counts = nullptr, *step_vals = nullptr,
           *rec_counts = nullptr, *rec_t = nullptr, *rec_v = nullptr;
   ND_CUDA_TRY(nd_alloc(&flen, n + 1, s));
@@ -864,7 +865,7 @@ extern "C" int nd_run_collective(const nd_graph* G, int kind, int64_t step_size,
   res->total_sampled = total - n_roots;
   res->total_recorded = total_rec;
   res->set(ND_F_FINAL_OFF, final_off, n + 1);
-  res->set(ND_F_FINAL_IDS, final_ids, total);
+  res->set(ND_F_FINAL_IDS32, final_ids, total);
   res->set(ND_F_ROOTS, roots_out, n_roots);
   res->set(ND_F_ROOTS_OFF, roots_off, n + 1);
   res->set(ND_F_STEP_COUNTS, step_counts, n_steps * n);

@@ -692,8 +692,47 @@ extern "C" int nd_result_info(const nd_result* r, int64_t* n_samples, int64_t* n
   return ND_OK;
 }
 
+// Runs write the final ids once, as int32 (ND_F_FINAL_IDS32: half the bytes of
+// every read and gather).  The reference-width int64 field is derived on the
+// first request, on the result's stream, and kept.
+__global__ void k_widen_ids(const int32_t* __restrict__ in, int64_t n, int64_t* __restrict__ out) {
+  const int64_t half = n >> 1;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < half; i += stride) {
+    const int2 x = reinterpret_cast<const int2*>(in)[i];
+    reinterpret_cast<longlong2*>(out)[i] = make_longlong2(x.x, x.y);
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) out[n - 1] = in[n - 1];
+}
+
+static std::mutex g_result_mu;
+
+// int64 field `f64` derived from its int32 source `f32` on first request
+static int ensure_wide(const nd_result* rc, int f64, int f32) {
+  nd_result* r = const_cast<nd_result*>(rc);
+  std::lock_guard<std::mutex> lock(g_result_mu);
+  if (r->ptr[f64] || !r->ptr[f32]) return ND_OK;
+  const int64_t n = r->cnt[f32];
+  int64_t* out = nullptr;
+  ND_CUDA_TRY(nd_alloc(&out, n > 0 ? n : 1, r->stream));
+  if (n)
+    k_widen_ids<<<nd_grid((n + 1) / 2, 256, 148 * 16), 256, 0, r->stream>>>(
+        static_cast<const int32_t*>(r->ptr[f32]), n, out);
+  ND_CUDA_TRY(cudaGetLastError());
+  ND_CUDA_TRY(cudaStreamSynchronize(r->stream));
+  r->set(f64, out, n);
+  return ND_OK;
+}
+
+static int ensure_derived(const nd_result* r, int field) {
+  if (field == ND_F_FINAL_IDS) return ensure_wide(r, ND_F_FINAL_IDS, ND_F_FINAL_IDS32);
+  if (field == ND_F_STEP_VALS) return ensure_wide(r, ND_F_STEP_VALS, ND_F_STEP_VALS32);
+  return ND_OK;
+}
+
 extern "C" int nd_result_field(const nd_result* r, int field, const void** ptr, int64_t* count) {
   if (!r || field < 0 || field >= ND_N_FIELDS) return ND_ERR_ARG;
+  ND_TRY(ensure_derived(r, field));
   *ptr = r->ptr[field];
   *count = r->cnt[field];
   return ND_OK;
@@ -707,6 +746,7 @@ extern "C" int nd_result_counters(const nd_result* r, int64_t* host_counters, in
 
 extern "C" int nd_result_copy(const nd_result* r, int field, void* dst, void* stream) {
   if (!r || field < 0 || field >= ND_N_FIELDS) return ND_ERR_ARG;
+  ND_TRY(ensure_derived(r, field));
   if (!r->ptr[field] || !r->cnt[field]) return ND_OK;
   cudaStream_t s = (cudaStream_t)stream;
   ND_CUDA_TRY(cudaMemcpyAsync(dst, r->ptr[field], r->cnt[field] * r->esz[field], cudaMemcpyDefault, s));

@@ -279,21 +279,15 @@ __global__ void k_keep_write(const uint32_t* __restrict__ pt, const int64_t* __r
     }
 }
 
-__global__ void k_widen(const int32_t* __restrict__ in, int64_t n, int64_t* __restrict__ out) {
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
-       j += (int64_t)gridDim.x * blockDim.x)
-    out[j] = in[j];
-}
-
 // final rows: roots, then each step's compacted values at R + cum + tix
 template <typename RootT>
 __global__ void k_ind_roots(const RootT* __restrict__ roots, int64_t n, int64_t R,
-                            const int64_t* __restrict__ off, int64_t* __restrict__ ids,
+                            const int64_t* __restrict__ off, int32_t* __restrict__ ids,
                             int64_t* __restrict__ roots_out, int64_t* __restrict__ roots_off) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * R;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t s = i / R;
-    ids[off[s] + (i - s * R)] = (int64_t)roots[i];
+    ids[off[s] + (i - s * R)] = (int32_t)roots[i];
     roots_out[i] = (int64_t)roots[i];
     if (i - s * R == 0) roots_off[s] = s * R;
     if (i == n * R - 1) roots_off[n] = n * R;
@@ -303,11 +297,11 @@ __global__ void k_ind_roots(const RootT* __restrict__ roots, int64_t n, int64_t 
 __global__ void k_ind_final(const uint32_t* __restrict__ npt, const int32_t* __restrict__ npsid,
                             const int32_t* __restrict__ nptix, int64_t cnt,
                             const int64_t* __restrict__ off, const int64_t* __restrict__ cum,
-                            int64_t R, int64_t* __restrict__ ids) {
+                            int64_t R, int32_t* __restrict__ ids) {
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < cnt;
        j += (int64_t)gridDim.x * blockDim.x) {
     const int32_t s = npsid[j];
-    ids[off[s] + R + cum[s] + nptix[j]] = (int64_t)npt[j];
+    ids[off[s] + R + cum[s] + nptix[j]] = (int32_t)npt[j];
   }
 }
 
@@ -580,8 +574,9 @@ extern "C" int nd_run_individual(const nd_graph* G, int app_code, const double* 
   }
   const int64_t n_steps = step;
   // ---- outputs ------------------------------------------------------------------
-  int64_t *flen = nullptr, *final_off = nullptr, *final_ids = nullptr, *roots_out = nullptr,
-          *roots_off = nullptr, *step_vals = nullptr;
+  int32_t* final_ids = nullptr;  // int32 vertex ids (F_FINAL_IDS32; int64 derived on request)
+  int32_t* step_vals = nullptr;  // int32 (F_STEP_VALS32; int64 derived on request)
+  int64_t *flen = nullptr, *final_off = nullptr, *roots_out = nullptr, *roots_off = nullptr;
   ND_CUDA_TRY(nd_alloc(&flen, n + 1, s));
   ND_CUDA_TRY(nd_alloc(&final_off, n + 1, s));
   ND_CUDA_TRY(nd_alloc(&roots_out, n * R, s));
@@ -622,11 +617,13 @@ extern "C" int nd_run_individual(const nd_graph* G, int app_code, const double* 
                                                           final_off, sd.cum, R, final_ids);
     if (sd.dedup) {
       if (sd.nnext)
-        k_widen<<<nd_grid(sd.nnext, 256), 256, 0, s>>>(reinterpret_cast<const int32_t*>(sd.npt),
-                                                       sd.nnext, step_vals + pos);
+        ND_CUDA_TRY(cudaMemcpyAsync(step_vals + pos, sd.npt, sd.nnext * sizeof(int32_t),
+                                    cudaMemcpyDeviceToDevice, s));
       pos += sd.nnext;
     } else {
-      if (sd.items) k_widen<<<nd_grid(sd.items, 256), 256, 0, s>>>(sd.out, sd.items, step_vals + pos);
+      if (sd.items)
+        ND_CUDA_TRY(cudaMemcpyAsync(step_vals + pos, sd.out, sd.items * sizeof(int32_t),
+                                    cudaMemcpyDeviceToDevice, s));
       pos += sd.items;
     }
   }
@@ -660,11 +657,11 @@ extern "C" int nd_run_individual(const nd_graph* G, int app_code, const double* 
   res->n_steps = n_steps;
   res->total_sampled = total - n * R;
   res->set(ND_F_FINAL_OFF, final_off, n + 1);
-  res->set(ND_F_FINAL_IDS, final_ids, total);
+  res->set(ND_F_FINAL_IDS32, final_ids, total);
   res->set(ND_F_ROOTS, roots_out, n * R);
   res->set(ND_F_ROOTS_OFF, roots_off, n + 1);
   res->set(ND_F_STEP_COUNTS, step_counts, n_steps * n);
-  res->set(ND_F_STEP_VALS, step_vals, total_items);
+  res->set(ND_F_STEP_VALS32, step_vals, total_items);
   res->set(ND_F_STATS, stats, 4 * n_steps);
   res->counters[NDC_ITEMS] = total_items;
   res->counters[NDC_SLOT_BYTES] = (int64_t)h_ctr[0];

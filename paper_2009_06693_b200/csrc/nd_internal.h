@@ -27,7 +27,7 @@ struct nd_graph {
   int device = 0;
 };
 
-constexpr int ND_N_FIELDS = 13;
+constexpr int ND_N_FIELDS = 14;
 constexpr int ND_N_COUNTERS = 10;
 
 struct nd_result {
@@ -37,7 +37,7 @@ struct nd_result {
   int64_t total_recorded = 0;
   void* ptr[ND_N_FIELDS] = {};
   int64_t cnt[ND_N_FIELDS] = {};
-  int esz[ND_N_FIELDS] = {8, 8, 8, 8, 8, 8, 8, 8, 8, 8, 8, 8, 4};  // bytes per element
+  int esz[ND_N_FIELDS] = {8, 8, 8, 8, 8, 8, 8, 8, 8, 8, 8, 8, 4, 4};  // bytes per element
   int64_t counters[ND_N_COUNTERS] = {};
   double prof_ms[4] = {};  // schedule, sample, compaction (nd_set_profiling)
   cudaStream_t stream = nullptr;

@@ -125,13 +125,13 @@ __global__ void k_chain_lengths(const int32_t* __restrict__ dstep, int64_t n, in
 
 template <typename RootT>
 __global__ void k_write_roots(const RootT* __restrict__ roots, int64_t n, int64_t R,
-                              const int64_t* __restrict__ off, int64_t* __restrict__ ids,
+                              const int64_t* __restrict__ off, int32_t* __restrict__ ids,
                               int64_t* __restrict__ roots_out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * R;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t w = i / R, k = i - w * R;
     const int64_t r = (int64_t)roots[i];
-    ids[off[w] + k] = r;
+    ids[off[w] + k] = (int32_t)r;
     if (roots_out) roots_out[i] = r;
   }
 }
@@ -139,7 +139,7 @@ __global__ void k_write_roots(const RootT* __restrict__ roots, int64_t n, int64_
 __global__ void k_scatter_records(const int32_t* __restrict__ rec_w, const int32_t* __restrict__ rec_v,
                                   int64_t total, const int64_t* __restrict__ step_base,
                                   int64_t n_steps, const int64_t* __restrict__ off, int64_t R,
-                                  int64_t* __restrict__ ids) {
+                                  int32_t* __restrict__ ids) {
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < total;
        r += (int64_t)gridDim.x * blockDim.x) {
     const int32_t v = rec_v[r];
@@ -166,7 +166,7 @@ __global__ void k_slab_counts(const int32_t* __restrict__ slab, int64_t n, int64
 }
 
 __global__ void k_slab_write(const int32_t* __restrict__ slab, int64_t n, int64_t S, int64_t R,
-                             const int64_t* __restrict__ off, int64_t* __restrict__ ids,
+                             const int64_t* __restrict__ off, int32_t* __restrict__ ids,
                              int64_t* __restrict__ chain) {
   for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < n;
        w += (int64_t)gridDim.x * blockDim.x) {
@@ -962,19 +962,19 @@ __global__ void k_pw_lengths(const int64_t* __restrict__ tot, const int32_t* __r
 }
 
 // copy one window's rows into the final layout: one warp per row, lanes
-// stream the row's non-NULL prefix (int32 reads, int64 writes, both coalesced)
+// stream the row's non-NULL prefix (int32 reads and writes, both coalesced)
 __global__ void k_pw_emit(const int32_t* __restrict__ wid, const int32_t* __restrict__ out,
                           const int32_t* __restrict__ nnz, int64_t n, int64_t Lw, int64_t step0,
-                          const int64_t* __restrict__ off, int64_t R, int64_t* __restrict__ ids) {
+                          const int64_t* __restrict__ off, int64_t R, int32_t* __restrict__ ids) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t r = warp; r < n; r += nw) {
     const int64_t k_end = nnz[r];
     const int64_t w = wid ? wid[r] : r;
-    int64_t* dst = ids + off[w] + R + step0;
+    int32_t* dst = ids + off[w] + R + step0;
     const int32_t* src = out + r * Lw;
-    for (int64_t k = lane; k < k_end; k += 32) dst[k] = (int64_t)src[k];
+    for (int64_t k = lane; k < k_end; k += 32) dst[k] = src[k];
   }
 }
 
@@ -1111,7 +1111,8 @@ static int run_chain_walk(const nd_graph* G, const NdApp& a, int64_t sample_lo, 
   // ---- output compaction -----------------------------------------------------------
   prof.mark();
   const size_t ef = prof.ev.size() - 1;
-  int64_t *flen = nullptr, *final_off = nullptr, *clen = nullptr, *final_ids = nullptr,
+  int32_t* final_ids = nullptr;  // int32 vertex ids (F_FINAL_IDS32; int64 derived on request)
+  int64_t *flen = nullptr, *final_off = nullptr, *clen = nullptr,
           *roots_out = nullptr, *d_step_base = nullptr;
   ND_CUDA_TRY(nd_alloc(&flen, n + 1, s));
   ND_CUDA_TRY(nd_alloc(&final_off, n + 1, s));
@@ -1160,7 +1161,7 @@ static int run_chain_walk(const nd_graph* G, const NdApp& a, int64_t sample_lo, 
   res->n_steps = n_steps;
   res->total_sampled = total - n * R;
   res->set(ND_F_FINAL_OFF, final_off, n + 1);
-  res->set(ND_F_FINAL_IDS, final_ids, total);
+  res->set(ND_F_FINAL_IDS32, final_ids, total);
   res->set(ND_F_ROOTS, roots_out, n * R);
   res->set(ND_F_CHAIN_LEN, clen, n);
   res->set(ND_F_STATS, stats, 4 * n_steps);
@@ -1312,7 +1313,8 @@ static int run_chain_walk_sp(const nd_graph* G, const NdApp& a, int64_t sample_l
   // ---- compaction into the final layout -------------------------------------------
   nd_trace("sp:windows-done");
   if (g_profile) cudaEventRecord(pe0, s);
-  int64_t *flen = nullptr, *final_off = nullptr, *clen = nullptr, *final_ids = nullptr,
+  int32_t* final_ids = nullptr;  // int32 vertex ids (F_FINAL_IDS32; int64 derived on request)
+  int64_t *flen = nullptr, *final_off = nullptr, *clen = nullptr,
           *roots_out = nullptr;
   unsigned long long *hist = nullptr, *stats = nullptr;
   ND_CUDA_TRY(nd_alloc(&flen, n + 1, s));
@@ -1381,7 +1383,7 @@ static int run_chain_walk_sp(const nd_graph* G, const NdApp& a, int64_t sample_l
   res->n_steps = n_steps;
   res->total_sampled = total - n * R;
   res->set(ND_F_FINAL_OFF, final_off, n + 1);
-  res->set(ND_F_FINAL_IDS, final_ids, total);
+  res->set(ND_F_FINAL_IDS32, final_ids, total);
   res->set(ND_F_ROOTS, roots_out, n * R);
   res->set(ND_F_CHAIN_LEN, clen, n);
   res->set(ND_F_STATS, stats, 4 * n_steps);
@@ -1456,7 +1458,8 @@ static int run_rootpick_walk(const nd_graph* G, const NdApp& a, int64_t sample_l
   }
   prof.mark();
   const size_t ef = prof.ev.size() - 1;
-  int64_t *flen = nullptr, *final_off = nullptr, *final_ids = nullptr, *roots_out = nullptr,
+  int32_t* final_ids = nullptr;  // int32 vertex ids (F_FINAL_IDS32; int64 derived on request)
+  int64_t *flen = nullptr, *final_off = nullptr, *roots_out = nullptr,
           *chain = nullptr, *clen = nullptr;
   ND_CUDA_TRY(nd_alloc(&flen, n + 1, s));
   ND_CUDA_TRY(nd_alloc(&final_off, n + 1, s));
@@ -1499,7 +1502,7 @@ static int run_rootpick_walk(const nd_graph* G, const NdApp& a, int64_t sample_l
   res->n_steps = n_steps;
   res->total_sampled = total - n * R;
   res->set(ND_F_FINAL_OFF, final_off, n + 1);
-  res->set(ND_F_FINAL_IDS, final_ids, total);
+  res->set(ND_F_FINAL_IDS32, final_ids, total);
   res->set(ND_F_ROOTS, roots_out, n * R);
   res->set(ND_F_CHAIN_LEN, clen, n);
   res->set(ND_F_CHAIN_VALS, chain, n * n_steps);
