@@ -80,3 +80,16 @@ def test_device_cache_roundtrip(tmp_path):
     h = dg.to_host()
     _same_graph(case, h.row_offsets, h.col_indices, h.weights, h.remap)
     dg.close()
+
+
+@pytest.mark.gpu
+def test_readme_quickstart(tmp_path):
+    """The README's usage snippet: ingest on device, sample, read rows."""
+    from paper_2009_06693_b200 import EngineConfig, make_app, make_samples, sp_run
+    from paper_2009_06693_b200.graph import DeviceGraph
+    case = next(c for c in META if c["name"] == "big_mixed")
+    g = DeviceGraph.from_edge_list(_write(tmp_path, case), weighted=True)
+    app = make_app("node2vec")
+    out = sp_run(app, g, make_samples(app, g, 1000, seed=7), EngineConfig(seed=7))
+    rows = out.final_rows()
+    assert len(rows) == 1000 and all(len(r) >= 1 for r in rows)
