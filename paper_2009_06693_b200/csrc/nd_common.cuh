@@ -156,6 +156,26 @@ struct __align__(16) NbrU {   // unit-weight graphs: neighbour + its header
   int64_t lo;
 };
 
+// Line-packed weighted-pick rows (DeepWalk / PPR).  A random read pulls a
+// 128-byte line from HBM anyway, so each line carries three consecutive pick
+// records of a row AND the guide entries of those three buckets (plus the
+// next bucket's): the exact-bucket bracket and the records around it are
+// usually in the line the bucket lands in.  Rows start on a line boundary
+// (vline[v] = first line of v).
+struct __align__(32) PickRec {
+  double pre;     // inclusive prefix of this edge
+  double total;   // prefix total of col's row (its pick target scale)
+  int32_t col;
+  int32_t deg;    // col's degree
+  int32_t llo;    // col's first line
+  int32_t pad;
+};
+struct __align__(128) PickLine {
+  PickRec r[3];   // edges 3L .. 3L+2 of the row (+inf prefix past its end)
+  int32_t g[4];   // guide[3L .. 3L+3] (deg past the row's end)
+  int32_t spare[4];
+};
+
 struct DevGraph {
   int64_t V = 0, E = 0;
   const int64_t* row = nullptr;
@@ -171,6 +191,8 @@ struct DevGraph {
   const NbrW* nbw = nullptr;      // optional neighbour records (node2vec tries)
   const NbrP* nbp = nullptr;      // optional neighbour records (weighted picks)
   const NbrU* nbu = nullptr;      // optional neighbour records (unit graphs)
+  const PickLine* pl = nullptr;   // optional line-packed pick rows (weighted graphs)
+  const int32_t* vline = nullptr; // [V] first line of each row (with pl)
   int unit = 0;
 };
 

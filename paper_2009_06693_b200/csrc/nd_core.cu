@@ -350,6 +350,8 @@ extern "C" int nd_graph_destroy(nd_graph* G) {
   cudaFree(G->nbw);
   cudaFree(G->nbp);
   cudaFree(G->nbu);
+  cudaFree(G->pl);
+  cudaFree(G->vline);
   delete G;
   return ND_OK;
 }

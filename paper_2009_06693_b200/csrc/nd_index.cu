@@ -6,6 +6,8 @@
 //     _ckernels.pyx:77-87): open addressing, linear probing, load <= 1/2.
 // Built once per graph on first use; answers are identical to the binary
 // searches they replace (tests/test_gpu_kernels.py::test_index_equivalence).
+#include <cub/cub.cuh>
+
 #include <cstdlib>
 #include <mutex>
 
@@ -111,6 +113,70 @@ __global__ void k_build_nbr(const int64_t* __restrict__ row, const int32_t* __re
   }
 }
 
+// lines per row: ceil(deg / 3)
+__global__ void k_line_counts(const int64_t* __restrict__ row, int64_t V, int64_t* __restrict__ cnt) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v <= V;
+       v += (int64_t)gridDim.x * blockDim.x)
+    cnt[v] = v < V ? (row[v + 1] - row[v] + 2) / 3 : 0;
+}
+
+__global__ void k_vline32(const int64_t* __restrict__ first, int64_t V, int32_t* __restrict__ out) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V;
+       v += (int64_t)gridDim.x * blockDim.x)
+    out[v] = (int32_t)first[v];
+}
+
+// one warp per row, a lane per line: the line's three records and
+// guide[j] = upper_bound(prefix row, rn(rn(total/deg) * j)) for its four
+// buckets, exactly as k_build_guide
+__global__ void k_build_lines(const int64_t* __restrict__ row, const int32_t* __restrict__ col,
+                              const double* __restrict__ pre, const int32_t* __restrict__ vline,
+                              int64_t V, PickLine* __restrict__ pl) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t v = warp; v < V; v += nw) {
+    const int64_t lo = row[v], deg = row[v + 1] - lo;
+    if (deg <= 0) continue;
+    const double total = pre[lo + deg - 1];
+    const double width = __ddiv_rn(total, (double)deg);
+    const int64_t n_lines = (deg + 2) / 3;
+    for (int64_t L = lane; L < n_lines; L += 32) {
+      PickLine ln;
+      for (int q = 0; q < 4; q++) {
+        const int64_t j = 3 * L + q;
+        int64_t a = deg;
+        if (j < deg && width > 0.0) {
+          const double y = __dmul_rn(width, (double)j);
+          int64_t b = deg;
+          a = 0;
+          while (a < b) {
+            const int64_t mid = (a + b) >> 1;
+            if (pre[lo + mid] <= y) a = mid + 1; else b = mid;
+          }
+        }
+        ln.g[q] = (int32_t)a;
+      }
+      for (int q = 0; q < 3; q++) {
+        const int64_t k = 3 * L + q;
+        PickRec r{__longlong_as_double(0x7FF0000000000000ll), 0.0, -1, 0, 0, 0};
+        if (k < deg) {
+          const int32_t u = col[lo + k];
+          const int64_t ulo = row[u], udeg = row[u + 1] - ulo;
+          r.pre = pre[lo + k];
+          r.total = udeg > 0 ? pre[ulo + udeg - 1] : 0.0;
+          r.col = u;
+          r.deg = (int32_t)udeg;
+          r.llo = vline[u];
+        }
+        ln.r[q] = r;
+      }
+      ln.spare[0] = ln.spare[1] = ln.spare[2] = ln.spare[3] = 0;
+      pl[vline[v] + L] = ln;
+    }
+  }
+}
+
 }  // namespace
 
 // lazy index builds may be requested by concurrent runs on one graph
@@ -180,6 +246,45 @@ int nd_graph_ensure_index(nd_graph* G, int want_hset, int want_guide, cudaStream
     ND_CUDA_TRY(cudaStreamSynchronize(s));
     G->g.hset = G->hset;
   }
+  return ND_OK;
+}
+
+int nd_graph_ensure_lines(nd_graph* G, cudaStream_t s) {
+  static const bool disabled = getenv("ND_NO_LINES") && getenv("ND_NO_LINES")[0] == '1';
+  if (disabled || G->g.unit || G->g.E <= 0) return ND_OK;
+  std::lock_guard<std::mutex> lock(g_index_mu);
+  if (G->pl) return ND_OK;
+  const int64_t V = G->g.V;
+  int64_t *cnt = nullptr, *first = nullptr;
+  ND_CUDA_TRY(nd_alloc(&cnt, V + 1, s));
+  ND_CUDA_TRY(nd_alloc(&first, V + 1, s));
+  k_line_counts<<<nd_grid(V + 1, 256), 256, 0, s>>>(G->row, V, cnt);
+  {
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, first, V + 1, s);
+    void* tmp = nullptr;
+    ND_CUDA_TRY(nd_alloc((char**)&tmp, tb, s));
+    ND_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, first, V + 1, s));
+    nd_free(tmp, s);
+  }
+  int64_t n_lines = 0;
+  ND_CUDA_TRY(cudaMemcpyAsync(&n_lines, first + V, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  ND_CUDA_TRY(cudaStreamSynchronize(s));
+  if (n_lines >= (1ll << 31)) {  // int32 line offsets
+    nd_free(cnt, s); nd_free(first, s);
+    return ND_OK;
+  }
+  ND_CUDA_TRY(cudaMalloc(&G->vline, V * sizeof(int32_t)));
+  ND_CUDA_TRY(cudaMalloc(&G->pl, (n_lines > 0 ? n_lines : 1) * sizeof(PickLine)));
+  G->bytes += V * 4 + n_lines * (int64_t)sizeof(PickLine);
+  k_vline32<<<nd_grid(V, 256), 256, 0, s>>>(first, V, G->vline);
+  k_build_lines<<<148 * 16, 256, 0, s>>>(G->row, G->col, G->pre, G->vline, V, G->pl);
+  ND_CUDA_TRY(cudaGetLastError());
+  nd_free(cnt, s);
+  nd_free(first, s);
+  ND_CUDA_TRY(cudaStreamSynchronize(s));
+  G->g.pl = G->pl;
+  G->g.vline = G->vline;
   return ND_OK;
 }
 

@@ -23,6 +23,8 @@ struct nd_graph {
   nd::NbrW* nbw = nullptr;
   nd::NbrP* nbp = nullptr;
   nd::NbrU* nbu = nullptr;
+  nd::PickLine* pl = nullptr;
+  int32_t* vline = nullptr;
   int64_t bytes = 0;
   int device = 0;
 };
@@ -65,6 +67,7 @@ int nd_pool_init();
 int64_t* nd_pinned_scratch();
 int nd_graph_ensure_index(nd_graph* G, int want_hset, int want_guide, cudaStream_t s);
 int nd_graph_ensure_records(nd_graph* G, int want_tries, cudaStream_t s);
+int nd_graph_ensure_lines(nd_graph* G, cudaStream_t s);
 int nd_dedup_segments(const int32_t* sid, const int32_t* val, int64_t m, int64_t n_samples,
                       int64_t n_vertices, int32_t** out_sid, int32_t** out_val, int64_t* out_m,
                       int64_t* counts, cudaStream_t s);

@@ -241,6 +241,8 @@ struct PWArgs {
   const NbrW* nbw;    // neighbour records (or null)
   const NbrP* nbp;
   const NbrU* nbu;
+  const PickLine* pl;    // line-packed pick rows (DeepWalk / PPR on weighted graphs) or null
+  const int32_t* vline;  // first line of each row (with pl)
 };
 
 // one 32-byte sector: row bounds, max weight and prefix total of v
@@ -362,6 +364,42 @@ __device__ __forceinline__ int64_t rec_pick(const PWArgs& A, int64_t lo, int64_t
   return h0.z;
 }
 
+// weighted pick over the line-packed rows (PickLine, nd_common.cuh): the
+// exact bucket's bracket guide[j], guide[j+1] sits in the line of bucket j,
+// next to the records around j (the upper-bound probes and the selected
+// record are usually sectors of that same line).
+__device__ __forceinline__ int64_t line_pick(const PWArgs& A, int64_t llo, int64_t deg, double tot,
+                                             double u01, NextHdr& nh, ItemStats& st) {
+  const PickLine* L = A.pl + llo;
+  const double x = __dmul_rn(u01, tot);
+  int64_t a = 0, b = deg;
+  const int64_t j = guide_bucket(x, tot, deg);
+  int64_t line = -1;
+  if (j >= 0) {
+    const int4 g = __ldg(reinterpret_cast<const int4*>(L[j / 3].g));  // 16-byte aligned
+    const int sidx = (int)(j % 3);
+    a = sidx == 0 ? g.x : sidx == 1 ? g.y : g.z;
+    b = sidx == 0 ? g.y : sidx == 1 ? g.z : g.w;
+    line = j / 3;
+    st.sect += 1;
+  }
+  while (a < b) {
+    const int64_t mid = (a + b) >> 1;
+    if (mid / 3 != line) { line = mid / 3; st.sect += 1; }
+    if (__ldg(&L[mid / 3].r[mid % 3].pre) <= x) a = mid + 1; else b = mid;
+  }
+  const int64_t k = a < deg - 1 ? a : deg - 1;
+  if (k / 3 != line) st.sect += 1;
+  int4 h0, h1;
+  ld32B(&L[k / 3].r[k % 3], h0, h1);
+  nh.tot = __longlong_as_double(((long long)(uint32_t)h0.w << 32) | (uint32_t)h0.z);
+  nh.deg = h1.y;
+  nh.lo = h1.z;
+  nh.mx = -1.0;
+  st.bytes += SECTOR + SECTOR * search_sectors(deg) + SECTOR + 8;
+  return h1.x;
+}
+
 // one node2vec rejection try over the neighbour records; -2 = rejected
 __device__ __forceinline__ int64_t rec_try(const PWArgs& A, int64_t lo, int64_t deg, int64_t t,
                                            int64_t tlo, int64_t thi, double env, uint64_t b,
@@ -434,6 +472,7 @@ __global__ void __launch_bounds__(256, MINB) k_walk_persistent(PWArgs A) {
           ik = key_item((uint64_t)(A.sample_lo + w), 0, 0);
           orow = A.out + row * A.Lw;
           load_vertex(A, v, lo, deg, mx, tot);
+          if (A.pl) lo = __ldg(A.vline + v);  // line-packed rows: lo is v's first line
           st.bytes += SECTOR + 8;
           st.sect += 1;
         }
@@ -470,9 +509,11 @@ __global__ void __launch_bounds__(256, MINB) k_walk_persistent(PWArgs A) {
         }
       } else if (A.a.code == ND_PPR) {
         if (to_unit(draw_u64(base0, ik)) < A.a.term) o = -1;
+        else if (A.pl) o = line_pick(A, lo, deg, tot, to_unit(draw_u64(base0 + C_DRAW, ik)), nh, st);
         else o = rec_pick(A, lo, deg, tot, to_unit(draw_u64(base0 + C_DRAW, ik)), nh, st);
       } else {  // DeepWalk, node2vec step 0: draw 0 weighted pick
-        o = rec_pick(A, lo, deg, tot, to_unit(draw_u64(base0, ik)), nh, st);
+        o = A.pl ? line_pick(A, lo, deg, tot, to_unit(draw_u64(base0, ik)), nh, st)
+                 : rec_pick(A, lo, deg, tot, to_unit(draw_u64(base0, ik)), nh, st);
       }
     } else if (n2v && t >= 0 && deg > 0) {
       if (j == 0) st.bytes += 2 * SECTOR;  // t offsets + max_w (§8 d pair term)
@@ -530,6 +571,7 @@ __global__ void __launch_bounds__(256, MINB) k_walk_persistent(PWArgs A) {
         if (n2v && mx < 0.0) { mx = __ldg(A.gv.mx + v); st.sect += 1; }  // after node2vec's step-0 pick
       } else {
         load_vertex(A, v, lo, deg, mx, tot);
+        if (A.pl) lo = __ldg(A.vline + v);
         st.sect += 1;
       }
       st.bytes += SECTOR + 8;
@@ -1276,7 +1318,8 @@ static int run_chain_walk_sp(const nd_graph* G, const NdApp& a, int64_t sample_l
     ND_CUDA_TRY(cudaMemsetAsync(ctl, 0, 2 * sizeof(int), s));
     PWArgs A{view(g), a, seed, sample_lo, rows, cwid, cv, ct, roots, roots32, R, step0,
              step0 + Lw, ld, W.out, W.nnz, died, nw, nv, nt, ctl + 1, ctl, ctl + 2, ctl + 3, ctr,
-             g.vrec, g.ecw, g.epc, g.nbw, g.nbp, g.nbu};
+             g.vrec, g.ecw, g.epc, g.nbw, g.nbp, g.nbu,
+             (a.code == ND_DEEPWALK || a.code == ND_PPR) ? g.pl : nullptr, g.vline};
     int64_t grid = (int64_t)nsm * occ;
     const int64_t need = (rows + 255) / 256;
     if (grid > need) grid = need;
@@ -1534,6 +1577,8 @@ extern "C" int nd_run_walk(const nd_graph* g, int app_code, const double* host_p
                                app_code != ND_MULTIRW, s));
   if (app_code != ND_MULTIRW && paradigm == ND_SP)
     ND_TRY(nd_graph_ensure_records(const_cast<nd_graph*>(g), app_code == ND_NODE2VEC, s));
+  if ((app_code == ND_DEEPWALK || app_code == ND_PPR) && paradigm == ND_SP)
+    ND_TRY(nd_graph_ensure_lines(const_cast<nd_graph*>(g), s));
   nd_result* res = new nd_result();
   res->stream = s;
   int rc;
