@@ -249,12 +249,12 @@ struct PWArgs {
 __device__ __forceinline__ void load_vertex(const PWArgs& A, int64_t v, int64_t& lo, int64_t& deg,
                                             double& mx, double& tot) {
   if (A.vrec != nullptr) {
-    const longlong2 a = __ldg(reinterpret_cast<const longlong2*>(A.vrec + v));
-    const double2 b = __ldg(reinterpret_cast<const double2*>(A.vrec + v) + 1);
-    lo = a.x;
-    deg = a.y;
-    mx = b.x;
-    tot = b.y;
+    int4 a, b;
+    ld32B(A.vrec + v, a, b);
+    lo = ((int64_t)(uint32_t)a.y << 32) | (uint32_t)a.x;
+    deg = ((int64_t)(uint32_t)a.w << 32) | (uint32_t)a.z;
+    mx = __longlong_as_double(((long long)(uint32_t)b.y << 32) | (uint32_t)b.x);
+    tot = __longlong_as_double(((long long)(uint32_t)b.w << 32) | (uint32_t)b.z);
   } else {
     lo = __ldg(A.gv.row + v);
     deg = __ldg(A.gv.row + v + 1) - lo;
@@ -416,13 +416,13 @@ __device__ __forceinline__ int64_t rec_try(const PWArgs& A, int64_t lo, int64_t 
     nh.lo = (int64_t)(((uint64_t)(uint32_t)r.w << 32) | (uint32_t)r.z);
     nh.mx = nh.deg > 0 ? 1.0 : 0.0;
   } else {
-    const int4 r0 = __ldg(reinterpret_cast<const int4*>(A.nbw + lo + k));
-    const double2 r1 = __ldg(reinterpret_cast<const double2*>(A.nbw + lo + k) + 1);
+    int4 r0, r1;
+    ld32B(A.nbw + lo + k, r0, r1);  // the whole record in one 32-byte request
     nb = r0.x;
     nh.deg = r0.y;
     nh.lo = (int64_t)(((uint64_t)(uint32_t)r0.w << 32) | (uint32_t)r0.z);
-    w = r1.x;
-    nh.mx = r1.y;
+    w = __longlong_as_double(((long long)(uint32_t)r1.y << 32) | (uint32_t)r1.x);
+    nh.mx = __longlong_as_double(((long long)(uint32_t)r1.w << 32) | (uint32_t)r1.z);
   }
   nh.tot = -1.0;
   return n2v_decide(A, nb, w, t, tlo, thi, env, b, ik, st);
