@@ -77,24 +77,9 @@ __device__ __forceinline__ uint64_t mod_u64(uint64_t u, uint64_t d) {
 // one 32-byte load (LDG.E.256): a whole record / hash-set chunk per request
 __device__ __forceinline__ void ld32B(const void* p, int4& lo, int4& hi) {
   unsigned long long a, b, c, d;
-  asm volatile("ld.global.nc.v4.u64 {%0,%1,%2,%3}, [%4];" : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(p));
+  asm("ld.global.nc.v4.u64 {%0,%1,%2,%3}, [%4];" : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(p));
   lo = make_int4((int)(uint32_t)a, (int)(uint32_t)(a >> 32), (int)(uint32_t)b, (int)(uint32_t)(b >> 32));
   hi = make_int4((int)(uint32_t)c, (int)(uint32_t)(c >> 32), (int)(uint32_t)d, (int)(uint32_t)(d >> 32));
-}
-
-__device__ __forceinline__ void st32B(void* p, int32_t a0, int32_t a1, int32_t a2, int32_t a3,
-                                      int32_t a4, int32_t a5, int32_t a6, int32_t a7) {
-  auto pk = [](int32_t lo, int32_t hi) {
-    return (unsigned long long)(uint32_t)lo | ((unsigned long long)(uint32_t)hi << 32);
-  };
-  asm volatile("st.global.v4.u64 [%0], {%1,%2,%3,%4};" ::"l"(p), "l"(pk(a0, a1)), "l"(pk(a2, a3)),
-               "l"(pk(a4, a5)), "l"(pk(a6, a7))
-               : "memory");
-}
-
-__device__ __forceinline__ int32_t pick8(const int4& a, const int4& b, int q) {
-  return q < 4 ? (q == 0 ? a.x : q == 1 ? a.y : q == 2 ? a.z : a.w)
-               : (q == 4 ? b.x : q == 5 ? b.y : q == 6 ? b.z : b.w);
 }
 
 // ---- device CSR -------------------------------------------------------------

@@ -580,397 +580,6 @@ __global__ void __launch_bounds__(256, MINB) k_walk_persistent(PWArgs A) {
   flush_stats(st, A.ctr);
 }
 
-// ---- helpers of the state-machine walker kernel below ------------------------------
-__device__ __forceinline__ int64_t hsize_of(int64_t deg) {  // next_pow2(2*deg), deg >= 1
-  return 1ll << (64 - __clzll(2 * deg - 1));
-}
-
-// band classification of one try (see n2v_accept): 1 accept, 0 reject,
-// 2 = decided by membership (lhs < (member ? pa : pf))
-__device__ __forceinline__ int n2v_class(const NdApp& a, int32_t nb, int32_t t, double w,
-                                         double u01, double env, double& lhs, double& pa,
-                                         double& pf) {
-  if (env <= 0.0) return 1;
-  lhs = __dmul_rn(u01, env);
-  if (nb == t) return lhs < __dmul_rn(w, a.f_ret) ? 1 : 0;
-  pa = __dmul_rn(w, a.f_adj);
-  pf = __dmul_rn(w, a.f_far);
-  if (lhs < pa && lhs < pf) return 1;
-  if (!(lhs < pa) && !(lhs < pf)) return 0;
-  return 2;
-}
-
-// ---- state-machine walker kernel ---------------------------------------------------
-// Each loop iteration every live lane issues exactly ONE round trip: two
-// 16-byte loads at the addresses its phase selects (the two halves of a
-// neighbour record, a 4-slot chunk of a hash set, or the guide entries that
-// bracket a weighted pick), then consumes the data with ALU-only code.
-// Lanes in different phases (a node2vec try, a membership probe, a search
-// step) thus wait on memory together, instead of the warp serialising the
-// divergent dependent loads of its lanes one branch after another.
-enum : int { PH_REC = 0, PH_PROBE = 1, PH_GUIDE = 2, PH_SEARCH = 3, PH_FINAL = 4, PH_NULL = 5 };
-
-__device__ __forceinline__ int32_t pick4(const int4& r, int q) {  // r[q], no local memory
-  return q == 0 ? r.x : q == 1 ? r.y : q == 2 ? r.z : r.w;
-}
-
-struct SMLane {
-  int32_t row = -1, w = 0, v = 0, t = -1, s = 0, deg = 0, tdeg = 0, j = 0;
-  int64_t lo = 0, tlo = 0;
-  double hv = 0.0;   // node2vec with t >= 0: max weight of v; picks: prefix total of v
-  uint64_t ik = 0;
-  int phase = PH_NULL;
-  // node2vec band try / pick search state
-  int32_t c_nb = 0, c_deg = 0;
-  int64_t c_lo = 0;
-  double c_hv = 0.0;
-  double x = 0.0;     // pick target u*total
-  int32_t sa = 0, sb = 0;
-  uint32_t pslot = 0;
-  bool accM = false, accF = false, have_c = false;
-};
-
-// set up the lane's first round trip of step s
-template <int APP, bool UNIT>
-__device__ __forceinline__ void sm_begin(const PWArgs& A, SMLane& L) {
-  if (L.deg <= 0) { L.phase = PH_NULL; return; }
-  const uint64_t base0 = key_base(A.seed, (uint64_t)L.s, 0, 0);
-  if (APP == ND_NODE2VEC && L.t >= 0) { L.phase = PH_REC; L.j = 0; return; }
-  if (APP == ND_PPR && to_unit(draw_u64(base0, L.ik)) < A.a.term) { L.phase = PH_NULL; return; }
-  const double u = to_unit(draw_u64(APP == ND_PPR ? base0 + C_DRAW : base0, L.ik));
-  if (UNIT) {  // floor identity: the record itself
-    int32_t k = (int32_t)__dmul_rn(u, (double)L.deg);
-    L.sa = k < L.deg - 1 ? k : L.deg - 1;
-    L.phase = PH_FINAL;
-    return;
-  }
-  L.x = __dmul_rn(u, L.hv);
-  L.have_c = false;
-  const int64_t jg = (A.gv.guide != nullptr && L.deg > GUIDE_MIN_DEG) ? guide_bucket(L.x, L.hv, L.deg) : -1;
-  if (jg >= 0) {
-    L.sa = (int32_t)jg;  // GUIDE reads guide[jg], guide[jg+1] (exact bucket bracket)
-    L.phase = PH_GUIDE;
-  } else {
-    L.sa = 0;
-    L.sb = L.deg;
-    L.phase = PH_SEARCH;
-  }
-}
-
-template <int APP, bool UNIT, int MINB, bool OB>
-__global__ void __launch_bounds__(256, MINB) k_walk_sm(PWArgs A) {
-  // OB: each lane stages its last 8 values in shared memory and writes them
-  // as one 32-byte store (the window row stride is padded to 8 values)
-  __shared__ int32_t obuf[OB ? 8 : 1][256];
-  ItemStats st;
-  const int lane = threadIdx.x & 31;
-  const unsigned lt_mask = (1u << lane) - 1;
-  const int32_t n = (int32_t)A.n;
-  const int32_t step0 = (int32_t)A.step0, step_end = (int32_t)A.step_end;
-  SMLane L;
-  int32_t wbeg = 0, wend = 0;  // this warp's claimed row range (warp-uniform)
-  while (true) {
-    const bool need = L.row < 0;
-    const unsigned m = __ballot_sync(0xffffffffu, need);
-    if (m) {
-      const int c = __popc(m);
-      const int rank = __popc(m & lt_mask);
-      const int32_t rem = wend - wbeg;
-      int32_t nbeg = 0;
-      if (rem < c) {
-        int base = 0;
-        if (lane == 0) base = atomicAdd(A.queue, PW_CHUNK);
-        nbeg = __shfl_sync(0xffffffffu, base, 0);
-      }
-      if (need) {
-        L.row = rank < rem ? wbeg + rank : nbeg + (rank - rem);
-        if (L.row < n) {
-          L.w = A.wid ? A.wid[L.row] : L.row;
-          if (A.v0) {
-            L.v = A.v0[L.row];
-            L.t = A.t0[L.row];
-          } else {
-            L.v = A.roots64 ? (int32_t)A.roots64[(int64_t)L.w * A.R] : A.roots32[(int64_t)L.w * A.R];
-            L.t = -1;
-          }
-          L.s = step0;
-          L.ik = key_item((uint64_t)(A.sample_lo + L.w), 0, 0);
-          const longlong2 r0 = __ldg(reinterpret_cast<const longlong2*>(A.vrec + L.v));
-          const double2 r1 = __ldg(reinterpret_cast<const double2*>(A.vrec + L.v) + 1);
-          L.lo = r0.x;
-          L.deg = (int32_t)r0.y;
-          L.hv = (APP == ND_NODE2VEC && L.t >= 0) ? r1.x : r1.y;
-          if (APP == ND_NODE2VEC && L.t >= 0) {  // continuation row: t's bounds
-            const longlong2 q = __ldg(reinterpret_cast<const longlong2*>(A.vrec + L.t));
-            L.tlo = q.x;
-            L.tdeg = (int32_t)q.y;
-            st.sect += 1;
-          }
-          st.bytes += SECTOR + 8;
-          st.sect += 1;
-          sm_begin<APP, UNIT>(A, L);
-        }
-      }
-      if (rem < c) {
-        wbeg = nbeg + (c - rem);
-        wend = nbeg + PW_CHUNK;
-      } else {
-        wbeg += c;
-      }
-    }
-    if (__all_sync(0xffffffffu, L.row >= n)) break;
-    if (L.row >= n) continue;
-
-    // ---- 1. this lane's round trip: one or two 32-byte loads -------------------------
-    const uint64_t base0 = key_base(A.seed, (uint64_t)L.s, 0, 0);
-    const void* p0 = nullptr;
-    const void* p1 = nullptr;
-    bool wide = true;    // 32-byte loads (16 for unit-weight records)
-    int ia = 0, ib = 0;  // GUIDE: int32 lanes of guide[jg-1] / guide[jg+2] in their chunks
-    switch (L.phase) {
-      case PH_REC: {
-        const int64_t k = (int64_t)mod_u64(draw_u64(base0 + 2 * C_DRAW * (uint64_t)L.j, L.ik),
-                                           (uint64_t)L.deg);
-        if (UNIT) { p0 = A.nbu + L.lo + k; wide = false; }
-        else p0 = A.nbw + L.lo + k;
-        break;
-      }
-      case PH_PROBE:
-        p0 = reinterpret_cast<const void*>(
-            reinterpret_cast<uintptr_t>(A.gv.hset + 4 * L.tlo + L.pslot) & ~(uintptr_t)31);
-        break;
-      case PH_GUIDE: {
-        const int32_t* gd = A.gv.guide + L.lo;
-        const int32_t ja = L.sa;
-        const int32_t jb = L.sa + 1 < L.deg ? L.sa + 1 : L.sa;
-        const uintptr_t qa = reinterpret_cast<uintptr_t>(gd + ja), qb = reinterpret_cast<uintptr_t>(gd + jb);
-        p0 = reinterpret_cast<const void*>(qa & ~(uintptr_t)31);
-        if ((qb & ~(uintptr_t)31) != (qa & ~(uintptr_t)31)) p1 = reinterpret_cast<const void*>(qb & ~(uintptr_t)31);
-        ia = (int)((qa >> 2) & 7);
-        ib = (int)((qb >> 2) & 7) + (p1 != nullptr ? 8 : 0);
-        break;
-      }
-      case PH_SEARCH:
-        p0 = A.nbp + L.lo + ((L.sa + L.sb) >> 1);
-        break;
-      case PH_FINAL:
-        if (UNIT) { p0 = A.nbu + L.lo + L.sa; wide = false; }
-        else p0 = A.nbp + L.lo + L.sa;
-        break;
-      default:
-        break;
-    }
-    int4 r0 = make_int4(0, 0, 0, 0), r1 = make_int4(0, 0, 0, 0), r2 = r0, r3 = r0;
-    if (p0 != nullptr) {
-      if (wide) ld32B(p0, r0, r1);
-      else r0 = __ldg(reinterpret_cast<const int4*>(p0));
-      st.sect += 1;
-    }
-    if (p1 != nullptr) { ld32B(p1, r2, r3); st.sect += 1; }
-
-    // ---- 2. consume it (ALU only) ---------------------------------------------------
-    int32_t o = -2;  // -2: the step continues next iteration
-    int32_t nlo_deg = 0;
-    int64_t nlo = 0;
-    double nhv = 0.0;
-    switch (L.phase) {
-      case PH_NULL:
-        o = -1;
-        break;
-      case PH_REC: {
-        int32_t nb;
-        double wt, hmx;
-        if (UNIT) {
-          nb = r0.x;
-          wt = 1.0;
-          hmx = r0.y > 0 ? 1.0 : 0.0;
-        } else {
-          nb = r0.x;
-          wt = __longlong_as_double(((long long)(uint32_t)r1.y << 32) | (uint32_t)r1.x);
-          hmx = __longlong_as_double(((long long)(uint32_t)r1.w << 32) | (uint32_t)r1.z);
-        }
-        const int32_t hdeg = r0.y;
-        const int64_t hlo = (int64_t)(((uint64_t)(uint32_t)r0.w << 32) | (uint32_t)r0.z);
-        const double env = __dmul_rn(L.hv, A.a.f_max);
-        const double u01 = to_unit(draw_u64(base0 + 2 * C_DRAW * (uint64_t)L.j + C_DRAW, L.ik));
-        double lhs = 0.0, pa = 0.0, pf = 0.0;
-        const int d = n2v_class(A.a, nb, L.t, wt, u01, env, lhs, pa, pf);
-        if (L.j == 0) st.bytes += 2 * SECTOR;  // t offsets + max_w (§8 d pair term)
-        st.tries++;
-        st.bytes += 2 * SECTOR;
-        if (d == 1) {
-          o = nb;
-          nlo = hlo;
-          nlo_deg = hdeg;
-          nhv = hmx;
-        } else if (d == 0) {
-          if (++L.j >= N2V_MAX_TRIES) { atomicExch(A.stall, 1); o = -1; }
-        } else {
-          L.c_nb = nb;
-          L.c_lo = hlo;
-          L.c_deg = hdeg;
-          L.c_hv = hmx;
-          L.accM = lhs < pa;
-          L.accF = lhs < pf;
-          const int64_t size = hsize_of(L.tdeg);
-          const int sh = 32 - (63 - __clzll(size));
-          L.pslot = hset_hash((uint32_t)nb) >> sh;
-          L.phase = PH_PROBE;
-          st.bytes += SECTOR * search_sectors(L.tdeg);
-        }
-        break;
-      }
-      case PH_PROBE: {
-        // scan t's table from pslot to the end of the loaded 32-byte chunk (or
-        // of the table); unresolved -> next chunk next iteration
-        const int64_t size = hsize_of(L.tdeg);
-        const int off = (int)((reinterpret_cast<uintptr_t>(A.gv.hset + 4 * L.tlo + L.pslot) >> 2) & 7);
-        const int n_in = (int)(8 - off < size - (int64_t)L.pslot ? 8 - off : size - (int64_t)L.pslot);
-        int res = -1;  // 1 member, 0 absent, -1 unresolved in this chunk
-#pragma unroll
-        for (int i = 0; i < 8; i++) {
-          if (i < n_in && res < 0) {
-            const int32_t xv = pick8(r0, r1, off + i);
-            if (xv == L.c_nb) res = 1;
-            else if (xv < 0) res = 0;
-          }
-        }
-        if (res < 0) {
-          L.pslot = (uint32_t)((L.pslot + n_in) & (size - 1));
-        } else if (res == 1 ? L.accM : L.accF) {
-          o = L.c_nb;
-          nlo = L.c_lo;
-          nlo_deg = L.c_deg;
-          nhv = L.c_hv;
-        } else {
-          L.phase = PH_REC;
-          if (++L.j >= N2V_MAX_TRIES) { atomicExch(A.stall, 1); o = -1; }
-        }
-        break;
-      }
-      case PH_GUIDE: {
-        const int32_t jg = L.sa;
-        L.sa = pick8(r0, r1, ia);
-        L.sb = jg + 1 < L.deg ? (ib < 8 ? pick8(r0, r1, ib) : pick8(r2, r3, ib - 8)) : L.deg;
-        L.phase = PH_SEARCH;
-        if (L.sa >= L.sb) {  // empty bracket (defensive): the clamped upper bound
-          L.sa = L.sa < L.deg - 1 ? L.sa : L.deg - 1;
-          L.phase = PH_FINAL;
-        }
-        break;
-      }
-      case PH_SEARCH: {
-        const int32_t mid = (L.sa + L.sb) >> 1;
-        const double pre = __longlong_as_double(((long long)(uint32_t)r0.y << 32) | (uint32_t)r0.x);
-        if (pre <= L.x) {
-          L.sa = mid + 1;
-        } else {
-          L.sb = mid;
-          L.have_c = true;
-          L.c_nb = r0.z;
-          L.c_deg = r0.w;
-          L.c_lo = ((int64_t)(uint32_t)r1.y << 32) | (uint32_t)r1.x;
-          L.c_hv = __longlong_as_double(((long long)(uint32_t)r1.w << 32) | (uint32_t)r1.z);
-        }
-        if (L.sa >= L.sb) {
-          if (L.have_c && L.sa < L.deg) {  // the first entry > x is the held record
-            o = L.c_nb;
-            nlo = L.c_lo;
-            nlo_deg = L.c_deg;
-            nhv = L.c_hv;
-          } else {  // x >= every probed prefix: the clamped last entry
-            L.sa = L.sa < L.deg - 1 ? L.sa : L.deg - 1;
-            L.phase = PH_FINAL;
-          }
-        }
-        break;
-      }
-      case PH_FINAL: {
-        if (UNIT) {
-          o = r0.x;
-          nlo_deg = r0.y;
-          nlo = (int64_t)(((uint64_t)(uint32_t)r0.w << 32) | (uint32_t)r0.z);
-          nhv = (double)r0.y;
-        } else {
-          o = r0.z;
-          nlo_deg = r0.w;
-          nlo = ((int64_t)(uint32_t)r1.y << 32) | (uint32_t)r1.x;
-          nhv = __longlong_as_double(((long long)(uint32_t)r1.w << 32) | (uint32_t)r1.z);
-        }
-        break;
-      }
-    }
-    if (o == -2) continue;
-
-    // ---- 3. the step is decided: byte model, output, next step -------------------------
-    if (L.phase == PH_SEARCH || L.phase == PH_FINAL || L.phase == PH_GUIDE) {
-      st.bytes += UNIT ? SECTOR + 8 : SECTOR + SECTOR * search_sectors(L.deg) + SECTOR + 8;
-      if (APP == ND_NODE2VEC && o >= 0) {  // the next step tests against v's max weight
-        nhv = UNIT ? (nlo_deg > 0 ? 1.0 : 0.0) : __ldg(A.gv.mx + o);
-        st.sect += UNIT ? 0 : 1;
-      }
-    }
-    {
-      const int32_t idx = L.s - step0;
-      if (OB) {
-        obuf[idx & 7][threadIdx.x] = o;
-        if ((idx & 7) == 7 || o < 0 || L.s + 1 == step_end) {
-          int32_t* dst = A.out + (int64_t)L.row * A.Lw + (idx & ~7);
-          if ((idx & 7) == 7) {
-            st32B(dst, obuf[0][threadIdx.x], obuf[1][threadIdx.x], obuf[2][threadIdx.x],
-                  obuf[3][threadIdx.x], obuf[4][threadIdx.x], obuf[5][threadIdx.x],
-                  obuf[6][threadIdx.x], obuf[7][threadIdx.x]);
-          } else {
-            for (int i = 0; i <= (idx & 7); i++) dst[i] = obuf[i][threadIdx.x];
-          }
-        }
-      } else {
-        A.out[(int64_t)L.row * A.Lw + idx] = o;
-      }
-    }
-    L.s++;
-    if (o < 0) {
-      A.nnz[L.row] = L.s - 1 - step0;
-      A.died[L.w] = 1;
-      atomicMax(A.max_len, L.s);
-      L.row = -1;
-    } else if (L.s == step_end) {
-      A.nnz[L.row] = L.s - step0;
-      atomicMax(A.max_len, L.s);
-      const int slot = atomicAdd(A.cont_n, 1);
-      A.cont_wid[slot] = L.w;
-      A.cont_v[slot] = o;
-      A.cont_t[slot] = L.v;
-      L.row = -1;
-    } else {
-      L.tlo = L.lo;
-      L.tdeg = L.deg;
-      L.t = L.v;
-      L.v = o;
-      L.lo = nlo;
-      L.deg = nlo_deg;
-      L.hv = nhv;
-      st.bytes += SECTOR + 8;
-      sm_begin<APP, UNIT>(A, L);
-    }
-  }
-  flush_stats(st, A.ctr);
-}
-
-template <int APP, bool OB>
-void (*sm_kernel_ob(bool unit, int minb))(PWArgs) {
-  if (unit)
-    return minb >= 6 ? k_walk_sm<APP, true, 6, OB> : minb == 5 ? k_walk_sm<APP, true, 5, OB>
-                                                                : k_walk_sm<APP, true, 4, OB>;
-  return minb >= 6 ? k_walk_sm<APP, false, 6, OB> : minb == 5 ? k_walk_sm<APP, false, 5, OB>
-                                                               : k_walk_sm<APP, false, 4, OB>;
-}
-
-template <int APP>
-void (*sm_kernel(bool unit, int minb, bool ob))(PWArgs) {
-  return ob ? sm_kernel_ob<APP, true>(unit, minb) : sm_kernel_ob<APP, false>(unit, minb);
-}
-
 // per-walker totals across windows
 __global__ void k_pw_accum(const int32_t* __restrict__ wid, const int32_t* __restrict__ nnz,
                            int64_t n, int64_t* __restrict__ tot) {
@@ -1272,22 +881,6 @@ static int run_chain_walk_sp(const nd_graph* G, const NdApp& a, int64_t sample_l
   void (*kern)(PWArgs) = minb >= 8 ? k_walk_persistent<8>
                          : minb == 6 ? k_walk_persistent<6>
                          : minb == 5 ? k_walk_persistent<5> : k_walk_persistent<4>;
-  // ND_WALK_KERNEL=sm selects the state-machine kernel (one round trip per
-  // lane per iteration; see k_walk_sm) when the records and hash sets it reads
-  // exist.  Measured on C2 it is within 3% of the generic kernel on node2vec
-  // and ~8% slower on PPR, so the generic kernel is the default.
-  static const bool use_sm = getenv("ND_WALK_KERNEL") && !strcmp(getenv("ND_WALK_KERNEL"), "sm");
-  if (use_sm && g.vrec != nullptr && (a.code != ND_NODE2VEC || g.hset != nullptr)) {
-    const bool unit_ok = g.unit && g.nbu != nullptr;
-    const bool w_ok = !g.unit && g.nbp != nullptr && (a.code != ND_NODE2VEC || g.nbw != nullptr);
-    if (unit_ok || w_ok) {
-      static const int smb = getenv("ND_SM_MINB") ? atoi(getenv("ND_SM_MINB")) : 4;
-      static const bool ob = !(getenv("ND_OUTBUF") && getenv("ND_OUTBUF")[0] == '0');
-      if (a.code == ND_DEEPWALK) kern = sm_kernel<ND_DEEPWALK>(g.unit, smb, ob);
-      else if (a.code == ND_PPR) kern = sm_kernel<ND_PPR>(g.unit, smb, ob);
-      else if (a.code == ND_NODE2VEC) kern = sm_kernel<ND_NODE2VEC>(g.unit, smb, ob);
-    }
-  }
   int occ = 4;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, 0);
   if (occ < 1) occ = 1;
