@@ -405,9 +405,24 @@ def main():
     e2e_value = e2e_edges / (e2e_ms / 1e3)
 
     # ---- roofline of the dominant kernel ----------------------------------------------
+    # The timed steps run the two apps concurrently, so a launch's event time
+    # there includes the other app's share of the GPU.  The kernel's own rate
+    # comes from a separate pass with the apps one after another (same
+    # kernels, same inputs, event-timed launches on their stream).
     peak, peak_kind = peaks()
-    samp_s = sum(sample_ms) / 1e3
-    achieved = (slot_bytes / samp_s / 1e9) if samp_s > 0 else None
+    L.nd_set_profiling(1)
+    rf_ms, rf_bytes, rf_sect = 0.0, 0, 0
+    for it in range(3):
+        for app in apps:
+            dr = run_device(app, dg, n_samples=n, sample_lo=lo, seed=SEED, paradigm=args.paradigm)
+            if it:
+                rf_ms += dr.profile_ms[1]
+                rf_bytes += dr.counters["slot_bytes"]
+                rf_sect += dr.counters.get("rand_sectors", 0)
+            dr.close()
+    L.nd_set_profiling(0)
+    samp_s = rf_ms / 1e3
+    achieved = (rf_bytes / samp_s / 1e9) if samp_s > 0 else None
     traffic = None
     prof_json = os.path.join(REPO, "profiles", "r01_ncu_summary.json")
     if os.path.exists(prof_json):
@@ -424,7 +439,7 @@ def main():
     ceil_bytes = int(min(dg.resident_bytes(), 8 << 30))
     gather = None
     if L.nd_gather_ceiling(ceil_bytes, 4, 64, C.byref(ceil), _lib.stream_ptr()) == 0 and samp_s > 0:
-        rate = rand_sect / samp_s
+        rate = rf_sect / samp_s
         gather = {"sectors_per_s": rate, "ceiling_sectors_per_s": ceil.value,
                   "frac": rate / ceil.value if ceil.value else None,
                   "ceiling_how": f"dependent random 32 B reads, 1 chain/thread, 4x256 threads/SM, "
@@ -475,7 +490,8 @@ def main():
                          "peak_kind": peak_kind,
                          "bytes_model": "SURVEY 8(d) sector model, counted on device",
                          "algorithmic_bytes_per_step": slot_bytes / len(times),
-                         "kernel_ms_per_step": sum(sample_ms) / len(sample_ms),
+                         "kernel_ms_per_step": rf_ms / 2,
+                         "kernel_timing": "apps one after another (2 passes), event-timed launches",
                          "gather": gather},
             "cpu_baseline": cpu, "parity_cpu_sample": parity, "paradigm_tp": tp_info,
             "clocks": clocks.summary(), "gpu_launches": launches,
