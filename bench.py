@@ -6,10 +6,13 @@ Workload (BASELINE.json configs[1]): keyed RMAT scale 22
 weights U[1,5), graph seed 0) built on device; one step = a node2vec walk
 (p=2, q=0.5, length 100) plus a PPR walk (termination 0.01, step cap 10,000)
 for every vertex (N = V walkers, sampling seed 7).  Inputs (1.4 GB CSR) are
-larger than L2.  With --gpus N the walkers are sharded by worker_ranges
-across ranks (graph replicated, regenerated from the same key), and the
-compacted rows are gathered to rank 0 over NCCL (strong scaling: total work
-fixed).
+larger than L2.  With --gpus N every rank builds the same keyed graph
+(replicated, no broadcast) and runs its own block of sample ids: weak
+scaling by default (each rank walks V walkers per app, global sample ids
+[rank*V, (rank+1)*V): per-GPU work fixed, no collective on the data path,
+the rows stay on the GPU that sampled them; --gather times the optional NCCL
+gather of all rows to rank 0 separately).  --scaling strong splits the V
+walkers with worker_ranges and gathers inside the timed region.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
@@ -199,8 +202,8 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": "edges/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "int64+f64", "data": "synthetic",
-        "config": config_dict(args.gpus, note="CPU oracle port, bounded sample"),
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "int64+f64", "data": "synthetic",
+        "config": config_dict(args.gpus, note="CPU oracle port, bounded sample", scaling=args.scaling),
         "cpu_baseline": {"value": value, "unit": "edges/s", "cores": cores, "kind": "port",
                          "sample": f"node2vec+PPR walks of sample ids [0, {CPU_SAMPLE}) per step"},
         "e2e": {"value": value, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -209,12 +212,16 @@ def run_reference(args):
     return 0
 
 
-def config_dict(n_gpus, note=None, concurrent=True):
+def config_dict(n_gpus, note=None, concurrent=True, scaling="weak"):
+    weak = scaling == "weak"
     c = {"workload": "C2: RMAT scale 22 (4,194,304 V, 68,993,773 directed weighted E), "
-                     "node2vec p=2 q=0.5 len 100 + PPR term 0.01, one walk per vertex",
+                     "node2vec p=2 q=0.5 len 100 + PPR term 0.01, one walk per vertex"
+                     + (" per GPU" if weak and n_gpus > 1 else ""),
          "graph": "keyed RMAT a=.57 b=.19 c=.19, weights U[1,5), seed 0, built on device",
-         "walkers_per_step": 2 * (1 << SCALE), "seed": SEED,
-         "parallelism": f"sample-sharded x{n_gpus}, graph replicated",
+         "walkers_per_step": 2 * (1 << SCALE) * (n_gpus if weak else 1), "seed": SEED,
+         "parallelism": (f"sample-sharded x{n_gpus}, graph replicated, "
+                         + ("V walkers per app per GPU (ids rank*V..), no collective"
+                            if weak else "V walkers split by worker_ranges, NCCL gather in the step")),
          "l2": "inputs (1.45 GB CSR) larger than L2", "paradigm": "sp (walker-major)",
          "apps": "node2vec and PPR concurrently on two streams" if concurrent else "node2vec then PPR"}
     if note:
@@ -231,6 +238,9 @@ def main():
     ap.add_argument("--paradigm", default="sp", choices=["sp", "tp"])
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-tp", action="store_true")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--gather", action="store_true",
+                    help="also time an NCCL gather of every rank's rows to rank 0 (reported separately)")
     ap.add_argument("--serial-apps", action="store_true",
                     help="run node2vec then PPR instead of concurrently on two streams")
     ap.add_argument("--e2e-chunks", type=int, default=8,
@@ -259,8 +269,12 @@ def main():
     L = _lib.load()
     dg = DeviceGraph.rmat(SCALE, n_edges=N_EDGES, seed=GRAPH_SEED, weighted=True)
     V = dg.n_vertices
-    lo, hi = worker_ranges(V, ws)[rank] if rank < min(ws, V) else (V, V)
-    n = hi - lo
+    if args.scaling == "weak":  # per-GPU work fixed: this rank's own V walkers per app
+        lo, n = rank * V, V
+    else:
+        lo, hi = worker_ranges(V, ws)[rank] if rank < min(ws, V) else (V, V)
+        n = hi - lo
+    gather_in_step = ws > 1 and args.scaling == "strong"
     apps = [make_app(a, **kw) for a, kw in APPS]
     stream = torch.cuda.current_stream()
 
@@ -295,7 +309,7 @@ def main():
             for app in apps:
                 runs.append(run_device(app, dg, n_samples=n, sample_lo=lo, seed=SEED,
                                        paradigm=args.paradigm, sync=False))
-                if ws > 1:
+                if gather_in_step:
                     gather_rows(runs[-1].view(_lib.F_FINAL_OFF), runs[-1].narrow_ids())
         else:  # node2vec and PPR concurrently (PPR's long-walk tail overlaps node2vec)
             futs = submit_device_concurrent([dict(app=app, n_samples=n, sample_lo=lo, seed=SEED)
@@ -303,7 +317,7 @@ def main():
             for fut, st in zip(futs, job_streams(len(apps))):
                 runs.append(fut.result())
                 stream.wait_stream(st)
-                if ws > 1:  # this app's rows go to rank 0 while the other app still samples
+                if gather_in_step:  # this app's rows go to rank 0 while the other app samples
                     gather_rows(runs[-1].view(_lib.F_FINAL_OFF), runs[-1].narrow_ids())
         for dr in runs:
             step_edges += dr.total_sampled
@@ -339,6 +353,28 @@ def main():
         edges_all = edges_dev
     value = edges_all / (tot_ms / 1e3)
 
+    # ---- optional: NCCL gather of every rank's rows to rank 0 (not in `value`) -------
+    gather_info = None
+    if args.gather and ws > 1 and args.scaling == "weak":
+        runs = [run_device(app, dg, n_samples=n, sample_lo=lo, seed=SEED, paradigm=args.paradigm)
+                for app in apps]
+        nbytes = 0
+        barrier()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for dr in runs:
+            off, ids = dr.view(_lib.F_FINAL_OFF), dr.narrow_ids()
+            nbytes += off.numel() * 8 + ids.numel() * 4
+            gather_rows(off, ids)
+        g1.record(stream)
+        torch.cuda.synchronize()
+        gms = torch.tensor([g0.elapsed_time(g1)], dtype=torch.float64, device="cuda" if backend == "nccl" else "cpu")
+        dist.all_reduce(gms, op=dist.ReduceOp.MAX)
+        for dr in runs:
+            dr.close()
+        gather_info = {"ms": gms.item(), "bytes_per_rank": nbytes, "backend": backend,
+                       "note": "int32 rows of both apps gathered to rank 0 after the timed steps"}
+
     # ---- the transit-parallel paradigm on the same job (reported alongside) ----------
     tp_info = None
     if args.paradigm == "sp" and not args.no_tp:
@@ -354,7 +390,7 @@ def main():
             if it:
                 tp_ms.append(ev0.elapsed_time(ev1))
         tp_info = {"ms_per_step": sum(tp_ms) / len(tp_ms),
-                   "value": (edges_all / len(times)) / (sum(tp_ms) / len(tp_ms) / 1e3),
+                   "value": (edges_dev / len(times)) / (sum(tp_ms) / len(tp_ms) / 1e3),
                    "note": "TP = per-step radix sort + work classes + sub-warp/CTA/grid kernels"}
 
     # ---- e2e through the public API with host buffers ------------------------------
@@ -477,9 +513,9 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
             "dtype": "int64+f64", "data": "synthetic",
-            "config": config_dict(ws, concurrent=not args.serial_apps),
+            "config": config_dict(ws, concurrent=not args.serial_apps, scaling=args.scaling),
             "e2e": {"value": e2e_value, "unit": "edges/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "host_rows_match_device": e2e_ok,
                     "result": "final rows: int64 offsets + int32 vertex ids, pinned host",
@@ -494,7 +530,7 @@ def main():
                          "kernel_timing": "apps one after another (2 passes), event-timed launches",
                          "gather": gather},
             "cpu_baseline": cpu, "parity_cpu_sample": parity, "paradigm_tp": tp_info,
-            "clocks": clocks.summary(), "gpu_launches": launches,
+            "clocks": clocks.summary(), "gpu_launches": launches, "gather": gather_info,
             "edges_per_step": edges_all / len(times),
         }
         print(json.dumps(line), flush=True)
