@@ -17,6 +17,8 @@
 // (exclusive scan), which also yields transit_idx and per-sample counts.
 #include <cub/cub.cuh>
 
+#include <cstdlib>
+
 #include <vector>
 
 #include "nd_tp.cuh"
@@ -324,7 +326,272 @@ struct StepData {
   int64_t* cum = nullptr;   // per-sample nnz before this step (for the final rows)
 };
 
+// ---- fixed-layout sample-parallel run (k-hop without unique steps) -------------
+// Every step's slots live in per-sample blocks with NULL holes where a parent
+// slot was NULL: block of sample i at step s has B_s = R * m_0 * ... * m_s
+// slots, item (i, p, slot) = parent p of the previous block (the roots at
+// s = 0) and slot < m_s.  A non-NULL parent's transit_idx is its rank among
+// the non-NULL entries of its block (core.py:97, driver.py:80-144), so the
+// draws are exactly the run loop's.  Nothing between steps needs the host:
+// one count pass, one scan and emit kernels build the reference's final rows,
+// step rows and statistics, with a single host synchronisation at the end.
+
+// per sample (one warp): rank of each non-NULL entry of `blk` (block size B),
+// the sample's non-NULL count, and the step's pair total for the statistics
+__global__ void k_fx_rank(const int32_t* __restrict__ blk, int64_t n, int64_t B,
+                          int32_t* __restrict__ rank, int64_t* __restrict__ nn,
+                          unsigned long long* __restrict__ fetch) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  unsigned long long tot = 0;
+  for (int64_t i = warp; i < n; i += nw) {
+    int32_t base = 0;
+    for (int64_t p0 = 0; p0 < B; p0 += 32) {
+      const int64_t p = p0 + lane;
+      const bool ok = p < B && blk[i * B + p] >= 0;
+      const unsigned m = __ballot_sync(0xffffffffu, ok);
+      if (p < B) rank[i * B + p] = ok ? base + __popc(m & ((1u << lane) - 1)) : -1;
+      base += __popc(m);
+    }
+    if (lane == 0) nn[i] = base;
+    tot += base;
+  }
+  if (lane == 0 && tot) atomicAdd(fetch, tot);
+}
+
+// one thread per (sample, parent, slot) item of step s
+__global__ void __launch_bounds__(IND_BLOCK) k_fx_sample(GView<int32_t> gv, NdApp a, uint64_t base0,
+                                                        int64_t sample_lo, int64_t n, int64_t Bp,
+                                                        int64_t m, const int32_t* __restrict__ prev,
+                                                        const int32_t* __restrict__ rank,
+                                                        int32_t* __restrict__ out, int* stall,
+                                                        unsigned long long* ctr) {
+  ItemStats st;
+  const int64_t total = n * Bp * m;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t ip = q / m, slot = q - ip * m;  // ip = i * Bp + p
+    const int32_t v = prev[ip];
+    if (v < 0) { out[q] = -1; continue; }
+    const int64_t i = ip / Bp;
+    const int64_t lo = __ldg(gv.row + v), deg = __ldg(gv.row + v + 1) - lo;
+    if (slot == 0) st.bytes += SECTOR + 8;
+    int stl = 0;
+    const uint64_t ik = key_item((uint64_t)(sample_lo + i), (uint64_t)rank[ip], (uint64_t)slot);
+    const int64_t o = run_item(gv, grow(gv, lo), a, v, deg, -1, base0, ik, st, &stl);
+    if (stl) atomicExch(stall, 1);
+    out[q] = (int32_t)o;
+  }
+  flush_stats(st, ctr);
+}
+
+// per sample (one warp): final row length R + non-NULL slots of every step
+struct FxSteps {
+  const int32_t* blk[8];
+  int64_t B[8];
+  int n_steps;
+};
+
+__global__ void k_fx_counts(FxSteps S, int64_t n, int64_t R, int64_t* __restrict__ flen) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i <= n; i += nw) {
+    if (i == n) { if (lane == 0) flen[n] = 0; continue; }
+    int64_t c = 0;
+    for (int s = 0; s < S.n_steps; s++)
+      for (int64_t p0 = 0; p0 < S.B[s]; p0 += 32) {
+        const int64_t p = p0 + lane;
+        c += __popc(__ballot_sync(0xffffffffu, p < S.B[s] && S.blk[s][i * S.B[s] + p] >= 0));
+      }
+    if (lane == 0) flen[i] = R + c;
+  }
+}
+
+// final rows: roots, then each step's non-NULL slots in block order
+template <typename RootT>
+__global__ void k_fx_final(FxSteps S, const RootT* __restrict__ roots, int64_t n, int64_t R,
+                           const int64_t* __restrict__ off, int32_t* __restrict__ ids,
+                           int64_t* __restrict__ roots_out, int64_t* __restrict__ roots_off) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i < n; i += nw) {
+    int32_t* dst = ids + off[i];
+    for (int64_t r = lane; r < R; r += 32) {
+      const int64_t x = (int64_t)roots[i * R + r];
+      dst[r] = (int32_t)x;
+      roots_out[i * R + r] = x;
+    }
+    if (lane == 0) {
+      roots_off[i] = i * R;
+      if (i == n - 1) roots_off[n] = n * R;
+    }
+    int64_t pos = R;
+    for (int s = 0; s < S.n_steps; s++)
+      for (int64_t p0 = 0; p0 < S.B[s]; p0 += 32) {
+        const int64_t p = p0 + lane;
+        const int32_t v = p < S.B[s] ? S.blk[s][i * S.B[s] + p] : -1;
+        const unsigned mk = __ballot_sync(0xffffffffu, v >= 0);
+        if (v >= 0) dst[pos + __popc(mk & ((1u << lane) - 1))] = v;
+        pos += __popc(mk);
+      }
+  }
+}
+
+// step rows (F_STEP_VALS): the slots of real pairs (non-NULL parents) of step s,
+// sample-major, at off_s[i] + rank(parent) * m + slot
+__global__ void k_fx_step_vals(const int32_t* __restrict__ out, const int32_t* __restrict__ prev_rank,
+                               int64_t n, int64_t Bp, int64_t m, const int64_t* __restrict__ soff,
+                               int32_t* __restrict__ vals) {
+  const int64_t total = n * Bp * m;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t ip = q / m, slot = q - ip * m;
+    const int32_t r = prev_rank[ip];
+    if (r < 0) continue;
+    vals[soff[ip / Bp] + (int64_t)r * m + slot] = out[q];
+  }
+}
+
+__global__ void k_fx_step_counts(const int64_t* __restrict__ nn, int64_t n, int64_t m,
+                                 int64_t* __restrict__ cnt) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    cnt[i] = nn[i] * m;
+}
+
 }  // namespace
+
+__global__ void k_fx_narrow_roots(const int64_t* __restrict__ in, int64_t n, int32_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (int32_t)in[i];
+}
+
+// fixed-layout SP run (see k_fx_*); returns ND_ERR_ARG when the layout does not apply
+static int run_individual_fixed(const nd_graph* G, const NdApp& a, const int64_t* fan, int64_t S,
+                                int64_t sample_lo, int64_t n, const int64_t* roots, int64_t R,
+                                uint64_t seed, cudaStream_t s, nd_result** out_res) {
+  const DevGraph& g = G->g;
+  if (S < 1 || S > 8 || n <= 0) return ND_ERR_ARG;
+  int64_t B[9];
+  B[0] = R;
+  double cells = 0;
+  for (int64_t k = 0; k < S; k++) {
+    B[k + 1] = B[k] * fan[k];
+    cells += (double)n * (double)B[k + 1];
+    if (B[k + 1] >= (1ll << 31)) return ND_ERR_ARG;
+  }
+  if (cells > 1.5e9) return ND_ERR_ARG;
+  nd_trace("fx:start");
+  int32_t* blk[9] = {};
+  int32_t* rank[8] = {};
+  int64_t* nn[8] = {};
+  ND_CUDA_TRY(nd_alloc(&blk[0], n * R, s));
+  if (roots) k_fx_narrow_roots<<<nd_grid(n * R, 256), 256, 0, s>>>(roots, n * R, blk[0]);
+  else ND_TRY(nd_uniform_roots_i32(g, R, seed, sample_lo, n, blk[0], s));
+  unsigned long long *stats = nullptr, *ctr = nullptr;
+  int* stall = nullptr;
+  ND_CUDA_TRY(nd_alloc(&stats, 4 * S, s));
+  ND_CUDA_TRY(nd_alloc(&ctr, 4, s));
+  ND_CUDA_TRY(nd_alloc(&stall, 1, s));
+  ND_CUDA_TRY(cudaMemsetAsync(stats, 0, 4 * S * sizeof(unsigned long long), s));
+  ND_CUDA_TRY(cudaMemsetAsync(ctr, 0, 4 * sizeof(unsigned long long), s));
+  ND_CUDA_TRY(cudaMemsetAsync(stall, 0, sizeof(int), s));
+  const GView<int32_t> gv = view(g);
+  for (int64_t k = 0; k < S; k++) {
+    ND_CUDA_TRY(nd_alloc(&rank[k], n * B[k], s));
+    ND_CUDA_TRY(nd_alloc(&nn[k], n, s));
+    ND_CUDA_TRY(nd_alloc(&blk[k + 1], n * B[k + 1], s));
+    k_fx_rank<<<nd_grid(n * 32, 256, 148 * 32), 256, 0, s>>>(blk[k], n, B[k], rank[k], nn[k],
+                                                            stats + 4 * k + 3);
+    const int64_t items = n * B[k + 1];
+    k_fx_sample<<<nd_grid(items, IND_BLOCK, 148 * 64), IND_BLOCK, 0, s>>>(
+        gv, a, key_base(seed, (uint64_t)k, 0, 0), sample_lo, n, B[k], fan[k], blk[k], rank[k],
+        blk[k + 1], stall, ctr);
+  }
+  // final rows and step rows: counts, scans, one synchronisation for the totals
+  FxSteps FS;
+  FS.n_steps = (int)S;
+  for (int64_t k = 0; k < S; k++) { FS.blk[k] = blk[k + 1]; FS.B[k] = B[k + 1]; }
+  int64_t *flen = nullptr, *final_off = nullptr, *step_counts = nullptr, *soff = nullptr;
+  ND_CUDA_TRY(nd_alloc(&flen, n + 1, s));
+  ND_CUDA_TRY(nd_alloc(&final_off, n + 1, s));
+  ND_CUDA_TRY(nd_alloc(&step_counts, S * n + 1, s));
+  ND_CUDA_TRY(nd_alloc(&soff, S * n + 1, s));
+  k_fx_counts<<<nd_grid((n + 1) * 32, 256, 148 * 32), 256, 0, s>>>(FS, n, R, flen);
+  for (int64_t k = 0; k < S; k++)
+    k_fx_step_counts<<<nd_grid(n, 256), 256, 0, s>>>(nn[k], n, fan[k], step_counts + k * n);
+  ND_CUDA_TRY(cudaMemsetAsync(step_counts + S * n, 0, sizeof(int64_t), s));
+  {
+    size_t t1 = 0, t2 = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, t1, flen, final_off, n + 1, s);
+    cub::DeviceScan::ExclusiveSum(nullptr, t2, step_counts, soff, S * n + 1, s);
+    void* tmp = nullptr;
+    ND_CUDA_TRY(nd_alloc((char**)&tmp, t1 > t2 ? t1 : t2, s));
+    ND_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, t1, flen, final_off, n + 1, s));
+    ND_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, t2, step_counts, soff, S * n + 1, s));
+    nd_free(tmp, s);
+  }
+  int64_t* h = nd_pinned_scratch();  // [0] total, [1] step values, [2] stall, [3..6] ctr, [8..] stats
+  ND_CUDA_TRY(cudaMemcpyAsync(h, final_off + n, 8, cudaMemcpyDeviceToHost, s));
+  ND_CUDA_TRY(cudaMemcpyAsync(h + 1, soff + S * n, 8, cudaMemcpyDeviceToHost, s));
+  ND_CUDA_TRY(cudaMemcpyAsync(h + 2, stall, sizeof(int), cudaMemcpyDeviceToHost, s));
+  ND_CUDA_TRY(cudaMemcpyAsync(h + 3, ctr, 4 * 8, cudaMemcpyDeviceToHost, s));
+  ND_CUDA_TRY(cudaMemcpyAsync(h + 8, stats, 4 * S * 8, cudaMemcpyDeviceToHost, s));
+  ND_CUDA_TRY(cudaStreamSynchronize(s));
+  nd_trace("fx:totals(synced)");
+  const int64_t total = h[0], total_items = h[1];
+  const int h_stall = (int)(h[2] & 0xFFFFFFFF);
+  const int64_t slot_bytes = h[3];
+  // the run loop stops once no sample has a transit left (core.py:187-203)
+  int64_t n_steps = S;
+  for (int64_t k = 0; k < S; k++)
+    if (h[8 + 4 * k + 3] == 0) { n_steps = k; break; }
+  int32_t *final_ids = nullptr, *step_vals = nullptr;
+  int64_t *roots_out = nullptr, *roots_off = nullptr;
+  ND_CUDA_TRY(nd_alloc(&final_ids, total > 0 ? total : 1, s));
+  ND_CUDA_TRY(nd_alloc(&step_vals, total_items > 0 ? total_items : 1, s));
+  ND_CUDA_TRY(nd_alloc(&roots_out, n * R, s));
+  ND_CUDA_TRY(nd_alloc(&roots_off, n + 1, s));
+  k_fx_final<int32_t><<<nd_grid(n * 32, 256, 148 * 32), 256, 0, s>>>(FS, blk[0], n, R, final_off,
+                                                                   final_ids, roots_out, roots_off);
+  for (int64_t k = 0; k < n_steps; k++) {
+    const int64_t items = n * B[k + 1];
+    k_fx_step_vals<<<nd_grid(items, 256, 148 * 64), 256, 0, s>>>(blk[k + 1], rank[k], n, B[k],
+                                                                 fan[k], soff + k * n, step_vals);
+  }
+  ND_CUDA_TRY(cudaGetLastError());
+  for (int64_t k = 0; k < S; k++) { nd_free(rank[k], s); nd_free(nn[k], s); }
+  for (int64_t k = 0; k <= S; k++) nd_free(blk[k], s);
+  nd_free(flen, s); nd_free(soff, s); nd_free(ctr, s); nd_free(stall, s);
+  if (h_stall) {
+    nd_free(final_off, s); nd_free(final_ids, s); nd_free(step_vals, s); nd_free(roots_out, s);
+    nd_free(roots_off, s); nd_free(step_counts, s); nd_free(stats, s);
+    return ND_ERR_STALL;
+  }
+  nd_result* res = new nd_result();
+  res->stream = s;
+  res->n = n;
+  res->n_steps = n_steps;
+  res->total_sampled = total - n * R;
+  res->set(ND_F_FINAL_OFF, final_off, n + 1);
+  res->set(ND_F_FINAL_IDS32, final_ids, total);
+  res->set(ND_F_ROOTS, roots_out, n * R);
+  res->set(ND_F_ROOTS_OFF, roots_off, n + 1);
+  res->set(ND_F_STEP_COUNTS, step_counts, n_steps * n);
+  res->set(ND_F_STEP_VALS32, step_vals, total_items);
+  res->set(ND_F_STATS, stats, 4 * n_steps);
+  res->counters[NDC_ITEMS] = total_items;
+  res->counters[NDC_SLOT_BYTES] = slot_bytes;
+  res->counters[NDC_STEPS] = n_steps;
+  res->counters[NDC_LAUNCHES] = 2 * S + 6 + n_steps;
+  *out_res = res;
+  nd_trace("fx:done");
+  return ND_OK;
+}
 
 extern "C" int nd_run_individual(const nd_graph* G, int app_code, const double* host_params,
                                  int64_t n_params, const int64_t* host_fanouts, int64_t n_fanouts,
@@ -342,6 +609,16 @@ extern "C" int nd_run_individual(const nd_graph* G, int app_code, const double* 
   const DevGraph& g = G->g;
   const int key_bits = key_bits_for(g.V);
   const int64_t S_max = n_fanouts < step_cap ? n_fanouts : step_cap;
+  // k-hop without unique steps, sample-parallel: the fixed-layout run (one
+  // host synchronisation; identical outputs).  ND_IND_FIXED=0 disables it.
+  static const bool fixed_off = getenv("ND_IND_FIXED") && getenv("ND_IND_FIXED")[0] == '0';
+  bool any_unique = false;
+  for (int64_t k = 0; k < S_max; k++) any_unique |= nd_unique_at(host_unique, n_unique, k);
+  if (!fixed_off && paradigm == ND_SP && app_code == ND_KHOP && !any_unique) {
+    const int rc = run_individual_fixed(G, a, host_fanouts, S_max, sample_lo, n, roots, R, seed, s,
+                                        out_res);
+    if (rc != ND_ERR_ARG) return rc;  // ND_ERR_ARG: the layout does not fit, run the loop
+  }
 
   int32_t* roots32 = nullptr;
   if (!roots) {
