@@ -726,10 +726,26 @@ static int ensure_wide(const nd_result* rc, int f64, int f32) {
   return ND_OK;
 }
 
+// a field the run deferred (nd_result::lazy_build), built once on request
+static int ensure_lazy(const nd_result* rc, int field) {
+  nd_result* r = const_cast<nd_result*>(rc);
+  std::lock_guard<std::mutex> lock(g_result_mu);
+  if (r->lazy_field != field || r->ptr[field] || !r->lazy_build) return ND_OK;
+  const int rc2 = r->lazy_build(r);
+  if (r->lazy_free) r->lazy_free();
+  r->lazy_build = nullptr;
+  r->lazy_free = nullptr;
+  if (rc2 == ND_OK) ND_CUDA_TRY(cudaStreamSynchronize(r->stream));
+  return rc2;
+}
+
 static int ensure_derived(const nd_result* r, int field) {
   if (field == ND_F_FINAL_IDS) return ensure_wide(r, ND_F_FINAL_IDS, ND_F_FINAL_IDS32);
-  if (field == ND_F_STEP_VALS) return ensure_wide(r, ND_F_STEP_VALS, ND_F_STEP_VALS32);
-  return ND_OK;
+  if (field == ND_F_STEP_VALS) {
+    ND_TRY(ensure_lazy(r, ND_F_STEP_VALS32));
+    return ensure_wide(r, ND_F_STEP_VALS, ND_F_STEP_VALS32);
+  }
+  return ensure_lazy(r, field);
 }
 
 extern "C" int nd_result_field(const nd_result* r, int field, const void** ptr, int64_t* count) {
@@ -783,6 +799,7 @@ extern "C" int nd_result_narrow_ids(nd_result* r, void* stream) {
 
 extern "C" int nd_result_destroy(nd_result* r) {
   if (!r) return ND_OK;
+  if (r->lazy_free) r->lazy_free();
   for (int f = 0; f < ND_N_FIELDS; f++)
     if (r->ptr[f]) cudaFreeAsync(r->ptr[f], r->stream);
   delete r;

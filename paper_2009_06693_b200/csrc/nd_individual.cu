@@ -361,29 +361,49 @@ __global__ void k_fx_rank(const int32_t* __restrict__ blk, int64_t n, int64_t B,
 }
 
 // one thread per (sample, parent, slot) item of step s
+// (also counts each sample's non-NULL slots into cnt[i]: warp-aggregated atomics)
 __global__ void __launch_bounds__(IND_BLOCK) k_fx_sample(GView<int32_t> gv, NdApp a, uint64_t base0,
                                                         int64_t sample_lo, int64_t n, int64_t Bp,
                                                         int64_t m, const int32_t* __restrict__ prev,
                                                         const int32_t* __restrict__ rank,
-                                                        int32_t* __restrict__ out, int* stall,
-                                                        unsigned long long* ctr) {
+                                                        int32_t* __restrict__ out,
+                                                        unsigned long long* __restrict__ cnt,
+                                                        int* stall, unsigned long long* ctr) {
   ItemStats st;
   const int64_t total = n * Bp * m;
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total;
-       q += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t ip = q / m, slot = q - ip * m;  // ip = i * Bp + p
-    const int32_t v = prev[ip];
-    if (v < 0) { out[q] = -1; continue; }
-    const int64_t i = ip / Bp;
-    const int64_t lo = __ldg(gv.row + v), deg = __ldg(gv.row + v + 1) - lo;
-    if (slot == 0) st.bytes += SECTOR + 8;
-    int stl = 0;
-    const uint64_t ik = key_item((uint64_t)(sample_lo + i), (uint64_t)rank[ip], (uint64_t)slot);
-    const int64_t o = run_item(gv, grow(gv, lo), a, v, deg, -1, base0, ik, st, &stl);
-    if (stl) atomicExch(stall, 1);
-    out[q] = (int32_t)o;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t q0 = blockIdx.x * (int64_t)blockDim.x; q0 < total; q0 += stride) {
+    const int64_t q = q0 + threadIdx.x;
+    int64_t i = -1;
+    int32_t o = -1;
+    if (q < total) {
+      const int64_t ip = q / m, slot = q - ip * m;  // ip = i * Bp + p
+      const int32_t v = prev[ip];
+      i = ip / Bp;
+      if (v >= 0) {
+        const int64_t lo = __ldg(gv.row + v), deg = __ldg(gv.row + v + 1) - lo;
+        if (slot == 0) st.bytes += SECTOR + 8;
+        int stl = 0;
+        const uint64_t ik = key_item((uint64_t)(sample_lo + i), (uint64_t)rank[ip], (uint64_t)slot);
+        o = (int32_t)run_item(gv, grow(gv, lo), a, v, deg, -1, base0, ik, st, &stl);
+        if (stl) atomicExch(stall, 1);
+      }
+      out[q] = o;
+    }
+    // per-sample non-NULL counts: lanes of one sample add once
+    const unsigned act = __ballot_sync(0xffffffffu, o >= 0);
+    const unsigned same = __match_any_sync(0xffffffffu, i);
+    const unsigned grp = act & same;
+    if (o >= 0 && (threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(cnt + i, (unsigned long long)__popc(grp));
   }
   flush_stats(st, ctr);
+}
+
+__global__ void k_fx_flen(const unsigned long long* __restrict__ cnt, int64_t n, int64_t R,
+                          int64_t* __restrict__ flen) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    flen[i] = i < n ? R + (int64_t)cnt[i] : 0;
 }
 
 // per sample (one warp): final row length R + non-NULL slots of every step
@@ -392,22 +412,6 @@ struct FxSteps {
   int64_t B[8];
   int n_steps;
 };
-
-__global__ void k_fx_counts(FxSteps S, int64_t n, int64_t R, int64_t* __restrict__ flen) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t i = warp; i <= n; i += nw) {
-    if (i == n) { if (lane == 0) flen[n] = 0; continue; }
-    int64_t c = 0;
-    for (int s = 0; s < S.n_steps; s++)
-      for (int64_t p0 = 0; p0 < S.B[s]; p0 += 32) {
-        const int64_t p = p0 + lane;
-        c += __popc(__ballot_sync(0xffffffffu, p < S.B[s] && S.blk[s][i * S.B[s] + p] >= 0));
-      }
-    if (lane == 0) flen[i] = R + c;
-  }
-}
 
 // final rows: roots, then each step's non-NULL slots in block order
 template <typename RootT>
@@ -500,6 +504,9 @@ static int run_individual_fixed(const nd_graph* G, const NdApp& a, const int64_t
   ND_CUDA_TRY(cudaMemsetAsync(stats, 0, 4 * S * sizeof(unsigned long long), s));
   ND_CUDA_TRY(cudaMemsetAsync(ctr, 0, 4 * sizeof(unsigned long long), s));
   ND_CUDA_TRY(cudaMemsetAsync(stall, 0, sizeof(int), s));
+  unsigned long long* scnt = nullptr;  // per-sample non-NULL slots over all steps
+  ND_CUDA_TRY(nd_alloc(&scnt, n, s));
+  ND_CUDA_TRY(cudaMemsetAsync(scnt, 0, n * sizeof(unsigned long long), s));
   const GView<int32_t> gv = view(g);
   for (int64_t k = 0; k < S; k++) {
     ND_CUDA_TRY(nd_alloc(&rank[k], n * B[k], s));
@@ -510,7 +517,7 @@ static int run_individual_fixed(const nd_graph* G, const NdApp& a, const int64_t
     const int64_t items = n * B[k + 1];
     k_fx_sample<<<nd_grid(items, IND_BLOCK, 148 * 64), IND_BLOCK, 0, s>>>(
         gv, a, key_base(seed, (uint64_t)k, 0, 0), sample_lo, n, B[k], fan[k], blk[k], rank[k],
-        blk[k + 1], stall, ctr);
+        blk[k + 1], scnt, stall, ctr);
   }
   // final rows and step rows: counts, scans, one synchronisation for the totals
   FxSteps FS;
@@ -521,7 +528,7 @@ static int run_individual_fixed(const nd_graph* G, const NdApp& a, const int64_t
   ND_CUDA_TRY(nd_alloc(&final_off, n + 1, s));
   ND_CUDA_TRY(nd_alloc(&step_counts, S * n + 1, s));
   ND_CUDA_TRY(nd_alloc(&soff, S * n + 1, s));
-  k_fx_counts<<<nd_grid((n + 1) * 32, 256, 148 * 32), 256, 0, s>>>(FS, n, R, flen);
+  k_fx_flen<<<nd_grid(n + 1, 256), 256, 0, s>>>(scnt, n, R, flen);
   for (int64_t k = 0; k < S; k++)
     k_fx_step_counts<<<nd_grid(n, 256), 256, 0, s>>>(nn[k], n, fan[k], step_counts + k * n);
   ND_CUDA_TRY(cudaMemsetAsync(step_counts + S * n, 0, sizeof(int64_t), s));
@@ -550,25 +557,28 @@ static int run_individual_fixed(const nd_graph* G, const NdApp& a, const int64_t
   int64_t n_steps = S;
   for (int64_t k = 0; k < S; k++)
     if (h[8 + 4 * k + 3] == 0) { n_steps = k; break; }
-  int32_t *final_ids = nullptr, *step_vals = nullptr;
+  int32_t* final_ids = nullptr;
   int64_t *roots_out = nullptr, *roots_off = nullptr;
   ND_CUDA_TRY(nd_alloc(&final_ids, total > 0 ? total : 1, s));
-  ND_CUDA_TRY(nd_alloc(&step_vals, total_items > 0 ? total_items : 1, s));
   ND_CUDA_TRY(nd_alloc(&roots_out, n * R, s));
   ND_CUDA_TRY(nd_alloc(&roots_off, n + 1, s));
   k_fx_final<int32_t><<<nd_grid(n * 32, 256, 148 * 32), 256, 0, s>>>(FS, blk[0], n, R, final_off,
                                                                    final_ids, roots_out, roots_off);
-  for (int64_t k = 0; k < n_steps; k++) {
-    const int64_t items = n * B[k + 1];
-    k_fx_step_vals<<<nd_grid(items, 256, 148 * 64), 256, 0, s>>>(blk[k + 1], rank[k], n, B[k],
-                                                                 fan[k], soff + k * n, step_vals);
-  }
   ND_CUDA_TRY(cudaGetLastError());
-  for (int64_t k = 0; k < S; k++) { nd_free(rank[k], s); nd_free(nn[k], s); }
-  for (int64_t k = 0; k <= S; k++) nd_free(blk[k], s);
-  nd_free(flen, s); nd_free(soff, s); nd_free(ctr, s); nd_free(stall, s);
+  for (int64_t k = 0; k < S; k++) nd_free(nn[k], s);
+  nd_free(flen, s); nd_free(scnt, s); nd_free(ctr, s); nd_free(stall, s);
+  // step rows (F_STEP_VALS32) are built on first request from the blocks and
+  // ranks, which the result keeps until then
+  std::vector<int32_t*> kb(blk, blk + S + 1), kr(rank, rank + S);
+  std::vector<int64_t> kB(B, B + S + 1), kf(fan, fan + S);
+  auto release = [kb, kr, soff, s]() {
+    for (auto p : kb) nd_free(p, s);
+    for (auto p : kr) nd_free(p, s);
+    nd_free(soff, s);
+  };
   if (h_stall) {
-    nd_free(final_off, s); nd_free(final_ids, s); nd_free(step_vals, s); nd_free(roots_out, s);
+    release();
+    nd_free(final_off, s); nd_free(final_ids, s); nd_free(roots_out, s);
     nd_free(roots_off, s); nd_free(step_counts, s); nd_free(stats, s);
     return ND_ERR_STALL;
   }
@@ -582,12 +592,26 @@ static int run_individual_fixed(const nd_graph* G, const NdApp& a, const int64_t
   res->set(ND_F_ROOTS, roots_out, n * R);
   res->set(ND_F_ROOTS_OFF, roots_off, n + 1);
   res->set(ND_F_STEP_COUNTS, step_counts, n_steps * n);
-  res->set(ND_F_STEP_VALS32, step_vals, total_items);
+  res->set(ND_F_STEP_VALS32, nullptr, total_items);
+  res->lazy_field = ND_F_STEP_VALS32;
+  res->lazy_build = [kb, kr, kB, kf, soff, n, n_steps, total_items](nd_result* r) {
+    int32_t* vals = nullptr;
+    ND_CUDA_TRY(nd_alloc(&vals, total_items > 0 ? total_items : 1, r->stream));
+    for (int64_t k = 0; k < n_steps; k++) {
+      const int64_t items = n * kB[k + 1];
+      k_fx_step_vals<<<nd_grid(items, 256, 148 * 64), 256, 0, r->stream>>>(
+          kb[k + 1], kr[k], n, kB[k], kf[k], soff + k * n, vals);
+    }
+    ND_CUDA_TRY(cudaGetLastError());
+    r->set(ND_F_STEP_VALS32, vals, total_items);
+    return ND_OK;
+  };
+  res->lazy_free = release;
   res->set(ND_F_STATS, stats, 4 * n_steps);
   res->counters[NDC_ITEMS] = total_items;
   res->counters[NDC_SLOT_BYTES] = slot_bytes;
   res->counters[NDC_STEPS] = n_steps;
-  res->counters[NDC_LAUNCHES] = 2 * S + 6 + n_steps;
+  res->counters[NDC_LAUNCHES] = 2 * S + 6;
   *out_res = res;
   nd_trace("fx:done");
   return ND_OK;

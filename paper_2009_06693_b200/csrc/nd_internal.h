@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <functional>
 #include <vector>
 
 #include "nd_common.cuh"
@@ -43,6 +44,12 @@ struct nd_result {
   int64_t counters[ND_N_COUNTERS] = {};
   double prof_ms[4] = {};  // schedule, sample, compaction (nd_set_profiling)
   cudaStream_t stream = nullptr;
+  // a field the run leaves to be built on first request (step rows of the
+  // fixed-layout k-hop): `lazy_field` is filled by `lazy_build`; `lazy_free`
+  // releases the device buffers it captured (after building, or at destroy)
+  int lazy_field = -1;
+  std::function<int(nd_result*)> lazy_build;
+  std::function<void()> lazy_free;
 
   void set(int f, void* p, int64_t c) {
     ptr[f] = p;
