@@ -74,6 +74,21 @@ __device__ __forceinline__ uint64_t mod_u64(uint64_t u, uint64_t d) {
   return (uint64_t)r2;
 }
 
+// Division by a run-constant 32-bit divisor d >= 1 for numerators < 2^32
+// (round-up multiplier method): q = (umulhi(x, m) + x) >> l, exact.
+struct FastDiv {
+  uint32_t d = 1, m = 0;
+  int l = 0;
+  FastDiv() = default;
+  __host__ explicit FastDiv(uint32_t dv) : d(dv) {
+    while ((1ull << l) < d) l++;
+    m = (uint32_t)((((1ull << l) - d) << 32) / d + 1);
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t x) const {
+    return (uint32_t)(((uint64_t)__umulhi(x, m) + x) >> l);
+  }
+};
+
 // one 32-byte load (LDG.E.256): a whole record / hash-set chunk per request
 __device__ __forceinline__ void ld32B(const void* p, int4& lo, int4& hi) {
   unsigned long long a, b, c, d;

@@ -363,23 +363,23 @@ __global__ void k_fx_rank(const int32_t* __restrict__ blk, int64_t n, int64_t B,
 // one thread per (sample, parent, slot) item of step s
 // (also counts each sample's non-NULL slots into cnt[i]: warp-aggregated atomics)
 __global__ void __launch_bounds__(IND_BLOCK) k_fx_sample(GView<int32_t> gv, NdApp a, uint64_t base0,
-                                                        int64_t sample_lo, int64_t n, int64_t Bp,
-                                                        int64_t m, const int32_t* __restrict__ prev,
+                                                        int64_t sample_lo, int64_t n, FastDiv Bp,
+                                                        FastDiv m, const int32_t* __restrict__ prev,
                                                         const int32_t* __restrict__ rank,
                                                         int32_t* __restrict__ out,
                                                         unsigned long long* __restrict__ cnt,
                                                         int* stall, unsigned long long* ctr) {
   ItemStats st;
-  const int64_t total = n * Bp * m;
+  const int64_t total = n * (int64_t)Bp.d * m.d;  // < 2^32 (checked by the host)
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t q0 = blockIdx.x * (int64_t)blockDim.x; q0 < total; q0 += stride) {
     const int64_t q = q0 + threadIdx.x;
     int64_t i = -1;
     int32_t o = -1;
     if (q < total) {
-      const int64_t ip = q / m, slot = q - ip * m;  // ip = i * Bp + p
+      const uint32_t ip = m.div((uint32_t)q), slot = (uint32_t)q - ip * m.d;  // ip = i * Bp + p
       const int32_t v = prev[ip];
-      i = ip / Bp;
+      i = Bp.div(ip);
       if (v >= 0) {
         const int64_t lo = __ldg(gv.row + v), deg = __ldg(gv.row + v + 1) - lo;
         if (slot == 0) st.bytes += SECTOR + 8;
@@ -412,6 +412,100 @@ struct FxSteps {
   int64_t B[8];
   int n_steps;
 };
+
+// ---- transit-parallel order for the fixed layout ------------------------------------
+// The parent slots of a step are radix-sorted by transit (NULL parents keyed
+// past every vertex), so the items of one transit -- all samples' pairs at a
+// hub -- run in consecutive threads and share its row in L1/L2
+// (transit_parallel.py:71-83's inversion); outputs land at the same fixed
+// positions, so the rows are identical to the sample-parallel order.
+__global__ void k_fx_keys(const int32_t* __restrict__ prev, const int32_t* __restrict__ rank,
+                          int64_t N, uint32_t sentinel, uint32_t* __restrict__ keys,
+                          uint64_t* __restrict__ vals) {
+  for (int64_t ip = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; ip < N;
+       ip += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = prev[ip];
+    keys[ip] = v >= 0 ? (uint32_t)v : sentinel;
+    vals[ip] = (uint64_t)(uint32_t)ip | ((uint64_t)(uint32_t)rank[ip] << 32);
+  }
+}
+
+// work classes of the step's transit groups (transit_parallel.py:86-101):
+// work = members * m; small < 32, medium 32..1024, large > 1024; [3] = groups
+__global__ void k_fx_classes(const uint32_t* __restrict__ keys, int64_t N, uint32_t sentinel,
+                             int64_t m, unsigned long long* __restrict__ stats) {
+  unsigned long long c0 = 0, c1 = 0, c2 = 0;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < N;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t k = keys[r];
+    if (k == sentinel || (r > 0 && keys[r - 1] == k)) continue;
+    int64_t lo = r + 1, hi = N;  // end of the group: first key > k
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (keys[mid] <= k) lo = mid + 1; else hi = mid;
+    }
+    const int64_t work = (lo - r) * m;
+    if (work < SMALL_MAX_WORK) c0++; else if (work <= LARGE_MIN_WORK) c1++; else c2++;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    c0 += __shfl_down_sync(0xffffffffu, c0, o);
+    c1 += __shfl_down_sync(0xffffffffu, c1, o);
+    c2 += __shfl_down_sync(0xffffffffu, c2, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (c0) atomicAdd(stats + 0, c0);
+    if (c1) atomicAdd(stats + 1, c1);
+    if (c2) atomicAdd(stats + 2, c2);
+    if (c0 + c1 + c2) atomicAdd(stats + 3, c0 + c1 + c2);
+  }
+}
+
+// one thread per (sorted parent, slot)
+// payload = parent slot ip (low 32 bits) | its transit_idx (high 32 bits)
+__global__ void __launch_bounds__(IND_BLOCK) k_fx_sample_tp(GView<int32_t> gv, NdApp a, uint64_t base0,
+                                                           int64_t sample_lo, int64_t N, FastDiv Bp,
+                                                           FastDiv m, uint32_t sentinel,
+                                                           const uint32_t* __restrict__ keys,
+                                                           const uint64_t* __restrict__ vals,
+                                                           int32_t* __restrict__ out, int* stall,
+                                                           unsigned long long* ctr) {
+  ItemStats st;
+  const int64_t total = N * (int64_t)m.d;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t r = m.div((uint32_t)q), slot = (uint32_t)q - r * m.d;
+    const uint64_t pv = vals[r];
+    const uint32_t ip = (uint32_t)pv;
+    const uint32_t v = keys[r];
+    int32_t o = -1;
+    if (v != sentinel) {
+      const int64_t lo = __ldg(gv.row + v), deg = __ldg(gv.row + v + 1) - lo;
+      if (slot == 0) st.bytes += SECTOR + 8;
+      int stl = 0;
+      const uint64_t ik = key_item((uint64_t)(sample_lo + Bp.div(ip)), pv >> 32, (uint64_t)slot);
+      o = (int32_t)run_item(gv, grow(gv, lo), a, (int64_t)v, deg, -1, base0, ik, st, &stl);
+      if (stl) atomicExch(stall, 1);
+    }
+    out[(int64_t)ip * m.d + slot] = o;
+  }
+  flush_stats(st, ctr);
+}
+
+// per sample (one warp): non-NULL slots of one step block, added to cnt[i]
+__global__ void k_fx_block_counts(const int32_t* __restrict__ blk, int64_t n, int64_t B,
+                                  unsigned long long* __restrict__ cnt) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i < n; i += nw) {
+    unsigned long long c = 0;
+    for (int64_t p0 = 0; p0 < B; p0 += 32) {
+      const int64_t p = p0 + lane;
+      c += __popc(__ballot_sync(0xffffffffu, p < B && blk[i * B + p] >= 0));
+    }
+    if (lane == 0) cnt[i] += c;
+  }
+}
 
 // final rows: roots, then each step's non-NULL slots in block order
 template <typename RootT>
@@ -477,7 +571,7 @@ __global__ void k_fx_narrow_roots(const int64_t* __restrict__ in, int64_t n, int
 // fixed-layout SP run (see k_fx_*); returns ND_ERR_ARG when the layout does not apply
 static int run_individual_fixed(const nd_graph* G, const NdApp& a, const int64_t* fan, int64_t S,
                                 int64_t sample_lo, int64_t n, const int64_t* roots, int64_t R,
-                                uint64_t seed, cudaStream_t s, nd_result** out_res) {
+                                uint64_t seed, bool tp, cudaStream_t s, nd_result** out_res) {
   const DevGraph& g = G->g;
   if (S < 1 || S > 8 || n <= 0) return ND_ERR_ARG;
   int64_t B[9];
@@ -504,6 +598,10 @@ static int run_individual_fixed(const nd_graph* G, const NdApp& a, const int64_t
   ND_CUDA_TRY(cudaMemsetAsync(stats, 0, 4 * S * sizeof(unsigned long long), s));
   ND_CUDA_TRY(cudaMemsetAsync(ctr, 0, 4 * sizeof(unsigned long long), s));
   ND_CUDA_TRY(cudaMemsetAsync(stall, 0, sizeof(int), s));
+  const int kbits = key_bits_for(g.V);
+  const uint32_t sentinel = 1u << kbits;  // past every vertex id
+  unsigned long long* tp_scratch = nullptr;  // TP mode: pair counts are not the fetches
+  ND_CUDA_TRY(nd_alloc(&tp_scratch, 1, s));
   unsigned long long* scnt = nullptr;  // per-sample non-NULL slots over all steps
   ND_CUDA_TRY(nd_alloc(&scnt, n, s));
   ND_CUDA_TRY(cudaMemsetAsync(scnt, 0, n * sizeof(unsigned long long), s));
@@ -512,12 +610,38 @@ static int run_individual_fixed(const nd_graph* G, const NdApp& a, const int64_t
     ND_CUDA_TRY(nd_alloc(&rank[k], n * B[k], s));
     ND_CUDA_TRY(nd_alloc(&nn[k], n, s));
     ND_CUDA_TRY(nd_alloc(&blk[k + 1], n * B[k + 1], s));
-    k_fx_rank<<<nd_grid(n * 32, 256, 148 * 32), 256, 0, s>>>(blk[k], n, B[k], rank[k], nn[k],
-                                                            stats + 4 * k + 3);
     const int64_t items = n * B[k + 1];
-    k_fx_sample<<<nd_grid(items, IND_BLOCK, 148 * 64), IND_BLOCK, 0, s>>>(
-        gv, a, key_base(seed, (uint64_t)k, 0, 0), sample_lo, n, B[k], fan[k], blk[k], rank[k],
-        blk[k + 1], scnt, stall, ctr);
+    if (!tp) {
+      k_fx_rank<<<nd_grid(n * 32, 256, 148 * 32), 256, 0, s>>>(blk[k], n, B[k], rank[k], nn[k],
+                                                              stats + 4 * k + 3);
+      k_fx_sample<<<nd_grid(items, IND_BLOCK, 148 * 64), IND_BLOCK, 0, s>>>(
+          gv, a, key_base(seed, (uint64_t)k, 0, 0), sample_lo, n, FastDiv((uint32_t)B[k]),
+          FastDiv((uint32_t)fan[k]), blk[k], rank[k], blk[k + 1], scnt, stall, ctr);
+      continue;
+    }
+    // transit-parallel order: sort the parent slots by transit, classify the groups
+    k_fx_rank<<<nd_grid(n * 32, 256, 148 * 32), 256, 0, s>>>(blk[k], n, B[k], rank[k], nn[k],
+                                                            tp_scratch);
+    const int64_t N = n * B[k];
+    uint32_t *k0 = nullptr, *k1 = nullptr;
+    uint64_t *v0 = nullptr, *v1 = nullptr;
+    ND_CUDA_TRY(nd_alloc(&k0, N, s)); ND_CUDA_TRY(nd_alloc(&k1, N, s));
+    ND_CUDA_TRY(nd_alloc(&v0, N, s)); ND_CUDA_TRY(nd_alloc(&v1, N, s));
+    k_fx_keys<<<nd_grid(N, 256), 256, 0, s>>>(blk[k], rank[k], N, sentinel, k0, v0);
+    {
+      size_t tb = 0;
+      cub::DeviceRadixSort::SortPairs(nullptr, tb, k0, k1, v0, v1, N, 0, kbits + 1, s);
+      void* tmp = nullptr;
+      ND_CUDA_TRY(nd_alloc((char**)&tmp, tb, s));
+      ND_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, tb, k0, k1, v0, v1, N, 0, kbits + 1, s));
+      nd_free(tmp, s);
+    }
+    k_fx_classes<<<nd_grid(N, 256, 148 * 16), 256, 0, s>>>(k1, N, sentinel, fan[k], stats + 4 * k);
+    k_fx_sample_tp<<<nd_grid(items, IND_BLOCK, 148 * 64), IND_BLOCK, 0, s>>>(
+        gv, a, key_base(seed, (uint64_t)k, 0, 0), sample_lo, N, FastDiv((uint32_t)B[k]),
+        FastDiv((uint32_t)fan[k]), sentinel, k1, v1, blk[k + 1], stall, ctr);
+    k_fx_block_counts<<<nd_grid(n * 32, 256, 148 * 32), 256, 0, s>>>(blk[k + 1], n, B[k + 1], scnt);
+    nd_free(k0, s); nd_free(k1, s); nd_free(v0, s); nd_free(v1, s);
   }
   // final rows and step rows: counts, scans, one synchronisation for the totals
   FxSteps FS;
@@ -566,7 +690,7 @@ static int run_individual_fixed(const nd_graph* G, const NdApp& a, const int64_t
                                                                    final_ids, roots_out, roots_off);
   ND_CUDA_TRY(cudaGetLastError());
   for (int64_t k = 0; k < S; k++) nd_free(nn[k], s);
-  nd_free(flen, s); nd_free(scnt, s); nd_free(ctr, s); nd_free(stall, s);
+  nd_free(flen, s); nd_free(scnt, s); nd_free(ctr, s); nd_free(stall, s); nd_free(tp_scratch, s);
   // step rows (F_STEP_VALS32) are built on first request from the blocks and
   // ranks, which the result keeps until then
   std::vector<int32_t*> kb(blk, blk + S + 1), kr(rank, rank + S);
@@ -633,14 +757,15 @@ extern "C" int nd_run_individual(const nd_graph* G, int app_code, const double* 
   const DevGraph& g = G->g;
   const int key_bits = key_bits_for(g.V);
   const int64_t S_max = n_fanouts < step_cap ? n_fanouts : step_cap;
-  // k-hop without unique steps, sample-parallel: the fixed-layout run (one
-  // host synchronisation; identical outputs).  ND_IND_FIXED=0 disables it.
+  // k-hop without unique steps: the fixed-layout run (sample-parallel, or
+  // transit-sorted for TP; one host synchronisation; identical outputs and
+  // TP class statistics).  ND_IND_FIXED=0 disables it.
   static const bool fixed_off = getenv("ND_IND_FIXED") && getenv("ND_IND_FIXED")[0] == '0';
   bool any_unique = false;
   for (int64_t k = 0; k < S_max; k++) any_unique |= nd_unique_at(host_unique, n_unique, k);
-  if (!fixed_off && paradigm == ND_SP && app_code == ND_KHOP && !any_unique) {
-    const int rc = run_individual_fixed(G, a, host_fanouts, S_max, sample_lo, n, roots, R, seed, s,
-                                        out_res);
+  if (!fixed_off && app_code == ND_KHOP && !any_unique) {
+    const int rc = run_individual_fixed(G, a, host_fanouts, S_max, sample_lo, n, roots, R, seed,
+                                        paradigm == ND_TP, s, out_res);
     if (rc != ND_ERR_ARG) return rc;  // ND_ERR_ARG: the layout does not fit, run the loop
   }
 
