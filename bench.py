@@ -243,9 +243,9 @@ def main():
                     help="also time an NCCL gather of every rank's rows to rank 0 (reported separately)")
     ap.add_argument("--serial-apps", action="store_true",
                     help="run node2vec then PPR instead of concurrently on two streams")
-    ap.add_argument("--e2e-chunks", type=int, default=8,
+    ap.add_argument("--e2e-chunks", type=int, default=6,
                     help="node2vec sample-id chunks of the host pipeline (D2H of chunk c overlaps chunk c+1)")
-    ap.add_argument("--e2e-ppr-chunks", type=int, default=4)
+    ap.add_argument("--e2e-ppr-chunks", type=int, default=3)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
