@@ -26,6 +26,9 @@ from .engine import DeviceRun, describe, run_device
 from .graph import as_device_graph
 from .sharding import worker_ranges
 
+import os as _os
+_NO_COPY = _os.environ.get("ND_PIPE_NOCOPY") == "1"  # dev: time the pipeline without D2H
+
 
 @dataclass
 class HostChunk:
@@ -78,9 +81,10 @@ class HostPipeline:
         one synchronisation at the end.  Returns one HostChunk list per job."""
         import torch
         from .engine import _job_pool, job_streams
+        L = _lib.load()
         dg = as_device_graph(graph)
         k = len(jobs)
-        while len(self._copy_streams) < k:
+        while len(self._copy_streams) < 1:
             self._copy_streams.append(torch.cuda.Stream())
         cur = torch.cuda.current_stream()
         dev = torch.cuda.current_device()
@@ -88,13 +92,18 @@ class HostPipeline:
         for st in streams:
             st.wait_stream(cur)
 
+        import threading
+        first_done = threading.Event()  # job 0's first chunk: its copies start the link
+
         def one(ji, job, st, cs):
             app, n_samples, seed, sample_lo, roots_host = job[:5]
             chunks = job[5] if len(job) > 5 and job[5] else self.chunks
             torch.cuda.set_device(dev)
             plan = describe(app)
-            parts = [(lo, hi) for lo, hi in worker_ranges(n_samples, chunks) if hi > lo]
+            parts = chunk_plan(n_samples, chunks, lead=(ji == 0 and k > 1))
             out, held = [], []
+            if ji > 0 and k > 1:
+                first_done.wait(timeout=60)  # the link gets busy before the GPU is shared
             with torch.cuda.stream(st):
                 for ci, (lo, hi) in enumerate(parts):
                     n = hi - lo
@@ -118,18 +127,26 @@ class HostPipeline:
                     cs.wait_event(ready)
                     h_off = self._buf((ji, ci, "off"), off)
                     h_ids = self._buf((ji, ci, "ids"), ids)
-                    with torch.cuda.stream(cs):
-                        h_off.copy_(off, non_blocking=True)
-                        h_ids.copy_(ids, non_blocking=True)
+                    if trace is not None:
+                        e_d0 = torch.cuda.Event(enable_timing=True)
+                        e_d0.record(cs)
+                    if not _NO_COPY:  # cudaMemcpyAsync on the copy stream (nd_result_copy)
+                        csp = _lib.stream_ptr(cs)
+                        _lib.check(L.nd_result_copy(dr._h, _lib.F_FINAL_OFF, _lib.ptr(h_off), csp),
+                                   "nd_result_copy")
+                        _lib.check(L.nd_result_copy(dr._h, _lib.F_FINAL_IDS32, _lib.ptr(h_ids), csp),
+                                   "nd_result_copy")
                     if trace is not None:
                         e_c1 = torch.cuda.Event(enable_timing=True)
                         e_c1.record(st)
                         e_d1 = torch.cuda.Event(enable_timing=True)
                         e_d1.record(cs)
-                        trace.append((getattr(app, "name", "?"), ci, e_c0, e_c1, e_d1,
+                        trace.append((getattr(app, "name", "?"), ci, e_c0, e_c1, e_d0, e_d1,
                                       h_ids.numel() * 4))
                     held.append(dr)
                     out.append(HostChunk(sample_lo + lo, n, h_off, h_ids, dr.total_sampled))
+                    if ji == 0:
+                        first_done.set()
             return out, held
 
         import os
@@ -138,23 +155,38 @@ class HostPipeline:
         if trace is not None:
             t0 = torch.cuda.Event(enable_timing=True)
             t0.record(cur)
-        futs = [_job_pool(k).submit(one, ji, job, st, cs)
-                for ji, (job, st, cs) in enumerate(zip(jobs, streams, self._copy_streams))]
+        # one copy stream for every job: the device has one D2H engine, so the
+        # copies go out in completion order
+        cs0 = self._copy_streams[0]
+        futs = [_job_pool(k).submit(one, ji, job, st, cs0)
+                for ji, (job, st) in enumerate(zip(jobs, streams))]
         done = [f.result() for f in futs]
-        for cs in self._copy_streams[:k]:
-            cur.wait_stream(cs)
+        cur.wait_stream(cs0)
         cur.synchronize()
         if trace is not None:  # chunk timeline (ms from the call): compute start/end, copy end
             import sys
-            for name, ci, c0, c1, d1, nb in trace:
+            for name, ci, c0, c1, d0, d1, nb in trace:
                 print(f"[pipe] {name:9s} chunk {ci}: compute {t0.elapsed_time(c0):7.2f} -> "
-                      f"{t0.elapsed_time(c1):7.2f}  copied {t0.elapsed_time(d1):7.2f}  "
-                      f"({nb / 1e6:.0f} MB)", file=sys.stderr)
+                      f"{t0.elapsed_time(c1):7.2f}  copy {t0.elapsed_time(d0):7.2f} -> "
+                      f"{t0.elapsed_time(d1):7.2f}  ({nb / 1e6:.0f} MB)", file=sys.stderr)
         for _, held in done:
             for h in held:
                 if isinstance(h, DeviceRun):
                     h.close()
         return [out for out, _ in done]
+
+
+def chunk_plan(n: int, chunks: int, lead: bool = False) -> list:
+    """Contiguous sample-id chunks.  With `lead`, the first chunk is a quarter
+    of the others, so its rows reach the host (and the PCIe link gets busy)
+    early while the rest of the GPU work is still ahead."""
+    if n <= 0:
+        return []
+    if chunks <= 1 or not lead:
+        return [(lo, hi) for lo, hi in worker_ranges(n, chunks) if hi > lo]
+    first = max(1, n // (4 * chunks - 3))
+    rest = [(first + lo, first + hi) for lo, hi in worker_ranges(n - first, chunks - 1) if hi > lo]
+    return [(0, first)] + rest
 
 
 def _run_walk_with_roots(plan, dg, droots, R, lo, n, seed, paradigm, step_cap) -> DeviceRun:

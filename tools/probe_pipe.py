@@ -1,0 +1,31 @@
+"""Dev probe: HostPipeline step time on C2 under ND_PIPE_NOCOPY / chunk settings."""
+import statistics
+import sys
+import os
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from oracle import oracle as O  # noqa: E402
+from paper_2009_06693_b200 import make_app  # noqa: E402
+from paper_2009_06693_b200.graph import DeviceGraph  # noqa: E402
+from paper_2009_06693_b200.streaming import HostPipeline  # noqa: E402
+
+dg = DeviceGraph.rmat(22, n_edges=68_993_773, seed=0, weighted=True)
+V = dg.n_vertices
+apps = [make_app("node2vec", p=2.0, q=0.5), make_app("ppr", termination_probability=0.01)]
+roots = torch.from_numpy(O.uniform_roots(V, 1, 7, 0, V).reshape(-1)).pin_memory()
+for cfg in sys.argv[1:] or ["6,3"]:
+    c1, c2 = (int(x) for x in cfg.split(","))
+    pipe = HostPipeline(chunks=c1)
+    jobs = [(apps[0], V, 7, 0, roots, c1), (apps[1], V, 7, 0, roots, c2)]
+    ms = []
+    for it in range(5):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        pipe.run_jobs(dg, jobs)
+        e.record()
+        torch.cuda.synchronize()
+        if it >= 2:
+            ms.append(s.elapsed_time(e))
+    print(cfg, os.environ.get("ND_PIPE_NOCOPY", "0"), round(statistics.median(ms), 2), flush=True)
