@@ -270,7 +270,12 @@ int nd_graph_ensure_lines(nd_graph* G, cudaStream_t s) {
   int64_t n_lines = 0;
   ND_CUDA_TRY(cudaMemcpyAsync(&n_lines, first + V, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   ND_CUDA_TRY(cudaStreamSynchronize(s));
-  if (n_lines >= (1ll << 31)) {  // int32 line offsets
+  // int32 line offsets; and the layout is an accelerator, not a requirement:
+  // without room for it (plus a margin) the picks use the nbp records
+  size_t fr = 0, tot = 0;
+  cudaMemGetInfo(&fr, &tot);
+  const double need = (double)n_lines * sizeof(PickLine) + (double)V * 4 + (double)(2ull << 30);
+  if (n_lines >= (1ll << 31) || need > (double)fr) {
     nd_free(cnt, s); nd_free(first, s);
     return ND_OK;
   }
