@@ -134,31 +134,32 @@ __global__ void k_select(SelCtx c, int64_t n) {
   }
 }
 
-// importance hits: one thread per (sample, slot, transit) triple
+// importance hits: one warp per (sample, slot), lanes over the sample's
+// transits (flag index tri_off[i] + slot * T + k, the triple order of
+// apps.py:286-312)
 __global__ void k_imp_hits(const DevGraph g, const int64_t* __restrict__ toff,
                            const int32_t* __restrict__ tv, const int32_t* __restrict__ out,
                            const uint8_t* __restrict__ alive, const int64_t* __restrict__ tri_off,
                            int64_t n, int64_t m, int64_t total_tri, uint8_t* __restrict__ flag) {
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < total_tri;
-       j += (int64_t)gridDim.x * blockDim.x) {
-    int64_t lo = 0, hi = n;  // sample: last i with tri_off[i] <= j
-    while (hi - lo > 1) {
-      int64_t mid = (lo + hi) >> 1;
-      if (tri_off[mid] <= j) lo = mid; else hi = mid;
-    }
-    const int64_t i = lo;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t ps = warp; ps < n * m; ps += nw) {
+    const int64_t i = ps / m, slot = ps - i * m;
+    if (!alive[i]) continue;
     const int64_t T = toff[i + 1] - toff[i];
-    const int64_t r = j - tri_off[i];
-    const int64_t slot = r / T, k = r - slot * T;
-    const int64_t t = tv[toff[i] + k];
     const int64_t v = out[i * m + slot];
-    const int64_t rlo = __ldg(g.row + t), rhi = __ldg(g.row + t + 1);
+    for (int64_t k = lane; k < T; k += 32) {
+      const int64_t j = tri_off[i] + slot * T + k;
+      const int64_t t = tv[toff[i] + k];
+      const int64_t rlo = __ldg(g.row + t), rhi = __ldg(g.row + t + 1);
     // has_edge(t, v) (graph.py:78-81): the exact hash set when built, else the
     // sorted-row binary search; same answer
-    const bool hit = (g.hset != nullptr && rhi - rlo > HASH_MIN_DEG)
-                         ? (v >= 0 && hset_contains(g.hset + 4 * rlo, hset_size(rhi - rlo), (int32_t)v))
-                         : has_edge(g.col, rlo, rhi, v);
-    flag[j] = hit ? 1 : 0;
+      const bool hit = (g.hset != nullptr && rhi - rlo > HASH_MIN_DEG)
+                           ? (v >= 0 && hset_contains(g.hset + 4 * rlo, hset_size(rhi - rlo), (int32_t)v))
+                           : has_edge(g.col, rlo, rhi, v);
+      flag[j] = hit ? 1 : 0;
+    }
   }
 }
 
@@ -652,8 +653,8 @@ extern "C" int nd_run_collective(const nd_graph* G, int kind, int64_t step_size,
       ND_CUDA_TRY(nd_alloc(&pos, tot_tri + 1, s));
       ND_CUDA_TRY(cudaMemsetAsync(fl, 0, tot_tri + 1, s));
       if (tot_tri)
-        k_imp_hits<<<nd_grid(tot_tri, 256, 148 * 64), 256, 0, s>>>(g, toff, tv, out, alive, tri_off,
-                                                                   n, m, tot_tri, fl);
+        k_imp_hits<<<nd_grid(n * m * 32, 256, 148 * 64), 256, 0, s>>>(g, toff, tv, out, alive,
+                                                                      tri_off, n, m, tot_tri, fl);
       // widen flags for the scan
       {
         auto widen = [] __device__(uint8_t x) { return (int64_t)x; };

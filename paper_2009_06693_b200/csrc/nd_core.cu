@@ -660,14 +660,69 @@ __global__ void k_uniform_roots(int64_t V, int64_t count, uint64_t base, int64_t
   }
 }
 
+// count > 1 (batch roots): one warp per sample.  The lanes draw the first
+// `count` keyed candidates at once; when they hold no repeat -- nearly always
+// for V >> count -- they are the roots (apps.py:92-101 keeps every draw that
+// is new).  Otherwise lane 0 replays the sequential rejection loop.
+constexpr int ROOTS_WARP_MAX = 256;
+
+template <typename OutT>
+__global__ void k_uniform_roots_warp(int64_t V, int64_t count, uint64_t base, int64_t sample_lo,
+                                     int64_t n, OutT* __restrict__ roots) {
+  __shared__ int64_t cand[8][ROOTS_WARP_MAX];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const bool distinct = V >= count;
+  for (int64_t i = warp; i < n; i += nw) {
+    const uint64_t ik = key_item((uint64_t)(sample_lo + i), 0, 0);
+    for (int64_t d = lane; d < count; d += 32)
+      cand[wib][d] = (int64_t)mod_u64(draw_u64(base + C_DRAW * (uint64_t)d, ik), (uint64_t)V);
+    __syncwarp();
+    bool dup = false;
+    if (distinct)
+      for (int64_t d = lane; d < count && !dup; d += 32)
+        for (int64_t e = 0; e < d; e++)
+          if (cand[wib][e] == cand[wib][d]) { dup = true; break; }
+    dup = __any_sync(0xffffffffu, dup);
+    OutT* r = roots + i * count;
+    if (!dup) {
+      for (int64_t d = lane; d < count; d += 32) r[d] = (OutT)cand[wib][d];
+    } else if (lane == 0) {
+      int64_t have = 0;
+      uint64_t b = base;
+      while (have < count) {
+        const int64_t v = (int64_t)mod_u64(draw_u64(b, ik), (uint64_t)V);
+        b += C_DRAW;
+        bool rep = false;
+        for (int64_t k = 0; k < have; k++)
+          if ((int64_t)r[k] == v) { rep = true; break; }
+        if (rep) continue;
+        r[have++] = (OutT)v;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+template <typename OutT>
+static void launch_uniform_roots(int64_t V, int64_t count, uint64_t base, int64_t sample_lo,
+                                 int64_t n, OutT* roots, cudaStream_t s) {
+  if (count > 1 && count <= ROOTS_WARP_MAX)
+    k_uniform_roots_warp<OutT><<<nd_grid(n * 32, 256, 148 * 32), 256, 0, s>>>(V, count, base,
+                                                                             sample_lo, n, roots);
+  else
+    k_uniform_roots<OutT><<<nd_grid(n, 128), 128, 0, s>>>(V, count, base, sample_lo, n, roots);
+}
+
 extern "C" int nd_uniform_roots(const nd_graph* g, int64_t count, uint64_t seed, int64_t sample_lo,
                                 int64_t n_samples, int64_t* roots, void* stream) {
   if (!g || count < 0 || n_samples < 0) return ND_ERR_ARG;
   if (!n_samples || !count) return ND_OK;
   if (g->g.V <= 0) return ND_ERR_ARG;
   cudaStream_t s = (cudaStream_t)stream;
-  k_uniform_roots<int64_t><<<nd_grid(n_samples, 128), 128, 0, s>>>(
-      g->g.V, count, key_base(seed, 0, 2, 0), sample_lo, n_samples, roots);
+  launch_uniform_roots<int64_t>(g->g.V, count, key_base(seed, 0, 2, 0), sample_lo, n_samples,
+                                roots, s);
   ND_CUDA_TRY(cudaGetLastError());
   return ND_OK;
 }
@@ -676,8 +731,7 @@ int nd_uniform_roots_i32(const DevGraph& g, int64_t count, uint64_t seed, int64_
                          int64_t n, int32_t* roots, cudaStream_t s) {
   if (!n || !count) return ND_OK;
   if (g.V <= 0) return ND_ERR_ARG;
-  k_uniform_roots<int32_t><<<nd_grid(n, 128), 128, 0, s>>>(g.V, count, key_base(seed, 0, 2, 0),
-                                                          sample_lo, n, roots);
+  launch_uniform_roots<int32_t>(g.V, count, key_base(seed, 0, 2, 0), sample_lo, n, roots, s);
   ND_CUDA_TRY(cudaGetLastError());
   return ND_OK;
 }
