@@ -249,6 +249,11 @@ int nd_set_profiling(int on);
  * gather-bound walk kernel actually faces (nd_probe.cu). */
 int nd_gather_ceiling(int64_t bytes, int ctas_per_sm, int iters, double *sectors_per_s,
                       void *stream);
+/* Dense final rows, the frontend's getFinalSamples (frontend/src/index.ts:
+ * 160-171): out[n * width] int32 (device), row i = roots then sampled
+ * vertices, padded with -1.  nd_result_max_row gives the natural width. */
+int nd_result_max_row(const nd_result *r, int64_t *host_width);
+int nd_result_dense(const nd_result *r, int64_t width, int32_t *out, void *stream);
 int nd_result_destroy(nd_result *r);
 
 #ifdef __cplusplus

@@ -62,6 +62,8 @@ SIGNATURES = {
     "nd_result_counters": [vp, pi64, i64],
     "nd_result_copy": [vp, i32, vp, vp],
     "nd_result_narrow_ids": [vp, vp],
+    "nd_result_max_row": [vp, pi64],
+    "nd_result_dense": [vp, i64, vp, vp],
     "nd_result_profile": [vp, C.POINTER(C.c_double), i64],
     "nd_set_profiling": [i32],
     "nd_gather_ceiling": [i64, i32, i32, C.POINTER(C.c_double), vp],

@@ -851,6 +851,61 @@ extern "C" int nd_result_narrow_ids(nd_result* r, void* stream) {
   return ND_OK;
 }
 
+// dense final rows (the frontend's getFinalSamples, frontend/src/index.ts:
+// 160-171): row i = sample i's roots then sampled vertices, padded with NULL
+__global__ void k_dense_rows(const int64_t* __restrict__ off, const int32_t* __restrict__ ids,
+                             int64_t n, int64_t width, int32_t* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i < n; i += nw) {
+    const int64_t a = off[i], len = off[i + 1] - a;
+    for (int64_t k = lane; k < width; k += 32) out[i * width + k] = k < len ? ids[a + k] : -1;
+  }
+}
+
+__global__ void k_max_row(const int64_t* __restrict__ off, int64_t n, unsigned long long* __restrict__ mx) {
+  unsigned long long m = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long len = (unsigned long long)(off[i + 1] - off[i]);
+    m = len > m ? len : m;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long x = __shfl_down_sync(0xffffffffu, m, o);
+    m = x > m ? x : m;
+  }
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(mx, m);
+}
+
+extern "C" int nd_result_max_row(const nd_result* r, int64_t* host_width) {
+  if (!r || !host_width) return ND_ERR_ARG;
+  *host_width = 0;
+  if (!r->ptr[ND_F_FINAL_OFF] || r->n <= 0) return ND_OK;
+  unsigned long long* mx = nullptr;
+  ND_CUDA_TRY(nd_alloc(&mx, 1, r->stream));
+  ND_CUDA_TRY(cudaMemsetAsync(mx, 0, sizeof(unsigned long long), r->stream));
+  k_max_row<<<nd_grid(r->n, 256), 256, 0, r->stream>>>(
+      static_cast<const int64_t*>(r->ptr[ND_F_FINAL_OFF]), r->n, mx);
+  unsigned long long h = 0;
+  ND_CUDA_TRY(cudaMemcpyAsync(&h, mx, sizeof(h), cudaMemcpyDeviceToHost, r->stream));
+  ND_CUDA_TRY(cudaStreamSynchronize(r->stream));
+  nd_free(mx, r->stream);
+  *host_width = (int64_t)h;
+  return ND_OK;
+}
+
+extern "C" int nd_result_dense(const nd_result* r, int64_t width, int32_t* out, void* stream) {
+  if (!r || width < 0 || (!out && r->n * width > 0)) return ND_ERR_ARG;
+  if (!r->ptr[ND_F_FINAL_OFF] || !r->ptr[ND_F_FINAL_IDS32] || r->n * width == 0) return ND_OK;
+  cudaStream_t s = stream ? (cudaStream_t)stream : r->stream;
+  k_dense_rows<<<nd_grid(r->n * 32, 256, 148 * 32), 256, 0, s>>>(
+      static_cast<const int64_t*>(r->ptr[ND_F_FINAL_OFF]),
+      static_cast<const int32_t*>(r->ptr[ND_F_FINAL_IDS32]), r->n, width, out);
+  ND_CUDA_TRY(cudaGetLastError());
+  return ND_OK;
+}
+
 extern "C" int nd_result_destroy(nd_result* r) {
   if (!r) return ND_OK;
   if (r->lazy_free) r->lazy_free();

@@ -288,6 +288,22 @@ class DeviceRun:
             self._h, _lib.stream_ptr() if stream is None else stream), "nd_result_narrow_ids")
         return self.view(_lib.F_FINAL_IDS32)
 
+    def final_samples(self, width: int | None = None):
+        """getFinalSamples (frontend/src/index.ts:160-171) without leaving the
+        GPU: an int32 CUDA tensor [n_samples, width], row i = sample i's roots
+        then its sampled vertices, padded with -1 (width: the longest row by
+        default).  Share it zero-copy with torch.utils.dlpack.to_dlpack."""
+        torch = _lib.require_cuda()
+        L = _lib.load()
+        if width is None:
+            w = C.c_int64()
+            _lib.check(L.nd_result_max_row(self._h, C.byref(w)), "nd_result_max_row")
+            width = w.value
+        out = torch.empty((self.n_samples, int(width)), dtype=torch.int32, device="cuda")
+        _lib.check(L.nd_result_dense(self._h, int(width), _lib.ptr(out), _lib.stream_ptr()),
+                   "nd_result_dense")
+        return out
+
     def view(self, f):
         p, c = self.field_count(f)
         return None if not p else device_view(p, c, _lib.FIELD_DTYPE.get(f, "int64"), self)

@@ -393,3 +393,25 @@ def test_concurrent_jobs_and_host_pipeline_match_plain_runs():
             got_len = np.concatenate([np.diff(c.offsets.numpy()) for c in parts])
             assert np.array_equal(got_ids, ids) and np.array_equal(got_len, np.diff(off))
             assert sum(c.n for c in parts) == n and parts[0].sample_lo == 17
+
+
+def test_final_samples_dense_matches_rows():
+    """DeviceRun.final_samples (the frontend's getFinalSamples): dense int32
+    rows padded with -1, equal to the final rows; exported through DLPack."""
+    import torch
+    from torch.utils.dlpack import from_dlpack, to_dlpack
+    from paper_2009_06693_b200 import _lib, make_app
+    from paper_2009_06693_b200.engine import run_device
+    from paper_2009_06693_b200.graph import DeviceGraph
+    dg = DeviceGraph.rmat(12, 16, seed=2, weighted=True)
+    for app in ("ppr", "khop", "fastgcn"):
+        dr = run_device(make_app(app), dg, n_samples=777, seed=5, paradigm="sp" if app != "fastgcn" else "tp")
+        off, ids = dr.host(_lib.F_FINAL_OFF), dr.host(_lib.F_FINAL_IDS)
+        dense = dr.final_samples()
+        width = int(np.diff(off).max())
+        assert dense.shape == (777, width) and dense.dtype == torch.int32
+        d = from_dlpack(to_dlpack(dense)).cpu().numpy()
+        for i in range(777):
+            row = ids[off[i]:off[i + 1]]
+            assert np.array_equal(d[i, :len(row)], row) and (d[i, len(row):] == -1).all()
+        dr.close()
