@@ -21,12 +21,28 @@ runs = [("deepwalk", {}, dg), ("ppr", {}, dg), ("node2vec", {}, dg), ("multirw",
         ("clustergcn", {"clusters_per_sample": 3, "num_clusters": 10}, du)]
 for name, kw, g in runs:
     for par in ("sp", "tp"):
-        app = make_app(name, **kw)
-        if name == "khop" and par == "tp":
-            app.unique = lambda s: s == 0
-        dr = run_device(app, g, n_samples=300, seed=5, paradigm=par)
-        dr.to_output()
-        dr.close()
+        for uniq in ((False, True) if name == "khop" else (False,)):
+            app = make_app(name, **kw)
+            if uniq:  # the step-loop engine (unique steps); otherwise the fixed layout
+                app.unique = lambda s: s == 0
+            dr = run_device(app, g, n_samples=300, seed=5, paradigm=par)
+            dr.to_output()
+            dr.final_samples()
+            dr.close()
+# edge-list ingestion on device (one non-ASCII line goes through the host)
+import os, tempfile  # noqa: E402
+with tempfile.TemporaryDirectory() as td:
+    path = os.path.join(td, "e.txt")
+    with open(path, "w", encoding="utf-8") as fh:
+        fh.write("# c\n0 1 2.5\n1 2\r\n2 0 1e-3\n\u0663 4 0.5\n4 0 7\r5 4\n")
+    g2 = DeviceGraph.from_edge_list(path, weighted=True, undirected=True)
+    dr = run_device(make_app("ppr"), g2, n_samples=50, seed=1, paradigm="sp")
+    dr.close()
+    g2.close()
+from paper_2009_06693_b200 import _lib  # noqa: E402
+import ctypes as C  # noqa: E402
+c = C.c_double()
+_lib.load().nd_gather_ceiling(64 << 20, 1, 4, C.byref(c), None)
 h = dg.to_host()
 n = 5000
 rng = np.random.default_rng(1)
