@@ -398,9 +398,15 @@ def main():
     # pinned host memory per chunk, final rows (int64 offsets + int32 ids)
     # copied back into pinned host buffers while the next chunk samples.
     L.nd_set_profiling(0)
-    from oracle import oracle as O  # noqa: F401  (roots on host: the reference's keyed rule)
     from paper_2009_06693_b200.streaming import HostPipeline
-    roots_host = torch.from_numpy(O.uniform_roots(V, 1, SEED, lo, n).reshape(-1)).pin_memory()
+    # the step's input: the keyed default roots (apps.py:83-103) as a host
+    # array, produced once by the library (nd_uniform_roots) outside the timed steps
+    import ctypes as C
+    droots = torch.empty(n, dtype=torch.int64, device="cuda")
+    _lib.check(L.nd_uniform_roots(dg.handle, 1, C.c_uint64(SEED), lo, n, _lib.ptr(droots),
+                                  _lib.stream_ptr()), "nd_uniform_roots")
+    roots_host = droots.cpu().pin_memory()
+    del droots
     e2e_times, e2e_edges, h2d, d2h = [], 0, 0, 0
     e2e_ok = True
     pipe = HostPipeline(chunks=args.e2e_chunks)

@@ -6,7 +6,6 @@ import os
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from oracle import oracle as O  # noqa: E402
 from paper_2009_06693_b200 import make_app  # noqa: E402
 from paper_2009_06693_b200.graph import DeviceGraph  # noqa: E402
 from paper_2009_06693_b200.streaming import HostPipeline  # noqa: E402
@@ -14,7 +13,11 @@ from paper_2009_06693_b200.streaming import HostPipeline  # noqa: E402
 dg = DeviceGraph.rmat(22, n_edges=68_993_773, seed=0, weighted=True)
 V = dg.n_vertices
 apps = [make_app("node2vec", p=2.0, q=0.5), make_app("ppr", termination_probability=0.01)]
-roots = torch.from_numpy(O.uniform_roots(V, 1, 7, 0, V).reshape(-1)).pin_memory()
+import ctypes as C  # noqa: E402
+from paper_2009_06693_b200 import _lib  # noqa: E402
+_d = torch.empty(V, dtype=torch.int64, device="cuda")
+_lib.check(_lib.load().nd_uniform_roots(dg.handle, 1, C.c_uint64(7), 0, V, _lib.ptr(_d), _lib.stream_ptr()))
+roots = _d.cpu().pin_memory()
 for cfg in sys.argv[1:] or ["6,3"]:
     c1, c2 = (int(x) for x in cfg.split(","))
     pipe = HostPipeline(chunks=c1)
