@@ -415,3 +415,28 @@ def test_final_samples_dense_matches_rows():
             row = ids[off[i]:off[i + 1]]
             assert np.array_equal(d[i, :len(row)], row) and (d[i, len(row):] == -1).all()
         dr.close()
+
+
+@pytest.mark.parametrize("par,R,fan", [("sp", 3, "6,4"), ("tp", 3, "6,4"), ("sp", 2, "4,3,2"),
+                                       ("tp", 1, "3,3,3,2")])
+def test_fixed_layout_matches_step_loop(par, R, fan, tmp_path):
+    """The fixed-layout k-hop (per-sample blocks, no host sync between steps)
+    against the step-loop engine (ND_IND_FIXED=0) on a directed RMAT graph with
+    dead ends: several roots per sample and 3-4 hops; final rows, step rows,
+    TP class counts and adjacency fetches equal."""
+    import os
+    import subprocess
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    helper = os.path.join(repo, "tests", "_khop_engine_dump.py")
+    res = {}
+    for fixed in ("1", "0"):
+        path = str(tmp_path / f"r{fixed}.npz")
+        env = dict(os.environ, ND_IND_FIXED=fixed)
+        subprocess.check_call([sys.executable, helper, repo, path, par, str(R), fan], env=env)
+        res[fixed] = np.load(path)
+    a, b = res["1"], res["0"]
+    for k in ("off", "ids", "sc", "sv", "n_steps", "fetch"):
+        assert np.array_equal(a[k], b[k]), k
+    if par == "tp":
+        assert np.array_equal(a["cls"], b["cls"])
