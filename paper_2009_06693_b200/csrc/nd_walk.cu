@@ -243,6 +243,7 @@ struct PWArgs {
   const NbrU* nbu;
   const PickLine* pl;    // line-packed pick rows (DeepWalk / PPR on weighted graphs) or null
   const int32_t* vline;  // first line of each row (with pl)
+  int chunk;             // walkers a warp claims per queue atomic (32 or 64)
 };
 
 // one 32-byte sector: row bounds, max weight and prefix total of v
@@ -428,7 +429,6 @@ __device__ __forceinline__ int64_t rec_try(const PWArgs& A, int64_t lo, int64_t 
   return n2v_decide(A, nb, w, t, tlo, thi, env, b, ik, st);
 }
 
-constexpr int PW_CHUNK = 64;  // walkers a warp claims per queue atomic
 
 template <int MINB>
 __global__ void __launch_bounds__(256, MINB) k_walk_persistent(PWArgs A) {
@@ -443,7 +443,7 @@ __global__ void __launch_bounds__(256, MINB) k_walk_persistent(PWArgs A) {
   int64_t wbeg = 0, wend = 0;  // this warp's claimed walker range (warp-uniform)
   const bool n2v = A.a.code == ND_NODE2VEC;
   while (true) {
-    // ---- hand out walkers from the warp's chunk (one atomic per PW_CHUNK)
+    // ---- hand out walkers from the warp's chunk (one atomic per A.chunk)
     const bool need = row < 0;
     const unsigned m = __ballot_sync(0xffffffffu, need);
     if (m) {
@@ -452,7 +452,7 @@ __global__ void __launch_bounds__(256, MINB) k_walk_persistent(PWArgs A) {
       int64_t rem = wend - wbeg, nbeg = 0;
       if (rem < c) {
         int base = 0;
-        if (lane == 0) base = atomicAdd(A.queue, PW_CHUNK);
+        if (lane == 0) base = atomicAdd(A.queue, A.chunk);
         nbeg = __shfl_sync(0xffffffffu, base, 0);
       }
       if (need) {
@@ -479,7 +479,7 @@ __global__ void __launch_bounds__(256, MINB) k_walk_persistent(PWArgs A) {
       }
       if (rem < c) {
         wbeg = nbeg + (c - rem);
-        wend = nbeg + PW_CHUNK;
+        wend = nbeg + A.chunk;
       } else {
         wbeg += c;
       }
@@ -913,12 +913,17 @@ static int run_chain_walk_sp(const nd_graph* G, const NdApp& a, int64_t sample_l
              step0 + Lw, ld, W.out, W.nnz, died, nw, nv, nt, ctl + 1, ctl, ctl + 2, ctl + 3, ctr,
              g.vrec, g.ecw, g.epc, g.nbw, g.nbp, g.nbu,
              (a.code == ND_DEEPWALK || a.code == ND_PPR) ? g.pl : nullptr, g.vline};
-    int64_t grid = (int64_t)nsm * occ;
-    const int64_t need = (rows + 255) / 256;
-    if (grid > need) grid = need;
+    // small windows (few walkers per lane, e.g. L2-resident graphs or the
+    // PPR tail): 128-thread CTAs spread over every SM, one walker per lane
+    int64_t tpb = 256, grid = (int64_t)nsm * occ;
+    if (rows < grid * 256) {
+      tpb = 128;
+      grid = std::min<int64_t>((int64_t)nsm * occ * 2, (rows + 127) / 128);
+    }
+    A.chunk = rows <= grid * tpb * 2 ? 32 : 64;
     nd_trace("sp:allocs");
     if (g_profile) cudaEventRecord(pe0, s);
-    kern<<<(unsigned)grid, 256, 0, s>>>(A);
+    kern<<<(unsigned)grid, (unsigned)tpb, 0, s>>>(A);
     if (g_profile) cudaEventRecord(pe1, s);
     ND_CUDA_TRY(cudaGetLastError());
     W.wid = cwid;
