@@ -391,7 +391,7 @@ def main():
                 tp_ms.append(ev0.elapsed_time(ev1))
         tp_info = {"ms_per_step": sum(tp_ms) / len(tp_ms),
                    "value": (edges_dev / len(times)) / (sum(tp_ms) / len(tp_ms) / 1e3),
-                   "note": "TP = per-step radix sort + work classes + sub-warp/CTA/grid kernels"}
+                   "note": "TP = per-step radix sort + work classes + sub-warp/CTA/grid kernels; walker-major tail with exact class statistics below 131,072 alive walkers"}
 
     # ---- e2e through the public API with host buffers ------------------------------
     # HostPipeline (paper_2009_06693_b200/streaming.py): roots uploaded from

@@ -475,6 +475,12 @@ __global__ void __launch_bounds__(256, MINB) k_walk_persistent(PWArgs A) {
           if (A.pl) lo = __ldg(A.vline + v);  // line-packed rows: lo is v's first line
           st.bytes += SECTOR + 8;
           st.sect += 1;
+          if (n2v && t >= 0) {  // continuing node2vec walker: t's row for the probes
+            tlo = __ldg(A.gv.row + t);
+            thi = __ldg(A.gv.row + t + 1);
+            if (mx < 0.0) mx = __ldg(A.gv.mx + v);
+            st.sect += 1;
+          }
         }
       }
       if (rem < c) {
@@ -649,6 +655,110 @@ extern "C" int nd_set_profiling(int on) {
 
 
 
+// One walker-major window: rows [n] (row -> walker wid, or the identity),
+// entering step step0 at vertex vin (previous vertex tin; both null: the roots).
+struct PWindow {
+  int32_t *wid, *out, *nnz, *vin, *tin;
+  int64_t n, step0, Lw, ld;  // Lw = steps this window covers, ld = row stride
+};
+
+static int pw_run_windows(const nd_graph* G, const NdApp& a, uint64_t seed, int64_t sample_lo,
+                          int64_t rows, int32_t* cwid, int32_t* cv, int32_t* ct,
+                          const int64_t* roots, const int32_t* roots32, int64_t R, int64_t step0,
+                          int64_t limit, int64_t Lw_base, int32_t* died, int* ctl,
+                          unsigned long long* ctr, bool keep_inputs, cudaStream_t s,
+                          std::vector<PWindow>& wins, int* h, double* sample_ms);
+static void pw_free_windows(std::vector<PWindow>& wins, cudaStream_t s);
+
+// ---- TP tail: once few walkers remain, TP groups are (nearly) singletons and a
+// step costs its launch chain; the remaining steps run in walker-major windows
+// (identical outputs: every draw is keyed by (sample, step)), and each tail
+// step's TP class statistics are computed exactly afterwards from the logged
+// transits (a radix sort of (step, transit) keys + run lengths).
+__global__ void k_tail_init(const uint32_t* __restrict__ cur, const uint64_t* __restrict__ wp,
+                            int64_t n, int32_t* __restrict__ wid, int32_t* __restrict__ v,
+                            int32_t* __restrict__ t) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t x = wp[i];
+    wid[i] = (int32_t)(x >> 32);
+    v[i] = (int32_t)cur[i];
+    t[i] = (int32_t)(uint32_t)(x & 0xFFFFFFFFull);
+  }
+}
+
+// per row: steps it entered (non-NULL values + the NULL that ended it) and,
+// for walkers that died in the window, their death step
+__global__ void k_tail_rows(const int32_t* __restrict__ wid, const int32_t* __restrict__ nnz,
+                            int64_t n, int64_t step0, int64_t Lw, int32_t* __restrict__ dstep,
+                            int64_t* __restrict__ ent) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    int64_t e = nnz[r];
+    if (e < Lw) {
+      dstep[wid[r]] = (int32_t)(step0 + e);
+      e += 1;
+    }
+    ent[r] = e;
+  }
+}
+
+// (step - tail0, transit) keys of every step a row entered, warp per row
+__global__ void k_tail_keys(const int32_t* __restrict__ vin, const int32_t* __restrict__ out,
+                            const int64_t* __restrict__ ent, const int64_t* __restrict__ koff,
+                            int64_t n, int64_t ld, int64_t rel0, int key_bits,
+                            uint64_t* __restrict__ keys) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < n; r += nw) {
+    const int64_t e = ent[r];
+    uint64_t* dst = keys + koff[r];
+    for (int64_t i = lane; i < e; i += 32) {
+      const int32_t v = i == 0 ? vin[r] : out[r * ld + i - 1];
+      dst[i] = ((uint64_t)(rel0 + i) << key_bits) | (uint32_t)v;
+    }
+  }
+}
+
+// class counts per tail step from the (step, transit) runs: each thread walks
+// a contiguous range of runs (sorted by step) and flushes per step
+__global__ void k_tail_classes(const uint64_t* __restrict__ ukeys, const int* __restrict__ counts,
+                               const int* __restrict__ n_runs, int key_bits, int64_t tail0,
+                               unsigned long long* __restrict__ stats) {
+  constexpr int64_t PER = 64;
+  const int64_t G = *n_runs;
+  for (int64_t b = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * PER; b < G;
+       b += (int64_t)gridDim.x * blockDim.x * PER) {
+    const int64_t e = b + PER < G ? b + PER : G;
+    int64_t cs = -1;
+    unsigned long long c[3] = {0, 0, 0};
+    for (int64_t i = b; i <= e; i++) {
+      const int64_t si = i < e ? tail0 + (int64_t)(ukeys[i] >> key_bits) : -2;
+      if (si != cs) {
+        if (cs >= 0) {
+          unsigned long long* st = stats + 4 * cs;
+          for (int k = 0; k < 3; k++)
+            if (c[k]) atomicAdd(st + k, c[k]);
+          atomicAdd(st + 3, c[0] + c[1] + c[2]);
+        }
+        cs = si;
+        c[0] = c[1] = c[2] = 0;
+      }
+      if (i < e) {
+        const int64_t work = counts[i];  // members * m, m = 1 for walks
+        c[work < SMALL_MAX_WORK ? 0 : (work <= LARGE_MIN_WORK ? 1 : 2)]++;
+      }
+    }
+  }
+}
+
+static int run_tp_tail(const nd_graph* G, const NdApp& a, uint64_t seed, int64_t sample_lo,
+                       int64_t n, int64_t A, const uint32_t* cur, const uint64_t* wp, int64_t R,
+                       int64_t step, int64_t limit, int64_t Lw_base, int key_bits, int32_t* dstep,
+                       int* stall, unsigned long long* ctr, unsigned long long* stats,
+                       cudaStream_t s, std::vector<PWindow>& wins, int64_t& n_steps,
+                       int64_t& items, double& sample_ms);
+
 // byte-model counters (see nd_item.cuh): ctr[0]=bytes, ctr[1]=tries
 static int run_chain_walk(const nd_graph* G, const NdApp& a, int64_t sample_lo, int64_t n,
                           const int64_t* roots, int64_t R, uint64_t seed, int64_t steps,
@@ -698,9 +808,16 @@ static int run_chain_walk(const nd_graph* G, const NdApp& a, int64_t sample_lo, 
   uint64_t* wp_alt = wp1;
   int* h_count = reinterpret_cast<int*>(nd_pinned_scratch());
   double sched_ms = 0, sample_ms = 0;
+  // TP tail threshold (ND_TP_TAIL=0: every step through the TP class kernels)
+  const int64_t tail_T = getenv("ND_TP_TAIL") ? atoll(getenv("ND_TP_TAIL")) : 131072;
+  bool tail = false;
   while (A > 0) {
     if (steps >= 0 && step >= steps) break;
     if (step >= step_cap) break;
+    if (paradigm == ND_TP && A <= tail_T && A * (max_steps - step) < (1ll << 31)) {
+      tail = true;
+      break;
+    }
     if (rec_base + A > rec_cap) {
       int64_t nc = rec_cap * 2 > rec_base + A ? rec_cap * 2 : rec_base + A;
       int32_t *nw = nullptr, *nv = nullptr;
@@ -757,8 +874,15 @@ static int run_chain_walk(const nd_graph* G, const NdApp& a, int64_t sample_lo, 
     A = *h_count;
     step++;
   }
-  const int64_t n_steps = step;
+  const int64_t tp_steps = step;
+  int64_t n_steps = step, tail_items = 0;
   step_base.push_back(rec_base);
+  std::vector<PWindow> tail_wins;
+  if (tail) {
+    ND_TRY(run_tp_tail(G, a, seed, sample_lo, n, A, cur_in, wp_in, R, step, max_steps,
+                       steps >= 0 ? max_steps - step : 128, key_bits, dstep, stall, ctr, stats, s,
+                       tail_wins, n_steps, tail_items, sample_ms));
+  }
   // ---- output compaction -----------------------------------------------------------
   prof.mark();
   const size_t ef = prof.ev.size() - 1;
@@ -769,8 +893,8 @@ static int run_chain_walk(const nd_graph* G, const NdApp& a, int64_t sample_lo, 
   ND_CUDA_TRY(nd_alloc(&final_off, n + 1, s));
   ND_CUDA_TRY(nd_alloc(&clen, n, s));
   ND_CUDA_TRY(nd_alloc(&roots_out, n * R, s));
-  ND_CUDA_TRY(nd_alloc(&d_step_base, n_steps + 1, s));
-  ND_CUDA_TRY(cudaMemcpyAsync(d_step_base, step_base.data(), (n_steps + 1) * sizeof(int64_t),
+  ND_CUDA_TRY(nd_alloc(&d_step_base, tp_steps + 1, s));
+  ND_CUDA_TRY(cudaMemcpyAsync(d_step_base, step_base.data(), (tp_steps + 1) * sizeof(int64_t),
                               cudaMemcpyHostToDevice, s));
   k_chain_lengths<<<nd_grid(n + 1, 256), 256, 0, s>>>(dstep, n, R, n_steps, flen, clen);
   {
@@ -795,7 +919,12 @@ static int run_chain_walk(const nd_graph* G, const NdApp& a, int64_t sample_lo, 
   }
   if (rec_base)
     k_scatter_records<<<nd_grid(rec_base, 256, 148 * 64), 256, 0, s>>>(
-        rec_w, rec_v, rec_base, d_step_base, n_steps, final_off, R, final_ids);
+        rec_w, rec_v, rec_base, d_step_base, tp_steps, final_off, R, final_ids);
+  for (auto& W : tail_wins)
+    if (W.n * W.Lw)
+      k_pw_emit<<<nd_grid(W.n * 32, 256, 148 * 32), 256, 0, s>>>(W.wid, W.out, W.nnz, W.n, W.ld,
+                                                                W.step0, final_off, R, final_ids);
+  pw_free_windows(tail_wins, s);
   prof.mark();
   ND_CUDA_TRY(cudaGetLastError());
   int h_stall = 0;
@@ -816,8 +945,8 @@ static int run_chain_walk(const nd_graph* G, const NdApp& a, int64_t sample_lo, 
   res->set(ND_F_ROOTS, roots_out, n * R);
   res->set(ND_F_CHAIN_LEN, clen, n);
   res->set(ND_F_STATS, stats, 4 * n_steps);
-  res->counters[NDC_ITEMS] = rec_base;
-  res->counters[NDC_PAIRS] = rec_base;
+  res->counters[NDC_ITEMS] = rec_base + tail_items;
+  res->counters[NDC_PAIRS] = rec_base + tail_items;
   res->counters[NDC_N2V_TRIES] = (int64_t)h_ctr[1];
   res->counters[NDC_SLOT_BYTES] = (int64_t)h_ctr[0];
   res->counters[NDC_STEPS] = n_steps;
@@ -839,6 +968,235 @@ __global__ void k_narrow(const int64_t* __restrict__ in, int64_t n, int32_t* __r
     out[i] = (int32_t)in[i];
 }
 
+
+// Run persistent-kernel windows from step0 until no walker continues or
+// `limit`.  Walkers that continue past a window re-enter the next one with
+// their (vertex, previous vertex); later windows get proportionally more
+// steps so a geometric tail runs in one or two launches.  ctl = [queue,
+// cont_n, max_len, stall] (max_len/stall accumulate).  keep_inputs keeps each
+// window's vin/tin (the TP tail derives its transits from them).
+static int pw_run_windows(const nd_graph* G, const NdApp& a, uint64_t seed, int64_t sample_lo,
+                          int64_t rows, int32_t* cwid, int32_t* cv, int32_t* ct,
+                          const int64_t* roots, const int32_t* roots32, int64_t R, int64_t step0,
+                          int64_t limit, int64_t Lw_base, int32_t* died, int* ctl,
+                          unsigned long long* ctr, bool keep_inputs, cudaStream_t s,
+                          std::vector<PWindow>& wins, int* h, double* sample_ms) {
+  const DevGraph& g = G->g;
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  // register/occupancy variant of the persistent kernel (ND_WALK_MINB = 4|5|6|8
+  // resident CTAs per SM requested from ptxas; default measured best)
+  static const int minb = getenv("ND_WALK_MINB") ? atoi(getenv("ND_WALK_MINB")) : 4;
+  void (*kern)(PWArgs) = minb >= 8 ? k_walk_persistent<8>
+                         : minb == 6 ? k_walk_persistent<6>
+                         : minb == 5 ? k_walk_persistent<5> : k_walk_persistent<4>;
+  int occ = 4;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, 0);
+  if (occ < 1) occ = 1;
+  cudaEvent_t pe0 = nullptr, pe1 = nullptr;
+  if (g_profile) {
+    cudaEventCreate(&pe0);
+    cudaEventCreate(&pe1);
+  }
+  const int64_t budget = (rows * Lw_base > (1ll << 24)) ? rows * Lw_base : (1ll << 24);
+  const int64_t first = step0;
+  int rc = ND_OK;
+  while (rows > 0 && step0 < limit) {
+    int64_t Lw = step0 == first ? Lw_base : budget / rows;
+    if (Lw < Lw_base) Lw = Lw_base;
+    if (Lw > limit - step0) Lw = limit - step0;
+    // row stride padded to 8 values: the kernels flush 32-byte aligned chunks
+    const int64_t ld = (Lw + 7) & ~int64_t(7);
+    PWindow W{cwid, nullptr, nullptr, cv, ct, rows, step0, Lw, ld};
+    nd_trace("sp:window-begin");
+    int32_t *nw = nullptr, *nv = nullptr, *nt = nullptr;
+    if (nd_alloc(&W.out, rows * ld, s) != cudaSuccess || nd_alloc(&W.nnz, rows, s) != cudaSuccess ||
+        nd_alloc(&nw, rows, s) != cudaSuccess || nd_alloc(&nv, rows, s) != cudaSuccess ||
+        nd_alloc(&nt, rows, s) != cudaSuccess) {
+      rc = ND_ERR_CUDA;
+    }
+    if (rc == ND_OK && cudaMemsetAsync(ctl, 0, 2 * sizeof(int), s) != cudaSuccess) rc = ND_ERR_CUDA;
+    if (rc != ND_OK) {
+      nd_free(W.out, s); nd_free(W.nnz, s); nd_free(nw, s); nd_free(nv, s); nd_free(nt, s);
+      break;
+    }
+    PWArgs A{view(g), a, seed, sample_lo, rows, cwid, cv, ct, roots, roots32, R, step0,
+             step0 + Lw, ld, W.out, W.nnz, died, nw, nv, nt, ctl + 1, ctl, ctl + 2, ctl + 3, ctr,
+             g.vrec, g.ecw, g.epc, g.nbw, g.nbp, g.nbu,
+             (a.code == ND_DEEPWALK || a.code == ND_PPR) ? g.pl : nullptr, g.vline};
+    // small windows (few walkers per lane, e.g. L2-resident graphs or the
+    // PPR tail): 128-thread CTAs spread over every SM, one walker per lane
+    int64_t tpb = 256, grid = (int64_t)nsm * occ;
+    if (rows < grid * 256) {
+      tpb = 128;
+      grid = std::min<int64_t>((int64_t)nsm * occ * 2, (rows + 127) / 128);
+    }
+    A.chunk = rows <= grid * tpb * 2 ? 32 : 64;
+    nd_trace("sp:allocs");
+    if (g_profile) cudaEventRecord(pe0, s);
+    kern<<<(unsigned)grid, (unsigned)tpb, 0, s>>>(A);
+    if (g_profile) cudaEventRecord(pe1, s);
+    if (cudaGetLastError() != cudaSuccess ||
+        cudaMemcpyAsync(h, ctl, 4 * sizeof(int), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+      rc = ND_ERR_CUDA;
+    nd_trace("sp:window-synced");
+    if (getenv("ND_TRACE") && getenv("ND_TRACE")[0] == '1')
+      fprintf(stderr, "[nd_trace]   window step0=%lld Lw=%lld rows=%lld -> continuing %d\n",
+              (long long)step0, (long long)Lw, (long long)rows, h[1]);
+    if (g_profile && rc == ND_OK) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, pe0, pe1);
+      *sample_ms += ms;
+    }
+    if (!keep_inputs) {
+      nd_free(cv, s);
+      nd_free(ct, s);
+      W.vin = W.tin = nullptr;
+    }
+    wins.push_back(W);
+    cwid = nw;
+    cv = nv;
+    ct = nt;
+    rows = h[1];
+    step0 += Lw;
+    if (rc != ND_OK) break;
+  }
+  nd_free(cwid, s); nd_free(cv, s); nd_free(ct, s);
+  if (g_profile) {
+    cudaEventDestroy(pe0);
+    cudaEventDestroy(pe1);
+  }
+  return rc;
+}
+
+static void pw_free_windows(std::vector<PWindow>& wins, cudaStream_t s) {
+  for (auto& W : wins) {
+    nd_free(W.out, s); nd_free(W.nnz, s); nd_free(W.wid, s); nd_free(W.vin, s); nd_free(W.tin, s);
+  }
+  wins.clear();
+}
+
+__global__ void k_or_flag(int* __restrict__ dst, const int* __restrict__ src) {
+  if (*src) *dst = 1;
+}
+
+static int bits_for(int64_t x) {
+  int b = 1;
+  while ((1ll << b) <= x) b++;
+  return b;
+}
+
+// TP tail (see k_tail_init): the A alive walkers (cur, wp) continue from
+// `step` in walker-major windows; dstep/stall/ctr/stats are updated as the TP
+// steps would have; the windows are returned for the final emission.
+static int run_tp_tail(const nd_graph* G, const NdApp& a, uint64_t seed, int64_t sample_lo,
+                       int64_t n, int64_t A, const uint32_t* cur, const uint64_t* wp, int64_t R,
+                       int64_t step, int64_t limit, int64_t Lw_base, int key_bits, int32_t* dstep,
+                       int* stall, unsigned long long* ctr, unsigned long long* stats,
+                       cudaStream_t s, std::vector<PWindow>& wins, int64_t& n_steps,
+                       int64_t& items, double& sample_ms) {
+  nd_trace("tp:tail-begin");
+  int32_t *wid = nullptr, *v = nullptr, *t = nullptr, *died = nullptr;
+  int* ctl = nullptr;
+  ND_CUDA_TRY(nd_alloc(&wid, A, s));
+  ND_CUDA_TRY(nd_alloc(&v, A, s));
+  ND_CUDA_TRY(nd_alloc(&t, A, s));
+  ND_CUDA_TRY(nd_alloc(&died, n, s));
+  ND_CUDA_TRY(nd_alloc(&ctl, 4, s));
+  ND_CUDA_TRY(cudaMemsetAsync(ctl, 0, 4 * sizeof(int), s));
+  k_tail_init<<<nd_grid(A, 256), 256, 0, s>>>(cur, wp, A, wid, v, t);
+  int* h = reinterpret_cast<int*>(nd_pinned_scratch());
+  h[1] = h[2] = h[3] = 0;
+  int rc = pw_run_windows(G, a, seed, sample_lo, A, wid, v, t, nullptr, nullptr, R, step, limit,
+                          Lw_base, died, ctl, ctr, true, s, wins, h, &sample_ms);
+  if (rc == ND_OK) {
+    k_or_flag<<<1, 1, 0, s>>>(stall, ctl + 3);
+    if ((int64_t)h[2] > n_steps) n_steps = h[2];
+  }
+  nd_free(died, s);
+  nd_free(ctl, s);
+  if (rc != ND_OK) return rc;
+  nd_trace("tp:tail-windows");
+  // entries per row, death steps, key offsets
+  std::vector<int64_t*> ent(wins.size(), nullptr), koff(wins.size(), nullptr);
+  std::vector<int64_t> kbase(wins.size(), 0);
+  int64_t E = 0;
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0;
+  auto need_tmp = [&](size_t b) -> int {
+    if (b <= tmp_bytes) return ND_OK;
+    nd_free(tmp, s);
+    tmp = nullptr;
+    tmp_bytes = b;
+    return nd_alloc((char**)&tmp, b, s) == cudaSuccess ? ND_OK : ND_ERR_CUDA;
+  };
+  for (size_t k = 0; k < wins.size() && rc == ND_OK; k++) {
+    const PWindow& W = wins[k];
+    if (nd_alloc(&ent[k], W.n + 1, s) != cudaSuccess || nd_alloc(&koff[k], W.n + 1, s) != cudaSuccess) {
+      rc = ND_ERR_CUDA;
+      break;
+    }
+    cudaMemsetAsync(ent[k] + W.n, 0, sizeof(int64_t), s);
+    k_tail_rows<<<nd_grid(W.n, 256), 256, 0, s>>>(W.wid, W.nnz, W.n, W.step0, W.Lw, dstep, ent[k]);
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, ent[k], koff[k], W.n + 1, s);
+    if ((rc = need_tmp(tb)) != ND_OK) break;
+    if (cub::DeviceScan::ExclusiveSum(tmp, tb, ent[k], koff[k], W.n + 1, s) != cudaSuccess) {
+      rc = ND_ERR_CUDA;
+      break;
+    }
+    int64_t* hk = nd_pinned_scratch() + 8;
+    if (cudaMemcpyAsync(hk, koff[k] + W.n, sizeof(int64_t), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess) {
+      rc = ND_ERR_CUDA;
+      break;
+    }
+    kbase[k] = E;
+    E += *hk;
+  }
+  uint64_t *keys = nullptr, *sorted = nullptr, *ukeys = nullptr;
+  int *counts = nullptr, *n_runs = nullptr;
+  if (rc == ND_OK && E > 0) {
+    const int end_bit = key_bits + bits_for(n_steps - step);
+    if (end_bit > 64 || E >= (1ll << 31)) rc = ND_ERR_ARG;
+    if (rc == ND_OK && (nd_alloc(&keys, E, s) != cudaSuccess || nd_alloc(&sorted, E, s) != cudaSuccess ||
+                        nd_alloc(&ukeys, E, s) != cudaSuccess || nd_alloc(&counts, E, s) != cudaSuccess ||
+                        nd_alloc(&n_runs, 1, s) != cudaSuccess))
+      rc = ND_ERR_CUDA;
+    for (size_t k = 0; k < wins.size() && rc == ND_OK; k++) {
+      const PWindow& W = wins[k];
+      k_tail_keys<<<nd_grid(W.n * 32, 256, 148 * 32), 256, 0, s>>>(
+          W.vin, W.out, ent[k], koff[k], W.n, W.ld, W.step0 - step, key_bits, keys + kbase[k]);
+    }
+    if (rc == ND_OK) {
+      size_t tb = 0;
+      cub::DeviceRadixSort::SortKeys(nullptr, tb, keys, sorted, (int)E, 0, end_bit, s);
+      size_t tb2 = 0;
+      cub::DeviceRunLengthEncode::Encode(nullptr, tb2, sorted, ukeys, counts, n_runs, (int)E, s);
+      if ((rc = need_tmp(tb > tb2 ? tb : tb2)) == ND_OK) {
+        if (cub::DeviceRadixSort::SortKeys(tmp, tb, keys, sorted, (int)E, 0, end_bit, s) != cudaSuccess ||
+            cub::DeviceRunLengthEncode::Encode(tmp, tb2, sorted, ukeys, counts, n_runs, (int)E, s) !=
+                cudaSuccess)
+          rc = ND_ERR_CUDA;
+      }
+    }
+    if (rc == ND_OK)
+      k_tail_classes<<<nd_grid(E / 64 + 1, 256), 256, 0, s>>>(ukeys, counts, n_runs, key_bits, step,
+                                                               stats);
+  }
+  items = E;
+  for (size_t k = 0; k < wins.size(); k++) {
+    nd_free(ent[k], s);
+    nd_free(koff[k], s);
+  }
+  nd_free(tmp, s); nd_free(keys, s); nd_free(sorted, s); nd_free(ukeys, s); nd_free(counts, s);
+  nd_free(n_runs, s);
+  if (rc == ND_OK && cudaGetLastError() != cudaSuccess) rc = ND_ERR_CUDA;
+  nd_trace("tp:tail-stats");
+  return rc;
+}
 
 // SP chain walk: walker-major persistent kernel over step windows of Lw.
 static int run_chain_walk_sp(const nd_graph* G, const NdApp& a, int64_t sample_lo, int64_t n,
@@ -864,93 +1222,31 @@ static int run_chain_walk_sp(const nd_graph* G, const NdApp& a, int64_t sample_l
     ND_CUDA_TRY(nd_alloc(&roots32, n * R, s));
     ND_TRY(nd_uniform_roots_i32(g, R, seed, sample_lo, n, roots32, s));
   }
-  struct Window {
-    int32_t *wid, *out, *nnz;
-    int64_t n, step0, Lw;
-  };
-  std::vector<Window> wins;
-  int32_t *cwid = nullptr, *cv = nullptr, *ct = nullptr;  // current window inputs
-  int64_t rows = limit > 0 ? n : 0, step0 = 0;
+  std::vector<PWindow> wins;
   int* h = reinterpret_cast<int*>(nd_pinned_scratch());
-  int dev = 0, nsm = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  // register/occupancy variant of the persistent kernel (ND_WALK_MINB = 4|5|6|8
-  // resident CTAs per SM requested from ptxas; default measured best)
-  static const int minb = getenv("ND_WALK_MINB") ? atoi(getenv("ND_WALK_MINB")) : 4;
-  void (*kern)(PWArgs) = minb >= 8 ? k_walk_persistent<8>
-                         : minb == 6 ? k_walk_persistent<6>
-                         : minb == 5 ? k_walk_persistent<5> : k_walk_persistent<4>;
-  int occ = 4;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, 0);
-  if (occ < 1) occ = 1;
+  h[1] = h[2] = h[3] = 0;
   int64_t launches = roots ? 0 : 1;
   double sample_ms = 0.0;
+  {
+    const int rc = pw_run_windows(G, a, seed, sample_lo, limit > 0 ? n : 0, nullptr, nullptr,
+                                  nullptr, roots, roots32, R, 0, limit, Lw_base, died, ctl, ctr,
+                                  false, s, wins, h, &sample_ms);
+    if (rc != ND_OK) {
+      pw_free_windows(wins, s);
+      return rc;
+    }
+  }
+  for (auto& W : wins) {
+    k_pw_accum<<<nd_grid(W.n, 256), 256, 0, s>>>(W.wid, W.nnz, W.n, tot);
+    launches += 2;
+  }
   cudaEvent_t pe0 = nullptr, pe1 = nullptr;
   if (g_profile) {
     cudaEventCreate(&pe0);
     cudaEventCreate(&pe1);
   }
-  // window budget: later windows (few long PPR walks) get proportionally
-  // more steps so the geometric tail runs in one or two launches
-  const int64_t budget = (rows * Lw_base > (1ll << 24)) ? rows * Lw_base : (1ll << 24);
-  while (rows > 0 && step0 < limit) {
-    int64_t Lw = step0 == 0 ? Lw_base : budget / rows;
-    if (Lw < Lw_base) Lw = Lw_base;
-    if (Lw > limit - step0) Lw = limit - step0;
-    // row stride padded to 8 values: the kernels flush 32-byte aligned chunks
-    const int64_t ld = (Lw + 7) & ~int64_t(7);
-    Window W{nullptr, nullptr, nullptr, rows, step0, ld};
-    nd_trace("sp:window-begin");
-    ND_CUDA_TRY(nd_alloc(&W.out, rows * ld, s));
-    ND_CUDA_TRY(nd_alloc(&W.nnz, rows, s));
-    int32_t *nw = nullptr, *nv = nullptr, *nt = nullptr;
-    ND_CUDA_TRY(nd_alloc(&nw, rows, s));
-    ND_CUDA_TRY(nd_alloc(&nv, rows, s));
-    ND_CUDA_TRY(nd_alloc(&nt, rows, s));
-    ND_CUDA_TRY(cudaMemsetAsync(ctl, 0, 2 * sizeof(int), s));
-    PWArgs A{view(g), a, seed, sample_lo, rows, cwid, cv, ct, roots, roots32, R, step0,
-             step0 + Lw, ld, W.out, W.nnz, died, nw, nv, nt, ctl + 1, ctl, ctl + 2, ctl + 3, ctr,
-             g.vrec, g.ecw, g.epc, g.nbw, g.nbp, g.nbu,
-             (a.code == ND_DEEPWALK || a.code == ND_PPR) ? g.pl : nullptr, g.vline};
-    // small windows (few walkers per lane, e.g. L2-resident graphs or the
-    // PPR tail): 128-thread CTAs spread over every SM, one walker per lane
-    int64_t tpb = 256, grid = (int64_t)nsm * occ;
-    if (rows < grid * 256) {
-      tpb = 128;
-      grid = std::min<int64_t>((int64_t)nsm * occ * 2, (rows + 127) / 128);
-    }
-    A.chunk = rows <= grid * tpb * 2 ? 32 : 64;
-    nd_trace("sp:allocs");
-    if (g_profile) cudaEventRecord(pe0, s);
-    kern<<<(unsigned)grid, (unsigned)tpb, 0, s>>>(A);
-    if (g_profile) cudaEventRecord(pe1, s);
-    ND_CUDA_TRY(cudaGetLastError());
-    W.wid = cwid;
-    ND_CUDA_TRY(cudaMemcpyAsync(h, ctl, 4 * sizeof(int), cudaMemcpyDeviceToHost, s));
-    ND_CUDA_TRY(cudaStreamSynchronize(s));
-    nd_trace("sp:window-synced");
-    if (getenv("ND_TRACE") && getenv("ND_TRACE")[0] == '1')
-      fprintf(stderr, "[nd_trace]   window step0=%lld Lw=%lld rows=%lld -> continuing %d\n",
-              (long long)step0, (long long)Lw, (long long)rows, h[1]);
-    if (g_profile) {
-      float ms = 0;
-      cudaEventElapsedTime(&ms, pe0, pe1);
-      sample_ms += ms;
-    }
-    k_pw_accum<<<nd_grid(rows, 256), 256, 0, s>>>(cwid, W.nnz, rows, tot);
-    launches += 2;
-    wins.push_back(W);
-    if (cv) { nd_free(cv, s); nd_free(ct, s); }
-    cwid = nw;
-    cv = nv;
-    ct = nt;
-    rows = h[1];
-    step0 += Lw;
-  }
   const int h_stall = h[3];
   const int64_t n_steps = h[2];
-  nd_free(cwid, s); nd_free(cv, s); nd_free(ct, s);
   // ---- compaction into the final layout -------------------------------------------
   nd_trace("sp:windows-done");
   if (g_profile) cudaEventRecord(pe0, s);
@@ -992,7 +1288,7 @@ static int run_chain_walk_sp(const nd_graph* G, const NdApp& a, int64_t sample_l
   int64_t items = 0;
   for (auto& W : wins) {
     if (W.n * W.Lw)
-      k_pw_emit<<<nd_grid(W.n * 32, 256, 148 * 32), 256, 0, s>>>(W.wid, W.out, W.nnz, W.n, W.Lw,
+      k_pw_emit<<<nd_grid(W.n * 32, 256, 148 * 32), 256, 0, s>>>(W.wid, W.out, W.nnz, W.n, W.ld,
                                                                 W.step0, final_off, R, final_ids);
     items += W.n;  // rows touched (upper bound of pairs)
     launches += 1;
@@ -1003,11 +1299,7 @@ static int run_chain_walk_sp(const nd_graph* G, const NdApp& a, int64_t sample_l
   ND_CUDA_TRY(cudaMemcpyAsync(h_ctr, ctr, sizeof(h_ctr), cudaMemcpyDeviceToHost, s));
   ND_CUDA_TRY(cudaGetLastError());
   ND_CUDA_TRY(cudaStreamSynchronize(s));
-  for (auto& W : wins) {
-    nd_free(W.out, s);
-    nd_free(W.nnz, s);
-    if (W.wid) nd_free(W.wid, s);
-  }
+  pw_free_windows(wins, s);
   if (g_profile) {
     float ms = 0;
     cudaEventElapsedTime(&ms, pe0, pe1);

@@ -100,7 +100,10 @@ class HostPipeline:
             chunks = job[5] if len(job) > 5 and job[5] else self.chunks
             torch.cuda.set_device(dev)
             plan = describe(app)
-            parts = chunk_plan(n_samples, chunks, lead=(ji == 0 and k > 1))
+            if isinstance(chunks, (list, tuple)):  # relative chunk sizes
+                parts = weighted_plan(n_samples, chunks)
+            else:
+                parts = chunk_plan(n_samples, chunks, lead=(ji == 0 and k > 1))
             out, held = [], []
             if ji > 0 and k > 1:
                 first_done.wait(timeout=60)  # the link gets busy before the GPU is shared
@@ -187,6 +190,19 @@ def chunk_plan(n: int, chunks: int, lead: bool = False) -> list:
     first = max(1, n // (4 * chunks - 3))
     rest = [(first + lo, first + hi) for lo, hi in worker_ranges(n - first, chunks - 1) if hi > lo]
     return [(0, first)] + rest
+
+
+def weighted_plan(n: int, weights) -> list:
+    """Contiguous sample-id chunks with sizes proportional to `weights`
+    (e.g. (1, 4, 4, 4, 1): small first and last chunks, so the link starts
+    early and the last exposed copy is short)."""
+    if n <= 0:
+        return []
+    w = np.asarray(weights, dtype=np.float64)
+    if w.ndim != 1 or len(w) == 0 or (w <= 0).any():
+        raise ValueError("chunk weights must be positive")
+    cuts = np.rint(np.concatenate([[0.0], np.cumsum(w)]) / w.sum() * n).astype(np.int64)
+    return [(int(a), int(b)) for a, b in zip(cuts[:-1], cuts[1:]) if b > a]
 
 
 def _run_walk_with_roots(plan, dg, droots, R, lo, n, seed, paradigm, step_cap) -> DeviceRun:

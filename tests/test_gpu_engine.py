@@ -1,6 +1,7 @@
 """End-to-end parity of the device engine (tp_run / sp_run through the
 C-ABI) against the reference's golden hashes and the C oracle."""
 
+import os
 import numpy as np
 import pytest
 
@@ -27,9 +28,15 @@ def _device_run(meta, paradigm):
     return run(app, dg, samples, EngineConfig(seed=meta["seed"]))
 
 
-@pytest.mark.parametrize("paradigm", ["tp", "sp"])
+@pytest.mark.parametrize("paradigm", ["tp", "tp-classes", "sp"])
 @pytest.mark.parametrize("meta", _cases(WALKS), ids=lambda m: f"{m['idx']}-{m['app']}-{m['graph']}")
-def test_walk_runs_match_reference(meta, paradigm):
+def test_walk_runs_match_reference(meta, paradigm, monkeypatch):
+    # "tp": golden runs are small, so every step runs in the TP tail (walker-major
+    # windows + class statistics from the logged transits); "tp-classes": every
+    # step through the TP class kernels (ND_TP_TAIL=0)
+    if paradigm == "tp-classes":
+        monkeypatch.setenv("ND_TP_TAIL", "0")
+        paradigm = "tp"
     out = _device_run(meta, paradigm)
     tf, ts = texts(out)
     assert out.n_steps == meta["n_steps"]
@@ -106,12 +113,21 @@ def test_walks_on_rmat_vs_oracle(app, params, weighted):
     a = make_app(app, **params)
     meta = {"app": app, "params": params, "n_samples": n, "seed": 9}
     ref = oracle_run(meta, og, paradigm="tp", n_threads=1)
-    for par in ("tp", "sp"):
-        dr = run_device(a, dg, n_samples=n, seed=9, paradigm=par)
+    # TP with every step in the class kernels, with the hand-off to the
+    # walker-major tail mid-run, and with the default threshold (all tail)
+    for par, tail in (("tp", "0"), ("tp", "5000"), ("tp", None), ("sp", None)):
+        if tail is None:
+            os.environ.pop("ND_TP_TAIL", None)
+        else:
+            os.environ["ND_TP_TAIL"] = tail
+        try:
+            dr = run_device(a, dg, n_samples=n, seed=9, paradigm=par)
+        finally:
+            os.environ.pop("ND_TP_TAIL", None)
         out = dr.to_output()
         off, ids = out.final_csr()
         roff, rids = ref.final_csr()
-        assert np.array_equal(off, roff) and np.array_equal(ids, rids), par
+        assert np.array_equal(off, roff) and np.array_equal(ids, rids), (par, tail)
         assert out.n_steps == ref.n_steps
         if par == "tp":
             st = dr.stats()
@@ -279,7 +295,7 @@ def test_index_paths_on_adversarial_hub_graph(app):
         dr = run_device(make_app(app), dg, n_samples=n, seed=33, paradigm=par)
         off, ids = dr.host(0), dr.host(1)
         roff, rids = ref.final_csr()
-        assert np.array_equal(off, roff) and np.array_equal(ids, rids), par
+        assert np.array_equal(off, roff) and np.array_equal(ids, rids), (par, tail)
         dr.close()
 
 

@@ -18,9 +18,13 @@ from paper_2009_06693_b200 import _lib  # noqa: E402
 _d = torch.empty(V, dtype=torch.int64, device="cuda")
 _lib.check(_lib.load().nd_uniform_roots(dg.handle, 1, C.c_uint64(7), 0, V, _lib.ptr(_d), _lib.stream_ptr()))
 roots = _d.cpu().pin_memory()
+def spec(x):  # "6" -> 6 chunks, "1:4:4:1" -> relative sizes
+    return tuple(float(v) for v in x.split(":")) if ":" in x else int(x)
+
+
 for cfg in sys.argv[1:] or ["6,3"]:
-    c1, c2 = (int(x) for x in cfg.split(","))
-    pipe = HostPipeline(chunks=c1)
+    c1, c2 = (spec(x) for x in cfg.split(","))
+    pipe = HostPipeline(chunks=c1 if isinstance(c1, int) else len(c1))
     jobs = [(apps[0], V, 7, 0, roots, c1), (apps[1], V, 7, 0, roots, c2)]
     ms = []
     for it in range(5):
