@@ -19,8 +19,17 @@ runs = [("deepwalk", {}, dg), ("ppr", {}, dg), ("node2vec", {}, dg), ("multirw",
         ("khop", {}, du), ("layer", {"max_size": 200, "step_size": 50}, du), ("fastgcn", {}, du),
         ("ladies", {"distribution": "degree_sq"}, du), ("mvs", {}, du),
         ("clustergcn", {"clusters_per_sample": 3, "num_clusters": 10}, du)]
+import os  # noqa: E402
 for name, kw, g in runs:
     for par in ("sp", "tp"):
+        if par == "tp" and name in ("ppr", "node2vec", "deepwalk"):
+            # TP walks: all steps in the class kernels, then a mid-run hand-off to the tail
+            for tail in ("0", "100"):
+                os.environ["ND_TP_TAIL"] = tail
+                dr = run_device(make_app(name, **kw), g, n_samples=300, seed=5, paradigm=par)
+                dr.to_output()
+                dr.close()
+            os.environ.pop("ND_TP_TAIL")
         for uniq in ((False, True) if name == "khop" else (False,)):
             app = make_app(name, **kw)
             if uniq:  # the step-loop engine (unique steps); otherwise the fixed layout
