@@ -422,7 +422,7 @@ def main():
         ev1.record(stream)
         torch.cuda.synchronize()
         step_edges = sum(c.total_sampled for chunks in res for c in chunks)
-        step_h2d = roots_host.numel() * roots_host.element_size() * len(apps)
+        step_h2d = pipe.last_h2d_bytes  # the roots, uploaded once for both apps
         step_d2h = sum(c.offsets.numel() * c.offsets.element_size() + c.ids.numel() * c.ids.element_size()
                        for chunks in res for c in chunks)
         if it == 0:  # host rows == device rows of a plain run (checksums, outside the timed steps)

@@ -26,8 +26,8 @@ from .engine import DeviceRun, describe, run_device
 from .graph import as_device_graph
 from .sharding import worker_ranges
 
-import os as _os
-_NO_COPY = _os.environ.get("ND_PIPE_NOCOPY") == "1"  # dev: time the pipeline without D2H
+import os
+_NO_COPY = os.environ.get("ND_PIPE_NOCOPY") == "1"  # dev: time the pipeline without D2H
 
 
 @dataclass
@@ -56,6 +56,7 @@ class HostPipeline:
         self.step_cap = step_cap
         self._pinned = {}
         self._copy_streams = []
+        self.last_h2d_bytes = 0  # host->device bytes of the last run (roots)
 
     def _buf(self, key, like):
         import torch
@@ -89,6 +90,19 @@ class HostPipeline:
         cur = torch.cuda.current_stream()
         dev = torch.cuda.current_device()
         streams = job_streams(k)
+        # every job's roots go up in one copy before any sampling starts: a
+        # host->device copy running under the walk kernels slows them several
+        # fold (tools/probe_copy_interference.py), device->host copies do not.
+        # Jobs sharing one host roots array share its upload.
+        per_chunk = os.environ.get("ND_PIPE_ROOTS") == "chunk"  # dev: the old per-chunk upload
+        dev_roots, self.last_h2d_bytes = {}, 0
+        if not per_chunk:
+            with torch.cuda.stream(cur):
+                for job in jobs:
+                    rh = job[4]
+                    if rh is not None and id(rh) not in dev_roots:
+                        dev_roots[id(rh)] = rh.to("cuda", non_blocking=True)
+                        self.last_h2d_bytes += rh.numel() * rh.element_size()
         for st in streams:
             st.wait_stream(cur)
 
@@ -115,7 +129,11 @@ class HostPipeline:
                         e_c0.record(st)
                     if roots_host is not None:
                         R = len(roots_host) // max(n_samples, 1)
-                        droots = roots_host[lo * R:hi * R].to("cuda", non_blocking=True)
+                        if per_chunk:
+                            droots = roots_host[lo * R:hi * R].to("cuda", non_blocking=True)
+                            self.last_h2d_bytes += droots.numel() * droots.element_size()
+                        else:
+                            droots = dev_roots[id(roots_host)][lo * R:hi * R]
                         held.append(droots)
                         dr = _run_walk_with_roots(plan, dg, droots, R, sample_lo + lo, n, seed,
                                                   self.paradigm, self.step_cap)
@@ -152,7 +170,6 @@ class HostPipeline:
                         first_done.set()
             return out, held
 
-        import os
         trace = [] if os.environ.get("ND_PIPE_TRACE") == "1" else None
         t0 = None
         if trace is not None:

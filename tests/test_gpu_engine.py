@@ -409,6 +409,31 @@ def test_concurrent_jobs_and_host_pipeline_match_plain_runs():
             got_len = np.concatenate([np.diff(c.offsets.numpy()) for c in parts])
             assert np.array_equal(got_ids, ids) and np.array_equal(got_len, np.diff(off))
             assert sum(c.n for c in parts) == n and parts[0].sample_lo == 17
+    # explicit host roots shared by the walk jobs (uploaded once, before sampling),
+    # weighted chunk plans, and the old per-chunk upload: rows equal plain runs
+    rng = np.random.default_rng(4)
+    roots = torch.from_numpy(rng.integers(0, dg.n_vertices, n)).pin_memory()
+    ref2 = []
+    for a in apps:
+        droots = roots.to("cuda")
+        from paper_2009_06693_b200.streaming import _run_walk_with_roots
+        from paper_2009_06693_b200.engine import describe
+        dr = _run_walk_with_roots(describe(a), dg, droots, 1, 17, n, seed, "sp", 10_000)
+        ref2.append((dr.host(_lib.F_FINAL_OFF), dr.host(_lib.F_FINAL_IDS)))
+        dr.close()
+    for mode, spec in ((None, 3), (None, (1, 5, 5, 2)), ("chunk", 2)):
+        if mode:
+            os.environ["ND_PIPE_ROOTS"] = mode
+        try:
+            pipe = HostPipeline(chunks=3)
+            res = pipe.run_jobs(dg, [(a, n, seed, 17, roots, spec) for a in apps])
+        finally:
+            os.environ.pop("ND_PIPE_ROOTS", None)
+        assert pipe.last_h2d_bytes == n * 8 * (len(apps) if mode else 1)
+        for parts, (off, ids) in zip(res, ref2):
+            got_ids = np.concatenate([c.ids.numpy().astype(np.int64) for c in parts])
+            got_len = np.concatenate([np.diff(c.offsets.numpy()) for c in parts])
+            assert np.array_equal(got_ids, ids) and np.array_equal(got_len, np.diff(off)), (mode, spec)
 
 
 def test_final_samples_dense_matches_rows():

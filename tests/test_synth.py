@@ -16,3 +16,14 @@ def test_generators_match_reference(key):
     assert np.array_equal(g.row_offsets, d[f"{key}/row_offsets"])
     assert np.array_equal(g.col_indices, d[f"{key}/col_indices"])
     assert np.array_equal(g.weights, d[f"{key}/weights"])
+
+
+def test_weighted_chunk_plan():
+    from paper_2009_06693_b200.streaming import chunk_plan, weighted_plan
+    assert weighted_plan(100, (1, 4, 4, 1)) == [(0, 10), (10, 50), (50, 90), (90, 100)]
+    assert weighted_plan(0, (1, 2)) == [] and chunk_plan(0, 3) == []
+    parts = weighted_plan(12345, (0.5, 5, 5, 5, 1))
+    assert parts[0][0] == 0 and parts[-1][1] == 12345
+    assert all(a[1] == b[0] for a, b in zip(parts, parts[1:]))
+    with pytest.raises(ValueError):
+        weighted_plan(10, (1, 0))
