@@ -80,7 +80,7 @@ def app_spec(app, params):
     raise ValueError(app)
 
 
-def oracle_run(meta, g: O.OGraph, paradigm="tp", n_threads=1):
+def oracle_run(meta, g: O.OGraph, paradigm="tp", n_threads=1, step_cap=10_000):
     """Run one golden case through the C oracle; returns SampleSetOutput."""
     app, n, seed = meta["app"], meta["n_samples"], meta["seed"]
     sp = app_spec(app, meta["params"])
@@ -93,7 +93,7 @@ def oracle_run(meta, g: O.OGraph, paradigm="tp", n_threads=1):
     if "kind" in sp:
         r = O.run_collective(g, sp["kind"], sp["m"], roots, seed, sp["steps"],
                              max_size=sp.get("max_size", 0), distribution=sp.get("distribution", 0),
-                             unique=um)
+                             unique=um, step_cap=step_cap)
         roff = np.concatenate([[0], np.cumsum([len(x) for x in roots])])
         out = SampleSetOutput(ids, roff, np.concatenate(roots), r["n_steps"], stats=r["stats"],
                               step_counts=r["step_counts"], step_vals=r["vals"],
@@ -101,12 +101,12 @@ def oracle_run(meta, g: O.OGraph, paradigm="tp", n_threads=1):
         return out
     if app == "khop":
         r = O.run_individual(g, 3, [], sp["fanouts"], roots, seed, sp["steps"], paradigm=paradigm,
-                             unique=um)
+                             unique=um, step_cap=step_cap)
         roff = np.concatenate([[0], np.cumsum([len(x) for x in r["roots"]])])
         return SampleSetOutput(ids, roff, np.concatenate(r["roots"]), r["n_steps"], stats=r["stats"],
                                step_counts=r["step_counts"], step_vals=r["vals"])
     r = O.run_chain(g, sp["code"], sp["kparams"], np.asarray(roots), seed, sp["steps"],
-                    paradigm=paradigm, n_threads=n_threads)
+                    paradigm=paradigm, n_threads=n_threads, step_cap=step_cap)
     R = r["roots"].shape[1]
     return SampleSetOutput(ids, np.arange(n + 1) * R, r["roots"].ravel(), r["n_steps"], stats=r["stats"],
                            chain_off=np.concatenate([[0], np.cumsum(r["chain_len"])]),

@@ -481,3 +481,79 @@ def test_fixed_layout_matches_step_loop(par, R, fan, tmp_path):
         assert np.array_equal(a[k], b[k]), k
     if par == "tp":
         assert np.array_equal(a["cls"], b["cls"])
+
+
+def _final_equal(dr, ref, tag):
+    out = dr.to_output()
+    off, ids = out.final_csr()
+    roff, rids = ref.final_csr()
+    assert np.array_equal(off, roff) and np.array_equal(ids, rids), tag
+    assert out.n_steps == ref.n_steps, tag
+    return out
+
+
+@pytest.mark.parametrize("app,params", [("ppr", {}), ("node2vec", {"walk_length": 30}),
+                                        ("deepwalk", {}), ("multirw", {"roots_per_sample": 4})])
+def test_step_cap_and_tp_tail_vs_oracle(app, params):
+    """Walks cut by a small step cap (INF-length PPR reaches it inside the
+    walker-major windows), for SP, TP in the class kernels, TP handing off to
+    the tail mid-run and TP all tail: rows, n_steps and TP class counts equal
+    the oracle's."""
+    from paper_2009_06693_b200 import make_app
+    from paper_2009_06693_b200.engine import run_device
+    from paper_2009_06693_b200.graph import DeviceGraph
+    dg = DeviceGraph.rmat(12, 16, seed=3, weighted=app != "multirw")
+    hg = dg.to_host()
+    og = O.OGraph(hg.n_vertices, hg.row_offsets, hg.col_indices, hg.weights,
+                  hg.per_vertex_weight_prefix, hg.per_vertex_max_weight, np.arange(hg.n_vertices))
+    n, cap = 3000, 9
+    meta = {"app": app, "params": params, "n_samples": n, "seed": 9}
+    ref = oracle_run(meta, og, paradigm="tp", step_cap=cap)
+    a = make_app(app, **params)
+    for par, tail in (("sp", None), ("tp", "0"), ("tp", "300"), ("tp", None)):
+        if tail is not None:
+            os.environ["ND_TP_TAIL"] = tail
+        try:
+            dr = run_device(a, dg, n_samples=n, seed=9, paradigm=par, step_cap=cap)
+        finally:
+            os.environ.pop("ND_TP_TAIL", None)
+        _final_equal(dr, ref, (app, par, tail))
+        if par == "tp":
+            st = dr.stats()
+            got = np.array([[t.groups_small, t.groups_medium, t.groups_large] for t in st.timings])
+            assert np.array_equal(got.reshape(-1, 3), ref.stats[:, :3]), (app, tail)
+        dr.close()
+
+
+def test_edgeless_graph_and_empty_jobs():
+    """A graph with vertices and no edges (every walk and hop ends at its
+    root; collective steps find nothing), and zero-sample jobs for every app
+    and paradigm."""
+    from paper_2009_06693_b200 import make_app
+    from paper_2009_06693_b200.engine import run_device
+    from paper_2009_06693_b200.graph import DeviceGraph
+    V = 64
+    dg0 = DeviceGraph.from_arrays(np.zeros(V + 1, dtype=np.int64), np.zeros(0, dtype=np.int64))
+    hg = dg0.to_host()
+    og = O.OGraph(hg.n_vertices, hg.row_offsets, hg.col_indices, hg.weights,
+                  hg.per_vertex_weight_prefix, hg.per_vertex_max_weight, np.arange(V))
+    dg = DeviceGraph.rmat(10, 8, seed=1, weighted=True)
+    cases = [("deepwalk", {}), ("ppr", {}), ("node2vec", {}), ("multirw", {"roots_per_sample": 4}),
+             ("khop", {}), ("layer", {"max_size": 40, "step_size": 8}), ("fastgcn", {}), ("mvs", {})]
+    for app, params in cases:
+        a = make_app(app, **params)
+        meta = {"app": app, "params": params, "n_samples": 40, "seed": 5}
+        ref = oracle_run(meta, og, paradigm="tp")
+        for par in ("sp", "tp"):
+            dr = run_device(a, dg0, n_samples=40, seed=5, paradigm=par)
+            out = dr.to_output()
+            off, ids = out.final_csr()
+            roff, rids = ref.final_csr()
+            assert np.array_equal(off, roff) and np.array_equal(ids, rids), (app, par)
+            assert dr.total_sampled == ref.total_sampled(), (app, par, dr.total_sampled,
+                                                             ref.total_sampled())
+            dr.close()
+            dr = run_device(a, dg, n_samples=0, seed=5, paradigm=par)
+            assert dr.total_sampled == 0, (app, par)
+            assert list(dr.to_output().final_csr()[0]) == [0], (app, par)
+            dr.close()
