@@ -38,6 +38,8 @@ struct ChainAct {
   int* ncount;
   int32_t* dstep;
   int* stall;
+  int32_t* rows;  // fixed-length walks: per-walker rows [n, ld] written in place (else records)
+  int64_t ld;
 
   template <class RowT>
   __device__ __forceinline__ void operator()(int64_t i, int64_t v, uint64_t val, const RowT& row,
@@ -48,8 +50,12 @@ struct ChainAct {
     const int64_t out = run_item(gv, row, a, v, deg, t, base0,
                                  key_item((uint64_t)(sample_lo + w), 0, 0), st, &stl);
     if (stl) atomicExch(stall, 1);
-    rec_w[i] = w;
-    rec_v[i] = (int32_t)out;
+    if (rows != nullptr) {
+      if (out >= 0) rows[(int64_t)w * ld + step] = (int32_t)out;
+    } else {
+      rec_w[i] = w;
+      rec_v[i] = (int32_t)out;
+    }
     const int64_t slot = warp_append(out >= 0, ncount);
     if (slot >= 0) {
       ncur[slot] = (uint32_t)out;
@@ -150,6 +156,23 @@ __global__ void k_scatter_records(const int32_t* __restrict__ rec_w, const int32
       if (step_base[mid] <= r) lo = mid; else hi = mid;
     }
     ids[off[rec_w[r]] + R + lo] = v;
+  }
+}
+
+// fixed-length TP walks: each walker's first min(len, steps) values from its row
+__global__ void k_rows_emit(const int32_t* __restrict__ rows, int64_t ld,
+                            const int32_t* __restrict__ dstep, int64_t n, int64_t n_steps,
+                            int64_t steps, const int64_t* __restrict__ off, int64_t R,
+                            int32_t* __restrict__ ids) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < n; w += nw) {
+    const int32_t d = dstep[w];
+    int64_t len = d >= 0 ? d : n_steps;
+    if (len > steps) len = steps;
+    const int32_t* src = rows + w * ld;
+    int32_t* dst = ids + off[w] + R;
+    for (int64_t k = lane; k < len; k += 32) dst[k] = src[k];
   }
 }
 
@@ -793,7 +816,13 @@ static int run_chain_walk(const nd_graph* G, const NdApp& a, int64_t sample_lo, 
     ND_TRY(nd_uniform_roots_i32(g, R, seed, sample_lo, n, roots32, s));
   }
   if (n) k_init_chain<<<nd_grid(n, 256), 256, 0, s>>>(roots, roots32, n, R, cur0, wp0, dstep);
-  rec_cap = steps >= 0 ? n * max_steps : n * 128;
+  // fixed-length walks write each value into its walker's row (one random
+  // 4-byte store, then a coalesced emission); INF-length walks keep per-step
+  // records scattered at the end
+  int32_t* rows = nullptr;
+  const bool direct = steps >= 0 && max_steps > 0;
+  if (direct) ND_CUDA_TRY(nd_alloc(&rows, n * max_steps, s));
+  rec_cap = direct ? 0 : (steps >= 0 ? n * max_steps : n * 128);
   ND_CUDA_TRY(nd_alloc(&rec_w, rec_cap, s));
   ND_CUDA_TRY(nd_alloc(&rec_v, rec_cap, s));
 
@@ -818,7 +847,7 @@ static int run_chain_walk(const nd_graph* G, const NdApp& a, int64_t sample_lo, 
       tail = true;
       break;
     }
-    if (rec_base + A > rec_cap) {
+    if (!direct && rec_base + A > rec_cap) {
       int64_t nc = rec_cap * 2 > rec_base + A ? rec_cap * 2 : rec_base + A;
       int32_t *nw = nullptr, *nv = nullptr;
       ND_CUDA_TRY(nd_alloc(&nw, nc, s));
@@ -846,7 +875,7 @@ static int run_chain_walk(const nd_graph* G, const NdApp& a, int64_t sample_lo, 
       // the sorted state is Current(); the next state is written to Alternate()
       ChainAct act{view(g), a, key_base(seed, (uint64_t)step, 0, 0), sample_lo, (int)step,
                    rec_w + rec_base, rec_v + rec_base, dk.Alternate(), dv.Alternate(), ncount,
-                   dstep, stall};
+                   dstep, stall, rows, max_steps};
       ND_TRY(tp_run_sorted(dk.Current(), dv.Current(), A, 1, g, stage_spec(need_pre, need_w), act,
                            S, ctr, st_step, s));
       cur_in = dk.Alternate();
@@ -856,7 +885,8 @@ static int run_chain_walk(const nd_graph* G, const NdApp& a, int64_t sample_lo, 
     } else {
       prof.mark();
       ChainAct act{view(g), a, key_base(seed, (uint64_t)step, 0, 0), sample_lo, (int)step,
-                   rec_w + rec_base, rec_v + rec_base, cur_alt, wp_alt, ncount, dstep, stall};
+                   rec_w + rec_base, rec_v + rec_base, cur_alt, wp_alt, ncount, dstep, stall,
+                   rows, max_steps};
       ND_TRY(sp_step(cur_in, wp_in, A, g, act, ctr, st_step, s));
       k_stats_fetch<<<1, 1, 0, s>>>(st_step, (unsigned long long)A);
       std::swap(cur_in, cur_alt);
@@ -917,7 +947,10 @@ static int run_chain_walk(const nd_graph* G, const NdApp& a, int64_t sample_lo, 
       k_write_roots<int32_t><<<nd_grid(n * R, 256), 256, 0, s>>>(roots32, n, R, final_off,
                                                                 final_ids, roots_out);
   }
-  if (rec_base)
+  if (direct && n && tp_steps)
+    k_rows_emit<<<nd_grid(n * 32, 256, 148 * 32), 256, 0, s>>>(rows, max_steps, dstep, n, n_steps,
+                                                               tp_steps, final_off, R, final_ids);
+  else if (!direct && rec_base)
     k_scatter_records<<<nd_grid(rec_base, 256, 148 * 64), 256, 0, s>>>(
         rec_w, rec_v, rec_base, d_step_base, tp_steps, final_off, R, final_ids);
   for (auto& W : tail_wins)
@@ -956,7 +989,7 @@ static int run_chain_walk(const nd_graph* G, const NdApp& a, int64_t sample_lo, 
 
   nd_free(cur0, s); nd_free(cur1, s); nd_free(wp0, s); nd_free(wp1, s);
   nd_free(dstep, s); nd_free(ncount, s); nd_free(stall, s); nd_free(ctr, s);
-  nd_free(rec_w, s); nd_free(rec_v, s); nd_free(roots32, s); nd_free(flen, s);
+  nd_free(rec_w, s); nd_free(rec_v, s); nd_free(rows, s); nd_free(roots32, s); nd_free(flen, s);
   nd_free(d_step_base, s);
   if (paradigm == ND_TP) S.release(s);
   return h_stall ? ND_ERR_STALL : ND_OK;
