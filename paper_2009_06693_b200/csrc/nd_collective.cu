@@ -44,7 +44,7 @@ int scan_excl(const T* in, T* out, int64_t n, cudaStream_t s) {
 
 template <typename T>
 int dcopy_to_host(T* h, const T* d, int64_t n, cudaStream_t s) {
-  ND_CUDA_TRY(cudaMemcpyAsync(h, d, n * sizeof(T), cudaMemcpyDeviceToHost, s));
+  ND_TRY(nd_d2h(h, d, n * sizeof(T), s));
   ND_CUDA_TRY(cudaStreamSynchronize(s));
   return ND_OK;
 }

@@ -86,6 +86,32 @@ int nd_pool_init() {
 
 // one pinned host word-block per thread for small D2H reads (no per-run
 // cudaMallocHost/cudaFreeHost, which serialise the device)
+__global__ void k_export(const unsigned char* __restrict__ src, unsigned char* __restrict__ dst,
+                         int64_t bytes) {
+  for (int64_t i = threadIdx.x; i < bytes; i += blockDim.x) dst[i] = src[i];
+}
+
+int nd_d2h(void* dst, const void* src, int64_t bytes, cudaStream_t s) {
+  constexpr int64_t CAP = 1 << 16;
+  static thread_local unsigned char* stage = nullptr;  // mapped pinned staging
+  static thread_local unsigned char* dstage = nullptr;
+  if (bytes <= 0) return ND_OK;
+  if (bytes > CAP) {
+    ND_TRY(nd_d2h(dst, src, bytes, s));
+    ND_CUDA_TRY(cudaStreamSynchronize(s));
+    return ND_OK;
+  }
+  if (!stage) {
+    ND_CUDA_TRY(cudaHostAlloc((void**)&stage, CAP, cudaHostAllocMapped | cudaHostAllocPortable));
+    ND_CUDA_TRY(cudaHostGetDevicePointer((void**)&dstage, stage, 0));
+  }
+  k_export<<<1, 256, 0, s>>>(static_cast<const unsigned char*>(src), dstage, bytes);
+  ND_CUDA_TRY(cudaGetLastError());
+  ND_CUDA_TRY(cudaStreamSynchronize(s));
+  std::memcpy(dst, stage, bytes);
+  return ND_OK;
+}
+
 int64_t* nd_pinned_scratch() {
   static thread_local int64_t* p = nullptr;
   if (!p) cudaMallocHost(&p, 64 * sizeof(int64_t));
@@ -217,7 +243,7 @@ extern "C" int nd_individual_batch(int app_code, const double* host_params, int6
                                                           out, stall);
   ND_CUDA_TRY(cudaGetLastError());
   int h = 0;
-  ND_CUDA_TRY(cudaMemcpyAsync(&h, stall, sizeof(int), cudaMemcpyDeviceToHost, s));
+  ND_TRY(nd_d2h(&h, stall, sizeof(int), s));
   nd_free(stall, s);
   ND_CUDA_TRY(cudaStreamSynchronize(s));
   return h ? ND_ERR_STALL : ND_OK;
@@ -305,7 +331,7 @@ static int graph_finish(nd_graph* G, const double* dev_w, const double* dev_pre,
     ND_CUDA_TRY(cudaMemsetAsync(flag, 0, sizeof(int), s));
     k_not_unit<<<nd_grid(E, 256), 256, 0, s>>>(dev_w, E, flag);
     int h = 0;
-    ND_CUDA_TRY(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+    ND_TRY(nd_d2h(&h, flag, sizeof(int), s));
     ND_CUDA_TRY(cudaStreamSynchronize(s));
     nd_free(flag, s);
     unit = !h;
@@ -389,7 +415,7 @@ extern "C" int nd_graph_create(const int64_t* row_offsets, const int64_t* col_in
     }
     if (n_edges) k_col_narrow<<<nd_grid(n_edges, 256), 256, 0, s>>>(col64, n_edges, G->col, n_vertices, bad);
     int hbad = 0;
-    cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s);
+    nd_d2h(&hbad, bad, sizeof(int), s);
     auto up = [&](const double* src, int64_t n, double** dst) -> int {
       if (!src) return ND_OK;
       if (nd_alloc(dst, n, s)) return ND_ERR_NOMEM;
@@ -509,7 +535,7 @@ static int build_from_edges_dev(const int64_t* src, const int64_t* dst, const do
     cub::DeviceScan::InclusiveScan(tmp2, tb2, ends, ends, MaxOp(), V + 1, s);
     nd_free(tmp2, s);
     int hbad = 0;
-    cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s);
+    nd_d2h(&hbad, bad, sizeof(int), s);
     if (cudaStreamSynchronize(s)) { rc = ND_ERR_CUDA; break; }
     if (hbad) { rc = ND_ERR_ARG; break; }
     rc = graph_finish(G, w ? wtmp : nullptr, nullptr, nullptr, s);
@@ -888,7 +914,7 @@ extern "C" int nd_result_max_row(const nd_result* r, int64_t* host_width) {
   k_max_row<<<nd_grid(r->n, 256), 256, 0, r->stream>>>(
       static_cast<const int64_t*>(r->ptr[ND_F_FINAL_OFF]), r->n, mx);
   unsigned long long h = 0;
-  ND_CUDA_TRY(cudaMemcpyAsync(&h, mx, sizeof(h), cudaMemcpyDeviceToHost, r->stream));
+  ND_TRY(nd_d2h(&h, mx, sizeof(h), r->stream));
   ND_CUDA_TRY(cudaStreamSynchronize(r->stream));
   nd_free(mx, r->stream);
   *host_width = (int64_t)h;

@@ -86,7 +86,7 @@ int nd_dedup_segments(const int32_t* sid, const int32_t* val, int64_t m, int64_t
   t = tb;
   ND_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, t, f, pos, m + 1, s));
   int64_t* h = nd_pinned_scratch();
-  ND_CUDA_TRY(cudaMemcpyAsync(h, pos + m, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  ND_TRY(nd_d2h(h, pos + m, sizeof(int64_t), s));
   ND_CUDA_TRY(cudaStreamSynchronize(s));
   const int64_t u = h[0];
   ND_CUDA_TRY(nd_alloc(out_sid, u, s));

@@ -268,7 +268,7 @@ int nd_graph_ensure_lines(nd_graph* G, cudaStream_t s) {
     nd_free(tmp, s);
   }
   int64_t n_lines = 0;
-  ND_CUDA_TRY(cudaMemcpyAsync(&n_lines, first + V, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  ND_TRY(nd_d2h(&n_lines, first + V, sizeof(int64_t), s));
   ND_CUDA_TRY(cudaStreamSynchronize(s));
   // int32 line offsets; and the layout is an accelerator, not a requirement:
   // without room for it (plus a margin) the picks use the nbp records

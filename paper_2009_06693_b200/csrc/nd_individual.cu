@@ -667,11 +667,11 @@ static int run_individual_fixed(const nd_graph* G, const NdApp& a, const int64_t
     nd_free(tmp, s);
   }
   int64_t* h = nd_pinned_scratch();  // [0] total, [1] step values, [2] stall, [3..6] ctr, [8..] stats
-  ND_CUDA_TRY(cudaMemcpyAsync(h, final_off + n, 8, cudaMemcpyDeviceToHost, s));
-  ND_CUDA_TRY(cudaMemcpyAsync(h + 1, soff + S * n, 8, cudaMemcpyDeviceToHost, s));
-  ND_CUDA_TRY(cudaMemcpyAsync(h + 2, stall, sizeof(int), cudaMemcpyDeviceToHost, s));
-  ND_CUDA_TRY(cudaMemcpyAsync(h + 3, ctr, 4 * 8, cudaMemcpyDeviceToHost, s));
-  ND_CUDA_TRY(cudaMemcpyAsync(h + 8, stats, 4 * S * 8, cudaMemcpyDeviceToHost, s));
+  ND_TRY(nd_d2h(h, final_off + n, 8, s));
+  ND_TRY(nd_d2h(h + 1, soff + S * n, 8, s));
+  ND_TRY(nd_d2h(h + 2, stall, sizeof(int), s));
+  ND_TRY(nd_d2h(h + 3, ctr, 4 * 8, s));
+  ND_TRY(nd_d2h(h + 8, stats, 4 * S * 8, s));
   ND_CUDA_TRY(cudaStreamSynchronize(s));
   nd_trace("fx:totals(synced)");
   const int64_t total = h[0], total_items = h[1];
@@ -838,7 +838,7 @@ extern "C" int nd_run_individual(const nd_graph* G, int app_code, const double* 
       void* tmp;
       ND_CUDA_TRY(nd_alloc((char**)&tmp, tb, s));
       ND_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tb, kf, kp, P + 1, s));
-      ND_CUDA_TRY(cudaMemcpyAsync(h_tmp, kp + P, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+      ND_TRY(nd_d2h(h_tmp, kp + P, sizeof(int64_t), s));
       ND_CUDA_TRY(cudaStreamSynchronize(s));
       const int64_t K = h_tmp[0];
       if (K > tp_cap) {
@@ -935,7 +935,7 @@ extern "C" int nd_run_individual(const nd_graph* G, int app_code, const double* 
       nd_free(tmp, s);
       nd_free(tmp2, s);
     }
-    ND_CUDA_TRY(cudaMemcpyAsync(h_tmp, sc + items, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    ND_TRY(nd_d2h(h_tmp, sc + items, sizeof(int64_t), s));
     ND_CUDA_TRY(cudaStreamSynchronize(s));
     const int64_t Pn = h_tmp[0];
     nd_trace("ind:compacted(synced)");
@@ -972,7 +972,7 @@ extern "C" int nd_run_individual(const nd_graph* G, int app_code, const double* 
       ND_CUDA_TRY(cudaMemsetAsync(nfb, 0, sizeof(int), s));
       if (n) k_fallback<<<nd_grid(n, 256), 256, 0, s>>>(nnz, n, m, fb, nfb);
       int hn = 0;
-      ND_CUDA_TRY(cudaMemcpyAsync(&hn, nfb, sizeof(int), cudaMemcpyDeviceToHost, s));
+      ND_TRY(nd_d2h(&hn, nfb, sizeof(int), s));
       ND_CUDA_TRY(cudaStreamSynchronize(s));
       n_flagged = hn;
       nd_free(sd.npt, s);
@@ -1018,7 +1018,7 @@ extern "C" int nd_run_individual(const nd_graph* G, int app_code, const double* 
     ND_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tb, flen, final_off, n + 1, s));
     nd_free(tmp, s);
   }
-  ND_CUDA_TRY(cudaMemcpyAsync(h_tmp, final_off + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  ND_TRY(nd_d2h(h_tmp, final_off + n, sizeof(int64_t), s));
   ND_CUDA_TRY(cudaStreamSynchronize(s));
   const int64_t total = h_tmp[0];
   nd_trace("ind:final-scan(synced)");
@@ -1056,8 +1056,8 @@ extern "C" int nd_run_individual(const nd_graph* G, int app_code, const double* 
   ND_CUDA_TRY(cudaGetLastError());
   int h_stall = 0;
   unsigned long long h_ctr[4];
-  ND_CUDA_TRY(cudaMemcpyAsync(&h_stall, stall, sizeof(int), cudaMemcpyDeviceToHost, s));
-  ND_CUDA_TRY(cudaMemcpyAsync(h_ctr, ctr, sizeof(h_ctr), cudaMemcpyDeviceToHost, s));
+  ND_TRY(nd_d2h(&h_stall, stall, sizeof(int), s));
+  ND_TRY(nd_d2h(h_ctr, ctr, sizeof(h_ctr), s));
   ND_CUDA_TRY(cudaStreamSynchronize(s));
   nd_trace("ind:done(synced)");
   for (auto& sd : steps) {

@@ -72,6 +72,11 @@ struct NdApp {
 int nd_make_app(int code, const double* params, int64_t n_params, NdApp* a);
 int nd_pool_init();
 int64_t* nd_pinned_scratch();
+// Small device->host read, synchronous on `s`: a one-block kernel copies the
+// bytes into mapped pinned memory, then the stream is synchronised.  Unlike a
+// cudaMemcpyAsync it does not queue behind bulk device->host copies on the
+// copy engine (the host pipeline's row copies on another stream).
+int nd_d2h(void* dst, const void* src, int64_t bytes, cudaStream_t s);
 int nd_graph_ensure_index(nd_graph* G, int want_hset, int want_guide, cudaStream_t s);
 int nd_graph_ensure_records(nd_graph* G, int want_tries, cudaStream_t s);
 int nd_graph_ensure_lines(nd_graph* G, cudaStream_t s);

@@ -106,10 +106,10 @@ extern "C" int nd_transit_schedule(const int64_t* pair_transit, int64_t n_pairs,
   t = tb;
   ND_CUDA_TRY(cub::DeviceScan::InclusiveSum(tmp, t, flags, gid, n, s));
   int64_t G = 0;
-  ND_CUDA_TRY(cudaMemcpyAsync(&G, gid + n - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  ND_TRY(nd_d2h(&G, gid + n - 1, sizeof(int64_t), s));
   k_groups<<<nd_grid(n, 256), 256, 0, s>>>(flags, gid, keys, n, group_start, group_transit);
   int hbad = 0;
-  ND_CUDA_TRY(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+  ND_TRY(nd_d2h(&hbad, bad, sizeof(int), s));
   ND_CUDA_TRY(cudaStreamSynchronize(s));
   ND_CUDA_TRY(nd_alloc(&ind, 3 * G, s));
   ND_CUDA_TRY(nd_alloc(&ranks, 3 * G, s));

@@ -893,7 +893,7 @@ static int run_chain_walk(const nd_graph* G, const NdApp& a, int64_t sample_lo, 
       std::swap(wp_in, wp_alt);
     }
     prof.mark();
-    ND_CUDA_TRY(cudaMemcpyAsync(h_count, ncount, sizeof(int), cudaMemcpyDeviceToHost, s));
+    ND_TRY(nd_d2h(h_count, ncount, sizeof(int), s));
     ND_CUDA_TRY(cudaStreamSynchronize(s));
     if (prof.on) {
       sched_ms += prof.between(e0, e0 + 1);
@@ -936,7 +936,7 @@ static int run_chain_walk(const nd_graph* G, const NdApp& a, int64_t sample_lo, 
     nd_free(tmp, s);
   }
   int64_t total = 0;
-  ND_CUDA_TRY(cudaMemcpyAsync(&total, final_off + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  ND_TRY(nd_d2h(&total, final_off + n, sizeof(int64_t), s));
   ND_CUDA_TRY(cudaStreamSynchronize(s));
   ND_CUDA_TRY(nd_alloc(&final_ids, total, s));
   if (n) {
@@ -962,8 +962,8 @@ static int run_chain_walk(const nd_graph* G, const NdApp& a, int64_t sample_lo, 
   ND_CUDA_TRY(cudaGetLastError());
   int h_stall = 0;
   unsigned long long h_ctr[4];
-  ND_CUDA_TRY(cudaMemcpyAsync(&h_stall, stall, sizeof(int), cudaMemcpyDeviceToHost, s));
-  ND_CUDA_TRY(cudaMemcpyAsync(h_ctr, ctr, sizeof(h_ctr), cudaMemcpyDeviceToHost, s));
+  ND_TRY(nd_d2h(&h_stall, stall, sizeof(int), s));
+  ND_TRY(nd_d2h(h_ctr, ctr, sizeof(h_ctr), s));
   ND_CUDA_TRY(cudaStreamSynchronize(s));
   if (prof.on) res->counters[NDC_STEPS] = 0;
   double final_ms = prof.on ? prof.between(ef, ef + 1) : 0.0;
@@ -1070,9 +1070,7 @@ static int pw_run_windows(const nd_graph* G, const NdApp& a, uint64_t seed, int6
     if (g_profile) cudaEventRecord(pe0, s);
     kern<<<(unsigned)grid, (unsigned)tpb, 0, s>>>(A);
     if (g_profile) cudaEventRecord(pe1, s);
-    if (cudaGetLastError() != cudaSuccess ||
-        cudaMemcpyAsync(h, ctl, 4 * sizeof(int), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-        cudaStreamSynchronize(s) != cudaSuccess)
+    if (cudaGetLastError() != cudaSuccess || nd_d2h(h, ctl, 4 * sizeof(int), s) != ND_OK)
       rc = ND_ERR_CUDA;
     nd_trace("sp:window-synced");
     if (getenv("ND_TRACE") && getenv("ND_TRACE")[0] == '1')
@@ -1181,8 +1179,7 @@ static int run_tp_tail(const nd_graph* G, const NdApp& a, uint64_t seed, int64_t
       break;
     }
     int64_t* hk = nd_pinned_scratch() + 8;
-    if (cudaMemcpyAsync(hk, koff[k] + W.n, sizeof(int64_t), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-        cudaStreamSynchronize(s) != cudaSuccess) {
+    if (nd_d2h(hk, koff[k] + W.n, sizeof(int64_t), s) != ND_OK) {
       rc = ND_ERR_CUDA;
       break;
     }
@@ -1306,7 +1303,7 @@ static int run_chain_walk_sp(const nd_graph* G, const NdApp& a, int64_t sample_l
     nd_free(tmp, s);
   }
   int64_t total = 0;
-  ND_CUDA_TRY(cudaMemcpyAsync(&total, final_off + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  ND_TRY(nd_d2h(&total, final_off + n, sizeof(int64_t), s));
   ND_CUDA_TRY(cudaStreamSynchronize(s));
   nd_trace("sp:scan-synced");
   ND_CUDA_TRY(nd_alloc(&final_ids, total, s));
@@ -1329,7 +1326,7 @@ static int run_chain_walk_sp(const nd_graph* G, const NdApp& a, int64_t sample_l
   launches += 2 /*lengths, stats*/ + 2 /*scan*/ + (n * R ? 1 : 0);
   if (g_profile) cudaEventRecord(pe1, s);
   unsigned long long h_ctr[4];
-  ND_CUDA_TRY(cudaMemcpyAsync(h_ctr, ctr, sizeof(h_ctr), cudaMemcpyDeviceToHost, s));
+  ND_TRY(nd_d2h(h_ctr, ctr, sizeof(h_ctr), s));
   ND_CUDA_TRY(cudaGetLastError());
   ND_CUDA_TRY(cudaStreamSynchronize(s));
   pw_free_windows(wins, s);
@@ -1442,7 +1439,7 @@ static int run_rootpick_walk(const nd_graph* G, const NdApp& a, int64_t sample_l
     nd_free(tmp, s);
   }
   int64_t total = 0;
-  ND_CUDA_TRY(cudaMemcpyAsync(&total, final_off + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  ND_TRY(nd_d2h(&total, final_off + n, sizeof(int64_t), s));
   ND_CUDA_TRY(cudaStreamSynchronize(s));
   ND_CUDA_TRY(nd_alloc(&final_ids, total, s));
   if (n * R)
@@ -1454,7 +1451,7 @@ static int run_rootpick_walk(const nd_graph* G, const NdApp& a, int64_t sample_l
     if (n) ND_CUDA_TRY(cudaMemcpyAsync(clen, h.data(), n * sizeof(int64_t), cudaMemcpyHostToDevice, s));
     prof.mark();
     unsigned long long h_ctr[4];
-    ND_CUDA_TRY(cudaMemcpyAsync(h_ctr, ctr, sizeof(h_ctr), cudaMemcpyDeviceToHost, s));
+    ND_TRY(nd_d2h(h_ctr, ctr, sizeof(h_ctr), s));
     ND_CUDA_TRY(cudaStreamSynchronize(s));
     res->counters[NDC_N2V_TRIES] = (int64_t)h_ctr[1];
     res->counters[NDC_SLOT_BYTES] = (int64_t)h_ctr[0];

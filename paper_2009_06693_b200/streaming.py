@@ -57,6 +57,8 @@ class HostPipeline:
         self._pinned = {}
         self._copy_streams = []
         self.last_h2d_bytes = 0  # host->device bytes of the last run (roots)
+        self._pending = []       # (copy-done event, device runs) of runs not waited for
+        self._phase = 0          # pinned buffer set of the next run (two alternate)
 
     def _buf(self, key, like):
         import torch
@@ -74,13 +76,23 @@ class HostPipeline:
         HostChunk per chunk, valid until the next run of this pipeline."""
         return self.run_jobs(graph, [(app, n_samples, seed, sample_lo, roots_host)])[0]
 
-    def run_jobs(self, graph, jobs) -> list:
+    def run_jobs(self, graph, jobs, wait: bool = True) -> list:
         """Several apps at once through one pipeline: job = (app, n_samples,
         seed, sample_lo, roots_host[, chunks]).  Each job runs on its own compute stream
         and host thread (engine.run_device_concurrent's scheme) with its own
         copy stream, so one job's copies and tail overlap the others' bulk;
-        one synchronisation at the end.  Returns one HostChunk list per job."""
+        one synchronisation at the end.  Returns one HostChunk list per job.
+
+        wait=False returns as soon as every chunk has sampled and its copy is
+        queued, so the caller's next run samples while this run's last rows
+        are still crossing PCIe; its rows are valid after `wait()`.  Runs
+        alternate between two pinned buffer sets, so a run's rows stay valid
+        while the next run is in flight."""
         import torch
+        self._release(block=False)
+        phase = self._phase
+        if not wait:
+            self._phase ^= 1
         from .engine import _job_pool, job_streams
         L = _lib.load()
         dg = as_device_graph(graph)
@@ -146,8 +158,8 @@ class HostPipeline:
                     ready = torch.cuda.Event()
                     ready.record(st)
                     cs.wait_event(ready)
-                    h_off = self._buf((ji, ci, "off"), off)
-                    h_ids = self._buf((ji, ci, "ids"), ids)
+                    h_off = self._buf((phase, ji, ci, "off"), off)
+                    h_ids = self._buf((phase, ji, ci, "ids"), ids)
                     if trace is not None:
                         e_d0 = torch.cuda.Event(enable_timing=True)
                         e_d0.record(cs)
@@ -181,6 +193,11 @@ class HostPipeline:
         futs = [_job_pool(k).submit(one, ji, job, st, cs0)
                 for ji, (job, st) in enumerate(zip(jobs, streams))]
         done = [f.result() for f in futs]
+        if not wait:  # the runs' buffers live until their copies are done
+            ev = torch.cuda.Event()
+            ev.record(cs0)
+            self._pending.append((ev, [h for _, held in done for h in held]))
+            return [out for out, _ in done]
         cur.wait_stream(cs0)
         cur.synchronize()
         if trace is not None:  # chunk timeline (ms from the call): compute start/end, copy end
@@ -193,7 +210,26 @@ class HostPipeline:
             for h in held:
                 if isinstance(h, DeviceRun):
                     h.close()
+        self._release(block=True)
         return [out for out, _ in done]
+
+    def wait(self) -> None:
+        """Wait for every run issued with wait=False (its rows are then in
+        host memory) and release its device buffers."""
+        self._release(block=True)
+
+    def _release(self, block: bool) -> None:
+        keep = []
+        for ev, held in self._pending:
+            if block:
+                ev.synchronize()
+            elif not ev.query():
+                keep.append((ev, held))
+                continue
+            for h in held:
+                if isinstance(h, DeviceRun):
+                    h.close()
+        self._pending = keep
 
 
 def chunk_plan(n: int, chunks: int, lead: bool = False) -> list:

@@ -430,6 +430,15 @@ def test_concurrent_jobs_and_host_pipeline_match_plain_runs():
         finally:
             os.environ.pop("ND_PIPE_ROOTS", None)
         assert pipe.last_h2d_bytes == n * 8 * (len(apps) if mode else 1)
+        if mode is None and spec == 3:  # back-to-back runs: both results valid after wait()
+            pipe2 = HostPipeline(chunks=3)
+            r1 = pipe2.run_jobs(dg, [(a, n, seed, 17, roots, 3) for a in apps], wait=False)
+            r2 = pipe2.run_jobs(dg, [(a, n, seed, 17, roots, 2) for a in apps], wait=False)
+            pipe2.wait()
+            for rr in (r1, r2):
+                for parts, (off, ids) in zip(rr, ref2):
+                    got = np.concatenate([c.ids.numpy().astype(np.int64) for c in parts])
+                    assert np.array_equal(got, ids)
         for parts, (off, ids) in zip(res, ref2):
             got_ids = np.concatenate([c.ids.numpy().astype(np.int64) for c in parts])
             got_len = np.concatenate([np.diff(c.offsets.numpy()) for c in parts])

@@ -36,3 +36,17 @@ for cfg in sys.argv[1:] or ["6,3"]:
         if it >= 2:
             ms.append(s.elapsed_time(e))
     print(cfg, os.environ.get("ND_PIPE_NOCOPY", "0"), round(statistics.median(ms), 2), flush=True)
+    # pipelined: K runs back to back (wait=False), one wait at the end
+    for K in (5,):
+        for _ in range(2):  # both pinned buffer sets allocated
+            pipe.run_jobs(dg, jobs, wait=False)
+        pipe.wait()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        s.record()
+        for _ in range(K):
+            pipe.run_jobs(dg, jobs, wait=False)
+        pipe.wait()
+        e.record()
+        torch.cuda.synchronize()
+        print(cfg, "pipelined", K, round(s.elapsed_time(e) / K, 2), flush=True)
