@@ -245,7 +245,7 @@ def main():
                     help="run node2vec then PPR instead of concurrently on two streams")
     ap.add_argument("--e2e-chunks", type=int, default=6,
                     help="node2vec sample-id chunks of the host pipeline (D2H of chunk c overlaps chunk c+1)")
-    ap.add_argument("--e2e-ppr-chunks", type=int, default=3)
+    ap.add_argument("--e2e-ppr-chunks", type=int, default=2)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
