@@ -49,6 +49,12 @@ int dcopy_to_host(T* h, const T* d, int64_t n, cudaStream_t s) {
   return ND_OK;
 }
 
+__global__ void k_widen_flags(const uint8_t* __restrict__ f, int64_t n, int64_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = f[i];
+}
+
 // degrees of the flattened transits (+1 trailing 0 for the exclusive scan)
 __global__ void k_tdeg(const int32_t* __restrict__ tv, int64_t T, const int64_t* __restrict__ row,
                        int64_t* __restrict__ d) {
@@ -727,17 +733,9 @@ extern "C" int nd_run_collective(const nd_graph* G, int kind, int64_t step_size,
       if (tot_tri)
         k_imp_hits<<<nd_grid(n * m * 32, 256, 148 * 64), 256, 0, s>>>(g, toff, tv, out, alive,
                                                                       tri_off, n, m, tot_tri, fl);
-      // widen flags for the scan
-      {
-        auto widen = [] __device__(uint8_t x) { return (int64_t)x; };
-        cub::TransformInputIterator<int64_t, decltype(widen), const uint8_t*> it(fl, widen);
-        size_t tb = 0;
-        cub::DeviceScan::ExclusiveSum(nullptr, tb, it, pos, tot_tri + 1, s);
-        void* tmp;
-        ND_CUDA_TRY(nd_alloc((char**)&tmp, tb, s));
-        ND_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tb, it, pos, tot_tri + 1, s));
-        nd_free(tmp, s);
-      }
+      // hit flags widened into pos, then scanned in place
+      k_widen_flags<<<nd_grid(tot_tri + 1, 256), 256, 0, s>>>(fl, tot_tri + 1, pos);
+      ND_TRY(scan_excl(pos, pos, tot_tri + 1, s));
       ND_TRY(dcopy_to_host(&cs.nrec, pos + tot_tri, 1, s));
       ND_CUDA_TRY(nd_alloc(&cs.rec_t, cs.nrec, s));
       ND_CUDA_TRY(nd_alloc(&cs.rec_v, cs.nrec, s));
