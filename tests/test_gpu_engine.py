@@ -264,19 +264,13 @@ def test_collective_on_rmat_vs_oracle(app, params):
     dr.close()
 
 
-@pytest.mark.parametrize("app", ["deepwalk", "ppr", "node2vec"])
-def test_index_paths_on_adversarial_hub_graph(app):
-    """Guide-table picks and hash-set membership on rows far above the index
-    thresholds, with zero weights (flat prefix runs), weights spanning six
-    decades, parallel edges and a dense hub neighbourhood: device == oracle."""
-    from paper_2009_06693_b200 import make_app
-    from paper_2009_06693_b200.engine import run_device
-    from paper_2009_06693_b200.graph import DeviceGraph
+def _hub_graph(V=3000, hub_deg=5000):
+    """Vertex 0 a hub of hub_deg out-edges; every other vertex a few edges
+    back to the hub and to random vertices; weights spanning six decades with
+    10% zeros; parallel edges kept."""
     rng = np.random.default_rng(21)
-    V, hub_deg = 3000, 5000
     src = [np.zeros(hub_deg, dtype=np.int64)]
     dst = [rng.integers(1, V, hub_deg)]
-    # every other vertex: a few edges back to the hub and to random vertices
     for v in range(1, V):
         k = int(rng.integers(1, 60))
         src.append(np.full(k, v))
@@ -286,7 +280,46 @@ def test_index_paths_on_adversarial_hub_graph(app):
     src, dst = np.concatenate(src), np.concatenate(dst)
     w = 10.0 ** rng.uniform(-3, 3, len(src))
     w[rng.random(len(src)) < 0.1] = 0.0
-    og = O.from_edges(src, dst, w, V)
+    return O.from_edges(src, dst, w, V)
+
+
+@pytest.mark.parametrize("app,params", [("clustergcn", {"clusters_per_sample": 3, "num_clusters": 7}),
+                                        ("mvs", {}), ("fastgcn", {}), ("layer", {})])
+def test_collective_on_hub_graph_vs_oracle(app, params):
+    """Collective apps where one transit's row (5,000 edges) spans several
+    of ClusterGCN's 1,024-edge scan units and many transits have short rows:
+    slots, recorded edges (order included) and final rows == oracle, both
+    paradigms."""
+    from paper_2009_06693_b200 import make_app
+    from paper_2009_06693_b200.engine import run_device
+    from paper_2009_06693_b200.graph import DeviceGraph
+    og = _hub_graph()
+    dg = DeviceGraph.from_arrays(og.row_offsets, og.col_indices, og.weights)
+    n = 5 if app == "clustergcn" else 64
+    meta = {"app": app, "params": params, "n_samples": n, "seed": 4}
+    ref = oracle_run(meta, og)
+    for par in ("sp", "tp"):
+        dr = run_device(make_app(app, **params), dg, n_samples=n, seed=4, paradigm=par)
+        out = dr.to_output()
+        assert np.array_equal(out.step_vals, ref.step_vals), par
+        if app != "layer":
+            assert np.array_equal(np.asarray(out.rec_counts), np.asarray(ref.rec_counts)), par
+            assert np.array_equal(out.rec_t, ref.rec_t) and np.array_equal(out.rec_v, ref.rec_v), par
+        off, ids = out.final_csr()
+        roff, rids = ref.final_csr()
+        assert np.array_equal(off, roff) and np.array_equal(ids, rids), par
+        dr.close()
+
+
+@pytest.mark.parametrize("app", ["deepwalk", "ppr", "node2vec"])
+def test_index_paths_on_adversarial_hub_graph(app):
+    """Guide-table picks and hash-set membership on rows far above the index
+    thresholds, with zero weights (flat prefix runs), weights spanning six
+    decades, parallel edges and a dense hub neighbourhood: device == oracle."""
+    from paper_2009_06693_b200 import make_app
+    from paper_2009_06693_b200.engine import run_device
+    from paper_2009_06693_b200.graph import DeviceGraph
+    og = _hub_graph()
     dg = DeviceGraph.from_arrays(og.row_offsets, og.col_indices, og.weights)
     n = 4000
     meta = {"app": app, "params": {}, "n_samples": n, "seed": 33}
@@ -295,7 +328,7 @@ def test_index_paths_on_adversarial_hub_graph(app):
         dr = run_device(make_app(app), dg, n_samples=n, seed=33, paradigm=par)
         off, ids = dr.host(0), dr.host(1)
         roff, rids = ref.final_csr()
-        assert np.array_equal(off, roff) and np.array_equal(ids, rids), (par, tail)
+        assert np.array_equal(off, roff) and np.array_equal(ids, rids), par
         dr.close()
 
 
