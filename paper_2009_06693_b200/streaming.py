@@ -58,12 +58,15 @@ class HostPipeline:
         self._copy_streams = []
         self.last_h2d_bytes = 0  # host->device bytes of the last run (roots)
         self._pending = []       # (copy-done event, device runs) of runs not waited for
+        self._retired = []       # replaced pinned buffers, kept until the next wait
         self._phase = 0          # pinned buffer set of the next run (two alternate)
 
     def _buf(self, key, like):
         import torch
         b = self._pinned.get(key)
         if b is None or b.numel() < like.numel() or b.dtype != like.dtype:
+            if b is not None:  # a copy of an earlier run may still target it
+                self._retired.append(b)
             b = torch.empty(max(like.numel(), 1), dtype=like.dtype, pin_memory=True)
             self._pinned[key] = b
         return b[:like.numel()]
@@ -230,6 +233,8 @@ class HostPipeline:
                 if isinstance(h, DeviceRun):
                     h.close()
         self._pending = keep
+        if not keep:
+            self._retired = []
 
 
 def chunk_plan(n: int, chunks: int, lead: bool = False) -> list:
