@@ -47,6 +47,7 @@ SEED = 7
 APPS = (("node2vec", {"p": 2.0, "q": 0.5}), ("ppr", {"termination_probability": 0.01}))
 METRIC = "sampled edges/sec (and % of HBM roofline) at 1/2/4/8 B200 vs CPU ref"
 CPU_SAMPLE = 1 << SCALE  # the full walker set: the C port runs it in ~10 s
+DEV_SCALE = None  # --scale other than C2's (quick checks only)
 
 
 def peaks():
@@ -188,7 +189,7 @@ def run_reference(args):
     cores = len(os.sched_getaffinity(0))
     from paper_2009_06693_b200.graph import DeviceGraph
     torch.cuda.set_device(0)
-    dg = DeviceGraph.rmat(SCALE, n_edges=N_EDGES, seed=GRAPH_SEED, weighted=True)
+    dg = DeviceGraph.rmat(DEV_SCALE or SCALE, n_edges=N_EDGES, seed=GRAPH_SEED, weighted=True)
     hg = host_graph_for_oracle(dg)
     dg.close()
     times, edges_tot = [], 0
@@ -218,7 +219,7 @@ def config_dict(n_gpus, note=None, concurrent=True, scaling="weak"):
                      "node2vec p=2 q=0.5 len 100 + PPR term 0.01, one walk per vertex"
                      + (" per GPU" if weak and n_gpus > 1 else ""),
          "graph": "keyed RMAT a=.57 b=.19 c=.19, weights U[1,5), seed 0, built on device",
-         "walkers_per_step": 2 * (1 << SCALE) * (n_gpus if weak else 1), "seed": SEED,
+         "walkers_per_step": 2 * (1 << (DEV_SCALE or SCALE)) * (n_gpus if weak else 1), "seed": SEED,
          "parallelism": (f"sample-sharded x{n_gpus}, graph replicated, "
                          + ("V walkers per app per GPU (ids rank*V..), no collective"
                             if weak else "V walkers split by worker_ranges, NCCL gather in the step")),
@@ -226,6 +227,8 @@ def config_dict(n_gpus, note=None, concurrent=True, scaling="weak"):
          "apps": "node2vec and PPR concurrently on two streams" if concurrent else "node2vec then PPR"}
     if note:
         c["note"] = note
+    if DEV_SCALE is not None:
+        c["dev_scale"] = f"RMAT scale {DEV_SCALE}, {N_EDGES} edges: NOT the C2 workload"
     return c
 
 
@@ -246,7 +249,14 @@ def main():
     ap.add_argument("--e2e-chunks", type=int, default=6,
                     help="node2vec sample-id chunks of the host pipeline (D2H of chunk c overlaps chunk c+1)")
     ap.add_argument("--e2e-ppr-chunks", type=int, default=2)
+    ap.add_argument("--scale", type=int, default=SCALE,
+                    help="RMAT scale (22 = C2; smaller only for quick multi-rank checks)")
     args = ap.parse_args()
+    if args.scale != SCALE:  # development scale: same mean degree, flagged in config
+        global N_EDGES, CPU_SAMPLE, DEV_SCALE
+        DEV_SCALE = args.scale
+        N_EDGES = int(N_EDGES / (1 << SCALE) * (1 << args.scale))
+        CPU_SAMPLE = 1 << args.scale
     if args.impl == "reference":
         return run_reference(args)
 
@@ -267,7 +277,7 @@ def main():
     from paper_2009_06693_b200.sharding import worker_ranges
 
     L = _lib.load()
-    dg = DeviceGraph.rmat(SCALE, n_edges=N_EDGES, seed=GRAPH_SEED, weighted=True)
+    dg = DeviceGraph.rmat(DEV_SCALE or SCALE, n_edges=N_EDGES, seed=GRAPH_SEED, weighted=True)
     V = dg.n_vertices
     if args.scaling == "weak":  # per-GPU work fixed: this rank's own V walkers per app
         lo, n = rank * V, V

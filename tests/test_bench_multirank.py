@@ -1,0 +1,39 @@
+"""bench.py's multi-rank path (the driver's scaling run) end to end: two ranks
+under torchrun on one GPU with CPU (gloo) collectives at a small RMAT scale.
+Checks the one-line contract: rank 0 alone prints, whole-job values, weak
+scaling, e2e rows verified, and the reference arm runs on rank 0 only."""
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _torchrun(args, n=2, port=29611):
+    env = dict(os.environ, ND_DIST_BACKEND="gloo", MASTER_ADDR="127.0.0.1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), "bench.py"] + args
+    p = subprocess.run(cmd, cwd=REPO, env=env, capture_output=True, text=True, timeout=900)
+    assert p.returncode == 0, p.stderr[-3000:]
+    lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
+    return lines
+
+
+@pytest.mark.gpu
+def test_bench_two_ranks_one_line():
+    common = ["--gpus", "2", "--scale", "14", "--steps", "2", "--warmup", "3", "--no-cpu", "--no-tp"]
+    lines = _torchrun(common)
+    assert len(lines) == 1  # rank 0 only
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "weak" and d["value"] > 0
+    assert d["e2e"]["host_rows_match_device"] is True and d["e2e"]["value"] > 0
+    assert "dev_scale" in d["config"] and d["gpu_launches"] > 0
+    assert d["config"]["walkers_per_step"] == 2 * 2 * (1 << 14)
+    ref = _torchrun(["--impl", "reference"] + common, port=29612)
+    assert len(ref) == 1
+    r = json.loads(ref[0])
+    assert r["impl"] == "reference" and r["value"] > 0 and r["e2e"]["h2d_bytes_per_step"] == 0
