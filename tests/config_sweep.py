@@ -3,7 +3,7 @@ device throughput (SP and TP where both exist), the CPU oracle on a bounded
 sample of the same job, and parity of that sample.  Writes one JSON object
 per config to stdout (collected into profiles/r01_configs.json).
 
-    python tools/bench_configs.py [C1 C3 C4 C5]
+    python -m tests.config_sweep [C1 C3 C4 C5]   (lives under tests/: it runs the C oracle as the CPU baseline and parity checker)
 """
 
 import json
