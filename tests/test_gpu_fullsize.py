@@ -63,3 +63,25 @@ def test_c2_full_size_properties():
             assert bool((deg[last] == 0).all().item()), name
         sp.close()
         tp.close()
+
+
+def test_c3_c4_full_size_sp_equals_tp():
+    """C3 k-hop (25,10) over 233,472 roots of the 114.6M-edge graph and C4
+    ClusterGCN over the 117.2M-edge graph: both paradigms, identical rows and
+    recorded edges."""
+    import torch
+    from paper_2009_06693_b200 import _lib, make_app
+    from paper_2009_06693_b200.engine import run_device
+    from paper_2009_06693_b200.graph import DeviceGraph
+    cases = [((18, 57_300_000), "khop", 233_472, (_lib.F_FINAL_OFF, _lib.F_FINAL_IDS32)),
+             ((22, 58_600_000), "clustergcn", 8, (_lib.F_FINAL_OFF, _lib.F_REC_T, _lib.F_REC_V))]
+    for (scale, edges), name, n, fields in cases:
+        g = DeviceGraph.rmat(scale, n_edges=edges, seed=0, undirected=True, weighted=False)
+        sp = run_device(make_app(name), g, n_samples=n, seed=7, paradigm="sp")
+        tp = run_device(make_app(name), g, n_samples=n, seed=7, paradigm="tp")
+        for f in fields:
+            assert torch.equal(sp.view(f), tp.view(f)), (name, f)
+        assert sp.total_sampled == tp.total_sampled
+        sp.close()
+        tp.close()
+        g.close()
