@@ -121,17 +121,6 @@ struct __align__(32) VRec {   // per vertex
   double mx;                  // per-row max weight (node2vec envelope)
   double total;               // prefix[hi-1] (weighted pick); deg for unit rows
 };
-struct __align__(16) EdgeCW {  // node2vec try: neighbour + its weight
-  int32_t col;
-  int32_t pad;
-  double w;
-};
-struct __align__(16) EdgePC {  // weighted pick: prefix + the neighbour it selects
-  double pre;
-  int32_t col;
-  int32_t pad;
-};
-
 // Neighbour records for the walker-major kernel: each edge record also
 // carries its destination's row header, so the record that selects the next
 // vertex delivers that vertex's header in the same sector (no separate
@@ -186,8 +175,6 @@ struct DevGraph {
   const int32_t* hset = nullptr;  // optional, 4E slots
   const int32_t* guide = nullptr; // optional, E entries
   const VRec* vrec = nullptr;     // optional packed vertex records
-  const EdgeCW* ecw = nullptr;    // optional packed (col, w) records
-  const EdgePC* epc = nullptr;    // optional packed (prefix, col) records
   const NbrW* nbw = nullptr;      // optional neighbour records (node2vec tries)
   const NbrP* nbp = nullptr;      // optional neighbour records (weighted picks)
   const NbrU* nbu = nullptr;      // optional neighbour records (unit graphs)

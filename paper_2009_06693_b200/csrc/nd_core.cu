@@ -371,8 +371,6 @@ extern "C" int nd_graph_destroy(nd_graph* G) {
   cudaFree(G->hset);
   cudaFree(G->guide);
   cudaFree(G->vrec);
-  cudaFree(G->ecw);
-  cudaFree(G->epc);
   cudaFree(G->nbw);
   cudaFree(G->nbp);
   cudaFree(G->nbu);

@@ -19,8 +19,6 @@ struct nd_graph {
   int32_t* hset = nullptr;   // optional exact indexes (nd_index.cu)
   int32_t* guide = nullptr;
   nd::VRec* vrec = nullptr;  // packed records (nd_index.cu)
-  nd::EdgeCW* ecw = nullptr;
-  nd::EdgePC* epc = nullptr;
   nd::NbrW* nbw = nullptr;
   nd::NbrP* nbp = nullptr;
   nd::NbrU* nbu = nullptr;

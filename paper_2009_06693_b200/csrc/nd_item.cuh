@@ -50,29 +50,6 @@ struct GRow {
   }
 };
 
-// v's row through the packed edge records (one 16-byte load per try / probe)
-struct PRow {
-  const EdgeCW* ecw;
-  const EdgePC* epc;
-  const int32_t* col;  // plain column ids (unit graphs)
-  const int32_t* gd;
-  __device__ __forceinline__ int64_t c(int64_t k) const {
-    return epc ? (int64_t)__ldg(&epc[k].col) : (int64_t)__ldg(col + k);
-  }
-  __device__ __forceinline__ double p(int64_t k) const { return __ldg(&epc[k].pre); }
-  __device__ __forceinline__ double wt(int64_t k) const { return __ldg(&ecw[k].w); }
-  __device__ __forceinline__ void cw(int64_t k, int64_t& c_, double& w_, int unit) const {
-    if (unit || !ecw) {
-      c_ = (int64_t)__ldg(col + k);
-      w_ = 1.0;
-      return;
-    }
-    const double2 r = __ldg(reinterpret_cast<const double2*>(ecw + k));
-    c_ = (int64_t)(int32_t)(uint32_t)(__double_as_longlong(r.x) & 0xFFFFFFFFull);
-    w_ = r.y;
-  }
-};
-
 template <typename ColT>
 __device__ __forceinline__ GRow<ColT> grow(const GView<ColT>& g, int64_t lo) {
   return GRow<ColT>{g.col + lo, g.unit ? nullptr : g.pre + lo, g.unit ? nullptr : g.w + lo,

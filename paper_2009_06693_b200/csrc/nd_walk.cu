@@ -259,8 +259,6 @@ struct PWArgs {
   int* stall;
   unsigned long long* ctr;
   const VRec* vrec;   // packed vertex records (or null)
-  const EdgeCW* ecw;
-  const EdgePC* epc;
   const NbrW* nbw;    // neighbour records (or null)
   const NbrP* nbp;
   const NbrU* nbu;
@@ -547,14 +545,8 @@ __global__ void __launch_bounds__(256, MINB) k_walk_persistent(PWArgs A) {
     } else if (n2v && t >= 0 && deg > 0) {
       if (j == 0) st.bytes += 2 * SECTOR;  // t offsets + max_w (§8 d pair term)
       const double env = __dmul_rn(mx >= 0.0 ? mx : __ldg(A.gv.mx + v), A.a.f_max);
-      if (A.vrec != nullptr) {
-        const PRow pr{A.ecw ? A.ecw + lo : nullptr, A.epc ? A.epc + lo : nullptr, A.gv.col + lo,
-                      A.gv.guide ? A.gv.guide + lo : nullptr};
-        o = n2v_try(A, pr, deg, t, tlo, thi, env, base0 + 2 * C_DRAW * (uint64_t)j, ik, st);
-      } else {
-        o = n2v_try(A, grow(A.gv, lo), deg, t, tlo, thi, env, base0 + 2 * C_DRAW * (uint64_t)j, ik,
-                    st);
-      }
+      o = n2v_try(A, grow(A.gv, lo), deg, t, tlo, thi, env, base0 + 2 * C_DRAW * (uint64_t)j, ik,
+                  st);
       if (o == -2) {
         if (++j >= N2V_MAX_TRIES) {
           atomicExch(A.stall, 1);
@@ -563,12 +555,8 @@ __global__ void __launch_bounds__(256, MINB) k_walk_persistent(PWArgs A) {
           continue;  // rejected: the lane tries again next iteration
         }
       }
-    } else if (A.vrec != nullptr) {
-      const PRow pr{A.ecw ? A.ecw + lo : nullptr, A.epc ? A.epc + lo : nullptr, A.gv.col + lo,
-                    A.gv.guide ? A.gv.guide + lo : nullptr};
-      o = run_item(A.gv, pr, A.a, v, deg, t, base0, ik, st, &stl, tlo, thi, mx, tot);
-    } else {
-      o = run_item(A.gv, grow(A.gv, lo), A.a, v, deg, t, base0, ik, st, &stl, tlo, thi);
+    } else {  // plain CSR rows (records not built: ND_NO_PACK)
+      o = run_item(A.gv, grow(A.gv, lo), A.a, v, deg, t, base0, ik, st, &stl, tlo, thi, mx, tot);
     }
     if (stl) atomicExch(A.stall, 1);
     orow[s - A.step0] = (int32_t)o;
@@ -1056,7 +1044,7 @@ static int pw_run_windows(const nd_graph* G, const NdApp& a, uint64_t seed, int6
     }
     PWArgs A{view(g), a, seed, sample_lo, rows, cwid, cv, ct, roots, roots32, R, step0,
              step0 + Lw, ld, W.out, W.nnz, died, nw, nv, nt, ctl + 1, ctl, ctl + 2, ctl + 3, ctr,
-             g.vrec, g.ecw, g.epc, g.nbw, g.nbp, g.nbu,
+             g.vrec, g.nbw, g.nbp, g.nbu,
              (a.code == ND_DEEPWALK || a.code == ND_PPR) ? g.pl : nullptr, g.vline};
     // small windows (few walkers per lane, e.g. L2-resident graphs or the
     // PPR tail): 128-thread CTAs spread over every SM, one walker per lane
