@@ -770,10 +770,12 @@ static int run_tp_tail(const nd_graph* G, const NdApp& a, uint64_t seed, int64_t
                        cudaStream_t s, std::vector<PWindow>& wins, int64_t& n_steps,
                        int64_t& items, double& sample_ms);
 
-// byte-model counters (see nd_item.cuh): ctr[0]=bytes, ctr[1]=tries
+// TP chain walk (SP chain walks run in run_chain_walk_sp).  Byte-model
+// counters (see nd_item.cuh): ctr[0]=bytes, ctr[1]=tries
 static int run_chain_walk(const nd_graph* G, const NdApp& a, int64_t sample_lo, int64_t n,
                           const int64_t* roots, int64_t R, uint64_t seed, int64_t steps,
                           int64_t step_cap, int paradigm, cudaStream_t s, nd_result* res) {
+  if (paradigm != ND_TP) return ND_ERR_ARG;
   const DevGraph& g = G->g;
   const int key_bits = key_bits_for(g.V);
   uint32_t *cur0 = nullptr, *cur1 = nullptr;
@@ -798,7 +800,7 @@ static int run_chain_walk(const nd_graph* G, const NdApp& a, int64_t sample_lo, 
   ND_CUDA_TRY(cudaMemsetAsync(ctr, 0, 4 * sizeof(unsigned long long), s));
   ND_CUDA_TRY(cudaMemsetAsync(stats, 0, 4 * (max_steps + 1) * sizeof(unsigned long long), s));
   ND_CUDA_TRY(cudaMemsetAsync(stall, 0, sizeof(int), s));
-  if (paradigm == ND_TP) ND_TRY(S.alloc(n, key_bits, s));
+  ND_TRY(S.alloc(n, key_bits, s));
   if (!roots) {
     ND_CUDA_TRY(nd_alloc(&roots32, n * R, s));
     ND_TRY(nd_uniform_roots_i32(g, R, seed, sample_lo, n, roots32, s));
@@ -855,7 +857,7 @@ static int run_chain_walk(const nd_graph* G, const NdApp& a, int64_t sample_lo, 
                                      (a.code == ND_NODE2VEC && step == 0));
     const int need_w = !g.unit && a.code == ND_NODE2VEC && step > 0;
     unsigned long long* st_step = stats + 4 * step;
-    if (paradigm == ND_TP) {
+    {
       cub::DoubleBuffer<uint32_t> dk(cur_in, cur_alt);
       cub::DoubleBuffer<uint64_t> dv(wp_in, wp_alt);
       ND_TRY(tp_sort(dk, dv, A, key_bits, S, s));
@@ -870,15 +872,6 @@ static int run_chain_walk(const nd_graph* G, const NdApp& a, int64_t sample_lo, 
       wp_in = dv.Alternate();
       cur_alt = dk.Current();
       wp_alt = dv.Current();
-    } else {
-      prof.mark();
-      ChainAct act{view(g), a, key_base(seed, (uint64_t)step, 0, 0), sample_lo, (int)step,
-                   rec_w + rec_base, rec_v + rec_base, cur_alt, wp_alt, ncount, dstep, stall,
-                   rows, max_steps};
-      ND_TRY(sp_step(cur_in, wp_in, A, g, act, ctr, st_step, s));
-      k_stats_fetch<<<1, 1, 0, s>>>(st_step, (unsigned long long)A);
-      std::swap(cur_in, cur_alt);
-      std::swap(wp_in, wp_alt);
     }
     prof.mark();
     ND_TRY(nd_d2h(h_count, ncount, sizeof(int), s));
