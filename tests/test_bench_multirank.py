@@ -37,3 +37,17 @@ def test_bench_two_ranks_one_line():
     assert len(ref) == 1
     r = json.loads(ref[0])
     assert r["impl"] == "reference" and r["value"] > 0 and r["e2e"]["h2d_bytes_per_step"] == 0
+
+
+@pytest.mark.gpu
+def test_run_sharded_two_ranks_equals_one_run(tmp_path):
+    """multigpu.run_sharded: each rank samples its worker_ranges share, rows
+    gathered to rank 0 in rank order == one single-process run (driver.py:175-186)."""
+    res = tmp_path / "sharded.json"
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29613", "tests/_sharded_worker.py", str(res)]
+    p = subprocess.run(cmd, cwd=REPO, env=env, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-3000:]
+    verdict = json.loads(res.read_text())
+    assert verdict == {"node2vec": True, "ppr": True, "khop": True}
