@@ -16,7 +16,7 @@ from .apps import make_app
 from .core import DEFAULT_STEP_CAP
 from .engine import EngineConfig, RunStats, make_samples, sp_run, tp_run
 from .errors import OutputMismatchError
-from .graph import Graph, load_edge_list
+from .graph import Graph  # noqa: F401  (type of synthetic graphs)
 from .output import LAYOUT_FINAL, SampleSetOutput, render_text
 from .sharding import worker_ranges
 from .synth import make_synthetic
@@ -40,12 +40,15 @@ class RunConfig:
     step_cap: int = DEFAULT_STEP_CAP
     use_kernels: bool = True
 
-    def load_graph(self) -> Graph:
+    def load_graph(self):
         """bench.py:45-50: file graphs keyed on the run seed; synthetic graphs
-        built with the run seed."""
+        built with the run seed.  Edge-list files are parsed and built on the
+        device (DeviceGraph.from_edge_list: same graph, ids, remap and errors as
+        the reference's load_edge_list)."""
         if self.graph_path:
-            return load_edge_list(self.graph_path, weighted=self.weighted,
-                                  undirected=self.undirected, seed=self.seed)
+            from .graph import DeviceGraph
+            return DeviceGraph.from_edge_list(self.graph_path, weighted=self.weighted,
+                                              undirected=self.undirected, seed=self.seed)
         return make_synthetic(self.synth or "powerlaw:1000", weighted=self.weighted, seed=self.seed)
 
 
