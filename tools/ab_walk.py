@@ -1,5 +1,5 @@
 """Dev tool: event-timed node2vec / PPR walks on the C2 graph under the
-current environment (ND_WALK_KERNEL, ND_FAST_MINB, ...); prints one JSON line
+current environment (ND_WALK_MINB, ND_NO_LINES, ND_NO_PACK, ...); prints one JSON line
 per app with the median of 5 runs and the run's byte-model counters."""
 import json
 import os
