@@ -64,3 +64,29 @@ def test_ppr_lengths_geometric():
     assert _chi2_p(counts, probs) > 1e-3, counts
     assert abs(L.mean() - (1 - term) / term) < 0.05
     dr.close()
+
+
+def test_node2vec_second_order_transitions():
+    """From v = 1 having come from t = 0: neighbours 0 (return, 1/p), 2
+    (adjacent to t, 1) and 3 (far, 1/q) with weights 1, 2, 3; p = 2, q = 0.5
+    (reciprocal convention) gives P ∝ (0.5, 2, 6).  Walks rooted at 0 whose
+    first step went to 1 are counted (tests/test_apps.py brute-force pattern)."""
+    from paper_2009_06693_b200 import _lib, make_app
+    from paper_2009_06693_b200.engine import run_device
+    from paper_2009_06693_b200.graph import DeviceGraph
+    src = [0, 0, 1, 1, 1, 2, 3, 4]
+    dst = [1, 2, 0, 2, 3, 1, 4, 0]
+    w = [1.0, 1.0, 1.0, 2.0, 3.0, 1.0, 1.0, 1.0]
+    g = DeviceGraph.from_edges(np.array(src), np.array(dst), np.array(w), 5)
+    for par in ("sp", "tp"):
+        dr = run_device(make_app("node2vec", p=2.0, q=0.5, walk_length=2), g, n_samples=500_000,
+                        seed=17, paradigm=par)
+        off, ids = dr.host(_lib.F_FINAL_OFF), dr.host(_lib.F_FINAL_IDS)
+        rows = np.diff(off) == 3
+        start = off[:-1][rows]
+        r0, r1, r2 = ids[start], ids[start + 1], ids[start + 2]
+        sel = (r0 == 0) & (r1 == 1)
+        counts = np.bincount(r2[sel], minlength=4)[[0, 2, 3]]
+        assert counts.sum() > 20_000
+        assert _chi2_p(counts, np.array([0.5, 2.0, 6.0]) / 8.5) > 1e-3, (par, counts)
+        dr.close()
