@@ -21,6 +21,7 @@
 // by members * degree, collective.py:107-114) are computed on device from a
 // radix sort of the step's transit occurrences.
 #include <cub/cub.cuh>
+#include <thrust/iterator/transform_iterator.h>
 
 #include <algorithm>
 #include <vector>
@@ -49,11 +50,9 @@ int dcopy_to_host(T* h, const T* d, int64_t n, cudaStream_t s) {
   return ND_OK;
 }
 
-__global__ void k_widen_flags(const uint8_t* __restrict__ f, int64_t n, int64_t* __restrict__ out) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = f[i];
-}
+struct WidenFlag {
+  __host__ __device__ int64_t operator()(uint8_t x) const { return (int64_t)x; }
+};
 
 // degrees of the flattened transits (+1 trailing 0 for the exclusive scan)
 __global__ void k_tdeg(const int32_t* __restrict__ tv, int64_t T, const int64_t* __restrict__ row,
@@ -733,9 +732,16 @@ extern "C" int nd_run_collective(const nd_graph* G, int kind, int64_t step_size,
       if (tot_tri)
         k_imp_hits<<<nd_grid(n * m * 32, 256, 148 * 64), 256, 0, s>>>(g, toff, tv, out, alive,
                                                                       tri_off, n, m, tot_tri, fl);
-      // hit flags widened into pos, then scanned in place
-      k_widen_flags<<<nd_grid(tot_tri + 1, 256), 256, 0, s>>>(fl, tot_tri + 1, pos);
-      ND_TRY(scan_excl(pos, pos, tot_tri + 1, s));
+      // exclusive scan of the byte flags, widened on the fly
+      {
+        auto it = thrust::make_transform_iterator(fl, WidenFlag{});
+        size_t tb = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, tb, it, pos, tot_tri + 1, s);
+        void* tmp = nullptr;
+        ND_CUDA_TRY(nd_alloc((char**)&tmp, tb, s));
+        ND_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tb, it, pos, tot_tri + 1, s));
+        nd_free(tmp, s);
+      }
       ND_TRY(dcopy_to_host(&cs.nrec, pos + tot_tri, 1, s));
       ND_CUDA_TRY(nd_alloc(&cs.rec_t, cs.nrec, s));
       ND_CUDA_TRY(nd_alloc(&cs.rec_v, cs.nrec, s));
