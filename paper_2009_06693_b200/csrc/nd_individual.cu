@@ -527,14 +527,25 @@ __global__ void k_fx_final(FxSteps S, const RootT* __restrict__ roots, int64_t n
       if (i == n - 1) roots_off[n] = n * R;
     }
     int64_t pos = R;
-    for (int s = 0; s < S.n_steps; s++)
-      for (int64_t p0 = 0; p0 < S.B[s]; p0 += 32) {
-        const int64_t p = p0 + lane;
-        const int32_t v = p < S.B[s] ? S.blk[s][i * S.B[s] + p] : -1;
-        const unsigned mk = __ballot_sync(0xffffffffu, v >= 0);
-        if (v >= 0) dst[pos + __popc(mk & ((1u << lane) - 1))] = v;
-        pos += __popc(mk);
+    for (int s = 0; s < S.n_steps; s++) {
+      const int64_t B = S.B[s];
+      const int32_t* src = S.blk[s] + i * B;
+      // eight 32-slot chunks loaded back to back, then compacted in order
+      for (int64_t p0 = 0; p0 < B; p0 += 32 * 8) {
+        int32_t v[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+          const int64_t p = p0 + 32 * u + lane;
+          v[u] = p < B ? src[p] : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+          const unsigned mk = __ballot_sync(0xffffffffu, v[u] >= 0);
+          if (v[u] >= 0) dst[pos + __popc(mk & ((1u << lane) - 1))] = v[u];
+          pos += __popc(mk);
+        }
       }
+    }
   }
 }
 
