@@ -19,6 +19,7 @@ from __future__ import annotations
 import ctypes as C
 import math
 import time
+import warnings
 from dataclasses import dataclass, field
 from typing import Optional, Sequence
 
@@ -156,7 +157,8 @@ def _describe(app) -> DevicePlan:
         m = [int(app.sample_size(s)) for s in range(max(steps, 1))] if steps >= 0 else [1]
         if code == 4 or any(x != 1 for x in m) or steps < 0:
             raise UnsupportedAppError(f"{name}: unsupported individual configuration")
-        return DevicePlan("walk", name, code=code, kparams=kp, steps=steps, R=R or 1)
+        return DevicePlan("walk", name, code=code, kparams=kp, steps=steps, R=R or 1,
+                          roots_kind=_roots_kind(app))
     if name in COLLECTIVE_KINDS:
         ck = COLLECTIVE_KINDS[name]
         plan = DevicePlan("collective", name, ckind=ck, steps=steps, unique=umask,
@@ -223,8 +225,11 @@ class SampleRange(Sequence):
             if st != 1:
                 raise ValueError("SampleRange slices must be contiguous")
             return SampleRange(self.app, self.graph, self.lo + a, max(0, b - a), self.seed)
+        i = int(i)
         if i < 0:
             i += self.n
+        if not 0 <= i < self.n:
+            raise IndexError("SampleRange index out of range")
         init = self.app.init_roots
         return Sample(self.lo + i, init(self.graph, self.lo + i, self.seed), self.graph)
 
@@ -519,6 +524,10 @@ def _run(app, graph, samples, config, paradigm) -> SampleSetOutput:
     config = config or EngineConfig()
     par = config.paradigm or paradigm
     dr = run_device(app, graph, samples, seed=config.seed, paradigm=par, step_cap=config.step_cap)
+    if dr.plan.steps < 0 and dr.n_steps >= config.step_cap:
+        # run_chain / run_loop (chain.py:93-98, driver.py:215-220)
+        warnings.warn(f"unbounded app {getattr(app, 'name', '?')!r} hit the "
+                      f"{config.step_cap}-step cap", RuntimeWarning, stacklevel=3)
     remap = getattr(graph, "remap", None)
     if isinstance(graph, DeviceGraph):
         remap = graph.remap

@@ -40,6 +40,41 @@ def _dev(a, dtype):
     return torch.from_numpy(arr.view(np.int64) if dtype == np.uint64 else arr).cuda()
 
 
+_GRAPH_CACHE = {}  # id(host array) -> (weakref, data pointer, nbytes, dtype, device tensor)
+
+
+def _graph_dev(a, dtype):
+    """Device copy of a borrowed read-only graph array (graph.py:36-39: the
+    Graph is frozen and its arrays are never written), uploaded once per array
+    object: the level-1 seam is called once per step with the same graph, and
+    re-uploading the CSR every call (1.7 GB on C2) would cost more than the
+    kernel.  Keyed by object identity and validated by data pointer, size and
+    dtype; entries die with the host array."""
+    import weakref
+    if a is None or _is_cuda(a):
+        return _dev(a, dtype)
+    if not isinstance(a, np.ndarray) or a.dtype != np.dtype(dtype) or not a.flags.c_contiguous:
+        return _dev(a, dtype)  # converted copies are not cacheable
+    key = id(a)
+    hit = _GRAPH_CACHE.get(key)
+    if hit is not None:
+        ref, ptr, nb, dt, t = hit
+        if ref() is a and ptr == a.ctypes.data and nb == a.nbytes and dt == a.dtype:
+            return t
+    t = _dev(a, dtype)
+    try:
+        ref = weakref.ref(a, lambda _r, k=key: _GRAPH_CACHE.pop(k, None))
+    except TypeError:
+        return t
+    _GRAPH_CACHE[key] = (ref, a.ctypes.data, a.nbytes, a.dtype, t)
+    return t
+
+
+def clear_graph_cache():
+    """Drop every cached device copy of host graph arrays."""
+    _GRAPH_CACHE.clear()
+
+
 def individual_batch(app_code, params, row_offsets, col_indices, weights, weight_prefix,
                      max_weight, transits, t_prev, sample_ids, transit_idxs, slots, seed, step,
                      out):
@@ -49,8 +84,9 @@ def individual_batch(app_code, params, row_offsets, col_indices, weights, weight
     torch = _lib.require_cuda()
     L = _lib.load()
     prm = np.ascontiguousarray(params if params is not None else [], dtype=np.float64)
-    args = [_dev(row_offsets, np.int64), _dev(col_indices, np.int64), _dev(weights, np.float64),
-            _dev(weight_prefix, np.float64), _dev(max_weight, np.float64)]
+    args = [_graph_dev(row_offsets, np.int64), _graph_dev(col_indices, np.int64),
+            _graph_dev(weights, np.float64), _graph_dev(weight_prefix, np.float64),
+            _graph_dev(max_weight, np.float64)]
     items = [_dev(x, np.int64) for x in (transits, t_prev, sample_ids, transit_idxs, slots)]
     n = len(items[0])
     dout = out if _is_cuda(out) else torch.empty(n, dtype=torch.int64, device="cuda")

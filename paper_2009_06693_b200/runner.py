@@ -165,6 +165,23 @@ def _concat(outs, graph, stats) -> SampleSetOutput:
                     b = o._step_base()
                     vals.append(o.step_vals[b[st]:b[st + 1]])
         kw = dict(step_counts=cnt, step_vals=cat(vals))
+        if outs and any(o.rec_counts is not None and o.rec_t is not None for o in outs):
+            # recorded edges, step-major like step_vals (multi_worker_run keeps them)
+            rc, rt, rv = [], [], []
+            for o in outs:
+                c = o.rec_counts if o.rec_counts is not None else np.zeros((0, o.n_samples),
+                                                                             np.int64)
+                rc.append(np.pad(np.asarray(c, np.int64), ((0, S - c.shape[0]), (0, 0))))
+            for st in range(S):
+                for o in outs:
+                    if o.rec_counts is None or o.rec_t is None or st >= len(o.rec_counts):
+                        continue
+                    tot = np.asarray(o.rec_counts).sum(axis=1)
+                    a = int(tot[:st].sum())
+                    b = a + int(tot[st])
+                    rt.append(o.rec_t[a:b])
+                    rv.append(o.rec_v[a:b])
+            kw.update(rec_counts=np.concatenate(rc, axis=1), rec_t=cat(rt), rec_v=cat(rv))
     return SampleSetOutput(ids, roots_off, roots, n_steps, remap=getattr(graph, "remap", None),
                            stats=stats, final_off=final_off, final_ids=cat(fids), **kw)
 

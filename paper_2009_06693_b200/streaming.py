@@ -136,6 +136,15 @@ class HostPipeline:
             out, held = [], []
             if ji > 0 and k > 1:
                 first_done.wait(timeout=60)  # the link gets busy before the GPU is shared
+            try:
+                return _chunks(ji, app, n_samples, seed, sample_lo, roots_host, st, cs, plan,
+                               parts, out, held)
+            finally:
+                if ji == 0:  # job 0 without chunks (or failing) must not stall the others
+                    first_done.set()
+
+        def _chunks(ji, app, n_samples, seed, sample_lo, roots_host, st, cs, plan, parts, out,
+                    held):
             with torch.cuda.stream(st):
                 for ci, (lo, hi) in enumerate(parts):
                     n = hi - lo

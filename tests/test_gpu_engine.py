@@ -599,3 +599,17 @@ def test_edgeless_graph_and_empty_jobs():
             assert dr.total_sampled == 0, (app, par)
             assert list(dr.to_output().final_csr()[0]) == [0], (app, par)
             dr.close()
+
+
+@pytest.mark.parametrize("paradigm", ["tp", "sp"])
+def test_unbounded_app_step_cap_warns(paradigm):
+    """An INF-step app that reaches the step cap warns like run_chain/run_loop
+    (chain.py:93-98, driver.py:215-220; reference test_engines.py:173-178)."""
+    from paper_2009_06693_b200 import EngineConfig, make_app, make_samples, sp_run, tp_run
+    from paper_2009_06693_b200.synth import cycle_graph
+    g = cycle_graph(1000, weighted=True, seed=2)
+    app = make_app("ppr", termination_probability=0.0001)  # walks outlive the cap
+    run = tp_run if paradigm == "tp" else sp_run
+    with pytest.warns(RuntimeWarning, match="step cap"):
+        out = run(app, g, make_samples(app, g, 4, seed=1), EngineConfig(seed=1, step_cap=50))
+    assert out.n_steps == 50

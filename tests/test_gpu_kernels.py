@@ -139,3 +139,34 @@ def test_empty_batch(K):
     e = np.empty(0, dtype=np.int64)
     K.individual_batch(0, [], g.row_offsets, g.col_indices, g.weights, g.per_vertex_weight_prefix,
                        g.per_vertex_max_weight, e, e, e, e, e, 1, 0, e)
+
+
+def test_graph_arrays_upload_once(K):
+    """The level-1 seam keeps one device copy per host graph array (the
+    reference's Graph is frozen, graph.py:36-39); repeated per-step calls reuse
+    it and give the same results."""
+    d = golden("batch_parity.npz")
+    g = {k: np.ascontiguousarray(d[f"g/{k}"]) for k in ("row_offsets", "col_indices", "weights",
+                                                         "prefix", "max_w")}
+    K.clear_graph_cache()
+    outs = []
+    for rep in range(3):
+        out = np.empty(len(d["c0/out"]), dtype=np.int64)
+        K.individual_batch(0, d["c0/params"], g["row_offsets"], g["col_indices"], g["weights"],
+                           g["prefix"], g["max_w"], d["c0/transits"], d["c0/t_prev"],
+                           d["c0/sample_ids"], d["c0/transit_idxs"], d["c0/slots"], 123, 2, out)
+        outs.append(out)
+        if rep == 0:
+            cached = {k: v[4].data_ptr() for k, v in K._GRAPH_CACHE.items()}
+            assert len(cached) == 5
+    assert {k: v[4].data_ptr() for k, v in K._GRAPH_CACHE.items()} == cached
+    for o in outs:
+        assert np.array_equal(o, d["c0/out"])
+    # a different array object is a different graph
+    w2 = g["weights"].copy()
+    K.individual_batch(0, d["c0/params"], g["row_offsets"], g["col_indices"], w2, g["prefix"],
+                       g["max_w"], d["c0/transits"], d["c0/t_prev"], d["c0/sample_ids"],
+                       d["c0/transit_idxs"], d["c0/slots"], 123, 2, outs[0])
+    assert len(K._GRAPH_CACHE) == 6
+    del w2
+    assert len(K._GRAPH_CACHE) == 5
