@@ -169,7 +169,27 @@ def cpu_walks(hg, lo, n, threads):
         vals = r["chain_vals"]
         edges += int((vals >= 0).sum())
         res[name] = r
+    res["roots"] = np.asarray(roots).reshape(-1)
     return edges, time.perf_counter() - t0, res
+
+
+def rows_equal_chain(off, ids, roots, r):
+    """Device final rows (offsets, ids) == the oracle's chains, value for
+    value: row i = roots[i] then chain i's non-NULL vertices in step order."""
+    clen, cv = np.asarray(r["chain_len"]), np.asarray(r["chain_vals"])
+    n = len(clen)
+    starts = np.concatenate([[0], np.cumsum(clen)[:-1]]).astype(np.int64)
+    ok = cv >= 0
+    nn = np.add.reduceat(ok.astype(np.int64), starts) if len(cv) else np.zeros(n, np.int64)
+    nn = np.where(clen > 0, nn, 0)
+    if len(off) != n + 1 or not np.array_equal(np.diff(off), 1 + nn):
+        return False
+    exp = np.empty(int(off[-1]), dtype=np.int64)
+    is_root = np.zeros(len(exp), dtype=bool)
+    is_root[off[:-1]] = True
+    exp[is_root] = roots
+    exp[~is_root] = cv[ok]
+    return bool(np.array_equal(np.asarray(ids, dtype=np.int64), exp))
 
 
 def host_graph_for_oracle(dg):
@@ -507,6 +527,7 @@ def main():
     # ---- CPU baseline (rank 0, N=1 only) ------------------------------------------------
     cpu = None
     parity = None
+    parity_values = 0
     if rank == 0 and ws == 1 and not args.no_cpu:
         cores = len(os.sched_getaffinity(0))
         hg = host_graph_for_oracle(dg)
@@ -514,21 +535,15 @@ def main():
         cpu = {"value": ce / cdt, "unit": "edges/s", "cores": cores, "kind": "port",
                "sample": f"node2vec+PPR walks for sample ids [0, {CPU_SAMPLE}) "
                          f"({ce} edges, {cdt:.1f} s)"}
-        # parity of the sampled rows on the CPU sample
+        # parity of every sampled row on the CPU sample: offsets and every
+        # vertex id (root, then the walk's non-NULL steps, chain.py:166-179)
         parity = True
         for (name, kw), app in zip(APPS, apps):
             dr = run_device(app, dg, n_samples=CPU_SAMPLE, seed=SEED, paradigm=args.paradigm)
             off, ids = dr.host(_lib.F_FINAL_OFF), dr.host(_lib.F_FINAL_IDS)
-            r = cres[name]
-            clen = r["chain_len"]
-            cv = r["chain_vals"]
-            nn = np.add.reduceat((cv >= 0).astype(np.int64), np.concatenate([[0], np.cumsum(clen)[:-1]])) \
-                if len(cv) else np.zeros(CPU_SAMPLE, dtype=np.int64)
-            nn = np.where(clen > 0, nn, 0)
-            parity &= bool(np.array_equal(np.diff(off), 1 + nn))
-            parity &= bool(np.array_equal(ids[off[:-1] + 1][nn > 0] if len(ids) else ids,
-                                          cv[np.concatenate([[0], np.cumsum(clen)[:-1]])][nn > 0]))
             dr.close()
+            parity &= bool(rows_equal_chain(off, ids, cres["roots"], cres[name]))
+        parity_values = int(sum(len(cres[k]["chain_vals"]) for k in ("node2vec", "ppr")))
 
     if rank == 0:
         ms_per_step = tot_ms / len(times)
@@ -555,7 +570,11 @@ def main():
                          "kernel_ms_per_step": rf_ms / 2,
                          "kernel_timing": "apps one after another (2 passes), event-timed launches",
                          "gather": gather},
-            "cpu_baseline": cpu, "parity_cpu_sample": parity, "paradigm_tp": tp_info,
+            "cpu_baseline": cpu, "parity_cpu_sample": parity,
+            "parity": {"ok": parity, "values_compared": parity_values if parity is not None else 0,
+                       "how": "every final-row offset and vertex id of the CPU sample's walkers "
+                              "(both apps) equals the C oracle's"} if parity is not None else None,
+            "paradigm_tp": tp_info,
             "clocks": clocks.summary(), "gpu_launches": launches, "gather": gather_info,
             "edges_per_step": edges_all / len(times),
         }

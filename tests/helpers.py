@@ -137,3 +137,63 @@ def build_app(meta):
         us = set(u)
         app.unique = lambda step, us=us: step in us
     return app
+
+
+def oracle_full_graph(dg) -> O.OGraph:
+    """The whole device CSR copied to the host for the oracle."""
+    h = dg.to_host()
+    return O.OGraph(h.n_vertices, h.row_offsets, h.col_indices, h.weights,
+                    h.per_vertex_weight_prefix, h.per_vertex_max_weight, None)
+
+
+def oracle_subgraph(dg, vertices) -> O.OGraph:
+    """An oracle graph with the device graph's rows of ``vertices`` only (every
+    other row empty), gathered on the device so a 1B-edge graph never crosses
+    to the host whole.  Sound for parity checks of runs whose transits are all
+    in ``vertices``: where the device and the oracle agree the oracle reads
+    exactly these rows, and where they first disagree the comparison fails
+    (a missing row makes the oracle's sample differ, never agree)."""
+    import torch
+    a = dg.arrays()
+    row = a["row_offsets"]
+    V = dg.n_vertices
+    v = torch.unique(torch.as_tensor(np.asarray(vertices, dtype=np.int64), device="cuda"))
+    v = v[(v >= 0) & (v < V)]
+    lo = row[v]
+    deg = row[v + 1] - lo
+    full = torch.zeros(V + 1, dtype=torch.int64, device="cuda")
+    full[v + 1] = deg
+    off = torch.cumsum(full, 0)
+    seg = torch.repeat_interleave(torch.arange(len(v), device="cuda"), deg)
+    start_new = off[v]
+    pos = torch.arange(int(deg.sum().item()), device="cuda") - start_new[seg] + lo[seg]
+    col = a["col"][pos].to(torch.int64)
+    if dg.unit_weights:
+        w = torch.ones(len(pos), dtype=torch.float64, device="cuda")
+        pre = (pos - lo[seg] + 1).to(torch.float64)
+    else:
+        w, pre = a["weights"][pos], a["prefix"][pos]
+    mx = torch.zeros(V, dtype=torch.float64, device="cuda")
+    mx[v] = a["max_w"][v]
+    return O.OGraph(V, off.cpu().numpy(), col.cpu().numpy(), w.cpu().numpy(), pre.cpu().numpy(),
+                    mx.cpu().numpy(), None)
+
+
+def expected_walk_rows(roots, r):
+    """(offsets, ids) of walk final rows from an oracle run_chain result:
+    row i = roots[i] then the chain's non-NULL vertices (chain.py:166-179)."""
+    roots = np.asarray(roots, dtype=np.int64).reshape(len(r["chain_len"]), -1)
+    clen, cv = np.asarray(r["chain_len"]), np.asarray(r["chain_vals"])
+    starts = np.concatenate([[0], np.cumsum(clen)[:-1]]).astype(np.int64)
+    ok = cv >= 0
+    nn = np.add.reduceat(ok.astype(np.int64), starts) if len(cv) else np.zeros(len(clen), np.int64)
+    nn = np.where(clen > 0, nn, 0)
+    R = roots.shape[1]
+    off = np.concatenate([[0], np.cumsum(R + nn)]).astype(np.int64)
+    ids = np.empty(int(off[-1]), dtype=np.int64)
+    is_root = np.zeros(len(ids), dtype=bool)
+    for k in range(R):
+        is_root[off[:-1] + k] = True
+    ids[is_root] = roots.ravel()
+    ids[~is_root] = cv[ok]
+    return off, ids
