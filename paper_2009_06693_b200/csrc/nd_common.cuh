@@ -89,6 +89,20 @@ struct FastDiv {
   }
 };
 
+// Exact u % d for a run-constant divisor d >= 1 (a hub's degree): with
+// M = floor((2^64-1)/d) >= 2^64/d - 1, q = umulhi(u, M) satisfies
+// u/d - 1 < q <= u/d, so one conditional subtraction gives the remainder.
+struct ModU64 {
+  uint64_t d = 1, M = ~0ull;
+  ModU64() = default;
+  __host__ __device__ explicit ModU64(uint64_t dv) : d(dv), M(dv ? ~0ull / dv : 0) {}
+  __device__ __forceinline__ uint64_t mod(uint64_t u) const {
+    const uint64_t q = __umul64hi(u, M);
+    const uint64_t r = u - q * d;
+    return r >= d ? r - d : r;
+  }
+};
+
 // one 32-byte load (LDG.E.256): a whole record / hash-set chunk per request
 __device__ __forceinline__ void ld32B(const void* p, int4& lo, int4& hi) {
   unsigned long long a, b, c, d;
@@ -258,6 +272,10 @@ inline cudaError_t nd_alloc(T** p, size_t n, cudaStream_t s) {
 inline void nd_free(void* p, cudaStream_t s) {
   if (p) cudaFreeAsync(p, s);
 }
+
+// column array entries to allocate: a multiple of 4 plus 4 of slack, so the
+// 16-byte-aligned superset of any row (nd_bulk.cuh row_span) is inside it
+inline int64_t nd_col_alloc(int64_t E) { return ((E + 3) & ~(int64_t)3) + 4; }
 
 inline int nd_grid(int64_t n, int block, int cap = 148 * 32) {
   int64_t g = (n + block - 1) / block;

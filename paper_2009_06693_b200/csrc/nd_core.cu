@@ -399,7 +399,7 @@ extern "C" int nd_graph_create(const int64_t* row_offsets, const int64_t* col_in
   int* bad = nullptr;
   do {
     if (cudaMalloc(&G->row, (n_vertices + 1) * sizeof(int64_t)) != cudaSuccess ||
-        cudaMalloc(&G->col, (n_edges ? n_edges : 1) * sizeof(int32_t)) != cudaSuccess) {
+        cudaMalloc(&G->col, nd_col_alloc(n_edges) * sizeof(int32_t)) != cudaSuccess) {
       rc = ND_ERR_NOMEM;
       break;
     }
@@ -503,7 +503,7 @@ static int build_from_edges_dev(const int64_t* src, const int64_t* dst, const do
   size_t tmp_bytes = 0;
   int rc = ND_OK;
   do {
-    if (cudaMalloc(&G->row, (V + 1) * sizeof(int64_t)) || cudaMalloc(&G->col, (E ? E : 1) * 4)) {
+    if (cudaMalloc(&G->row, (V + 1) * sizeof(int64_t)) || cudaMalloc(&G->col, nd_col_alloc(E) * 4)) {
       rc = ND_ERR_NOMEM;
       break;
     }

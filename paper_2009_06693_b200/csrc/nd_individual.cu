@@ -17,10 +17,13 @@
 // (exclusive scan), which also yields transit_idx and per-sample counts.
 #include <cub/cub.cuh>
 
+#include <cstdio>
 #include <cstdlib>
 
+#include <string>
 #include <vector>
 
+#include "nd_bulk.cuh"
 #include "nd_tp.cuh"
 
 using namespace nd;
@@ -491,6 +494,659 @@ __global__ void __launch_bounds__(IND_BLOCK) k_fx_sample_tp(GView<int32_t> gv, N
   flush_stats(st, ctr);
 }
 
+// ---- transit-parallel order for the fixed layout: hub-bucket inversion ----------
+// The transit -> sample inversion (transit_parallel.py:71-83) without a sort:
+// one pass counts each transit's members with warp-aggregated atomics (the
+// returned old count is the member's position in its group), and a transit is
+// appended to the hub list when its count crosses the medium threshold
+// (work = members*m >= 32, transit_parallel.py:86-101).  The per-step class
+// counts fall out of the same pass: groups = transits reaching 1 member,
+// medium+large = crossings of the medium threshold, large = crossings of the
+// large one (work > 1024).  A placement pass then writes every hub member's
+// record at its group position and collects the small-class parents.  Class
+// kernels:
+//   sub-warp     small class: the m lanes of one parent cache the transit's
+//                row in registers when it fits and read it with shuffles;
+//   warp         hubs with work <= HUB_WARP_MAX: one warp per hub;
+//   thread block hubs up to HUB_UNIT items: one CTA;
+//   grid         larger hubs: HUB_UNIT-item units over several CTAs.
+// The warp and CTA tiers stage the row (and the CTA tier the unit's member
+// records) in shared memory by bulk copies (nd_bulk.cuh), the next hub's
+// copy in flight while the current one is sampled.  Output positions are
+// fixed per (parent, slot), so any member order gives the same rows.
+constexpr int HUB_WARP_MAX = 256;   // work of a warp-tier hub
+constexpr int HUB_UNIT = 8192;      // items per CTA unit (larger hubs span several CTAs)
+constexpr int HUB_SLICE_W = 512;    // staged row entries per warp stage
+constexpr int HUB_SLICE_C = 2048;   // staged row entries per CTA stage
+constexpr int HUB_MEM_SLICE = 1024; // staged member records per CTA stage
+constexpr int REG_K = 4;            // row entries cached per sub-warp lane
+constexpr int FX_ILP = 4;           // independent items (or parents) in flight per thread
+
+struct HubThr {
+  int32_t tm, tl;  // member counts at which a group becomes medium / large
+};
+inline HubThr hub_thresholds(int64_t m) {
+  HubThr t;
+  if (m <= 0) { t.tm = t.tl = 0x7fffffff; return t; }
+  t.tm = (int32_t)((SMALL_MAX_WORK + m - 1) / m);  // members*m >= 32
+  t.tl = (int32_t)(LARGE_MIN_WORK / m + 1);        // members*m > 1024
+  return t;
+}
+
+// A parent slot as the class kernels see it: its index (output position
+// ip*m + slot) and the sample/transit part of its RNG key,
+// C_SAMPLE*(sid+1) + C_TRANSIT*(tix+1) (rng.py:52-71), computed once per
+// parent instead of once per slot.
+struct __align__(16) MemRec {
+  uint32_t ip, pad;
+  uint64_t key;
+};
+
+// Per-warp staging of list appends: a warp collects up to 32 entries in
+// shared memory and reserves their global slots with one atomic.  Every lane
+// calls push/flush with warp-uniform control flow.
+template <typename T>
+struct WarpBuf {
+  T* sbuf;      // this warp's 32 entries in shared memory
+  int n = 0;    // buffered entries (warp-uniform)
+  __device__ __forceinline__ int64_t flush(T* glist, int32_t* gcount) {
+    const int lane = threadIdx.x & 31;
+    int base = 0;
+    if (n) {
+      if (lane == 0) base = atomicAdd(gcount, n);
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (lane < n) glist[base + lane] = sbuf[lane];
+      __syncwarp();
+    }
+    n = 0;
+    return base;
+  }
+  __device__ __forceinline__ void push(bool f, const T& x, T* glist, int32_t* gcount) {
+    const unsigned bm = __ballot_sync(0xffffffffu, f);
+    if (!bm) return;
+    if (n + __popc(bm) > 32) flush(glist, gcount);
+    if (f) sbuf[n + __popc(bm & ((1u << (threadIdx.x & 31)) - 1))] = x;
+    n += __popc(bm);
+    __syncwarp();
+  }
+};
+
+__device__ __forceinline__ void hub_flush(WarpBuf<int32_t>& wb, int32_t* hubs, int32_t* nhub,
+                                          int2* vinfo) {
+  const int lane = threadIdx.x & 31;
+  const int cnt = wb.n;
+  const int32_t v = lane < cnt ? wb.sbuf[lane] : 0;
+  const int64_t base = wb.flush(hubs, nhub);
+  if (lane < cnt) vinfo[v].y = (int32_t)(base + lane);
+}
+
+// Member counting of Q tiles of 32 parent slots (every lane calls it; lane
+// entries with v >= 0 are non-NULL parents ip with transit v): the Q tiles'
+// warp-aggregated atomics on the per-vertex count are in flight together; the
+// returned old count is each member's position in its group, and threshold
+// crossings go to the hub list through the warp buffer.
+template <int Q>
+__device__ __forceinline__ void count_tiles(const int32_t (&v)[Q], const int64_t (&ip)[Q],
+                                            int2* vinfo, int32_t* gpos, WarpBuf<int32_t>& wb,
+                                            int32_t* hubs, int32_t* nhub, const HubThr& th,
+                                            unsigned long long& ng, unsigned long long& nm,
+                                            unsigned long long& nl) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1;
+  int old[Q], c[Q];
+  unsigned peers[Q];
+#pragma unroll
+  for (int q = 0; q < Q; q++) {
+    const bool ok = v[q] >= 0;
+    const unsigned mk = __ballot_sync(0xffffffffu, ok);
+    old[q] = 0;
+    c[q] = 0;
+    peers[q] = 0;
+    if (ok) {
+      peers[q] = __match_any_sync(mk, v[q]);
+      c[q] = __popc(peers[q]);
+      if (lane == __ffs(peers[q]) - 1) old[q] = atomicAdd(&vinfo[v[q]].x, c[q]);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < Q; q++) {
+    bool cross = false;
+    if (v[q] >= 0) {
+      const int leader = __ffs(peers[q]) - 1;
+      const int o = __shfl_sync(peers[q], old[q], leader);
+      gpos[ip[q]] = o + __popc(peers[q] & lt);
+      if (lane == leader) {
+        ng += o == 0;
+        cross = o < th.tm && o + c[q] >= th.tm;
+        nm += cross;
+        nl += o < th.tl && o + c[q] >= th.tl;
+      }
+    }
+    const unsigned cm = __ballot_sync(0xffffffffu, cross);
+    if (cm) {
+      if (wb.n + __popc(cm) > 32) hub_flush(wb, hubs, nhub, vinfo);
+      if (cross) wb.sbuf[wb.n + __popc(cm & lt)] = v[q];
+      wb.n += __popc(cm);
+      __syncwarp();
+    }
+  }
+}
+
+// transit_idx ranks as k_fx_rank (rank among the sample block's non-NULL
+// entries), per-sample non-NULL counts, and member counting.  Blocks of B < 32
+// slots: several samples per 32-lane tile (one lane segment each), FX_ILP
+// tiles per warp iteration; larger blocks: one sample per warp, its 32-slot
+// chunks in order.  vinfo[v] = {member count, hub index}.
+template <int Q>
+__global__ void __launch_bounds__(256) k_fx_rank_count(const int32_t* __restrict__ blk, int64_t n,
+                                                       int64_t B, int32_t* __restrict__ rank,
+                                                       int64_t* __restrict__ nn,
+                                                       int2* __restrict__ vinfo,
+                                                       int32_t* __restrict__ gpos,
+                                                       int32_t* __restrict__ hubs,
+                                                       int32_t* __restrict__ nhub, HubThr th,
+                                                       unsigned long long* __restrict__ stats) {
+  __shared__ int32_t s_hub[256];
+  WarpBuf<int32_t> wb;
+  wb.sbuf = s_hub + (threadIdx.x & ~31);
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  unsigned long long ng = 0, nm = 0, nl = 0;
+  if (B < 32) {
+    const int spw = 32 / (int)B, seg = lane / (int)B, pos = lane % (int)B;
+    const unsigned segm = (unsigned)(((1ull << B) - 1) << (seg * B));
+    const int64_t tiles = (n + spw - 1) / spw;
+    for (int64_t t0 = warp * Q; t0 < tiles; t0 += nw * Q) {
+      int32_t v[Q];
+      int64_t ip[Q];
+#pragma unroll
+      for (int q = 0; q < Q; q++) {
+        const int64_t i = (t0 + q) * spw + seg;
+        const bool valid = seg < spw && i < n;
+        ip[q] = valid ? i * B + pos : -1;
+        v[q] = valid ? blk[ip[q]] : -2;
+      }
+#pragma unroll
+      for (int q = 0; q < Q; q++) {
+        const unsigned mk = __ballot_sync(0xffffffffu, v[q] >= 0);
+        if (ip[q] >= 0) {
+          rank[ip[q]] = v[q] >= 0 ? __popc(mk & segm & lt) : -1;
+          if (pos == 0) nn[ip[q] / B] = __popc(mk & segm);
+        }
+      }
+      count_tiles<Q>(v, ip, vinfo, gpos, wb, hubs, nhub, th, ng, nm, nl);
+    }
+  } else {
+    for (int64_t i = warp; i < n; i += nw) {
+      int32_t base = 0;
+      for (int64_t p0 = 0; p0 < B; p0 += 32) {
+        const int64_t p = p0 + lane;
+        int32_t v[1] = {p < B ? blk[i * B + p] : -2};
+        int64_t ip[1] = {p < B ? i * B + p : -1};
+        const unsigned mk = __ballot_sync(0xffffffffu, v[0] >= 0);
+        if (p < B) rank[ip[0]] = v[0] >= 0 ? base + __popc(mk & lt) : -1;
+        base += __popc(mk);
+        count_tiles<1>(v, ip, vinfo, gpos, wb, hubs, nhub, th, ng, nm, nl);
+      }
+      if (lane == 0) nn[i] = base;
+    }
+  }
+  hub_flush(wb, hubs, nhub, vinfo);
+  for (int o = 16; o > 0; o >>= 1) {
+    ng += __shfl_down_sync(0xffffffffu, ng, o);
+    nm += __shfl_down_sync(0xffffffffu, nm, o);
+    nl += __shfl_down_sync(0xffffffffu, nl, o);
+  }
+  // a warp can cross a threshold of a group another warp opened: the class
+  // deltas are signed per warp and sum to the exact counts over the grid
+  if (lane == 0 && (ng | nm | nl)) {
+    if (ng != nm) atomicAdd(stats + 0, ng - nm);
+    if (nm != nl) atomicAdd(stats + 1, nm - nl);
+    if (nl) atomicAdd(stats + 2, nl);
+    if (ng) atomicAdd(stats + 3, ng);
+  }
+}
+
+// hub sizes (members) and CTA-unit counts, zero past the hub count
+__global__ void k_hub_sizes(const int32_t* __restrict__ hubs, const int32_t* __restrict__ nhub,
+                            int64_t cap, const int2* __restrict__ vinfo, int64_t m,
+                            int32_t* __restrict__ hsz, int32_t* __restrict__ hun) {
+  const int64_t H = *nhub;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j <= cap;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    int32_t c = 0, u = 0;
+    if (j < H) {
+      c = vinfo[hubs[j]].x;
+      const int64_t w = (int64_t)c * m;
+      u = w > HUB_WARP_MAX ? (int32_t)((w + HUB_UNIT - 1) / HUB_UNIT) : 0;
+    }
+    hsz[j] = c;
+    hun[j] = u;
+  }
+}
+
+// the CTA units of the hubs above the warp tier: one 32-byte descriptor per
+// unit (row, group start, item range) for the producer warp of k_fx_hub_cta
+struct __align__(32) HubUnit {
+  int64_t lo;
+  int32_t deg, start, t0, t1, pad0, pad1;
+};
+
+__global__ void k_hub_units(const int32_t* __restrict__ nhub, const int32_t* __restrict__ hubs,
+                            const int32_t* __restrict__ hoff, const int32_t* __restrict__ uoff,
+                            const int32_t* __restrict__ hun, const int64_t* __restrict__ row,
+                            int64_t m, HubUnit* __restrict__ units) {
+  const int64_t H = *nhub;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < H;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t nu = hun[j];
+    if (nu == 0) continue;
+    const int32_t v = hubs[j];
+    HubUnit d;
+    d.lo = row[v];
+    d.deg = (int32_t)(row[v + 1] - d.lo);
+    d.start = hoff[j];
+    const int64_t work = (int64_t)(hoff[j + 1] - d.start) * m;
+    d.pad0 = d.pad1 = 0;
+    const int32_t u0 = uoff[j];
+    for (int32_t c = 0; c < nu; c++) {
+      d.t0 = c * HUB_UNIT;
+      d.t1 = (int32_t)min(work, (int64_t)d.t0 + HUB_UNIT);
+      units[u0 + c] = d;
+    }
+  }
+}
+
+// Placement, FX_ILP tiles of 32 consecutive parent slots per warp: NULL
+// parents give m NULL slots; hub members' records go to their group
+// position, small-class parents' records to the small list.  The final-row
+// lengths come from here too: a k-hop pick from a non-empty row is never
+// NULL, so a sample gains m values per parent whose transit has edges.
+template <int Q>
+__global__ void __launch_bounds__(256) k_fx_place(const int32_t* __restrict__ prev,
+                                                  const int32_t* __restrict__ rank, int64_t N,
+                                                  FastDiv Bp, int64_t m, int64_t sample_lo,
+                                                  const int64_t* __restrict__ row,
+                                                  const int2* __restrict__ vinfo, int32_t tm,
+                                                  const int32_t* __restrict__ gpos,
+                                                  const int32_t* __restrict__ hoff,
+                                                  MemRec* __restrict__ perm,
+                                                  MemRec* __restrict__ small,
+                                                  int32_t* __restrict__ nsmall,
+                                                  int32_t* __restrict__ out,
+                                                  unsigned long long* __restrict__ scnt) {
+  __shared__ MemRec s_small[256];
+  const int lane = threadIdx.x & 31;
+  WarpBuf<MemRec> wb;
+  wb.sbuf = s_small + (threadIdx.x & ~31);
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t b0 = warp * 32 * Q; b0 < N; b0 += nw * 32 * Q) {
+    int32_t v[Q], rk[Q], gp[Q], ho[Q];
+    int2 vi[Q];
+    int64_t dg[Q];
+#pragma unroll
+    for (int q = 0; q < Q; q++) {
+      const int64_t ip = b0 + q * 32 + lane;
+      v[q] = ip < N ? prev[ip] : -2;
+      rk[q] = ip < N ? rank[ip] : -1;
+      gp[q] = ip < N ? gpos[ip] : 0;
+    }
+#pragma unroll
+    for (int q = 0; q < Q; q++) {
+      vi[q] = v[q] >= 0 ? vinfo[v[q]] : make_int2(0, 0);
+      dg[q] = v[q] >= 0 ? __ldg(row + v[q] + 1) - __ldg(row + v[q]) : 0;
+    }
+#pragma unroll
+    for (int q = 0; q < Q; q++) ho[q] = vi[q].x >= tm ? hoff[vi[q].y] : 0;
+#pragma unroll
+    for (int q = 0; q < Q; q++) {
+      const int64_t ip = b0 + q * 32 + lane;
+      bool sm = false;
+      MemRec r;
+      const int64_t i = v[q] >= 0 ? (int64_t)Bp.div((uint32_t)ip) : -1;
+      if (v[q] == -1) {
+        for (int64_t j = 0; j < m; j++) out[ip * m + j] = -1;
+      } else if (v[q] >= 0) {
+        r.ip = (uint32_t)ip;
+        r.pad = 0;
+        r.key = C_SAMPLE * (uint64_t)(sample_lo + i + 1) + C_TRANSIT * (uint64_t)(rk[q] + 1);
+        if (vi[q].x >= tm) perm[ho[q] + gp[q]] = r;
+        else sm = true;
+      }
+      wb.push(sm, r, small, nsmall);
+      // per-sample non-NULL slots: lanes of one sample add once
+      const bool gain = dg[q] > 0;
+      const unsigned gb = __ballot_sync(0xffffffffu, gain);
+      const unsigned same = __match_any_sync(0xffffffffu, i);
+      const unsigned grp = gb & same;
+      if (gain && lane == __ffs(grp) - 1) atomicAdd(scnt + i, (unsigned long long)(__popc(grp) * m));
+    }
+  }
+  wb.flush(small, nsmall);
+}
+
+struct FxHub {
+  GView<int32_t> gv;
+  uint64_t base0;   // key_base(seed, step, 0, 0)
+  FastDiv m;
+  const int32_t* hubs;
+  const int32_t* nhub;
+  const int32_t* hoff;  // [cap+1] member offsets into perm
+  const int32_t* uoff;  // [cap+1] CTA-unit offsets (uoff[cap] = unit count)
+  int64_t cap;
+  const HubUnit* units; // CTA-unit descriptors
+  const MemRec* perm;   // member records in group order
+  int32_t* out;
+  unsigned long long* ctr;
+};
+
+// one item: slot `slot` of member record `r`, the transit's row at `srow`
+// (shared memory) or `col + lo`; returns the vertex (NULL for an empty row)
+__device__ __forceinline__ int32_t fx_pick(uint64_t base0, const MemRec& r, uint32_t slot,
+                                           const ModU64& md, int64_t deg, const int32_t* srow,
+                                           const int32_t* col, int64_t lo) {
+  if (deg <= 0) return -1;  // a transit without out-edges gives NULL slots (_ckernels.pyx:212-223)
+  const uint64_t k = md.mod(draw_u64(base0, r.key + C_SLOT * (uint64_t)(slot + 1)));
+  return srow ? srow[k] : __ldg(col + lo + (int64_t)k);
+}
+
+// Algorithmic bytes of a range [t0, t1) of a hub's items:
+// S+8 per pair (slot 0 items) plus S+8 per slot when the row is non-empty.
+__device__ __forceinline__ int64_t fx_range_bytes(int32_t t0, int32_t t1, uint32_t m, int64_t deg) {
+  const int64_t pairs = (int64_t)((t1 + m - 1) / m) - (int64_t)((t0 + m - 1) / m);
+  return pairs * (SECTOR + 8) + (deg > 0 ? (int64_t)(t1 - t0) * (SECTOR + 8) : 0);
+}
+
+// small class: one thread per (small parent, slot); the lanes of one parent
+// form a sub-warp that holds the transit's row in registers when it fits
+// (REG_K entries per lane) and reads it with warp shuffles
+__global__ void __launch_bounds__(IND_BLOCK) k_fx_small(GView<int32_t> gv, uint64_t base0,
+                                                       FastDiv m, const int32_t* __restrict__ prev,
+                                                       const MemRec* __restrict__ small,
+                                                       const int32_t* __restrict__ nsmall,
+                                                       int32_t* __restrict__ out,
+                                                       unsigned long long* __restrict__ ctr) {
+  ItemStats st;
+  const int lane = threadIdx.x & 31;
+  const int64_t total = (int64_t)(*nsmall) * m.d;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t q0 = blockIdx.x * (int64_t)blockDim.x; q0 < total; q0 += stride) {
+    const int64_t q = q0 + threadIdx.x;
+    const bool act = q < total;
+    const unsigned am = __ballot_sync(0xffffffffu, act);
+    if (!act) continue;
+    const uint32_t e = m.div((uint32_t)q), slot = (uint32_t)q - e * m.d;
+    const unsigned peers = __match_any_sync(am, e);
+    const int leader = __ffs(peers) - 1;
+    const int sw = __popc(peers);
+    const int r = lane - leader;
+    MemRec rec;
+    int64_t lo = 0, hi = 0;
+    if (lane == leader) {
+      rec = small[e];
+      const int32_t v = prev[rec.ip];
+      lo = __ldg(gv.row + v);
+      hi = __ldg(gv.row + v + 1);
+    }
+    rec.ip = __shfl_sync(peers, rec.ip, leader);
+    rec.key = __shfl_sync(peers, rec.key, leader);
+    lo = __shfl_sync(peers, lo, leader);
+    hi = __shfl_sync(peers, hi, leader);
+    const int64_t deg = hi - lo;
+    int32_t o = -1;
+    if (slot == 0) st.bytes += SECTOR + 8;
+    if (deg > 0) {
+      st.bytes += SECTOR + 8;
+      const uint64_t k = mod_u64(draw_u64(base0, rec.key + C_SLOT * (uint64_t)(slot + 1)),
+                                 (uint64_t)deg);
+      if (deg <= (int64_t)REG_K * sw) {
+        // the row in the sub-warp's registers: lane r holds entries r, r+sw, ...
+        int32_t c[REG_K];
+#pragma unroll
+        for (int j = 0; j < REG_K; j++) {
+          const int64_t x = r + (int64_t)j * sw;
+          c[j] = x < deg ? __ldg(gv.col + lo + x) : -1;
+        }
+        const int src = leader + (int)(k % (uint64_t)sw);
+        const int kj = (int)(k / (uint64_t)sw);
+#pragma unroll
+        for (int j = 0; j < REG_K; j++) {
+          const int32_t x = __shfl_sync(peers, c[j], src);
+          if (j == kj) o = x;
+        }
+      } else {
+        o = __ldg(gv.col + lo + (int64_t)k);
+      }
+    }
+    out[(uint64_t)rec.ip * m.d + slot] = o;
+  }
+  flush_stats(st, ctr);
+}
+
+__device__ __forceinline__ bool hub_stage(int64_t deg, int64_t items, int64_t slice) {
+  // stage when the copy costs less than the picks' random sectors (8 entries each)
+  return deg > 0 && deg + 8 <= slice && deg <= 8 * items;
+}
+
+// warp tier: one warp per hub with work <= HUB_WARP_MAX, two bulk-copy stages
+// per warp (the next hub's row lands while this one is sampled)
+__global__ void __launch_bounds__(IND_BLOCK) k_fx_hub_warp(FxHub h) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(dsm) + 2 * wib;
+  int32_t* buf0 = reinterpret_cast<int32_t*>(dsm + 16 * (IND_BLOCK / 32)) +
+                  (size_t)wib * 2 * (HUB_SLICE_W + 8);
+  if (lane == 0) {
+    mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
+    mbar_fence_init();
+  }
+  __syncwarp();
+  ItemStats st;
+  const int64_t H = *h.nhub;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint32_t m = h.m.d;
+  uint32_t ph = 0;  // bit b: parity of stage b's next phase
+  // hub j's descriptor (warp-uniform); staged when in the warp tier and worth it
+  auto desc = [&](int64_t j, int64_t& lo, int64_t& deg, int32_t& start, int32_t& work,
+                  bool& staged, int b) {
+    const int32_t v = h.hubs[j];
+    lo = __ldg(h.gv.row + v);
+    deg = __ldg(h.gv.row + v + 1) - lo;
+    start = h.hoff[j];
+    const int64_t w = (int64_t)(h.hoff[j + 1] - start) * m;
+    work = w <= HUB_WARP_MAX ? (int32_t)w : 0;  // larger hubs: the CTA tiers
+    staged = work > 0 && hub_stage(deg, work, HUB_SLICE_W);
+    if (staged && lane == 0)
+      stage_row_bulk(buf0 + b * (HUB_SLICE_W + 8), h.gv.col, row_span(lo, deg), bar + b);
+  };
+  int64_t lo = 0, deg = 0;
+  int32_t start = 0, work = 0;
+  bool staged = false;
+  if (w0 < H) desc(w0, lo, deg, start, work, staged, 0);
+  int it = 0;
+  for (int64_t j = w0; j < H; j += nw, it++) {
+    const int b = it & 1;
+    int64_t nlo = 0, ndeg = 0;
+    int32_t nstart = 0, nwork = 0;
+    bool nstaged = false;
+    if (j + nw < H) desc(j + nw, nlo, ndeg, nstart, nwork, nstaged, b ^ 1);  // prefetch
+    if (work > 0) {
+      const int32_t* srow = nullptr;
+      if (staged) {
+        mbar_wait(bar + b, (ph >> b) & 1u);
+        ph ^= 1u << b;
+        srow = buf0 + b * (HUB_SLICE_W + 8) + row_span(lo, deg).skew;
+      }
+      const ModU64 md((uint64_t)(deg > 0 ? deg : 1));
+      if (lane == 0) st.bytes += fx_range_bytes(0, work, m, deg);
+      for (int32_t tb = 0; tb < work; tb += 32 * FX_ILP) {
+        MemRec r[FX_ILP];
+        uint32_t slot[FX_ILP];
+#pragma unroll
+        for (int q = 0; q < FX_ILP; q++) {
+          const int32_t t = min(tb + q * 32 + lane, work - 1);
+          const uint32_t mem = h.m.div((uint32_t)t);
+          slot[q] = (uint32_t)t - mem * m;
+          r[q] = h.perm[start + mem];
+        }
+        int32_t o[FX_ILP];
+#pragma unroll
+        for (int q = 0; q < FX_ILP; q++) o[q] = fx_pick(h.base0, r[q], slot[q], md, deg, srow, h.gv.col, lo);
+#pragma unroll
+        for (int q = 0; q < FX_ILP; q++)
+          if (tb + q * 32 + lane < work) h.out[r[q].ip * m + slot[q]] = o[q];
+      }
+    }
+    __syncwarp();
+    lo = nlo; deg = ndeg; start = nstart; work = nwork; staged = nstaged;
+  }
+  flush_stats(st, h.ctr);
+}
+
+// thread-block tier (a hub's items in one CTA) and grid tier (a hub above
+// HUB_UNIT items split over several CTAs), one CTA per unit of the unit
+// list, warp-specialised: the producer warp walks the CTA's units ahead of the
+// consumers and stages, by bulk copies into a ring of HUB_STAGES shared-memory
+// stages, the unit's row (when it fits and pays) and its slice of the member
+// records (full barrier: the bytes landed; empty barrier: every consumer warp
+// is done with the stage).  The eight consumer warps sample, FX_ILP items per
+// thread in flight.
+constexpr int HUB_STAGES = 4;
+constexpr int HUB_STAGE_MEMS = 0;  // stage the unit's member records too (1) or read them through L1 (0)
+constexpr int HUB_CONSUMERS = IND_BLOCK / 32;
+constexpr size_t HUB_STAGE_BYTES = (size_t)(HUB_SLICE_C + 8) * 4 + (size_t)HUB_MEM_SLICE * 16 * HUB_STAGE_MEMS;
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+struct HubStage {
+  HubUnit d;
+  int32_t rskew;  // row entry 0 in the row buffer, or -1 (not staged)
+  int32_t mstg;   // member records staged (from member t0/m)
+  int32_t m0;     // first member of the unit
+};
+
+// the consumer loop of one unit: Q items per thread in flight
+template <int Q, bool SREC, bool SROW>
+__device__ __forceinline__ void hub_items(const FxHub& h, const MemRec* __restrict__ recs,
+                                          const int32_t* __restrict__ srow, int32_t t0, int32_t t1,
+                                          int warp, int lane, const ModU64& md, int64_t deg,
+                                          int64_t lo) {
+  const uint32_t m = h.m.d;
+  for (int32_t tb = t0 + warp * 32 * Q; tb < t1; tb += IND_BLOCK * Q) {
+    MemRec r[Q];
+    uint32_t slot[Q];
+#pragma unroll
+    for (int q = 0; q < Q; q++) {
+      const int32_t t = min(tb + q * 32 + lane, t1 - 1);
+      const uint32_t mem = h.m.div((uint32_t)t);
+      slot[q] = (uint32_t)t - mem * m;
+      if (SREC) {
+        r[q] = recs[mem];
+      } else {
+        const int4 x = __ldg(reinterpret_cast<const int4*>(recs + mem));
+        r[q].ip = (uint32_t)x.x;
+        r[q].key = (uint64_t)(uint32_t)x.z | ((uint64_t)(uint32_t)x.w << 32);
+      }
+    }
+    int32_t o[Q];
+#pragma unroll
+    for (int q = 0; q < Q; q++) {
+      if (deg <= 0) { o[q] = -1; continue; }
+      const uint64_t k = md.mod(draw_u64(h.base0, r[q].key + C_SLOT * (uint64_t)(slot[q] + 1)));
+      o[q] = SROW ? srow[k] : __ldg(h.gv.col + lo + (int64_t)k);
+    }
+#pragma unroll
+    for (int q = 0; q < Q; q++)
+      if (tb + q * 32 + lane < t1) h.out[r[q].ip * m + slot[q]] = o[q];
+  }
+}
+
+template <int Q>
+__global__ void __launch_bounds__(IND_BLOCK + 32, 4) k_fx_hub_cta(FxHub h) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  __shared__ HubStage sd[HUB_STAGES];
+  uint64_t* full = reinterpret_cast<uint64_t*>(dsm);
+  uint64_t* empty = full + HUB_STAGES;
+  unsigned char* stage0 = dsm + 16 * HUB_STAGES;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < HUB_STAGES; k++) {
+      mbar_init(full + k, 1);
+      mbar_init(empty + k, HUB_CONSUMERS);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const int64_t U = h.uoff[h.cap];
+  const uint32_t m = h.m.d;
+  if (warp == HUB_CONSUMERS) {  // producer
+    if (lane == 0) {
+      int it = 0;
+      for (int64_t u = blockIdx.x; u < U; u += gridDim.x, it++) {
+        const int sg = it % HUB_STAGES, use = it / HUB_STAGES;
+        if (use > 0) mbar_wait(empty + sg, (use - 1) & 1);
+        HubStage g;
+        g.d = h.units[u];
+        int32_t* rbuf = reinterpret_cast<int32_t*>(stage0 + sg * HUB_STAGE_BYTES);
+        MemRec* mbuf = reinterpret_cast<MemRec*>(rbuf + HUB_SLICE_C + 8);
+        const bool stg = hub_stage(g.d.deg, g.d.t1 - g.d.t0, HUB_SLICE_C);
+        g.m0 = g.d.t0 / (int32_t)m;
+        const int32_t nm = (g.d.t1 - 1) / (int32_t)m + 1 - g.m0;
+        g.mstg = HUB_STAGE_MEMS && nm <= HUB_MEM_SLICE;
+        const RowSpan rs = row_span(g.d.lo, g.d.deg);
+        g.rskew = stg ? (int32_t)rs.skew : -1;
+        sd[sg] = g;
+        const uint32_t bytes = (stg ? rs.n * 4u : 0u) + (g.mstg ? (uint32_t)nm * 16u : 0u);
+        if (bytes) {
+          mbar_arrive_expect_tx(full + sg, bytes);
+          if (stg) bulk_g2s(rbuf, h.gv.col + rs.a, rs.n * 4u, full + sg);
+          if (g.mstg) bulk_g2s(mbuf, h.perm + g.d.start + g.m0, (uint32_t)nm * 16u, full + sg);
+        } else {
+          mbar_arrive(full + sg);
+        }
+      }
+    }
+    return;
+  }
+  ItemStats st;
+  int it = 0;
+  for (int64_t u = blockIdx.x; u < U; u += gridDim.x, it++) {
+    const int sg = it % HUB_STAGES, use = it / HUB_STAGES;
+    mbar_wait(full + sg, use & 1);
+    const HubStage g = sd[sg];
+    const int32_t* rbuf = reinterpret_cast<const int32_t*>(stage0 + sg * HUB_STAGE_BYTES);
+    const MemRec* mbuf = reinterpret_cast<const MemRec*>(rbuf + HUB_SLICE_C + 8);
+    const int32_t* srow = g.rskew >= 0 ? rbuf + g.rskew : nullptr;
+    const int64_t lo = g.d.lo, deg = g.d.deg;
+    const ModU64 md((uint64_t)(deg > 0 ? deg : 1));
+    if (threadIdx.x == 0) st.bytes += fx_range_bytes(g.d.t0, g.d.t1, m, deg);
+    // member records from the stage (shared) or from global memory; the row
+    // from the stage or global: four specialised loops keep every load typed
+    if (g.mstg) {
+      const MemRec* recs = mbuf - g.m0;
+      if (srow) hub_items<Q, true, true>(h, recs, srow, g.d.t0, g.d.t1, warp, lane, md, deg, lo);
+      else hub_items<Q, true, false>(h, recs, srow, g.d.t0, g.d.t1, warp, lane, md, deg, lo);
+    } else {
+      const MemRec* recs = h.perm + g.d.start;
+      if (srow) hub_items<Q, false, true>(h, recs, srow, g.d.t0, g.d.t1, warp, lane, md, deg, lo);
+      else hub_items<Q, false, false>(h, recs, srow, g.d.t0, g.d.t1, warp, lane, md, deg, lo);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + sg);
+  }
+  flush_stats(st, h.ctr);
+}
+
+constexpr size_t HUB_WARP_SMEM = 16 * (IND_BLOCK / 32) + (size_t)(IND_BLOCK / 32) * 2 * (HUB_SLICE_W + 8) * 4;
+constexpr size_t HUB_CTA_SMEM = 16 * HUB_STAGES + HUB_STAGES * HUB_STAGE_BYTES;
+
 // per sample (one warp): non-NULL slots of one step block, added to cnt[i]
 __global__ void k_fx_block_counts(const int32_t* __restrict__ blk, int64_t n, int64_t B,
                                   unsigned long long* __restrict__ cnt) {
@@ -579,6 +1235,42 @@ __global__ void k_fx_narrow_roots(const int64_t* __restrict__ in, int64_t n, int
     out[i] = (int32_t)in[i];
 }
 
+// launch knobs of the TP fixed-layout kernels (ND_FX_KNOBS="rc,pl,hc,rc_grid,pl_grid,hc_grid,
+// hw_grid": ILP of the rank/count, placement and CTA-tier kernels and grid sizes; for
+// ablations only, the defaults are the measured best)
+struct FxKnobs {
+  int rc = 4, pl = 4, hc = 4;
+  int rc_grid = 148 * 32, pl_grid = 148 * 16, hc_grid = 148 * 4, hw_grid = 148 * 6;
+};
+static FxKnobs fx_knobs() {
+  static FxKnobs k = [] {
+    FxKnobs x;
+    if (const char* e = getenv("ND_FX_KNOBS"))
+      sscanf(e, "%d,%d,%d,%d,%d,%d,%d", &x.rc, &x.pl, &x.hc, &x.rc_grid, &x.pl_grid, &x.hc_grid,
+             &x.hw_grid);
+    return x;
+  }();
+  return k;
+}
+
+// dynamic shared memory above 48 KB for the hub kernels (once per process)
+static int fx_hub_attrs() {
+  static int rc = -1;
+  if (rc < 0) {
+    rc = ND_OK;
+    if (cudaFuncSetAttribute(k_fx_hub_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)HUB_WARP_SMEM) != cudaSuccess ||
+        cudaFuncSetAttribute(k_fx_hub_cta<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)HUB_CTA_SMEM) != cudaSuccess ||
+        cudaFuncSetAttribute(k_fx_hub_cta<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)HUB_CTA_SMEM) != cudaSuccess ||
+        cudaFuncSetAttribute(k_fx_hub_cta<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)HUB_CTA_SMEM) != cudaSuccess)
+      rc = ND_ERR_CUDA;
+  }
+  return rc;
+}
+
 // fixed-layout SP run (see k_fx_*); returns ND_ERR_ARG when the layout does not apply
 static int run_individual_fixed(const nd_graph* G, const NdApp& a, const int64_t* fan, int64_t S,
                                 int64_t sample_lo, int64_t n, const int64_t* roots, int64_t R,
@@ -617,6 +1309,15 @@ static int run_individual_fixed(const nd_graph* G, const NdApp& a, const int64_t
   ND_CUDA_TRY(nd_alloc(&scnt, n, s));
   ND_CUDA_TRY(cudaMemsetAsync(scnt, 0, n * sizeof(unsigned long long), s));
   const GView<int32_t> gv = view(g);
+  static const bool sort_tp = getenv("ND_FX_TP") && std::string(getenv("ND_FX_TP")) == "sort";
+  const FxKnobs knob = fx_knobs();
+  int2* vinfo = nullptr;  // TP: per-vertex {member count, hub index}
+  int32_t* nhub = nullptr;
+  if (tp && !sort_tp) {
+    ND_TRY(fx_hub_attrs());
+    ND_CUDA_TRY(nd_alloc(&vinfo, g.V, s));
+    ND_CUDA_TRY(nd_alloc(&nhub, 2, s));  // [0] hubs, [1] small parents
+  }
   for (int64_t k = 0; k < S; k++) {
     ND_CUDA_TRY(nd_alloc(&rank[k], n * B[k], s));
     ND_CUDA_TRY(nd_alloc(&nn[k], n, s));
@@ -630,29 +1331,87 @@ static int run_individual_fixed(const nd_graph* G, const NdApp& a, const int64_t
           FastDiv((uint32_t)fan[k]), blk[k], rank[k], blk[k + 1], scnt, stall, ctr);
       continue;
     }
-    // transit-parallel order: sort the parent slots by transit, classify the groups
-    k_fx_rank<<<nd_grid(n * 32, 256, 148 * 32), 256, 0, s>>>(blk[k], n, B[k], rank[k], nn[k],
-                                                            tp_scratch);
-    const int64_t N = n * B[k];
-    uint32_t *k0 = nullptr, *k1 = nullptr;
-    uint64_t *v0 = nullptr, *v1 = nullptr;
-    ND_CUDA_TRY(nd_alloc(&k0, N, s)); ND_CUDA_TRY(nd_alloc(&k1, N, s));
-    ND_CUDA_TRY(nd_alloc(&v0, N, s)); ND_CUDA_TRY(nd_alloc(&v1, N, s));
-    k_fx_keys<<<nd_grid(N, 256), 256, 0, s>>>(blk[k], rank[k], N, sentinel, k0, v0);
-    {
-      size_t tb = 0;
-      cub::DeviceRadixSort::SortPairs(nullptr, tb, k0, k1, v0, v1, N, 0, kbits + 1, s);
-      void* tmp = nullptr;
-      ND_CUDA_TRY(nd_alloc((char**)&tmp, tb, s));
-      ND_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, tb, k0, k1, v0, v1, N, 0, kbits + 1, s));
-      nd_free(tmp, s);
+    if (sort_tp) {  // ND_FX_TP=sort: the round-1 radix-sorted order (A/B only)
+      k_fx_rank<<<nd_grid(n * 32, 256, 148 * 32), 256, 0, s>>>(blk[k], n, B[k], rank[k], nn[k],
+                                                              tp_scratch);
+      const int64_t N = n * B[k];
+      uint32_t *k0 = nullptr, *k1 = nullptr;
+      uint64_t *v0 = nullptr, *v1 = nullptr;
+      ND_CUDA_TRY(nd_alloc(&k0, N, s)); ND_CUDA_TRY(nd_alloc(&k1, N, s));
+      ND_CUDA_TRY(nd_alloc(&v0, N, s)); ND_CUDA_TRY(nd_alloc(&v1, N, s));
+      k_fx_keys<<<nd_grid(N, 256), 256, 0, s>>>(blk[k], rank[k], N, sentinel, k0, v0);
+      {
+        size_t tb = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, tb, k0, k1, v0, v1, N, 0, kbits + 1, s);
+        void* tmp = nullptr;
+        ND_CUDA_TRY(nd_alloc((char**)&tmp, tb, s));
+        ND_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, tb, k0, k1, v0, v1, N, 0, kbits + 1, s));
+        nd_free(tmp, s);
+      }
+      k_fx_classes<<<nd_grid(N, 256, 148 * 16), 256, 0, s>>>(k1, N, sentinel, fan[k], stats + 4 * k);
+      k_fx_sample_tp<<<nd_grid(items, IND_BLOCK, 148 * 64), IND_BLOCK, 0, s>>>(
+          gv, a, key_base(seed, (uint64_t)k, 0, 0), sample_lo, N, FastDiv((uint32_t)B[k]),
+          FastDiv((uint32_t)fan[k]), sentinel, k1, v1, blk[k + 1], stall, ctr);
+      k_fx_block_counts<<<nd_grid(n * 32, 256, 148 * 32), 256, 0, s>>>(blk[k + 1], n, B[k + 1], scnt);
+      nd_free(k0, s); nd_free(k1, s); nd_free(v0, s); nd_free(v1, s);
+      continue;
     }
-    k_fx_classes<<<nd_grid(N, 256, 148 * 16), 256, 0, s>>>(k1, N, sentinel, fan[k], stats + 4 * k);
-    k_fx_sample_tp<<<nd_grid(items, IND_BLOCK, 148 * 64), IND_BLOCK, 0, s>>>(
-        gv, a, key_base(seed, (uint64_t)k, 0, 0), sample_lo, N, FastDiv((uint32_t)B[k]),
-        FastDiv((uint32_t)fan[k]), sentinel, k1, v1, blk[k + 1], stall, ctr);
-    k_fx_block_counts<<<nd_grid(n * 32, 256, 148 * 32), 256, 0, s>>>(blk[k + 1], n, B[k + 1], scnt);
-    nd_free(k0, s); nd_free(k1, s); nd_free(v0, s); nd_free(v1, s);
+    // transit-parallel order: hub-bucket inversion, small class by sub-warps,
+    // hubs in the warp / thread-block / grid tiers
+    {
+      const int64_t N = n * B[k];
+      const HubThr th = hub_thresholds(fan[k]);
+      const int64_t cap = th.tm >= 0x7fffffff ? 1 : N / th.tm + 1;
+      const int64_t ucap = cap + N * fan[k] / HUB_UNIT + 1;
+      int32_t *gpos = nullptr, *hubs = nullptr, *hsz = nullptr, *hun = nullptr, *hoff = nullptr,
+              *uoff = nullptr;
+      MemRec *perm = nullptr, *small = nullptr;
+      HubUnit* units = nullptr;
+      ND_CUDA_TRY(nd_alloc(&gpos, N, s));
+      ND_CUDA_TRY(nd_alloc(&hubs, cap, s));
+      ND_CUDA_TRY(nd_alloc(&hsz, cap + 1, s));
+      ND_CUDA_TRY(nd_alloc(&hun, cap + 1, s));
+      ND_CUDA_TRY(nd_alloc(&hoff, cap + 1, s));
+      ND_CUDA_TRY(nd_alloc(&uoff, cap + 1, s));
+      ND_CUDA_TRY(nd_alloc(&units, ucap, s));
+      ND_CUDA_TRY(nd_alloc(&perm, N, s));
+      ND_CUDA_TRY(nd_alloc(&small, N, s));
+      ND_CUDA_TRY(cudaMemsetAsync(vinfo, 0, g.V * sizeof(int2), s));
+      ND_CUDA_TRY(cudaMemsetAsync(nhub, 0, 2 * sizeof(int32_t), s));
+      {
+        auto krc = knob.rc == 1 ? k_fx_rank_count<1> : knob.rc == 2 ? k_fx_rank_count<2>
+                                                                    : k_fx_rank_count<4>;
+        krc<<<nd_grid(n * 32, 256, knob.rc_grid), 256, 0, s>>>(blk[k], n, B[k], rank[k], nn[k], vinfo,
+                                                              gpos, hubs, nhub, th, stats + 4 * k);
+      }
+      k_hub_sizes<<<nd_grid(cap + 1, 256), 256, 0, s>>>(hubs, nhub, cap, vinfo, fan[k], hsz, hun);
+      {
+        size_t tb = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, tb, hsz, hoff, cap + 1, s);
+        void* tmp = nullptr;
+        ND_CUDA_TRY(nd_alloc((char**)&tmp, tb, s));
+        ND_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tb, hsz, hoff, cap + 1, s));
+        ND_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tb, hun, uoff, cap + 1, s));
+        nd_free(tmp, s);
+      }
+      k_hub_units<<<nd_grid(cap, 256), 256, 0, s>>>(nhub, hubs, hoff, uoff, hun, g.row, fan[k],
+                                                   units);
+      const FastDiv fB((uint32_t)B[k]), fm((uint32_t)fan[k]);
+      auto kpl = knob.pl == 1 ? k_fx_place<1> : knob.pl == 2 ? k_fx_place<2> : k_fx_place<4>;
+      kpl<<<nd_grid(N, 256 * knob.pl, knob.pl_grid), 256, 0, s>>>(
+          blk[k], rank[k], N, fB, fan[k], sample_lo, g.row, vinfo, th.tm, gpos, hoff, perm, small,
+          nhub + 1, blk[k + 1], scnt);
+      const uint64_t b0 = key_base(seed, (uint64_t)k, 0, 0);
+      k_fx_small<<<nd_grid(items, IND_BLOCK, 148 * 16), IND_BLOCK, 0, s>>>(
+          gv, b0, fm, blk[k], small, nhub + 1, blk[k + 1], ctr);
+      FxHub hb{gv, b0, fm, hubs, nhub, hoff, uoff, cap, units, perm, blk[k + 1], ctr};
+      k_fx_hub_warp<<<knob.hw_grid, IND_BLOCK, HUB_WARP_SMEM, s>>>(hb);
+      auto kh = knob.hc == 1 ? k_fx_hub_cta<1> : knob.hc == 2 ? k_fx_hub_cta<2> : k_fx_hub_cta<4>;
+      kh<<<knob.hc_grid, IND_BLOCK + 32, HUB_CTA_SMEM, s>>>(hb);
+      ND_CUDA_TRY(cudaGetLastError());
+      nd_free(gpos, s); nd_free(hubs, s); nd_free(hsz, s); nd_free(hun, s); nd_free(hoff, s);
+      nd_free(uoff, s); nd_free(units, s); nd_free(perm, s); nd_free(small, s);
+    }
   }
   // final rows and step rows: counts, scans, one synchronisation for the totals
   FxSteps FS;
@@ -702,6 +1461,7 @@ static int run_individual_fixed(const nd_graph* G, const NdApp& a, const int64_t
   ND_CUDA_TRY(cudaGetLastError());
   for (int64_t k = 0; k < S; k++) nd_free(nn[k], s);
   nd_free(flen, s); nd_free(scnt, s); nd_free(ctr, s); nd_free(stall, s); nd_free(tp_scratch, s);
+  nd_free(vinfo, s); nd_free(nhub, s);
   // step rows (F_STEP_VALS32) are built on first request from the blocks and
   // ranks, which the result keeps until then
   std::vector<int32_t*> kb(blk, blk + S + 1), kr(rank, rank + S);
