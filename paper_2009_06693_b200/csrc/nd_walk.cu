@@ -327,12 +327,36 @@ struct NextHdr {
   double tot = -1.0;
 };
 
-__device__ __forceinline__ int64_t rec_pick(const PWArgs& A, int64_t lo, int64_t deg, double tot,
-                                            double u01, NextHdr& nh, ItemStats& st) {
-  if (A.nbu != nullptr) {  // unit weights: floor identity
+// 32-byte record / 16-byte loads from global memory (read-only path) or from
+// a row staged in shared memory (SH) by the transit-parallel hub kernels
+template <bool SH>
+__device__ __forceinline__ void ldrec32(const void* p, int4& a, int4& b) {
+  if (SH) {
+    a = reinterpret_cast<const int4*>(p)[0];
+    b = reinterpret_cast<const int4*>(p)[1];
+  } else {
+    ld32B(p, a, b);
+  }
+}
+template <bool SH>
+__device__ __forceinline__ int4 ldrec16(const void* p) {
+  return SH ? *reinterpret_cast<const int4*>(p) : __ldg(reinterpret_cast<const int4*>(p));
+}
+template <bool SH>
+__device__ __forceinline__ double ldf64(const double* p) {
+  return SH ? *p : __ldg(p);
+}
+
+// weighted pick over a row's neighbour records rp[0, deg) (or unit records
+// ru); gd = the row's guide table (global) or null
+template <bool SH>
+__device__ __forceinline__ int64_t rec_pick_at(const NbrP* rp, const NbrU* ru, const int32_t* gd0,
+                                               int64_t deg, double tot, double u01, NextHdr& nh,
+                                               ItemStats& st) {
+  if (ru != nullptr) {  // unit weights: floor identity
     int64_t k = (int64_t)__dmul_rn(u01, (double)deg);
     if (k > deg - 1) k = deg - 1;
-    const int4 r = __ldg(reinterpret_cast<const int4*>(A.nbu + lo + k));
+    const int4 r = ldrec16<SH>(ru + k);
     nh.deg = r.y;
     nh.lo = (int64_t)(((uint64_t)(uint32_t)r.w << 32) | (uint32_t)r.z);
     nh.mx = nh.deg > 0 ? 1.0 : 0.0;
@@ -341,13 +365,12 @@ __device__ __forceinline__ int64_t rec_pick(const PWArgs& A, int64_t lo, int64_t
     st.sect += 1;
     return r.x;
   }
-  const NbrP* rp = A.nbp + lo;
   const double x = __dmul_rn(u01, tot);
   int64_t a = 0, b = deg;
-  if (A.gv.guide != nullptr && deg > GUIDE_MIN_DEG) {
+  if (gd0 != nullptr && deg > GUIDE_MIN_DEG) {
     const int64_t j = guide_bucket(x, tot, deg);
     if (j >= 0) {  // guide[j], guide[j+1]: adjacent, one sector unless they straddle
-      const int32_t* gd = A.gv.guide + lo + j;
+      const int32_t* gd = gd0 + j;
       a = __ldg(gd);
       b = j + 1 < deg ? (int64_t)__ldg(gd + 1) : deg;
       st.sect += 1 + (j + 1 < deg && (reinterpret_cast<uintptr_t>(gd) >> 5) !=
@@ -361,7 +384,7 @@ __device__ __forceinline__ int64_t rec_pick(const PWArgs& A, int64_t lo, int64_t
   while (a < b) {
     const int64_t mid = (a + b) >> 1;
     int4 q0, q1;
-    ld32B(rp + mid, q0, q1);
+    ldrec32<SH>(rp + mid, q0, q1);
     st.sect += 1;
     const double pre = __longlong_as_double(((long long)(uint32_t)q0.y << 32) | (uint32_t)q0.x);
     if (pre <= x) {
@@ -375,7 +398,7 @@ __device__ __forceinline__ int64_t rec_pick(const PWArgs& A, int64_t lo, int64_t
   }
   const int64_t k = a < deg - 1 ? a : deg - 1;
   if (k != have) {
-    ld32B(rp + k, h0, h1);
+    ldrec32<SH>(rp + k, h0, h1);
     st.sect += 1;
   }
   nh.deg = h0.w;
@@ -386,19 +409,25 @@ __device__ __forceinline__ int64_t rec_pick(const PWArgs& A, int64_t lo, int64_t
   return h0.z;
 }
 
+__device__ __forceinline__ int64_t rec_pick(const PWArgs& A, int64_t lo, int64_t deg, double tot,
+                                            double u01, NextHdr& nh, ItemStats& st) {
+  return rec_pick_at<false>(A.nbu ? nullptr : A.nbp + lo, A.nbu ? A.nbu + lo : nullptr,
+                            A.gv.guide ? A.gv.guide + lo : nullptr, deg, tot, u01, nh, st);
+}
+
 // weighted pick over the line-packed rows (PickLine, nd_common.cuh): the
 // exact bucket's bracket guide[j], guide[j+1] sits in the line of bucket j,
 // next to the records around j (the upper-bound probes and the selected
-// record are usually sectors of that same line).
-__device__ __forceinline__ int64_t line_pick(const PWArgs& A, int64_t llo, int64_t deg, double tot,
-                                             double u01, NextHdr& nh, ItemStats& st) {
-  const PickLine* L = A.pl + llo;
+// record are usually sectors of that same line).  L = the row's first line.
+template <bool SH>
+__device__ __forceinline__ int64_t line_pick_at(const PickLine* L, int64_t deg, double tot,
+                                                double u01, NextHdr& nh, ItemStats& st) {
   const double x = __dmul_rn(u01, tot);
   int64_t a = 0, b = deg;
   const int64_t j = guide_bucket(x, tot, deg);
   int64_t line = -1;
   if (j >= 0) {
-    const int4 g = __ldg(reinterpret_cast<const int4*>(L[j / 3].g));  // 16-byte aligned
+    const int4 g = ldrec16<SH>(L[j / 3].g);  // 16-byte aligned
     const int sidx = (int)(j % 3);
     a = sidx == 0 ? g.x : sidx == 1 ? g.y : g.z;
     b = sidx == 0 ? g.y : sidx == 1 ? g.z : g.w;
@@ -408,12 +437,12 @@ __device__ __forceinline__ int64_t line_pick(const PWArgs& A, int64_t llo, int64
   while (a < b) {
     const int64_t mid = (a + b) >> 1;
     if (mid / 3 != line) { line = mid / 3; st.sect += 1; }
-    if (__ldg(&L[mid / 3].r[mid % 3].pre) <= x) a = mid + 1; else b = mid;
+    if (ldf64<SH>(&L[mid / 3].r[mid % 3].pre) <= x) a = mid + 1; else b = mid;
   }
   const int64_t k = a < deg - 1 ? a : deg - 1;
   if (k / 3 != line) st.sect += 1;
   int4 h0, h1;
-  ld32B(&L[k / 3].r[k % 3], h0, h1);
+  ldrec32<SH>(&L[k / 3].r[k % 3], h0, h1);
   nh.tot = __longlong_as_double(((long long)(uint32_t)h0.w << 32) | (uint32_t)h0.z);
   nh.deg = h1.y;
   nh.lo = h1.z;
@@ -422,16 +451,24 @@ __device__ __forceinline__ int64_t line_pick(const PWArgs& A, int64_t llo, int64
   return h1.x;
 }
 
-// one node2vec rejection try over the neighbour records; -2 = rejected
-__device__ __forceinline__ int64_t rec_try(const PWArgs& A, int64_t lo, int64_t deg, int64_t t,
-                                           int64_t tlo, int64_t thi, double env, uint64_t b,
-                                           uint64_t ik, NextHdr& nh, ItemStats& st) {
+__device__ __forceinline__ int64_t line_pick(const PWArgs& A, int64_t llo, int64_t deg, double tot,
+                                             double u01, NextHdr& nh, ItemStats& st) {
+  return line_pick_at<false>(A.pl + llo, deg, tot, u01, nh, st);
+}
+
+// one node2vec rejection try over the row's neighbour records rw (or unit
+// records ru); -2 = rejected
+template <bool SH>
+__device__ __forceinline__ int64_t rec_try_at(const PWArgs& A, const NbrW* rw, const NbrU* ru,
+                                              int64_t deg, int64_t t, int64_t tlo, int64_t thi,
+                                              double env, uint64_t b, uint64_t ik, NextHdr& nh,
+                                              ItemStats& st) {
   const int64_t k = (int64_t)mod_u64(draw_u64(b, ik), (uint64_t)deg);
   int64_t nb;
   double w;
   st.sect += 1;
-  if (A.nbu != nullptr) {
-    const int4 r = __ldg(reinterpret_cast<const int4*>(A.nbu + lo + k));
+  if (ru != nullptr) {
+    const int4 r = ldrec16<SH>(ru + k);
     nb = r.x;
     w = 1.0;
     nh.deg = r.y;
@@ -439,7 +476,7 @@ __device__ __forceinline__ int64_t rec_try(const PWArgs& A, int64_t lo, int64_t 
     nh.mx = nh.deg > 0 ? 1.0 : 0.0;
   } else {
     int4 r0, r1;
-    ld32B(A.nbw + lo + k, r0, r1);  // the whole record in one 32-byte request
+    ldrec32<SH>(rw + k, r0, r1);  // the whole record in one 32-byte request
     nb = r0.x;
     nh.deg = r0.y;
     nh.lo = (int64_t)(((uint64_t)(uint32_t)r0.w << 32) | (uint32_t)r0.z);
@@ -448,6 +485,13 @@ __device__ __forceinline__ int64_t rec_try(const PWArgs& A, int64_t lo, int64_t 
   }
   nh.tot = -1.0;
   return n2v_decide(A, nb, w, t, tlo, thi, env, b, ik, st);
+}
+
+__device__ __forceinline__ int64_t rec_try(const PWArgs& A, int64_t lo, int64_t deg, int64_t t,
+                                           int64_t tlo, int64_t thi, double env, uint64_t b,
+                                           uint64_t ik, NextHdr& nh, ItemStats& st) {
+  return rec_try_at<false>(A, A.nbu ? nullptr : A.nbw + lo, A.nbu ? A.nbu + lo : nullptr, deg, t,
+                           tlo, thi, env, b, ik, nh, st);
 }
 
 
@@ -707,7 +751,7 @@ __global__ void k_tail_rows(const int32_t* __restrict__ wid, const int32_t* __re
        r += (int64_t)gridDim.x * blockDim.x) {
     int64_t e = nnz[r];
     if (e < Lw) {
-      dstep[wid[r]] = (int32_t)(step0 + e);
+      if (dstep) dstep[wid[r]] = (int32_t)(step0 + e);
       e += 1;
     }
     ent[r] = e;
@@ -768,7 +812,9 @@ static int run_tp_tail(const nd_graph* G, const NdApp& a, uint64_t seed, int64_t
                        int64_t step, int64_t limit, int64_t Lw_base, int key_bits, int32_t* dstep,
                        int* stall, unsigned long long* ctr, unsigned long long* stats,
                        cudaStream_t s, std::vector<PWindow>& wins, int64_t& n_steps,
-                       int64_t& items, double& sample_ms);
+                       int64_t& items, double& sample_ms, int32_t* wid_in = nullptr,
+                       int32_t* v_in = nullptr, int32_t* t_in = nullptr,
+                       int32_t* died_ext = nullptr);
 
 // TP chain walk (SP chain walks run in run_chain_walk_sp).  Byte-model
 // counters (see nd_item.cuh): ctr[0]=bytes, ctr[1]=tries
@@ -1108,17 +1154,25 @@ static int run_tp_tail(const nd_graph* G, const NdApp& a, uint64_t seed, int64_t
                        int64_t step, int64_t limit, int64_t Lw_base, int key_bits, int32_t* dstep,
                        int* stall, unsigned long long* ctr, unsigned long long* stats,
                        cudaStream_t s, std::vector<PWindow>& wins, int64_t& n_steps,
-                       int64_t& items, double& sample_ms) {
+                       int64_t& items, double& sample_ms, int32_t* wid_in,
+                       int32_t* v_in, int32_t* t_in,
+                       int32_t* died_ext) {
   nd_trace("tp:tail-begin");
-  int32_t *wid = nullptr, *v = nullptr, *t = nullptr, *died = nullptr;
+  // inputs: the sort engine's (cur, wp) state, or (wid, v, t) rows handed over
+  // (the windows take ownership of them)
+  int32_t *wid = wid_in, *v = v_in, *t = t_in, *died = died_ext;
   int* ctl = nullptr;
-  ND_CUDA_TRY(nd_alloc(&wid, A, s));
-  ND_CUDA_TRY(nd_alloc(&v, A, s));
-  ND_CUDA_TRY(nd_alloc(&t, A, s));
-  ND_CUDA_TRY(nd_alloc(&died, n, s));
+  if (!cur) {
+    if (!wid || !v || !t) return ND_ERR_ARG;
+  } else {
+    ND_CUDA_TRY(nd_alloc(&wid, A, s));
+    ND_CUDA_TRY(nd_alloc(&v, A, s));
+    ND_CUDA_TRY(nd_alloc(&t, A, s));
+  }
+  if (!died_ext) ND_CUDA_TRY(nd_alloc(&died, n, s));
   ND_CUDA_TRY(nd_alloc(&ctl, 4, s));
   ND_CUDA_TRY(cudaMemsetAsync(ctl, 0, 4 * sizeof(int), s));
-  k_tail_init<<<nd_grid(A, 256), 256, 0, s>>>(cur, wp, A, wid, v, t);
+  if (cur) k_tail_init<<<nd_grid(A, 256), 256, 0, s>>>(cur, wp, A, wid, v, t);
   int* h = reinterpret_cast<int*>(nd_pinned_scratch());
   h[1] = h[2] = h[3] = 0;
   int rc = pw_run_windows(G, a, seed, sample_lo, A, wid, v, t, nullptr, nullptr, R, step, limit,
@@ -1127,7 +1181,7 @@ static int run_tp_tail(const nd_graph* G, const NdApp& a, uint64_t seed, int64_t
     k_or_flag<<<1, 1, 0, s>>>(stall, ctl + 3);
     if ((int64_t)h[2] > n_steps) n_steps = h[2];
   }
-  nd_free(died, s);
+  if (!died_ext) nd_free(died, s);
   nd_free(ctl, s);
   if (rc != ND_OK) return rc;
   nd_trace("tp:tail-windows");
@@ -1460,6 +1514,373 @@ static int run_rootpick_walk(const nd_graph* G, const NdApp& a, int64_t sample_l
   return ND_OK;
 }
 
+#include "nd_bulk.cuh"
+#include "nd_walk_hub.cuh"
+
+// dynamic shared memory above 48 KB for the hub kernels (once per process)
+static int tw_attrs() {
+  static int rc = -1;
+  if (rc < 0) {
+    rc = ND_OK;
+    if (cudaFuncSetAttribute(k_tw_hub_cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)TW_CTA_SMEM) != cudaSuccess ||
+        cudaFuncSetAttribute(k_tw_hub_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)TW_WARP_SMEM) != cudaSuccess)
+      rc = ND_ERR_CUDA;
+  }
+  return rc;
+}
+
+// The hub engine applies when the walker-major records exist (the SP kernel's
+// record paths) and edge offsets fit the 32-bit state.
+static bool tw_applicable(const DevGraph& g, const NdApp& a) {
+  if (getenv("ND_TP_ENGINE") && strcmp(getenv("ND_TP_ENGINE"), "sort") == 0) return false;
+  if (g.E >= (1ll << 32) || !g.vrec) return false;
+  const bool n2v = a.code == ND_NODE2VEC;
+  if (a.code != ND_DEEPWALK && a.code != ND_PPR && !n2v) return false;
+  if (g.unit) return g.nbu != nullptr;
+  return g.nbp != nullptr && (!n2v || g.nbw != nullptr);
+}
+
+// TP chain walk through the hub-bucket inversion (nd_walk_hub.cuh): windows of
+// per-step kernels over the alive walkers' rows; walks still alive at a
+// window's end continue in the next window, and once at most ND_TP_TAIL
+// walkers are alive the rest runs in the walker-major tail (run_tp_tail).
+static int run_chain_walk_hub(const nd_graph* G, const NdApp& a, int64_t sample_lo, int64_t n,
+                              const int64_t* roots, int64_t R, uint64_t seed, int64_t steps,
+                              int64_t step_cap, cudaStream_t s, nd_result* res) {
+  const DevGraph& g = G->g;
+  ND_TRY(tw_attrs());
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  int occ = 4;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tw_sample<4>, TW_BLOCK, 0);
+  if (occ < 1) occ = 1;
+  const int64_t max_steps = steps >= 0 ? (steps < step_cap ? steps : step_cap) : step_cap;
+  const int64_t tail_T = getenv("ND_TP_TAIL") ? atoll(getenv("ND_TP_TAIL")) : 131072;
+  const int key_bits = key_bits_for(g.V);
+  const bool n2v = a.code == ND_NODE2VEC;
+  const int64_t V = g.V;
+  const int64_t hcap = n / TW_TM + 2;                 // hubs per step
+  const int64_t ucap = hcap + n / TW_UNIT + 2;        // CTA units per step
+  int32_t *roots32 = nullptr, *died = nullptr, *maxlen = nullptr, *hoff = nullptr;
+  TwRec* hrec = nullptr;
+  int32_t *pos = nullptr, *slist = nullptr, *cnt = nullptr, *vhub = nullptr, *hubs = nullptr;
+  int32_t *cur[2] = {}, *dg[2] = {};
+  uint32_t* lo[2] = {};
+  double* hd[2] = {};
+  TwCtl* ctl = nullptr;
+  TwUnit *wunits = nullptr, *cunits = nullptr;
+  int64_t* tot = nullptr;
+  unsigned long long *ctr = nullptr, *stats = nullptr;
+  int* stall = nullptr;
+  ND_CUDA_TRY(nd_alloc(&died, n, s));
+  ND_CUDA_TRY(nd_alloc(&tot, n, s));
+  ND_CUDA_TRY(nd_alloc(&maxlen, 1, s));
+  ND_CUDA_TRY(nd_alloc(&stall, 1, s));
+  ND_CUDA_TRY(nd_alloc(&ctr, 4, s));
+  ND_CUDA_TRY(nd_alloc(&stats, 4 * (max_steps + 1), s));
+  ND_CUDA_TRY(nd_alloc(&ctl, 2, s));
+  ND_CUDA_TRY(nd_alloc(&hoff, hcap, s));
+  ND_CUDA_TRY(nd_alloc(&wunits, hcap, s));
+  ND_CUDA_TRY(nd_alloc(&cunits, ucap, s));
+  ND_CUDA_TRY(nd_alloc(&hrec, n, s));
+  ND_CUDA_TRY(nd_alloc(&pos, n, s));
+  ND_CUDA_TRY(nd_alloc(&slist, n, s));
+  ND_CUDA_TRY(nd_alloc(&cnt, V, s));
+  ND_CUDA_TRY(nd_alloc(&vhub, V, s));
+  ND_CUDA_TRY(nd_alloc(&hubs, hcap, s));
+  ND_CUDA_TRY(cudaMemsetAsync(cnt, 0, V * sizeof(int32_t), s));
+  for (int b = 0; b < 2; b++) {
+    ND_CUDA_TRY(nd_alloc(&cur[b], n, s));
+    ND_CUDA_TRY(nd_alloc(&lo[b], n, s));
+    ND_CUDA_TRY(nd_alloc(&dg[b], n, s));
+    ND_CUDA_TRY(nd_alloc(&hd[b], n, s));
+  }
+  ND_CUDA_TRY(cudaMemsetAsync(died, 0, n * sizeof(int32_t), s));
+  ND_CUDA_TRY(cudaMemsetAsync(tot, 0, n * sizeof(int64_t), s));
+  ND_CUDA_TRY(cudaMemsetAsync(maxlen, 0, sizeof(int32_t), s));
+  ND_CUDA_TRY(cudaMemsetAsync(stall, 0, sizeof(int), s));
+  ND_CUDA_TRY(cudaMemsetAsync(ctr, 0, 4 * sizeof(unsigned long long), s));
+  ND_CUDA_TRY(cudaMemsetAsync(stats, 0, 4 * (max_steps + 1) * sizeof(unsigned long long), s));
+  if (!roots) {
+    ND_CUDA_TRY(nd_alloc(&roots32, n * R, s));
+    ND_TRY(nd_uniform_roots_i32(g, R, seed, sample_lo, n, roots32, s));
+  }
+  // The member counts take one random atomic per (tile, transit) and one
+  // random read per walker every step: keep them resident in L2 (persisting
+  // window over cnt) so the walk's record traffic does not evict them.
+  cudaStreamAttrValue l2win{}, l2off{};
+  bool l2set = false;
+  {
+    int max_persist = 0;
+    cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
+    const size_t want = (size_t)V * sizeof(int32_t);
+    if (max_persist > 0 && !getenv("ND_TW_NO_L2PIN")) {
+      size_t lim = 0;
+      cudaDeviceGetLimit(&lim, cudaLimitPersistingL2CacheSize);
+      const size_t setaside = std::min<size_t>((size_t)max_persist, std::max(lim, want));
+      if (lim < setaside) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, setaside);
+      l2win.accessPolicyWindow.base_ptr = cnt;
+      l2win.accessPolicyWindow.num_bytes = want;
+      l2win.accessPolicyWindow.hitRatio = want <= setaside ? 1.0f : (float)setaside / (float)want;
+      l2win.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      l2win.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      l2set = cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &l2win) == cudaSuccess;
+      cudaGetLastError();
+    }
+  }
+
+  PWArgs P{};
+  P.gv = view(g);
+  P.a = a;
+  P.seed = seed;
+  P.sample_lo = sample_lo;
+  P.R = R;
+  P.stall = stall;
+  P.ctr = ctr;
+  P.vrec = g.vrec;
+  P.nbw = g.nbw;
+  P.nbp = g.nbp;
+  P.nbu = g.nbu;
+  P.pl = (a.code == ND_DEEPWALK || a.code == ND_PPR) ? g.pl : nullptr;
+  P.vline = g.vline;
+
+  // bytes per edge of the records a hub's members read (k_tw_prep's rmode)
+  auto rmode = [&](int tries) {
+    if (tries || !P.pl) return g.unit ? 1 : 0;
+    return 2;
+  };
+  int64_t next_Lw = 1;
+  struct TWin {
+    int32_t *wid, *out, *nnz;
+    int64_t rows, step0, Lw;
+  };
+  std::vector<TWin> twins;
+  std::vector<PWindow> tail_wins;
+  int32_t *wid = nullptr, *v0 = nullptr, *t0 = nullptr;
+  int64_t rows = max_steps > 0 ? n : 0, step = 0, n_steps = 0, tail_items = 0;
+  int* h = reinterpret_cast<int*>(nd_pinned_scratch());
+  Profiler prof;
+  prof.on = g_profile;
+  prof.s = s;
+  prof.mark();
+  bool tail = false;
+  int rc = ND_OK;
+  while (rows > 0 && step < max_steps) {
+    if (rows <= tail_T && rows * (max_steps - step) < (1ll << 31)) {
+      tail = true;
+      break;
+    }
+    // windows of 1, 4, 16, 64, 256 steps (32 for walks of unbounded length,
+    // whose alive count falls every step): the alive walkers are compacted
+    // between windows and the tail hand-off is checked there
+    const int64_t Lw = std::min<int64_t>(max_steps - step, next_Lw);
+    next_Lw = std::min<int64_t>(next_Lw * 4, steps >= 0 ? 256 : 32);
+    TWin W{wid, nullptr, nullptr, rows, step, Lw};
+    int32_t *cw = nullptr, *cv = nullptr, *ct = nullptr;
+    int* cont_n = nullptr;
+    ND_CUDA_TRY(nd_alloc(&W.out, Lw * rows, s));
+    ND_CUDA_TRY(nd_alloc(&W.nnz, rows, s));
+    ND_CUDA_TRY(nd_alloc(&cw, rows, s));
+    ND_CUDA_TRY(nd_alloc(&cv, rows, s));
+    ND_CUDA_TRY(nd_alloc(&ct, rows, s));
+    ND_CUDA_TRY(nd_alloc(&cont_n, 1, s));
+    ND_CUDA_TRY(cudaMemsetAsync(cont_n, 0, sizeof(int), s));
+    ND_CUDA_TRY(cudaMemsetAsync(ctl, 0, 2 * sizeof(TwCtl), s));
+    TwArgs A{};
+    A.P = P;
+    A.rows = rows;
+    A.wid = wid;
+    A.Lw = Lw;
+    A.pos = pos;
+    A.out = W.out;
+    A.nnz = W.nnz;
+    A.died = died;
+    A.cont_wid = cw;
+    A.cont_v = cv;
+    A.cont_t = ct;
+    A.cont_n = cont_n;
+    A.max_len = maxlen;
+    A.hoff = hoff;
+    A.hrec = hrec;
+    A.hcap = n;
+    A.cnt = cnt;
+    A.vhub = vhub;
+    A.hubs = hubs;
+    A.wunits = wunits;
+    A.cunits = cunits;
+    A.slist = slist;
+    // window start: state of every row
+    A.s = step;
+    A.cur = cur[0]; A.lo = lo[0]; A.deg = dg[0]; A.hd = hd[0];
+    A.ncur = cur[1]; A.nlo = lo[1]; A.ndeg = dg[1]; A.nhd = hd[1];
+    k_tw_init<<<nd_grid(rows, TW_BLOCK, nsm * 8), TW_BLOCK, 0, s>>>(A, roots, roots32, R, v0, t0);
+    const int gq = nd_grid(rows, TW_TILE, nsm * 8);
+    for (int64_t k = 0; k < Lw; k++) {
+      const int64_t st_ = step + k;
+      const int b = (int)(st_ & 1), pb = b ^ 1;
+      const int in = (int)(k & 1), ou = in ^ 1;
+      A.s = st_;
+      A.k = k;
+      A.last = k == Lw - 1;
+      A.tries = n2v && st_ > 0;
+      A.cur = cur[in]; A.lo = lo[in]; A.deg = dg[in]; A.hd = hd[in];
+      A.ncur = cur[ou]; A.nlo = lo[ou]; A.ndeg = dg[ou]; A.nhd = hd[ou];
+      A.ctl = ctl + b;
+      A.nctl = ctl + pb;
+      A.stats = stats + 4 * st_;
+      A.rmode = rmode(A.tries);
+      {
+        const int64_t thr = (int64_t)nsm * occ * TW_BLOCK;
+        A.P.chunk = rows > 8 * thr ? 128 : rows > 2 * thr ? 64 : 32;
+      }
+      k_tw_count<<<gq, TW_BLOCK, 0, s>>>(A);
+      k_tw_prep<<<nd_grid(rows / TW_TM + 1, 256, nsm * 4), 256, 0, s>>>(A);
+      k_tw_place<<<gq, TW_BLOCK, 0, s>>>(A);
+      k_tw_sample<4><<<nsm * occ, TW_BLOCK, 0, s>>>(A);
+      k_tw_hub_warp<<<nsm * 4, TW_BLOCK, TW_WARP_SMEM, s>>>(A);
+      k_tw_hub_cta<<<nsm * 2, TW_BLOCK, TW_CTA_SMEM, s>>>(A);
+      if (cudaGetLastError() != cudaSuccess) { rc = ND_ERR_CUDA; break; }
+      if (getenv("ND_TW_DEBUG") && (st_ % 10 == 1)) {  // development: per-step tier sizes
+        TwCtl hc;
+        if (nd_d2h(&hc, ctl + b, sizeof(TwCtl), s) == ND_OK)
+          fprintf(stderr, "[tw] step %lld hubs %d groups %d small %d warp-hubs %d cta-units %d "
+                  "grid-members %d staged-members %d\n", (long long)st_, hc.nhub, 0,
+                  hc.nsmall, hc.nwarp, hc.nunit, hc.back, hc.front);
+      }
+    }
+    k_pw_accum<<<nd_grid(rows, 256), 256, 0, s>>>(wid, W.nnz, rows, tot);
+    if (rc == ND_OK && nd_d2h(h, cont_n, sizeof(int), s) != ND_OK) rc = ND_ERR_CUDA;
+    nd_free(cont_n, s);
+    nd_free(v0, s);
+    nd_free(t0, s);
+    twins.push_back(W);
+    if (rc != ND_OK) {
+      nd_free(cw, s); nd_free(cv, s); nd_free(ct, s);
+      wid = v0 = t0 = nullptr;
+      break;
+    }
+    wid = cw;
+    v0 = cv;
+    t0 = ct;
+    rows = h[0];
+    step += Lw;
+  }
+  double sample_ms = 0.0;
+  if (rc == ND_OK && tail && step == 0) {  // every walker in the tail: rows from the roots
+    if (nd_alloc(&wid, rows, s) != cudaSuccess || nd_alloc(&v0, rows, s) != cudaSuccess ||
+        nd_alloc(&t0, rows, s) != cudaSuccess)
+      rc = ND_ERR_CUDA;
+    else
+      k_tw_rows0<<<nd_grid(rows, 256), 256, 0, s>>>(roots, roots32, R, rows, wid, v0, t0);
+  }
+  if (rc == ND_OK && tail) {
+    // the remaining walkers (rows of wid/v0/t0) continue walker-major
+    int64_t ns = 0;
+    rc = run_tp_tail(G, a, seed, sample_lo, n, rows, nullptr, nullptr, R, step, max_steps,
+                     steps >= 0 ? max_steps - step : 128, key_bits, nullptr, stall, ctr, stats, s,
+                     tail_wins, ns, tail_items, sample_ms, wid, v0, t0, died);
+    if (ns > n_steps) n_steps = ns;
+    wid = v0 = t0 = nullptr;  // owned by the tail windows
+    for (auto& W : tail_wins) k_pw_accum<<<nd_grid(W.n, 256), 256, 0, s>>>(W.wid, W.nnz, W.n, tot);
+  } else {
+    nd_free(v0, s);
+    nd_free(t0, s);
+  }
+  if (l2set) {  // back to normal caching for the stream; release the persisting lines
+    l2off.accessPolicyWindow.num_bytes = 0;
+    cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &l2off);
+    cudaCtxResetPersistingL2Cache();
+    cudaGetLastError();
+  }
+  prof.mark();
+  int h_stall = 0;
+  if (rc == ND_OK) {
+    int mlen = 0;
+    if (nd_d2h(&mlen, maxlen, sizeof(int), s) != ND_OK) rc = ND_ERR_CUDA;
+    if (mlen > n_steps) n_steps = mlen;
+  }
+  // ---- compaction into the final layout -------------------------------------------
+  int32_t* final_ids = nullptr;
+  int64_t *flen = nullptr, *final_off = nullptr, *clen = nullptr, *roots_out = nullptr;
+  unsigned long long* hist = nullptr;
+  int64_t total = 0;
+  if (rc == ND_OK) {
+    const int64_t hl = max_steps + 2;
+    ND_CUDA_TRY(nd_alloc(&flen, n + 1, s));
+    ND_CUDA_TRY(nd_alloc(&final_off, n + 1, s));
+    ND_CUDA_TRY(nd_alloc(&clen, n, s));
+    ND_CUDA_TRY(nd_alloc(&roots_out, n * R, s));
+    ND_CUDA_TRY(nd_alloc(&hist, hl, s));
+    ND_CUDA_TRY(cudaMemsetAsync(hist, 0, hl * sizeof(unsigned long long), s));
+    k_pw_lengths<<<nd_grid(n + 1, 256, nsm * 4), 256, 0, s>>>(tot, died, n, R, flen, clen, hist, hl);
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, flen, final_off, n + 1, s);
+    void* tmp = nullptr;
+    ND_CUDA_TRY(nd_alloc((char**)&tmp, tb, s));
+    ND_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tb, flen, final_off, n + 1, s));
+    nd_free(tmp, s);
+    ND_TRY(nd_d2h(&total, final_off + n, sizeof(int64_t), s));
+    ND_CUDA_TRY(nd_alloc(&final_ids, total, s));
+    if (n * R) {
+      if (roots)
+        k_write_roots<int64_t><<<nd_grid(n * R, 256), 256, 0, s>>>(roots, n, R, final_off,
+                                                                  final_ids, roots_out);
+      else
+        k_write_roots<int32_t><<<nd_grid(n * R, 256), 256, 0, s>>>(roots32, n, R, final_off,
+                                                                  final_ids, roots_out);
+    }
+    for (auto& W : twins)
+      if (W.rows * W.Lw)
+        k_tw_emit<<<nd_grid((W.rows + 31) / 32 * ((W.Lw + 31) / 32) * 32, 256, nsm * 16), 256, 0, s>>>(
+            W.out, W.rows, W.Lw, W.nnz, W.wid, W.step0, final_off, R, final_ids);
+    for (auto& W : tail_wins)
+      if (W.n * W.Lw)
+        k_pw_emit<<<nd_grid(W.n * 32, 256, nsm * 32), 256, 0, s>>>(W.wid, W.out, W.nnz, W.n, W.ld,
+                                                                  W.step0, final_off, R, final_ids);
+    unsigned long long h_ctr[4];
+    ND_TRY(nd_d2h(&h_stall, stall, sizeof(int), s));
+    ND_TRY(nd_d2h(h_ctr, ctr, sizeof(h_ctr), s));
+    ND_CUDA_TRY(cudaGetLastError());
+    res->counters[NDC_N2V_TRIES] = (int64_t)h_ctr[1];
+    res->counters[NDC_SLOT_BYTES] = (int64_t)h_ctr[0];
+    res->counters[NDC_RAND_SECTORS] = (int64_t)h_ctr[2];
+  }
+  prof.mark();
+  if (prof.on && rc == ND_OK) {
+    res->prof_ms[1] = prof.between(0, 1);
+    res->prof_ms[2] = prof.between(1, 2);
+  }
+  prof.destroy();
+  for (auto& W : twins) { nd_free(W.wid, s); nd_free(W.out, s); nd_free(W.nnz, s); }
+  pw_free_windows(tail_wins, s);
+  nd_free(wid, s);
+  nd_free(roots32, s); nd_free(died, s); nd_free(tot, s); nd_free(maxlen, s); nd_free(stall, s);
+  nd_free(ctr, s); nd_free(ctl, s); nd_free(hoff, s); nd_free(wunits, s); nd_free(cunits, s);
+  nd_free(hrec, s); nd_free(pos, s); nd_free(flen, s); nd_free(hist, s);
+  nd_free(slist, s); nd_free(cnt, s); nd_free(vhub, s); nd_free(hubs, s);
+  for (int b = 0; b < 2; b++) { nd_free(cur[b], s); nd_free(lo[b], s); nd_free(dg[b], s); nd_free(hd[b], s); }
+  if (rc != ND_OK) {
+    nd_free(stats, s); nd_free(final_off, s); nd_free(final_ids, s); nd_free(clen, s); nd_free(roots_out, s);
+    return rc;
+  }
+  res->n = n;
+  res->n_steps = n_steps;
+  res->total_sampled = total - n * R;
+  res->set(ND_F_FINAL_OFF, final_off, n + 1);
+  res->set(ND_F_FINAL_IDS32, final_ids, total);
+  res->set(ND_F_ROOTS, roots_out, n * R);
+  res->set(ND_F_CHAIN_LEN, clen, n);
+  res->set(ND_F_STATS, stats, 4 * n_steps);
+  res->counters[NDC_ITEMS] = total - n * R;
+  res->counters[NDC_PAIRS] = res->counters[NDC_ITEMS];
+  res->counters[NDC_STEPS] = n_steps;
+  ND_CUDA_TRY(cudaStreamSynchronize(s));
+  return h_stall ? ND_ERR_STALL : ND_OK;
+}
+
 extern "C" int nd_run_walk(const nd_graph* g, int app_code, const double* host_params,
                            int64_t n_params, int64_t sample_lo, int64_t n_samples,
                            const int64_t* roots, int64_t roots_per_sample, uint64_t seed,
@@ -1476,9 +1897,10 @@ extern "C" int nd_run_walk(const nd_graph* g, int app_code, const double* host_p
   // picks, hash sets for node2vec membership
   ND_TRY(nd_graph_ensure_index(const_cast<nd_graph*>(g), app_code == ND_NODE2VEC,
                                app_code != ND_MULTIRW, s));
-  if (app_code != ND_MULTIRW && paradigm == ND_SP)
+  // packed records: the walker-major kernel and the TP hub engine read them
+  if (app_code != ND_MULTIRW)
     ND_TRY(nd_graph_ensure_records(const_cast<nd_graph*>(g), app_code == ND_NODE2VEC, s));
-  if ((app_code == ND_DEEPWALK || app_code == ND_PPR) && paradigm == ND_SP)
+  if (app_code == ND_DEEPWALK || app_code == ND_PPR)
     ND_TRY(nd_graph_ensure_lines(const_cast<nd_graph*>(g), s));
   nd_result* res = new nd_result();
   res->stream = s;
@@ -1489,6 +1911,9 @@ extern "C" int nd_run_walk(const nd_graph* g, int app_code, const double* host_p
   else if (paradigm == ND_SP)
     rc = run_chain_walk_sp(g, a, sample_lo, n_samples, roots, roots_per_sample, seed, steps,
                            step_cap, s, res);
+  else if (tw_applicable(g->g, a))
+    rc = run_chain_walk_hub(g, a, sample_lo, n_samples, roots, roots_per_sample, seed, steps,
+                            step_cap, s, res);
   else
     rc = run_chain_walk(g, a, sample_lo, n_samples, roots, roots_per_sample, seed, steps,
                         step_cap, paradigm, s, res);
