@@ -1517,17 +1517,12 @@ static int run_rootpick_walk(const nd_graph* G, const NdApp& a, int64_t sample_l
 #include "nd_bulk.cuh"
 #include "nd_walk_hub.cuh"
 
-// dynamic shared memory above 48 KB for the hub kernels (once per process)
+// dynamic shared memory above 48 KB for the hub kernel (once per process)
 static int tw_attrs() {
   static int rc = -1;
-  if (rc < 0) {
-    rc = ND_OK;
-    if (cudaFuncSetAttribute(k_tw_hub_cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)TW_CTA_SMEM) != cudaSuccess ||
-        cudaFuncSetAttribute(k_tw_hub_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)TW_WARP_SMEM) != cudaSuccess)
-      rc = ND_ERR_CUDA;
-  }
+  if (rc < 0)
+    rc = cudaFuncSetAttribute(k_tw_hub<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)TW_HUB_SMEM) == cudaSuccess ? ND_OK : ND_ERR_CUDA;
   return rc;
 }
 
@@ -1557,6 +1552,9 @@ static int run_chain_walk_hub(const nd_graph* G, const NdApp& a, int64_t sample_
   int occ = 4;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tw_sample<4>, TW_BLOCK, 0);
   if (occ < 1) occ = 1;
+  int hocc = 4;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hocc, k_tw_hub<4>, TW_BLOCK, TW_HUB_SMEM);
+  if (hocc < 1) hocc = 1;
   const int64_t max_steps = steps >= 0 ? (steps < step_cap ? steps : step_cap) : step_cap;
   const int64_t tail_T = getenv("ND_TP_TAIL") ? atoll(getenv("ND_TP_TAIL")) : 131072;
   const int key_bits = key_bits_for(g.V);
@@ -1564,9 +1562,9 @@ static int run_chain_walk_hub(const nd_graph* G, const NdApp& a, int64_t sample_
   const int64_t V = g.V;
   const int64_t hcap = n / TW_TM + 2;                 // hubs per step
   const int64_t ucap = hcap + n / TW_UNIT + 2;        // CTA units per step
-  int32_t *roots32 = nullptr, *died = nullptr, *maxlen = nullptr, *hoff = nullptr;
+  int32_t *roots32 = nullptr, *died = nullptr, *maxlen = nullptr;
   TwRec* hrec = nullptr;
-  int32_t *pos = nullptr, *slist = nullptr, *cnt = nullptr, *vhub = nullptr, *hubs = nullptr;
+  int32_t *pos = nullptr, *cnt[2] = {}, *vhub[2] = {}, *hubs[2] = {};
   int32_t *cur[2] = {}, *dg[2] = {};
   uint32_t* lo[2] = {};
   double* hd[2] = {};
@@ -1582,16 +1580,17 @@ static int run_chain_walk_hub(const nd_graph* G, const NdApp& a, int64_t sample_
   ND_CUDA_TRY(nd_alloc(&ctr, 4, s));
   ND_CUDA_TRY(nd_alloc(&stats, 4 * (max_steps + 1), s));
   ND_CUDA_TRY(nd_alloc(&ctl, 2, s));
-  ND_CUDA_TRY(nd_alloc(&hoff, hcap, s));
   ND_CUDA_TRY(nd_alloc(&wunits, hcap, s));
   ND_CUDA_TRY(nd_alloc(&cunits, ucap, s));
   ND_CUDA_TRY(nd_alloc(&hrec, n, s));
   ND_CUDA_TRY(nd_alloc(&pos, n, s));
-  ND_CUDA_TRY(nd_alloc(&slist, n, s));
-  ND_CUDA_TRY(nd_alloc(&cnt, V, s));
-  ND_CUDA_TRY(nd_alloc(&vhub, V, s));
-  ND_CUDA_TRY(nd_alloc(&hubs, hcap, s));
-  ND_CUDA_TRY(cudaMemsetAsync(cnt, 0, V * sizeof(int32_t), s));
+  ND_CUDA_TRY(nd_alloc(&cnt[0], 2 * V, s));  // both parities, one L2 window
+  cnt[1] = cnt[0] + V;
+  ND_CUDA_TRY(cudaMemsetAsync(cnt[0], 0, 2 * V * sizeof(int32_t), s));
+  for (int b = 0; b < 2; b++) {
+    ND_CUDA_TRY(nd_alloc(&vhub[b], V, s));
+    ND_CUDA_TRY(nd_alloc(&hubs[b], hcap, s));
+  }
   for (int b = 0; b < 2; b++) {
     ND_CUDA_TRY(nd_alloc(&cur[b], n, s));
     ND_CUDA_TRY(nd_alloc(&lo[b], n, s));
@@ -1616,13 +1615,13 @@ static int run_chain_walk_hub(const nd_graph* G, const NdApp& a, int64_t sample_
   {
     int max_persist = 0;
     cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
-    const size_t want = (size_t)V * sizeof(int32_t);
+    const size_t want = (size_t)2 * V * sizeof(int32_t);
     if (max_persist > 0 && !getenv("ND_TW_NO_L2PIN")) {
       size_t lim = 0;
       cudaDeviceGetLimit(&lim, cudaLimitPersistingL2CacheSize);
       const size_t setaside = std::min<size_t>((size_t)max_persist, std::max(lim, want));
       if (lim < setaside) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, setaside);
-      l2win.accessPolicyWindow.base_ptr = cnt;
+      l2win.accessPolicyWindow.base_ptr = cnt[0];
       l2win.accessPolicyWindow.num_bytes = want;
       l2win.accessPolicyWindow.hitRatio = want <= setaside ? 1.0f : (float)setaside / (float)want;
       l2win.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
@@ -1653,6 +1652,33 @@ static int run_chain_walk_hub(const nd_graph* G, const NdApp& a, int64_t sample_
     return 2;
   };
   int64_t next_Lw = 1;
+  // ND_TW_PROFILE=1 (development): event-timed phases of every step, summed
+  struct TwPhases {
+    bool on = getenv("ND_TW_PROFILE") != nullptr;
+    std::vector<cudaEvent_t> ev;
+    std::vector<int> ph;
+    void mark(cudaStream_t st, int p) {
+      if (!on) return;
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      cudaEventRecord(e, st);
+      ev.push_back(e);
+      ph.push_back(p);
+    }
+    void report() {
+      if (!on) return;
+      cudaEventSynchronize(ev.empty() ? nullptr : ev.back());
+      double t[8] = {};
+      for (size_t i = 1; i < ev.size(); i++)
+        if (ph[i] == ph[i - 1] + 1) {
+          float ms = 0;
+          cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
+          t[ph[i - 1]] += ms;
+        }
+      fprintf(stderr, "[tw-profile] prep %.3f sample %.3f hub %.3f ms\n", t[0], t[1], t[2]);
+      for (auto e : ev) cudaEventDestroy(e);
+    }
+  } tp;
   struct TWin {
     int32_t *wid, *out, *nnz;
     int64_t rows, step0, Lw;
@@ -1703,21 +1729,22 @@ static int run_chain_walk_hub(const nd_graph* G, const NdApp& a, int64_t sample_
     A.cont_t = ct;
     A.cont_n = cont_n;
     A.max_len = maxlen;
-    A.hoff = hoff;
     A.hrec = hrec;
     A.hcap = n;
-    A.cnt = cnt;
-    A.vhub = vhub;
-    A.hubs = hubs;
+
     A.wunits = wunits;
     A.cunits = cunits;
-    A.slist = slist;
     // window start: state of every row
     A.s = step;
     A.cur = cur[0]; A.lo = lo[0]; A.deg = dg[0]; A.hd = hd[0];
     A.ncur = cur[1]; A.nlo = lo[1]; A.ndeg = dg[1]; A.nhd = hd[1];
     k_tw_init<<<nd_grid(rows, TW_BLOCK, nsm * 8), TW_BLOCK, 0, s>>>(A, roots, roots32, R, v0, t0);
-    const int gq = nd_grid(rows, TW_TILE, nsm * 8);
+    {
+      const int b = (int)(step & 1);
+      A.nctl = ctl + b; A.ncnt = cnt[b]; A.nhubs = hubs[b];
+      A.nstats = stats + 4 * step;
+      k_tw_count0<<<nd_grid(rows, TW_BLOCK, nsm * 8), TW_BLOCK, 0, s>>>(A);
+    }
     for (int64_t k = 0; k < Lw; k++) {
       const int64_t st_ = step + k;
       const int b = (int)(st_ & 1), pb = b ^ 1;
@@ -1728,27 +1755,28 @@ static int run_chain_walk_hub(const nd_graph* G, const NdApp& a, int64_t sample_
       A.tries = n2v && st_ > 0;
       A.cur = cur[in]; A.lo = lo[in]; A.deg = dg[in]; A.hd = hd[in];
       A.ncur = cur[ou]; A.nlo = lo[ou]; A.ndeg = dg[ou]; A.nhd = hd[ou];
-      A.ctl = ctl + b;
-      A.nctl = ctl + pb;
-      A.stats = stats + 4 * st_;
+      A.ctl = ctl + b; A.cnt = cnt[b]; A.vhub = vhub[b]; A.hubs = hubs[b];
+      A.nctl = ctl + pb; A.ncnt = cnt[pb]; A.nhubs = hubs[pb];
+      A.nstats = stats + 4 * (st_ + 1);
       A.rmode = rmode(A.tries);
       {
         const int64_t thr = (int64_t)nsm * occ * TW_BLOCK;
         A.P.chunk = rows > 8 * thr ? 128 : rows > 2 * thr ? 64 : 32;
       }
-      k_tw_count<<<gq, TW_BLOCK, 0, s>>>(A);
+      tp.mark(s, 0);
       k_tw_prep<<<nd_grid(rows / TW_TM + 1, 256, nsm * 4), 256, 0, s>>>(A);
-      k_tw_place<<<gq, TW_BLOCK, 0, s>>>(A);
+      tp.mark(s, 1);
       k_tw_sample<4><<<nsm * occ, TW_BLOCK, 0, s>>>(A);
-      k_tw_hub_warp<<<nsm * 4, TW_BLOCK, TW_WARP_SMEM, s>>>(A);
-      k_tw_hub_cta<<<nsm * 2, TW_BLOCK, TW_CTA_SMEM, s>>>(A);
+      tp.mark(s, 2);
+      k_tw_hub<4><<<nsm * hocc, TW_BLOCK, TW_HUB_SMEM, s>>>(A);
+      tp.mark(s, 3);
       if (cudaGetLastError() != cudaSuccess) { rc = ND_ERR_CUDA; break; }
       if (getenv("ND_TW_DEBUG") && (st_ % 10 == 1)) {  // development: per-step tier sizes
         TwCtl hc;
         if (nd_d2h(&hc, ctl + b, sizeof(TwCtl), s) == ND_OK)
           fprintf(stderr, "[tw] step %lld hubs %d groups %d small %d warp-hubs %d cta-units %d "
-                  "grid-members %d staged-members %d\n", (long long)st_, hc.nhub, 0,
-                  hc.nsmall, hc.nwarp, hc.nunit, hc.back, hc.front);
+                  "grid-members %d staged-members %d\n", (long long)st_, hc.nhub, 0, 0,
+                  hc.nwarp, hc.nunit, 0, hc.front);
       }
     }
     k_pw_accum<<<nd_grid(rows, 256), 256, 0, s>>>(wid, W.nnz, rows, tot);
@@ -1789,6 +1817,7 @@ static int run_chain_walk_hub(const nd_graph* G, const NdApp& a, int64_t sample_
     nd_free(v0, s);
     nd_free(t0, s);
   }
+  tp.report();
   if (l2set) {  // back to normal caching for the stream; release the persisting lines
     l2off.accessPolicyWindow.num_bytes = 0;
     cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &l2off);
@@ -1858,9 +1887,10 @@ static int run_chain_walk_hub(const nd_graph* G, const NdApp& a, int64_t sample_
   pw_free_windows(tail_wins, s);
   nd_free(wid, s);
   nd_free(roots32, s); nd_free(died, s); nd_free(tot, s); nd_free(maxlen, s); nd_free(stall, s);
-  nd_free(ctr, s); nd_free(ctl, s); nd_free(hoff, s); nd_free(wunits, s); nd_free(cunits, s);
+  nd_free(ctr, s); nd_free(ctl, s); nd_free(wunits, s); nd_free(cunits, s);
   nd_free(hrec, s); nd_free(pos, s); nd_free(flen, s); nd_free(hist, s);
-  nd_free(slist, s); nd_free(cnt, s); nd_free(vhub, s); nd_free(hubs, s);
+  nd_free(cnt[0], s);
+  for (int b = 0; b < 2; b++) { nd_free(vhub[b], s); nd_free(hubs[b], s); }
   for (int b = 0; b < 2; b++) { nd_free(cur[b], s); nd_free(lo[b], s); nd_free(dg[b], s); nd_free(hd[b], s); }
   if (rc != ND_OK) {
     nd_free(stats, s); nd_free(final_off, s); nd_free(final_ids, s); nd_free(clen, s); nd_free(roots_out, s);

@@ -8,19 +8,15 @@
 // > 1024; :86-101) and runs each class with its own kernel.
 // Here that step is built from member counts instead of a radix sort:
 //
-//   count     — one streaming pass over the window's rows: the walkers of a
-//               1024-row tile are counted per distinct transit in a shared-
-//               memory hash table, then one atomicAdd per (tile, transit) on
-//               cnt[v] returns the tile's base position in the group (a hub's
-//               many members cost one global atomic per tile); each walker's
-//               position = base + its rank in the tile.  The group count
-//               (0 -> 1 crossings), the medium and large class counts
-//               (crossings of 32 and 1025 members) and the hub list (groups
-//               reaching 32 members: every medium and large group) fall out
-//               of the same atomics, exactly;
-//   prep      — one thread per hub: its tier and its member slots (disjoint
-//               ranges reserved by atomics, staged tiers from the front of the
-//               member array, the grid tier from the back);
+//   count     — fused into the previous step's emission: a walker landing on
+//               vertex o does atomicAdd(cnt_{s+1}[o], 1) (its result consumed
+//               one lane iteration later, behind the next walker's loads); the
+//               returned old count is its position in o's group, and the +1
+//               crossings of 0, 32 and 1025 members give the group count, the
+//               medium and large class counts and the hub list (groups
+//               reaching 32 members: every medium and large group), exactly;
+//   prep      — one thread per hub: its tier and, for the staged tiers, its
+//               member slots (disjoint ranges reserved by atomics);
 //   place     — a second streaming pass writes every hub member's record at
 //               its group position and lists the small-class walkers;
 //   small     — the sub-warp class (m = 1: one lane per member): a
@@ -33,8 +29,9 @@
 //               bulk copy (cp.async.bulk + mbarrier, nd_bulk.cuh) of the
 //               transit's record row into shared memory, awaited after the
 //               first members' records are in flight.
-// The sampling kernels clear cnt[v] of the transits they step, so the next
-// step's count starts from zero without a separate pass.
+// Counts alternate between two buffers by step parity: the sampling kernels
+// of step s clear cnt_s[v] of the transits they step while counting into
+// cnt_{s+1}, so no separate clearing pass is needed.
 //
 // Walker state is held per window row in HBM as structure-of-arrays
 // (vertex, row start, degree, max weight or prefix total), double-buffered:
@@ -51,16 +48,12 @@ constexpr int TW_TM = 32;           // members at which a walk group is medium (
 constexpr int TW_TL = 1025;         // members at which it is large (work > 1024)
 constexpr int TW_WARP_MAX = 256;    // members of a warp-tier hub
 constexpr int TW_UNIT = 2048;       // members per CTA unit
-constexpr int TW_STAGE_W = 4096;    // staged row bytes per warp
-constexpr int TW_STAGE_C = 96 * 1024;  // staged row bytes per CTA
+constexpr int TW_STAGE_W = 2048;    // staged row bytes per warp
+constexpr int TW_STAGE_C = 32 * 1024;  // staged row bytes per CTA
 constexpr int TW_PAY = 64;          // stage when row bytes <= members * TW_PAY
-constexpr int TW_Q = 4;             // tiles of 32 rows per warp in the streaming passes
-constexpr int TW_TILE = TW_BLOCK * TW_Q;  // rows per CTA tile
-constexpr int TW_HT = 2048;         // hash slots per tile (>= 2 * TW_TILE)
-constexpr int TW_PLACE_ROWS = 4096; // rows per place CTA chunk (small list staged in smem)
 
 struct TwCtl {  // per step (alternating by step parity)
-  int nhub, nsmall, queue, nwarp, nunit, front, back, pad;
+  int nhub, queue, nwarp, nunit, front, wq, uq, pad;
 };
 
 struct __align__(16) TwUnit {
@@ -106,17 +99,18 @@ struct TwArgs {
   int32_t* cont_t;
   int* cont_n;
   int* max_len;
-  // this step's groups
+  // this step's groups (counted by the previous step's emission)
   TwCtl* ctl;
-  TwCtl* nctl;          // the next step's (reset by prep)
-  int32_t* cnt;         // member counts (zero between steps)
-  int32_t* vhub;        // hub index of a vertex (valid while cnt >= TW_TM)
+  int32_t* cnt;         // member counts (cleared by this step's sampling)
+  int32_t* vhub;        // staged hub's first member slot, -1 grid tier (valid while cnt >= TW_TM)
   int32_t* hubs;
-  unsigned long long* stats;
-  int32_t* hoff;        // per hub: first member slot
+  // the next step's, counted by this step's emission
+  TwCtl* nctl;          // (reset by prep)
+  int32_t* ncnt;
+  int32_t* nhubs;
+  unsigned long long* nstats;
   TwRec* hrec;          // hub members in group order
   int64_t hcap;         // member slots
-  int32_t* slist;       // small-class rows
   TwUnit* wunits;
   TwUnit* cunits;
 };
@@ -136,13 +130,7 @@ struct TwLane {
   uint64_t ik = 0;
 };
 
-// ---- count: member positions, class counts and the hub list ------------------
-struct TwTable {
-  int32_t key[TW_HT];
-  int32_t num[TW_HT];
-  int32_t base[TW_HT];
-};
-
+// ---- member counting ------------------------------------------------------------
 // warp-aggregated append of the lanes with f set; returns each lane's slot
 __device__ __forceinline__ int tw_warp_append(bool f, int* gcount) {
   const int lane = threadIdx.x & 31;
@@ -154,69 +142,45 @@ __device__ __forceinline__ int tw_warp_append(bool f, int* gcount) {
   return f ? base + __popc(m & ((1u << lane) - 1)) : -1;
 }
 
-// One CTA tile of TW_TILE rows (every thread calls it; v[q] >= 0 are alive
-// walkers at transit v).
-template <int Q>
-__device__ __forceinline__ void tw_count_tile(const TwArgs& A, const int32_t (&v)[Q], int64_t b0,
-                                              TwCounts& cc, TwTable& T) {
-  const int lane = threadIdx.x & 31;
-  int slot[Q], loc[Q];
-#pragma unroll
-  for (int q = 0; q < Q; q++) {
-    slot[q] = -1;
-    loc[q] = 0;
-    if (v[q] < 0) continue;
-    uint32_t h = hset_hash((uint32_t)v[q]) >> (32 - 11);
-    while (true) {
-      const int32_t k = atomicCAS(&T.key[h], -1, v[q]);
-      if (k == -1 || k == v[q]) break;
-      h = (h + 1) & (TW_HT - 1);
-    }
-    slot[q] = (int)h;
-    loc[q] = atomicAdd(&T.num[h], 1);
+// A walker counted at vertex o of the next step (the emission's atomicAdd
+// on ncnt[o]; its result is consumed after the lane's next pick, so the
+// atomic's latency hides behind that pick's loads).  The returned old count is
+// the walker's position in its group; +1 crossings of 0, 32 and 1025 members
+// give the group count, the medium / large class counts and the hub list,
+// exactly.
+struct TwPend {
+  bool on = false;
+  int32_t o = 0, old = 0;
+  int64_t row = 0;
+};
+
+__device__ __forceinline__ void tw_count_issue(const TwArgs& A, TwPend& p, bool live, int32_t o,
+                                               int64_t row) {
+  if (live) {
+    p.on = true;
+    p.o = o;
+    p.row = row;
+    p.old = atomicAdd(A.ncnt + o, 1);
   }
-  __syncthreads();
-  // one global atomic per distinct transit of the tile, all in flight together
-  constexpr int PER = TW_HT / TW_BLOCK;
-  int32_t kv[PER], c[PER], o[PER];
-#pragma unroll
-  for (int k = 0; k < PER; k++) {
-    const int sl = k * TW_BLOCK + threadIdx.x;
-    kv[k] = T.key[sl];
-    c[k] = T.num[sl];
-    o[k] = kv[k] >= 0 ? atomicAdd(A.cnt + kv[k], c[k]) : 0;
-  }
-#pragma unroll
-  for (int k = 0; k < PER; k++) {
-    bool hm = false;
-    if (kv[k] >= 0) {
-      T.base[k * TW_BLOCK + threadIdx.x] = o[k];
-      cc.ng += o[k] == 0;
-      hm = o[k] < TW_TM && o[k] + c[k] >= TW_TM;
-      cc.nm += hm;
-      cc.nl += o[k] < TW_TL && o[k] + c[k] >= TW_TL;
-    }
-    const int idx = tw_warp_append(hm, &A.ctl->nhub);  // rare: a group becomes a hub
-    if (hm) {
-      A.hubs[idx] = kv[k];
-      A.vhub[kv[k]] = idx;
-    }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int q = 0; q < Q; q++)
-    if (slot[q] >= 0) A.pos[b0 + q * 32 + lane] = T.base[slot[q]] + loc[q];
-  __syncthreads();
-#pragma unroll
-  for (int k = 0; k < PER; k++) {
-    T.key[k * TW_BLOCK + threadIdx.x] = -1;
-    T.num[k * TW_BLOCK + threadIdx.x] = 0;
-  }
-  __syncthreads();
 }
 
-// per-warp class deltas (a tile can cross a threshold of a group another tile
-// opened: the signed deltas sum to the exact counts over the grid)
+// warp-uniform call
+__device__ __forceinline__ void tw_count_take(const TwArgs& A, TwPend& p, TwCounts& cc) {
+  bool hm = false;
+  if (p.on) {
+    A.pos[p.row] = p.old;
+    cc.ng += p.old == 0;
+    hm = p.old == TW_TM - 1;
+    cc.nm += hm;
+    cc.nl += p.old == TW_TL - 1;
+  }
+  const int idx = tw_warp_append(hm, &A.nctl->nhub);  // rare: a group becomes a hub
+  if (hm) A.nhubs[idx] = p.o;
+  p.on = false;
+}
+
+// per-warp class deltas (a walker can cross a threshold of a group another
+// warp opened: the signed deltas sum to the exact counts over the grid)
 __device__ __forceinline__ void tw_flush_classes(TwCounts cc, unsigned long long* stats) {
   for (int o = 16; o > 0; o >>= 1) {
     cc.ng += __shfl_down_sync(0xffffffffu, cc.ng, o);
@@ -231,28 +195,6 @@ __device__ __forceinline__ void tw_flush_classes(TwCounts cc, unsigned long long
   }
 }
 
-__global__ void __launch_bounds__(TW_BLOCK) k_tw_count(TwArgs A) {
-  __shared__ TwTable T;
-  for (int k = threadIdx.x; k < TW_HT; k += TW_BLOCK) {
-    T.key[k] = -1;
-    T.num[k] = 0;
-  }
-  __syncthreads();
-  TwCounts cc;
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  for (int64_t t0 = blockIdx.x * (int64_t)TW_TILE; t0 < A.rows; t0 += (int64_t)gridDim.x * TW_TILE) {
-    const int64_t b0 = t0 + wib * 32 * TW_Q;
-    int32_t v[TW_Q];
-#pragma unroll
-    for (int q = 0; q < TW_Q; q++) {
-      const int64_t row = b0 + q * 32 + lane;
-      v[q] = row < A.rows ? A.cur[row] : -1;
-    }
-    tw_count_tile<TW_Q>(A, v, b0, cc, T);
-  }
-  tw_flush_classes(cc, A.stats);
-}
-
 // ---- prep: hub tiers and member slots (one thread per hub) --------------------
 // A hub's members read its record row; staging pays when the row is at most
 // TW_PAY bytes per member.  Tiers:
@@ -261,9 +203,9 @@ __global__ void __launch_bounds__(TW_BLOCK) k_tw_count(TwArgs A) {
 //          staged;
 //   grid   rows too large to stage (or not worth it): the members of every
 //          such hub spread over the whole grid, rows read from global memory.
-// Member slots: disjoint ranges reserved with warp-aggregated atomics, the
-// staged tiers from the front of the member array, the grid tier from the
-// back, so the grid tier's members are one contiguous range.
+// Member slots: disjoint ranges reserved with warp-aggregated atomics for the
+// staged tiers; the grid tier needs none (its members are stepped where the
+// sampling kernel meets them, each carrying its own row header).
 __device__ __forceinline__ uint32_t tw_rbytes(int rmode, int64_t deg) {
   if (deg <= 0) return 0;
   const int64_t b = rmode == 2 ? (deg + 2) / 3 * 128 : deg * (rmode == 1 ? 16 : 32);
@@ -296,7 +238,7 @@ __global__ void __launch_bounds__(256) k_tw_prep(TwArgs A) {
   if (blockIdx.x == 0 && threadIdx.x == 0) *A.nctl = TwCtl{};
   for (int jb = blockIdx.x * blockDim.x; jb < H; jb += gridDim.x * blockDim.x) {
     const int j = jb + threadIdx.x;
-    int32_t v = -1, c = 0, t = -1, nu = 0;
+    int32_t v = -1, c = 0, t = 2, nu = 0;
     if (j < H) {
       v = A.hubs[j];
       c = A.cnt[v];
@@ -304,82 +246,17 @@ __global__ void __launch_bounds__(256) k_tw_prep(TwArgs A) {
       t = tw_tier(c, tw_rbytes(A.rmode, r1 - r0));
       if (t == 1) nu = (c + TW_UNIT - 1) / TW_UNIT;
     }
-    const int mf = tw_warp_reserve(t == 0 || t == 1 ? c : 0, &A.ctl->front);
-    const int mg = tw_warp_reserve(t == 2 ? c : 0, &A.ctl->back);
+    const int m0 = tw_warp_reserve(t < 2 ? c : 0, &A.ctl->front);
     const int wu = tw_warp_reserve(t == 0 ? 1 : 0, &A.ctl->nwarp);
     const int cu = tw_warp_reserve(nu, &A.ctl->nunit);
     if (j < H) {
-      const int m0 = t == 2 ? (int)(A.hcap - mg - c) : mf;
-      A.hoff[j] = m0;
+      // the sampling kernel reads vhub of a hub member's transit: the staged
+      // hub's first member slot, or -1 (grid tier: stepped in place)
+      A.vhub[v] = t < 2 ? m0 : -1;
       if (t == 0) A.wunits[wu] = TwUnit{v, m0, m0 + c, j};
       for (int q = 0; q < nu; q++)
         A.cunits[cu + q] = TwUnit{v, m0 + q * TW_UNIT, m0 + min(c, (q + 1) * TW_UNIT), j};
     }
-  }
-}
-
-// ---- place: hub member records at their group positions, the small list -------
-// Each CTA takes chunks of TW_PLACE_ROWS consecutive rows, collects its small
-// rows in shared memory and reserves their list slots with one atomic.
-__global__ void __launch_bounds__(TW_BLOCK) k_tw_place(TwArgs A) {
-  __shared__ int32_t s_small[TW_PLACE_ROWS];
-  __shared__ int s_n, s_base;
-  const int lane = threadIdx.x & 31;
-  for (int64_t c0 = blockIdx.x * (int64_t)TW_PLACE_ROWS; c0 < A.rows;
-       c0 += (int64_t)gridDim.x * TW_PLACE_ROWS) {
-    if (threadIdx.x == 0) s_n = 0;
-    __syncthreads();
-    const int64_t c1 = A.rows < c0 + TW_PLACE_ROWS ? A.rows : c0 + TW_PLACE_ROWS;
-    for (int64_t r0 = c0 + (threadIdx.x & ~31) * TW_Q; r0 < c1; r0 += TW_TILE) {
-      int32_t v[TW_Q], c[TW_Q];
-#pragma unroll
-      for (int q = 0; q < TW_Q; q++) {
-        const int64_t row = r0 + q * 32 + lane;
-        v[q] = row < c1 ? A.cur[row] : -2;
-      }
-#pragma unroll
-      for (int q = 0; q < TW_Q; q++) c[q] = v[q] >= 0 ? A.cnt[v[q]] : 0;
-#pragma unroll
-      for (int q = 0; q < TW_Q; q++) {
-        const int64_t row = r0 + q * 32 + lane;
-        if (v[q] == -1) A.ncur[row] = -1;  // ended earlier in the window
-        const bool hub = v[q] >= 0 && c[q] >= TW_TM;
-        if (hub) {
-          const int32_t j = A.vhub[v[q]], p = A.pos[row];
-          TwRec r;
-          r.row = (int32_t)row;
-          r.w = A.wid ? A.wid[row] : (int32_t)row;
-          r.v = v[q];
-          r.deg = A.deg[row];
-          r.lo = A.lo[row];
-          r.hd = A.hd[row];
-          r.t = -1;
-          r.tdeg = 0;
-          r.tlo = 0;
-          if (A.tries) {
-            r.t = A.ncur[row];
-            r.tlo = A.nlo[row];
-            r.tdeg = A.ndeg[row];
-          }
-          r.pos = p;
-          r.j = j;
-          A.hrec[A.hoff[j] + p] = r;
-        }
-        const bool sm = v[q] >= 0 && c[q] < TW_TM;
-        const unsigned m = __ballot_sync(0xffffffffu, sm);
-        if (m) {
-          int base = 0;
-          if (lane == 0) base = atomicAdd(&s_n, __popc(m));
-          base = __shfl_sync(0xffffffffu, base, 0);
-          if (sm) s_small[base + __popc(m & ((1u << lane) - 1))] = (int32_t)row;
-        }
-      }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) s_base = s_n ? atomicAdd(&A.ctl->nsmall, s_n) : 0;
-    __syncthreads();
-    for (int k = threadIdx.x; k < s_n; k += TW_BLOCK) A.slist[s_base + k] = s_small[k];
-    __syncthreads();
   }
 }
 
@@ -443,7 +320,7 @@ __device__ __forceinline__ bool tw_work(const TwArgs& A, TwLane& L, const unsign
 // walker decided): the value and the next state, or the walk's end (NULL) /
 // the window's continuation list.
 __device__ __forceinline__ void tw_emit(const TwArgs& A, bool fin, const TwLane& L, int64_t o,
-                                        const NextHdr& nh, int& mlen, ItemStats& st) {
+                                        const NextHdr& nh, int& mlen, ItemStats& st, TwPend& pd) {
   if (fin) {
     A.out[A.k * A.rows + L.row] = (int32_t)o;
     mlen = max(mlen, (int)A.s + 1);
@@ -463,6 +340,7 @@ __device__ __forceinline__ void tw_emit(const TwArgs& A, bool fin, const TwLane&
       A.nlo[L.row] = (uint32_t)nh.lo;
       A.ndeg[L.row] = (int32_t)nh.deg;
       A.nhd[L.row] = nhd;
+      tw_count_issue(A, pd, true, (int32_t)o, L.row);
     }
   }
   if (A.last) {
@@ -502,8 +380,9 @@ __device__ __forceinline__ void tw_load_rec(const TwArgs& A, TwLane& L, const Tw
 }
 
 // Persistent lane loop over N work items: `load(i, L)` fills a lane from item
-// i; lanes refill from a warp-claimed chunk of a global queue as their walker
-// decides (node2vec's rejection tries keep every lane busy).
+// i (false: nothing to sample, the lane takes the next item); lanes refill
+// from a warp-claimed chunk of a global queue as their walker decides
+// (node2vec's rejection tries keep every lane busy).
 template <bool SH, class Load>
 __device__ __forceinline__ void tw_lanes(const TwArgs& A, int64_t N, int* queue, int chunk,
                                          const unsigned char* srec, Load load, ItemStats& st,
@@ -512,7 +391,10 @@ __device__ __forceinline__ void tw_lanes(const TwArgs& A, int64_t N, int* queue,
   const unsigned lt_mask = (1u << lane) - 1;
   const uint64_t base0 = key_base(A.P.seed, (uint64_t)A.s, 0, 0);
   TwLane L;
+  TwPend pd;
+  TwCounts cc;
   int64_t wbeg = 0, wend = 0, i = -1;
+  bool has = false;
   while (true) {
     const bool need = i < 0;
     const unsigned m = __ballot_sync(0xffffffffu, need);
@@ -528,7 +410,10 @@ __device__ __forceinline__ void tw_lanes(const TwArgs& A, int64_t N, int* queue,
       }
       if (need) {
         i = rank < rem ? wbeg + rank : nbeg + (rank - rem);
-        if (i < N) load(i, L);
+        if (i < N) {
+          has = load(i, L);
+          if (!has) i = -1;
+        }
       }
       if (rem < c) {
         wbeg = nbeg + (c - rem);
@@ -537,46 +422,75 @@ __device__ __forceinline__ void tw_lanes(const TwArgs& A, int64_t N, int* queue,
         wbeg += c;
       }
     }
-    if (__all_sync(0xffffffffu, i >= N)) break;
+    if (__all_sync(0xffffffffu, i >= N)) {
+      tw_count_take(A, pd, cc);
+      break;
+    }
     bool fin = false;
     int64_t o = -1;
     NextHdr nh;
-    if (i < N) fin = tw_work<SH>(A, L, srec, base0, o, nh, st);
-    tw_emit(A, fin, L, o, nh, mlen, st);
-    if (fin) i = -1;
+    if (has) fin = tw_work<SH>(A, L, srec, base0, o, nh, st);
+    tw_count_take(A, pd, cc);  // the previous iteration's count, after this one's picks
+    tw_emit(A, fin, L, o, nh, mlen, st, pd);
+    if (fin) {
+      i = -1;
+      has = false;
+    }
   }
+  tw_flush_classes(cc, A.nstats);
 }
 
-// ---- small class and grid tier: one persistent kernel --------------------------
-// Items [0, nsmall) are the small-class walkers (the sub-warp kernel, m = 1:
-// one lane per member); items [nsmall, nsmall + back) are the members of
-// every hub whose row is not staged (the grid kernel: one hub's members over
-// the whole grid, the row read from global memory).  One queue feeds both.
+// ---- small class and grid tier: persistent over the window's rows ---------------
+// The sub-warp kernel (m = 1: one lane per member) and the grid kernel (a
+// hub's members over the whole grid, its row read from global memory).  A
+// lane takes a row: a walker of the small class or of a grid-tier hub is
+// stepped right away, a member of a staged hub has its record written at its
+// group position for the hub kernel, an ended row is skipped.
 template <int MINB>
 __global__ void __launch_bounds__(TW_BLOCK, MINB) k_tw_sample(TwArgs A) {
   ItemStats st;
   int mlen = 0;
-  const int64_t NS = A.ctl->nsmall, NG = A.ctl->back, M0 = A.hcap - NG;
-  tw_lanes<false>(A, NS + NG, &A.ctl->queue, A.P.chunk, nullptr,
-                  [&](int64_t i, TwLane& L) {
-                    if (i >= NS) {
-                      tw_load_rec(A, L, A.hrec + M0 + (i - NS), st);
-                      return;
+  tw_lanes<false>(A, A.rows, &A.ctl->queue, A.P.chunk, nullptr,
+                  [&](int64_t row, TwLane& L) -> bool {
+                    const int32_t v = A.cur[row];
+                    if (v < 0) {  // ended earlier in the window
+                      A.ncur[row] = -1;
+                      return false;
                     }
-                    const int64_t row = A.slist[i];
-                    L.row = row;
-                    L.w = A.wid ? A.wid[row] : row;
-                    L.v = A.cur[row];
-                    L.lo = A.lo[row];
-                    L.deg = A.deg[row];
-                    L.hd = A.hd[row];
+                    const uint32_t lo = A.lo[row];
+                    const int32_t deg = A.deg[row];
+                    const double hd = A.hd[row];
+                    int32_t t = -1, tdeg = 0;
+                    uint32_t tlo = 0;
                     if (A.tries) {
-                      L.t = A.ncur[row];
-                      L.tlo = A.nlo[row];
-                      L.tdeg = A.ndeg[row];
+                      t = A.ncur[row];
+                      tlo = A.nlo[row];
+                      tdeg = A.ndeg[row];
                     }
-                    A.cnt[L.v] = 0;  // the next step counts from zero
+                    const int32_t w = A.wid ? A.wid[row] : (int32_t)row;
+                    if (A.cnt[v] >= TW_TM) {  // hub member
+                      const int32_t m0 = A.vhub[v];
+                      if (m0 >= 0) {  // staged tier: the record at its group position
+                        const int32_t p = A.pos[row];
+                        A.hrec[m0 + p] = TwRec{(int32_t)row, w, v, deg, lo, t, tdeg, tlo, hd, p, 0};
+                        return false;
+                      }
+                    }
+                    // small class or grid tier: stepped here.  Clearing the count
+                    // early only turns later grid-tier members of the same hub
+                    // into "small" ones, which are stepped here as well.
+                    A.cnt[v] = 0;
+                    L.row = row;
+                    L.w = w;
+                    L.v = v;
+                    L.lo = lo;
+                    L.deg = deg;
+                    L.hd = hd;
+                    L.t = t;
+                    L.tlo = tlo;
+                    L.tdeg = tdeg;
                     tw_lane_start(A, L, st);
+                    return true;
                   },
                   st, mlen);
   flush_stats(st, A.P.ctr);
@@ -610,6 +524,8 @@ __device__ __forceinline__ void tw_hub_members(const TwArgs& A, const TwUnit& d,
   const unsigned lt_mask = (1u << lane) - 1;
   const uint64_t base0 = key_base(A.P.seed, (uint64_t)A.s, 0, 0);
   TwLane L;
+  TwPend pd;
+  TwCounts cc;
   bool done = false, waited = false;
   while (true) {
     const bool need = L.row < 0 && !done;
@@ -624,7 +540,10 @@ __device__ __forceinline__ void tw_hub_members(const TwArgs& A, const TwUnit& d,
         else done = true;
       }
     }
-    if (__all_sync(0xffffffffu, L.row < 0 && done)) break;
+    if (__all_sync(0xffffffffu, L.row < 0 && done)) {
+      tw_count_take(A, pd, cc);
+      break;
+    }
     if (!waited) {
       mbar_wait(bar, parity);
       waited = true;
@@ -633,76 +552,81 @@ __device__ __forceinline__ void tw_hub_members(const TwArgs& A, const TwUnit& d,
     int64_t o = -1;
     NextHdr nh;
     if (L.row >= 0) fin = tw_work<true>(A, L, srec, base0, o, nh, st);
-    tw_emit(A, fin, L, o, nh, mlen, st);
+    tw_count_take(A, pd, cc);
+    tw_emit(A, fin, L, o, nh, mlen, st, pd);
     if (fin) L.row = -1;
   }
   if (!waited) mbar_wait(bar, parity);  // keep the barrier's phases in step
+  tw_flush_classes(cc, A.nstats);
 }
 
-// ---- warp tier: one warp per hub of <= TW_WARP_MAX members, row staged --------
-__global__ void __launch_bounds__(TW_BLOCK) k_tw_hub_warp(TwArgs A) {
+// ---- hub kernel: thread-block and warp tiers --------------------------------------
+// Every CTA first takes thread-block units (the whole CTA on one unit of a
+// hub's members, the row staged in the CTA's stage), then each warp takes
+// warp-tier hubs (row staged in the warp's stage).
+constexpr size_t TW_HUB_HDR = 128;  // barriers and cursors
+constexpr size_t TW_HUB_SMEM = TW_HUB_HDR + TW_STAGE_C + (size_t)(TW_BLOCK / 32) * TW_STAGE_W;
+
+template <int MINB>
+__global__ void __launch_bounds__(TW_BLOCK, MINB) k_tw_hub(TwArgs A) {
   extern __shared__ __align__(128) unsigned char dsm[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(dsm) + wib;
-  int* cursor = reinterpret_cast<int*>(dsm + 8 * (TW_BLOCK / 32)) + wib;
-  unsigned char* buf = dsm + 128 * ((12 * (TW_BLOCK / 32) + 127) / 128) + (size_t)wib * TW_STAGE_W;
-  if (lane == 0) {
-    mbar_init(bar, 1);
-    mbar_fence_init();
-  }
-  __syncwarp();
-  ItemStats st;
-  int mlen = 0;
-  const int64_t U = A.ctl->nwarp;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  uint32_t ph = 0;
-  for (int64_t u = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; u < U; u += nw) {
-    const TwUnit d = A.wunits[u];
-    if (lane == 0) {
-      *cursor = 0;
-      const TwRec* r0 = A.hrec + d.m0;
-      const void* src = nullptr;
-      const uint32_t bytes = tw_row_bytes(A, r0->lo, r0->deg, &src);
-      mbar_arrive_expect_tx(bar, bytes);
-      bulk_g2s(buf, src, bytes, bar);
-    }
-    __syncwarp();
-    tw_hub_members(A, d, buf, bar, ph, cursor, st, mlen);
-    ph ^= 1u;
-    __syncwarp();
-  }
-  flush_stats(st, A.P.ctr);
-  tw_flush_len(mlen, A.max_len);
-}
-
-// ---- thread-block tier: one CTA per unit of <= TW_UNIT members, row staged ----
-__global__ void __launch_bounds__(TW_BLOCK) k_tw_hub_cta(TwArgs A) {
-  extern __shared__ __align__(128) unsigned char dsm[];
-  __shared__ uint64_t bar;
-  __shared__ int cursor;
-  if (threadIdx.x == 0) {
-    mbar_init(&bar, 1);
-    mbar_fence_init();
-  }
+  uint64_t* cbar = reinterpret_cast<uint64_t*>(dsm);
+  uint64_t* wbar = cbar + 1 + wib;
+  int* ccur = reinterpret_cast<int*>(dsm + 8 * (1 + TW_BLOCK / 32));
+  int* wcur = ccur + 1 + wib;
+  int* s_u = ccur + 1 + TW_BLOCK / 32;
+  unsigned char* cbuf = dsm + TW_HUB_HDR;
+  unsigned char* wbuf = cbuf + TW_STAGE_C + (size_t)wib * TW_STAGE_W;
+  if (threadIdx.x == 0) mbar_init(cbar, 1);
+  if (lane == 0) mbar_init(wbar, 1);
+  if (threadIdx.x == 0) mbar_fence_init();
   __syncthreads();
   ItemStats st;
   int mlen = 0;
-  const int64_t U = A.ctl->nunit;
+  // thread-block tier
+  const int U = A.ctl->nunit;
   uint32_t ph = 0;
-  for (int64_t u = blockIdx.x; u < U; u += gridDim.x) {
+  while (true) {
+    if (threadIdx.x == 0) *s_u = U ? atomicAdd(&A.ctl->uq, 1) : U;
+    __syncthreads();
+    const int u = *s_u;
+    if (u >= U) break;
     const TwUnit d = A.cunits[u];
     if (threadIdx.x == 0) {
-      cursor = 0;
+      *ccur = 0;
       const TwRec* r0 = A.hrec + d.m0;
       const void* src = nullptr;
       const uint32_t bytes = tw_row_bytes(A, r0->lo, r0->deg, &src);
-      mbar_arrive_expect_tx(&bar, bytes);
-      bulk_g2s(dsm, src, bytes, &bar);
+      mbar_arrive_expect_tx(cbar, bytes);
+      bulk_g2s(cbuf, src, bytes, cbar);
     }
     __syncthreads();
-    tw_hub_members(A, d, dsm, &bar, ph, &cursor, st, mlen);
+    tw_hub_members(A, d, cbuf, cbar, ph, ccur, st, mlen);
     ph ^= 1u;
     __syncthreads();
+  }
+  // warp tier
+  const int W = A.ctl->nwarp;
+  uint32_t wph = 0;
+  while (true) {
+    int u = W;
+    if (lane == 0 && W) u = atomicAdd(&A.ctl->wq, 1);
+    u = __shfl_sync(0xffffffffu, u, 0);
+    if (u >= W) break;
+    const TwUnit d = A.wunits[u];
+    if (lane == 0) {
+      *wcur = 0;
+      const TwRec* r0 = A.hrec + d.m0;
+      const void* src = nullptr;
+      const uint32_t bytes = tw_row_bytes(A, r0->lo, r0->deg, &src);
+      mbar_arrive_expect_tx(wbar, bytes);
+      bulk_g2s(wbuf, src, bytes, wbar);
+    }
+    __syncwarp();
+    tw_hub_members(A, d, wbuf, wbar, wph, wcur, st, mlen);
+    wph ^= 1u;
+    __syncwarp();
   }
   flush_stats(st, A.P.ctr);
   tw_flush_len(mlen, A.max_len);
@@ -739,6 +663,18 @@ __global__ void __launch_bounds__(TW_BLOCK) k_tw_init(TwArgs A, const int64_t* _
       A.ndeg[row] = t >= 0 ? (int32_t)(__ldg(A.P.gv.row + t + 1) - __ldg(A.P.gv.row + t)) : 0;
     }
   }
+}
+
+// the window's first step: members counted (into the n* buffers) per row
+__global__ void __launch_bounds__(TW_BLOCK) k_tw_count0(TwArgs A) {
+  TwCounts cc;
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x; b < A.rows; b += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = b + threadIdx.x;
+    TwPend pd;
+    if (row < A.rows) tw_count_issue(A, pd, true, A.cur[row], row);
+    tw_count_take(A, pd, cc);
+  }
+  tw_flush_classes(cc, A.nstats);
 }
 
 // rows of a run that starts in the walker-major tail
@@ -788,7 +724,5 @@ __global__ void __launch_bounds__(256) k_tw_emit(const int32_t* __restrict__ out
   }
 }
 
-constexpr size_t TW_WARP_SMEM = 128 * ((12 * (TW_BLOCK / 32) + 127) / 128) + (size_t)(TW_BLOCK / 32) * TW_STAGE_W;
-constexpr size_t TW_CTA_SMEM = TW_STAGE_C;
 
 }  // namespace
