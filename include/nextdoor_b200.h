@@ -230,7 +230,9 @@ int nd_result_info(const nd_result *r, int64_t *n_samples, int64_t *n_steps,
 int nd_result_field(const nd_result *r, int field, const void **ptr, int64_t *count);
 /* counters: {items, pairs, n2v_tries, n2v_probes, search, pair_bytes,
  * slot_bytes (SURVEY 8(d) model bytes), steps, launches, rand_sectors (random
- * 32-byte sector reads the walk kernels issued)} */
+ * 32-byte sector reads the walk kernels issued), tp_staged (TP walks: hub
+ * members stepped from a row staged in shared memory), tp_inplace (TP walks:
+ * small-class and grid-tier walkers stepped from global rows)} */
 int nd_result_counters(const nd_result *r, int64_t *host_counters, int64_t n);
 /* Ensure ND_F_FINAL_IDS32 (int32 final ids; vertex ids < 2^31, the device
  * CSR's column width).  Every run now writes it directly, so this is a no-op

@@ -29,7 +29,7 @@ struct nd_graph {
 };
 
 constexpr int ND_N_FIELDS = 14;
-constexpr int ND_N_COUNTERS = 10;
+constexpr int ND_N_COUNTERS = 12;
 
 struct nd_result {
   int64_t n = 0;
@@ -58,7 +58,7 @@ struct nd_result {
 // counters slots (nd_result_counters)
 enum { NDC_ITEMS = 0, NDC_PAIRS = 1, NDC_N2V_TRIES = 2, NDC_N2V_PROBES = 3, NDC_SEARCH = 4,
        NDC_PAIR_BYTES = 5, NDC_SLOT_BYTES = 6, NDC_STEPS = 7, NDC_LAUNCHES = 8,
-       NDC_RAND_SECTORS = 9 };
+       NDC_RAND_SECTORS = 9, NDC_TP_STAGED = 10, NDC_TP_INPLACE = 11 };
 
 // app parameters as the kernels see them (_ckernels.pyx:157-181)
 struct NdApp {

@@ -1577,7 +1577,7 @@ static int run_chain_walk_hub(const nd_graph* G, const NdApp& a, int64_t sample_
   ND_CUDA_TRY(nd_alloc(&tot, n, s));
   ND_CUDA_TRY(nd_alloc(&maxlen, 1, s));
   ND_CUDA_TRY(nd_alloc(&stall, 1, s));
-  ND_CUDA_TRY(nd_alloc(&ctr, 4, s));
+  ND_CUDA_TRY(nd_alloc(&ctr, 6, s));  // [0..2] byte model, [4] staged, [5] in place
   ND_CUDA_TRY(nd_alloc(&stats, 4 * (max_steps + 1), s));
   ND_CUDA_TRY(nd_alloc(&ctl, 2, s));
   ND_CUDA_TRY(nd_alloc(&wunits, hcap, s));
@@ -1601,7 +1601,7 @@ static int run_chain_walk_hub(const nd_graph* G, const NdApp& a, int64_t sample_
   ND_CUDA_TRY(cudaMemsetAsync(tot, 0, n * sizeof(int64_t), s));
   ND_CUDA_TRY(cudaMemsetAsync(maxlen, 0, sizeof(int32_t), s));
   ND_CUDA_TRY(cudaMemsetAsync(stall, 0, sizeof(int), s));
-  ND_CUDA_TRY(cudaMemsetAsync(ctr, 0, 4 * sizeof(unsigned long long), s));
+  ND_CUDA_TRY(cudaMemsetAsync(ctr, 0, 6 * sizeof(unsigned long long), s));
   ND_CUDA_TRY(cudaMemsetAsync(stats, 0, 4 * (max_steps + 1) * sizeof(unsigned long long), s));
   if (!roots) {
     ND_CUDA_TRY(nd_alloc(&roots32, n * R, s));
@@ -1721,6 +1721,7 @@ static int run_chain_walk_hub(const nd_graph* G, const NdApp& a, int64_t sample_
     A.wid = wid;
     A.Lw = Lw;
     A.pos = pos;
+    A.tier = ctr + 4;
     A.out = W.out;
     A.nnz = W.nnz;
     A.died = died;
@@ -1869,13 +1870,15 @@ static int run_chain_walk_hub(const nd_graph* G, const NdApp& a, int64_t sample_
       if (W.n * W.Lw)
         k_pw_emit<<<nd_grid(W.n * 32, 256, nsm * 32), 256, 0, s>>>(W.wid, W.out, W.nnz, W.n, W.ld,
                                                                   W.step0, final_off, R, final_ids);
-    unsigned long long h_ctr[4];
+    unsigned long long h_ctr[6];
     ND_TRY(nd_d2h(&h_stall, stall, sizeof(int), s));
     ND_TRY(nd_d2h(h_ctr, ctr, sizeof(h_ctr), s));
     ND_CUDA_TRY(cudaGetLastError());
     res->counters[NDC_N2V_TRIES] = (int64_t)h_ctr[1];
     res->counters[NDC_SLOT_BYTES] = (int64_t)h_ctr[0];
     res->counters[NDC_RAND_SECTORS] = (int64_t)h_ctr[2];
+    res->counters[NDC_TP_STAGED] = (int64_t)h_ctr[4];
+    res->counters[NDC_TP_INPLACE] = (int64_t)h_ctr[5];
   }
   prof.mark();
   if (prof.on && rc == ND_OK) {

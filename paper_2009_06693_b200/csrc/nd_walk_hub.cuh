@@ -91,6 +91,7 @@ struct TwArgs {
   int32_t* ndeg;
   double* nhd;
   int32_t* pos;         // group position of the row's walker this step
+  unsigned long long* tier;  // [0] staged hub members stepped, [1] walkers stepped in place
   int32_t* out;         // [Lw, rows]
   int32_t* nnz;         // per row: non-NULL values of the window
   int32_t* died;        // per walker: ended with a NULL
@@ -354,6 +355,11 @@ __device__ __forceinline__ void tw_emit(const TwArgs& A, bool fin, const TwLane&
   }
 }
 
+__device__ __forceinline__ void tw_flush_tier(unsigned long long n, unsigned long long* dst) {
+  for (int o = 16; o > 0; o >>= 1) n += __shfl_down_sync(0xffffffffu, n, o);
+  if ((threadIdx.x & 31) == 0 && n) atomicAdd(dst, n);
+}
+
 __device__ __forceinline__ void tw_lane_start(const TwArgs& A, TwLane& L, ItemStats& st) {
   L.j = 0;
   L.ik = key_item((uint64_t)(A.P.sample_lo + L.w), 0, 0);
@@ -450,6 +456,7 @@ template <int MINB>
 __global__ void __launch_bounds__(TW_BLOCK, MINB) k_tw_sample(TwArgs A) {
   ItemStats st;
   int mlen = 0;
+  unsigned long long inplace = 0;
   tw_lanes<false>(A, A.rows, &A.ctl->queue, A.P.chunk, nullptr,
                   [&](int64_t row, TwLane& L) -> bool {
                     const int32_t v = A.cur[row];
@@ -490,11 +497,13 @@ __global__ void __launch_bounds__(TW_BLOCK, MINB) k_tw_sample(TwArgs A) {
                     L.tlo = tlo;
                     L.tdeg = tdeg;
                     tw_lane_start(A, L, st);
+                    inplace++;
                     return true;
                   },
                   st, mlen);
   flush_stats(st, A.P.ctr);
   tw_flush_len(mlen, A.max_len);
+  tw_flush_tier(inplace, A.tier + 1);
 }
 
 // bytes and source of the records a hub's members read this step
@@ -526,6 +535,7 @@ __device__ __forceinline__ void tw_hub_members(const TwArgs& A, const TwUnit& d,
   TwLane L;
   TwPend pd;
   TwCounts cc;
+  unsigned long long staged = 0;
   bool done = false, waited = false;
   while (true) {
     const bool need = L.row < 0 && !done;
@@ -536,8 +546,12 @@ __device__ __forceinline__ void tw_hub_members(const TwArgs& A, const TwUnit& d,
       base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
       if (need) {
         const int mem = d.m0 + base + __popc(m & lt_mask);
-        if (mem < d.m1) tw_load_rec(A, L, A.hrec + mem, st);
-        else done = true;
+        if (mem < d.m1) {
+          tw_load_rec(A, L, A.hrec + mem, st);
+          staged++;
+        } else {
+          done = true;
+        }
       }
     }
     if (__all_sync(0xffffffffu, L.row < 0 && done)) {
@@ -558,6 +572,7 @@ __device__ __forceinline__ void tw_hub_members(const TwArgs& A, const TwUnit& d,
   }
   if (!waited) mbar_wait(bar, parity);  // keep the barrier's phases in step
   tw_flush_classes(cc, A.nstats);
+  tw_flush_tier(staged, A.tier);
 }
 
 // ---- hub kernel: thread-block and warp tiers --------------------------------------

@@ -273,10 +273,11 @@ class DeviceRun:
         _lib.check(L.nd_result_info(handle, C.byref(n), C.byref(s), C.byref(ts), C.byref(tr)))
         self.n_samples, self.n_steps = n.value, s.value
         self.total_sampled, self.total_recorded = ts.value, tr.value
-        ctr = (C.c_int64 * 10)()
-        L.nd_result_counters(handle, ctr, 10)
+        ctr = (C.c_int64 * 12)()
+        L.nd_result_counters(handle, ctr, 12)
         self.counters = dict(zip(["items", "pairs", "n2v_tries", "n2v_probes", "search",
-                                  "pair_bytes", "slot_bytes", "steps", "launches", "rand_sectors"],
+                                  "pair_bytes", "slot_bytes", "steps", "launches", "rand_sectors",
+                                  "tp_staged", "tp_inplace"],
                                  list(ctr)))
         prof = (C.c_double * 4)()
         L.nd_result_profile(handle, prof, 4)
