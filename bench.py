@@ -406,22 +406,54 @@ def main():
                        "note": "int32 rows of both apps gathered to rank 0 after the timed steps"}
 
     # ---- the transit-parallel paradigm on the same job (reported alongside) ----------
+    # tp_run's engine (nd_walk_hub.cuh): per step, member counts fused into the
+    # previous step's emission, hub tiers, staged rows; the same two apps
+    # concurrently on two streams as the SP step, then each app alone
     tp_info = None
     if args.paradigm == "sp" and not args.no_tp:
-        tp_ms = []
+        from paper_2009_06693_b200.engine import run_device_concurrent
+        tp_ms, tp_app = [], {a.name: [] for a in apps}
+        tp_rows_equal = None
         for it in range(3):
             barrier()
             ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             ev0.record(stream)
-            for app in apps:
-                run_device(app, dg, n_samples=n, sample_lo=lo, seed=SEED, paradigm="tp").close()
+            runs = run_device_concurrent([dict(app=app, n_samples=n, sample_lo=lo, seed=SEED)
+                                          for app in apps], dg, paradigm="tp")
             ev1.record(stream)
             torch.cuda.synchronize()
             if it:
                 tp_ms.append(ev0.elapsed_time(ev1))
-        tp_info = {"ms_per_step": sum(tp_ms) / len(tp_ms),
-                   "value": (edges_dev / len(times)) / (sum(tp_ms) / len(tp_ms) / 1e3),
-                   "note": "TP = per-step radix sort + work classes + sub-warp/CTA/grid kernels; walker-major tail with exact class statistics below 131,072 alive walkers"}
+            else:  # the TP rows equal the SP rows (checked once, on device)
+                sp_runs = run_device_concurrent([dict(app=app, n_samples=n, sample_lo=lo, seed=SEED)
+                                                 for app in apps], dg, paradigm="sp")
+                tp_rows_equal = all(
+                    torch.equal(a.view(_lib.F_FINAL_OFF), b.view(_lib.F_FINAL_OFF))
+                    and torch.equal(a.narrow_ids(), b.narrow_ids())
+                    for a, b in zip(runs, sp_runs))
+                for dr in sp_runs:
+                    dr.close()
+            for dr in runs:
+                dr.close()
+        for it in range(2):
+            for app in apps:
+                ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                ev0.record(stream)
+                run_device(app, dg, n_samples=n, sample_lo=lo, seed=SEED, paradigm="tp").close()
+                ev1.record(stream)
+                torch.cuda.synchronize()
+                tp_app[app.name].append(ev0.elapsed_time(ev1))
+        tp_step = sum(tp_ms) / len(tp_ms)
+        tp_info = {"ms_per_step": tp_step,
+                   "value": (edges_dev / len(times)) / (tp_step / 1e3),
+                   "vs_sp": tp_step / (sum(times) / len(times)),
+                   "ms_per_app_alone": {k: min(v) for k, v in tp_app.items()},
+                   "rows_equal_sp": tp_rows_equal,
+                   "note": "tp_run's engine: per step, member counts fused into the previous step's "
+                           "emission (exact class statistics), prep of the hub tiers, sub-warp + "
+                           "grid tiers stepped in place, warp / thread-block tiers from rows staged "
+                           "by bulk copy; walker-major tail with exact class statistics below "
+                           "131,072 alive walkers; both apps concurrently as in the SP step"}
 
     # ---- e2e through the public API with host buffers ------------------------------
     # HostPipeline (paper_2009_06693_b200/streaming.py): roots uploaded from
