@@ -158,6 +158,13 @@ int nd_graph_build_index(nd_graph *g, int flags, void *stream);
 /* sizes and device pointers (read-only views) */
 int nd_graph_info(const nd_graph *g, int64_t *n_vertices, int64_t *n_edges, int *unit_weights,
                   int64_t *bytes);
+/* HBM footprint: CSR bytes at creation, bytes of the lazily built indexes and
+ * records, host time spent building them (ms), and bit sets of the structures
+ * built / left out for lack of room (1 vrec, 2 nbw, 4 nbp, 8 nbu, 16 guide,
+ * 32 hset, 64 pick lines).  A left-out structure means the kernels read the
+ * plain CSR instead: same answers, more dependent reads. */
+int nd_graph_footprint(const nd_graph *g, int64_t *csr_bytes, int64_t *index_bytes,
+                       double *prep_ms, int *built, int *skipped);
 int nd_graph_arrays(const nd_graph *g, const int64_t **row_offsets, const int32_t **col,
                     const double **weights, const double **prefix, const double **max_w);
 

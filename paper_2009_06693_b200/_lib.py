@@ -49,6 +49,8 @@ SIGNATURES = {
     "nd_graph_destroy": [vp],
     "nd_graph_build_index": [vp, i32, vp],
     "nd_graph_info": [vp, pi64, pi64, C.POINTER(C.c_int), pi64],
+    "nd_graph_footprint": [vp, pi64, pi64, C.POINTER(C.c_double), C.POINTER(C.c_int),
+                           C.POINTER(C.c_int)],
     "nd_graph_arrays": [vp, pp, pp, pp, pp, pp],
     "nd_uniform_roots": [vp, i64, u64, i64, i64, vp, vp],
     "nd_run_walk": [vp, i32, vp, i64, i64, i64, vp, i64, u64, i64, i64, i32, vp, pp],

@@ -356,6 +356,7 @@ static int graph_finish(nd_graph* G, const double* dev_w, const double* dev_pre,
     k_unit_max<<<nd_grid(V, 256), 256, 0, s>>>(G->row, V, G->mx);
   }
   graph_views(G);
+  G->csr_bytes = G->bytes;
   ND_CUDA_TRY(cudaGetLastError());
   ND_CUDA_TRY(cudaStreamSynchronize(s));
   return ND_OK;
@@ -643,6 +644,17 @@ extern "C" int nd_graph_info(const nd_graph* g, int64_t* n_vertices, int64_t* n_
   if (n_edges) *n_edges = g->g.E;
   if (unit_weights) *unit_weights = g->g.unit;
   if (bytes) *bytes = g->bytes;
+  return ND_OK;
+}
+
+extern "C" int nd_graph_footprint(const nd_graph* g, int64_t* csr_bytes, int64_t* index_bytes,
+                                  double* prep_ms, int* built, int* skipped) {
+  if (!g) return ND_ERR_ARG;
+  if (csr_bytes) *csr_bytes = g->csr_bytes;
+  if (index_bytes) *index_bytes = g->bytes - g->csr_bytes;
+  if (prep_ms) *prep_ms = g->prep_ms;
+  if (built) *built = g->built;
+  if (skipped) *skipped = g->skipped;
   return ND_OK;
 }
 

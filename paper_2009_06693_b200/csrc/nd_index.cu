@@ -8,6 +8,7 @@
 // searches they replace (tests/test_gpu_kernels.py::test_index_equivalence).
 #include <cub/cub.cuh>
 
+#include <chrono>
 #include <cstdlib>
 #include <mutex>
 
@@ -182,40 +183,84 @@ __global__ void k_build_lines(const int64_t* __restrict__ row, const int32_t* __
 // lazy index builds may be requested by concurrent runs on one graph
 static std::mutex g_index_mu;
 
+// Every structure below is an accelerator, not a requirement: the kernels
+// fall back to the plain CSR (row/col/weights/prefix, same answers) when a
+// pointer is null.  A structure is built only when it fits beside a margin
+// kept free for the runs' own buffers (walk windows, final rows, sort
+// scratch): ND_INDEX_MARGIN_MB, default 8 GiB.
+static bool room_for(double need) {
+  static const double margin = [] {
+    const char* e = getenv("ND_INDEX_MARGIN_MB");
+    return (e && e[0] ? atof(e) : 8192.0) * (1 << 20);
+  }();
+  size_t fr = 0, tot = 0;
+  if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) return false;
+  return need + margin <= (double)fr;
+}
+
+namespace {
+struct PrepTimer {  // host wall time of a build (each build ends in a stream sync)
+  nd_graph* G;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  explicit PrepTimer(nd_graph* g) : G(g) {}
+  ~PrepTimer() {
+    G->prep_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
+                      .count();
+  }
+};
+}  // namespace
+
 int nd_graph_ensure_records(nd_graph* G, int want_tries, cudaStream_t s) {
   static const bool disabled = getenv("ND_NO_PACK") && getenv("ND_NO_PACK")[0] == '1';
   if (disabled) return ND_OK;
   std::lock_guard<std::mutex> lock(g_index_mu);
   const int64_t V = G->g.V, E = G->g.E;
+  const bool need_vrec = !G->vrec && V > 0 && !(G->skipped & ND_IDX_VREC);
+  const bool need_nbu = E > 0 && G->g.unit && !G->nbu && !(G->skipped & ND_IDX_NBU);
+  const bool need_nbp = E > 0 && !G->g.unit && !G->nbp && !(G->skipped & ND_IDX_NBP);
+  const bool need_nbw = E > 0 && !G->g.unit && want_tries && !G->nbw && !(G->skipped & ND_IDX_NBW);
+  if (!need_vrec && !need_nbu && !need_nbp && !need_nbw) return ND_OK;
+  PrepTimer timer(G);
   bool built = false;
-  if (!G->vrec && V > 0) {
-    built = true;
-    ND_CUDA_TRY(cudaMalloc(&G->vrec, V * sizeof(VRec)));
-    G->bytes += V * sizeof(VRec);
-    k_build_vrec<<<nd_grid(V, 256), 256, 0, s>>>(G->row, G->mx, G->g.unit ? nullptr : G->pre, V,
-                                                  G->vrec);
-    ND_CUDA_TRY(cudaGetLastError());
-    G->g.vrec = G->vrec;
-  }
-  if (E > 0) {
-    NbrW* nw = nullptr;
-    NbrP* np_ = nullptr;
-    NbrU* nu = nullptr;
-    if (G->g.unit) {
-      if (!G->nbu) ND_CUDA_TRY(cudaMalloc(&nu, E * sizeof(NbrU)));
-    } else {
-      if (!G->nbp) ND_CUDA_TRY(cudaMalloc(&np_, E * sizeof(NbrP)));
-      if (want_tries && !G->nbw) ND_CUDA_TRY(cudaMalloc(&nw, E * sizeof(NbrW)));
-    }
-    if (nw || np_ || nu) {
+  if (need_vrec) {
+    if (room_for((double)V * sizeof(VRec))) {
       built = true;
-      k_build_nbr<<<nd_grid(E, 256, 148 * 64), 256, 0, s>>>(G->row, G->col, G->w, G->pre, G->mx,
-                                                             E, nw, np_, nu);
+      ND_CUDA_TRY(cudaMalloc(&G->vrec, V * sizeof(VRec)));
+      G->bytes += V * sizeof(VRec);
+      G->built |= ND_IDX_VREC;
+      k_build_vrec<<<nd_grid(V, 256), 256, 0, s>>>(G->row, G->mx, G->g.unit ? nullptr : G->pre, V,
+                                                    G->vrec);
       ND_CUDA_TRY(cudaGetLastError());
-      if (nw) { G->nbw = nw; G->g.nbw = nw; G->bytes += E * sizeof(NbrW); }
-      if (np_) { G->nbp = np_; G->g.nbp = np_; G->bytes += E * sizeof(NbrP); }
-      if (nu) { G->nbu = nu; G->g.nbu = nu; G->bytes += E * sizeof(NbrU); }
+      G->g.vrec = G->vrec;
+    } else {
+      G->skipped |= ND_IDX_VREC;
     }
+  }
+  NbrW* nw = nullptr;
+  NbrP* np_ = nullptr;
+  NbrU* nu = nullptr;
+  if (need_nbu) {
+    if (room_for((double)E * sizeof(NbrU))) ND_CUDA_TRY(cudaMalloc(&nu, E * sizeof(NbrU)));
+    else G->skipped |= ND_IDX_NBU;
+  }
+  if (need_nbp) {
+    if (room_for((double)E * sizeof(NbrP))) ND_CUDA_TRY(cudaMalloc(&np_, E * sizeof(NbrP)));
+    else G->skipped |= ND_IDX_NBP;
+  }
+  if (need_nbw) {  // tries read nbw only beside nbp: without nbp it would sit idle
+    if ((np_ || G->nbp) && room_for((double)E * sizeof(NbrW)))
+      ND_CUDA_TRY(cudaMalloc(&nw, E * sizeof(NbrW)));
+    else
+      G->skipped |= ND_IDX_NBW;
+  }
+  if (nw || np_ || nu) {
+    built = true;
+    k_build_nbr<<<nd_grid(E, 256, 148 * 64), 256, 0, s>>>(G->row, G->col, G->w, G->pre, G->mx, E,
+                                                           nw, np_, nu);
+    ND_CUDA_TRY(cudaGetLastError());
+    if (nw) { G->nbw = nw; G->g.nbw = nw; G->bytes += E * sizeof(NbrW); G->built |= ND_IDX_NBW; }
+    if (np_) { G->nbp = np_; G->g.nbp = np_; G->bytes += E * sizeof(NbrP); G->built |= ND_IDX_NBP; }
+    if (nu) { G->nbu = nu; G->g.nbu = nu; G->bytes += E * sizeof(NbrU); G->built |= ND_IDX_NBU; }
   }
   // other streams may use the records as soon as this call returns
   if (built) ND_CUDA_TRY(cudaStreamSynchronize(s));
@@ -227,24 +272,39 @@ int nd_graph_ensure_index(nd_graph* G, int want_hset, int want_guide, cudaStream
   if (disabled) return ND_OK;
   std::lock_guard<std::mutex> lock(g_index_mu);
   const int64_t V = G->g.V, E = G->g.E;
-  if (want_guide && !G->guide && !G->g.unit && E > 0) {
+  const bool need_guide = want_guide && !G->guide && !G->g.unit && E > 0 &&
+                          !(G->skipped & ND_IDX_GUIDE);
+  const bool need_hset = want_hset && !G->hset && E > 0 && !(G->skipped & ND_IDX_HSET);
+  if (!need_guide && !need_hset) return ND_OK;
+  PrepTimer timer(G);
+  if (need_guide) {
     // +8 entries: the walker kernels read guide entries as aligned 32-byte chunks
-    ND_CUDA_TRY(cudaMalloc(&G->guide, (E + 8) * sizeof(int32_t)));
-    G->bytes += E * 4;
-    k_build_guide<<<148 * 16, 256, 0, s>>>(G->row, G->pre, V, G->guide);
-    ND_CUDA_TRY(cudaGetLastError());
-    ND_CUDA_TRY(cudaStreamSynchronize(s));
-    G->g.guide = G->guide;
+    if (room_for((double)(E + 8) * sizeof(int32_t))) {
+      ND_CUDA_TRY(cudaMalloc(&G->guide, (E + 8) * sizeof(int32_t)));
+      G->bytes += E * 4;
+      G->built |= ND_IDX_GUIDE;
+      k_build_guide<<<148 * 16, 256, 0, s>>>(G->row, G->pre, V, G->guide);
+      ND_CUDA_TRY(cudaGetLastError());
+      ND_CUDA_TRY(cudaStreamSynchronize(s));
+      G->g.guide = G->guide;
+    } else {
+      G->skipped |= ND_IDX_GUIDE;
+    }
   }
-  if (want_hset && !G->hset && E > 0) {
+  if (need_hset) {
     // +8 slots: the walker kernels read the tables as aligned 32-byte chunks
-    ND_CUDA_TRY(cudaMalloc(&G->hset, (4 * E + 8) * sizeof(int32_t)));
-    G->bytes += 16 * E;
-    ND_CUDA_TRY(cudaMemsetAsync(G->hset, 0xFF, (4 * E + 8) * sizeof(int32_t), s));
-    k_build_hset<<<148 * 16, 256, 0, s>>>(G->row, G->col, V, G->hset);
-    ND_CUDA_TRY(cudaGetLastError());
-    ND_CUDA_TRY(cudaStreamSynchronize(s));
-    G->g.hset = G->hset;
+    if (room_for((double)(4 * E + 8) * sizeof(int32_t))) {
+      ND_CUDA_TRY(cudaMalloc(&G->hset, (4 * E + 8) * sizeof(int32_t)));
+      G->bytes += 16 * E;
+      G->built |= ND_IDX_HSET;
+      ND_CUDA_TRY(cudaMemsetAsync(G->hset, 0xFF, (4 * E + 8) * sizeof(int32_t), s));
+      k_build_hset<<<148 * 16, 256, 0, s>>>(G->row, G->col, V, G->hset);
+      ND_CUDA_TRY(cudaGetLastError());
+      ND_CUDA_TRY(cudaStreamSynchronize(s));
+      G->g.hset = G->hset;
+    } else {
+      G->skipped |= ND_IDX_HSET;
+    }
   }
   return ND_OK;
 }
@@ -253,7 +313,8 @@ int nd_graph_ensure_lines(nd_graph* G, cudaStream_t s) {
   static const bool disabled = getenv("ND_NO_LINES") && getenv("ND_NO_LINES")[0] == '1';
   if (disabled || G->g.unit || G->g.E <= 0) return ND_OK;
   std::lock_guard<std::mutex> lock(g_index_mu);
-  if (G->pl) return ND_OK;
+  if (G->pl || (G->skipped & ND_IDX_LINES)) return ND_OK;
+  PrepTimer timer(G);
   const int64_t V = G->g.V;
   int64_t *cnt = nullptr, *first = nullptr;
   ND_CUDA_TRY(nd_alloc(&cnt, V + 1, s));
@@ -270,18 +331,17 @@ int nd_graph_ensure_lines(nd_graph* G, cudaStream_t s) {
   int64_t n_lines = 0;
   ND_TRY(nd_d2h(&n_lines, first + V, sizeof(int64_t), s));
   ND_CUDA_TRY(cudaStreamSynchronize(s));
-  // int32 line offsets; and the layout is an accelerator, not a requirement:
-  // without room for it (plus a margin) the picks use the nbp records
-  size_t fr = 0, tot = 0;
-  cudaMemGetInfo(&fr, &tot);
-  const double need = (double)n_lines * sizeof(PickLine) + (double)V * 4 + (double)(2ull << 30);
-  if (n_lines >= (1ll << 31) || need > (double)fr) {
+  // int32 line offsets; without room the picks use the nbp records
+  const double need = (double)n_lines * sizeof(PickLine) + (double)V * 4;
+  if (n_lines >= (1ll << 31) || !room_for(need)) {
+    G->skipped |= ND_IDX_LINES;
     nd_free(cnt, s); nd_free(first, s);
     return ND_OK;
   }
   ND_CUDA_TRY(cudaMalloc(&G->vline, V * sizeof(int32_t)));
   ND_CUDA_TRY(cudaMalloc(&G->pl, (n_lines > 0 ? n_lines : 1) * sizeof(PickLine)));
   G->bytes += V * 4 + n_lines * (int64_t)sizeof(PickLine);
+  G->built |= ND_IDX_LINES;
   k_vline32<<<nd_grid(V, 256), 256, 0, s>>>(first, V, G->vline);
   k_build_lines<<<148 * 16, 256, 0, s>>>(G->row, G->col, G->pre, G->vline, V, G->pl);
   ND_CUDA_TRY(cudaGetLastError());

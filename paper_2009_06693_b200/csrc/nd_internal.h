@@ -24,9 +24,17 @@ struct nd_graph {
   nd::NbrU* nbu = nullptr;
   nd::PickLine* pl = nullptr;
   int32_t* vline = nullptr;
-  int64_t bytes = 0;
+  int64_t bytes = 0;       // everything resident (CSR + built indexes/records)
+  int64_t csr_bytes = 0;   // row/col/weights/prefix/max at creation
+  double prep_ms = 0.0;    // host wall time of the lazy index/record builds
+  int built = 0;           // ND_IDX_* bits of the structures built
+  int skipped = 0;         // ND_IDX_* bits left out for lack of room (plain-CSR path)
   int device = 0;
 };
+
+// nd_graph_footprint bits (one per optional structure, nd_index.cu)
+enum { ND_IDX_VREC = 1, ND_IDX_NBW = 2, ND_IDX_NBP = 4, ND_IDX_NBU = 8, ND_IDX_GUIDE = 16,
+       ND_IDX_HSET = 32, ND_IDX_LINES = 64 };
 
 constexpr int ND_N_FIELDS = 14;
 constexpr int ND_N_COUNTERS = 12;

@@ -400,12 +400,25 @@ class DeviceRun:
 
 def run_device(app, graph, samples=None, *, seed: int = 0, paradigm: str = "tp",
                step_cap: int = DEFAULT_STEP_CAP, n_samples: int | None = None,
-               sample_lo: int = 0, stream=None, sync: bool = True) -> DeviceRun:
-    """Run a whole sampling job on the device; outputs stay in HBM."""
+               sample_lo: int = 0, stream=None, sync: bool = True,
+               roots_device=None) -> DeviceRun:
+    """Run a whole sampling job on the device; outputs stay in HBM.
+
+    `roots_device` (walk and individual apps): a device int64 tensor
+    [n_samples * R] of caller-uploaded roots for samples [sample_lo,
+    sample_lo + n_samples), used in place of the keyed default roots."""
     torch = _lib.require_cuda()
     L = _lib.load()
     plan = describe(app)
     dg = as_device_graph(graph)
+    if roots_device is not None:
+        if plan.kind == "collective":
+            raise ValueError("roots_device is for walk and individual apps")
+        n = int(n_samples or 0)
+        if n <= 0 or roots_device.numel() % n or roots_device.dtype != torch.int64:
+            raise ValueError("roots_device must be int64 [n_samples * R]")
+        return _run_rooted(plan, dg, roots_device, roots_device.numel() // n, sample_lo, n, seed,
+                           paradigm, step_cap, stream, sync)
     if samples is None:
         samples = SampleRange(app, graph, sample_lo, n_samples or 0, seed)
     lo, n, roots, roots_off = _sample_spec(samples, plan, seed)
@@ -460,6 +473,32 @@ def run_device(app, graph, samples=None, *, seed: int = 0, paradigm: str = "tp",
     return DeviceRun(h, plan, dg, paradigm, lo, time.perf_counter() - t0)
 
 
+def _run_rooted(plan, dg, droots, R, lo, n, seed, paradigm, step_cap, stream, sync) -> DeviceRun:
+    """nd_run_walk / nd_run_individual with caller-uploaded device roots."""
+    import torch
+    L = _lib.load()
+    kp = np.ascontiguousarray(plan.kparams, dtype=np.float64)
+    par = _lib.ND_TP if paradigm == "tp" else _lib.ND_SP
+    sp = _lib.stream_ptr(stream)
+    h = C.c_void_p()
+    t0 = time.perf_counter()
+    if plan.kind == "walk":
+        _lib.check(L.nd_run_walk(dg.handle, plan.code, _lib.ptr(kp), len(kp), lo, n, _lib.ptr(droots),
+                                 R, C.c_uint64(seed & (2**64 - 1)), plan.steps, step_cap, par, sp,
+                                 C.byref(h)), "nd_run_walk")
+    else:
+        fan = np.ascontiguousarray(plan.fanouts, dtype=np.int64)
+        um = None if plan.unique is None else np.ascontiguousarray(plan.unique)
+        _lib.check(L.nd_run_individual(dg.handle, plan.code, _lib.ptr(kp), len(kp), _lib.ptr(fan),
+                                       len(fan), lo, n, _lib.ptr(droots), R,
+                                       C.c_uint64(seed & (2**64 - 1)), step_cap, par, _lib.ptr(um),
+                                       0 if um is None else len(um), sp, C.byref(h)),
+                   "nd_run_individual")
+    if sync:
+        torch.cuda.synchronize()
+    return DeviceRun(h, plan, dg, paradigm, lo, time.perf_counter() - t0)
+
+
 _JOB_STREAMS = []
 _JOB_POOL = None
 
@@ -488,7 +527,8 @@ def submit_device_concurrent(jobs, graph, *, paradigm: str = "sp",
     n_samples=..., sample_lo=0, seed=0).  Returns one future per job whose
     result is a finished DeviceRun (its outputs complete in HBM); a job whose
     tail leaves the GPU idle (a few long PPR walks) overlaps the others' bulk.
-    Outputs are exactly those of separate run_device calls."""
+    Outputs are exactly those of separate run_device calls; a job may carry
+    `roots_device` (run_device's caller-uploaded roots)."""
     import torch
     _lib.require_cuda()
     dg = as_device_graph(graph)
@@ -503,7 +543,8 @@ def submit_device_concurrent(jobs, graph, *, paradigm: str = "sp",
         with torch.cuda.stream(st):
             return run_device(job["app"], dg, n_samples=job["n_samples"],
                               sample_lo=job.get("sample_lo", 0), seed=job.get("seed", 0),
-                              paradigm=paradigm, step_cap=step_cap, stream=st, sync=False)
+                              paradigm=paradigm, step_cap=step_cap, stream=st, sync=False,
+                              roots_device=job.get("roots_device"))
 
     return [_job_pool(len(jobs)).submit(one, j, st) for j, st in zip(jobs, streams)]
 

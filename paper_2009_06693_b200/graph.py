@@ -238,6 +238,22 @@ class DeviceGraph:
                                              C.byref(B)))
         return B.value
 
+    INDEX_BITS = (("vrec", 1), ("nbw", 2), ("nbp", 4), ("nbu", 8), ("guide", 16), ("hset", 32),
+                  ("pick_lines", 64))
+
+    def footprint(self) -> dict:
+        """HBM held by the CSR and by the lazily built indexes/records, the host
+        time their builds took, and which were built or left out for lack of
+        room (nd_graph_footprint; left-out structures mean plain-CSR reads)."""
+        cb, ib = C.c_int64(), C.c_int64()
+        ms = C.c_double()
+        built, skipped = C.c_int(), C.c_int()
+        _lib.check(_lib.load().nd_graph_footprint(self._h, C.byref(cb), C.byref(ib), C.byref(ms),
+                                                  C.byref(built), C.byref(skipped)))
+        return {"csr_bytes": cb.value, "index_bytes": ib.value, "prep_ms": ms.value,
+                "built": [n for n, b in self.INDEX_BITS if built.value & b],
+                "skipped_no_room": [n for n, b in self.INDEX_BITS if skipped.value & b]}
+
     @property
     def remap(self):
         return self._remap

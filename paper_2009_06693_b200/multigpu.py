@@ -5,9 +5,11 @@ One process per GPU.  The graph is replicated (each rank regenerates the same
 keyed graph or uploads the same arrays); sample ids are split by
 ``worker_ranges`` and each rank runs its contiguous range with the global ids,
 so the concatenated rows are byte-identical to a single-GPU run.  The only
-collective is the final gather of the compacted rows to rank 0:
-``all_gather`` of the per-rank sizes, then a padded ``gather`` (NCCL over
-NVLink on GPUs, gloo on CPU tensors in the tests).
+collective is the final gather of the compacted rows to rank 0: an
+``all_gather`` of the per-rank sizes, then point-to-point sends of each
+rank's exact row bytes straight into their place in rank 0's output (NCCL
+over NVLink on GPUs, gloo on CPU tensors in the tests; no padding, no
+concatenation copy).
 """
 
 from __future__ import annotations
@@ -23,36 +25,57 @@ def gather_rows(off, ids, group=None, dst: int = 0):
     Works for any torch.distributed backend; tensors live on the backend's
     device (CUDA for NCCL, CPU for gloo).  `ids` may be int64 (F_FINAL_IDS) or
     int32 (F_FINAL_IDS32, half the NVLink bytes).  Returns (off, ids) concatenated in
-    rank order on `dst` (None elsewhere)."""
+    rank order on `dst` (None elsewhere).  On NCCL the transfers are queued
+    on the communicator's stream, ordered after the caller's current stream;
+    the returned tensors are ready for the caller's current stream."""
     import torch
     import torch.distributed as dist
     ws = dist.get_world_size(group)
     rank = dist.get_rank(group)
     if dist.get_backend(group) == "gloo" and ids.is_cuda:
-        off, ids = off.cpu(), ids.cpu()  # gloo gathers host tensors
+        off, ids = off.cpu(), ids.cpu()  # gloo moves host tensors
     dev = ids.device
     sizes = torch.tensor([off.numel() - 1, ids.numel()], dtype=torch.int64, device=dev)
     all_sizes = [torch.zeros_like(sizes) for _ in range(ws)]
     dist.all_gather(all_sizes, sizes, group=group)
-    n_max = int(max(s[0].item() for s in all_sizes))
-    e_max = int(max(s[1].item() for s in all_sizes))
-    pad_off = torch.zeros(n_max + 1, dtype=torch.int64, device=dev)
-    pad_off[:off.numel()] = off
-    pad_ids = torch.full((max(e_max, 1),), -1, dtype=ids.dtype, device=dev)
-    pad_ids[:ids.numel()] = ids
-    offs = [torch.empty_like(pad_off) for _ in range(ws)] if rank == dst else None
-    idss = [torch.empty_like(pad_ids) for _ in range(ws)] if rank == dst else None
-    dist.gather(pad_off, offs, dst=dst, group=group)
-    dist.gather(pad_ids, idss, dst=dst, group=group)
+    ns = [int(s[0]) for s in all_sizes]
+    es = [int(s[1]) for s in all_sizes]
+    peer = (lambda r: dist.get_global_rank(group, r)) if group is not None else (lambda r: r)
+    ops = []
     if rank != dst:
+        if ns[rank] > 0:  # offsets without the leading 0, then the ids
+            ops.append(dist.P2POp(dist.isend, off[1:].contiguous(), peer(dst), group))
+        if es[rank] > 0:
+            ops.append(dist.P2POp(dist.isend, ids.contiguous(), peer(dst), group))
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
         return None, None
-    out_off, out_ids, base = [torch.zeros(1, dtype=torch.int64, device=dev)], [], 0
+    out_off = torch.empty(sum(ns) + 1, dtype=torch.int64, device=dev)
+    out_ids = torch.empty(sum(es), dtype=ids.dtype, device=dev)
+    out_off[:1] = 0
+    n0, e0, bases = 0, 0, []
     for r in range(ws):
-        n_r, e_r = int(all_sizes[r][0]), int(all_sizes[r][1])
-        out_off.append(offs[r][1:n_r + 1] + base)
-        out_ids.append(idss[r][:e_r])
-        base += e_r
-    return torch.cat(out_off), torch.cat(out_ids)
+        o_sl = out_off[1 + n0:1 + n0 + ns[r]]
+        i_sl = out_ids[e0:e0 + es[r]]
+        if r == rank:
+            o_sl.copy_(off[1:])
+            i_sl.copy_(ids)
+        else:
+            if ns[r] > 0:
+                ops.append(dist.P2POp(dist.irecv, o_sl, peer(r), group))
+            if es[r] > 0:
+                ops.append(dist.P2POp(dist.irecv, i_sl, peer(r), group))
+        bases.append((o_sl, e0))
+        n0 += ns[r]
+        e0 += es[r]
+    if ops:
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+    for o_sl, base in bases:  # rank-local offsets -> global
+        if base and o_sl.numel():
+            o_sl += base
+    return out_off, out_ids
 
 
 def run_sharded(app, graph, n_samples: int, seed: int, paradigm: str = "sp", group=None):
@@ -70,3 +93,117 @@ def run_sharded(app, graph, n_samples: int, seed: int, paradigm: str = "sp", gro
         off, ids = off.clone(), ids.clone()
     dr.close()
     return off, ids
+
+
+class ShardedJob:
+    """A whole multi-app sampling job split over the ranks of `group`, through
+    the public API end to end (bench.py:123-153 +
+    driver.py:175-186 of the reference): every rank holds the replicated
+    graph and runs its ``worker_ranges`` share of each app's sample ids.
+
+    Per ``run()``: each rank uploads its shards' roots from pinned host memory,
+    samples every app concurrently (one stream and host thread per app), and
+    sends each app's compacted rows to `dst` as soon as that app finishes
+    (NCCL over NVLink; the gather of one app overlaps the others' sampling);
+    `dst` then copies the gathered rows into pinned host buffers
+    (``to_host``).  Rows on `dst` equal one single-GPU run of the whole job.
+
+    jobs: list of (app, n_samples_total, seed).  Roots are the keyed defaults
+    (apps.py:83-103), produced once at construction into pinned memory."""
+
+    def __init__(self, graph, jobs, group=None, dst: int = 0, paradigm: str = "sp",
+                 to_host: bool = True):
+        import ctypes as C
+        import torch
+        import torch.distributed as dist
+        from . import _lib
+        from .engine import describe
+        from .graph import as_device_graph
+        self.dg = as_device_graph(graph)
+        self.group, self.dst, self.paradigm, self.to_host = group, dst, paradigm, to_host
+        self.dist = dist.is_available() and dist.is_initialized()
+        ws = dist.get_world_size(group) if self.dist else 1
+        rank = dist.get_rank(group) if self.dist else 0
+        self.rank, self.ws = rank, ws
+        self.jobs = []
+        L = _lib.load()
+        for app, n_total, seed in jobs:
+            plan = describe(app)
+            lo, hi = shard_for_rank(n_total, ws, rank)
+            n = hi - lo
+            droots = torch.empty(max(n * plan.R, 1), dtype=torch.int64, device="cuda")
+            if n:
+                _lib.check(L.nd_uniform_roots(self.dg.handle, plan.R, C.c_uint64(seed), lo, n,
+                                              _lib.ptr(droots), _lib.stream_ptr()),
+                           "nd_uniform_roots")
+            roots_host = droots[:n * plan.R].cpu().pin_memory()
+            self.jobs.append(dict(app=app, n_total=n_total, seed=seed, lo=lo, n=n,
+                                  roots_host=roots_host))
+        self._host = {}
+        self._copy = torch.cuda.Stream()
+        self.last = {}
+
+    def _pinned(self, key, like):
+        import torch
+        b = self._host.get(key)
+        if b is None or b.numel() < like.numel() or b.dtype != like.dtype:
+            b = torch.empty(max(like.numel(), 1), dtype=like.dtype, pin_memory=True)
+            self._host[key] = b
+        return b[:like.numel()]
+
+    def run(self, order=None):
+        """One step.  Returns a list (job order) of (off, ids) host tensors on
+        `dst` (device tensors when to_host=False; None on other ranks), valid
+        until the next run.  `order`: the gather order of the jobs (the same on
+        every rank; default: job order).  self.last holds this rank's sampled
+        edge count and the H2D / D2H bytes of the step."""
+        import torch
+        from . import _lib
+        from .engine import job_streams, submit_device_concurrent
+        cur = torch.cuda.current_stream()
+        h2d = 0
+        specs = []
+        for j in self.jobs:
+            d = j["roots_host"].to("cuda", non_blocking=True) if j["n"] else None
+            h2d += j["roots_host"].numel() * 8 if j["n"] else 0
+            specs.append(dict(app=j["app"], n_samples=j["n"], sample_lo=j["lo"], seed=j["seed"],
+                              roots_device=d))
+        live = [i for i, s in enumerate(specs) if s["n_samples"] > 0]
+        futs = dict(zip(live, submit_device_concurrent([specs[i] for i in live], self.dg,
+                                                       paradigm=self.paradigm)))
+        streams = dict(zip(live, job_streams(len(live))))
+        out = [None] * len(self.jobs)
+        edges, d2h, runs = 0, 0, []
+        empty_off = torch.zeros(1, dtype=torch.int64, device="cuda")
+        empty_ids = torch.empty(0, dtype=torch.int32, device="cuda")
+        for i in (order if order is not None else range(len(self.jobs))):
+            if i in futs:
+                dr = futs[i].result()
+                runs.append(dr)
+                cur.wait_stream(streams[i])
+                edges += dr.total_sampled
+                off, ids = dr.view(_lib.F_FINAL_OFF), dr.narrow_ids()
+            else:
+                off, ids = empty_off, empty_ids
+            if self.dist and self.ws > 1:
+                off, ids = gather_rows(off, ids, self.group, self.dst)
+            if off is None:
+                continue
+            if self.to_host:  # rank dst: rows to pinned host memory on the copy stream
+                self._copy.wait_stream(cur)
+                ho, hi = self._pinned((i, "off"), off), self._pinned((i, "ids"), ids)
+                with torch.cuda.stream(self._copy):
+                    ho.copy_(off, non_blocking=True)
+                    hi.copy_(ids, non_blocking=True)
+                off.record_stream(self._copy)
+                ids.record_stream(self._copy)
+                d2h += off.numel() * 8 + ids.numel() * ids.element_size()
+                out[i] = (ho, hi)
+            else:
+                out[i] = (off.clone() if self.ws == 1 else off, ids.clone() if self.ws == 1 else ids)
+        if self.to_host:
+            cur.wait_stream(self._copy)
+        for dr in runs:  # freed once the current stream (gathers, copies) is past them
+            dr.close()
+        self.last = dict(edges=edges, h2d_bytes=h2d, d2h_bytes=d2h)
+        return out
