@@ -198,35 +198,157 @@ def host_graph_for_oracle(dg):
 
 # ---------------------------------------------------------------------------
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def split_ranges(lo, n, parts):
+    """worker_ranges (driver.py:175-186) of [lo, lo+n): contiguous, sizes
+    differing by at most one, larger first."""
+    parts = max(1, min(parts, n)) if n else 1
+    base, extra = divmod(n, parts)
+    out, a = [], lo
+    for w in range(parts):
+        b = a + base + (1 if w < extra else 0)
+        out.append((a, b))
+        a = b
+    return out
+
+
+# the reference itself (trawl, installed into baseline/_ref): forked worker
+# processes share the graph copy-on-write (the process-parallel plan of
+# BASELINE.md §3; the reference's own multi_worker_run, bench.py:123-153)
+_REF = {}
+
+
+def ref_trawl():
+    """Import the installed reference (baseline/_ref) with its compiled
+    kernels; (module, None) or (None, why)."""
+    path = os.path.join(REPO, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(path, "trawl")):
+        return None, "baseline/_ref/trawl is not installed"
+    if path not in sys.path:
+        sys.path.insert(0, path)
+    try:
+        import trawl
+    except Exception as e:  # noqa: BLE001
+        return None, f"import trawl failed: {e}"
+    if trawl.BACKEND_NAME != "compiled":
+        return None, f"trawl backend is {trawl.BACKEND_NAME}, not compiled"
+    return trawl, None
+
+
+def _ref_task(rng):
+    """One worker process: both apps over its sample-id range, each through
+    the reference engine (sp_run / tp_run) with global sample ids."""
+    trawl, g, engine = _REF["trawl"], _REF["graph"], _REF["engine"]
+    from trawl.bench import _make_sample_range
+    lo, hi = rng
+    edges, eng_s = 0, 0.0
+    for name, kw in APPS:
+        app = trawl.make_app(name, **kw)
+        samples = _make_sample_range(app, g, lo, hi, SEED)
+        t0 = time.perf_counter()
+        out = engine(app, g, samples, trawl.EngineConfig(seed=SEED, n_workers=1))
+        eng_s += time.perf_counter() - t0
+        edges += sum(s.total_sampled() for s in out.samples)
+    return edges, eng_s
+
+
+def trawl_walks(trawl, g, lo, n, procs, engine="sp"):
+    """node2vec + PPR for sample ids [lo, lo+n) through the reference engine
+    on `procs` forked processes.  Returns (edges, critical-path engine
+    seconds = the slowest process, wall seconds)."""
+    import multiprocessing as mp
+    _REF.update(trawl=trawl, graph=g, engine=trawl.sp_run if engine == "sp" else trawl.tp_run)
+    ranges = [r for r in split_ranges(lo, n, procs) if r[1] > r[0]]
+    t0 = time.perf_counter()
+    with mp.get_context("fork").Pool(len(ranges)) as pool:
+        res = pool.map(_ref_task, ranges, chunksize=1)
+    wall = time.perf_counter() - t0
+    return sum(r[0] for r in res), max(r[1] for r in res), wall
+
+
+def trawl_graph(trawl, hg):
+    """The reference's Graph over the same CSR arrays (prefix and max passed
+    through: bit-identical to the reference's own, checked by the golden
+    CSR tests)."""
+    return trawl.Graph(hg.n_vertices, np.asarray(hg.row_offsets, dtype=np.int64),
+                       np.asarray(hg.col_indices, dtype=np.int64),
+                       np.asarray(hg.weights, dtype=np.float64),
+                       np.arange(hg.n_vertices, dtype=np.int64),
+                       per_vertex_max_weight=np.asarray(hg.per_vertex_max_weight),
+                       per_vertex_weight_prefix=np.asarray(hg.per_vertex_weight_prefix))
+
+
+REF_SAMPLE = 1 << 18  # walkers per app per reference-arm step (BASELINE.md §3: >= 2^17)
+
+
 def run_reference(args):
-    """--impl reference: the reference's CPU implementation of the path (the
-    C oracle port; oracle/_ref is not buildable for a Python reference) on all
-    host cores, bounded sample per step, same metric/config."""
-    import torch
+    """--impl reference: the reference itself (trawl from baseline/_ref, its
+    compiled kernels, sp_run) on all host cores in forked worker processes,
+    over a bounded prefix of the same walks per step; the C oracle port
+    timed beside it on the same sample.  The input graph is built on the
+    host by the oracle's keyed RMAT generator and from_edges (the same CSR
+    the GPU arm builds on device; no library of this repo is loaded)."""
     ws, rank, local = dist_env()
     if rank != 0:
         return 0
     cores = len(os.sched_getaffinity(0))
-    from paper_2009_06693_b200.graph import DeviceGraph
-    torch.cuda.set_device(0)
-    dg = DeviceGraph.rmat(DEV_SCALE or SCALE, n_edges=N_EDGES, seed=GRAPH_SEED, weighted=True)
-    hg = host_graph_for_oracle(dg)
-    dg.close()
-    times, edges_tot = [], 0
+    from oracle import oracle as O
+    scale = DEV_SCALE or SCALE
+    t0 = time.perf_counter()
+    src, dst, w = O.rmat_edges(scale, N_EDGES, seed=GRAPH_SEED, undirected=False, weighted=True)
+    og = O.from_edges(src, dst, w, 1 << scale)
+    del src, dst, w
+    build_s = time.perf_counter() - t0
+    sample = min(REF_SAMPLE, 1 << scale)
+    trawl, why = ref_trawl()
+    kind = "reference" if trawl is not None else "port"
+    if trawl is not None:
+        g = trawl_graph(trawl, og)
+    times, walls, edges_tot = [], [], 0
     for i in range(args.warmup + args.steps):
-        e, dt, _ = cpu_walks(hg, 0, CPU_SAMPLE, cores)
+        if trawl is not None:
+            e, crit, wall = trawl_walks(trawl, g, 0, sample, cores, engine=args.ref_engine)
+        else:
+            e, crit, _ = cpu_walks(og, 0, sample, cores)
+            wall = crit
         if i >= args.warmup:
-            times.append(dt)
+            times.append(crit)
+            walls.append(wall)
             edges_tot += e
     value = edges_tot / sum(times)
+    # the oracle port on the same sample, for the record (and the check that
+    # both CPU implementations sampled the same edges)
+    pe, pdt, _ = cpu_walks(og, 0, sample, cores)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "edges/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
         "scaling": args.scaling, "vs_baseline": None, "dtype": "int64+f64", "data": "synthetic",
-        "config": config_dict(args.gpus, note="CPU oracle port, bounded sample", scaling=args.scaling),
-        "cpu_baseline": {"value": value, "unit": "edges/s", "cores": cores, "kind": "port",
-                         "sample": f"node2vec+PPR walks of sample ids [0, {CPU_SAMPLE}) per step"},
+        "config": config_dict(args.gpus, scaling=args.scaling),
+        "cpu_baseline": {
+            "value": value, "unit": "edges/s", "cores": cores, "kind": kind,
+            "cpu_model": cpu_model(),
+            "sample": f"node2vec+PPR walks of sample ids [0, {sample}) per step "
+                      f"({edges_tot // len(times)} edges)",
+            "how": (f"trawl {args.ref_engine}_run (baseline/_ref, compiled kernels) in {cores} forked "
+                    "processes over worker_ranges; time = slowest process's engine time"
+                    if trawl is not None else f"C oracle port, {cores} threads ({why})"),
+            "wall_ms_per_step": 1e3 * sum(walls) / len(walls),
+            "port": {"value": pe / pdt, "cores": cores, "edges": pe,
+                     "same_edges_as_reference": (pe == edges_tot // len(times))
+                     if trawl is not None else None},
+            "graph": f"keyed RMAT scale {scale} on the host (oracle rmat_edges + from_edges), "
+                     f"{og.n_edges} edges, {build_s:.1f} s, outside the timed steps"},
         "e2e": {"value": value, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -252,6 +374,191 @@ def config_dict(n_gpus, note=None, concurrent=True, scaling="weak"):
     return c
 
 
+# ---------------------------------------------------------------------------
+# C5 (BASELINE.json configs[4]): DeepWalk + k-hop on the 1B-edge RMAT graph,
+# the job split over the ranks (worker_ranges), rows gathered to rank 0
+
+C5_SCALE, C5_EDGES, C5_WALKERS, C5_ROOTS = 26, 1 << 30, 1 << 23, 1 << 20
+
+
+def c5_leg(args, ws, rank, barrier, rdev):
+    """Strong-sharded C5 step through multigpu.ShardedJob: each rank builds the
+    same keyed graph (replicated), runs its worker_ranges share of the 2^23
+    DeepWalk walkers and the 2^20 k-hop (25, 10) roots concurrently, and sends
+    each app's rows to rank 0 over NCCL as soon as the app finishes (k-hop
+    first; its gather overlaps DeepWalk).  `value` includes the gather; `e2e`
+    adds the roots' upload from pinned host memory on every rank and rank 0's
+    copy of all gathered rows to pinned host memory."""
+    import torch
+    from paper_2009_06693_b200 import _lib, make_app
+    from paper_2009_06693_b200.engine import run_device
+    from paper_2009_06693_b200.graph import DeviceGraph
+    from paper_2009_06693_b200.multigpu import ShardedJob
+    from paper_2009_06693_b200.sharding import shard_for_rank
+    dev = DEV_SCALE is not None
+    scale = DEV_SCALE if dev else C5_SCALE
+    n_edges = (16 << scale) if dev else C5_EDGES
+    walkers = (1 << (scale - 3)) if dev else C5_WALKERS
+    roots = (1 << (scale - 6)) if dev else C5_ROOTS
+    L = _lib.load()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    dg = DeviceGraph.rmat(scale, n_edges=n_edges, seed=GRAPH_SEED, weighted=True)
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t0
+    dw, kh = make_app("deepwalk"), make_app("khop", fanouts=[25, 10])
+    jobs = [(dw, walkers, SEED), (kh, roots, SEED)]
+    order = [1, 0]  # k-hop finishes first: its rows travel while DeepWalk samples
+    stream = torch.cuda.current_stream()
+
+    def timed_steps(job, k, w):
+        for _ in range(w):
+            job.run(order)
+        barrier()
+        times, edges, last = [], 0, None
+        for _ in range(k):
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            last = job.run(order)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+            edges += job.last["edges"]
+        ms = torch.tensor([sum(times)], dtype=torch.float64, device=rdev)
+        ed = torch.tensor([edges], dtype=torch.int64, device=rdev)
+        if ws > 1:
+            torch.distributed.all_reduce(ms, op=torch.distributed.ReduceOp.MAX)
+            torch.distributed.all_reduce(ed)
+        return ms.item(), int(ed.item()), last
+
+    dev_job = ShardedJob(dg, jobs, to_host=False)
+    dev_ms, dev_edges, rows = timed_steps(dev_job, args.steps, args.warmup)
+    # rows on rank 0 (the whole job, in sample order): a checksum that is the
+    # same at every N when the gathered rows equal the single-GPU run's
+    checks = None
+    if rank == 0:
+        checks = {}
+        for (app, n_total, _), (off, ids) in zip(jobs, rows):
+            checks[app.name] = {"rows": int(off.numel() - 1), "values": int(ids.numel()),
+                                "sum_ids": int(ids.to(torch.int64).sum().item()),
+                                "sum_off": int(off.sum().item())}
+    host_job = ShardedJob(dg, jobs, to_host=True)
+    e2e_ms, e2e_edges, _ = timed_steps(host_job, args.steps, max(1, args.warmup // 2))
+    h2d, d2h = host_job.last["h2d_bytes"], host_job.last["d2h_bytes"]
+    del dev_job, host_job, rows
+    # each app's own kernel rate on this rank's shard (apps one after another,
+    # event-timed launches; SURVEY 8(d) bytes counted on device)
+    L.nd_set_profiling(1)
+    kern = {}
+    for app, n_total, _ in jobs:
+        lo, hi = shard_for_rank(n_total, ws, rank)
+        ms_k, b_k, e_k = 0.0, 0, 0
+        for it in range(2):
+            dr = run_device(app, dg, n_samples=hi - lo, sample_lo=lo, seed=SEED, paradigm="sp")
+            if it:
+                ms_k, b_k, e_k = dr.profile_ms[1], dr.counters["slot_bytes"], dr.total_sampled
+            dr.close()
+        kern[app.name] = (ms_k, b_k, e_k)
+    L.nd_set_profiling(0)
+    fp = dg.footprint()
+    dg.close()
+    torch.cuda.empty_cache()
+    peak, peak_kind = peaks()
+    roof = {}
+    for name, (ms_k, b_k, e_k) in kern.items():
+        gbs = b_k / (ms_k / 1e3) / 1e9 if ms_k > 0 else None
+        roof[name] = {"kernel": "k_walk_persistent" if name == "deepwalk" else "k_fx_sample (fixed layout)",
+                      "achieved": gbs, "peak": peak, "unit": "GB/s", "peak_kind": peak_kind,
+                      "frac": gbs / peak if gbs else None, "kernel_ms": ms_k,
+                      "algorithmic_bytes": b_k, "edges": e_k,
+                      "edges_per_s": e_k / (ms_k / 1e3) if ms_k > 0 else None}
+    return {
+        "workload": (f"C5: RMAT scale {scale} ({dg.n_vertices:,} V, {dg.n_edges:,} directed weighted E), "
+                     f"DeepWalk {walkers:,} walkers x 100 + k-hop (25,10) {roots:,} roots, "
+                     f"split over {ws} GPU(s) by worker_ranges, rows gathered to rank 0 (NCCL)"
+                     + ("" if not dev else " [dev scale: NOT C5]")),
+        "value": dev_edges / (dev_ms / 1e3), "unit": "edges/s", "ms_per_step": dev_ms / args.steps,
+        "scaling": "strong", "steps": args.steps, "warmup": args.warmup,
+        "timing": "CUDA events around ShardedJob.run (sampling + NCCL gather of both apps' rows "
+                  "to rank 0), max over ranks",
+        "edges_per_step": dev_edges / args.steps,
+        "e2e": {"value": e2e_edges / (e2e_ms / 1e3), "unit": "edges/s",
+                "ms_per_step": e2e_ms / args.steps, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h,
+                "result": "rank 0: every rank's final rows (int64 offsets + int32 ids) in pinned host memory",
+                "timing": "roots H2D on every rank + sampling + NCCL gather + rank-0 D2H, per step"},
+        "rows_on_rank0": checks,
+        "per_rank_kernels": roof,
+        "graph": {"build_s": build_s, **fp},
+        "note": "strong scaling: the same 2^23 + 2^20 samples at every N; the checksums of rank 0's "
+                "rows are identical at every N when the gathered rows equal the 1-GPU run",
+    }
+
+
+def c3_leg(args, ws, rank, barrier, rdev):
+    """C3 (BASELINE.json configs[2]): GraphSAGE k-hop (25, 10) on the
+    Reddit-shaped RMAT-18 graph (57.3M undirected edges, 114.6M directed, unit
+    weights), 228 batches of 1024 roots as one launch, this rank's
+    worker_ranges share; SP (fixed layout) and TP (hub-bucket inversion)
+    event-timed, the sampling kernels' §8(d) bytes against the HBM peak."""
+    import torch
+    from paper_2009_06693_b200 import _lib, make_app
+    from paper_2009_06693_b200.engine import profiling, run_device
+    from paper_2009_06693_b200.graph import DeviceGraph
+    from paper_2009_06693_b200.sharding import shard_for_rank
+    dev = DEV_SCALE is not None
+    scale = min(DEV_SCALE, 18) if dev else 18
+    dg = DeviceGraph.rmat(scale, n_edges=int(57_300_000 / (1 << 18) * (1 << scale)), seed=GRAPH_SEED,
+                          undirected=True, weighted=False)
+    app = make_app("khop", fanouts=[25, 10])
+    N = 1024 * 228
+    lo, hi = shard_for_rank(N, ws, rank)
+    stream = torch.cuda.current_stream()
+    peak, peak_kind = peaks()
+    out = {"workload": f"C3: k-hop (25,10), {N:,} roots (228 x 1024) on RMAT scale {scale} "
+                       f"({dg.n_vertices:,} V, {dg.n_edges:,} directed unit E), split over {ws} GPU(s)"
+                       + (" [dev scale: NOT C3]" if dev else "")}
+    for par in ("sp", "tp"):
+        for _ in range(3):
+            run_device(app, dg, n_samples=hi - lo, sample_lo=lo, seed=SEED, paradigm=par).close()
+        ms_l, edges = [], 0
+        for _ in range(5):
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            dr = run_device(app, dg, n_samples=hi - lo, sample_lo=lo, seed=SEED, paradigm=par,
+                            sync=False)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms_l.append(e0.elapsed_time(e1))
+            edges = dr.total_sampled
+            dr.close()
+        with profiling():
+            dr = run_device(app, dg, n_samples=hi - lo, sample_lo=lo, seed=SEED, paradigm=par)
+        k_ms, k_bytes, steps = dr.profile_ms[1], dr.counters["slot_bytes"], dr.step_ms
+        dr.close()
+        ms = torch.tensor([statistics.median(ms_l)], dtype=torch.float64, device=rdev)
+        ed = torch.tensor([edges], dtype=torch.int64, device=rdev)
+        if ws > 1:
+            torch.distributed.all_reduce(ms, op=torch.distributed.ReduceOp.MAX)
+            torch.distributed.all_reduce(ed)
+        gbs = k_bytes / (k_ms / 1e3) / 1e9 if k_ms > 0 else None
+        out[par] = {"ms": ms.item(), "edges": int(ed.item()),
+                    "value": int(ed.item()) / (ms.item() / 1e3), "unit": "edges/s",
+                    "timing": "median of 5 event-timed whole runs (sampling, inversion, compaction)",
+                    "roofline": {"achieved": gbs, "peak": peak, "unit": "GB/s", "peak_kind": peak_kind,
+                                 "frac": gbs / peak if gbs else None,
+                                 "kernel_ms": k_ms, "algorithmic_bytes": k_bytes,
+                                 "step_build_sample_ms": steps,
+                                 "kernels": "k_fx_sample" if par == "sp" else
+                                            "k_fx_small + k_fx_hub_warp + k_fx_hub_cta"}}
+    out["tp_vs_sp"] = out["tp"]["ms"] / out["sp"]["ms"]
+    dg.close()
+    torch.cuda.empty_cache()
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -261,6 +568,10 @@ def main():
     ap.add_argument("--paradigm", default="sp", choices=["sp", "tp"])
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-tp", action="store_true")
+    ap.add_argument("--no-c5", action="store_true", help="skip the C5 (1B-edge, strong-sharded) leg")
+    ap.add_argument("--no-c3", action="store_true", help="skip the C3 (k-hop) leg")
+    ap.add_argument("--ref-engine", default="sp", choices=["sp", "tp"],
+                    help="the reference engine timed by --impl reference (sp_run: its faster CPU path)")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--gather", action="store_true",
                     help="also time an NCCL gather of every rank's rows to rank 0 (reported separately)")
@@ -533,12 +844,18 @@ def main():
     L.nd_set_profiling(0)
     samp_s = rf_ms / 1e3
     achieved = (rf_bytes / samp_s / 1e9) if samp_s > 0 else None
-    traffic = None
-    prof_json = os.path.join(REPO, "profiles", "r01_ncu_summary.json")
-    if os.path.exists(prof_json):
+    # DRAM bytes of the same kernel launches from the newest committed
+    # `ncu --set full` capture of this code (tools/ncu_walk.sh writes it each
+    # round; ncu cannot run inside the timed bench)
+    traffic, traffic_src = None, None
+    import glob
+    for prof_json in sorted(glob.glob(os.path.join(REPO, "profiles", "r*_ncu_summary.json")),
+                            reverse=True):
         try:
             with open(prof_json) as fh:
                 traffic = json.load(fh).get("traffic_bytes_per_step")
+            traffic_src = os.path.relpath(prof_json, REPO)
+            break
         except Exception:
             traffic = None
     # the random-gather ceiling of this GPU (nd_gather_ceiling: dependent random
@@ -564,9 +881,25 @@ def main():
         cores = len(os.sched_getaffinity(0))
         hg = host_graph_for_oracle(dg)
         ce, cdt, cres = cpu_walks(hg, 0, CPU_SAMPLE, cores)
-        cpu = {"value": ce / cdt, "unit": "edges/s", "cores": cores, "kind": "port",
-               "sample": f"node2vec+PPR walks for sample ids [0, {CPU_SAMPLE}) "
-                         f"({ce} edges, {cdt:.1f} s)"}
+        port = {"value": ce / cdt, "unit": "edges/s", "cores": cores, "kind": "port",
+                "sample": f"node2vec+PPR walks for sample ids [0, {CPU_SAMPLE}) "
+                          f"({ce} edges, {cdt:.1f} s)", "threads": cores}
+        cpu = dict(port)
+        # the reference itself (trawl from baseline/_ref) on the same cores,
+        # forked worker processes over a bounded prefix
+        trawl, why = ref_trawl()
+        if trawl is not None:
+            re_, crit, wall = trawl_walks(trawl, trawl_graph(trawl, hg), 0,
+                                          min(REF_SAMPLE, CPU_SAMPLE), cores)
+            cpu = {"value": re_ / crit, "unit": "edges/s", "cores": cores, "kind": "reference",
+                   "sample": f"node2vec+PPR walks for sample ids [0, {min(REF_SAMPLE, CPU_SAMPLE)}) "
+                             f"({re_} edges)",
+                   "how": f"trawl sp_run (baseline/_ref, compiled kernels) in {cores} forked "
+                          "processes over worker_ranges; time = slowest process's engine time",
+                   "wall_s": wall, "port": port}
+        else:
+            cpu["reference_unavailable"] = why
+        cpu["cpu_model"] = cpu_model()
         # parity of every sampled row on the CPU sample: offsets and every
         # vertex id (root, then the walk's non-NULL steps, chain.py:166-179)
         parity = True
@@ -576,6 +909,14 @@ def main():
             dr.close()
             parity &= bool(rows_equal_chain(off, ids, cres["roots"], cres[name]))
         parity_values = int(sum(len(cres[k]["chain_vals"]) for k in ("node2vec", "ppr")))
+
+    c2_footprint = dg.footprint()
+    dg.close()
+    torch.cuda.empty_cache()
+    c3 = None if args.no_c3 else c3_leg(args, ws, rank, barrier, rdev)
+    c5 = None
+    if not args.no_c5:
+        c5 = c5_leg(args, ws, rank, barrier, rdev)
 
     if rank == 0:
         ms_per_step = tot_ms / len(times)
@@ -595,6 +936,11 @@ def main():
                               "barrier + synchronize around all K"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                         "traffic_source": traffic_src,
+                         # traffic is per step; samp_s covers the 2 timed passes
+                         "dram_gbs": (traffic / (samp_s / 2) / 1e9) if (traffic and samp_s > 0) else None,
+                         "dram_frac": (traffic / (samp_s / 2) / 1e9 / peak) if (traffic and samp_s > 0)
+                         else None,
                          "kernel": "k_walk_persistent" if args.paradigm == "sp" else "TP class kernels",
                          "peak_kind": peak_kind,
                          "bytes_model": "SURVEY 8(d) sector model, counted on device",
@@ -609,6 +955,9 @@ def main():
             "paradigm_tp": tp_info,
             "clocks": clocks.summary(), "gpu_launches": launches, "gather": gather_info,
             "edges_per_step": edges_all / len(times),
+            "graph_footprint": c2_footprint,
+            "c3": c3,
+            "c5": c5,
         }
         print(json.dumps(line), flush=True)
     if ws > 1:

@@ -251,6 +251,14 @@ int nd_result_copy(const nd_result *r, int field, void *dst, void *stream);
 /* event-timed phases when nd_set_profiling(1): {schedule_ms, sample_ms,
  * compaction_ms, 0} */
 int nd_result_profile(const nd_result *r, double *ms, int64_t n);
+/* Per-step event times when nd_set_profiling(1) was on during the run
+ * (StepTiming.build_s / sample_s, driver.py:42-48, transit_parallel.py:204-228):
+ * build = the step's transit->sample inversion / scheduling index, sample =
+ * its sampling kernels.  *n_out = the number of timed steps (0 for the
+ * walker-major SP walk kernel, which has no step boundaries); up to n_max are
+ * written. */
+int nd_result_step_times(const nd_result *r, double *build_ms, double *sample_ms, int64_t n_max,
+                         int64_t *n_out);
 int nd_set_profiling(int on);
 /* Measured ceiling of dependent random 32-byte sector reads (sectors/s): one
  * pointer-chasing chain per thread, ctas_per_sm x 256 threads per SM, over a

@@ -559,6 +559,7 @@ extern "C" int nd_run_collective(const nd_graph* G, int kind, int64_t step_size,
                                  const int64_t* roots_in, uint64_t seed, int64_t step_cap,
                                  const uint8_t* host_unique, int64_t n_unique, void* stream,
                                  nd_result** out_res) {
+  NvtxRange nvtx_run("nd_run_collective");
   nd_pool_init();
   if (!G || n < 0 || sample_lo < 0 || step_size < 1 || kind < 0 || kind > 3) return kind < 0 || kind > 3 ? ND_ERR_APP : ND_ERR_ARG;
   cudaStream_t s = (cudaStream_t)stream;
@@ -669,9 +670,11 @@ extern "C" int nd_run_collective(const nd_graph* G, int kind, int64_t step_size,
   const int key_bits = key_bits_for(V);
   int64_t step = 0;
   int64_t total_rec = 0;
+  Profiler prof(s);
   while (step < S_max) {
     if (n) k_alive_from_toff<<<nd_grid(n, 256), 256, 0, s>>>(toff, n, alive);
     if (T == 0) break;  // no sample has transits (is_alive, core.py:195-203)
+    prof.step_begin();
     CStep cs;
     // TP build statistics over the step's transit occurrences
     {
@@ -701,6 +704,7 @@ extern "C" int nd_run_collective(const nd_graph* G, int kind, int64_t step_size,
     ND_CUDA_TRY(nd_alloc(&cdeg, T + 1, s));
     k_tdeg<<<nd_grid(T + 1, 256), 256, 0, s>>>(tv, T, g.row, dg);
     ND_TRY(scan_excl(dg, cdeg, T + 1, s));
+    prof.step_built();
     int32_t* out = nullptr;
     int32_t* rec1 = nullptr;
     ND_CUDA_TRY(nd_alloc(&out, n * m, s));
@@ -812,6 +816,7 @@ extern "C" int nd_run_collective(const nd_graph* G, int kind, int64_t step_size,
       nd_free(bm, s); nd_free(ucnt, s); nd_free(ubase, s); nd_free(hb, s);
     }
     total_rec += cs.nrec;
+    prof.step_sampled();
     const bool uniq = nd_unique_at(host_unique, n_unique, step);
     // next transits = non-NULL slots (stable); with unique() the sorted distinct
     // values per sample (finish_step, driver.py:165-172)
@@ -960,6 +965,12 @@ extern "C" int nd_run_collective(const nd_graph* G, int kind, int64_t step_size,
   res->set(ND_F_REC_V, rec_v, total_rec);
   res->set(ND_F_STATS, stats, 4 * n_steps);
   res->counters[NDC_STEPS] = n_steps;
+  if (prof.on) {  // the stream was synchronised above
+    const auto st = prof.to_result(res);
+    res->prof_ms[0] = st[0];
+    res->prof_ms[1] = st[1];
+  }
+  prof.destroy();
   *out_res = res;
   return ND_OK;
 }

@@ -202,6 +202,7 @@ namespace {
 struct PrepTimer {  // host wall time of a build (each build ends in a stream sync)
   nd_graph* G;
   std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  NvtxRange nvtx{"nd_graph index build"};
   explicit PrepTimer(nd_graph* g) : G(g) {}
   ~PrepTimer() {
     G->prep_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)

@@ -1318,17 +1318,21 @@ static int run_individual_fixed(const nd_graph* G, const NdApp& a, const int64_t
     ND_CUDA_TRY(nd_alloc(&vinfo, g.V, s));
     ND_CUDA_TRY(nd_alloc(&nhub, 2, s));  // [0] hubs, [1] small parents
   }
+  Profiler prof(s);
   for (int64_t k = 0; k < S; k++) {
     ND_CUDA_TRY(nd_alloc(&rank[k], n * B[k], s));
     ND_CUDA_TRY(nd_alloc(&nn[k], n, s));
     ND_CUDA_TRY(nd_alloc(&blk[k + 1], n * B[k + 1], s));
     const int64_t items = n * B[k + 1];
+    prof.step_begin();
     if (!tp) {
       k_fx_rank<<<nd_grid(n * 32, 256, 148 * 32), 256, 0, s>>>(blk[k], n, B[k], rank[k], nn[k],
                                                               stats + 4 * k + 3);
+      prof.step_built();
       k_fx_sample<<<nd_grid(items, IND_BLOCK, 148 * 64), IND_BLOCK, 0, s>>>(
           gv, a, key_base(seed, (uint64_t)k, 0, 0), sample_lo, n, FastDiv((uint32_t)B[k]),
           FastDiv((uint32_t)fan[k]), blk[k], rank[k], blk[k + 1], scnt, stall, ctr);
+      prof.step_sampled();
       continue;
     }
     if (sort_tp) {  // ND_FX_TP=sort: the round-1 radix-sorted order (A/B only)
@@ -1349,10 +1353,12 @@ static int run_individual_fixed(const nd_graph* G, const NdApp& a, const int64_t
         nd_free(tmp, s);
       }
       k_fx_classes<<<nd_grid(N, 256, 148 * 16), 256, 0, s>>>(k1, N, sentinel, fan[k], stats + 4 * k);
+      prof.step_built();
       k_fx_sample_tp<<<nd_grid(items, IND_BLOCK, 148 * 64), IND_BLOCK, 0, s>>>(
           gv, a, key_base(seed, (uint64_t)k, 0, 0), sample_lo, N, FastDiv((uint32_t)B[k]),
           FastDiv((uint32_t)fan[k]), sentinel, k1, v1, blk[k + 1], stall, ctr);
       k_fx_block_counts<<<nd_grid(n * 32, 256, 148 * 32), 256, 0, s>>>(blk[k + 1], n, B[k + 1], scnt);
+      prof.step_sampled();
       nd_free(k0, s); nd_free(k1, s); nd_free(v0, s); nd_free(v1, s);
       continue;
     }
@@ -1401,6 +1407,7 @@ static int run_individual_fixed(const nd_graph* G, const NdApp& a, const int64_t
       kpl<<<nd_grid(N, 256 * knob.pl, knob.pl_grid), 256, 0, s>>>(
           blk[k], rank[k], N, fB, fan[k], sample_lo, g.row, vinfo, th.tm, gpos, hoff, perm, small,
           nhub + 1, blk[k + 1], scnt);
+      prof.step_built();
       const uint64_t b0 = key_base(seed, (uint64_t)k, 0, 0);
       k_fx_small<<<nd_grid(items, IND_BLOCK, 148 * 16), IND_BLOCK, 0, s>>>(
           gv, b0, fm, blk[k], small, nhub + 1, blk[k + 1], ctr);
@@ -1408,6 +1415,7 @@ static int run_individual_fixed(const nd_graph* G, const NdApp& a, const int64_t
       k_fx_hub_warp<<<knob.hw_grid, IND_BLOCK, HUB_WARP_SMEM, s>>>(hb);
       auto kh = knob.hc == 1 ? k_fx_hub_cta<1> : knob.hc == 2 ? k_fx_hub_cta<2> : k_fx_hub_cta<4>;
       kh<<<knob.hc_grid, IND_BLOCK + 32, HUB_CTA_SMEM, s>>>(hb);
+      prof.step_sampled();
       ND_CUDA_TRY(cudaGetLastError());
       nd_free(gpos, s); nd_free(hubs, s); nd_free(hsz, s); nd_free(hun, s); nd_free(hoff, s);
       nd_free(uoff, s); nd_free(units, s); nd_free(perm, s); nd_free(small, s);
@@ -1422,6 +1430,7 @@ static int run_individual_fixed(const nd_graph* G, const NdApp& a, const int64_t
   ND_CUDA_TRY(nd_alloc(&final_off, n + 1, s));
   ND_CUDA_TRY(nd_alloc(&step_counts, S * n + 1, s));
   ND_CUDA_TRY(nd_alloc(&soff, S * n + 1, s));
+  const size_t e_fin0 = prof.mark();
   k_fx_flen<<<nd_grid(n + 1, 256), 256, 0, s>>>(scnt, n, R, flen);
   for (int64_t k = 0; k < S; k++)
     k_fx_step_counts<<<nd_grid(n, 256), 256, 0, s>>>(nn[k], n, fan[k], step_counts + k * n);
@@ -1458,6 +1467,7 @@ static int run_individual_fixed(const nd_graph* G, const NdApp& a, const int64_t
   ND_CUDA_TRY(nd_alloc(&roots_off, n + 1, s));
   k_fx_final<int32_t><<<nd_grid(n * 32, 256, 148 * 32), 256, 0, s>>>(FS, blk[0], n, R, final_off,
                                                                    final_ids, roots_out, roots_off);
+  const size_t e_fin1 = prof.mark();
   ND_CUDA_TRY(cudaGetLastError());
   for (int64_t k = 0; k < S; k++) nd_free(nn[k], s);
   nd_free(flen, s); nd_free(scnt, s); nd_free(ctr, s); nd_free(stall, s); nd_free(tp_scratch, s);
@@ -1475,6 +1485,7 @@ static int run_individual_fixed(const nd_graph* G, const NdApp& a, const int64_t
     release();
     nd_free(final_off, s); nd_free(final_ids, s); nd_free(roots_out, s);
     nd_free(roots_off, s); nd_free(step_counts, s); nd_free(stats, s);
+    prof.destroy();
     return ND_ERR_STALL;
   }
   nd_result* res = new nd_result();
@@ -1507,6 +1518,14 @@ static int run_individual_fixed(const nd_graph* G, const NdApp& a, const int64_t
   res->counters[NDC_SLOT_BYTES] = slot_bytes;
   res->counters[NDC_STEPS] = n_steps;
   res->counters[NDC_LAUNCHES] = 2 * S + 6;
+  if (prof.on) {
+    ND_CUDA_TRY(cudaStreamSynchronize(s));
+    const auto st = prof.to_result(res);
+    res->prof_ms[0] = st[0];
+    res->prof_ms[1] = st[1];
+    res->prof_ms[2] = prof.between(e_fin0, e_fin1);
+  }
+  prof.destroy();
   *out_res = res;
   nd_trace("fx:done");
   return ND_OK;
@@ -1518,6 +1537,7 @@ extern "C" int nd_run_individual(const nd_graph* G, int app_code, const double* 
                                  uint64_t seed, int64_t step_cap, int paradigm,
                                  const uint8_t* host_unique, int64_t n_unique, void* stream,
                                  nd_result** out_res) {
+  NvtxRange nvtx_run("nd_run_individual");
   NdApp a;
   ND_TRY(nd_make_app(app_code, host_params, n_params, &a));
   if (!G || n < 0 || R < 1 || n_fanouts < 0 || sample_lo < 0 || n >= (1ll << 31)) return ND_ERR_ARG;
@@ -1585,6 +1605,7 @@ extern "C" int nd_run_individual(const nd_graph* G, int app_code, const double* 
   ND_CUDA_TRY(nd_alloc(&scratch_stats, 4, s));
   int64_t n_flagged = 0;      // host copy for the current step
   int64_t step = 0;
+  Profiler prof(s);
   nd_trace("ind:start");
   while (step < S_max && P > 0) {
     nd_trace("ind:step-begin");
@@ -1598,6 +1619,7 @@ extern "C" int nd_run_individual(const nd_graph* G, int app_code, const double* 
     IndCtx c{view(g), a, key_base(seed, (uint64_t)step, 0, 0), sample_lo, m, pt, psid, ptix,
              sd.out, stall};
     unsigned long long* st_step = reinterpret_cast<unsigned long long*>(stats + 4 * step);
+    prof.step_begin();
     if (paradigm == ND_TP && n_flagged > 0) {
       // statistics over the unflagged pairs only; flagged pairs are single fetches
       int64_t *kf = nullptr, *kp = nullptr;
@@ -1669,15 +1691,19 @@ extern "C" int nd_run_individual(const nd_graph* G, int app_code, const double* 
                                                       TS.counters + 1, TS.large_units,
                                                       TS.counters + 2, st_step);
       const StageSpec sp = stage_spec(!g.unit && (app_code == ND_DEEPWALK || app_code == ND_PPR), 0);
+      prof.step_built();
       k_ind_small<<<148 * 8, IND_BLOCK, 0, s>>>(c, keys, vals, TS.gstart, TS.med_list,
                                                 TS.counters + 1, ctr);
       k_ind_group<<<148 * 4, IND_BLOCK, STAGE_BYTES, s>>>(c, keys, vals, TS.gstart,
                                                           TS.large_units, TS.counters + 2, g, sp,
                                                           ctr);
+      prof.step_sampled();
       ND_CUDA_TRY(cudaGetLastError());
       nd_free(k0, s); nd_free(k1, s); nd_free(v0, s); nd_free(v1, s);
     } else {
+      prof.step_built();
       k_ind_flat<<<(unsigned)((items + IND_BLOCK - 1) / IND_BLOCK), IND_BLOCK, 0, s>>>(c, P, ctr);
+      prof.step_sampled();
       // SP fetches: one adjacency read per (sample, transit) pair
       k_add_fetch<<<1, 1, 0, s>>>(st_step, (unsigned long long)P);
     }
@@ -1846,6 +1872,7 @@ extern "C" int nd_run_individual(const nd_graph* G, int app_code, const double* 
   if (h_stall) {
     nd_free(final_off, s); nd_free(final_ids, s); nd_free(roots_out, s); nd_free(roots_off, s);
     nd_free(step_vals, s); nd_free(step_counts, s); nd_free(stats, s);
+    prof.destroy();
     return ND_ERR_STALL;
   }
   nd_result* res = new nd_result();
@@ -1863,6 +1890,12 @@ extern "C" int nd_run_individual(const nd_graph* G, int app_code, const double* 
   res->counters[NDC_ITEMS] = total_items;
   res->counters[NDC_SLOT_BYTES] = (int64_t)h_ctr[0];
   res->counters[NDC_STEPS] = n_steps;
+  if (prof.on) {  // the stream was synchronised above
+    const auto st = prof.to_result(res);
+    res->prof_ms[0] = st[0];
+    res->prof_ms[1] = st[1];
+  }
+  prof.destroy();
   *out_res = res;
   return ND_OK;
 }

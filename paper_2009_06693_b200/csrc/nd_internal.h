@@ -4,6 +4,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <nvtx3/nvToolsExt.h>
+
+#include <array>
 #include <functional>
 #include <vector>
 
@@ -49,6 +52,9 @@ struct nd_result {
   int esz[ND_N_FIELDS] = {8, 8, 8, 8, 8, 8, 8, 8, 8, 8, 8, 8, 4, 4};  // bytes per element
   int64_t counters[ND_N_COUNTERS] = {};
   double prof_ms[4] = {};  // schedule, sample, compaction (nd_set_profiling)
+  // per-step build (schedule / inversion) and sample times of step-structured
+  // runs (nd_set_profiling): RunStats.timings (driver.py:42-48)
+  std::vector<float> step_build_ms, step_sample_ms;
   cudaStream_t stream = nullptr;
   // a field the run leaves to be built on first request (step rows of the
   // fixed-layout k-hop): `lazy_field` is filled by `lazy_build`; `lazy_free`
@@ -97,3 +103,59 @@ inline bool nd_unique_at(const uint8_t* mask, int64_t n, int64_t step) {
 // device counters block reset/read helpers
 int nd_uniform_roots_i32(const nd::DevGraph& g, int64_t count, uint64_t seed, int64_t sample_lo,
                          int64_t n, int32_t* roots, cudaStream_t s);
+
+int nd_profiling();  // nd_set_profiling state
+
+// CUDA-event marks on a run's stream, recorded only under nd_set_profiling(1):
+// phase totals (res->prof_ms) and per-step build / sample times
+// (StepTiming, transit_parallel.py:204-228).  Read after the run's final sync.
+struct Profiler {
+  bool on = false;
+  cudaStream_t s = nullptr;
+  std::vector<cudaEvent_t> ev;
+  std::vector<std::array<size_t, 3>> steps;  // event indices: start, built, sampled
+  Profiler() = default;
+  explicit Profiler(cudaStream_t st) : on(nd_profiling() != 0), s(st) {}
+  size_t mark() {  // index of the recorded event (0 when off)
+    if (!on) return 0;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, s);
+    ev.push_back(e);
+    return ev.size() - 1;
+  }
+  void step_begin() { if (on) steps.push_back({mark(), 0, 0}); }
+  void step_built() { if (on && !steps.empty()) steps.back()[1] = mark(); }
+  void step_sampled() { if (on && !steps.empty()) steps.back()[2] = mark(); }
+  float between(size_t a, size_t b) {
+    float ms = 0;
+    if (on && a < ev.size() && b < ev.size()) cudaEventElapsedTime(&ms, ev[a], ev[b]);
+    return ms;
+  }
+  // per-step times into the result; returns (sum build, sum sample)
+  std::array<double, 2> to_result(nd_result* r) {
+    std::array<double, 2> tot{0.0, 0.0};
+    if (!on) return tot;
+    for (auto& st : steps) {
+      const float b = between(st[0], st[1]), m = between(st[1], st[2]);
+      r->step_build_ms.push_back(b);
+      r->step_sample_ms.push_back(m);
+      tot[0] += b;
+      tot[1] += m;
+    }
+    return tot;
+  }
+  void destroy() {
+    for (auto e : ev) cudaEventDestroy(e);
+    ev.clear();
+  }
+};
+
+// NVTX range over a host scope (the run and its phases show up by name in
+// nsys / ncu --nvtx timelines); header-only NVTX v3, no-op without a tool
+struct NvtxRange {
+  explicit NvtxRange(const char* m) { nvtxRangePushA(m); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};

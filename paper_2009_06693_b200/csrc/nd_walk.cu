@@ -204,28 +204,6 @@ __global__ void k_slab_write(const int32_t* __restrict__ slab, int64_t n, int64_
 
 __global__ void k_stats_fetch(unsigned long long* stats, unsigned long long n) { stats[3] += n; }
 
-struct Profiler {
-  bool on = false;
-  cudaStream_t s;
-  std::vector<cudaEvent_t> ev;
-  double sched_ms = 0, sample_ms = 0, final_ms = 0;
-  void mark() {
-    if (!on) return;
-    cudaEvent_t e;
-    cudaEventCreate(&e);
-    cudaEventRecord(e, s);
-    ev.push_back(e);
-  }
-  float between(size_t a, size_t b) {
-    float ms = 0;
-    cudaEventElapsedTime(&ms, ev[a], ev[b]);
-    return ms;
-  }
-  void destroy() {
-    for (auto e : ev) cudaEventDestroy(e);
-  }
-};
-
 
 // ---- walker-major persistent kernel (SP) ------------------------------------------
 // Each lane owns one walker at a time and advances it step after step with the
@@ -703,6 +681,7 @@ __global__ void k_pw_stats(const unsigned long long* __restrict__ hist, int64_t 
 }  // namespace
 
 static int g_profile = 0;
+int nd_profiling() { return g_profile; }
 extern "C" int nd_set_profiling(int on) {
   g_profile = on;
   return ND_OK;
@@ -862,9 +841,7 @@ static int run_chain_walk(const nd_graph* G, const NdApp& a, int64_t sample_lo, 
   ND_CUDA_TRY(nd_alloc(&rec_w, rec_cap, s));
   ND_CUDA_TRY(nd_alloc(&rec_v, rec_cap, s));
 
-  Profiler prof;
-  prof.on = g_profile;
-  prof.s = s;
+  Profiler prof(s);
   std::vector<int64_t> step_base;
   int64_t A = n, rec_base = 0, step = 0;
   uint32_t* cur_in = cur0;
@@ -925,6 +902,7 @@ static int run_chain_walk(const nd_graph* G, const NdApp& a, int64_t sample_lo, 
     if (prof.on) {
       sched_ms += prof.between(e0, e0 + 1);
       sample_ms += prof.between(e0 + 1, e0 + 2);
+      prof.steps.push_back({e0, e0 + 1, e0 + 2});
     }
     step_base.push_back(rec_base);
     rec_base += A;
@@ -994,6 +972,7 @@ static int run_chain_walk(const nd_graph* G, const NdApp& a, int64_t sample_lo, 
   ND_CUDA_TRY(cudaStreamSynchronize(s));
   if (prof.on) res->counters[NDC_STEPS] = 0;
   double final_ms = prof.on ? prof.between(ef, ef + 1) : 0.0;
+  prof.to_result(res);
   prof.destroy();
 
   // stats as int64 (unsigned long long has the same layout)
@@ -1423,9 +1402,7 @@ static int run_rootpick_walk(const nd_graph* G, const NdApp& a, int64_t sample_l
     ND_TRY(nd_uniform_roots_i32(g, R, seed, sample_lo, n, roots32, s));
   }
   if (paradigm == ND_TP) ND_TRY(S.alloc(n, key_bits, s));
-  Profiler prof;
-  prof.on = g_profile;
-  prof.s = s;
+  Profiler prof(s);
   double sched_ms = 0, sample_ms = 0;
   for (int64_t step = 0; step < n_steps; step++) {
     size_t e0 = prof.ev.size();
@@ -1452,6 +1429,7 @@ static int run_rootpick_walk(const nd_graph* G, const NdApp& a, int64_t sample_l
       ND_CUDA_TRY(cudaStreamSynchronize(s));
       sched_ms += prof.between(e0, e0 + 1);
       sample_ms += prof.between(e0 + 1, e0 + 2);
+      prof.steps.push_back({e0, e0 + 1, e0 + 2});
     }
   }
   prof.mark();
@@ -1495,6 +1473,7 @@ static int run_rootpick_walk(const nd_graph* G, const NdApp& a, int64_t sample_l
   res->prof_ms[0] = sched_ms;
   res->prof_ms[1] = sample_ms;
   res->prof_ms[2] = prof.on ? prof.between(ef, ef + 1) : 0.0;
+  prof.to_result(res);
   prof.destroy();
   res->n = n;
   res->n_steps = n_steps;
@@ -1688,10 +1667,8 @@ static int run_chain_walk_hub(const nd_graph* G, const NdApp& a, int64_t sample_
   int32_t *wid = nullptr, *v0 = nullptr, *t0 = nullptr;
   int64_t rows = max_steps > 0 ? n : 0, step = 0, n_steps = 0, tail_items = 0;
   int* h = reinterpret_cast<int*>(nd_pinned_scratch());
-  Profiler prof;
-  prof.on = g_profile;
-  prof.s = s;
-  prof.mark();
+  Profiler prof(s);
+  const size_t e_run = prof.mark();
   bool tail = false;
   int rc = ND_OK;
   while (rows > 0 && step < max_steps) {
@@ -1765,11 +1742,14 @@ static int run_chain_walk_hub(const nd_graph* G, const NdApp& a, int64_t sample_
         A.P.chunk = rows > 8 * thr ? 128 : rows > 2 * thr ? 64 : 32;
       }
       tp.mark(s, 0);
+      prof.step_begin();
       k_tw_prep<<<nd_grid(rows / TW_TM + 1, 256, nsm * 4), 256, 0, s>>>(A);
+      prof.step_built();
       tp.mark(s, 1);
       k_tw_sample<4><<<nsm * occ, TW_BLOCK, 0, s>>>(A);
       tp.mark(s, 2);
       k_tw_hub<4><<<nsm * hocc, TW_BLOCK, TW_HUB_SMEM, s>>>(A);
+      prof.step_sampled();
       tp.mark(s, 3);
       if (cudaGetLastError() != cudaSuccess) { rc = ND_ERR_CUDA; break; }
       if (getenv("ND_TW_DEBUG") && (st_ % 10 == 1)) {  // development: per-step tier sizes
@@ -1825,7 +1805,7 @@ static int run_chain_walk_hub(const nd_graph* G, const NdApp& a, int64_t sample_
     cudaCtxResetPersistingL2Cache();
     cudaGetLastError();
   }
-  prof.mark();
+  const size_t e_sampled = prof.mark();
   int h_stall = 0;
   if (rc == ND_OK) {
     int mlen = 0;
@@ -1880,10 +1860,13 @@ static int run_chain_walk_hub(const nd_graph* G, const NdApp& a, int64_t sample_
     res->counters[NDC_TP_STAGED] = (int64_t)h_ctr[4];
     res->counters[NDC_TP_INPLACE] = (int64_t)h_ctr[5];
   }
-  prof.mark();
+  const size_t e_done = prof.mark();
   if (prof.on && rc == ND_OK) {
-    res->prof_ms[1] = prof.between(0, 1);
-    res->prof_ms[2] = prof.between(1, 2);
+    ND_CUDA_TRY(cudaStreamSynchronize(s));
+    const auto st = prof.to_result(res);
+    res->prof_ms[0] = st[0];
+    res->prof_ms[1] = prof.between(e_run, e_sampled) - st[0];
+    res->prof_ms[2] = prof.between(e_sampled, e_done);
   }
   prof.destroy();
   for (auto& W : twins) { nd_free(W.wid, s); nd_free(W.out, s); nd_free(W.nnz, s); }
@@ -1919,6 +1902,7 @@ extern "C" int nd_run_walk(const nd_graph* g, int app_code, const double* host_p
                            const int64_t* roots, int64_t roots_per_sample, uint64_t seed,
                            int64_t steps, int64_t step_cap, int paradigm, void* stream,
                            nd_result** out) {
+  NvtxRange nvtx_run("nd_run_walk");
   NdApp a;
   ND_TRY(nd_make_app(app_code, host_params, n_params, &a));
   if (!g || n_samples < 0 || roots_per_sample < 1 || step_cap < 0 || sample_lo < 0)
@@ -1962,5 +1946,17 @@ extern "C" int nd_run_walk(const nd_graph* g, int app_code, const double* host_p
 extern "C" int nd_result_profile(const nd_result* r, double* ms, int64_t n) {
   if (!r) return ND_ERR_ARG;
   for (int64_t i = 0; i < n && i < 4; i++) ms[i] = r->prof_ms[i];
+  return ND_OK;
+}
+
+extern "C" int nd_result_step_times(const nd_result* r, double* build_ms, double* sample_ms,
+                                    int64_t n_max, int64_t* n_out) {
+  if (!r || !n_out) return ND_ERR_ARG;
+  const int64_t k = (int64_t)r->step_build_ms.size();
+  *n_out = k;
+  for (int64_t i = 0; i < k && i < n_max; i++) {
+    if (build_ms) build_ms[i] = r->step_build_ms[i];
+    if (sample_ms) sample_ms[i] = r->step_sample_ms[i];
+  }
   return ND_OK;
 }

@@ -42,6 +42,7 @@ class EngineConfig:
     step_cap: int = DEFAULT_STEP_CAP
     use_kernels: bool = True
     paradigm: Optional[str] = None   # None: taken from tp_run / sp_run
+    step_timing: bool = False        # event-time every step (RunStats.timings build_s/sample_s)
 
 
 @dataclass
@@ -282,6 +283,12 @@ class DeviceRun:
         prof = (C.c_double * 4)()
         L.nd_result_profile(handle, prof, 4)
         self.profile_ms = list(prof)
+        k = C.c_int64()
+        L.nd_result_step_times(handle, None, None, 0, C.byref(k))
+        bt, st = (C.c_double * max(k.value, 1))(), (C.c_double * max(k.value, 1))()
+        if k.value:
+            L.nd_result_step_times(handle, bt, st, k.value, C.byref(k))
+        self.step_ms = [(bt[i], st[i]) for i in range(k.value)]  # (build, sample) per step
 
     def field_count(self, f):
         p, c = C.c_void_p(), C.c_int64()
@@ -327,7 +334,9 @@ class DeviceRun:
         st = np.zeros((0, 4), dtype=np.int64) if st is None else st.reshape(-1, 4)
         rs = RunStats(paradigm=self.paradigm, n_samples=self.n_samples, total_s=self.wall_s)
         for i, row in enumerate(st):
-            rs.timings.append(StepTiming(step=i, groups_small=int(row[0]),
+            b_ms, s_ms = self.step_ms[i] if i < len(self.step_ms) else (0.0, 0.0)
+            rs.timings.append(StepTiming(step=i, build_s=b_ms / 1e3, sample_s=s_ms / 1e3,
+                                         groups_small=int(row[0]),
                                          groups_medium=int(row[1]), groups_large=int(row[2])))
         rs.adjacency_fetches = int(st[:, 3].sum()) if len(st) else 0
         rs.build_total_s, rs.sample_total_s, rs.compact_total_s = (x / 1e3 for x in self.profile_ms[:3])
@@ -562,10 +571,37 @@ def run_device_concurrent(jobs, graph, *, paradigm: str = "sp",
     return runs
 
 
+class profiling:
+    """Context manager: CUDA-event timing of every run inside it (phase totals
+    in DeviceRun.profile_ms, per-step build/sample times in DeviceRun.step_ms
+    and RunStats.timings; nd_set_profiling).  Process-wide switch; each
+    step-structured run then records events per step and synchronises at
+    its end."""
+
+    _depth = 0
+
+    def __enter__(self):
+        if profiling._depth == 0:
+            _lib.load().nd_set_profiling(1)
+        profiling._depth += 1
+        return self
+
+    def __exit__(self, *a):
+        profiling._depth -= 1
+        if profiling._depth == 0:
+            _lib.load().nd_set_profiling(0)
+
+
 def _run(app, graph, samples, config, paradigm) -> SampleSetOutput:
     config = config or EngineConfig()
     par = config.paradigm or paradigm
-    dr = run_device(app, graph, samples, seed=config.seed, paradigm=par, step_cap=config.step_cap)
+    if config.step_timing:
+        with profiling():
+            dr = run_device(app, graph, samples, seed=config.seed, paradigm=par,
+                            step_cap=config.step_cap)
+    else:
+        dr = run_device(app, graph, samples, seed=config.seed, paradigm=par,
+                        step_cap=config.step_cap)
     if dr.plan.steps < 0 and dr.n_steps >= config.step_cap:
         # run_chain / run_loop (chain.py:93-98, driver.py:215-220)
         warnings.warn(f"unbounded app {getattr(app, 'name', '?')!r} hit the "

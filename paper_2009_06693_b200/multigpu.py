@@ -195,15 +195,20 @@ class ShardedJob:
                 with torch.cuda.stream(self._copy):
                     ho.copy_(off, non_blocking=True)
                     hi.copy_(ids, non_blocking=True)
-                off.record_stream(self._copy)
-                ids.record_stream(self._copy)
+                if off.is_cuda:
+                    off.record_stream(self._copy)
+                    ids.record_stream(self._copy)
                 d2h += off.numel() * 8 + ids.numel() * ids.element_size()
                 out[i] = (ho, hi)
             else:
                 out[i] = (off.clone() if self.ws == 1 else off, ids.clone() if self.ws == 1 else ids)
         if self.to_host:
             cur.wait_stream(self._copy)
-        for dr in runs:  # freed once the current stream (gathers, copies) is past them
+        # a run's buffers are freed stream-ordered on its own stream: order that
+        # stream after the gathers and copies (the current stream waited on them)
+        for i in futs:
+            streams[i].wait_stream(cur)
+        for dr in runs:
             dr.close()
         self.last = dict(edges=edges, h2d_bytes=h2d, d2h_bytes=d2h)
         return out
