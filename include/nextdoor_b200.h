@@ -71,6 +71,7 @@ extern "C" {
 
 typedef struct nd_graph nd_graph;
 typedef struct nd_result nd_result;
+typedef struct nd_ooc_graph nd_ooc_graph;
 
 /* last error text of this thread (for the Python shim) */
 const char *nd_last_error(void);
@@ -272,6 +273,35 @@ int nd_gather_ceiling(int64_t bytes, int ctas_per_sm, int iters, double *sectors
 int nd_result_max_row(const nd_result *r, int64_t *host_width);
 int nd_result_dense(const nd_result *r, int64_t width, int32_t *out, void *stream);
 int nd_result_destroy(nd_result *r);
+
+/* ---- out-of-core sub-graph shuttling ------
+ * A graph that does not fit the device stays in host memory (caller-owned
+ * arrays, kept alive until destroy): int64 row offsets [V+1], int32 columns
+ * [E], and the f64 inclusive per-row prefix [E] (NULL: unit weights).  Its
+ * vertices are cut into contiguous partitions whose slices fit half of
+ * `device_budget_bytes` after the resident row offsets; register_host
+ * page-locks the column / prefix arrays for async uploads.  ND_ERR_NOMEM when
+ * the budget cannot hold two slices of the largest row. */
+int nd_ooc_graph_create(const int64_t *row_offsets, const int32_t *col, const double *prefix,
+                        int64_t n_vertices, int64_t n_edges, int64_t device_budget_bytes,
+                        int register_host, void *stream, nd_ooc_graph **out);
+int nd_ooc_graph_destroy(nd_ooc_graph *g);
+/* partitions, edges per slice buffer, device bytes held, host->device slice
+ * bytes shuttled so far, slice uploads so far */
+int nd_ooc_graph_info(const nd_ooc_graph *g, int64_t *n_parts, int64_t *slice_edges,
+                      int64_t *device_bytes, int64_t *bytes_shuttled, int64_t *uploads);
+/* vertex cut points [n_parts + 1] */
+int nd_ooc_graph_parts(const nd_ooc_graph *g, int64_t *vcut, int64_t n_max);
+/* DeepWalk (ND_DEEPWALK; others ND_ERR_APP) over a shuttled graph: same rows
+ * as nd_run_walk.  roots: device int64 [n] or NULL (keyed roots). */
+int nd_run_walk_ooc(nd_ooc_graph *g, int app_code, const double *host_params, int64_t n_params,
+                    int64_t sample_lo, int64_t n_samples, const int64_t *roots, uint64_t seed,
+                    int64_t steps, void *stream, nd_result **out);
+/* k-hop (ND_KHOP; others ND_ERR_APP) over a shuttled graph: same rows as
+ * nd_run_individual. */
+int nd_run_individual_ooc(nd_ooc_graph *g, int app_code, const int64_t *host_fanouts,
+                          int64_t n_fanouts, int64_t sample_lo, int64_t n_samples,
+                          const int64_t *roots, uint64_t seed, void *stream, nd_result **out);
 
 #ifdef __cplusplus
 }

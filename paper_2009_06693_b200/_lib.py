@@ -71,6 +71,12 @@ SIGNATURES = {
     "nd_set_profiling": [i32],
     "nd_gather_ceiling": [i64, i32, i32, C.POINTER(C.c_double), vp],
     "nd_result_destroy": [vp],
+    "nd_ooc_graph_create": [vp, vp, vp, i64, i64, i64, i32, vp, pp],
+    "nd_ooc_graph_destroy": [vp],
+    "nd_ooc_graph_info": [vp, pi64, pi64, pi64, pi64, pi64],
+    "nd_ooc_graph_parts": [vp, vp, i64],
+    "nd_run_walk_ooc": [vp, i32, vp, i64, i64, i64, vp, C.c_uint64, i64, vp, pp],
+    "nd_run_individual_ooc": [vp, i32, vp, i64, i64, i64, vp, C.c_uint64, vp, pp],
 }
 _RESTYPE = {"nd_last_error": C.c_char_p}
 

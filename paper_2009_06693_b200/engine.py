@@ -419,6 +419,14 @@ def run_device(app, graph, samples=None, *, seed: int = 0, paradigm: str = "tp",
     torch = _lib.require_cuda()
     L = _lib.load()
     plan = describe(app)
+    from .outofcore import ShuttledGraph, run_out_of_core
+    if isinstance(graph, ShuttledGraph):  # graph in host memory, shuttled per partition
+        if roots_device is not None:
+            raise ValueError("roots_device is for device-resident graphs")
+        if samples is None:
+            samples = SampleRange(app, graph, sample_lo, n_samples or 0, seed)
+        lo, n, roots, _ = _sample_spec(samples, plan, seed)
+        return run_out_of_core(plan, graph, lo, n, roots, seed, paradigm, stream)
     dg = as_device_graph(graph)
     if roots_device is not None:
         if plan.kind == "collective":

@@ -1,0 +1,140 @@
+"""Out-of-core sub-graph shuttling.
+
+NextDoor samples graphs larger than GPU memory by keeping the graph in host
+memory and moving it to the device one sub-graph at a time, running every
+sample whose transit lies in the resident sub-graph.  Here the graph's
+vertices are cut into contiguous partitions whose column (and prefix) slices
+fit the given device budget; the CUDA side (csrc/nd_ooc.cu) double-buffers
+the slices on a copy stream and advances DeepWalk walkers / k-hop parents in
+the resident partition.  Rows are identical to an in-core run of the same
+job (keyed RNG), so ``tp_run``/``sp_run``/``run_device`` accept a
+``ShuttledGraph`` where they accept a device graph:
+
+    sg = ShuttledGraph.from_graph(graph, device_budget_bytes=8 << 30)
+    out = tp_run(make_app("deepwalk"), sg, make_samples(app, sg, N, seed), cfg)
+
+Supported apps: DeepWalk and k-hop (the C5 apps).  node2vec reads the
+previous transit's row as well (has_edge) and PPR walks have no length
+bound; both raise UnsupportedAppError on a shuttled graph.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from .errors import UnsupportedAppError
+
+
+class ShuttledGraph:
+    """A CSR kept in host memory and shuttled to the device per partition.
+
+    row_offsets int64 [V+1], col_indices (any int dtype, stored int32),
+    prefix f64 [E] (the reference's sequential per-row inclusive prefix,
+    graph.py:49-55) or None for unit weights."""
+
+    def __init__(self, row_offsets, col_indices, prefix=None, *, device_budget_bytes: int,
+                 register_host: bool = True, remap=None):
+        L = _lib.load()
+        self._row = np.ascontiguousarray(row_offsets, dtype=np.int64)
+        self._col = np.ascontiguousarray(col_indices, dtype=np.int32)
+        self._pre = None if prefix is None else np.ascontiguousarray(prefix, dtype=np.float64)
+        self.n_vertices = len(self._row) - 1
+        self.n_edges = len(self._col)
+        if self._pre is not None and len(self._pre) != self.n_edges:
+            raise ValueError("prefix must have one entry per edge")
+        self.unit_weights = self._pre is None
+        self._remap = remap
+        h = C.c_void_p()
+        _lib.check(L.nd_ooc_graph_create(_lib.ptr(self._row), _lib.ptr(self._col),
+                                         _lib.ptr(self._pre), self.n_vertices, self.n_edges,
+                                         int(device_budget_bytes), int(bool(register_host)),
+                                         _lib.stream_ptr(), C.byref(h)), "nd_ooc_graph_create")
+        self._h = h
+
+    @classmethod
+    def from_graph(cls, graph, device_budget_bytes: int, register_host: bool = True):
+        """From a host Graph (this package's or the reference's): unit-weight
+        graphs shuttle columns only, weighted ones columns + prefix."""
+        w = np.asarray(graph.weights)
+        unit = bool(np.all(w == 1.0))
+        pre = None if unit else np.asarray(graph.per_vertex_weight_prefix)
+        return cls(graph.row_offsets, graph.col_indices, pre, device_budget_bytes=device_budget_bytes,
+                   register_host=register_host, remap=getattr(graph, "remap", None))
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def remap(self):
+        return self._remap
+
+    def info(self) -> dict:
+        """Partitions, edges per slice buffer, device bytes held, host->device
+        slice bytes shuttled and slice uploads so far."""
+        v = [C.c_int64() for _ in range(5)]
+        _lib.check(_lib.load().nd_ooc_graph_info(self._h, *[C.byref(x) for x in v]))
+        keys = ("parts", "slice_edges", "device_bytes", "bytes_shuttled", "uploads")
+        return dict(zip(keys, (x.value for x in v)))
+
+    def partitions(self) -> np.ndarray:
+        """Vertex cut points [parts + 1]."""
+        P = self.info()["parts"]
+        out = np.zeros(P + 1, dtype=np.int64)
+        _lib.check(_lib.load().nd_ooc_graph_parts(self._h, _lib.ptr(out), P + 1))
+        return out
+
+    def degree(self, v: int) -> int:
+        return int(self._row[v + 1] - self._row[v])
+
+    def close(self):
+        if self._h is not None and _lib._lib is not None:
+            _lib._lib.nd_ooc_graph_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def run_out_of_core(plan, sg: ShuttledGraph, lo: int, n: int, roots, seed: int, paradigm: str,
+                    stream=None):
+    """One job over a shuttled graph (engine.run_device dispatches here);
+    returns a DeviceRun.  `roots`: host int64 [n] or None (keyed roots)."""
+    import time
+
+    import torch
+
+    from .engine import DeviceRun
+    L = _lib.load()
+    droots = None
+    if roots is not None:
+        if plan.R != 1 or len(roots) != n:
+            raise UnsupportedAppError("out-of-core runs take one root per sample")
+        droots = torch.from_numpy(np.ascontiguousarray(roots, dtype=np.int64)).cuda()
+    h = C.c_void_p()
+    sp = _lib.stream_ptr(stream)
+    t0 = time.perf_counter()
+    if plan.kind == "walk" and plan.code == 0 and plan.R == 1 and plan.steps >= 0:
+        kp = np.ascontiguousarray(plan.kparams, dtype=np.float64)
+        _lib.check(L.nd_run_walk_ooc(sg.handle, plan.code, _lib.ptr(kp), len(kp), lo, n,
+                                     _lib.ptr(droots), C.c_uint64(seed & (2**64 - 1)), plan.steps,
+                                     sp, C.byref(h)), "nd_run_walk_ooc")
+    elif (plan.kind == "individual" and plan.code == 3 and plan.R == 1 and plan.unique is None
+          and len(plan.fanouts) >= 1):
+        fan = np.ascontiguousarray(plan.fanouts, dtype=np.int64)
+        _lib.check(L.nd_run_individual_ooc(sg.handle, plan.code, _lib.ptr(fan), len(fan), lo, n,
+                                           _lib.ptr(droots), C.c_uint64(seed & (2**64 - 1)), sp,
+                                           C.byref(h)), "nd_run_individual_ooc")
+    else:
+        raise UnsupportedAppError(
+            f"app {plan.name!r} cannot run on a shuttled graph: out-of-core runs cover DeepWalk "
+            "and k-hop (fixed fanouts, no unique steps); node2vec reads a second row per step "
+            "and PPR walks have no length bound")
+    torch.cuda.synchronize()
+    return DeviceRun(h, plan, sg, paradigm, lo, time.perf_counter() - t0)

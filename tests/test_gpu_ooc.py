@@ -1,0 +1,130 @@
+"""Out-of-core sub-graph shuttling: a
+graph held in host memory, cut into partitions that fit a small device
+budget, gives the same rows as the in-core run of the same job (keyed draws,
+chain.py:64-179 / driver.py:203-235), and the C oracle agrees."""
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from tests.helpers import expected_walk_rows, oracle_full_graph
+
+pytestmark = pytest.mark.gpu
+
+SEED = 7
+
+
+def _rows(dr):
+    from paper_2009_06693_b200 import _lib
+    off, ids = dr.host(_lib.F_FINAL_OFF), dr.host(_lib.F_FINAL_IDS)
+    dr.close()
+    return off, ids
+
+
+def _shuttled(dg, parts_wanted):
+    from paper_2009_06693_b200.outofcore import ShuttledGraph
+    hg = dg.to_host()
+    bpe = 4 if dg.unit_weights else 12
+    budget = (dg.n_vertices + 1) * 8 + 2 * bpe * (dg.n_edges // parts_wanted + 1)
+    # the largest row must fit a slice: grow the budget until it does
+    maxdeg = int(np.diff(hg.row_offsets).max())
+    budget = max(budget, (dg.n_vertices + 1) * 8 + 2 * bpe * maxdeg)
+    sg = ShuttledGraph.from_graph(hg, device_budget_bytes=budget)
+    return hg, sg
+
+
+@pytest.fixture(scope="module", params=[True, False], ids=["weighted", "unit"])
+def graphs(request):
+    from paper_2009_06693_b200.graph import DeviceGraph
+    dg = DeviceGraph.rmat(16, 16, seed=5, weighted=request.param)
+    hg, sg = _shuttled(dg, 6)
+    yield dg, hg, sg
+    sg.close()
+    dg.close()
+
+
+def test_partitions_cover_the_graph(graphs):
+    dg, hg, sg = graphs
+    info = sg.info()
+    cut = sg.partitions()
+    assert info["parts"] >= 4 and cut[0] == 0 and cut[-1] == dg.n_vertices
+    assert np.all(np.diff(cut) > 0)
+    row = hg.row_offsets
+    assert max(row[cut[p + 1]] - row[cut[p]] for p in range(info["parts"])) <= info["slice_edges"]
+    assert info["device_bytes"] < dg.resident_bytes()
+
+
+@pytest.mark.parametrize("paradigm", ["sp", "tp"])
+def test_deepwalk_equals_in_core(graphs, paradigm):
+    from paper_2009_06693_b200 import make_app
+    from paper_2009_06693_b200.engine import run_device
+    dg, hg, sg = graphs
+    app = make_app("deepwalk", walk_length=40)
+    n = 20_000
+    before = sg.info()["bytes_shuttled"]
+    o_off, o_ids = _rows(run_device(app, sg, n_samples=n, seed=SEED, paradigm=paradigm))
+    i_off, i_ids = _rows(run_device(app, dg, n_samples=n, seed=SEED, paradigm=paradigm))
+    assert np.array_equal(o_off, i_off) and np.array_equal(o_ids, i_ids)
+    # walkers cross partitions: the graph went up several times
+    assert sg.info()["bytes_shuttled"] - before > 2 * hg.n_edges * 4
+
+
+def test_deepwalk_vs_oracle_and_sample_block(graphs):
+    from paper_2009_06693_b200 import make_app
+    from paper_2009_06693_b200.engine import run_device
+    dg, hg, sg = graphs
+    og = oracle_full_graph(dg)
+    lo, n = 1000, 3000
+    roots = O.uniform_roots(dg.n_vertices, 1, SEED, lo, n)
+    r = O.run_chain(og, 0, [], roots, SEED, 100, paradigm="sp", sample_lo=lo)
+    e_off, e_ids = expected_walk_rows(r["roots"], r)
+    off, ids = _rows(run_device(make_app("deepwalk"), sg, n_samples=n, sample_lo=lo, seed=SEED))
+    assert np.array_equal(off, e_off) and np.array_equal(ids, e_ids)
+
+
+def test_khop_equals_in_core_with_step_rows(graphs):
+    from paper_2009_06693_b200 import EngineConfig, make_app, sp_run, tp_run
+    from paper_2009_06693_b200.engine import make_samples
+    dg, hg, sg = graphs
+    app = make_app("khop", fanouts=[25, 10])
+    samples = make_samples(app, dg, 2048, SEED)
+    a = tp_run(app, sg, make_samples(app, sg, 2048, SEED), EngineConfig(seed=SEED))
+    b = sp_run(app, dg, samples, EngineConfig(seed=SEED))
+    ao, ai = a.final_csr()
+    bo, bi = b.final_csr()
+    assert np.array_equal(ao, bo) and np.array_equal(ai, bi)
+    assert a.n_steps == b.n_steps
+    assert np.array_equal(np.asarray(a.step_vals), np.asarray(b.step_vals))
+    assert np.array_equal(np.asarray(a.step_counts), np.asarray(b.step_counts))
+
+
+def test_khop_vs_oracle(graphs):
+    from paper_2009_06693_b200 import make_app
+    from paper_2009_06693_b200.engine import run_device
+    dg, hg, sg = graphs
+    og = oracle_full_graph(dg)
+    n = 1024
+    roots = list(O.uniform_roots(dg.n_vertices, 1, SEED, 0, n))
+    ref = O.run_individual(og, 3, [], [25, 10], roots, SEED, 2, paradigm="sp")
+    dr = run_device(make_app("khop", fanouts=[25, 10]), sg, n_samples=n, seed=SEED)
+    out = dr.to_output()
+    dr.close()
+    assert np.array_equal(np.asarray(out.step_vals), ref["vals"])
+
+
+def test_unsupported_apps_and_budget():
+    from paper_2009_06693_b200 import make_app
+    from paper_2009_06693_b200.engine import run_device
+    from paper_2009_06693_b200.errors import DeviceError, UnsupportedAppError
+    from paper_2009_06693_b200.graph import DeviceGraph
+    from paper_2009_06693_b200.outofcore import ShuttledGraph
+    dg = DeviceGraph.rmat(12, 16, seed=1, weighted=True)
+    hg = dg.to_host()
+    sg = ShuttledGraph.from_graph(hg, device_budget_bytes=1 << 24)
+    for name in ("node2vec", "ppr"):
+        with pytest.raises(UnsupportedAppError):
+            run_device(make_app(name), sg, n_samples=16, seed=SEED)
+    sg.close()
+    with pytest.raises((DeviceError, MemoryError, ValueError)):
+        ShuttledGraph.from_graph(hg, device_budget_bytes=(hg.n_vertices + 1) * 8 + 64)
+    dg.close()
