@@ -432,21 +432,34 @@ def c5_leg(args, ws, rank, barrier, rdev):
             torch.distributed.all_reduce(ed)
         return ms.item(), int(ed.item()), last
 
+    def checksum(rows):
+        """Order-free checksum of rank 0's rows (the same at every N and chunking
+        when the gathered rows equal the single-GPU run's): rows, values, the
+        sum of the ids and of the squared row lengths."""
+        out = {}
+        for (app, n_total, _), pieces in zip(jobs, rows):
+            c = {"rows": 0, "values": 0, "sum_ids": 0, "sum_len_sq": 0}
+            for off, ids in pieces:
+                ln = (off[1:] - off[:-1]).to(torch.int64)
+                c["rows"] += int(ln.numel())
+                c["values"] += int(ids.numel())
+                c["sum_ids"] += int(ids.to(torch.int64).sum().item())
+                c["sum_len_sq"] += int((ln * ln).sum().item())
+            out[app.name] = c
+        return out
+
     dev_job = ShardedJob(dg, jobs, to_host=False)
     dev_ms, dev_edges, rows = timed_steps(dev_job, args.steps, args.warmup)
-    # rows on rank 0 (the whole job, in sample order): a checksum that is the
-    # same at every N when the gathered rows equal the single-GPU run's
-    checks = None
-    if rank == 0:
-        checks = {}
-        for (app, n_total, _), (off, ids) in zip(jobs, rows):
-            checks[app.name] = {"rows": int(off.numel() - 1), "values": int(ids.numel()),
-                                "sum_ids": int(ids.to(torch.int64).sum().item()),
-                                "sum_off": int(off.sum().item())}
-    host_job = ShardedJob(dg, jobs, to_host=True)
-    e2e_ms, e2e_edges, _ = timed_steps(host_job, args.steps, max(1, args.warmup // 2))
+    checks = checksum(rows) if rank == 0 else None
+    del rows
+    # e2e: DeepWalk's shard in pieces, so the rows of piece c cross PCIe while
+    # piece c+1 samples
+    host_jobs = [(dw, walkers, SEED, args.c5_chunks), (kh, roots, SEED)]
+    host_job = ShardedJob(dg, host_jobs, to_host=True)
+    e2e_ms, e2e_edges, hrows = timed_steps(host_job, args.steps, max(1, args.warmup // 2))
+    e2e_checks = checksum(hrows) if rank == 0 else None
     h2d, d2h = host_job.last["h2d_bytes"], host_job.last["d2h_bytes"]
-    del dev_job, host_job, rows
+    del dev_job, host_job, hrows
     # each app's own kernel rate on this rank's shard (apps one after another,
     # event-timed launches; SURVEY 8(d) bytes counted on device)
     L.nd_set_profiling(1)
@@ -487,6 +500,8 @@ def c5_leg(args, ws, rank, barrier, rdev):
                 "ms_per_step": e2e_ms / args.steps, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
                 "result": "rank 0: every rank's final rows (int64 offsets + int32 ids) in pinned host memory",
+                "chunks": {"deepwalk": args.c5_chunks, "khop": 1},
+                "rows_match_device": e2e_checks == checks if rank == 0 else None,
                 "timing": "roots H2D on every rank + sampling + NCCL gather + rank-0 D2H, per step"},
         "rows_on_rank0": checks,
         "per_rank_kernels": roof,
@@ -570,6 +585,8 @@ def main():
     ap.add_argument("--no-tp", action="store_true")
     ap.add_argument("--no-c5", action="store_true", help="skip the C5 (1B-edge, strong-sharded) leg")
     ap.add_argument("--no-c3", action="store_true", help="skip the C3 (k-hop) leg")
+    ap.add_argument("--c5-chunks", type=int, default=6,
+                    help="C5 e2e: DeepWalk pieces per rank (piece c's rows cross PCIe while c+1 samples)")
     ap.add_argument("--ref-engine", default="sp", choices=["sp", "tp"],
                     help="the reference engine timed by --impl reference (sp_run: its faster CPU path)")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])

@@ -101,15 +101,18 @@ class ShardedJob:
     driver.py:175-186 of the reference): every rank holds the replicated
     graph and runs its ``worker_ranges`` share of each app's sample ids.
 
-    Per ``run()``: each rank uploads its shards' roots from pinned host memory,
-    samples every app concurrently (one stream and host thread per app), and
-    sends each app's compacted rows to `dst` as soon as that app finishes
-    (NCCL over NVLink; the gather of one app overlaps the others' sampling);
-    `dst` then copies the gathered rows into pinned host buffers
-    (``to_host``).  Rows on `dst` equal one single-GPU run of the whole job.
+    Per ``run()``: each rank uploads its shards' roots from pinned host memory
+    and samples every app concurrently (one stream and host thread per app).
+    An app's shard may be cut into ``chunks`` contiguous pieces run one after
+    another on its stream; each piece's compacted rows go to `dst` over NCCL
+    as soon as it is done (the gather of one piece overlaps the sampling of
+    the next and of the other apps), and `dst` copies them into pinned host
+    buffers on a copy stream (``to_host``).  The rows on `dst` equal one
+    single-GPU run of the whole job, piece by piece.
 
-    jobs: list of (app, n_samples_total, seed).  Roots are the keyed defaults
-    (apps.py:83-103), produced once at construction into pinned memory."""
+    jobs: list of (app, n_samples_total, seed[, chunks]).  Roots are the keyed
+    defaults (apps.py:83-103), produced once at construction into pinned
+    memory."""
 
     def __init__(self, graph, jobs, group=None, dst: int = 0, paradigm: str = "sp",
                  to_host: bool = True):
@@ -127,18 +130,24 @@ class ShardedJob:
         self.rank, self.ws = rank, ws
         self.jobs = []
         L = _lib.load()
-        for app, n_total, seed in jobs:
+        for job in jobs:
+            app, n_total, seed = job[:3]
+            chunks = max(1, int(job[3])) if len(job) > 3 else 1
             plan = describe(app)
+            if plan.R != 1 or plan.kind == "collective":
+                raise ValueError("ShardedJob runs walk and individual apps with one root per sample")
             lo, hi = shard_for_rank(n_total, ws, rank)
             n = hi - lo
-            droots = torch.empty(max(n * plan.R, 1), dtype=torch.int64, device="cuda")
+            droots = torch.empty(max(n, 1), dtype=torch.int64, device="cuda")
             if n:
-                _lib.check(L.nd_uniform_roots(self.dg.handle, plan.R, C.c_uint64(seed), lo, n,
+                _lib.check(L.nd_uniform_roots(self.dg.handle, 1, C.c_uint64(seed), lo, n,
                                               _lib.ptr(droots), _lib.stream_ptr()),
                            "nd_uniform_roots")
-            roots_host = droots[:n * plan.R].cpu().pin_memory()
+            roots_host = droots[:n].cpu().pin_memory()
+            pieces = [(lo + a, lo + b) for a, b in worker_ranges(n, chunks)] if n else []
+            pieces += [(hi, hi)] * (chunks - len(pieces))  # every rank gathers `chunks` pieces
             self.jobs.append(dict(app=app, n_total=n_total, seed=seed, lo=lo, n=n,
-                                  roots_host=roots_host))
+                                  roots_host=roots_host, pieces=pieces))
         self._host = {}
         self._copy = torch.cuda.Stream()
         self.last = {}
@@ -152,35 +161,57 @@ class ShardedJob:
         return b[:like.numel()]
 
     def run(self, order=None):
-        """One step.  Returns a list (job order) of (off, ids) host tensors on
-        `dst` (device tensors when to_host=False; None on other ranks), valid
-        until the next run.  `order`: the gather order of the jobs (the same on
-        every rank; default: job order).  self.last holds this rank's sampled
-        edge count and the H2D / D2H bytes of the step."""
+        """One step.  Returns, per job (job order), the list of its pieces'
+        (off, ids) on `dst` -- pinned host tensors (device tensors when
+        to_host=False) valid until the next run; piece c holds every rank's
+        c-th chunk in rank order; None on other ranks.  `order`: the order in
+        which the jobs' pieces are gathered (the same on every rank; default
+        job order).  self.last: this rank's sampled edges, H2D / D2H bytes."""
+        import queue
+
         import torch
         from . import _lib
-        from .engine import job_streams, submit_device_concurrent
+        from .engine import _job_pool, job_streams, run_device
         cur = torch.cuda.current_stream()
+        dev = torch.cuda.current_device()
         h2d = 0
-        specs = []
+        droots = []
         for j in self.jobs:
-            d = j["roots_host"].to("cuda", non_blocking=True) if j["n"] else None
+            droots.append(j["roots_host"].to("cuda", non_blocking=True) if j["n"] else None)
             h2d += j["roots_host"].numel() * 8 if j["n"] else 0
-            specs.append(dict(app=j["app"], n_samples=j["n"], sample_lo=j["lo"], seed=j["seed"],
-                              roots_device=d))
-        live = [i for i, s in enumerate(specs) if s["n_samples"] > 0]
-        futs = dict(zip(live, submit_device_concurrent([specs[i] for i in live], self.dg,
-                                                       paradigm=self.paradigm)))
-        streams = dict(zip(live, job_streams(len(live))))
-        out = [None] * len(self.jobs)
+        k = len(self.jobs)
+        streams = job_streams(k)
+        for st in streams:
+            st.wait_stream(cur)
+        queues = [queue.Queue() for _ in range(k)]
+
+        def runner(i, st):
+            j = self.jobs[i]
+            torch.cuda.set_device(dev)
+            with torch.cuda.stream(st):
+                for a, b in j["pieces"]:
+                    dr = None
+                    if b > a:
+                        dr = run_device(j["app"], self.dg, n_samples=b - a, sample_lo=a,
+                                        seed=j["seed"], paradigm=self.paradigm, stream=st,
+                                        sync=False,
+                                        roots_device=droots[i][a - j["lo"]:b - j["lo"]])
+                    ev = torch.cuda.Event()
+                    ev.record(st)
+                    queues[i].put((dr, ev))
+
+        futs = [_job_pool(k).submit(runner, i, st) for i, st in enumerate(streams)]
+        out = [[] for _ in range(k)]
         edges, d2h, runs = 0, 0, []
         empty_off = torch.zeros(1, dtype=torch.int64, device="cuda")
         empty_ids = torch.empty(0, dtype=torch.int32, device="cuda")
-        for i in (order if order is not None else range(len(self.jobs))):
-            if i in futs:
-                dr = futs[i].result()
+        seq = [(i, c) for i in (order if order is not None else range(k))
+               for c in range(len(self.jobs[i]["pieces"]))]
+        for i, c in seq:
+            dr, ev = queues[i].get()
+            cur.wait_event(ev)
+            if dr is not None:
                 runs.append(dr)
-                cur.wait_stream(streams[i])
                 edges += dr.total_sampled
                 off, ids = dr.view(_lib.F_FINAL_OFF), dr.narrow_ids()
             else:
@@ -191,7 +222,7 @@ class ShardedJob:
                 continue
             if self.to_host:  # rank dst: rows to pinned host memory on the copy stream
                 self._copy.wait_stream(cur)
-                ho, hi = self._pinned((i, "off"), off), self._pinned((i, "ids"), ids)
+                ho, hi = self._pinned((i, c, "off"), off), self._pinned((i, c, "ids"), ids)
                 with torch.cuda.stream(self._copy):
                     ho.copy_(off, non_blocking=True)
                     hi.copy_(ids, non_blocking=True)
@@ -199,16 +230,19 @@ class ShardedJob:
                     off.record_stream(self._copy)
                     ids.record_stream(self._copy)
                 d2h += off.numel() * 8 + ids.numel() * ids.element_size()
-                out[i] = (ho, hi)
+                out[i].append((ho, hi))
             else:
-                out[i] = (off.clone() if self.ws == 1 else off, ids.clone() if self.ws == 1 else ids)
+                out[i].append((off.clone() if self.ws == 1 else off,
+                               ids.clone() if self.ws == 1 else ids))
+        for f in futs:
+            f.result()
         if self.to_host:
             cur.wait_stream(self._copy)
         # a run's buffers are freed stream-ordered on its own stream: order that
         # stream after the gathers and copies (the current stream waited on them)
-        for i in futs:
-            streams[i].wait_stream(cur)
+        for st in streams:
+            st.wait_stream(cur)
         for dr in runs:
             dr.close()
         self.last = dict(edges=edges, h2d_bytes=h2d, d2h_bytes=d2h)
-        return out
+        return out if (not self.dist or self.ws == 1 or self.rank == self.dst) else None

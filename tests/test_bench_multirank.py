@@ -51,3 +51,19 @@ def test_run_sharded_two_ranks_equals_one_run(tmp_path):
     assert p.returncode == 0, p.stderr[-3000:]
     verdict = json.loads(res.read_text())
     assert verdict == {"node2vec": True, "ppr": True, "khop": True}
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [1, 2, 3])
+def test_sharded_job_pieces_equal_one_run(tmp_path, n):
+    """multigpu.ShardedJob (the C5 step): DeepWalk shards in pieces, k-hop
+    whole, rows gathered piece by piece to rank 0's pinned host memory; in
+    sample-id order they equal one single-process run (driver.py:175-186)."""
+    res = tmp_path / "job.json"
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29620 + n),
+           "tests/_shardedjob_worker.py", str(res)]
+    p = subprocess.run(cmd, cwd=REPO, env=env, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-3000:]
+    assert json.loads(res.read_text()) == {"deepwalk": True, "khop": True}
