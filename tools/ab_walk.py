@@ -25,7 +25,7 @@ for name in sys.argv[1:] or ["node2vec", "ppr", "deepwalk"]:
     for it in range(6):
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
-        dr = run_device(a, dg, n_samples=N, seed=7, paradigm="sp")
+        dr = run_device(a, dg, n_samples=N, seed=7, paradigm=os.environ.get("AB_PARADIGM", "sp"))
         e.record()
         torch.cuda.synchronize()
         if it:
