@@ -61,4 +61,26 @@ for code, prm in ((0, []), (1, [0.1]), (2, [2.0, 0.5, 0.0]), (3, []), (4, [])):
                        h.per_vertex_max_weight, rng.integers(0, h.n_vertices, n), rng.integers(-1, h.n_vertices, n),
                        rng.integers(0, 1000, n), rng.integers(0, 5, n), rng.integers(0, 5, n), 7, 1, out)
 transit_schedule(rng.integers(0, 50, 2000), 3)
+# round 2: step timing (events per step), the k-hop TP hub tiers on a denser
+# graph (warp and thread-block tiers), out-of-core shuttling, ShardedJob
+from paper_2009_06693_b200.engine import profiling  # noqa: E402
+from paper_2009_06693_b200.multigpu import ShardedJob  # noqa: E402
+from paper_2009_06693_b200.outofcore import ShuttledGraph  # noqa: E402
+dd = DeviceGraph.rmat(10, 64, seed=4, undirected=True, weighted=False)
+with profiling():
+    for par in ("sp", "tp"):
+        dr = run_device(make_app("khop", fanouts=[25, 10]), dd, n_samples=2000, seed=5, paradigm=par)
+        dr.to_output()
+        dr.close()
+        dr = run_device(make_app("fastgcn"), du, n_samples=64, seed=5, paradigm=par)
+        dr.close()
+hg = dg.to_host()
+sg = ShuttledGraph.from_graph(hg, device_budget_bytes=(hg.n_vertices + 1) * 8 + 2 * 12 * (hg.n_edges // 4 + 64))
+for name, kw in (("deepwalk", {"walk_length": 20}), ("khop", {"fanouts": [5, 3]})):
+    dr = run_device(make_app(name, **kw), sg, n_samples=300, seed=5)
+    dr.to_output()
+    dr.close()
+sg.close()
+job = ShardedJob(dg, [(make_app("deepwalk"), 500, 5, 3), (make_app("khop"), 200, 5)], to_host=True)
+job.run(order=[1, 0])
 print("sanitize smoke ok")
