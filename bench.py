@@ -511,6 +511,86 @@ def c5_leg(args, ws, rank, barrier, rdev):
     }
 
 
+def _timed_runs(app, dg, lo, n, par, reps=5, warm=2):
+    """Median event time of whole runs (sampling, inversion, compaction) of
+    this rank's block, and the last run's sampled / recorded counts."""
+    import torch
+    from paper_2009_06693_b200.engine import run_device
+    stream = torch.cuda.current_stream()
+    for _ in range(warm):
+        run_device(app, dg, n_samples=n, sample_lo=lo, seed=SEED, paradigm=par).close()
+    ms, sampled, recorded = [], 0, 0
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        dr = run_device(app, dg, n_samples=n, sample_lo=lo, seed=SEED, paradigm=par, sync=False)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+        sampled, recorded = dr.total_sampled, dr.total_recorded
+        dr.close()
+    return statistics.median(ms), sampled, recorded
+
+
+def _rank_max_sum(ms, cnt, ws, rdev):
+    import torch
+    a = torch.tensor([ms], dtype=torch.float64, device=rdev)
+    b = torch.tensor([cnt], dtype=torch.int64, device=rdev)
+    if ws > 1:
+        torch.distributed.all_reduce(a, op=torch.distributed.ReduceOp.MAX)
+        torch.distributed.all_reduce(b)
+    return a.item(), int(b.item())
+
+
+def c1_c4_legs(args, ws, rank, barrier, rdev):
+    """C1 (BASELINE.json configs[0]: DeepWalk x 56,944 on the reference's own
+    powerlaw(56944, attach 7) graph, L2-resident) and C4 (configs[3]:
+    FastGCN / LADIES (deg^2) / MVS over 4,096 samples and ClusterGCN over 8
+    on the Orkut-shaped RMAT-22 graph, 117.2M directed unit edges), each
+    rank its worker_ranges block; median event times of whole runs.  Parity
+    of these configurations is in tests/test_gpu_configs.py."""
+    import torch
+    from paper_2009_06693_b200 import make_app
+    from paper_2009_06693_b200.graph import DeviceGraph
+    from paper_2009_06693_b200.sharding import shard_for_rank
+    from paper_2009_06693_b200.synth import powerlaw_graph
+    out = {}
+    g = powerlaw_graph(56944, attach=7, weighted=True, seed=0)
+    dg = DeviceGraph.from_arrays(g.row_offsets, g.col_indices, g.weights)
+    lo, hi = shard_for_rank(g.n_vertices, ws, rank)
+    c1 = {"workload": "C1: DeepWalk len 100, one walk per vertex, powerlaw(56944, attach 7, "
+                      "weighted, seed 0): 797,132 edges, L2-resident (HBM roofline not binding)"}
+    for par in ("sp", "tp"):
+        ms, e, _ = _timed_runs(make_app("deepwalk"), dg, lo, hi - lo, par)
+        ms, e = _rank_max_sum(ms, e, ws, rdev)
+        c1[par] = {"ms": ms, "edges": e, "value": e / (ms / 1e3), "unit": "edges/s"}
+    dg.close()
+    out["c1"] = c1
+    if DEV_SCALE is None:
+        dg = DeviceGraph.rmat(22, n_edges=58_600_000, seed=GRAPH_SEED, undirected=True, weighted=False)
+    else:
+        dg = DeviceGraph.rmat(DEV_SCALE, n_edges=int(58_600_000 / (1 << 22) * (1 << DEV_SCALE)),
+                              seed=GRAPH_SEED, undirected=True, weighted=False)
+    c4 = {"workload": f"C4: collective apps on RMAT scale {DEV_SCALE or 22} "
+                      f"({dg.n_vertices:,} V, {dg.n_edges:,} directed unit E), tp_run's engine",
+          "unit": "sampled + recorded edges/s"}
+    for name, kw, N in (("fastgcn", {}, 4096), ("ladies", {"distribution": "degree_sq"}, 4096),
+                        ("mvs", {}, 4096), ("clustergcn", {}, 8)):
+        lo, hi = shard_for_rank(N, ws, rank)
+        if hi > lo:
+            ms, smp, rec = _timed_runs(make_app(name, **kw), dg, lo, hi - lo, "tp", reps=3, warm=1)
+        else:
+            ms, smp, rec = 0.0, 0, 0
+        ms, smp = _rank_max_sum(ms, smp, ws, rdev)
+        _, rec = _rank_max_sum(0.0, rec, ws, rdev)
+        c4[name] = {"N": N, "ms": ms, "sampled": smp, "recorded": rec,
+                    "value": (smp + rec) / (ms / 1e3) if ms > 0 else None}
+    dg.close()
+    torch.cuda.empty_cache()
+    out["c4"] = c4
+    return out
+
+
 def c3_leg(args, ws, rank, barrier, rdev):
     """C3 (BASELINE.json configs[2]): GraphSAGE k-hop (25, 10) on the
     Reddit-shaped RMAT-18 graph (57.3M undirected edges, 114.6M directed, unit
@@ -585,6 +665,7 @@ def main():
     ap.add_argument("--no-tp", action="store_true")
     ap.add_argument("--no-c5", action="store_true", help="skip the C5 (1B-edge, strong-sharded) leg")
     ap.add_argument("--no-c3", action="store_true", help="skip the C3 (k-hop) leg")
+    ap.add_argument("--no-c14", action="store_true", help="skip the C1 (DeepWalk) and C4 (collective) legs")
     ap.add_argument("--c5-chunks", type=int, default=6,
                     help="C5 e2e: DeepWalk pieces per rank (piece c's rows cross PCIe while c+1 samples)")
     ap.add_argument("--ref-engine", default="sp", choices=["sp", "tp"],
@@ -931,6 +1012,7 @@ def main():
     dg.close()
     torch.cuda.empty_cache()
     c3 = None if args.no_c3 else c3_leg(args, ws, rank, barrier, rdev)
+    c14 = {} if args.no_c14 else c1_c4_legs(args, ws, rank, barrier, rdev)
     c5 = None
     if not args.no_c5:
         c5 = c5_leg(args, ws, rank, barrier, rdev)
@@ -973,7 +1055,9 @@ def main():
             "clocks": clocks.summary(), "gpu_launches": launches, "gather": gather_info,
             "edges_per_step": edges_all / len(times),
             "graph_footprint": c2_footprint,
+            "c1": c14.get("c1"),
             "c3": c3,
+            "c4": c14.get("c4"),
             "c5": c5,
         }
         print(json.dumps(line), flush=True)
