@@ -649,6 +649,52 @@ def c3_leg(args, ws, rank, barrier, rdev):
                                  "kernels": "k_fx_sample" if par == "sp" else
                                             "k_fx_small + k_fx_hub_warp + k_fx_hub_cta"}}
     out["tp_vs_sp"] = out["tp"]["ms"] / out["sp"]["ms"]
+    # single 1,024-root batches (report C3's batch latency):
+    # run_device per batch vs the CUDA-graph plan (minibatch.KhopBatchSampler)
+    # replayed over 228 batches back to back, keyed roots of each batch's ids
+    import ctypes as C
+    from paper_2009_06693_b200.minibatch import KhopBatchSampler
+    nb, bs = 228, 1024
+    L = _lib.load()
+    allroots = torch.empty(nb * bs, dtype=torch.int64, device="cuda")
+    _lib.check(L.nd_uniform_roots(dg.handle, 1, C.c_uint64(SEED), 0, nb * bs, _lib.ptr(allroots),
+                                  _lib.stream_ptr()), "nd_uniform_roots")
+    one = []
+    for b in range(25):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        dr = run_device(app, dg, n_samples=bs, sample_lo=b * bs, seed=SEED, paradigm="sp", sync=False)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if b >= 5:
+            one.append(e0.elapsed_time(e1))
+        dr.close()
+    sampler = KhopBatchSampler(dg, [25, 10], bs)
+    for b in range(5):
+        sampler.sample(allroots[b * bs:(b + 1) * bs], sample_lo=b * bs, seed=SEED)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    edges = 0
+    e0.record(stream)
+    for b in range(nb):
+        off, _, _ = sampler.sample(allroots[b * bs:(b + 1) * bs], sample_lo=b * bs, seed=SEED)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    plan_ms = e0.elapsed_time(e1) / nb
+    # the last batch's rows equal a plain run of it
+    dr = run_device(app, dg, n_samples=bs, sample_lo=(nb - 1) * bs, seed=SEED, paradigm="sp")
+    same = bool(torch.equal(off, dr.view(_lib.F_FINAL_OFF))
+                and torch.equal(sampler.final_ids[:int(off[-1])], dr.view(_lib.F_FINAL_IDS32)))
+    edges = dr.total_sampled
+    dr.close()
+    sampler.close()
+    out["single_batch"] = {"roots": bs, "edges": edges,
+                           "run_device_ms": statistics.median(one),
+                           "plan_ms": plan_ms, "plan_edges_per_s": edges / (plan_ms / 1e3),
+                           "plan_rows_equal_run": same,
+                           "how": "run_device: median of 20 event-timed single-batch runs; plan: "
+                                  f"{nb} batches replayed back to back (one CUDA graph launch each), "
+                                  "event time / batches"}
     dg.close()
     torch.cuda.empty_cache()
     return out

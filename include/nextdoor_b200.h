@@ -72,6 +72,7 @@ extern "C" {
 typedef struct nd_graph nd_graph;
 typedef struct nd_result nd_result;
 typedef struct nd_ooc_graph nd_ooc_graph;
+typedef struct nd_khop_plan nd_khop_plan;
 
 /* last error text of this thread (for the Python shim) */
 const char *nd_last_error(void);
@@ -302,6 +303,27 @@ int nd_run_walk_ooc(nd_ooc_graph *g, int app_code, const double *host_params, in
 int nd_run_individual_ooc(nd_ooc_graph *g, int app_code, const int64_t *host_fanouts,
                           int64_t n_fanouts, int64_t sample_lo, int64_t n_samples,
                           const int64_t *roots, uint64_t seed, void *stream, nd_result **out);
+
+/* ---- k-hop minibatch plans (CUDA graphs) -------------------------------------
+ * GraphSAGE-style sampling of many equal-size batches (driver.py:203-235 per
+ * batch, SURVEY §8(d) C3's 1,024-root batches): the fixed-layout SP k-hop run
+ * for n samples captured once into a CUDA graph over preallocated buffers;
+ * each batch is then a device parameter write, an optional roots copy and
+ * one graph launch, with no allocation and no host synchronisation.  Rows
+ * equal nd_run_individual's for the same roots and sample ids. */
+int nd_khop_plan_create(const nd_graph *g, const int64_t *host_fanouts, int64_t n_fanouts,
+                        int64_t n_samples, void *stream, nd_khop_plan **out);
+/* roots: device int64 [n] copied into the plan (NULL: the plan's own roots
+ * buffer, nd_khop_plan_outputs, was filled by the caller); asynchronous. */
+int nd_khop_plan_run(nd_khop_plan *p, const int64_t *roots, int64_t sample_lo, uint64_t seed,
+                     void *stream);
+/* device views: the plan's roots buffer, final offsets [n+1] (total =
+ * final_off[n]), final ids (capacity *cap), and each step's block
+ * (int32 [n * B], NULL slots -1) with its size */
+int nd_khop_plan_outputs(const nd_khop_plan *p, int64_t **roots, const int64_t **final_off,
+                         const int32_t **final_ids, int64_t *cap, const int32_t **blocks,
+                         int64_t *block_sizes, int64_t n_max);
+int nd_khop_plan_destroy(nd_khop_plan *p);
 
 #ifdef __cplusplus
 }

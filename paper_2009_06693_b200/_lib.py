@@ -72,6 +72,10 @@ SIGNATURES = {
     "nd_gather_ceiling": [i64, i32, i32, C.POINTER(C.c_double), vp],
     "nd_result_destroy": [vp],
     "nd_ooc_graph_create": [vp, vp, vp, i64, i64, i64, i32, vp, pp],
+    "nd_khop_plan_create": [vp, vp, i64, i64, vp, pp],
+    "nd_khop_plan_run": [vp, vp, i64, C.c_uint64, vp],
+    "nd_khop_plan_outputs": [vp, pp, pp, pp, pi64, pp, pi64, i64],
+    "nd_khop_plan_destroy": [vp],
     "nd_ooc_graph_destroy": [vp],
     "nd_ooc_graph_info": [vp, pi64, pi64, pi64, pi64, pi64],
     "nd_ooc_graph_parts": [vp, vp, i64],

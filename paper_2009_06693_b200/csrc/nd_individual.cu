@@ -1899,3 +1899,212 @@ extern "C" int nd_run_individual(const nd_graph* G, int app_code, const double* 
   *out_res = res;
   return ND_OK;
 }
+
+// ---- k-hop minibatch plans: one CUDA graph per (graph, fanouts, batch size) ----
+// GraphSAGE trains on many small batches (1,024 roots); a
+// batch through nd_run_individual is ~15 launches, stream-ordered
+// allocations and one host synchronisation (totals size the outputs), so a
+// single batch costs far more than its sampling.  A plan allocates every
+// buffer once with upper-bound sizes (final ids: n * (1 + sum of the step
+// blocks)), captures the fixed-layout SP run for n samples into a CUDA graph
+// whose kernels read the batch's roots and (sample_lo, seed) from device
+// memory, and replays it per batch: no allocation, no host synchronisation,
+// one graph launch.  Rows equal nd_run_individual's for the same roots and
+// sample ids (driver.py:203-235 with keyed draws, tests/test_gpu_khop_plan.py).
+
+struct KhopDyn {
+  int64_t sample_lo;
+  uint64_t seed;
+};
+
+namespace {
+
+__global__ void k_khop_set_dyn(KhopDyn* d, int64_t sample_lo, uint64_t seed) {
+  d->sample_lo = sample_lo;
+  d->seed = seed;
+}
+
+// one thread per (sample, parent, slot) of step s: u % deg over the parent's
+// row (_ckernels.pyx:212-223), key (seed, sample, step, rank, slot) read from
+// the batch's device parameters; per-sample non-NULL counts as k_fx_sample
+__global__ void __launch_bounds__(IND_BLOCK) k_fxg_sample(const int64_t* __restrict__ row,
+                                                         const int32_t* __restrict__ col,
+                                                         const KhopDyn* __restrict__ dyn, int step,
+                                                         int64_t n, FastDiv Bp, FastDiv m,
+                                                         const int32_t* __restrict__ prev,
+                                                         const int32_t* __restrict__ rank,
+                                                         int32_t* __restrict__ out,
+                                                         unsigned long long* __restrict__ cnt) {
+  const int64_t sample_lo = dyn->sample_lo;
+  const uint64_t base0 = key_base(dyn->seed, (uint64_t)step, 0, 0);
+  const int64_t total = n * (int64_t)Bp.d * m.d;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t q0 = blockIdx.x * (int64_t)blockDim.x; q0 < total; q0 += stride) {
+    const int64_t q = q0 + threadIdx.x;
+    int64_t i = -1;
+    int32_t o = -1;
+    if (q < total) {
+      const uint32_t ip = m.div((uint32_t)q), slot = (uint32_t)q - ip * m.d;
+      const int32_t v = prev[ip];
+      i = Bp.div(ip);
+      if (v >= 0) {
+        const int64_t lo = __ldg(row + v), deg = __ldg(row + v + 1) - lo;
+        if (deg > 0) {
+          const uint64_t ik = key_item((uint64_t)(sample_lo + i), (uint64_t)rank[ip], (uint64_t)slot);
+          o = __ldg(col + lo + (int64_t)mod_u64(draw_u64(base0, ik), (uint64_t)deg));
+        }
+      }
+      out[q] = o;
+    }
+    const unsigned act = __ballot_sync(0xffffffffu, o >= 0);
+    const unsigned same = __match_any_sync(0xffffffffu, i);
+    const unsigned grp = act & same;
+    if (o >= 0 && (threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(cnt + i, (unsigned long long)__popc(grp));
+  }
+}
+
+}  // namespace
+
+struct nd_khop_plan {
+  const nd_graph* G = nullptr;
+  int64_t n = 0, S = 0, cap = 0;
+  int64_t B[9] = {}, fan[8] = {};
+  int64_t* roots = nullptr;      // int64 [n], filled per batch
+  KhopDyn* dyn = nullptr;
+  int32_t* blk[9] = {};
+  int32_t* rank[8] = {};
+  int64_t* nn[8] = {};
+  unsigned long long* scnt = nullptr;
+  unsigned long long* fetch = nullptr;
+  int64_t *flen = nullptr, *final_off = nullptr, *roots_out = nullptr, *roots_off = nullptr;
+  int32_t* final_ids = nullptr;
+  void* tmp = nullptr;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+};
+
+extern "C" int nd_khop_plan_destroy(nd_khop_plan* p) {
+  if (!p) return ND_OK;
+  if (p->exec) cudaGraphExecDestroy(p->exec);
+  if (p->graph) cudaGraphDestroy(p->graph);
+  for (auto* x : p->blk) cudaFree(x);
+  for (auto* x : p->rank) cudaFree(x);
+  for (auto* x : p->nn) cudaFree(x);
+  cudaFree(p->roots); cudaFree(p->dyn); cudaFree(p->scnt); cudaFree(p->fetch);
+  cudaFree(p->flen); cudaFree(p->final_off); cudaFree(p->roots_out); cudaFree(p->roots_off);
+  cudaFree(p->final_ids); cudaFree(p->tmp);
+  delete p;
+  return ND_OK;
+}
+
+extern "C" int nd_khop_plan_create(const nd_graph* G, const int64_t* host_fanouts, int64_t n_fanouts,
+                                   int64_t n_samples, void* stream, nd_khop_plan** out) {
+  NvtxRange nvtx("nd_khop_plan_create");
+  if (!G || !out || n_samples <= 0 || n_samples >= (1ll << 31) || n_fanouts < 1 || n_fanouts > 8)
+    return ND_ERR_ARG;
+  auto* p = new nd_khop_plan();
+  p->G = G;
+  p->n = n_samples;
+  p->S = n_fanouts;
+  p->B[0] = 1;
+  int64_t cells = 1;
+  for (int64_t k = 0; k < n_fanouts; k++) {
+    if (host_fanouts[k] < 1) { delete p; return ND_ERR_ARG; }
+    p->fan[k] = host_fanouts[k];
+    p->B[k + 1] = p->B[k] * host_fanouts[k];
+    cells += p->B[k + 1];
+    if ((double)n_samples * (double)p->B[k + 1] >= 4.0e9) { delete p; return ND_ERR_ARG; }
+  }
+  const int64_t n = n_samples;
+  p->cap = n * cells;  // roots + every slot of every step: the final ids' upper bound
+  auto fail = [&](cudaError_t e) {
+    nd_set_last_error(cudaGetErrorString(e), __FILE__, __LINE__);
+    nd_khop_plan_destroy(p);
+    return e == cudaErrorMemoryAllocation ? ND_ERR_NOMEM : ND_ERR_CUDA;
+  };
+  cudaError_t e = cudaSuccess;
+#define PLAN_ALLOC(ptr, count) \
+  if ((e = cudaMalloc(&(ptr), (size_t)(count) * sizeof(*(ptr)))) != cudaSuccess) return fail(e)
+  PLAN_ALLOC(p->roots, n);
+  PLAN_ALLOC(p->dyn, 1);
+  for (int64_t k = 0; k <= p->S; k++) PLAN_ALLOC(p->blk[k], n * p->B[k]);
+  for (int64_t k = 0; k < p->S; k++) {
+    PLAN_ALLOC(p->rank[k], n * p->B[k]);
+    PLAN_ALLOC(p->nn[k], n);
+  }
+  PLAN_ALLOC(p->scnt, n);
+  PLAN_ALLOC(p->fetch, 1);
+  PLAN_ALLOC(p->flen, n + 1);
+  PLAN_ALLOC(p->final_off, n + 1);
+  PLAN_ALLOC(p->roots_out, n);
+  PLAN_ALLOC(p->roots_off, n + 1);
+  PLAN_ALLOC(p->final_ids, p->cap);
+  size_t tb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, p->flen, p->final_off, n + 1);
+  PLAN_ALLOC(*reinterpret_cast<char**>(&p->tmp), tb + 16);
+#undef PLAN_ALLOC
+  // capture the batch: roots -> blocks -> counts -> offsets -> final rows
+  cudaStream_t cs;
+  if ((e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking)) != cudaSuccess) return fail(e);
+  const DevGraph& g = G->g;
+  FxSteps FS;
+  FS.n_steps = (int)p->S;
+  for (int64_t k = 0; k < p->S; k++) { FS.blk[k] = p->blk[k + 1]; FS.B[k] = p->B[k + 1]; }
+  e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+  if (e == cudaSuccess) {
+    cudaMemsetAsync(p->scnt, 0, n * sizeof(unsigned long long), cs);
+    k_fx_narrow_roots<<<nd_grid(n, 256), 256, 0, cs>>>(p->roots, n, p->blk[0]);
+    for (int64_t k = 0; k < p->S; k++) {
+      k_fx_rank<<<nd_grid(n * 32, 256, 148 * 32), 256, 0, cs>>>(p->blk[k], n, p->B[k], p->rank[k],
+                                                                p->nn[k], p->fetch);
+      k_fxg_sample<<<nd_grid(n * p->B[k + 1], IND_BLOCK, 148 * 64), IND_BLOCK, 0, cs>>>(
+          g.row, g.col, p->dyn, (int)k, n, FastDiv((uint32_t)p->B[k]), FastDiv((uint32_t)p->fan[k]),
+          p->blk[k], p->rank[k], p->blk[k + 1], p->scnt);
+    }
+    k_fx_flen<<<nd_grid(n + 1, 256), 256, 0, cs>>>(p->scnt, n, 1, p->flen);
+    cub::DeviceScan::ExclusiveSum(p->tmp, tb, p->flen, p->final_off, n + 1, cs);
+    k_fx_final<int32_t><<<nd_grid(n * 32, 256, 148 * 32), 256, 0, cs>>>(FS, p->blk[0], n, 1, p->final_off,
+                                                                       p->final_ids, p->roots_out,
+                                                                       p->roots_off);
+    e = cudaStreamEndCapture(cs, &p->graph);
+  }
+  if (e == cudaSuccess) e = cudaGraphInstantiate(&p->exec, p->graph, 0);
+  cudaStreamDestroy(cs);
+  if (e != cudaSuccess) return fail(e);
+  (void)stream;
+  *out = p;
+  return ND_OK;
+}
+
+// One batch: the roots (device int64 [n], copied into the plan; NULL: the
+// plan's roots buffer was filled by the caller) with sample ids
+// [sample_lo, sample_lo + n) and the seed, then the captured graph.  Fully
+// asynchronous on `stream`; outputs (nd_khop_plan_outputs) are valid after it.
+extern "C" int nd_khop_plan_run(nd_khop_plan* p, const int64_t* roots, int64_t sample_lo,
+                                uint64_t seed, void* stream) {
+  if (!p || sample_lo < 0) return ND_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  k_khop_set_dyn<<<1, 1, 0, s>>>(p->dyn, sample_lo, seed);
+  if (roots && roots != p->roots)
+    ND_CUDA_TRY(cudaMemcpyAsync(p->roots, roots, p->n * sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+  ND_CUDA_TRY(cudaGraphLaunch(p->exec, s));
+  return ND_OK;
+}
+
+// Device views: roots buffer (int64 [n]), final offsets (int64 [n+1]; the
+// total is final_off[n]), final ids (int32, capacity `cap`), and step k's
+// block (int32 [n * B_{k+1}], NULL slots -1) for k < n_steps.
+extern "C" int nd_khop_plan_outputs(const nd_khop_plan* p, int64_t** roots, const int64_t** final_off,
+                                    const int32_t** final_ids, int64_t* cap, const int32_t** blocks,
+                                    int64_t* block_sizes, int64_t n_max) {
+  if (!p) return ND_ERR_ARG;
+  if (roots) *roots = p->roots;
+  if (final_off) *final_off = p->final_off;
+  if (final_ids) *final_ids = p->final_ids;
+  if (cap) *cap = p->cap;
+  for (int64_t k = 0; k < p->S && k < n_max; k++) {
+    if (blocks) blocks[k] = p->blk[k + 1];
+    if (block_sizes) block_sizes[k] = p->n * p->B[k + 1];
+  }
+  return ND_OK;
+}
