@@ -191,11 +191,15 @@ class ShardedJob:
             with torch.cuda.stream(st):
                 for a, b in j["pieces"]:
                     dr = None
-                    if b > a:
-                        dr = run_device(j["app"], self.dg, n_samples=b - a, sample_lo=a,
-                                        seed=j["seed"], paradigm=self.paradigm, stream=st,
-                                        sync=False,
-                                        roots_device=droots[i][a - j["lo"]:b - j["lo"]])
+                    try:
+                        if b > a:
+                            dr = run_device(j["app"], self.dg, n_samples=b - a, sample_lo=a,
+                                            seed=j["seed"], paradigm=self.paradigm, stream=st,
+                                            sync=False,
+                                            roots_device=droots[i][a - j["lo"]:b - j["lo"]])
+                    except BaseException as e:  # the main thread re-raises it in order
+                        queues[i].put((e, None))
+                        return
                     ev = torch.cuda.Event()
                     ev.record(st)
                     queues[i].put((dr, ev))
@@ -209,6 +213,13 @@ class ShardedJob:
                for c in range(len(self.jobs[i]["pieces"]))]
         for i, c in seq:
             dr, ev = queues[i].get()
+            if isinstance(dr, BaseException):
+                # the other jobs finish before the error propagates (no orphaned work)
+                for f in futs:
+                    f.exception()
+                for r in runs:
+                    r.close()
+                raise dr
             cur.wait_event(ev)
             if dr is not None:
                 runs.append(dr)
