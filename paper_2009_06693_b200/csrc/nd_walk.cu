@@ -1024,12 +1024,13 @@ static int pw_run_windows(const nd_graph* G, const NdApp& a, uint64_t seed, int6
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  // register/occupancy variant of the persistent kernel (ND_WALK_MINB = 4|5|6|8
+  // register/occupancy variant of the persistent kernel (ND_WALK_MINB = 3|4|5|6|8
   // resident CTAs per SM requested from ptxas; default measured best)
   static const int minb = getenv("ND_WALK_MINB") ? atoi(getenv("ND_WALK_MINB")) : 4;
   void (*kern)(PWArgs) = minb >= 8 ? k_walk_persistent<8>
                          : minb == 6 ? k_walk_persistent<6>
-                         : minb == 5 ? k_walk_persistent<5> : k_walk_persistent<4>;
+                         : minb == 5 ? k_walk_persistent<5>
+                         : minb == 3 ? k_walk_persistent<3> : k_walk_persistent<4>;
   int occ = 4;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, 0);
   if (occ < 1) occ = 1;
