@@ -30,7 +30,7 @@ torch.cuda.synchronize()
 build = time.perf_counter() - t0
 L.nd_set_profiling(1)
 ms = []
-for it in range(4):
+for it in range(int(os.environ.get('PROBE_ITERS', '4'))):
     dr = run_device(make_app("deepwalk"), dg, n_samples=1 << 23, seed=7, paradigm="sp")
     ms.append(dr.profile_ms[1])
     dr.close()
