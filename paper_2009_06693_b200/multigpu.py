@@ -16,7 +16,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from .sharding import shard_for_rank, worker_ranges  # noqa: F401
+from .sharding import piece_ranges, shard_for_rank, worker_ranges  # noqa: F401
 
 
 def gather_rows(off, ids, group=None, dst: int = 0):
@@ -138,14 +138,13 @@ class ShardedJob:
                 raise ValueError("ShardedJob runs walk and individual apps with one root per sample")
             lo, hi = shard_for_rank(n_total, ws, rank)
             n = hi - lo
+            pieces = piece_ranges(n_total, ws, rank, chunks)
             droots = torch.empty(max(n, 1), dtype=torch.int64, device="cuda")
             if n:
                 _lib.check(L.nd_uniform_roots(self.dg.handle, 1, C.c_uint64(seed), lo, n,
                                               _lib.ptr(droots), _lib.stream_ptr()),
                            "nd_uniform_roots")
             roots_host = droots[:n].cpu().pin_memory()
-            pieces = [(lo + a, lo + b) for a, b in worker_ranges(n, chunks)] if n else []
-            pieces += [(hi, hi)] * (chunks - len(pieces))  # every rank gathers `chunks` pieces
             self.jobs.append(dict(app=app, n_total=n_total, seed=seed, lo=lo, n=n,
                                   roots_host=roots_host, pieces=pieces))
         self._host = {}

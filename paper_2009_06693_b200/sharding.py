@@ -26,3 +26,14 @@ def shard_for_rank(n: int, world_size: int, rank: int) -> tuple[int, int]:
     if rank < len(ranges):
         return ranges[rank]
     return (n, n)
+
+
+def piece_ranges(n: int, world_size: int, rank: int, chunks: int) -> list[tuple[int, int]]:
+    """This rank's shard cut into `chunks` contiguous pieces (worker_ranges of
+    the shard); ranks with fewer samples than pieces get empty pieces at the
+    end, so every rank has exactly `chunks` pieces (multigpu.ShardedJob
+    gathers piece c of every rank together)."""
+    lo, hi = shard_for_rank(n, world_size, rank)
+    chunks = max(1, int(chunks))
+    pieces = [(lo + a, lo + b) for a, b in worker_ranges(hi - lo, chunks)] if hi > lo else []
+    return pieces + [(hi, hi)] * (chunks - len(pieces))

@@ -53,3 +53,18 @@ def test_dedup_and_fallback_boundary():
     # SP fallback iff 0 < distinct < m_i
     assert not fallback_check(0, 4) and fallback_check(1, 4) and fallback_check(3, 4)
     assert not fallback_check(4, 4) and not fallback_check(5, 4)
+
+
+def test_validation_row_format_and_cli_flag():
+    """validate.ValidationRow prints the reference's line (bench.py:224-236)
+    and the CLI accepts --validate (cli.py:58)."""
+    from paper_2009_06693_b200.cli import build_parser
+    from paper_2009_06693_b200.validate import ValidationRow, _empirical_counts
+    import numpy as np
+    row = ValidationRow("deepwalk", "weighted-pick max |err|", 0.0012345, 0.005, True)
+    assert row.line() == ("pass  deepwalk   weighted-pick max |err|      value=0.001235 "
+                          "threshold=0.005")
+    assert ValidationRow("ppr", "geometric fit p-value", 0.0, 0.001, False).line().startswith("FAIL  ppr")
+    assert np.array_equal(_empirical_counts(np.array([3, 1, 3, 7]), np.array([1, 3, 7])), [1, 2, 1])
+    args = build_parser().parse_args(["--app", "khop", "--synth", "cycle:8", "--validate"])
+    assert args.validate is True

@@ -84,3 +84,23 @@ def test_worker_ranges_cover_exactly():
             if cover is not None:
                 assert cover == list(range(n))
             assert sum(hi - lo for lo, hi in rs) == n
+
+
+def test_piece_ranges_cover_each_sample_once():
+    """multigpu.ShardedJob's pieces: every rank has exactly `chunks` pieces,
+    piece c of all ranks together with the other pieces covers [0, n) once,
+    and each rank's pieces are its worker_ranges shard in order."""
+    from paper_2009_06693_b200.sharding import piece_ranges, shard_for_rank
+    for n in (0, 1, 5, 7, 1000, 8_388_608):
+        for ws in (1, 2, 3, 8):
+            for chunks in (1, 3, 6):
+                seen = 0
+                for r in range(ws):
+                    ps = piece_ranges(n, ws, r, chunks)
+                    assert len(ps) == chunks
+                    lo, hi = shard_for_rank(n, ws, r)
+                    assert ps[0][0] == lo and ps[-1][1] == hi
+                    assert all(a <= b for a, b in ps)
+                    assert all(ps[k][1] == ps[k + 1][0] for k in range(chunks - 1))
+                    seen += sum(b - a for a, b in ps)
+                assert seen == n
