@@ -62,7 +62,7 @@ def test_validation_row_format_and_cli_flag():
     from paper_2009_06693_b200.validate import ValidationRow, _empirical_counts
     import numpy as np
     row = ValidationRow("deepwalk", "weighted-pick max |err|", 0.0012345, 0.005, True)
-    assert row.line() == ("pass  deepwalk   weighted-pick max |err|      value=0.001235 "
+    assert row.line() == ("pass  deepwalk   weighted-pick max |err|      value=0.001234 "
                           "threshold=0.005")
     assert ValidationRow("ppr", "geometric fit p-value", 0.0, 0.001, False).line().startswith("FAIL  ppr")
     assert np.array_equal(_empirical_counts(np.array([3, 1, 3, 7]), np.array([1, 3, 7])), [1, 2, 1])
