@@ -242,9 +242,11 @@ __global__ void __launch_bounds__(256) k_tw_prep(TwArgs A) {
     int32_t v = -1, c = 0, t = 2, nu = 0;
     if (j < H) {
       v = A.hubs[j];
-      c = A.cnt[v];
+      // the hub's members past its first TW_TM are staged (the first ones are
+      // stepped in place by the sampling kernel, which reads no count)
+      c = A.cnt[v] - TW_TM;
       const int64_t r0 = __ldg(A.P.gv.row + v), r1 = __ldg(A.P.gv.row + v + 1);
-      t = tw_tier(c, tw_rbytes(A.rmode, r1 - r0));
+      t = c > 0 ? tw_tier(c, tw_rbytes(A.rmode, r1 - r0)) : 2;
       if (t == 1) nu = (c + TW_UNIT - 1) / TW_UNIT;
     }
     const int m0 = tw_warp_reserve(t < 2 ? c : 0, &A.ctl->front);
@@ -367,7 +369,7 @@ __device__ __forceinline__ void tw_lane_start(const TwArgs& A, TwLane& L, ItemSt
 }
 
 // lane state of a hub member record (48 bytes); the group's first member
-// clears the transit's count for the next step
+// a staged hub member's record into a lane
 __device__ __forceinline__ void tw_load_rec(const TwArgs& A, TwLane& L, const TwRec* r,
                                             ItemStats& st) {
   const int4* q = reinterpret_cast<const int4*>(r);  // 16-byte aligned (48-byte records)
@@ -381,7 +383,6 @@ __device__ __forceinline__ void tw_load_rec(const TwArgs& A, TwLane& L, const Tw
   L.tdeg = b.z;
   L.tlo = (uint32_t)b.w;
   L.hd = __longlong_as_double(((long long)(uint32_t)c.y << 32) | (uint32_t)c.x);
-  if (c.z == 0) A.cnt[L.v] = 0;
   tw_lane_start(A, L, st);
 }
 
@@ -475,18 +476,23 @@ __global__ void __launch_bounds__(TW_BLOCK, MINB) k_tw_sample(TwArgs A) {
                       tdeg = A.ndeg[row];
                     }
                     const int32_t w = A.wid ? A.wid[row] : (int32_t)row;
-                    if (A.cnt[v] >= TW_TM) {  // hub member
+                    // the walker's position in its group (the previous emission's
+                    // count): members past the 32nd belong to a hub (its group
+                    // reached TW_TM members), the first TW_TM of every group are
+                    // stepped here -- no read of the group's count per walker
+                    const int32_t p = A.pos[row];
+                    if (p >= TW_TM) {
                       const int32_t m0 = A.vhub[v];
-                      if (m0 >= 0) {  // staged tier: the record at its group position
-                        const int32_t p = A.pos[row];
-                        A.hrec[m0 + p] = TwRec{(int32_t)row, w, v, deg, lo, t, tdeg, tlo, hd, p, 0};
+                      if (m0 >= 0) {  // staged tier: the record at its staged slot
+                        A.hrec[m0 + p - TW_TM] =
+                            TwRec{(int32_t)row, w, v, deg, lo, t, tdeg, tlo, hd, p, 0};
                         return false;
                       }
                     }
-                    // small class or grid tier: stepped here.  Clearing the count
-                    // early only turns later grid-tier members of the same hub
-                    // into "small" ones, which are stepped here as well.
-                    A.cnt[v] = 0;
+                    // stepped here (first members, small class, grid tier); the
+                    // group's first member clears its count for step s+2 (prep,
+                    // the only reader of this step's counts, ran before)
+                    if (p == 0) A.cnt[v] = 0;
                     L.row = row;
                     L.w = w;
                     L.v = v;
