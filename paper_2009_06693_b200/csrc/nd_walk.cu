@@ -1672,6 +1672,14 @@ static int run_chain_walk_hub(const nd_graph* G, const NdApp& a, int64_t sample_
   const size_t e_run = prof.mark();
   bool tail = false;
   int rc = ND_OK;
+  // staged hub tiers on until a window shows they do not engage (ND_TW_STAGE=1:
+  // always on, 0: always off; development)
+  const char* stg_env = getenv("ND_TW_STAGE");
+  bool staging = !(stg_env && stg_env[0] == '0');
+  const bool stage_fixed = stg_env != nullptr;
+  unsigned long long hubs_prev = 0, staged_prev = 0;
+  if (!staging)
+    for (int b = 0; b < 2; b++) ND_CUDA_TRY(cudaMemsetAsync(vhub[b], 0xFF, V * sizeof(int32_t), s));
   while (rows > 0 && step < max_steps) {
     if (rows <= tail_T && rows * (max_steps - step) < (1ll << 31)) {
       tail = true;
@@ -1710,6 +1718,7 @@ static int run_chain_walk_hub(const nd_graph* G, const NdApp& a, int64_t sample_
     A.max_len = maxlen;
     A.hrec = hrec;
     A.hcap = n;
+    A.hubs_seen = ctr + 3;
 
     A.wunits = wunits;
     A.cunits = cunits;
@@ -1744,12 +1753,16 @@ static int run_chain_walk_hub(const nd_graph* G, const NdApp& a, int64_t sample_
       }
       tp.mark(s, 0);
       prof.step_begin();
-      k_tw_prep<<<nd_grid(rows / TW_TM + 1, 256, nsm * 4), 256, 0, s>>>(A);
+      if (staging) {
+        k_tw_prep<<<nd_grid(rows / TW_TM + 1, 256, nsm * 4), 256, 0, s>>>(A);
+      } else {  // every hub in the grid tier: the prep's only other duty
+        ND_CUDA_TRY(cudaMemsetAsync(A.nctl, 0, sizeof(TwCtl), s));
+      }
       prof.step_built();
       tp.mark(s, 1);
       k_tw_sample<4><<<nsm * occ, TW_BLOCK, 0, s>>>(A);
       tp.mark(s, 2);
-      k_tw_hub<4><<<nsm * hocc, TW_BLOCK, TW_HUB_SMEM, s>>>(A);
+      if (staging) k_tw_hub<4><<<nsm * hocc, TW_BLOCK, TW_HUB_SMEM, s>>>(A);
       prof.step_sampled();
       tp.mark(s, 3);
       if (cudaGetLastError() != cudaSuccess) { rc = ND_ERR_CUDA; break; }
@@ -1777,6 +1790,23 @@ static int run_chain_walk_hub(const nd_graph* G, const NdApp& a, int64_t sample_
     t0 = ct;
     rows = h[0];
     step += Lw;
+    // Staged tiers that never engage: when this window's prep kernels classed
+    // hubs but none of their members was sampled from a staged row (rows too
+    // long for their members to pay, PAPER.md:832-838's trade-off), the
+    // remaining windows run every hub in the grid tier and skip the prep and
+    // hub launches.  Which tier samples a member does not change any row;
+    // the class statistics come from the count crossings either way.
+    if (staging && !stage_fixed) {
+      unsigned long long hc[2];
+      if (nd_d2h(hc, ctr + 3, sizeof(hc), s) != ND_OK) { rc = ND_ERR_CUDA; break; }
+      if (hc[0] > hubs_prev && hc[1] == staged_prev) {
+        staging = false;
+        for (int b = 0; b < 2; b++)
+          ND_CUDA_TRY(cudaMemsetAsync(vhub[b], 0xFF, V * sizeof(int32_t), s));
+      }
+      hubs_prev = hc[0];
+      staged_prev = hc[1];
+    }
   }
   double sample_ms = 0.0;
   if (rc == ND_OK && tail && step == 0) {  // every walker in the tail: rows from the roots

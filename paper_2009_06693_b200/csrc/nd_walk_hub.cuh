@@ -92,6 +92,7 @@ struct TwArgs {
   double* nhd;
   int32_t* pos;         // group position of the row's walker this step
   unsigned long long* tier;  // [0] staged hub members stepped, [1] walkers stepped in place
+  unsigned long long* hubs_seen;  // hubs the prep kernels have classed (all steps)
   int32_t* out;         // [Lw, rows]
   int32_t* nnz;         // per row: non-NULL values of the window
   int32_t* died;        // per walker: ended with a NULL
@@ -236,7 +237,10 @@ __device__ __forceinline__ int tw_warp_reserve(int n, int* gcount) {
 
 __global__ void __launch_bounds__(256) k_tw_prep(TwArgs A) {
   const int H = A.ctl->nhub;
-  if (blockIdx.x == 0 && threadIdx.x == 0) *A.nctl = TwCtl{};
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *A.nctl = TwCtl{};
+    if (H) atomicAdd(A.hubs_seen, (unsigned long long)H);
+  }
   for (int jb = blockIdx.x * blockDim.x; jb < H; jb += gridDim.x * blockDim.x) {
     const int j = jb + threadIdx.x;
     int32_t v = -1, c = 0, t = 2, nu = 0;
