@@ -1678,6 +1678,10 @@ static int run_chain_walk_hub(const nd_graph* G, const NdApp& a, int64_t sample_
   bool staging = !(stg_env && stg_env[0] == '0');
   const bool stage_fixed = stg_env != nullptr;
   unsigned long long hubs_prev = 0, staged_prev = 0;
+  bool ctl_clean = false;  // the next step's control was zeroed by a sampling kernel
+  unsigned int* done = nullptr;
+  ND_CUDA_TRY(nd_alloc(&done, 1, s));
+  ND_CUDA_TRY(cudaMemsetAsync(done, 0, sizeof(unsigned int), s));
   if (!staging)
     for (int b = 0; b < 2; b++) ND_CUDA_TRY(cudaMemsetAsync(vhub[b], 0xFF, V * sizeof(int32_t), s));
   while (rows > 0 && step < max_steps) {
@@ -1719,6 +1723,8 @@ static int run_chain_walk_hub(const nd_graph* G, const NdApp& a, int64_t sample_
     A.hrec = hrec;
     A.hcap = n;
     A.hubs_seen = ctr + 3;
+    A.done = done;
+    ctl_clean = false;  // the window start zeroed both controls; count0 fills the first
 
     A.wunits = wunits;
     A.cunits = cunits;
@@ -1753,10 +1759,18 @@ static int run_chain_walk_hub(const nd_graph* G, const NdApp& a, int64_t sample_
       }
       tp.mark(s, 0);
       prof.step_begin();
+      A.reset_self = nullptr;
       if (staging) {
         k_tw_prep<<<nd_grid(rows / TW_TM + 1, 256, nsm * 4), 256, 0, s>>>(A);
-      } else {  // every hub in the grid tier: the prep's only other duty
-        ND_CUDA_TRY(cudaMemsetAsync(A.nctl, 0, sizeof(TwCtl), s));
+        ctl_clean = false;
+      } else {
+        // every hub in the grid tier; the prep's other duty, zeroing the step
+        // control the emission fills, is done by the previous step's last CTA
+        // (its own control), except at the first step of a window or after
+        // a staged step
+        if (!ctl_clean) ND_CUDA_TRY(cudaMemsetAsync(A.nctl, 0, sizeof(TwCtl), s));
+        A.reset_self = A.ctl;
+        ctl_clean = true;
       }
       prof.step_built();
       tp.mark(s, 1);
@@ -1908,6 +1922,7 @@ static int run_chain_walk_hub(const nd_graph* G, const NdApp& a, int64_t sample_
   nd_free(hrec, s); nd_free(pos, s); nd_free(flen, s); nd_free(hist, s);
   nd_free(cnt[0], s);
   for (int b = 0; b < 2; b++) { nd_free(vhub[b], s); nd_free(hubs[b], s); }
+  nd_free(done, s);
   for (int b = 0; b < 2; b++) { nd_free(cur[b], s); nd_free(lo[b], s); nd_free(dg[b], s); nd_free(hd[b], s); }
   if (rc != ND_OK) {
     nd_free(stats, s); nd_free(final_off, s); nd_free(final_ids, s); nd_free(clen, s); nd_free(roots_out, s);

@@ -93,6 +93,9 @@ struct TwArgs {
   int32_t* pos;         // group position of the row's walker this step
   unsigned long long* tier;  // [0] staged hub members stepped, [1] walkers stepped in place
   unsigned long long* hubs_seen;  // hubs the prep kernels have classed (all steps)
+  TwCtl* reset_self;    // staged tiers off: the sampling kernel's last CTA zeroes its own
+                        // step control (the next-but-one step's), no prep launch needed
+  unsigned int* done;   // CTAs finished (last-CTA detection; reset by the last one)
   int32_t* out;         // [Lw, rows]
   int32_t* nnz;         // per row: non-NULL values of the window
   int32_t* died;        // per walker: ended with a NULL
@@ -514,6 +517,17 @@ __global__ void __launch_bounds__(TW_BLOCK, MINB) k_tw_sample(TwArgs A) {
   flush_stats(st, A.P.ctr);
   tw_flush_len(mlen, A.max_len);
   tw_flush_tier(inplace, A.tier + 1);
+  if (A.reset_self) {  // every CTA is past the step's work queue: the last one resets it
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      if (atomicAdd(A.done, 1u) == gridDim.x - 1) {
+        *A.reset_self = TwCtl{};
+        *A.done = 0;
+        __threadfence();
+      }
+    }
+  }
 }
 
 // bytes and source of the records a hub's members read this step
