@@ -1057,8 +1057,13 @@ def main():
     c2_footprint = dg.footprint()
     dg.close()
     torch.cuda.empty_cache()
+    # every leg starts from a trimmed allocation pool (the C2 legs leave it
+    # shaped by multi-GB windows; the k-hop TP steps measured 5% slower on it)
+    L.nd_pool_trim(0)
     c3 = None if args.no_c3 else c3_leg(args, ws, rank, barrier, rdev)
+    L.nd_pool_trim(0)
     c14 = {} if args.no_c14 else c1_c4_legs(args, ws, rank, barrier, rdev)
+    L.nd_pool_trim(0)
     c5 = None
     if not args.no_c5:
         c5 = c5_leg(args, ws, rank, barrier, rdev)

@@ -262,6 +262,9 @@ int nd_result_profile(const nd_result *r, double *ms, int64_t n);
 int nd_result_step_times(const nd_result *r, double *build_ms, double *sample_ms, int64_t n_max,
                          int64_t *n_out);
 int nd_set_profiling(int on);
+/* Return the stream-ordered allocation pool's unused memory beyond `keep`
+ * bytes to the device (between large jobs). */
+int nd_pool_trim(int64_t keep);
 /* Measured ceiling of dependent random 32-byte sector reads (sectors/s): one
  * pointer-chasing chain per thread, ctas_per_sm x 256 threads per SM, over a
  * `bytes` buffer (rounded down to a power of two).  The roofline a

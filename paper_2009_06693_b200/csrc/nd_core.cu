@@ -84,6 +84,19 @@ int nd_pool_init() {
   return ND_OK;
 }
 
+// Return the stream-ordered pool's unused memory to the device beyond `keep`
+// bytes (after a large job, so the next job's allocations are not carved
+// from a pool shaped by the previous one).
+extern "C" int nd_pool_trim(int64_t keep) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return ND_ERR_CUDA;
+  cudaDeviceSynchronize();
+  ND_CUDA_TRY(cudaMemPoolTrimTo(pool, keep > 0 ? (size_t)keep : 0));
+  return ND_OK;
+}
+
 // one pinned host word-block per thread for small D2H reads (no per-run
 // cudaMallocHost/cudaFreeHost, which serialise the device)
 __global__ void k_export(const unsigned char* __restrict__ src, unsigned char* __restrict__ dst,

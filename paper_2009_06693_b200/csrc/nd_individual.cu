@@ -1369,19 +1369,39 @@ static int run_individual_fixed(const nd_graph* G, const NdApp& a, const int64_t
       const HubThr th = hub_thresholds(fan[k]);
       const int64_t cap = th.tm >= 0x7fffffff ? 1 : N / th.tm + 1;
       const int64_t ucap = cap + N * fan[k] / HUB_UNIT + 1;
+      // the step's scratch in one pool allocation (nine arrays carved from it):
+      // fewer stream-ordered allocations per step keep the step's cost
+      // independent of how earlier jobs left the pool
       int32_t *gpos = nullptr, *hubs = nullptr, *hsz = nullptr, *hun = nullptr, *hoff = nullptr,
               *uoff = nullptr;
       MemRec *perm = nullptr, *small = nullptr;
       HubUnit* units = nullptr;
-      ND_CUDA_TRY(nd_alloc(&gpos, N, s));
-      ND_CUDA_TRY(nd_alloc(&hubs, cap, s));
-      ND_CUDA_TRY(nd_alloc(&hsz, cap + 1, s));
-      ND_CUDA_TRY(nd_alloc(&hun, cap + 1, s));
-      ND_CUDA_TRY(nd_alloc(&hoff, cap + 1, s));
-      ND_CUDA_TRY(nd_alloc(&uoff, cap + 1, s));
-      ND_CUDA_TRY(nd_alloc(&units, ucap, s));
-      ND_CUDA_TRY(nd_alloc(&perm, N, s));
-      ND_CUDA_TRY(nd_alloc(&small, N, s));
+      char* arena = nullptr;
+      size_t scan_bytes = 0, o_scan = 0;
+      {
+        size_t off = 0;
+        auto carve = [&](size_t bytes) {
+          const size_t at = off;
+          off += (bytes + 255) & ~(size_t)255;
+          return at;
+        };
+        const size_t o_gpos = carve(N * 4), o_hubs = carve(cap * 4), o_hsz = carve((cap + 1) * 4),
+                     o_hun = carve((cap + 1) * 4), o_hoff = carve((cap + 1) * 4),
+                     o_uoff = carve((cap + 1) * 4), o_units = carve(ucap * sizeof(HubUnit)),
+                     o_perm = carve(N * sizeof(MemRec)), o_small = carve(N * sizeof(MemRec));
+        cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, hsz, hoff, cap + 1, s);
+        o_scan = carve(scan_bytes);
+        ND_CUDA_TRY(nd_alloc(&arena, off, s));
+        gpos = reinterpret_cast<int32_t*>(arena + o_gpos);
+        hubs = reinterpret_cast<int32_t*>(arena + o_hubs);
+        hsz = reinterpret_cast<int32_t*>(arena + o_hsz);
+        hun = reinterpret_cast<int32_t*>(arena + o_hun);
+        hoff = reinterpret_cast<int32_t*>(arena + o_hoff);
+        uoff = reinterpret_cast<int32_t*>(arena + o_uoff);
+        units = reinterpret_cast<HubUnit*>(arena + o_units);
+        perm = reinterpret_cast<MemRec*>(arena + o_perm);
+        small = reinterpret_cast<MemRec*>(arena + o_small);
+      }
       ND_CUDA_TRY(cudaMemsetAsync(vinfo, 0, g.V * sizeof(int2), s));
       ND_CUDA_TRY(cudaMemsetAsync(nhub, 0, 2 * sizeof(int32_t), s));
       {
@@ -1392,13 +1412,10 @@ static int run_individual_fixed(const nd_graph* G, const NdApp& a, const int64_t
       }
       k_hub_sizes<<<nd_grid(cap + 1, 256), 256, 0, s>>>(hubs, nhub, cap, vinfo, fan[k], hsz, hun);
       {
-        size_t tb = 0;
-        cub::DeviceScan::ExclusiveSum(nullptr, tb, hsz, hoff, cap + 1, s);
-        void* tmp = nullptr;
-        ND_CUDA_TRY(nd_alloc((char**)&tmp, tb, s));
+        size_t tb = scan_bytes;
+        void* tmp = arena + o_scan;
         ND_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tb, hsz, hoff, cap + 1, s));
         ND_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tb, hun, uoff, cap + 1, s));
-        nd_free(tmp, s);
       }
       k_hub_units<<<nd_grid(cap, 256), 256, 0, s>>>(nhub, hubs, hoff, uoff, hun, g.row, fan[k],
                                                    units);
@@ -1417,8 +1434,7 @@ static int run_individual_fixed(const nd_graph* G, const NdApp& a, const int64_t
       kh<<<knob.hc_grid, IND_BLOCK + 32, HUB_CTA_SMEM, s>>>(hb);
       prof.step_sampled();
       ND_CUDA_TRY(cudaGetLastError());
-      nd_free(gpos, s); nd_free(hubs, s); nd_free(hsz, s); nd_free(hun, s); nd_free(hoff, s);
-      nd_free(uoff, s); nd_free(units, s); nd_free(perm, s); nd_free(small, s);
+      nd_free(arena, s);
     }
   }
   // final rows and step rows: counts, scans, one synchronisation for the totals

@@ -17,6 +17,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "nd_tp.cuh"
@@ -682,6 +683,10 @@ __global__ void k_pw_stats(const unsigned long long* __restrict__ hist, int64_t 
 
 static int g_profile = 0;
 int nd_profiling() { return g_profile; }
+// persisting-L2 set-aside shared by concurrent TP walk runs (nd_walk_hub engine)
+static std::mutex g_l2_mu;
+static int g_l2_users = 0;
+static size_t g_l2_prev = 0;
 extern "C" int nd_set_profiling(int on) {
   g_profile = on;
   return ND_OK;
@@ -1591,14 +1596,21 @@ static int run_chain_walk_hub(const nd_graph* G, const NdApp& a, int64_t sample_
   // random read per walker every step: keep them resident in L2 (persisting
   // window over cnt) so the walk's record traffic does not evict them.
   cudaStreamAttrValue l2win{}, l2off{};
-  bool l2set = false;
+  bool l2set = false, l2pin = false;
   {
     int max_persist = 0;
     cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
     const size_t want = (size_t)2 * V * sizeof(int32_t);
     if (max_persist > 0 && !getenv("ND_TW_NO_L2PIN")) {
+      // The set-aside is device-wide and outlives the run: the first of any
+      // concurrent TP runs records the previous limit, the last one restores
+      // it, so later kernels get the whole L2 back.
       size_t lim = 0;
-      cudaDeviceGetLimit(&lim, cudaLimitPersistingL2CacheSize);
+      {
+        std::lock_guard<std::mutex> lk(g_l2_mu);
+        cudaDeviceGetLimit(&lim, cudaLimitPersistingL2CacheSize);
+        if (g_l2_users++ == 0) g_l2_prev = lim;
+      }
       const size_t setaside = std::min<size_t>((size_t)max_persist, std::max(lim, want));
       if (lim < setaside) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, setaside);
       l2win.accessPolicyWindow.base_ptr = cnt[0];
@@ -1607,6 +1619,7 @@ static int run_chain_walk_hub(const nd_graph* G, const NdApp& a, int64_t sample_
       l2win.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
       l2win.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
       l2set = cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &l2win) == cudaSuccess;
+      l2pin = true;
       cudaGetLastError();
     }
   }
@@ -1847,7 +1860,15 @@ static int run_chain_walk_hub(const nd_graph* G, const NdApp& a, int64_t sample_
   if (l2set) {  // back to normal caching for the stream; release the persisting lines
     l2off.accessPolicyWindow.num_bytes = 0;
     cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &l2off);
-    cudaCtxResetPersistingL2Cache();
+    cudaGetLastError();
+  }
+  if (l2pin) {
+    std::lock_guard<std::mutex> lk(g_l2_mu);
+    if (--g_l2_users == 0) {
+      cudaStreamSynchronize(s);
+      cudaCtxResetPersistingL2Cache();
+      cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, g_l2_prev);
+    }
     cudaGetLastError();
   }
   const size_t e_sampled = prof.mark();
