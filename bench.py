@@ -564,6 +564,7 @@ def c1_c4_legs(args, ws, rank, barrier, rdev):
         ms, e, _ = _timed_runs(make_app("deepwalk"), dg, lo, hi - lo, par)
         ms, e = _rank_max_sum(ms, e, ws, rdev)
         c1[par] = {"ms": ms, "edges": e, "value": e / (ms / 1e3), "unit": "edges/s"}
+    c1["graph_footprint"] = dg.footprint()
     dg.close()
     out["c1"] = c1
     if DEV_SCALE is None:
@@ -585,6 +586,7 @@ def c1_c4_legs(args, ws, rank, barrier, rdev):
         _, rec = _rank_max_sum(0.0, rec, ws, rdev)
         c4[name] = {"N": N, "ms": ms, "sampled": smp, "recorded": rec,
                     "value": (smp + rec) / (ms / 1e3) if ms > 0 else None}
+    c4["graph_footprint"] = dg.footprint()
     dg.close()
     torch.cuda.empty_cache()
     out["c4"] = c4
@@ -649,6 +651,7 @@ def c3_leg(args, ws, rank, barrier, rdev):
                                  "kernels": "k_fx_sample" if par == "sp" else
                                             "k_fx_small + k_fx_hub_warp + k_fx_hub_cta"}}
     out["tp_vs_sp"] = out["tp"]["ms"] / out["sp"]["ms"]
+    out["graph_footprint"] = dg.footprint()
     # single 1,024-root batches (report C3's batch latency):
     # run_device per batch vs the CUDA-graph plan (minibatch.KhopBatchSampler)
     # replayed over 228 batches back to back, keyed roots of each batch's ids
