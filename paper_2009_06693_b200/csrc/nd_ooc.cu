@@ -286,7 +286,7 @@ __global__ void k_ooc_narrow(const int64_t* __restrict__ in, int64_t n, int32_t*
 // for the copy before the partition's kernel.
 struct Shuttle {
   nd_ooc_graph* G;
-  cudaStream_t s, cs;
+  cudaStream_t s = nullptr, cs = nullptr;
   cudaEvent_t copied[2] = {}, freed[2] = {};
   int next_buf = 0;
   int init() {
@@ -316,14 +316,17 @@ struct Shuttle {
   }
   int use(int b) { ND_CUDA_TRY(cudaStreamWaitEvent(s, copied[b], 0)); return ND_OK; }
   int release(int b) { ND_CUDA_TRY(cudaEventRecord(freed[b], s)); return ND_OK; }
-  void destroy() {
-    cudaStreamSynchronize(cs);
+  void destroy() {  // idempotent; also run by the destructor on early returns
+    if (cs) cudaStreamSynchronize(cs);
     for (int b = 0; b < 2; b++) {
       if (copied[b]) cudaEventDestroy(copied[b]);
       if (freed[b]) cudaEventDestroy(freed[b]);
+      copied[b] = freed[b] = nullptr;
     }
     if (cs) cudaStreamDestroy(cs);
+    cs = nullptr;
   }
+  ~Shuttle() { destroy(); }
 };
 
 // partitions with work, in order, from a device histogram
