@@ -1737,6 +1737,7 @@ static int run_chain_walk_hub(const nd_graph* G, const NdApp& a, int64_t sample_
     A.hcap = n;
     A.hubs_seen = ctr + 3;
     A.done = done;
+    A.no_hub_list = !staging;
     ctl_clean = false;  // the window start zeroed both controls; count0 fills the first
 
     A.wunits = wunits;

@@ -96,6 +96,7 @@ struct TwArgs {
   TwCtl* reset_self;    // staged tiers off: the sampling kernel's last CTA zeroes its own
                         // step control (the next-but-one step's), no prep launch needed
   unsigned int* done;   // CTAs finished (last-CTA detection; reset by the last one)
+  int no_hub_list;      // staged tiers off for good: skip the hub list appends
   int32_t* out;         // [Lw, rows]
   int32_t* nnz;         // per row: non-NULL values of the window
   int32_t* died;        // per walker: ended with a NULL
@@ -179,8 +180,12 @@ __device__ __forceinline__ void tw_count_take(const TwArgs& A, TwPend& p, TwCoun
     cc.nm += hm;
     cc.nl += p.old == TW_TL - 1;
   }
-  const int idx = tw_warp_append(hm, &A.nctl->nhub);  // rare: a group becomes a hub
-  if (hm) A.nhubs[idx] = p.o;
+  // the hub list feeds the prep kernel only: with the staged tiers off it is
+  // not built (its single counter is the most contended address of a step)
+  if (!A.no_hub_list) {
+    const int idx = tw_warp_append(hm, &A.nctl->nhub);  // a group becomes a hub
+    if (hm) A.nhubs[idx] = p.o;
+  }
   p.on = false;
 }
 
