@@ -296,8 +296,9 @@ int nd_ooc_graph_info(const nd_ooc_graph *g, int64_t *n_parts, int64_t *slice_ed
                       int64_t *device_bytes, int64_t *bytes_shuttled, int64_t *uploads);
 /* vertex cut points [n_parts + 1] */
 int nd_ooc_graph_parts(const nd_ooc_graph *g, int64_t *vcut, int64_t n_max);
-/* DeepWalk (ND_DEEPWALK; others ND_ERR_APP) over a shuttled graph: same rows
- * as nd_run_walk.  roots: device int64 [n] or NULL (keyed roots). */
+/* DeepWalk (steps = walk length) or PPR (steps = the step cap; host_params =
+ * {termination probability}) over a shuttled graph (others ND_ERR_APP): same
+ * rows as nd_run_walk.  roots: device int64 [n] or NULL (keyed roots). */
 int nd_run_walk_ooc(nd_ooc_graph *g, int app_code, const double *host_params, int64_t n_params,
                     int64_t sample_lo, int64_t n_samples, const int64_t *roots, uint64_t seed,
                     int64_t steps, void *stream, nd_result **out);

@@ -16,9 +16,12 @@
 //     slots.
 // Every draw is keyed on (seed, sample, step, transit_idx, slot) exactly as
 // in-core, so the rows equal nd_run_walk / nd_run_individual byte for byte
-// whatever the partition schedule (tests/test_gpu_ooc.py).  Apps whose next()
-// reads a second row (node2vec's has_edge on the previous transit) or whose
-// walks have unbounded length (PPR) are not shuttled: ND_ERR_APP.
+// whatever the partition schedule (tests/test_gpu_ooc.py).
+//   * PPR (unbounded walks, step cap): as DeepWalk, with each step's value
+//     appended to a (walker, vertex) log that a stable sort by walker turns
+//     into the final rows.
+// node2vec's next() reads a second row (has_edge on the previous transit),
+// which a single resident partition cannot answer: ND_ERR_APP.
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -40,6 +43,8 @@ struct nd_ooc_graph {
   const int32_t* col_h = nullptr;
   const double* pre_h = nullptr;     // null for unit-weight graphs
   bool reg_col = false, reg_pre = false;
+  const int32_t* col_map = nullptr;  // device views of the registered host arrays (zero copy)
+  const double* pre_map = nullptr;
   std::vector<int64_t> vcut;         // partition p = vertices [vcut[p], vcut[p+1])
   int64_t* vcut_d = nullptr;
   int64_t slice_cap = 0;             // edges per slice buffer
@@ -138,6 +143,89 @@ __global__ void k_ooc_walk_emit(const int32_t* __restrict__ roots, const int32_t
       roots_out[i] = roots[i];
     }
     for (int64_t s = lane; s + 1 < len; s += 32) ids[o + 1 + s] = out[i * (int64_t)L + s];
+  }
+}
+
+// PPR steps (apps.py:47-49: draw 0 < term ends the walk with NULL, else
+// draw 1 picks) of the walkers in [v0, v1).  Walks have no length bound, so
+// each step's value is appended to a log of (walker << 32 | vertex) words; a
+// walker stops where the log is full (it resumes there next round).  nnz[i]
+// counts its logged values; clen[i] is set when it ends (NULL included).
+__global__ void k_ooc_ppr(const int64_t* __restrict__ row, const int32_t* __restrict__ colp,
+                          const double* __restrict__ prep, int64_t ebase, int64_t v0, int64_t v1,
+                          int unit, double term, int32_t* __restrict__ cur,
+                          int32_t* __restrict__ stp, int64_t* __restrict__ clen,
+                          int32_t* __restrict__ nnz, uint64_t* __restrict__ log,
+                          unsigned long long* __restrict__ log_n, int64_t log_cap, int cap,
+                          int64_t n, uint64_t seed, int64_t sample_lo,
+                          unsigned long long* __restrict__ ctr) {
+  unsigned long long bytes = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int s = stp[i];
+    if (s >= cap) continue;
+    int64_t v = cur[i];
+    if (v < v0 || v >= v1) continue;
+    const uint64_t ik = key_item((uint64_t)(sample_lo + i), 0, 0);  // chain.py:52-54
+    int k = nnz[i];
+    while (true) {
+      const uint64_t base0 = key_base(seed, (uint64_t)s, 0, 0);
+      const int64_t lo = __ldg(row + v), deg = __ldg(row + v + 1) - lo;
+      if (deg <= 0 || to_unit(draw_u64(base0, ik)) < term) {  // NULL: the walk ends
+        clen[i] = s + 1;
+        s = cap;
+        break;
+      }
+      const unsigned long long slot = atomicAdd(log_n, 1ull);
+      if ((int64_t)slot >= log_cap) break;  // log full: resume here next round
+      const SRow r{colp + (lo - ebase), unit ? nullptr : prep + (lo - ebase), nullptr};
+      const int64_t nb = r.c(pick_rel(r, unit, deg, to_unit(draw_u64(base0 + C_DRAW, ik))));
+      bytes += 2 * SECTOR + 8 + (unit ? 0 : SECTOR * search_sectors(deg));
+      log[slot] = ((uint64_t)i << 32) | (uint32_t)nb;
+      k++;
+      if (++s == cap) {  // the step cap (core.py:37): no NULL
+        clen[i] = cap;
+        v = nb;
+        break;
+      }
+      v = nb;
+      if (v < v0 || v >= v1) break;
+    }
+    nnz[i] = k;
+    stp[i] = s;
+    cur[i] = (int32_t)v;
+  }
+  for (int o = 16; o > 0; o >>= 1) bytes += __shfl_down_sync(0xffffffffu, bytes, o);
+  if ((threadIdx.x & 31) == 0 && bytes) atomicAdd(ctr, bytes);
+}
+
+__global__ void k_ooc_flen(const int32_t* __restrict__ nnz, int64_t n, int64_t* __restrict__ flen) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    flen[i] = i < n ? 1 + nnz[i] : 0;
+}
+
+// the walker-sorted log into the final rows: entry k of walker w (its
+// (k - logoff[w])-th step) after w's root
+__global__ void k_ooc_log_emit(const uint64_t* __restrict__ sorted, int64_t m,
+                               const int64_t* __restrict__ off, int32_t* __restrict__ ids) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t e = sorted[k];
+    const int64_t w = (int64_t)(e >> 32);
+    // off[w] - w = values logged by walkers before w (each row holds 1 root)
+    const int64_t j = k - (off[w] - w);
+    ids[off[w] + 1 + j] = (int32_t)(uint32_t)e;
+  }
+}
+
+__global__ void k_ooc_roots_emit(const int32_t* __restrict__ roots, int64_t n,
+                                 const int64_t* __restrict__ off, int32_t* __restrict__ ids,
+                                 int64_t* __restrict__ roots_out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    ids[off[i]] = roots[i];
+    roots_out[i] = roots[i];
   }
 }
 
@@ -329,6 +417,17 @@ struct Shuttle {
   ~Shuttle() { destroy(); }
 };
 
+// Few walkers left (the geometric tail of PPR, the last DeepWalk stragglers):
+// uploading whole partitions for them costs more than reading their rows
+// straight from the page-locked host arrays over the link (zero copy), so
+// below this many waiting walkers one launch over the whole vertex range
+// finishes them (ND_OOC_ZC: the threshold; 0 disables).
+static int64_t zero_copy_threshold(int64_t n) {
+  static const int64_t env = getenv("ND_OOC_ZC") ? atoll(getenv("ND_OOC_ZC")) : -1;
+  if (env >= 0) return env;
+  return std::max<int64_t>(4096, n / 32);
+}
+
 // partitions with work, in order, from a device histogram
 static int busy_parts(const unsigned long long* cnt_d, int64_t P, cudaStream_t s,
                       std::vector<int64_t>& busy, int64_t* total) {
@@ -409,6 +508,16 @@ extern "C" int nd_ooc_graph_create(const int64_t* row_offsets, const int32_t* co
         cudaGetLastError();
     }
   }
+  if (G->reg_col && (G->unit || G->reg_pre)) {  // zero-copy views for sparse late rounds
+    void* dc = nullptr;
+    void* dp = nullptr;
+    if (cudaHostGetDevicePointer(&dc, (void*)col, 0) == cudaSuccess &&
+        (G->unit || cudaHostGetDevicePointer(&dp, (void*)prefix, 0) == cudaSuccess)) {
+      G->col_map = static_cast<const int32_t*>(dc);
+      G->pre_map = static_cast<const double*>(dp);
+    }
+    cudaGetLastError();
+  }
   if (rc == ND_OK &&
       (e = cudaMemcpyAsync(G->row_d, row_offsets, (n_vertices + 1) * 8, cudaMemcpyHostToDevice, s)) != cudaSuccess)
     fail(e);
@@ -457,12 +566,168 @@ extern "C" int nd_ooc_graph_parts(const nd_ooc_graph* G, int64_t* vcut, int64_t 
   return ND_OK;
 }
 
+// PPR over a shuttled graph: rounds over the partitions holding live walkers
+// until every walk has ended (NULL) or reached `cap` steps (the run loop's
+// step cap, core.py:37); values go to a growing log, sorted by walker
+// (stable: each walker's values stay in step order) into the final rows.
+static int run_ppr_ooc(nd_ooc_graph* G, double term, int64_t sample_lo, int64_t n,
+                       const int64_t* roots, uint64_t seed, int64_t cap_steps, cudaStream_t s,
+                       nd_result** out) {
+  if (cap_steps < 1 || cap_steps >= (1ll << 30)) return ND_ERR_ARG;
+  const int cap = (int)cap_steps;
+  const int P = (int)G->parts();
+  DevGraph gv;
+  gv.V = G->V;
+  int32_t *roots32 = nullptr, *cur = nullptr, *stp = nullptr, *nnz = nullptr;
+  int64_t* clen = nullptr;
+  uint64_t* log = nullptr;
+  unsigned long long *hist = nullptr, *ctr = nullptr, *log_n = nullptr;
+  int64_t log_cap = std::max<int64_t>(n * 32, 1 << 20);
+  ND_CUDA_TRY(nd_alloc(&roots32, std::max<int64_t>(n, 1), s));
+  ND_CUDA_TRY(nd_alloc(&cur, std::max<int64_t>(n, 1), s));
+  ND_CUDA_TRY(nd_alloc(&stp, std::max<int64_t>(n, 1), s));
+  ND_CUDA_TRY(nd_alloc(&nnz, std::max<int64_t>(n, 1), s));
+  ND_CUDA_TRY(nd_alloc(&clen, std::max<int64_t>(n, 1), s));
+  ND_CUDA_TRY(nd_alloc(&log, log_cap, s));
+  ND_CUDA_TRY(nd_alloc(&hist, P, s));
+  ND_CUDA_TRY(nd_alloc(&ctr, 1, s));
+  ND_CUDA_TRY(nd_alloc(&log_n, 1, s));
+  ND_CUDA_TRY(cudaMemsetAsync(ctr, 0, 8, s));
+  ND_CUDA_TRY(cudaMemsetAsync(log_n, 0, 8, s));
+  if (roots) {
+    if (n) k_ooc_narrow<<<nd_grid(n, 256), 256, 0, s>>>(roots, n, roots32);
+  } else {
+    ND_TRY(nd_uniform_roots_i32(gv, 1, seed, sample_lo, n, roots32, s));
+  }
+  if (n) ND_CUDA_TRY(cudaMemcpyAsync(cur, roots32, n * 4, cudaMemcpyDeviceToDevice, s));
+  ND_CUDA_TRY(cudaMemsetAsync(stp, 0, std::max<int64_t>(n, 1) * 4, s));
+  ND_CUDA_TRY(cudaMemsetAsync(nnz, 0, std::max<int64_t>(n, 1) * 4, s));
+  ND_CUDA_TRY(cudaMemsetAsync(clen, 0, std::max<int64_t>(n, 1) * 8, s));
+  Shuttle sh{G, s, nullptr};
+  ND_TRY(sh.init());
+  std::vector<int64_t> busy;
+  int64_t waiting = 0, rounds = 0;
+  unsigned long long* h = reinterpret_cast<unsigned long long*>(nd_pinned_scratch());
+  while (n > 0) {
+    ND_CUDA_TRY(cudaMemsetAsync(hist, 0, P * 8, s));
+    k_ooc_walk_hist<<<nd_grid(n, 256), 256, 0, s>>>(cur, stp, n, cap, G->vcut_d, P, hist);
+    ND_TRY(busy_parts(hist, P, s, busy, &waiting));
+    if (waiting == 0) break;
+    rounds++;
+    if (G->col_map && waiting <= zero_copy_threshold(n)) {  // the geometric tail, zero copy
+      k_ooc_ppr<<<nd_grid(n, 256, 148 * 16), 256, 0, s>>>(
+          G->row_d, G->col_map, G->pre_map, 0, 0, G->V, G->unit, term, cur, stp, clen, nnz, log,
+          log_n, log_cap, cap, n, seed, sample_lo, ctr);
+      ND_CUDA_TRY(cudaGetLastError());
+    } else {
+      int b = 0, nb = 0;
+      ND_TRY(sh.upload(busy[0], b));
+      for (size_t k = 0; k < busy.size(); k++) {
+        const int64_t p = busy[k];
+        if (k + 1 < busy.size()) ND_TRY(sh.upload(busy[k + 1], nb));
+        ND_TRY(sh.use(b));
+        k_ooc_ppr<<<nd_grid(n, 256, 148 * 16), 256, 0, s>>>(
+            G->row_d, G->col_d[b], G->pre_d[b], G->e0(p), G->vcut[p], G->vcut[p + 1], G->unit,
+            term, cur, stp, clen, nnz, log, log_n, log_cap, cap, n, seed, sample_lo, ctr);
+        ND_CUDA_TRY(cudaGetLastError());
+        ND_TRY(sh.release(b));
+        b = nb;
+      }
+    }
+    // a full log: grow it (the walkers that found no slot resume next round)
+    ND_TRY(nd_d2h(h, log_n, 8, s));
+    ND_CUDA_TRY(cudaStreamSynchronize(s));
+    if ((int64_t)h[0] >= log_cap) {
+      const int64_t valid = log_cap;
+      const int64_t ncap = log_cap * 2;
+      uint64_t* nl = nullptr;
+      ND_CUDA_TRY(nd_alloc(&nl, ncap, s));
+      ND_CUDA_TRY(cudaMemcpyAsync(nl, log, valid * 8, cudaMemcpyDeviceToDevice, s));
+      nd_free(log, s);
+      log = nl;
+      log_cap = ncap;
+      const unsigned long long v = (unsigned long long)valid;
+      ND_CUDA_TRY(cudaMemcpyAsync(log_n, &v, 8, cudaMemcpyHostToDevice, s));
+      ND_CUDA_TRY(cudaStreamSynchronize(s));
+    }
+  }
+  sh.destroy();
+  // the log sorted by walker (stable), the final rows
+  ND_TRY(nd_d2h(h, log_n, 8, s));
+  ND_CUDA_TRY(cudaStreamSynchronize(s));
+  const int64_t m = std::min<int64_t>((int64_t)h[0], log_cap);
+  int wbits = 1;
+  while ((1ll << wbits) < std::max<int64_t>(n, 2)) wbits++;
+  uint64_t* sorted = nullptr;
+  int64_t *flen = nullptr, *final_off = nullptr, *roots_out = nullptr, *roots_off = nullptr;
+  ND_CUDA_TRY(nd_alloc(&sorted, std::max<int64_t>(m, 1), s));
+  ND_CUDA_TRY(nd_alloc(&flen, n + 1, s));
+  ND_CUDA_TRY(nd_alloc(&final_off, n + 1, s));
+  ND_CUDA_TRY(nd_alloc(&roots_out, std::max<int64_t>(n, 1), s));
+  ND_CUDA_TRY(nd_alloc(&roots_off, n + 1, s));
+  {
+    size_t t1 = 0, t2 = 0;
+    if (m) cub::DeviceRadixSort::SortKeys(nullptr, t1, log, sorted, m, 32, 32 + wbits, s);
+    cub::DeviceScan::ExclusiveSum(nullptr, t2, flen, final_off, n + 1, s);
+    void* tmp = nullptr;
+    ND_CUDA_TRY(nd_alloc((char**)&tmp, std::max(t1, t2), s));
+    if (m) ND_CUDA_TRY(cub::DeviceRadixSort::SortKeys(tmp, t1, log, sorted, m, 32, 32 + wbits, s));
+    k_ooc_flen<<<nd_grid(n + 1, 256), 256, 0, s>>>(nnz, n, flen);
+    ND_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, t2, flen, final_off, n + 1, s));
+    nd_free(tmp, s);
+  }
+  int64_t* mx = nullptr;
+  ND_CUDA_TRY(nd_alloc(&mx, 1, s));
+  {
+    size_t tb = 0;
+    cub::DeviceReduce::Max(nullptr, tb, clen, mx, std::max<int64_t>(n, 1), s);
+    void* tmp = nullptr;
+    ND_CUDA_TRY(nd_alloc((char**)&tmp, tb, s));
+    if (n) ND_CUDA_TRY(cub::DeviceReduce::Max(tmp, tb, clen, mx, n, s));
+    else ND_CUDA_TRY(cudaMemsetAsync(mx, 0, 8, s));
+    nd_free(tmp, s);
+  }
+  int64_t* hh = nd_pinned_scratch();
+  ND_TRY(nd_d2h(hh, final_off + n, 8, s));
+  ND_TRY(nd_d2h(hh + 1, mx, 8, s));
+  ND_TRY(nd_d2h(hh + 2, ctr, 8, s));
+  ND_CUDA_TRY(cudaStreamSynchronize(s));
+  const int64_t total = hh[0], n_steps = hh[1], slot_bytes = hh[2];
+  int32_t* final_ids = nullptr;
+  ND_CUDA_TRY(nd_alloc(&final_ids, std::max<int64_t>(total, 1), s));
+  if (n) k_ooc_roots_emit<<<nd_grid(n, 256), 256, 0, s>>>(roots32, n, final_off, final_ids, roots_out);
+  if (m) k_ooc_log_emit<<<nd_grid(m, 256, 148 * 64), 256, 0, s>>>(sorted, m, final_off, final_ids);
+  k_iota_off<<<nd_grid(n + 1, 256), 256, 0, s>>>(roots_off, n + 1);
+  ND_CUDA_TRY(cudaGetLastError());
+  nd_result* res = new nd_result();
+  res->stream = s;
+  res->n = n;
+  res->n_steps = n_steps;
+  res->total_sampled = total - n;
+  res->set(ND_F_FINAL_OFF, final_off, n + 1);
+  res->set(ND_F_FINAL_IDS32, final_ids, total);
+  res->set(ND_F_ROOTS, roots_out, n);
+  res->set(ND_F_ROOTS_OFF, roots_off, n + 1);
+  res->set(ND_F_CHAIN_LEN, clen, n);
+  res->counters[NDC_SLOT_BYTES] = slot_bytes;
+  res->counters[NDC_STEPS] = rounds;
+  *out = res;
+  nd_free(roots32, s); nd_free(cur, s); nd_free(stp, s); nd_free(nnz, s); nd_free(log, s);
+  nd_free(sorted, s); nd_free(hist, s); nd_free(ctr, s); nd_free(log_n, s); nd_free(flen, s);
+  nd_free(mx, s);
+  return ND_OK;
+}
+
 extern "C" int nd_run_walk_ooc(nd_ooc_graph* G, int app_code, const double* host_params,
                                int64_t n_params, int64_t sample_lo, int64_t n, const int64_t* roots,
                                uint64_t seed, int64_t steps, void* stream, nd_result** out) {
   NvtxRange nvtx("nd_run_walk_ooc");
   if (!G || !out || n < 0 || sample_lo < 0 || n >= (1ll << 31) || steps < 0 || steps >= (1 << 20))
     return ND_ERR_ARG;
+  if (app_code == ND_PPR) {
+    if (!host_params || n_params < 1) return ND_ERR_ARG;
+    return run_ppr_ooc(G, host_params[0], sample_lo, n, roots, seed, steps, (cudaStream_t)stream, out);
+  }
   if (app_code != ND_DEEPWALK) return ND_ERR_APP;  // see the file comment
   (void)host_params;
   (void)n_params;
@@ -502,6 +767,13 @@ extern "C" int nd_run_walk_ooc(nd_ooc_graph* G, int app_code, const double* host
     ND_TRY(busy_parts(hist, P, s, busy, &waiting));
     if (waiting == 0) break;
     rounds++;
+    if (G->col_map && waiting <= zero_copy_threshold(n)) {  // the stragglers, zero copy
+      k_ooc_walk<<<nd_grid(n, 256, 148 * 16), 256, 0, s>>>(
+          G->row_d, G->col_map, G->pre_map, 0, 0, G->V, G->unit, cur, stp, clen, win, L, n, seed,
+          sample_lo, ctr);
+      ND_CUDA_TRY(cudaGetLastError());
+      continue;
+    }
     int b = 0, nb = 0;
     ND_TRY(sh.upload(busy[0], b));
     for (size_t k = 0; k < busy.size(); k++) {

@@ -426,7 +426,7 @@ def run_device(app, graph, samples=None, *, seed: int = 0, paradigm: str = "tp",
         if samples is None:
             samples = SampleRange(app, graph, sample_lo, n_samples or 0, seed)
         lo, n, roots, _ = _sample_spec(samples, plan, seed)
-        return run_out_of_core(plan, graph, lo, n, roots, seed, paradigm, stream)
+        return run_out_of_core(plan, graph, lo, n, roots, seed, paradigm, stream, step_cap)
     dg = as_device_graph(graph)
     if roots_device is not None:
         if plan.kind == "collective":

@@ -13,9 +13,9 @@ job (keyed RNG), so ``tp_run``/``sp_run``/``run_device`` accept a
     sg = ShuttledGraph.from_graph(graph, device_budget_bytes=8 << 30)
     out = tp_run(make_app("deepwalk"), sg, make_samples(app, sg, N, seed), cfg)
 
-Supported apps: DeepWalk and k-hop (the C5 apps).  node2vec reads the
-previous transit's row as well (has_edge) and PPR walks have no length
-bound; both raise UnsupportedAppError on a shuttled graph.
+Supported apps: DeepWalk, PPR (unbounded walks up to the step cap) and
+k-hop.  node2vec reads the previous transit's row as well (has_edge) and
+raises UnsupportedAppError on a shuttled graph.
 """
 
 from __future__ import annotations
@@ -103,7 +103,7 @@ class ShuttledGraph:
 
 
 def run_out_of_core(plan, sg: ShuttledGraph, lo: int, n: int, roots, seed: int, paradigm: str,
-                    stream=None):
+                    stream=None, step_cap: int = 10_000):
     """One job over a shuttled graph (engine.run_device dispatches here);
     returns a DeviceRun.  `roots`: host int64 [n] or None (keyed roots)."""
     import time
@@ -120,10 +120,14 @@ def run_out_of_core(plan, sg: ShuttledGraph, lo: int, n: int, roots, seed: int, 
     h = C.c_void_p()
     sp = _lib.stream_ptr(stream)
     t0 = time.perf_counter()
-    if plan.kind == "walk" and plan.code == 0 and plan.R == 1 and plan.steps >= 0:
+    walk = plan.kind == "walk" and plan.R == 1
+    if walk and ((plan.code == 0 and plan.steps >= 0) or plan.code == 1):
+        # DeepWalk: its walk length; PPR: unbounded walks up to the step cap
         kp = np.ascontiguousarray(plan.kparams, dtype=np.float64)
+        steps = plan.steps if plan.code == 0 else (min(plan.steps, step_cap) if plan.steps >= 0
+                                                   else step_cap)
         _lib.check(L.nd_run_walk_ooc(sg.handle, plan.code, _lib.ptr(kp), len(kp), lo, n,
-                                     _lib.ptr(droots), C.c_uint64(seed & (2**64 - 1)), plan.steps,
+                                     _lib.ptr(droots), C.c_uint64(seed & (2**64 - 1)), steps,
                                      sp, C.byref(h)), "nd_run_walk_ooc")
     elif (plan.kind == "individual" and plan.code == 3 and plan.R == 1 and plan.unique is None
           and len(plan.fanouts) >= 1):
@@ -133,8 +137,8 @@ def run_out_of_core(plan, sg: ShuttledGraph, lo: int, n: int, roots, seed: int, 
                                            C.byref(h)), "nd_run_individual_ooc")
     else:
         raise UnsupportedAppError(
-            f"app {plan.name!r} cannot run on a shuttled graph: out-of-core runs cover DeepWalk "
-            "and k-hop (fixed fanouts, no unique steps); node2vec reads a second row per step "
-            "and PPR walks have no length bound")
+            f"app {plan.name!r} cannot run on a shuttled graph: out-of-core runs cover DeepWalk, "
+            "PPR and k-hop (fixed fanouts, no unique steps); node2vec reads a second row (its "
+            "previous transit's) per step")
     torch.cuda.synchronize()
     return DeviceRun(h, plan, sg, paradigm, lo, time.perf_counter() - t0)

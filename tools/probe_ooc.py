@@ -1,5 +1,5 @@
-"""Out-of-core shuttling at C2 scale: DeepWalk (4,194,304 walkers x 100) and
-k-hop (25,10) x 233,472 roots on the C2 RMAT graph held in host memory with a
+"""Out-of-core shuttling at C2 scale: DeepWalk (4,194,304 walkers x 100),
+PPR (4,194,304 walkers, term 0.01) and k-hop (25,10) x 233,472 roots on the C2 RMAT graph held in host memory with a
 device budget that cuts it into ~4 partitions, against the in-core runs of
 the same jobs (rows compared, times event-based, shuttled bytes reported).
 
@@ -40,7 +40,8 @@ def timed(fn):
     return e0.elapsed_time(e1), dr
 
 
-for name, kw, n in (("deepwalk", {}, dg.n_vertices), ("khop", {"fanouts": [25, 10]}, 1024 * 228)):
+for name, kw, n in (("deepwalk", {}, dg.n_vertices), ("ppr", {}, dg.n_vertices),
+                    ("khop", {"fanouts": [25, 10]}, 1024 * 228)):
     app = make_app(name, **kw)
     res = {}
     rows = {}
