@@ -759,6 +759,73 @@ __global__ void k_tail_keys(const int32_t* __restrict__ vin, const int32_t* __re
   }
 }
 
+// TP tail class statistics of small graphs by counting (no sort): per window,
+// chunks of K steps count every entry (row r, window step i < ent[r], transit
+// v = i ? out[r][i-1] : vin[r]) into cnt[(i - j0) * V + v], K*V counters small
+// enough to stay in L2.  The atomic's old value marks the member that opens
+// its group (0), makes it medium (31: the 32nd) or large (1024: the 1025th):
+// transit_parallel.py:86-101's classes with m = 1.  A second pass zeroes the
+// counters it touched.
+constexpr int TAIL_K_MAX = 64;
+template <bool CLEAR>
+__global__ void k_tail_count(const int32_t* __restrict__ vin, const int32_t* __restrict__ out,
+                             const int64_t* __restrict__ ent, int64_t n, int64_t ld, int64_t j0,
+                             int logK, int kk, int64_t V, int32_t* __restrict__ cnt,
+                             unsigned long long* __restrict__ cls) {
+  __shared__ unsigned int sc[TAIL_K_MAX * 3];
+  if (!CLEAR) {
+    for (int i = threadIdx.x; i < 3 * kk; i += blockDim.x) sc[i] = 0;
+    __syncthreads();
+  }
+  const int64_t total = n << logK;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = q >> logK;
+    const int j = (int)(q & ((1 << logK) - 1));
+    const int64_t i = j0 + j;
+    if (j >= kk || i >= ent[r]) continue;
+    const int32_t v = i == 0 ? vin[r] : out[r * ld + i - 1];
+    int32_t* c = cnt + (int64_t)j * V + v;
+    if (CLEAR) {
+      *c = 0;
+    } else {
+      const int32_t old = atomicAdd(c, 1);
+      const int k = old == 0 ? 0 : old == 31 ? 1 : old == 1024 ? 2 : -1;
+      if (k >= 0) atomicAdd(&sc[3 * j + k], 1u);
+    }
+  }
+  if (!CLEAR) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < 3 * kk; i += blockDim.x)
+      if (sc[i]) atomicAdd(cls + i, (unsigned long long)sc[i]);
+  }
+}
+
+// chunk counts -> per-step stats {small, medium, large, groups}; clears cls
+__global__ void k_tail_flush(unsigned long long* __restrict__ cls, int K, int64_t step,
+                             unsigned long long* __restrict__ stats) {
+  for (int j = threadIdx.x; j < K; j += blockDim.x) {
+    const unsigned long long g = cls[3 * j], med = cls[3 * j + 1], lg = cls[3 * j + 2];
+    if (g) {
+      unsigned long long* st = stats + 4 * (step + j);
+      st[0] += g - med;
+      st[1] += med - lg;
+      st[2] += lg;
+      st[3] += g;
+    }
+    cls[3 * j] = cls[3 * j + 1] = cls[3 * j + 2] = 0;
+  }
+}
+
+__global__ void k_sum_i64(const int64_t* __restrict__ x, int64_t n, unsigned long long* __restrict__ sum) {
+  unsigned long long t = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    t += (unsigned long long)x[i];
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
+  if ((threadIdx.x & 31) == 0 && t) atomicAdd(sum, t);
+}
+
 // class counts per tail step from the (step, transit) runs: each thread walks
 // a contiguous range of runs (sorted by step) and flushes per step
 __global__ void k_tail_classes(const uint64_t* __restrict__ ukeys, const int* __restrict__ counts,
@@ -1170,6 +1237,53 @@ static int run_tp_tail(const nd_graph* G, const NdApp& a, uint64_t seed, int64_t
   nd_free(ctl, s);
   if (rc != ND_OK) return rc;
   nd_trace("tp:tail-windows");
+  {
+    // small graphs: the class counts by counting into L2-resident counters
+    const int64_t V = G->g.V;
+    int64_t K = TAIL_K_MAX;
+    while (K > 1 && K * V * 4 > (32ll << 20)) K >>= 1;
+    static const bool force_sort = getenv("ND_TAIL_SORT") && getenv("ND_TAIL_SORT")[0] == '1';
+    if (K >= 16 && !force_sort) {
+      int logK = 0;
+      while ((1ll << logK) < K) logK++;
+      int32_t* cnt = nullptr;
+      unsigned long long *cls = nullptr, *dsum = nullptr;
+      int64_t* ent = nullptr;
+      int64_t max_n = 1;
+      for (const PWindow& W : wins) max_n = std::max(max_n, W.n);
+      if (nd_alloc(&cnt, K * V, s) != cudaSuccess || nd_alloc(&cls, 3 * TAIL_K_MAX, s) != cudaSuccess ||
+          nd_alloc(&ent, max_n + 1, s) != cudaSuccess || nd_alloc(&dsum, 1, s) != cudaSuccess)
+        rc = ND_ERR_CUDA;
+      if (rc == ND_OK) {
+        cudaMemsetAsync(cnt, 0, K * V * sizeof(int32_t), s);
+        cudaMemsetAsync(cls, 0, 3 * TAIL_K_MAX * sizeof(unsigned long long), s);
+        cudaMemsetAsync(dsum, 0, sizeof(unsigned long long), s);
+      }
+      for (size_t k = 0; k < wins.size() && rc == ND_OK; k++) {
+        const PWindow& W = wins[k];
+        k_tail_rows<<<nd_grid(W.n, 256), 256, 0, s>>>(W.wid, W.nnz, W.n, W.step0, W.Lw, dstep, ent);
+        k_sum_i64<<<nd_grid(W.n, 256), 256, 0, s>>>(ent, W.n, dsum);
+        for (int64_t j0 = 0; j0 < W.Lw; j0 += K) {
+          const int kk = (int)std::min<int64_t>(K, W.Lw - j0);
+          const int grid = nd_grid(W.n << logK, 256, 148 * 16);
+          k_tail_count<false><<<grid, 256, 0, s>>>(W.vin, W.out, ent, W.n, W.ld, j0, logK, kk, V,
+                                                  cnt, cls);
+          k_tail_count<true><<<grid, 256, 0, s>>>(W.vin, W.out, ent, W.n, W.ld, j0, logK, kk, V,
+                                                 cnt, cls);
+          k_tail_flush<<<1, 64, 0, s>>>(cls, kk, W.step0 + j0, stats);
+        }
+        if (cudaGetLastError() != cudaSuccess) rc = ND_ERR_CUDA;
+      }
+      if (rc == ND_OK) {
+        unsigned long long* hs = reinterpret_cast<unsigned long long*>(nd_pinned_scratch() + 8);
+        if (nd_d2h(hs, dsum, sizeof(unsigned long long), s) != ND_OK) rc = ND_ERR_CUDA;
+        else items = (int64_t)*hs;
+      }
+      nd_free(cnt, s); nd_free(cls, s); nd_free(ent, s); nd_free(dsum, s);
+      nd_trace("tp:tail-stats");
+      return rc;
+    }
+  }
   // entries per row, death steps, key offsets
   std::vector<int64_t*> ent(wins.size(), nullptr), koff(wins.size(), nullptr);
   std::vector<int64_t> kbase(wins.size(), 0);
