@@ -153,6 +153,16 @@ int nd_graph_rmat(int scale, int64_t n_edges, uint32_t ta, uint32_t tab, uint32_
                   uint64_t seed, int undirected, int weighted, void *stream,
                   nd_graph **out);
 int nd_graph_destroy(nd_graph *g);
+/* A graph whose column / weight / prefix arrays stay in (page-locked) host
+ * memory and are read in place over the host link (zero copy); row offsets
+ * and per-row maxima are device-resident and no index is built.  The
+ * out-of-core path for apps the partition shuttle does not run (node2vec,
+ * MultiRW, the collective apps): rows identical to a resident graph's.
+ * weights / prefix both NULL for unit weights.  Host arrays stay owned by
+ * the caller and alive until nd_graph_destroy. */
+int nd_graph_create_mapped(const int64_t *row_offsets, const int32_t *col, const double *weights,
+                           const double *prefix, int64_t n_vertices, int64_t n_edges,
+                           void *stream, nd_graph **out);
 /* Build the exact search indexes (flags: 1 = node2vec membership hash sets,
  * 2 = weighted-pick guide tables).  nd_run_walk builds what it needs on first
  * use; answers are identical to the reference's binary searches. */

@@ -47,6 +47,7 @@ SIGNATURES = {
     "nd_text_remap": [vp, vp],
     "nd_text_destroy": [vp],
     "nd_graph_destroy": [vp],
+    "nd_graph_create_mapped": [vp, vp, vp, vp, i64, i64, vp, pp],
     "nd_graph_build_index": [vp, i32, vp],
     "nd_graph_info": [vp, pi64, pi64, C.POINTER(C.c_int), pi64],
     "nd_graph_footprint": [vp, pi64, pi64, C.POINTER(C.c_double), C.POINTER(C.c_int),

@@ -378,9 +378,12 @@ static int graph_finish(nd_graph* G, const double* dev_w, const double* dev_pre,
 extern "C" int nd_graph_destroy(nd_graph* G) {
   if (!G) return ND_OK;
   cudaFree(G->row);
-  cudaFree(G->col);
-  cudaFree(G->w);
-  cudaFree(G->pre);
+  if (!G->host_mapped) {
+    cudaFree(G->col);
+    cudaFree(G->w);
+    cudaFree(G->pre);
+  }
+  for (const void* p : G->registered) cudaHostUnregister(const_cast<void*>(p));
   cudaFree(G->mx);
   cudaFree(G->hset);
   cudaFree(G->guide);
@@ -657,6 +660,76 @@ extern "C" int nd_graph_info(const nd_graph* g, int64_t* n_vertices, int64_t* n_
   if (n_edges) *n_edges = g->g.E;
   if (unit_weights) *unit_weights = g->g.unit;
   if (bytes) *bytes = g->bytes;
+  return ND_OK;
+}
+
+// A graph whose column / weight / prefix arrays stay in host memory and are
+// read by the kernels in place over the host link (zero copy): the
+// out-of-core fallback for apps the partition shuttle does not run
+// (node2vec's second row, collective apps).  Row offsets and per-row maxima
+// are device-resident; no index or record structure is ever built (the
+// kernels take their plain-CSR paths).  Host arrays: int64 row offsets
+// [V+1], int32 columns [E], f64 weights and inclusive prefix [E] (both NULL
+// for unit weights); caller-owned, alive until destroy.
+static const void* map_host(const void* p, size_t bytes, nd_graph* G, cudaError_t* err) {
+  cudaError_t e = cudaHostRegister(const_cast<void*>(p), bytes,
+                                   cudaHostRegisterMapped | cudaHostRegisterReadOnly);
+  if (e == cudaSuccess) G->registered.push_back(p);
+  else if (e != cudaErrorHostMemoryAlreadyRegistered) { *err = e; return nullptr; }
+  cudaGetLastError();
+  void* d = nullptr;
+  e = cudaHostGetDevicePointer(&d, const_cast<void*>(p), 0);
+  if (e != cudaSuccess) { *err = e; return nullptr; }
+  return d;
+}
+
+extern "C" int nd_graph_create_mapped(const int64_t* row_offsets, const int32_t* col,
+                                      const double* weights, const double* prefix,
+                                      int64_t n_vertices, int64_t n_edges, void* stream,
+                                      nd_graph** out) {
+  if (!row_offsets || !out || n_vertices <= 0 || n_edges <= 0 || !col || n_vertices >= (1ll << 31) ||
+      (!weights) != (!prefix))
+    return ND_ERR_ARG;
+  if (row_offsets[0] != 0 || row_offsets[n_vertices] != n_edges) return ND_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  auto* G = new nd_graph();
+  G->host_mapped = true;
+  G->device = 0;
+  cudaGetDevice(&G->device);
+  G->g.V = n_vertices;
+  G->g.E = n_edges;
+  G->skipped = ND_IDX_VREC | ND_IDX_NBW | ND_IDX_NBP | ND_IDX_NBU | ND_IDX_GUIDE | ND_IDX_HSET |
+               ND_IDX_LINES;
+  cudaError_t err = cudaSuccess;
+  G->col = const_cast<int32_t*>(static_cast<const int32_t*>(map_host(col, n_edges * 4, G, &err)));
+  if (weights && G->col) {
+    G->w = const_cast<double*>(static_cast<const double*>(map_host(weights, n_edges * 8, G, &err)));
+    G->pre = const_cast<double*>(static_cast<const double*>(map_host(prefix, n_edges * 8, G, &err)));
+  }
+  if (err == cudaSuccess) err = cudaMalloc(&G->row, (n_vertices + 1) * sizeof(int64_t));
+  if (err == cudaSuccess) err = cudaMalloc(&G->mx, n_vertices * sizeof(double));
+  if (err == cudaSuccess)
+    err = cudaMemcpyAsync(G->row, row_offsets, (n_vertices + 1) * 8, cudaMemcpyHostToDevice, s);
+  if (err != cudaSuccess) {
+    nd_set_last_error(cudaGetErrorString(err), __FILE__, __LINE__);
+    nd_graph_destroy(G);
+    return ND_ERR_CUDA;
+  }
+  G->bytes = (n_vertices + 1) * 8 + n_vertices * 8;
+  G->g.unit = weights ? 0 : 1;
+  if (weights) {
+    int rc = nd_segment_max(G->w, G->row, n_vertices, G->mx, s);  // streams the weights once
+    if (rc != ND_OK) { nd_graph_destroy(G); return rc; }
+  } else {
+    k_unit_max<<<nd_grid(n_vertices, 256), 256, 0, s>>>(G->row, n_vertices, G->mx);
+  }
+  graph_views(G);
+  G->csr_bytes = G->bytes;
+  if (cudaStreamSynchronize(s) != cudaSuccess || cudaGetLastError() != cudaSuccess) {
+    nd_graph_destroy(G);
+    return ND_ERR_CUDA;
+  }
+  *out = G;
   return ND_OK;
 }
 

@@ -33,6 +33,10 @@ struct nd_graph {
   int built = 0;           // ND_IDX_* bits of the structures built
   int skipped = 0;         // ND_IDX_* bits left out for lack of room (plain-CSR path)
   int device = 0;
+  // col / w / pre are device views of page-locked host arrays (zero copy,
+  // nd_graph_create_mapped): not freed here, unregistered when we registered
+  bool host_mapped = false;
+  std::vector<const void*> registered;
 };
 
 // nd_graph_footprint bits (one per optional structure, nd_index.cu)

@@ -419,8 +419,12 @@ def run_device(app, graph, samples=None, *, seed: int = 0, paradigm: str = "tp",
     torch = _lib.require_cuda()
     L = _lib.load()
     plan = describe(app)
-    from .outofcore import ShuttledGraph, run_out_of_core
+    from .outofcore import ShuttledGraph, run_out_of_core, shuttle_supported
     if isinstance(graph, ShuttledGraph):  # graph in host memory, shuttled per partition
+        if not shuttle_supported(plan):  # read in place over the host link instead
+            return run_device(app, graph.mapped(), samples, seed=seed, paradigm="sp",
+                              step_cap=step_cap, n_samples=n_samples, sample_lo=sample_lo,
+                              stream=stream, sync=sync, roots_device=roots_device)
         if roots_device is not None:
             raise ValueError("roots_device is for device-resident graphs")
         if samples is None:

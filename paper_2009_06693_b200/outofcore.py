@@ -13,9 +13,11 @@ job (keyed RNG), so ``tp_run``/``sp_run``/``run_device`` accept a
     sg = ShuttledGraph.from_graph(graph, device_budget_bytes=8 << 30)
     out = tp_run(make_app("deepwalk"), sg, make_samples(app, sg, N, seed), cfg)
 
-Supported apps: DeepWalk, PPR (unbounded walks up to the step cap) and
-k-hop.  node2vec reads the previous transit's row as well (has_edge) and
-raises UnsupportedAppError on a shuttled graph.
+Shuttled apps: DeepWalk, PPR (unbounded walks up to the step cap) and
+k-hop.  Every other app (node2vec reads its previous transit's row as well;
+MultiRW; the collective apps) runs the ordinary sample-parallel kernels over
+the same graph read in place from host memory (``ShuttledGraph.mapped()``,
+zero copy), slower but with the same rows.
 """
 
 from __future__ import annotations
@@ -36,11 +38,16 @@ class ShuttledGraph:
     graph.py:49-55) or None for unit weights."""
 
     def __init__(self, row_offsets, col_indices, prefix=None, *, device_budget_bytes: int,
-                 register_host: bool = True, remap=None):
+                 register_host: bool = True, remap=None, weights=None):
         L = _lib.load()
         self._row = np.ascontiguousarray(row_offsets, dtype=np.int64)
         self._col = np.ascontiguousarray(col_indices, dtype=np.int32)
         self._pre = None if prefix is None else np.ascontiguousarray(prefix, dtype=np.float64)
+        # the weights themselves are read only by the zero-copy path (node2vec's
+        # acceptance test, the collective apps)
+        self._w = None if (weights is None or prefix is None) else np.ascontiguousarray(
+            weights, dtype=np.float64)
+        self._mapped = None
         self.n_vertices = len(self._row) - 1
         self.n_edges = len(self._col)
         if self._pre is not None and len(self._pre) != self.n_edges:
@@ -62,7 +69,26 @@ class ShuttledGraph:
         unit = bool(np.all(w == 1.0))
         pre = None if unit else np.asarray(graph.per_vertex_weight_prefix)
         return cls(graph.row_offsets, graph.col_indices, pre, device_budget_bytes=device_budget_bytes,
-                   register_host=register_host, remap=getattr(graph, "remap", None))
+                   register_host=register_host, remap=getattr(graph, "remap", None),
+                   weights=None if unit else w)
+
+    def mapped(self):
+        """The same graph read in place from host memory by the ordinary
+        kernels (zero copy, nd_graph_create_mapped): a DeviceGraph whose only
+        device-resident arrays are the row offsets and per-row maxima.  The
+        out-of-core path of every app the partition shuttle does not run."""
+        if self._mapped is None:
+            from .graph import DeviceGraph
+            if self._pre is not None and self._w is None:
+                raise UnsupportedAppError("zero-copy runs of a weighted graph need its weights "
+                                          "(ShuttledGraph.from_graph keeps them)")
+            h = C.c_void_p()
+            _lib.check(_lib.load().nd_graph_create_mapped(
+                _lib.ptr(self._row), _lib.ptr(self._col), _lib.ptr(self._w), _lib.ptr(self._pre),
+                self.n_vertices, self.n_edges, _lib.stream_ptr(), C.byref(h)),
+                "nd_graph_create_mapped")
+            self._mapped = DeviceGraph(h, remap=self._remap)
+        return self._mapped
 
     @property
     def handle(self):
@@ -91,6 +117,9 @@ class ShuttledGraph:
         return int(self._row[v + 1] - self._row[v])
 
     def close(self):
+        if self._mapped is not None:
+            self._mapped.close()
+            self._mapped = None
         if self._h is not None and _lib._lib is not None:
             _lib._lib.nd_ooc_graph_destroy(self._h)
             self._h = None
@@ -100,6 +129,17 @@ class ShuttledGraph:
             self.close()
         except Exception:
             pass
+
+
+def shuttle_supported(plan) -> bool:
+    """Apps the partition shuttle runs (one resident row per step): DeepWalk,
+    PPR and k-hop with fixed fanouts; everything else runs zero copy."""
+    if plan.R != 1:
+        return False
+    if plan.kind == "walk":
+        return (plan.code == 0 and plan.steps >= 0) or plan.code == 1
+    return (plan.kind == "individual" and plan.code == 3 and plan.unique is None
+            and len(plan.fanouts) >= 1)
 
 
 def run_out_of_core(plan, sg: ShuttledGraph, lo: int, n: int, roots, seed: int, paradigm: str,
@@ -136,9 +176,7 @@ def run_out_of_core(plan, sg: ShuttledGraph, lo: int, n: int, roots, seed: int, 
                                            _lib.ptr(droots), C.c_uint64(seed & (2**64 - 1)), sp,
                                            C.byref(h)), "nd_run_individual_ooc")
     else:
-        raise UnsupportedAppError(
-            f"app {plan.name!r} cannot run on a shuttled graph: out-of-core runs cover DeepWalk, "
-            "PPR and k-hop (fixed fanouts, no unique steps); node2vec reads a second row (its "
-            "previous transit's) per step")
+        raise UnsupportedAppError(f"app {plan.name!r} is not shuttled (engine.run_device runs "
+                                  "it zero copy over ShuttledGraph.mapped())")
     torch.cuda.synchronize()
     return DeviceRun(h, plan, sg, paradigm, lo, time.perf_counter() - t0)

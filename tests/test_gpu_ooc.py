@@ -164,19 +164,35 @@ def test_ppr_step_cap_and_log_growth():
     a.close(); b.close(); sg.close(); dg.close()
 
 
-def test_unsupported_apps_and_budget():
-    from paper_2009_06693_b200 import make_app
+@pytest.mark.parametrize("name,kw", [("node2vec", {"p": 2.0, "q": 0.5}), ("multirw", {}),
+                                     ("fastgcn", {}), ("mvs", {}), ("layer", {"max_size": 300})])
+def test_zero_copy_apps_equal_in_core(graphs, name, kw):
+    """Apps the shuttle does not run read the host-resident graph in place
+    (ShuttledGraph.mapped()): rows, step rows and recorded edges equal the
+    resident graph's."""
+    from paper_2009_06693_b200 import _lib, make_app
     from paper_2009_06693_b200.engine import run_device
-    from paper_2009_06693_b200.errors import DeviceError, UnsupportedAppError
+    dg, hg, sg = graphs
+    app = make_app(name, **kw)
+    n = 600 if name in ("node2vec", "multirw") else 64
+    a = run_device(app, sg, n_samples=n, seed=SEED).to_output()
+    b = run_device(app, dg, n_samples=n, seed=SEED, paradigm="sp").to_output()
+    ao, ai = a.final_csr()
+    bo, bi = b.final_csr()
+    assert np.array_equal(ao, bo) and np.array_equal(ai, bi)
+    if a.rec_t is not None or b.rec_t is not None:
+        assert np.array_equal(np.asarray(a.rec_t), np.asarray(b.rec_t))
+        assert np.array_equal(np.asarray(a.rec_v), np.asarray(b.rec_v))
+    fp = sg.mapped().footprint()
+    assert fp["built"] == [] and fp["index_bytes"] == 0  # nothing E-sized on the device
+
+
+def test_unsupported_apps_and_budget():
+    from paper_2009_06693_b200.errors import DeviceError
     from paper_2009_06693_b200.graph import DeviceGraph
     from paper_2009_06693_b200.outofcore import ShuttledGraph
     dg = DeviceGraph.rmat(12, 16, seed=1, weighted=True)
     hg = dg.to_host()
-    sg = ShuttledGraph.from_graph(hg, device_budget_bytes=1 << 24)
-    for name in ("node2vec", "multirw"):
-        with pytest.raises(UnsupportedAppError):
-            run_device(make_app(name), sg, n_samples=16, seed=SEED)
-    sg.close()
     with pytest.raises((DeviceError, MemoryError, ValueError)):
         ShuttledGraph.from_graph(hg, device_budget_bytes=(hg.n_vertices + 1) * 8 + 64)
     dg.close()

@@ -1,5 +1,6 @@
 """Out-of-core shuttling at C2 scale: DeepWalk (4,194,304 walkers x 100),
-PPR (4,194,304 walkers, term 0.01) and k-hop (25,10) x 233,472 roots on the C2 RMAT graph held in host memory with a
+PPR (4,194,304 walkers, term 0.01), k-hop (25,10) x 233,472 roots and
+node2vec (4,194,304 walkers, read in place from host memory: zero copy) on the C2 RMAT graph held in host memory with a
 device budget that cuts it into ~4 partitions, against the in-core runs of
 the same jobs (rows compared, times event-based, shuttled bytes reported).
 
@@ -41,7 +42,8 @@ def timed(fn):
 
 
 for name, kw, n in (("deepwalk", {}, dg.n_vertices), ("ppr", {}, dg.n_vertices),
-                    ("khop", {"fanouts": [25, 10]}, 1024 * 228)):
+                    ("khop", {"fanouts": [25, 10]}, 1024 * 228),
+                    ("node2vec", {"p": 2.0, "q": 0.5}, dg.n_vertices)):  # zero copy
     app = make_app(name, **kw)
     res = {}
     rows = {}
