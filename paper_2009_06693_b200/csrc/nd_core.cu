@@ -672,11 +672,15 @@ extern "C" int nd_graph_info(const nd_graph* g, int64_t* n_vertices, int64_t* n_
 // [V+1], int32 columns [E], f64 weights and inclusive prefix [E] (both NULL
 // for unit weights); caller-owned, alive until destroy.
 static const void* map_host(const void* p, size_t bytes, nd_graph* G, cudaError_t* err) {
-  cudaError_t e = cudaHostRegister(const_cast<void*>(p), bytes,
-                                   cudaHostRegisterMapped | cudaHostRegisterReadOnly);
-  if (e == cudaSuccess) G->registered.push_back(p);
-  else if (e != cudaErrorHostMemoryAlreadyRegistered) { *err = e; return nullptr; }
-  cudaGetLastError();
+  cudaPointerAttributes at{};
+  cudaError_t e = cudaPointerGetAttributes(&at, p);
+  if (e != cudaSuccess || at.type != cudaMemoryTypeHost) {  // not page-locked yet: register it
+    cudaGetLastError();
+    e = cudaHostRegister(const_cast<void*>(p), bytes,
+                         cudaHostRegisterMapped | cudaHostRegisterReadOnly);
+    if (e != cudaSuccess) { *err = e; return nullptr; }
+    G->registered.push_back(p);
+  }
   void* d = nullptr;
   e = cudaHostGetDevicePointer(&d, const_cast<void*>(p), 0);
   if (e != cudaSuccess) { *err = e; return nullptr; }

@@ -497,21 +497,33 @@ extern "C" int nd_ooc_graph_create(const int64_t* row_offsets, const int32_t* co
   }
   if (rc == ND_OK && register_host && n_edges > 0) {
     // page-lock the host slices so uploads run at full link speed, async
-    if (cudaHostRegister((void*)col, n_edges * 4, cudaHostRegisterReadOnly) == cudaSuccess)
+    // (memory the caller already page-locked is used as is)
+    auto pinned = [](const void* p) {
+      cudaPointerAttributes at{};
+      const bool ok = cudaPointerGetAttributes(&at, p) == cudaSuccess && at.type == cudaMemoryTypeHost;
+      cudaGetLastError();
+      return ok;
+    };
+    if (!pinned(col) &&
+        cudaHostRegister((void*)col, n_edges * 4, cudaHostRegisterMapped | cudaHostRegisterReadOnly) ==
+            cudaSuccess)
       G->reg_col = true;
-    else
-      cudaGetLastError();  // already pinned / not registrable: pageable copies still work
-    if (!G->unit) {
-      if (cudaHostRegister((void*)prefix, n_edges * 8, cudaHostRegisterReadOnly) == cudaSuccess)
-        G->reg_pre = true;
-      else
-        cudaGetLastError();
-    }
+    cudaGetLastError();  // not registrable: pageable copies still work
+    if (!G->unit && !pinned(prefix) &&
+        cudaHostRegister((void*)prefix, n_edges * 8,
+                         cudaHostRegisterMapped | cudaHostRegisterReadOnly) == cudaSuccess)
+      G->reg_pre = true;
+    cudaGetLastError();
   }
-  if (G->reg_col && (G->unit || G->reg_pre)) {  // zero-copy views for sparse late rounds
+  if (register_host && n_edges > 0) {  // zero-copy views for sparse late rounds
     void* dc = nullptr;
     void* dp = nullptr;
-    if (cudaHostGetDevicePointer(&dc, (void*)col, 0) == cudaSuccess &&
+    cudaPointerAttributes ac{}, ap{};
+    const bool cm = cudaPointerGetAttributes(&ac, col) == cudaSuccess && ac.type == cudaMemoryTypeHost;
+    const bool pm = G->unit || (cudaPointerGetAttributes(&ap, prefix) == cudaSuccess &&
+                                ap.type == cudaMemoryTypeHost);
+    cudaGetLastError();
+    if (cm && pm && cudaHostGetDevicePointer(&dc, (void*)col, 0) == cudaSuccess &&
         (G->unit || cudaHostGetDevicePointer(&dp, (void*)prefix, 0) == cudaSuccess)) {
       G->col_map = static_cast<const int32_t*>(dc);
       G->pre_map = static_cast<const double*>(dp);

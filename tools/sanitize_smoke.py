@@ -76,11 +76,21 @@ with profiling():
         dr.close()
 hg = dg.to_host()
 sg = ShuttledGraph.from_graph(hg, device_budget_bytes=(hg.n_vertices + 1) * 8 + 2 * 12 * (hg.n_edges // 4 + 64))
-for name, kw in (("deepwalk", {"walk_length": 20}), ("khop", {"fanouts": [5, 3]})):
-    dr = run_device(make_app(name, **kw), sg, n_samples=300, seed=5)
+for name, kw in (("deepwalk", {"walk_length": 20}), ("khop", {"fanouts": [5, 3]}),
+                 ("ppr", {"termination_probability": 0.05}), ("node2vec", {"walk_length": 10}),
+                 ("fastgcn", {"batch_size": 8, "step_size": 8, "steps": 2})):
+    dr = run_device(make_app(name, **kw), sg, n_samples=300, seed=5)  # shuttled / zero copy
     dr.to_output()
     dr.close()
 sg.close()
+from paper_2009_06693_b200.minibatch import KhopBatchSampler  # noqa: E402
+import torch  # noqa: E402
+smp = KhopBatchSampler(du, [5, 3], 256)
+for b in range(3):
+    smp.sample(torch.randint(0, du.n_vertices, (256,), device="cuda", dtype=torch.int64),
+               sample_lo=b * 256, seed=5)
+torch.cuda.synchronize()
+smp.close()
 job = ShardedJob(dg, [(make_app("deepwalk"), 500, 5, 3), (make_app("khop"), 200, 5)], to_host=True)
 job.run(order=[1, 0])
 print("sanitize smoke ok")
