@@ -1080,6 +1080,33 @@ __global__ void k_narrow(const int64_t* __restrict__ in, int64_t n, int32_t* __r
 }
 
 
+struct MinbTable {
+  int t[8] = {4, 3, 3, 4, 4, 4, 4, 4};  // by app code: PPR (1), node2vec (2) -> 3
+  MinbTable() {
+    int* table = t;
+    if (const char* e = getenv("ND_WALK_MINB")) {
+      if (!strchr(e, '=')) {
+        for (int i = 0; i < 8; ++i) table[i] = atoi(e);
+      } else {
+        for (const char* p = e; *p;) {
+          int c = atoi(p);
+          const char* q = strchr(p, '=');
+          if (!q) break;
+          if (c >= 0 && c < 8) table[c] = atoi(q + 1);
+          p = strchr(q, ',');
+          if (!p) break;
+          ++p;
+        }
+      }
+    }
+  }
+};
+
+static int walk_minb(int code) {
+  static const MinbTable m;  // parsed once, thread-safe initialisation
+  return code >= 0 && code < 8 ? m.t[code] : 4;
+}
+
 // Run persistent-kernel windows from step0 until no walker continues or
 // `limit`.  Walkers that continue past a window re-enter the next one with
 // their (vertex, previous vertex); later windows get proportionally more
@@ -1096,9 +1123,13 @@ static int pw_run_windows(const nd_graph* G, const NdApp& a, uint64_t seed, int6
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  // register/occupancy variant of the persistent kernel (ND_WALK_MINB = 3|4|5|6|8
-  // resident CTAs per SM requested from ptxas; default measured best)
-  static const int minb = getenv("ND_WALK_MINB") ? atoi(getenv("ND_WALK_MINB")) : 4;
+  // register/occupancy variant of the persistent kernel: resident CTAs per SM
+  // requested from ptxas.  Default per app, measured on C2:
+  // node2vec and PPR 3 (PPR 6% faster alone, node2vec equal alone, and the
+  // two run concurrently in 21.2-21.8 vs 23.2-23.8 ms at 4 on 4 of 5 boxes),
+  // DeepWalk 4 (22% slower at 3).  ND_WALK_MINB = "3" sets every app,
+  // "1=3,2=4" per app code.
+  const int minb = walk_minb(a.code);
   void (*kern)(PWArgs) = minb >= 8 ? k_walk_persistent<8>
                          : minb == 6 ? k_walk_persistent<6>
                          : minb == 5 ? k_walk_persistent<5>
