@@ -117,7 +117,7 @@ struct Profiler {
   bool on = false;
   cudaStream_t s = nullptr;
   std::vector<cudaEvent_t> ev;
-  std::vector<std::array<size_t, 3>> steps;  // event indices: start, built, sampled
+  std::vector<std::array<size_t, 4>> steps;  // event indices: start, built, sampled; steps spanned
   Profiler() = default;
   explicit Profiler(cudaStream_t st) : on(nd_profiling() != 0), s(st) {}
   size_t mark() {  // index of the recorded event (0 when off)
@@ -128,7 +128,8 @@ struct Profiler {
     ev.push_back(e);
     return ev.size() - 1;
   }
-  void step_begin() { if (on) steps.push_back({mark(), 0, 0}); }
+  // span: steps one launch covers (their times split evenly between them)
+  void step_begin(size_t span = 1) { if (on) steps.push_back({mark(), 0, 0, span}); }
   void step_built() { if (on && !steps.empty()) steps.back()[1] = mark(); }
   void step_sampled() { if (on && !steps.empty()) steps.back()[2] = mark(); }
   float between(size_t a, size_t b) {
@@ -142,8 +143,10 @@ struct Profiler {
     if (!on) return tot;
     for (auto& st : steps) {
       const float b = between(st[0], st[1]), m = between(st[1], st[2]);
-      r->step_build_ms.push_back(b);
-      r->step_sample_ms.push_back(m);
+      for (size_t k = 0; k < st[3]; k++) {
+        r->step_build_ms.push_back(b / st[3]);
+        r->step_sample_ms.push_back(m / st[3]);
+      }
       tot[0] += b;
       tot[1] += m;
     }

@@ -974,7 +974,7 @@ static int run_chain_walk(const nd_graph* G, const NdApp& a, int64_t sample_lo, 
     if (prof.on) {
       sched_ms += prof.between(e0, e0 + 1);
       sample_ms += prof.between(e0 + 1, e0 + 2);
-      prof.steps.push_back({e0, e0 + 1, e0 + 2});
+      prof.steps.push_back({e0, e0 + 1, e0 + 2, 1});
     }
     step_base.push_back(rec_base);
     rec_base += A;
@@ -1080,31 +1080,27 @@ __global__ void k_narrow(const int64_t* __restrict__ in, int64_t n, int32_t* __r
 }
 
 
-struct MinbTable {
-  int t[8] = {4, 3, 3, 4, 4, 4, 4, 4};  // by app code: PPR (1), node2vec (2) -> 3
-  MinbTable() {
-    int* table = t;
-    if (const char* e = getenv("ND_WALK_MINB")) {
-      if (!strchr(e, '=')) {
-        for (int i = 0; i < 8; ++i) table[i] = atoi(e);
-      } else {
-        for (const char* p = e; *p;) {
-          int c = atoi(p);
-          const char* q = strchr(p, '=');
-          if (!q) break;
-          if (c >= 0 && c < 8) table[c] = atoi(q + 1);
-          p = strchr(q, ',');
-          if (!p) break;
-          ++p;
-        }
-      }
-    }
+// A per-app integer knob from the environment: "K" for every app, or
+// "code=K,code=K" per app code (ND_DEEPWALK 0, ND_PPR 1, ND_NODE2VEC 2, ...);
+// apps not named keep their default.  Parsed per call (no shared state).
+static int app_knob(const char* name, int code, int dflt) {
+  const char* e = getenv(name);
+  if (!e || !*e) return dflt;
+  if (!strchr(e, '=')) return atoi(e);
+  for (const char* p = e; *p;) {
+    const int c = atoi(p);
+    const char* q = strchr(p, '=');
+    if (!q) break;
+    if (c == code) return atoi(q + 1);
+    p = strchr(q, ',');
+    if (!p) break;
+    ++p;
   }
-};
+  return dflt;
+}
 
 static int walk_minb(int code) {
-  static const MinbTable m;  // parsed once, thread-safe initialisation
-  return code >= 0 && code < 8 ? m.t[code] : 4;
+  return app_knob("ND_WALK_MINB", code, (code == ND_PPR || code == ND_NODE2VEC) ? 3 : 4);
 }
 
 // Run persistent-kernel windows from step0 until no walker continues or
@@ -1580,7 +1576,7 @@ static int run_rootpick_walk(const nd_graph* G, const NdApp& a, int64_t sample_l
       ND_CUDA_TRY(cudaStreamSynchronize(s));
       sched_ms += prof.between(e0, e0 + 1);
       sample_ms += prof.between(e0 + 1, e0 + 2);
-      prof.steps.push_back({e0, e0 + 1, e0 + 2});
+      prof.steps.push_back({e0, e0 + 1, e0 + 2, 1});
     }
   }
   prof.mark();
@@ -1685,6 +1681,17 @@ static int run_chain_walk_hub(const nd_graph* G, const NdApp& a, int64_t sample_
   int hocc = 4;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hocc, k_tw_hub<4>, TW_BLOCK, TW_HUB_SMEM);
   if (hocc < 1) hocc = 1;
+  // k_tw_multi's resident CTAs per SM requested from ptxas (ND_TW_MINB 3 | 4)
+  void (*kmul)(TwArgs) = app_knob("ND_TW_MINB", a.code, 4) == 3 ? k_tw_multi<3> : k_tw_multi<4>;
+  int mocc = 4;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&mocc, kmul, TW_BLOCK, 0);
+  if (mocc < 1) mocc = 1;
+  // steps per launch once the staged tiers are off (k_tw_multi; ND_TW_MULTI,
+  // 1: one step per launch through k_tw_sample)
+  const int kmulti = [&] {
+    const int k = app_knob("ND_TW_MULTI", a.code, 3);
+    return k < 1 ? 1 : (k > TW_KMAX ? TW_KMAX : k);
+  }();
   const int64_t max_steps = steps >= 0 ? (steps < step_cap ? steps : step_cap) : step_cap;
   const int64_t tail_T = getenv("ND_TP_TAIL") ? atoll(getenv("ND_TP_TAIL")) : 131072;
   const int key_bits = key_bits_for(g.V);
@@ -1714,9 +1721,15 @@ static int run_chain_walk_hub(const nd_graph* G, const NdApp& a, int64_t sample_
   ND_CUDA_TRY(nd_alloc(&cunits, ucap, s));
   ND_CUDA_TRY(nd_alloc(&hrec, n, s));
   ND_CUDA_TRY(nd_alloc(&pos, n, s));
-  ND_CUDA_TRY(nd_alloc(&cnt[0], 2 * V, s));  // both parities, one L2 window
+  // member counts: both parities (k_tw_sample), or k_tw_multi's kmulti
+  // per-step arrays over the same memory, behind its row queue; one L2 window
+  const int64_t ncnt = std::max<int64_t>(2, kmulti) * V;
+  int32_t* karena = nullptr;
+  ND_CUDA_TRY(nd_alloc(&karena, 32 + ncnt, s));
+  int* kqueue = karena;
+  cnt[0] = karena + 32;
   cnt[1] = cnt[0] + V;
-  ND_CUDA_TRY(cudaMemsetAsync(cnt[0], 0, 2 * V * sizeof(int32_t), s));
+  ND_CUDA_TRY(cudaMemsetAsync(karena, 0, (32 + ncnt) * sizeof(int32_t), s));
   for (int b = 0; b < 2; b++) {
     ND_CUDA_TRY(nd_alloc(&vhub[b], V, s));
     ND_CUDA_TRY(nd_alloc(&hubs[b], hcap, s));
@@ -1745,7 +1758,7 @@ static int run_chain_walk_hub(const nd_graph* G, const NdApp& a, int64_t sample_
   {
     int max_persist = 0;
     cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
-    const size_t want = (size_t)2 * V * sizeof(int32_t);
+    const size_t want = (size_t)ncnt * sizeof(int32_t);
     if (max_persist > 0 && !getenv("ND_TW_NO_L2PIN")) {
       // The set-aside is device-wide and outlives the run: the first of any
       // concurrent TP runs records the previous limit, the last one restores
@@ -1892,13 +1905,45 @@ static int run_chain_walk_hub(const nd_graph* G, const NdApp& a, int64_t sample_
     A.cur = cur[0]; A.lo = lo[0]; A.deg = dg[0]; A.hd = hd[0];
     A.ncur = cur[1]; A.nlo = lo[1]; A.ndeg = dg[1]; A.nhd = hd[1];
     k_tw_init<<<nd_grid(rows, TW_BLOCK, nsm * 8), TW_BLOCK, 0, s>>>(A, roots, roots32, R, v0, t0);
+    // staged tiers off: K steps per launch (k_tw_multi), counts in zeroed
+    // per-step arrays instead of the parity pair the sampling kernel clears
+    const bool multi = !staging && kmulti > 1;
     {
       const int b = (int)(step & 1);
       A.nctl = ctl + b; A.ncnt = cnt[b]; A.nhubs = hubs[b];
+      if (multi) {
+        A.ncnt = cnt[0];
+        ND_CUDA_TRY(cudaMemsetAsync(cnt[0], 0, V * sizeof(int32_t), s));
+      }
       A.nstats = stats + 4 * step;
       k_tw_count0<<<nd_grid(rows, TW_BLOCK, nsm * 8), TW_BLOCK, 0, s>>>(A);
     }
-    for (int64_t k = 0; k < Lw; k++) {
+    {
+      const int64_t thr = (int64_t)nsm * occ * TW_BLOCK;
+      A.P.chunk = rows > 8 * thr ? 128 : rows > 2 * thr ? 64 : 32;
+    }
+    for (int64_t k = 0; multi && k < Lw;) {
+      const int Ke = (int)std::min<int64_t>(kmulti, Lw - k);
+      const int64_t st_ = step + k;
+      const int in = (int)(k & 1), ou = in ^ 1;
+      A.s = st_;
+      A.k = k;
+      A.K = Ke;
+      A.cur = cur[in]; A.lo = lo[in]; A.deg = dg[in]; A.hd = hd[in];
+      A.ncur = cur[ou]; A.nlo = lo[ou]; A.ndeg = dg[ou]; A.nhd = hd[ou];
+      A.kcnt = cnt[0];
+      A.kV = V;
+      A.kqueue = kqueue;
+      A.nstats = stats + 4 * (st_ + 1);
+      prof.step_begin(Ke);
+      ND_CUDA_TRY(cudaMemsetAsync(karena, 0, (32 + Ke * V) * sizeof(int32_t), s));
+      prof.step_built();
+      kmul<<<nsm * mocc, TW_BLOCK, 0, s>>>(A);
+      prof.step_sampled();
+      if (cudaGetLastError() != cudaSuccess) { rc = ND_ERR_CUDA; break; }
+      k += Ke;
+    }
+    for (int64_t k = 0; !multi && k < Lw; k++) {
       const int64_t st_ = step + k;
       const int b = (int)(st_ & 1), pb = b ^ 1;
       const int in = (int)(k & 1), ou = in ^ 1;
@@ -2087,7 +2132,7 @@ static int run_chain_walk_hub(const nd_graph* G, const NdApp& a, int64_t sample_
   nd_free(roots32, s); nd_free(died, s); nd_free(tot, s); nd_free(maxlen, s); nd_free(stall, s);
   nd_free(ctr, s); nd_free(ctl, s); nd_free(wunits, s); nd_free(cunits, s);
   nd_free(hrec, s); nd_free(pos, s); nd_free(flen, s); nd_free(hist, s);
-  nd_free(cnt[0], s);
+  nd_free(karena, s);
   for (int b = 0; b < 2; b++) { nd_free(vhub[b], s); nd_free(hubs[b], s); }
   nd_free(done, s);
   for (int b = 0; b < 2; b++) { nd_free(cur[b], s); nd_free(lo[b], s); nd_free(dg[b], s); nd_free(hd[b], s); }

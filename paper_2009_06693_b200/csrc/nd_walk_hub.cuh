@@ -119,6 +119,12 @@ struct TwArgs {
   int64_t hcap;         // member slots
   TwUnit* wunits;
   TwUnit* cunits;
+  // k_tw_multi (staged tiers off): K steps per launch, step j's member counts
+  // in kcnt + j * V (zeroed before the launch), rows claimed from *kqueue
+  int32_t* kcnt;
+  int64_t kV;
+  int* kqueue;
+  int K;
 };
 
 struct TwCounts {
@@ -286,14 +292,15 @@ __device__ __forceinline__ void tw_flush_len(int mlen, int* max_len) {
 // the transit's record row staged in shared memory (SH).  Returns true when
 // the step is decided (o = next vertex or NULL).
 template <bool SH>
-__device__ __forceinline__ bool tw_work(const TwArgs& A, TwLane& L, const unsigned char* srec,
-                                        uint64_t base0, int64_t& o, NextHdr& nh, ItemStats& st) {
+__device__ __forceinline__ bool tw_work(const TwArgs& A, bool tries, TwLane& L,
+                                        const unsigned char* srec, uint64_t base0, int64_t& o,
+                                        NextHdr& nh, ItemStats& st) {
   const PWArgs& P = A.P;
   if (L.deg <= 0) {
     o = -1;
     return true;
   }
-  if (A.tries) {
+  if (tries) {
     if (L.j == 0) st.bytes += 2 * SECTOR;  // t offsets + max_w (§8 d pair term)
     const double env = __dmul_rn(L.hd, P.a.f_max);
     const NbrW* rw = P.nbu ? nullptr : (SH ? reinterpret_cast<const NbrW*>(srec) : P.nbw + L.lo);
@@ -448,7 +455,7 @@ __device__ __forceinline__ void tw_lanes(const TwArgs& A, int64_t N, int* queue,
     bool fin = false;
     int64_t o = -1;
     NextHdr nh;
-    if (has) fin = tw_work<SH>(A, L, srec, base0, o, nh, st);
+    if (has) fin = tw_work<SH>(A, A.tries, L, srec, base0, o, nh, st);
     tw_count_take(A, pd, cc);  // the previous iteration's count, after this one's picks
     tw_emit(A, fin, L, o, nh, mlen, st, pd);
     if (fin) {
@@ -535,6 +542,190 @@ __global__ void __launch_bounds__(TW_BLOCK, MINB) k_tw_sample(TwArgs A) {
   }
 }
 
+// ---- staged tiers off: K steps per launch ----------------------------------------
+// When no hub is staged (every member is stepped in place by k_tw_sample; on
+// C2 the staged tiers never pay), a step's only TP duty
+// besides sampling is its exact class statistics, and those come from the
+// count crossings at emission time -- in whatever order the walkers are
+// counted.  So K consecutive steps run in one launch with the walker state in
+// registers between them (one state round trip per K steps instead of per
+// step): step j's landings are counted into their own zeroed array kcnt + j*V
+// and its crossings summed per CTA in shared memory, then flushed as signed
+// deltas to the statistics of step s+j+1.  No later kernel reads the counts
+// (no tier prep), so the host zeroes the arrays before the next launch.
+// Rows and statistics equal the one-step launches' (every draw is keyed by
+// (walker, step)).
+constexpr int TW_KMAX = 8;
+
+template <int MINB>
+__global__ void __launch_bounds__(TW_BLOCK, MINB) k_tw_multi(TwArgs A) {
+  __shared__ unsigned int scls[TW_KMAX][3];  // per step: groups opened, medium, large
+  for (int q = threadIdx.x; q < TW_KMAX * 3; q += blockDim.x) (&scls[0][0])[q] = 0;
+  __syncthreads();
+  const PWArgs& P = A.P;
+  const int lane = threadIdx.x & 31;
+  const unsigned lt_mask = (1u << lane) - 1;
+  const bool n2v = P.a.code == ND_NODE2VEC;
+  const int K = A.K;
+  // the state after the launch: buffer parity of step k + K
+  int32_t* fcur = (K & 1) ? A.ncur : const_cast<int32_t*>(A.cur);
+  uint32_t* flo = (K & 1) ? A.nlo : const_cast<uint32_t*>(A.lo);
+  int32_t* fdeg = (K & 1) ? A.ndeg : const_cast<int32_t*>(A.deg);
+  double* fhd = (K & 1) ? A.nhd : const_cast<double*>(A.hd);
+  int32_t* tcur = (K & 1) ? const_cast<int32_t*>(A.cur) : A.ncur;
+  uint32_t* tlo = (K & 1) ? const_cast<uint32_t*>(A.lo) : A.nlo;
+  int32_t* tdeg = (K & 1) ? const_cast<int32_t*>(A.deg) : A.ndeg;
+  const bool has_last = A.k + K == A.Lw;  // the launch ends the window
+  ItemStats st;
+  int mlen = 0;
+  unsigned long long inplace = 0;
+  TwLane L;
+  int jj = 0;            // the lane walker's step within the launch
+  uint64_t base0 = 0;
+  bool pon = false;      // a count whose result is taken one iteration later
+  int pold = 0, pj = 0;
+  int64_t wbeg = 0, wend = 0, i = -1;
+  bool has = false;
+  const int64_t N = A.rows;
+  while (true) {
+    const bool need = i < 0;
+    const unsigned m = __ballot_sync(0xffffffffu, need);
+    if (m) {
+      const int c = __popc(m);
+      const int rank = __popc(m & lt_mask);
+      const int64_t rem = wend - wbeg;
+      int64_t nbeg = 0;
+      if (rem < c) {
+        int base = 0;
+        if (lane == 0) base = atomicAdd(A.kqueue, P.chunk);
+        nbeg = __shfl_sync(0xffffffffu, base, 0);
+      }
+      if (need) {
+        i = rank < rem ? wbeg + rank : nbeg + (rank - rem);
+        if (i < N) {
+          const int64_t row = i;
+          const int32_t v = A.cur[row];
+          if (v < 0) {  // ended earlier in the window
+            if (K & 1) A.ncur[row] = -1;
+            has = false;
+            i = -1;
+          } else {
+            L.row = row;
+            L.w = A.wid ? A.wid[row] : (int32_t)row;
+            L.v = v;
+            L.lo = A.lo[row];
+            L.deg = A.deg[row];
+            L.hd = A.hd[row];
+            if (n2v) {
+              L.t = A.ncur[row];
+              L.tlo = A.nlo[row];
+              L.tdeg = A.ndeg[row];
+            } else {
+              L.t = -1;
+            }
+            jj = 0;
+            base0 = key_base(P.seed, (uint64_t)A.s, 0, 0);
+            tw_lane_start(A, L, st);
+            has = true;
+          }
+        }
+      }
+      if (rem < c) {
+        wbeg = nbeg + (c - rem);
+        wend = nbeg + P.chunk;
+      } else {
+        wbeg += c;
+      }
+    }
+    const bool all_done = __all_sync(0xffffffffu, i >= N);
+    bool fin = false;
+    int64_t o = -1;
+    NextHdr nh;
+    if (!all_done && has) fin = tw_work<false>(A, n2v && A.s + jj > 0, L, nullptr, base0, o, nh, st);
+    if (pon) {  // the previous landing's count: class crossings of its step
+      if (pold == 0) atomicAdd(&scls[pj][0], 1u);
+      if (pold == TW_TM - 1) atomicAdd(&scls[pj][1], 1u);
+      if (pold == TW_TL - 1) atomicAdd(&scls[pj][2], 1u);
+      pon = false;
+    }
+    if (all_done) break;
+    bool cont = false;
+    if (fin) {
+      const int64_t ks = A.k + jj;  // step within the window
+      const int64_t row = L.row;
+      A.out[ks * A.rows + row] = (int32_t)o;
+      mlen = max(mlen, (int)(A.s + jj) + 1);
+      inplace++;
+      if (o < 0) {
+        A.nnz[row] = (int32_t)ks;
+        A.died[L.w] = 1;
+        fcur[row] = -1;
+        i = -1;
+        has = false;
+      } else if (ks == A.Lw - 1) {
+        A.nnz[row] = (int32_t)ks + 1;
+        cont = true;
+        i = -1;
+        has = false;
+      } else {
+        double nhd = n2v ? nh.mx : nh.tot;
+        if (nhd < 0.0) {  // node2vec after its step-0 pick: max weight of the new vertex
+          nhd = __ldg(P.gv.mx + o);
+          st.sect += 1;
+        }
+        pold = atomicAdd(A.kcnt + (int64_t)jj * A.kV + o, 1);
+        pon = true;
+        pj = jj;
+        if (jj + 1 == K) {  // the launch's last step: state for the next launch
+          fcur[row] = (int32_t)o;
+          flo[row] = (uint32_t)nh.lo;
+          fdeg[row] = (int32_t)nh.deg;
+          fhd[row] = nhd;
+          if (n2v) {
+            tcur[row] = L.v;
+            tlo[row] = (uint32_t)L.lo;
+            tdeg[row] = L.deg;
+          }
+          i = -1;
+          has = false;
+        } else {  // next step in registers
+          L.t = L.v;
+          L.tlo = L.lo;
+          L.tdeg = L.deg;
+          L.v = (int32_t)o;
+          L.lo = nh.lo;
+          L.deg = (int32_t)nh.deg;
+          L.hd = nhd;
+          jj++;
+          base0 = key_base(P.seed, (uint64_t)(A.s + jj), 0, 0);
+          tw_lane_start(A, L, st);
+        }
+      }
+    }
+    if (has_last) {
+      const int slot = tw_warp_append(cont, A.cont_n);
+      if (cont) {
+        A.cont_wid[slot] = (int32_t)L.w;
+        A.cont_v[slot] = (int32_t)o;
+        A.cont_t[slot] = L.v;
+      }
+    }
+  }
+  flush_stats(st, P.ctr);
+  tw_flush_len(mlen, A.max_len);
+  tw_flush_tier(inplace, A.tier + 1);
+  __syncthreads();
+  if (threadIdx.x < K) {
+    const unsigned long long ng = scls[threadIdx.x][0], nm = scls[threadIdx.x][1],
+                             nl = scls[threadIdx.x][2];
+    unsigned long long* stt = A.nstats + 4 * threadIdx.x;  // statistics of step s + j + 1
+    if (ng != nm) atomicAdd(stt + 0, ng - nm);
+    if (nm != nl) atomicAdd(stt + 1, nm - nl);
+    if (nl) atomicAdd(stt + 2, nl);
+    if (ng) atomicAdd(stt + 3, ng);
+  }
+}
+
 // bytes and source of the records a hub's members read this step
 __device__ __forceinline__ uint32_t tw_row_bytes(const TwArgs& A, int64_t lo, int32_t deg,
                                                  const void** src) {
@@ -594,7 +785,7 @@ __device__ __forceinline__ void tw_hub_members(const TwArgs& A, const TwUnit& d,
     bool fin = false;
     int64_t o = -1;
     NextHdr nh;
-    if (L.row >= 0) fin = tw_work<true>(A, L, srec, base0, o, nh, st);
+    if (L.row >= 0) fin = tw_work<true>(A, A.tries, L, srec, base0, o, nh, st);
     tw_count_take(A, pd, cc);
     tw_emit(A, fin, L, o, nh, mlen, st, pd);
     if (fin) L.row = -1;

@@ -112,3 +112,33 @@ def test_staged_tiers_match_oracle(name, kw, monkeypatch):
     exp = np.concatenate(exp)
     assert np.array_equal(tp[_lib.F_FINAL_IDS32].astype(np.int64), exp)
     assert np.array_equal(tp[_lib.F_CHAIN_LEN], ref["chain_len"])
+
+
+@pytest.mark.parametrize("kmulti", ["3", "4", "8"])
+@pytest.mark.parametrize("unit", [False, True], ids=["weighted", "unit"])
+@pytest.mark.parametrize("name,kw", APPS, ids=[a for a, _ in APPS])
+def test_multi_step_launches_match(name, kw, unit, kmulti, monkeypatch):
+    """Staged tiers off (ND_TW_STAGE=0): K steps per launch (k_tw_multi,
+    counts in per-step arrays, walker state in registers between steps) give
+    the one-step-per-launch engine's rows, step counts and per-step class
+    statistics, and the sort engine's statistics."""
+    from paper_2009_06693_b200 import _lib, make_app
+    from paper_2009_06693_b200.graph import DeviceGraph
+    dg = DeviceGraph.rmat(14, 16, seed=4, weighted=not unit) if kmulti != "3" else _graph(unit)
+    app = make_app(name, **kw)
+    samples = _samples(60_000, n_roots=4096 if kmulti != "3" else 64)
+    env = {"ND_TP_TAIL": "0", "ND_TW_STAGE": "0"}
+    one = _run(app, dg, samples, "tp", {**env, "ND_TW_MULTI": "1"}, monkeypatch)
+    mul = _run(app, dg, samples, "tp", {**env, "ND_TW_MULTI": kmulti}, monkeypatch)
+    srt = _run(app, dg, samples, "tp", {"ND_TP_TAIL": "0", "ND_TP_ENGINE": "sort"}, monkeypatch)
+    sp = _run(app, dg, samples, "sp", {}, monkeypatch)
+    for f in (_lib.F_FINAL_OFF, _lib.F_FINAL_IDS32, _lib.F_CHAIN_LEN):
+        assert np.array_equal(one[f], mul[f]), f
+        assert np.array_equal(sp[f], mul[f]), f
+    assert np.array_equal(one[_lib.F_STATS], mul[_lib.F_STATS])
+    assert np.array_equal(srt[_lib.F_STATS], mul[_lib.F_STATS])
+    assert one["steps"] == mul["steps"] == sp["steps"]
+    c = mul["counters"]
+    assert c["tp_staged"] == 0
+    assert c["tp_inplace"] == int(mul[_lib.F_CHAIN_LEN].sum())
+    assert c["slot_bytes"] == one["counters"]["slot_bytes"]  # the §8(d) byte model is per step
