@@ -24,12 +24,20 @@ for name, kw, g in runs:
     for par in ("sp", "tp"):
         if par == "tp" and name in ("ppr", "node2vec", "deepwalk"):
             # TP walks: all steps in the class kernels, then a mid-run hand-off to the tail
-            for tail in ("0", "100"):
+            # (and with the staged tiers off: k_tw_multi, 3 and 4 steps per launch)
+            for tail, stage, multi in (("0", None, None), ("100", None, None), ("0", "0", "3"),
+                                       ("0", "0", "4")):
                 os.environ["ND_TP_TAIL"] = tail
+                for k, v in (("ND_TW_STAGE", stage), ("ND_TW_MULTI", multi)):
+                    if v is None:
+                        os.environ.pop(k, None)
+                    else:
+                        os.environ[k] = v
                 dr = run_device(make_app(name, **kw), g, n_samples=300, seed=5, paradigm=par)
                 dr.to_output()
                 dr.close()
-            os.environ.pop("ND_TP_TAIL")
+            for k in ("ND_TP_TAIL", "ND_TW_STAGE", "ND_TW_MULTI"):
+                os.environ.pop(k, None)
         for uniq in ((False, True) if name == "khop" else (False,)):
             app = make_app(name, **kw)
             if uniq:  # the step-loop engine (unique steps); otherwise the fixed layout
