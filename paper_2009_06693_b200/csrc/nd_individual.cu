@@ -737,13 +737,16 @@ struct __align__(32) HubUnit {
 __global__ void k_hub_units(const int32_t* __restrict__ nhub, const int32_t* __restrict__ hubs,
                             const int32_t* __restrict__ hoff, const int32_t* __restrict__ uoff,
                             const int32_t* __restrict__ hun, const int64_t* __restrict__ row,
-                            int64_t m, HubUnit* __restrict__ units) {
+                            int64_t m, HubUnit* __restrict__ units, int2* __restrict__ vinfo) {
   const int64_t H = *nhub;
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < H;
        j += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = hubs[j];
+    // the hub's first member slot replaces its hub index: placement reads it
+    // with the member count, one dependent lookup fewer per member
+    vinfo[v].y = hoff[j];
     const int32_t nu = hun[j];
     if (nu == 0) continue;
-    const int32_t v = hubs[j];
     HubUnit d;
     d.lo = row[v];
     d.deg = (int32_t)(row[v + 1] - d.lo);
@@ -800,7 +803,7 @@ __global__ void __launch_bounds__(256) k_fx_place(const int32_t* __restrict__ pr
       dg[q] = v[q] >= 0 ? __ldg(row + v[q] + 1) - __ldg(row + v[q]) : 0;
     }
 #pragma unroll
-    for (int q = 0; q < Q; q++) ho[q] = vi[q].x >= tm ? hoff[vi[q].y] : 0;
+    for (int q = 0; q < Q; q++) ho[q] = vi[q].x >= tm ? vi[q].y : 0;  // hub's first slot (k_hub_units)
 #pragma unroll
     for (int q = 0; q < Q; q++) {
       const int64_t ip = b0 + q * 32 + lane;
@@ -1418,7 +1421,7 @@ static int run_individual_fixed(const nd_graph* G, const NdApp& a, const int64_t
         ND_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tb, hun, uoff, cap + 1, s));
       }
       k_hub_units<<<nd_grid(cap, 256), 256, 0, s>>>(nhub, hubs, hoff, uoff, hun, g.row, fan[k],
-                                                   units);
+                                                   units, vinfo);
       const FastDiv fB((uint32_t)B[k]), fm((uint32_t)fan[k]);
       auto kpl = knob.pl == 1 ? k_fx_place<1> : knob.pl == 2 ? k_fx_place<2> : k_fx_place<4>;
       kpl<<<nd_grid(N, 256 * knob.pl, knob.pl_grid), 256, 0, s>>>(
