@@ -37,6 +37,14 @@ def test_binding_table_matches_header():
     assert L.nd_version() == 1
 
 
+def test_integration_guide_covers_every_entry_point():
+    """INTEGRATION.md maps every declared entry point to the reference
+    interface it replaces (or says it has none)."""
+    doc = open(os.path.join(os.path.dirname(HDR), "..", "INTEGRATION.md")).read()
+    missing = [n for n in declared() if n not in doc]
+    assert not missing, missing
+
+
 def test_engine_fails_loudly_without_cuda():
     import pytest
     import torch
