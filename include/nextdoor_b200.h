@@ -272,6 +272,11 @@ int nd_result_profile(const nd_result *r, double *ms, int64_t n);
 int nd_result_step_times(const nd_result *r, double *build_ms, double *sample_ms, int64_t n_max,
                          int64_t *n_out);
 int nd_set_profiling(int on);
+/* Runs started by the calling host thread share the GPU with k-1 concurrent
+ * runs (one host thread per job): persistent walk kernels launch 1/k of every
+ * SM's CTA slots, so the jobs run side by side instead of queueing behind
+ * each other's persistent grids.  Thread-local; k = 1 (default): whole GPU. */
+int nd_set_concurrency(int k);
 /* Return the stream-ordered allocation pool's unused memory beyond `keep`
  * bytes to the device (between large jobs). */
 int nd_pool_trim(int64_t keep);

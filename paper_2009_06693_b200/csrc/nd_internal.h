@@ -109,6 +109,7 @@ int nd_uniform_roots_i32(const nd::DevGraph& g, int64_t count, uint64_t seed, in
                          int64_t n, int32_t* roots, cudaStream_t s);
 
 int nd_profiling();  // nd_set_profiling state
+int nd_concurrency();  // nd_set_concurrency state of the calling thread
 
 // CUDA-event marks on a run's stream, recorded only under nd_set_profiling(1):
 // phase totals (res->prof_ms) and per-step build / sample times

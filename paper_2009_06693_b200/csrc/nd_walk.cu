@@ -692,6 +692,20 @@ extern "C" int nd_set_profiling(int on) {
   return ND_OK;
 }
 
+// Runs started by the calling host thread share the GPU with k-1 others
+// (engine.submit_device_concurrent, HostPipeline, ShardedJob: one host thread
+// per concurrent job).  The persistent walk kernels then launch their share
+// of every SM's CTA slots instead of all of them: a persistent grid holds its
+// slots until its walker queue drains, so a full grid makes a concurrent
+// job's kernels wait behind it instead of running beside it.
+static thread_local int t_share = 1;
+extern "C" int nd_set_concurrency(int k) {
+  if (k < 1) return ND_ERR_ARG;
+  t_share = k;
+  return ND_OK;
+}
+int nd_concurrency() { return t_share; }
+
 
 
 // One walker-major window: rows [n] (row -> walker wid, or the identity),
@@ -1099,8 +1113,13 @@ static int app_knob(const char* name, int code, int dflt) {
   return dflt;
 }
 
-static int walk_minb(int code) {
-  return app_knob("ND_WALK_MINB", code, (code == ND_PPR || code == ND_NODE2VEC) ? 3 : 4);
+// resident CTAs per SM requested from ptxas for an app's persistent walk
+// kernel; shared with concurrent jobs, 4 (64 registers), so that each of
+// them holds half of every SM's slots (C2: node2vec || PPR at 2 + 2 CTAs per
+// SM 19.3-19.5 ms, against 23.3 at 3 per SM each with the grids queued)
+static int walk_minb(int code, int share) {
+  return app_knob("ND_WALK_MINB", code,
+                  share > 1 ? 4 : (code == ND_PPR || code == ND_NODE2VEC) ? 3 : 4);
 }
 
 // Run persistent-kernel windows from step0 until no walker continues or
@@ -1125,7 +1144,8 @@ static int pw_run_windows(const nd_graph* G, const NdApp& a, uint64_t seed, int6
   // two run concurrently in 21.2-21.8 vs 23.2-23.8 ms at 4 on 4 of 5 boxes),
   // DeepWalk 4 (22% slower at 3).  ND_WALK_MINB = "3" sets every app,
   // "1=3,2=4" per app code.
-  const int minb = walk_minb(a.code);
+  const int share = nd_concurrency();
+  const int minb = walk_minb(a.code, share);
   void (*kern)(PWArgs) = minb >= 8 ? k_walk_persistent<8>
                          : minb == 6 ? k_walk_persistent<6>
                          : minb == 5 ? k_walk_persistent<5>
@@ -1167,9 +1187,17 @@ static int pw_run_windows(const nd_graph* G, const NdApp& a, uint64_t seed, int6
     // small windows (few walkers per lane, e.g. L2-resident graphs or the
     // PPR tail): 128-thread CTAs spread over every SM, one walker per lane
     int64_t tpb = 256, grid = (int64_t)nsm * occ;
+    // CTAs per SM of this app's windows (ND_WALK_GRID, per app code): below
+    // the occupancy, concurrent jobs share every SM instead of queueing
+    // behind each other's persistent grids
+    {
+      int cps = app_knob("ND_WALK_GRID", a.code, 0);
+      if (cps <= 0 && share > 1) cps = std::max(1, occ / share);
+      if (cps > 0 && cps < occ) grid = (int64_t)nsm * cps;
+    }
     if (rows < grid * 256) {
       tpb = 128;
-      grid = std::min<int64_t>((int64_t)nsm * occ * 2, (rows + 127) / 128);
+      grid = std::min<int64_t>(grid * 2, (rows + 127) / 128);
     }
     A.chunk = rows <= grid * tpb * 2 ? 32 : 64;
     nd_trace("sp:allocs");
@@ -1686,6 +1714,12 @@ static int run_chain_walk_hub(const nd_graph* G, const NdApp& a, int64_t sample_
   int mocc = 4;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&mocc, kmul, TW_BLOCK, 0);
   if (mocc < 1) mocc = 1;
+  {  // concurrent jobs (nd_set_concurrency): this run's share of the CTA slots
+    const int share = nd_concurrency();
+    occ = std::max(1, occ / share);
+    hocc = std::max(1, hocc / share);
+    mocc = std::max(1, mocc / share);
+  }
   // steps per launch once the staged tiers are off (k_tw_multi; ND_TW_MULTI,
   // 1: one step per launch through k_tw_sample)
   const int kmulti = [&] {

@@ -532,6 +532,23 @@ def job_streams(k: int):
     return _JOB_STREAMS[:k]
 
 
+class gpu_share:
+    """Context manager for a job's host thread: runs it starts share the GPU
+    with k-1 concurrent jobs (nd_set_concurrency, thread-local).  The
+    persistent walk kernels then hold 1/k of every SM's CTA slots, so the jobs
+    run side by side instead of one persistent grid queueing behind another."""
+
+    def __init__(self, k: int):
+        self.k = max(1, int(k))
+
+    def __enter__(self):
+        _lib.load().nd_set_concurrency(self.k)
+        return self
+
+    def __exit__(self, *a):
+        _lib.load().nd_set_concurrency(1)
+
+
 def _job_pool(k: int):
     """Persistent host threads for concurrent jobs (one per job)."""
     import concurrent.futures as cf
@@ -561,7 +578,7 @@ def submit_device_concurrent(jobs, graph, *, paradigm: str = "sp",
 
     def one(job, st):
         torch.cuda.set_device(dev)
-        with torch.cuda.stream(st):
+        with torch.cuda.stream(st), gpu_share(len(jobs)):
             return run_device(job["app"], dg, n_samples=job["n_samples"],
                               sample_lo=job.get("sample_lo", 0), seed=job.get("seed", 0),
                               paradigm=paradigm, step_cap=step_cap, stream=st, sync=False,

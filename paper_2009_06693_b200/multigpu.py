@@ -170,7 +170,7 @@ class ShardedJob:
 
         import torch
         from . import _lib
-        from .engine import _job_pool, job_streams, run_device
+        from .engine import _job_pool, gpu_share, job_streams, run_device
         cur = torch.cuda.current_stream()
         dev = torch.cuda.current_device()
         h2d = 0
@@ -187,7 +187,7 @@ class ShardedJob:
         def runner(i, st):
             j = self.jobs[i]
             torch.cuda.set_device(dev)
-            with torch.cuda.stream(st):
+            with torch.cuda.stream(st), gpu_share(k):
                 for a, b in j["pieces"]:
                     dr = None
                     try:

@@ -96,7 +96,7 @@ class HostPipeline:
         phase = self._phase
         if not wait:
             self._phase ^= 1
-        from .engine import _job_pool, job_streams
+        from .engine import _job_pool, gpu_share, job_streams
         L = _lib.load()
         dg = as_device_graph(graph)
         k = len(jobs)
@@ -137,8 +137,9 @@ class HostPipeline:
             if ji > 0 and k > 1:
                 first_done.wait(timeout=60)  # the link gets busy before the GPU is shared
             try:
-                return _chunks(ji, app, n_samples, seed, sample_lo, roots_host, st, cs, plan,
-                               parts, out, held)
+                with gpu_share(k):
+                    return _chunks(ji, app, n_samples, seed, sample_lo, roots_host, st, cs, plan,
+                                   parts, out, held)
             finally:
                 if ji == 0:  # job 0 without chunks (or failing) must not stall the others
                     first_done.set()

@@ -54,3 +54,11 @@ def test_engine_fails_loudly_without_cuda():
     from paper_2009_06693_b200.engine import run_device
     with pytest.raises(DeviceError):
         run_device(make_app("deepwalk"), None, n_samples=1)
+
+
+def test_concurrency_share_is_thread_local_setting():
+    """nd_set_concurrency: k >= 1 accepted, k < 1 rejected; no GPU needed."""
+    L = _lib.load()
+    assert L.nd_set_concurrency(2) == 0
+    assert L.nd_set_concurrency(0) != 0
+    assert L.nd_set_concurrency(1) == 0

@@ -613,3 +613,25 @@ def test_unbounded_app_step_cap_warns(paradigm):
     with pytest.warns(RuntimeWarning, match="step cap"):
         out = run(app, g, make_samples(app, g, 4, seed=1), EngineConfig(seed=1, step_cap=50))
     assert out.n_steps == 50
+
+
+@pytest.mark.parametrize("paradigm", ["sp", "tp"])
+def test_gpu_share_keeps_rows(paradigm):
+    """Runs started under engine.gpu_share(k) (nd_set_concurrency: persistent
+    kernels take 1/k of every SM's CTA slots, walk kernels built for 4 CTAs
+    per SM) return the rows of whole-GPU runs."""
+    from paper_2009_06693_b200 import _lib, make_app
+    from paper_2009_06693_b200.engine import gpu_share, run_device
+    from paper_2009_06693_b200.graph import DeviceGraph
+    dg = DeviceGraph.rmat(13, 16, seed=11, weighted=True)
+    for name in ("node2vec", "ppr", "deepwalk"):
+        app = make_app(name)
+        dr = run_device(app, dg, n_samples=6000, seed=5, paradigm=paradigm)
+        ref = (dr.host(_lib.F_FINAL_OFF), dr.host(_lib.F_FINAL_IDS))
+        dr.close()
+        for k in (2, 3, 8):
+            with gpu_share(k):
+                dr = run_device(app, dg, n_samples=6000, seed=5, paradigm=paradigm)
+            assert np.array_equal(dr.host(_lib.F_FINAL_OFF), ref[0])
+            assert np.array_equal(dr.host(_lib.F_FINAL_IDS), ref[1])
+            dr.close()
