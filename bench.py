@@ -1100,6 +1100,13 @@ def main():
                          "algorithmic_bytes_per_step": slot_bytes / len(times),
                          "kernel_ms_per_step": rf_ms / 2,
                          "kernel_timing": "apps one after another (2 passes), event-timed launches",
+                         # the timed step runs both apps' kernels side by side (each on
+                         # half of every SM's CTA slots): their combined algorithmic
+                         # bytes over the whole step time (a lower bound, the step also
+                         # holds the roots, the compaction and the host syncs)
+                         "step_achieved": (slot_bytes / len(times)) / (sum(times) / len(times) / 1e3) / 1e9,
+                         "step_frac": (slot_bytes / len(times)) / (sum(times) / len(times) / 1e3) / 1e9
+                         / peak,
                          "gather": gather},
             "cpu_baseline": cpu, "parity_cpu_sample": parity,
             "parity": {"ok": parity, "values_compared": parity_values if parity is not None else 0,
