@@ -724,7 +724,7 @@ def main():
                     help="also time an NCCL gather of every rank's rows to rank 0 (reported separately)")
     ap.add_argument("--serial-apps", action="store_true",
                     help="run node2vec then PPR instead of concurrently on two streams")
-    ap.add_argument("--e2e-chunks", type=int, default=3,
+    ap.add_argument("--e2e-chunks", type=int, default=2,
                     help="node2vec sample-id chunks of the host pipeline (D2H of chunk c overlaps chunk c+1)")
     ap.add_argument("--e2e-ppr-chunks", type=int, default=1)
     ap.add_argument("--scale", type=int, default=SCALE,
