@@ -411,6 +411,8 @@ def c5_leg(args, ws, rank, barrier, rdev):
     order = [1, 0]  # k-hop finishes first: its rows travel while DeepWalk samples
     stream = torch.cuda.current_stream()
 
+    step_times = []
+
     def timed_steps(job, k, w):
         for _ in range(w):
             job.run(order)
@@ -430,6 +432,7 @@ def c5_leg(args, ws, rank, barrier, rdev):
         if ws > 1:
             torch.distributed.all_reduce(ms, op=torch.distributed.ReduceOp.MAX)
             torch.distributed.all_reduce(ed)
+        step_times.append([round(t, 3) for t in times])  # this rank's, per step
         return ms.item(), int(ed.item()), last
 
     def checksum(rows):
@@ -492,6 +495,7 @@ def c5_leg(args, ws, rank, barrier, rdev):
                      f"split over {ws} GPU(s) by worker_ranges, rows gathered to rank 0 (NCCL)"
                      + ("" if not dev else " [dev scale: NOT C5]")),
         "value": dev_edges / (dev_ms / 1e3), "unit": "edges/s", "ms_per_step": dev_ms / args.steps,
+        "step_ms_rank0": {"device": step_times[0], "e2e": step_times[1]},
         "scaling": "strong", "steps": args.steps, "warmup": args.warmup,
         "timing": "CUDA events around ShardedJob.run (sampling + NCCL gather of both apps' rows "
                   "to rank 0), max over ranks",
