@@ -414,10 +414,11 @@ def c5_leg(args, ws, rank, barrier, rdev):
     step_times = []
 
     def timed_steps(job, k, w):
-        for _ in range(w):
-            job.run(order)
+        last = None
+        for _ in range(w):  # as in the timed steps, the previous step's rows stay alive
+            last = job.run(order)
         barrier()
-        times, edges, last = [], 0, None
+        times, edges = [], 0
         for _ in range(k):
             barrier()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
