@@ -720,7 +720,7 @@ def main():
     ap.add_argument("--no-c5", action="store_true", help="skip the C5 (1B-edge, strong-sharded) leg")
     ap.add_argument("--no-c3", action="store_true", help="skip the C3 (k-hop) leg")
     ap.add_argument("--no-c14", action="store_true", help="skip the C1 (DeepWalk) and C4 (collective) legs")
-    ap.add_argument("--c5-chunks", type=int, default=6,
+    ap.add_argument("--c5-chunks", type=int, default=8,
                     help="C5 e2e: DeepWalk pieces per rank (piece c's rows cross PCIe while c+1 samples)")
     ap.add_argument("--ref-engine", default="sp", choices=["sp", "tp"],
                     help="the reference engine timed by --impl reference (sp_run: its faster CPU path)")
