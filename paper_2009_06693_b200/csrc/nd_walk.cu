@@ -1117,9 +1117,20 @@ static int app_knob(const char* name, int code, int dflt) {
 // kernel; shared with concurrent jobs, 4 (64 registers), so that each of
 // them holds half of every SM's slots (C2: node2vec || PPR at 2 + 2 CTAs per
 // SM 19.3-19.5 ms, against 23.3 at 3 per SM each with the grids queued)
-static int walk_minb(int code, int share) {
+static int walk_minb(int code, int share, bool big) {
   return app_knob("ND_WALK_MINB", code,
-                  share > 1 ? 4 : (code == ND_PPR || code == ND_NODE2VEC) ? 3 : 4);
+                  share > 1 ? 4 : (big || code == ND_PPR || code == ND_NODE2VEC) ? 3 : 4);
+}
+
+// A graph whose resident structures exceed ND_WALK_BIG_GB (default 32 GB):
+// its random reads spread over more memory than the translation caches
+// cover, and with every CTA slot busy the walk kernel's time turns bimodal
+// from run to run (C5 DeepWalk alone: 16.2 or 21.7-22.5 ms at 4 CTAs per SM);
+// at 2 CTAs per SM (built for 3) it is a steady 17.6 ms.
+static bool walk_big_graph(const nd_graph* G) {
+  const char* e = getenv("ND_WALK_BIG_GB");
+  const double gb = e ? atof(e) : 32.0;
+  return (double)G->bytes > gb * 1e9;
 }
 
 // Run persistent-kernel windows from step0 until no walker continues or
@@ -1145,7 +1156,8 @@ static int pw_run_windows(const nd_graph* G, const NdApp& a, uint64_t seed, int6
   // DeepWalk 4 (22% slower at 3).  ND_WALK_MINB = "3" sets every app,
   // "1=3,2=4" per app code.
   const int share = nd_concurrency();
-  const int minb = walk_minb(a.code, share);
+  const bool big = share == 1 && walk_big_graph(G);
+  const int minb = walk_minb(a.code, share, big);
   void (*kern)(PWArgs) = minb >= 8 ? k_walk_persistent<8>
                          : minb == 6 ? k_walk_persistent<6>
                          : minb == 5 ? k_walk_persistent<5>
@@ -1193,6 +1205,7 @@ static int pw_run_windows(const nd_graph* G, const NdApp& a, uint64_t seed, int6
     {
       int cps = app_knob("ND_WALK_GRID", a.code, 0);
       if (cps <= 0 && share > 1) cps = std::max(1, occ / share);
+      if (cps <= 0 && big) cps = 2;
       if (cps > 0 && cps < occ) grid = (int64_t)nsm * cps;
     }
     if (rows < grid * 256) {

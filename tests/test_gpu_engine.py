@@ -635,3 +635,23 @@ def test_gpu_share_keeps_rows(paradigm):
             assert np.array_equal(dr.host(_lib.F_FINAL_OFF), ref[0])
             assert np.array_equal(dr.host(_lib.F_FINAL_IDS), ref[1])
             dr.close()
+
+
+def test_big_graph_walk_grid_keeps_rows(monkeypatch):
+    """Graphs above ND_WALK_BIG_GB run the walk kernel at 2 CTAs per SM
+    (forced here on a small graph): rows equal the default grid's."""
+    from paper_2009_06693_b200 import _lib, make_app
+    from paper_2009_06693_b200.engine import run_device
+    from paper_2009_06693_b200.graph import DeviceGraph
+    dg = DeviceGraph.rmat(13, 16, seed=11, weighted=True)
+    for name in ("node2vec", "ppr", "deepwalk"):
+        app = make_app(name)
+        dr = run_device(app, dg, n_samples=6000, seed=5, paradigm="sp")
+        ref = (dr.host(_lib.F_FINAL_OFF), dr.host(_lib.F_FINAL_IDS))
+        dr.close()
+        monkeypatch.setenv("ND_WALK_BIG_GB", "0.000001")
+        dr = run_device(app, dg, n_samples=6000, seed=5, paradigm="sp")
+        monkeypatch.delenv("ND_WALK_BIG_GB")
+        assert np.array_equal(dr.host(_lib.F_FINAL_OFF), ref[0])
+        assert np.array_equal(dr.host(_lib.F_FINAL_IDS), ref[1])
+        dr.close()
