@@ -277,6 +277,15 @@ int nd_set_profiling(int on);
  * SM's CTA slots, so the jobs run side by side instead of queueing behind
  * each other's persistent grids.  Thread-local; k = 1 (default): whole GPU. */
 int nd_set_concurrency(int k);
+/* Text rows (output.py:72-92 render_text, remap output.py:145-150) printed
+ * on the device: one line "<sample id>: <v0> <v1> ..." per row of the CSR
+ * (off [n+1], ids int32 or int64 by id_bytes, sample_ids [n], remap
+ * [max id + 1] or NULL), all device pointers.  host_out NULL: only the text's
+ * byte length in *text_len; else the text (no terminating NUL) into host_out
+ * of cap >= *text_len bytes. */
+int nd_format_rows(const int64_t *off, const void *ids, int id_bytes, const int64_t *sample_ids,
+                   int64_t n, const int64_t *remap, void *stream, char *host_out, int64_t cap,
+                   int64_t *text_len);
 /* Return the stream-ordered allocation pool's unused memory beyond `keep`
  * bytes to the device (between large jobs). */
 int nd_pool_trim(int64_t keep);

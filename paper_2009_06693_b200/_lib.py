@@ -71,6 +71,7 @@ SIGNATURES = {
     "nd_result_step_times": [vp, C.POINTER(C.c_double), C.POINTER(C.c_double), i64, pi64],
     "nd_set_profiling": [i32],
     "nd_set_concurrency": [i32],
+    "nd_format_rows": [vp, vp, i32, vp, i64, vp, vp, vp, i64, pi64],
     "nd_pool_trim": [i64],
     "nd_gather_ceiling": [i64, i32, i32, C.POINTER(C.c_double), vp],
     "nd_result_destroy": [vp],

@@ -218,28 +218,86 @@ def _fmt_rows(sample_ids, off, ids, lines):
         lines.append(f"{int(sid)}: " + " ".join(map(str, row.tolist())))
 
 
-def render_text(output: SampleSetOutput, layout: str) -> str:
-    lines = [f"# layout={layout}"]
+# outputs with at least this many ids are printed on the GPU (nd_format_rows)
+DEVICE_FORMAT_MIN_IDS = 1 << 16
+
+
+def _device_rows_text(sample_ids, off, ids, remap):
+    """The block's text lines printed on the device (nd_format_rows, one
+    warp per row), byte-identical to _fmt_rows, as a uint8 array (any
+    bytes-like use: file writes, b"".join, bytes()); None without CUDA."""
+    try:
+        import torch
+    except ImportError:  # pragma: no cover
+        return None
+    if not torch.cuda.is_available():
+        return None
+    import ctypes as C
+
+    from . import _lib
+    L = _lib.load()
+    ids = np.asarray(ids)
+    ids = ids if ids.dtype in (np.int32, np.int64) else ids.astype(np.int64)
+    d_off = torch.from_numpy(np.ascontiguousarray(off, dtype=np.int64)).cuda()
+    d_ids = torch.from_numpy(np.ascontiguousarray(ids)).cuda()
+    d_sid = torch.from_numpy(np.ascontiguousarray(sample_ids, dtype=np.int64)).cuda()
+    d_map = None if remap is None else torch.from_numpy(
+        np.ascontiguousarray(remap, dtype=np.int64)).cuda()
+    n = len(off) - 1
+    tl = C.c_int64()
+    args = (_lib.ptr(d_off), _lib.ptr(d_ids), ids.dtype.itemsize, _lib.ptr(d_sid), n,
+            _lib.ptr(d_map), _lib.stream_ptr())
+    _lib.check(L.nd_format_rows(*args, None, 0, C.byref(tl)), "nd_format_rows")
+    # a pageable buffer: pinning a GB-sized one costs more than the slower copy
+    buf = np.empty(tl.value, dtype=np.uint8)
+    _lib.check(L.nd_format_rows(*args, _lib.ptr(buf), tl.value, C.byref(tl)), "nd_format_rows")
+    return buf
+
+
+def _rows_bytes(output: "SampleSetOutput", off, ids):
+    """One block's lines (each ending in a newline), bytes-like."""
+    if len(ids) >= DEVICE_FORMAT_MIN_IDS:
+        text = _device_rows_text(output.sample_ids, off, ids, output.remap)
+        if text is not None:
+            return text
+    lines = []
+    _fmt_rows(output.sample_ids, off, output._remap(ids), lines)
+    return "".join(line + "\n" for line in lines).encode()
+
+
+def _render_parts(output: SampleSetOutput, layout: str) -> list:
+    parts = [f"# layout={layout}\n".encode()]
     if layout == LAYOUT_FINAL:
         off, ids = output.final_csr()
-        _fmt_rows(output.sample_ids, off, output._remap(ids), lines)
+        parts.append(_rows_bytes(output, off, ids))
     elif layout == LAYOUT_PER_STEP:
         if output.n_samples:
-            lines.append("roots:")
+            parts.append(b"roots:\n")
             off, ids = output.step_csr(-1)
-            _fmt_rows(output.sample_ids, off, output._remap(ids), lines)
+            parts.append(_rows_bytes(output, off, ids))
             for st in range(output.n_steps):
-                lines.append(f"step {st}:")
+                parts.append(f"step {st}:\n".encode())
                 off, ids = output.step_csr(st)
-                _fmt_rows(output.sample_ids, off, output._remap(ids), lines)
+                parts.append(_rows_bytes(output, off, ids))
     else:
         raise ValueError(f"unknown layout {layout!r}")
-    return "\n".join(lines) + "\n"
+    return parts
+
+
+def render_bytes(output: SampleSetOutput, layout: str) -> bytes:
+    """render_text as UTF-8 bytes; large blocks are printed on the GPU."""
+    return b"".join(_render_parts(output, layout))
+
+
+def render_text(output: SampleSetOutput, layout: str) -> str:
+    """The reference's text layouts (output.py:72-92)."""
+    return render_bytes(output, layout).decode()
 
 
 def emit(output: SampleSetOutput, layout: str, path) -> None:
-    with open(path, "w", encoding="utf-8") as fh:
-        fh.write(render_text(output, layout))
+    with open(path, "wb") as fh:
+        for part in _render_parts(output, layout):
+            fh.write(part)
 
 
 def write_binary(output: SampleSetOutput, layout: str, path) -> None:
