@@ -101,4 +101,13 @@ torch.cuda.synchronize()
 smp.close()
 job = ShardedJob(dg, [(make_app("deepwalk"), 500, 5, 3), (make_app("khop"), 200, 5)], to_host=True)
 job.run(order=[1, 0])
+# text rows printed on the device (nd_format_rows), both layouts, with gpu_share
+from paper_2009_06693_b200 import output as OUT  # noqa: E402
+from paper_2009_06693_b200.engine import gpu_share  # noqa: E402
+OUT.DEVICE_FORMAT_MIN_IDS = 0
+for name in ("node2vec", "khop"):
+    with gpu_share(2):
+        o = run_device(make_app(name), dg, n_samples=300, seed=5).to_output()
+    for layout in (OUT.LAYOUT_FINAL, OUT.LAYOUT_PER_STEP):
+        OUT.render_bytes(o, layout)
 print("sanitize smoke ok")
