@@ -646,6 +646,22 @@ def c3_leg(args, ws, rank, barrier, rdev):
             torch.distributed.all_reduce(ms, op=torch.distributed.ReduceOp.MAX)
             torch.distributed.all_reduce(ed)
         gbs = k_bytes / (k_ms / 1e3) / 1e9 if k_ms > 0 else None
+        # measured DRAM bytes of the same sampling kernels per run (the
+        # newest committed ncu capture of this workload, tools/ncu_round.sh)
+        dram = None
+        try:
+            import glob
+            prof = sorted(glob.glob(os.path.join(REPO, "profiles", "r*_ncu_summary.json")))[-1]
+            kh = json.load(open(prof))["workloads"]["khop"]
+            names = ["k_fx_sample"] if par == "sp" else ["k_fx_small", "k_fx_hub_warp",
+                                                        "k_fx_hub_cta<4>"]
+            # the capture holds one SP run and one TP run: both steps' launches of each
+            b_run = sum(kh[k]["dram_bytes"] for k in names if k in kh)
+            dram = {"bytes_per_run": b_run, "gbs": b_run / (k_ms / 1e3) / 1e9 if k_ms > 0 else None,
+                    "frac": b_run / (k_ms / 1e3) / 1e9 / peak if k_ms > 0 else None,
+                    "source": os.path.relpath(prof, REPO)}
+        except Exception:
+            dram = None
         out[par] = {"ms": ms.item(), "edges": int(ed.item()),
                     "value": int(ed.item()) / (ms.item() / 1e3), "unit": "edges/s",
                     "timing": "median of 5 event-timed whole runs (sampling, inversion, compaction)",
@@ -654,7 +670,8 @@ def c3_leg(args, ws, rank, barrier, rdev):
                                  "kernel_ms": k_ms, "algorithmic_bytes": k_bytes,
                                  "step_build_sample_ms": steps,
                                  "kernels": "k_fx_sample" if par == "sp" else
-                                            "k_fx_small + k_fx_hub_warp + k_fx_hub_cta"}}
+                                            "k_fx_small + k_fx_hub_warp + k_fx_hub_cta",
+                                 "dram": dram}}
     out["tp_vs_sp"] = out["tp"]["ms"] / out["sp"]["ms"]
     out["graph_footprint"] = dg.footprint()
     # single 1,024-root batches (report C3's batch latency):
