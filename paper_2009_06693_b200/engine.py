@@ -623,18 +623,20 @@ class profiling:
 
 def _run(app, graph, samples, config, paradigm) -> SampleSetOutput:
     config = config or EngineConfig()
-    par = config.paradigm or paradigm
-    if config.step_timing:
+    # the reference's own EngineConfig (driver.py:34-40: seed, n_workers,
+    # step_cap, use_kernels) is accepted as well as this package's
+    par = getattr(config, "paradigm", None) or paradigm
+    seed = getattr(config, "seed", 0)
+    step_cap = getattr(config, "step_cap", DEFAULT_STEP_CAP)
+    if getattr(config, "step_timing", False):
         with profiling():
-            dr = run_device(app, graph, samples, seed=config.seed, paradigm=par,
-                            step_cap=config.step_cap)
+            dr = run_device(app, graph, samples, seed=seed, paradigm=par, step_cap=step_cap)
     else:
-        dr = run_device(app, graph, samples, seed=config.seed, paradigm=par,
-                        step_cap=config.step_cap)
-    if dr.plan.steps < 0 and dr.n_steps >= config.step_cap:
+        dr = run_device(app, graph, samples, seed=seed, paradigm=par, step_cap=step_cap)
+    if dr.plan.steps < 0 and dr.n_steps >= step_cap:
         # run_chain / run_loop (chain.py:93-98, driver.py:215-220)
         warnings.warn(f"unbounded app {getattr(app, 'name', '?')!r} hit the "
-                      f"{config.step_cap}-step cap", RuntimeWarning, stacklevel=3)
+                      f"{step_cap}-step cap", RuntimeWarning, stacklevel=3)
     remap = getattr(graph, "remap", None)
     if isinstance(graph, DeviceGraph):
         remap = graph.remap
