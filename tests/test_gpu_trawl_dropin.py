@@ -57,3 +57,36 @@ def test_reference_objects_same_rows(trawl, name, kw, paradigm):
         for (t0, v0), (t1, v1) in zip(rs.recorded_edges, os_.recorded_edges):
             assert np.array_equal(np.asarray(t0), np.asarray(t1))
             assert np.array_equal(np.asarray(v0), np.asarray(v1))
+
+
+@pytest.mark.parametrize("paradigm", ["tp", "sp"])
+@pytest.mark.parametrize("name,kw", CASES[:5], ids=[c[0] for c in CASES[:5]])
+def test_kernel_backend_seam(trawl, name, kw, paradigm, monkeypatch):
+    """Level 1 of the boundary (kernels/__init__.py:29-44): trawl's own
+    engines with this package's device kernels bound in place of its
+    compiled backend (individual_batch; segmented_prefix_sum / segment_max
+    for the graph) give the rows of trawl with its own kernels."""
+    from paper_2009_06693_b200 import kernels as K
+    from trawl.engine import chain, sample_parallel, transit_parallel
+    import trawl.graph as TG
+    graph = trawl["synth"].powerlaw_graph(300, attach=4, weighted=True, seed=5)
+    app = trawl["apps"].make_app(name, **kw)
+    cfg = trawl["driver"].EngineConfig(seed=13)
+    run = trawl[paradigm + "_run"]
+    ref = run(app, graph, trawl["driver"].make_samples(app, graph, 40, 13), cfg)
+    calls = []
+
+    def device_batch(*a, **k):  # the device kernel, counted
+        calls.append(1)
+        return K.individual_batch(*a, **k)
+
+    for mod in (chain, sample_parallel, transit_parallel):
+        monkeypatch.setattr(mod, "individual_batch", device_batch)
+    monkeypatch.setattr(TG, "segmented_prefix_sum", K.segmented_prefix_sum)
+    monkeypatch.setattr(TG, "segment_max", K.segment_max)
+    graph2 = trawl["synth"].powerlaw_graph(300, attach=4, weighted=True, seed=5)
+    assert np.array_equal(graph2.per_vertex_weight_prefix, graph.per_vertex_weight_prefix)
+    ours = run(app, graph2, trawl["driver"].make_samples(app, graph2, 40, 13), cfg)
+    assert calls, "trawl's engine did not reach the bound device kernel"
+    for a, b in zip(ref.final_rows(), ours.final_rows()):
+        assert np.array_equal(np.asarray(a), np.asarray(b))
