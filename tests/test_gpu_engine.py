@@ -655,3 +655,27 @@ def test_big_graph_walk_grid_keeps_rows(monkeypatch):
         assert np.array_equal(dr.host(_lib.F_FINAL_OFF), ref[0])
         assert np.array_equal(dr.host(_lib.F_FINAL_IDS), ref[1])
         dr.close()
+
+
+@pytest.mark.parametrize("env", [{}, {"ND_TP_TAIL": "0"}, {"ND_TP_TAIL": "0", "ND_TW_STAGE": "0"},
+                                 {"ND_TP_TAIL": "0", "ND_TW_STAGE": "0", "ND_TW_MULTI": "1"}],
+                         ids=["tail", "hub", "multi", "one-step"])
+@pytest.mark.parametrize("paradigm", ["sp", "tp"])
+def test_node2vec_stall_raises(paradigm, env, monkeypatch):
+    """node2vec whose acceptance is ~0 (p = q = 1e300) exhausts its tries on
+    the second step and the run raises SamplerStallError (chain.py stall
+    contract), in every walk engine: walker-major, TP tail, TP hub steps,
+    K-step TP launches and one-step TP launches."""
+    from paper_2009_06693_b200 import make_app
+    from paper_2009_06693_b200.engine import run_device
+    from paper_2009_06693_b200.errors import SamplerStallError
+    from paper_2009_06693_b200.graph import DeviceGraph
+    from paper_2009_06693_b200.synth import cycle_graph
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    g = cycle_graph(64, weighted=True, seed=1)
+    dg = DeviceGraph.from_arrays(g.row_offsets, g.col_indices, g.weights)
+    app = make_app("node2vec", p=1e300, q=1e300)
+    with pytest.raises(SamplerStallError):
+        dr = run_device(app, dg, n_samples=500, seed=3, paradigm=paradigm)
+        dr.to_output()
