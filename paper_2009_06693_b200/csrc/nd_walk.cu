@@ -1336,8 +1336,9 @@ static int run_tp_tail(const nd_graph* G, const NdApp& a, uint64_t seed, int64_t
           const int grid = nd_grid(W.n << logK, 256, 148 * 16);
           k_tail_count<false><<<grid, 256, 0, s>>>(W.vin, W.out, ent, W.n, W.ld, j0, logK, kk, V,
                                                   cnt, cls);
-          k_tail_count<true><<<grid, 256, 0, s>>>(W.vin, W.out, ent, W.n, W.ld, j0, logK, kk, V,
-                                                 cnt, cls);
+          // the chunk's counters back to zero: one contiguous memset of kk * V
+          // (<= 32 MB, L2-resident) instead of a second pass over the rows
+          cudaMemsetAsync(cnt, 0, (size_t)kk * V * sizeof(int32_t), s);
           k_tail_flush<<<1, 64, 0, s>>>(cls, kk, W.step0 + j0, stats);
         }
         if (cudaGetLastError() != cudaSuccess) rc = ND_ERR_CUDA;
