@@ -109,8 +109,8 @@ int nd_d2h(void* dst, const void* src, int64_t bytes, cudaStream_t s) {
   static thread_local unsigned char* stage = nullptr;  // mapped pinned staging
   static thread_local unsigned char* dstage = nullptr;
   if (bytes <= 0) return ND_OK;
-  if (bytes > CAP) {
-    ND_TRY(nd_d2h(dst, src, bytes, s));
+  if (bytes > CAP) {  // large reads: a plain copy (pageable or pinned destination)
+    ND_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
     ND_CUDA_TRY(cudaStreamSynchronize(s));
     return ND_OK;
   }

@@ -679,3 +679,36 @@ def test_node2vec_stall_raises(paradigm, env, monkeypatch):
     with pytest.raises(SamplerStallError):
         dr = run_device(app, dg, n_samples=500, seed=3, paradigm=paradigm)
         dr.to_output()
+
+
+@pytest.mark.parametrize("name", ["fastgcn", "layer"])
+def test_collective_many_explicit_samples(name):
+    """Collective apps over more than 8,192 caller-given samples (the roots'
+    offsets read back exceed the 64 KB staging block of nd_d2h): the rows
+    equal those of the two halves run separately."""
+    from dataclasses import dataclass
+
+    from paper_2009_06693_b200 import _lib, make_app
+    from paper_2009_06693_b200.engine import run_device
+    from paper_2009_06693_b200.graph import DeviceGraph
+
+    @dataclass
+    class S:
+        id: int
+        roots: tuple
+
+    dg = DeviceGraph.rmat(12, 8, seed=3, undirected=True, weighted=False)
+    rng = np.random.default_rng(5)
+    samples = [S(i, (int(rng.integers(0, dg.n_vertices)),)) for i in range(9000)]
+    app = make_app(name)
+
+    def rows(ss):
+        dr = run_device(app, dg, ss, seed=9, paradigm="tp")
+        off, ids = dr.host(_lib.F_FINAL_OFF), dr.host(_lib.F_FINAL_IDS)
+        dr.close()
+        return [ids[off[i]:off[i + 1]] for i in range(len(off) - 1)]
+
+    whole = rows(samples)
+    halves = rows(samples[:4500]) + rows(samples[4500:])
+    assert len(whole) == len(halves) == 9000
+    assert all(np.array_equal(a, b) for a, b in zip(whole, halves))
