@@ -538,15 +538,28 @@ class gpu_share:
     persistent walk kernels then hold 1/k of every SM's CTA slots, so the jobs
     run side by side instead of one persistent grid queueing behind another."""
 
+    _tls = None
+
     def __init__(self, k: int):
         self.k = max(1, int(k))
 
+    @classmethod
+    def _state(cls):
+        import threading
+        if cls._tls is None:
+            cls._tls = threading.local()
+        return cls._tls
+
     def __enter__(self):
+        st = self._state()
+        self._prev = getattr(st, "k", 1)
+        st.k = self.k
         _lib.load().nd_set_concurrency(self.k)
         return self
 
     def __exit__(self, *a):
-        _lib.load().nd_set_concurrency(1)
+        self._state().k = self._prev  # nested shares restore the enclosing one
+        _lib.load().nd_set_concurrency(self._prev)
 
 
 def _job_pool(k: int):

@@ -62,3 +62,13 @@ def test_concurrency_share_is_thread_local_setting():
     assert L.nd_set_concurrency(2) == 0
     assert L.nd_set_concurrency(0) != 0
     assert L.nd_set_concurrency(1) == 0
+
+
+def test_gpu_share_nests_and_restores():
+    from paper_2009_06693_b200.engine import gpu_share
+    with gpu_share(3) as a:
+        assert gpu_share._state().k == 3
+        with gpu_share(2):
+            assert gpu_share._state().k == 2
+        assert gpu_share._state().k == 3
+    assert gpu_share._state().k == 1 and a.k == 3
