@@ -1893,6 +1893,7 @@ static int run_chain_walk_hub(const nd_graph* G, const NdApp& a, int64_t sample_
   int rc = ND_OK;
   // staged hub tiers on until a window shows they do not engage (ND_TW_STAGE=1:
   // always on, 0: always off; development)
+  const bool tw_debug = getenv("ND_TW_DEBUG") != nullptr;
   const char* stg_env = getenv("ND_TW_STAGE");
   bool staging = !(stg_env && stg_env[0] == '0');
   const bool stage_fixed = stg_env != nullptr;
@@ -2032,7 +2033,7 @@ static int run_chain_walk_hub(const nd_graph* G, const NdApp& a, int64_t sample_
       prof.step_sampled();
       tp.mark(s, 3);
       if (cudaGetLastError() != cudaSuccess) { rc = ND_ERR_CUDA; break; }
-      if (getenv("ND_TW_DEBUG") && (st_ % 10 == 1)) {  // development: per-step tier sizes
+      if (tw_debug && (st_ % 10 == 1)) {  // development: per-step tier sizes
         TwCtl hc;
         if (nd_d2h(&hc, ctl + b, sizeof(TwCtl), s) == ND_OK)
           fprintf(stderr, "[tw] step %lld hubs %d groups %d small %d warp-hubs %d cta-units %d "
